@@ -1,0 +1,234 @@
+/* divscope-b200 — B200-native drop-in for the randomized classical-MDS path
+ * of the reference `divscope` toolkit (arXiv:1803.02272).
+ *
+ * This is the C ABI the reference's own FFI binds for the MDS path. The
+ * status enum, handle types, option struct and the semantics of every entry
+ * point that also exists in the reference are kept exactly; each declaration
+ * cites the reference declaration it replaces
+ * (/root/reference/proj/include/divscope.h = "ref divscope.h", and
+ * /root/reference/proj/src/capi.cpp = "ref capi.cpp").
+ *
+ * Conventions (ref divscope.h:1-9, ref capi.cpp:66-87):
+ *  - every call returns divscope_status; nothing throws across the ABI;
+ *  - NULL required arguments -> DIVSCOPE_ERR_INVALID_ARGUMENT ("null argument");
+ *  - the failure message is thread-local (divscope_last_error);
+ *  - out-handles are written only on success; the caller frees them;
+ *  - handles are immutable once created and may be shared across threads.
+ *
+ * Device model: matrices live in the HBM of the calling process's CUDA
+ * device (one process per GPU). divscope_gram returns a *lazy* gram handle:
+ * it keeps the distance matrix resident plus its row means / grand mean and
+ * never materializes G = -1/2 J D^2 J; divscope_matrix_get / _write evaluate
+ * G on demand. The `threads` arguments are accepted for ABI compatibility and
+ * ignored (the GPU path is not thread-count dependent). There is no CPU
+ * fallback: without a usable CUDA device every compute call fails with
+ * DIVSCOPE_ERR_INTERNAL.
+ */
+#ifndef DIVSCOPE_H
+#define DIVSCOPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ref divscope.h:22-42 (values mirror errc, ref src/error.hpp:10-30) */
+typedef enum divscope_status {
+    DIVSCOPE_OK = 0,
+    DIVSCOPE_ERR_IO,
+    DIVSCOPE_ERR_EMPTY_INPUT,
+    DIVSCOPE_ERR_INVALID_CHARACTER,
+    DIVSCOPE_ERR_DUPLICATE_ID,
+    DIVSCOPE_ERR_SAMPLE_TOO_LARGE,
+    DIVSCOPE_ERR_EMPTY_SEQUENCE,
+    DIVSCOPE_ERR_BAD_FORMAT,
+    DIVSCOPE_ERR_TRUNCATED,
+    DIVSCOPE_ERR_NOT_SYMMETRIC,
+    DIVSCOPE_ERR_RANK_TOO_LARGE,
+    DIVSCOPE_ERR_ZERO_MATRIX,
+    DIVSCOPE_ERR_BAD_GAP,
+    DIVSCOPE_ERR_SHAPE_MISMATCH,
+    DIVSCOPE_ERR_MISSING_LABEL,
+    DIVSCOPE_ERR_JOIN_ERROR,
+    DIVSCOPE_ERR_BAD_AXIS,
+    DIVSCOPE_ERR_INVALID_ARGUMENT,
+    DIVSCOPE_ERR_INTERNAL
+} divscope_status;
+
+/* ref divscope.h:44 */
+const char* divscope_status_name(divscope_status s);
+/* ref divscope.h:49 */
+const char* divscope_last_error(void);
+/* ref divscope.h:51 */
+const char* divscope_version(void);
+
+/* ---- read-set ids (only what divscope_embed needs) ---------------------- */
+
+/* ref divscope.h:55 (opaque type). FASTA ingestion is out of scope for this
+ * path; a readset here is an ordered list of row ids. */
+typedef struct divscope_readset divscope_readset;
+/* NEW: build a readset of `count` ids (copied). */
+divscope_status divscope_readset_from_ids(const char* const* ids, size_t count,
+                                          divscope_readset** out);
+/* ref divscope.h:62, :64, :71 */
+size_t divscope_readset_size(const divscope_readset* rs);
+const char* divscope_readset_id(const divscope_readset* rs, size_t i);
+void divscope_readset_free(divscope_readset* rs);
+
+/* ---- matrices ------------------------------------------------------------ */
+
+/* ref divscope.h:103 */
+typedef struct divscope_matrix divscope_matrix;
+
+/* NEW (in-memory constructor a cgo/ctypes binding needs; the reference only
+ * builds matrices via pairwise alignment or DVS files): copy a row-major
+ * rows x cols float64 host buffer into device memory. Pinned host memory
+ * gives the fastest upload. */
+divscope_status divscope_matrix_from_host(const double* values, size_t rows, size_t cols,
+                                          int symmetric, divscope_matrix** out);
+/* NEW: float32 storage (BASELINE config 4). All arithmetic on it is fp64
+ * (d is widened before squaring, so d^2 is exact). */
+divscope_status divscope_matrix_from_host_f32(const float* values, size_t rows, size_t cols,
+                                              int symmetric, divscope_matrix** out);
+/* ref divscope.h:114-117 */
+size_t divscope_matrix_rows(const divscope_matrix* m);
+size_t divscope_matrix_cols(const divscope_matrix* m);
+int divscope_matrix_symmetric(const divscope_matrix* m);
+double divscope_matrix_get(const divscope_matrix* m, size_t i, size_t j);
+/* NEW: copy the whole matrix (materializing G for a lazy gram) to a host
+ * row-major buffer of rows*cols doubles. */
+divscope_status divscope_matrix_copy_to_host(const divscope_matrix* m, double* out);
+/* ref divscope.h:118-121 (DVS1 container, ref src/distmat.hpp:42-44) */
+divscope_status divscope_matrix_write(const divscope_matrix* m, const char* dvs_path);
+divscope_status divscope_matrix_read(const char* dvs_path, divscope_matrix** out);
+/* ref divscope.h:128 */
+void divscope_matrix_free(divscope_matrix* m);
+
+/* ---- distance builders that feed the path (no reference equivalent) ----- */
+
+/* NEW (BASELINE configs 1-4 input): exact Euclidean distances of `n` points
+ * in R^dim (row-major host buffer), computed on the GPU with the reference
+ * fixture's operation order (ref tests/testdata.cpp:165-184: sequential
+ * coordinate sum, no FMA contraction, sqrt), so the result is bit-identical
+ * to the CPU formula and exactly symmetric. store_f32 != 0 rounds the
+ * stored distances to float32. */
+divscope_status divscope_matrix_euclidean(const double* points, size_t n, size_t dim,
+                                          int store_f32, divscope_matrix** out);
+/* NEW (BASELINE config 5): normalized Hamming distance of `count` DNA reads
+ * of equal `length` over {A,C,G,T} (concatenated, no separators): D_ij =
+ * h_ij / length, h_ij = number of differing positions, computed on the GPU
+ * from a 2-bit packed copy (XOR / fold / popcount). Reads containing any
+ * other character fail with DIVSCOPE_ERR_INVALID_CHARACTER. */
+divscope_status divscope_matrix_hamming(const char* reads, size_t count, size_t length,
+                                        divscope_matrix** out);
+/* NEW: the integer counts h (count x count, uint32) of the same computation,
+ * for bit-exact checks. */
+divscope_status divscope_hamming_counts(const char* reads, size_t count, size_t length,
+                                        uint32_t* out);
+
+/* ---- spectra and embeddings --------------------------------------------- */
+
+/* ref divscope.h:132-137 */
+typedef struct divscope_solver_options {
+    size_t rank;
+    size_t oversampling; /* clamped so rank + oversampling <= n for embed */
+    size_t power_iters;
+    uint64_t seed;
+} divscope_solver_options;
+
+/* ref divscope.h:140: rank 50, oversampling 10, power_iters 2, seed 0 */
+void divscope_solver_options_init(divscope_solver_options* o);
+
+/* ref divscope.h:144-145. Validates (square + symmetric flag, n > 0,
+ * |d_ij - d_ji| <= 1e-12 max(1, max|d|)) and computes the row means of D^2
+ * and the grand mean in one streaming pass over D (kernel K1). Returns a lazy
+ * gram handle (G is never materialized). */
+divscope_status divscope_gram(const divscope_matrix* dist, unsigned threads,
+                              divscope_matrix** out);
+
+/* ref divscope.h:151-154. Works on a lazy gram or on any explicit symmetric
+ * matrix (symmetry checked to 1e-10 max(1, max|g|), ref rsvd.cpp:46-60). */
+divscope_status divscope_eigs(const divscope_matrix* gram, const divscope_solver_options* opts,
+                              unsigned threads, double* eigenvalues, size_t* count,
+                              double* resid);
+
+/* ref divscope.h:157-158: ||G||_F^2 / ||G||_S^2 (power iteration on the GPU). */
+divscope_status divscope_stable_rank(const divscope_matrix* gram, unsigned threads,
+                                     double* out);
+
+/* ref divscope.h:160 */
+typedef struct divscope_embedding divscope_embedding;
+
+/* ref divscope.h:165-168 */
+divscope_status divscope_embed(const divscope_matrix* gram, const divscope_solver_options* opts,
+                               unsigned threads, const divscope_readset* ids,
+                               divscope_embedding** out);
+/* ref divscope.h:169-178 */
+size_t divscope_embedding_rows(const divscope_embedding* e);
+size_t divscope_embedding_dims(const divscope_embedding* e);
+const char* divscope_embedding_id(const divscope_embedding* e, size_t i);
+double divscope_embedding_get(const divscope_embedding* e, size_t i, size_t c);
+size_t divscope_embedding_eigenvalues(const divscope_embedding* e, double* out, size_t cap);
+double divscope_embedding_dropped_negative_mass(const divscope_embedding* e);
+int divscope_embedding_truncated(const divscope_embedding* e);
+/* NEW: pointer to the n x dims row-major coordinates (valid for the life of
+ * the handle; NULL when dims == 0). */
+const double* divscope_embedding_coords(const divscope_embedding* e);
+/* NEW: Frobenius-gap residual of the spectrum the embedding came from. */
+double divscope_embedding_resid(const divscope_embedding* e);
+/* ref divscope.h:180-185 (TSV `id dim1..dimr` + key=value meta sidecar) */
+divscope_status divscope_embedding_write(const divscope_embedding* e, const char* tsv_path,
+                                         const char* meta_path);
+divscope_status divscope_embedding_load(const char* tsv_path, divscope_embedding** out);
+void divscope_embedding_free(divscope_embedding* e);
+
+/* NEW (ports the C++-only reference entry randomized_range, ref
+ * src/rsvd.hpp:43-44, for its orthonormality / subspace KATs): writes the
+ * n x (rank + oversampling) basis, row-major. Numerically rank-deficient
+ * directions come back as zero columns (K3). */
+divscope_status divscope_randomized_range(const divscope_matrix* gram,
+                                          const divscope_solver_options* opts, double* q_out);
+
+/* ---- seeded workload synthesis (NEW; BASELINE.json configs) ------------ */
+
+/* Points of BASELINE config `config` (1..4), n x dim row-major into `out`
+ * (dim = 20, 50, 100, 64). Every draw follows the reference RNG conventions
+ * (ref src/rng.hpp:16-48, std::mt19937_64(seed)); the recipe per config is
+ * in DESIGN.md "Synthetic inputs". Returns the dimension via *dim_out. */
+divscope_status divscope_synth_points(int config, size_t n, uint64_t seed, double* out,
+                                      size_t* dim_out);
+/* Config 5 reads: `count` reads of `length` bases copied from `ancestors`
+ * seeded random ancestors with independent `sub_rate` substitutions,
+ * concatenated into `out` (count * length chars, no terminator). */
+divscope_status divscope_synth_reads(size_t count, size_t length, size_t ancestors,
+                                     double sub_rate, uint64_t seed, char* out);
+
+/* ---- device / instrumentation (NEW) ------------------------------------- */
+
+/* Select the CUDA device used by this process (default: current device). */
+divscope_status divscope_set_device(int device);
+
+typedef struct divscope_stats {
+    uint64_t kernel_launches;   /* kernels this library launched */
+    uint64_t product_launches;  /* K2 launches (streaming product passes) */
+    double product_ms;          /* summed K2 device time (CUDA events), when timing on */
+    uint64_t stats_launches;    /* K1 launches (pass 0) */
+    double stats_ms;            /* summed K1 device time, when timing on */
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+} divscope_stats;
+
+/* timing on => CUDA events are recorded around K1/K2 on the library stream */
+void divscope_stats_enable_timing(int on);
+void divscope_stats_reset(void);
+void divscope_stats_get(divscope_stats* out);
+/* stream the library enqueues on (cudaStream_t as void*) */
+void* divscope_stream(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DIVSCOPE_H */

@@ -1,0 +1,196 @@
+// oracle/_ref harness — TEST INFRASTRUCTURE ONLY.
+//
+// Compiles the reference's own hot-path sources (read from /root/reference at
+// build time, never copied into this repo) against the Eigen-API shim in
+// oracle/eigen_shim, and exposes them through a flat C ABI for the pytest
+// checkers, the golden-fixture generator and bench.py's reference arm.
+//
+//   rsvd.cpp is #included (not compiled separately) so that its
+//   anonymous-namespace multiply_sym (rsvd.cpp:18-36) — the reference's
+//   streaming pass — can be timed on its own.
+//   mds.cpp, distmat.cpp, align.cpp, seqio.cpp and tests/testdata.cpp are
+//   compiled as separate translation units by oracle/Makefile.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+// --impl reference) load the resulting library.
+#include "rsvd.cpp"  // NOLINT: intentional, see header comment
+
+#include <cstring>
+#include <string>
+
+#include "distmat.hpp"
+#include "error.hpp"
+#include "mds.hpp"
+#include "rng.hpp"
+#include "testdata.hpp"
+
+using namespace divscope;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return 0;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return static_cast<int>(e.code());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return static_cast<int>(errc::internal);
+    }
+}
+
+DistanceMatrix make_matrix(const double* v, std::size_t rows, std::size_t cols, int sym) {
+    DistanceMatrix d;
+    d.rows = rows;
+    d.cols = cols;
+    d.symmetric = sym != 0;
+    d.values.assign(v, v + rows * cols);
+    return d;
+}
+
+SolverOptions make_opts(std::size_t rank, std::size_t p, std::size_t q, std::uint64_t seed) {
+    SolverOptions o;
+    o.rank = rank;
+    o.oversampling = p;
+    o.power_iters = q;
+    o.seed = seed;
+    return o;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// rng.hpp:38-48 with engine std::mt19937_64(seed) as in rsvd.cpp:90-92
+void ref_fill_gaussian(std::uint64_t seed, double* out, std::size_t count) {
+    std::mt19937_64 eng(seed);
+    fill_gaussian(eng, out, count);
+}
+
+// raw engine stream (for pinning the restated engine)
+void ref_mt19937_64(std::uint64_t seed, std::uint64_t* out, std::size_t count) {
+    std::mt19937_64 eng(seed);
+    for (std::size_t i = 0; i < count; ++i) out[i] = eng();
+}
+
+// tests/testdata.cpp:157-163
+void ref_uniform_box(std::size_t n, std::size_t dim, std::uint64_t seed, double* out) {
+    const std::vector<double> p = testdata::uniform_box(n, dim, seed);
+    std::memcpy(out, p.data(), p.size() * sizeof(double));
+}
+
+// tests/testdata.cpp:165-184
+void ref_euclidean_matrix(const double* pts, std::size_t n, std::size_t dim, double* out) {
+    const std::vector<double> p(pts, pts + n * dim);
+    const DistanceMatrix d = testdata::euclidean_matrix(p, n, dim);
+    std::memcpy(out, d.values.data(), d.values.size() * sizeof(double));
+}
+
+// tests/testdata.cpp:28-37: reads of `length` over ACGT, concatenated
+void ref_random_reads(std::size_t count, std::size_t length, std::uint64_t seed, char* out) {
+    const ReadSet rs = testdata::random_reads(count, length, seed);
+    for (std::size_t i = 0; i < count; ++i)
+        std::memcpy(out + i * length, rs.reads[i].sequence.data(), length);
+}
+
+// src/mds.cpp:14-60
+int ref_gram(const double* d, std::size_t rows, std::size_t cols, int sym, unsigned threads,
+             double* g_out) {
+    return guarded([&] {
+        const GramMatrix g = gram_from_distances(make_matrix(d, rows, cols, sym), threads);
+        std::memcpy(g_out, g.values.data(), g.values.size() * sizeof(double));
+    });
+}
+
+// src/rsvd.cpp:18-36 (the streaming pass)
+void ref_multiply_sym(const double* g, std::size_t n, const double* m, std::size_t k,
+                      unsigned threads, double* out) {
+    RowMatrix mm(static_cast<Eigen::Index>(n), static_cast<Eigen::Index>(k));
+    std::memcpy(mm.data(), m, n * k * sizeof(double));
+    const RowMatrix r = multiply_sym(SymView{g, n}, mm, threads);
+    std::memcpy(out, r.data(), n * k * sizeof(double));
+}
+
+// src/rsvd.cpp:64-79
+double ref_frobenius_sq(const double* g, std::size_t n, unsigned threads) {
+    return frobenius_sq(SymView{g, n}, threads);
+}
+
+// src/rsvd.cpp:81-100; q_out is n x (rank + p)
+int ref_randomized_range(const double* g, std::size_t n, std::size_t rank, std::size_t p,
+                         std::size_t q, std::uint64_t seed, unsigned threads, double* q_out) {
+    return guarded([&] {
+        const RowMatrix r = randomized_range(SymView{g, n}, make_opts(rank, p, q, seed), threads);
+        std::memcpy(q_out, r.data(), static_cast<std::size_t>(r.size()) * sizeof(double));
+    });
+}
+
+// src/rsvd.cpp:102-145; vecs_out (may be NULL) is n x keep, keep <= rank
+int ref_eigs_sym(const double* g, std::size_t n, std::size_t rank, std::size_t p, std::size_t q,
+                 std::uint64_t seed, unsigned threads, double* vals_out, double* vecs_out,
+                 std::size_t* keep_out, double* resid_out) {
+    return guarded([&] {
+        const Spectrum s = eigs_sym(SymView{g, n}, make_opts(rank, p, q, seed), threads);
+        *keep_out = s.eigenvalues.size();
+        for (std::size_t i = 0; i < s.eigenvalues.size(); ++i) vals_out[i] = s.eigenvalues[i];
+        if (vecs_out)
+            std::memcpy(vecs_out, s.vectors.data(),
+                        static_cast<std::size_t>(s.vectors.size()) * sizeof(double));
+        *resid_out = s.resid;
+    });
+}
+
+// src/rsvd.cpp:147-178
+int ref_stable_rank(const double* g, std::size_t n, unsigned threads, double* out) {
+    return guarded([&] { *out = stable_rank(SymView{g, n}, threads); });
+}
+
+// src/mds.cpp:116-124 (+ embed_from_spectrum :81-114); coords_out holds n*rank
+int ref_embed(const double* g, std::size_t n, std::size_t rank, std::size_t p, std::size_t q,
+              std::uint64_t seed, unsigned threads, double* coords_out, double* evals_out,
+              std::size_t* r_out, double* mass_out, int* truncated_out) {
+    return guarded([&] {
+        const Embedding e = embed(SymView{g, n}, rank, make_opts(rank, p, q, seed), threads);
+        *r_out = e.r;
+        std::memcpy(coords_out, e.coords.data(), e.coords.size() * sizeof(double));
+        for (std::size_t i = 0; i < e.eigenvalues.size(); ++i) evals_out[i] = e.eigenvalues[i];
+        *mass_out = e.dropped_negative_mass;
+        *truncated_out = e.truncated ? 1 : 0;
+    });
+}
+
+// src/mds.cpp:126-150
+double ref_reconstruction_error(const double* g, std::size_t n, const double* coords,
+                                std::size_t r, unsigned threads) {
+    Embedding e;
+    e.n = n;
+    e.r = r;
+    e.coords.assign(coords, coords + n * r);
+    return reconstruction_error(SymView{g, n}, e, threads);
+}
+
+// src/distmat.cpp:169-187
+int ref_write_matrix(const char* path, const double* v, std::size_t rows, std::size_t cols,
+                     int sym) {
+    return guarded([&] { write_matrix(make_matrix(v, rows, cols, sym), path); });
+}
+
+// src/distmat.cpp:189-222; call with v=NULL to query the shape
+int ref_read_matrix(const char* path, double* v, std::size_t* rows, std::size_t* cols,
+                    int* sym) {
+    return guarded([&] {
+        const DistanceMatrix d = read_matrix(path);
+        *rows = d.rows;
+        *cols = d.cols;
+        *sym = d.symmetric ? 1 : 0;
+        if (v) std::memcpy(v, d.values.data(), d.values.size() * sizeof(double));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,422 @@
+"""divscope-b200: B200-native drop-in for the randomized classical-MDS path of
+the reference ``divscope`` toolkit (arXiv:1803.02272).
+
+This module is the Python (ctypes) binding of the C ABI in
+``include/divscope.h`` — the same binding a maintainer of the reference would
+write against its shared library. Names, argument meaning
+and error behaviour follow the reference's C API
+(/root/reference/proj/include/divscope.h:130-185, src/capi.cpp:286-414):
+
+* every failing call raises :class:`DivscopeError` carrying the reference
+  status code and the thread-local message (``divscope_last_error``);
+* ``threads`` arguments are accepted and ignored (the GPU path is
+  thread-count independent);
+* there is no CPU fallback: importing fails loudly when the CUDA library has
+  not been built, and compute calls fail with ``DIVSCOPE_ERR_INTERNAL`` when
+  no sm_100 device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from pathlib import Path
+from typing import Sequence
+
+import numpy as np
+
+__all__ = [
+    "Status", "DivscopeError", "SolverOptions", "Matrix", "Embedding", "Stats", "lib",
+    "matrix_from_host", "matrix_from_host_f32", "matrix_read", "matrix_euclidean",
+    "matrix_hamming", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
+    "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
+    "stats_enable_timing", "stats_reset", "stats_get", "set_device", "LIB_PATH",
+]
+
+LIB_PATH = Path(__file__).resolve().parent / "libdivscope_b200.so"
+
+
+class Status(enum.IntEnum):
+    """ref include/divscope.h:22-42"""
+    OK = 0
+    ERR_IO = 1
+    ERR_EMPTY_INPUT = 2
+    ERR_INVALID_CHARACTER = 3
+    ERR_DUPLICATE_ID = 4
+    ERR_SAMPLE_TOO_LARGE = 5
+    ERR_EMPTY_SEQUENCE = 6
+    ERR_BAD_FORMAT = 7
+    ERR_TRUNCATED = 8
+    ERR_NOT_SYMMETRIC = 9
+    ERR_RANK_TOO_LARGE = 10
+    ERR_ZERO_MATRIX = 11
+    ERR_BAD_GAP = 12
+    ERR_SHAPE_MISMATCH = 13
+    ERR_MISSING_LABEL = 14
+    ERR_JOIN_ERROR = 15
+    ERR_BAD_AXIS = 16
+    ERR_INVALID_ARGUMENT = 17
+    ERR_INTERNAL = 18
+
+
+class DivscopeError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        self.status = Status(status)
+        self.message = message
+        super().__init__(f"{self.status.name}: {message}")
+
+
+class SolverOptions(C.Structure):
+    """ref include/divscope.h:132-137"""
+    _fields_ = [("rank", C.c_size_t), ("oversampling", C.c_size_t),
+                ("power_iters", C.c_size_t), ("seed", C.c_uint64)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("kernel_launches", C.c_uint64), ("product_launches", C.c_uint64),
+                ("product_ms", C.c_double), ("stats_launches", C.c_uint64),
+                ("stats_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_vp = C.c_void_p
+_sz = C.c_size_t
+_st = C.c_int
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: the CUDA library must be built first "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    L = C.CDLL(str(LIB_PATH))
+    sig = {
+        "divscope_status_name": ([_st], C.c_char_p),
+        "divscope_last_error": ([], C.c_char_p),
+        "divscope_version": ([], C.c_char_p),
+        "divscope_readset_from_ids": ([C.POINTER(C.c_char_p), _sz, C.POINTER(_vp)], _st),
+        "divscope_readset_size": ([_vp], _sz),
+        "divscope_readset_id": ([_vp, _sz], C.c_char_p),
+        "divscope_readset_free": ([_vp], None),
+        "divscope_matrix_from_host": ([_dp, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
+        "divscope_matrix_from_host_f32": ([_fp, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
+        "divscope_matrix_rows": ([_vp], _sz),
+        "divscope_matrix_cols": ([_vp], _sz),
+        "divscope_matrix_symmetric": ([_vp], C.c_int),
+        "divscope_matrix_get": ([_vp, _sz, _sz], C.c_double),
+        "divscope_matrix_copy_to_host": ([_vp, _dp], _st),
+        "divscope_matrix_write": ([_vp, C.c_char_p], _st),
+        "divscope_matrix_read": ([C.c_char_p, C.POINTER(_vp)], _st),
+        "divscope_matrix_free": ([_vp], None),
+        "divscope_matrix_euclidean": ([_dp, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
+        "divscope_matrix_hamming": ([C.c_char_p, _sz, _sz, C.POINTER(_vp)], _st),
+        "divscope_hamming_counts": ([C.c_char_p, _sz, _sz, C.POINTER(C.c_uint32)], _st),
+        "divscope_solver_options_init": ([C.POINTER(SolverOptions)], None),
+        "divscope_gram": ([_vp, C.c_uint, C.POINTER(_vp)], _st),
+        "divscope_eigs": ([_vp, C.POINTER(SolverOptions), C.c_uint, _dp, C.POINTER(_sz), _dp], _st),
+        "divscope_stable_rank": ([_vp, C.c_uint, _dp], _st),
+        "divscope_embed": ([_vp, C.POINTER(SolverOptions), C.c_uint, _vp, C.POINTER(_vp)], _st),
+        "divscope_embedding_rows": ([_vp], _sz),
+        "divscope_embedding_dims": ([_vp], _sz),
+        "divscope_embedding_id": ([_vp, _sz], C.c_char_p),
+        "divscope_embedding_get": ([_vp, _sz, _sz], C.c_double),
+        "divscope_embedding_eigenvalues": ([_vp, _dp, _sz], _sz),
+        "divscope_embedding_dropped_negative_mass": ([_vp], C.c_double),
+        "divscope_embedding_truncated": ([_vp], C.c_int),
+        "divscope_embedding_coords": ([_vp], _dp),
+        "divscope_embedding_resid": ([_vp], C.c_double),
+        "divscope_embedding_write": ([_vp, C.c_char_p, C.c_char_p], _st),
+        "divscope_embedding_load": ([C.c_char_p, C.POINTER(_vp)], _st),
+        "divscope_embedding_free": ([_vp], None),
+        "divscope_randomized_range": ([_vp, C.POINTER(SolverOptions), _dp], _st),
+        "divscope_synth_points": ([C.c_int, _sz, C.c_uint64, _dp, C.POINTER(_sz)], _st),
+        "divscope_synth_reads": ([_sz, _sz, _sz, C.c_double, C.c_uint64, C.c_char_p], _st),
+        "divscope_set_device": ([C.c_int], _st),
+        "divscope_stats_enable_timing": ([C.c_int], None),
+        "divscope_stats_reset": ([], None),
+        "divscope_stats_get": ([C.POINTER(Stats)], None),
+        "divscope_stream": ([], _vp),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    return L
+
+
+lib = _load()
+
+#: every symbol include/divscope.h declares (checked by the CPU test-suite)
+EXPORTED = sorted(n for n in dir(lib) if n.startswith("divscope_"))
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise DivscopeError(status, (lib.divscope_last_error() or b"").decode())
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def solver_options_init() -> SolverOptions:
+    """ref capi.cpp:288-294 (rank 50, oversampling 10, power_iters 2, seed 0)"""
+    o = SolverOptions()
+    lib.divscope_solver_options_init(C.byref(o))
+    return o
+
+
+def _opts(rank=None, oversampling=None, power_iters=None, seed=None, opts=None) -> SolverOptions:
+    o = opts if opts is not None else solver_options_init()
+    if rank is not None:
+        o.rank = rank
+    if oversampling is not None:
+        o.oversampling = oversampling
+    if power_iters is not None:
+        o.power_iters = power_iters
+    if seed is not None:
+        o.seed = seed
+    return o
+
+
+class Matrix:
+    """Owning wrapper of a ``divscope_matrix*`` (device resident)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.divscope_matrix_free(h)
+            self._h = C.c_void_p()
+
+    @property
+    def rows(self) -> int:
+        return lib.divscope_matrix_rows(self._h)
+
+    @property
+    def cols(self) -> int:
+        return lib.divscope_matrix_cols(self._h)
+
+    @property
+    def symmetric(self) -> bool:
+        return bool(lib.divscope_matrix_symmetric(self._h))
+
+    def get(self, i: int, j: int) -> float:
+        return lib.divscope_matrix_get(self._h, i, j)
+
+    def to_numpy(self) -> np.ndarray:
+        out = np.empty((self.rows, self.cols), np.float64)
+        _check(lib.divscope_matrix_copy_to_host(self._h, out.ctypes.data_as(_dp)))
+        return out
+
+    def write(self, path) -> None:
+        _check(lib.divscope_matrix_write(self._h, str(path).encode()))
+
+
+def _new_matrix(fn, *args) -> Matrix:
+    h = _vp()
+    _check(fn(*args, C.byref(h)))
+    return Matrix(h.value)
+
+
+def matrix_from_host(values: np.ndarray, symmetric: bool = True) -> Matrix:
+    a = _f64(values)
+    rows, cols = a.shape
+    return _new_matrix(lib.divscope_matrix_from_host, a.ctypes.data_as(_dp), rows, cols,
+                       int(symmetric))
+
+
+def matrix_from_host_f32(values: np.ndarray, symmetric: bool = True) -> Matrix:
+    a = np.ascontiguousarray(values, dtype=np.float32)
+    rows, cols = a.shape
+    return _new_matrix(lib.divscope_matrix_from_host_f32, a.ctypes.data_as(_fp), rows, cols,
+                       int(symmetric))
+
+
+def matrix_read(path) -> Matrix:
+    return _new_matrix(lib.divscope_matrix_read, str(path).encode())
+
+
+def matrix_euclidean(points: np.ndarray, store_f32: bool = False) -> Matrix:
+    p = _f64(points)
+    n, dim = p.shape
+    return _new_matrix(lib.divscope_matrix_euclidean, p.ctypes.data_as(_dp), n, dim,
+                       int(store_f32))
+
+
+def _reads_bytes(reads) -> tuple[bytes, int, int]:
+    if isinstance(reads, (bytes, bytearray)):
+        raise TypeError("pass a list of equal-length reads")
+    reads = [r.encode() if isinstance(r, str) else bytes(r) for r in reads]
+    if not reads:
+        return b"", 0, 0
+    length = len(reads[0])
+    if any(len(r) != length for r in reads):
+        raise DivscopeError(Status.ERR_SHAPE_MISMATCH, "reads must have equal length")
+    return b"".join(reads), len(reads), length
+
+
+def matrix_hamming(reads: Sequence[str | bytes]) -> Matrix:
+    buf, count, length = _reads_bytes(reads)
+    return _new_matrix(lib.divscope_matrix_hamming, buf, count, length)
+
+
+def hamming_counts(reads: Sequence[str | bytes]) -> np.ndarray:
+    buf, count, length = _reads_bytes(reads)
+    out = np.empty((count, count), np.uint32)
+    _check(lib.divscope_hamming_counts(buf, count, length, out.ctypes.data_as(C.POINTER(C.c_uint32))))
+    return out
+
+
+def gram(dist: Matrix, threads: int = 1) -> Matrix:
+    """ref divscope_gram (capi.cpp:296-307): lazy gram handle."""
+    return _new_matrix(lib.divscope_gram, dist.handle, threads)
+
+
+def eigs(g: Matrix, rank=None, oversampling=None, power_iters=None, seed=None, opts=None,
+         threads: int = 1) -> tuple[np.ndarray, float]:
+    """ref divscope_eigs (capi.cpp:309-325): (eigenvalues[count], resid)."""
+    o = _opts(rank, oversampling, power_iters, seed, opts)
+    vals = np.zeros(max(int(o.rank), 1), np.float64)
+    count = _sz(0)
+    resid = C.c_double(-1.0)
+    _check(lib.divscope_eigs(g.handle, C.byref(o), threads, vals.ctypes.data_as(_dp),
+                             C.byref(count), C.byref(resid)))
+    return vals[: count.value].copy(), resid.value
+
+
+def stable_rank(g: Matrix, threads: int = 1) -> float:
+    out = C.c_double(0.0)
+    _check(lib.divscope_stable_rank(g.handle, threads, C.byref(out)))
+    return out.value
+
+
+def randomized_range(g: Matrix, rank=None, oversampling=None, power_iters=None, seed=None,
+                     opts=None) -> np.ndarray:
+    o = _opts(rank, oversampling, power_iters, seed, opts)
+    n = g.rows
+    out = np.zeros((n, int(o.rank + o.oversampling)), np.float64)
+    _check(lib.divscope_randomized_range(g.handle, C.byref(o), out.ctypes.data_as(_dp)))
+    return out
+
+
+class Embedding:
+    """Owning wrapper of a ``divscope_embedding*`` (coordinates on the host)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.divscope_embedding_free(h)
+            self._h = C.c_void_p()
+
+    @property
+    def rows(self) -> int:
+        return lib.divscope_embedding_rows(self._h)
+
+    @property
+    def dims(self) -> int:
+        return lib.divscope_embedding_dims(self._h)
+
+    def id(self, i: int) -> str | None:
+        s = lib.divscope_embedding_id(self._h, i)
+        return None if s is None else s.decode()
+
+    def get(self, i: int, c: int) -> float:
+        return lib.divscope_embedding_get(self._h, i, c)
+
+    @property
+    def coords(self) -> np.ndarray:
+        n, r = self.rows, self.dims
+        if n * r == 0:
+            return np.zeros((n, r))
+        p = lib.divscope_embedding_coords(self._h)
+        return np.ctypeslib.as_array(p, shape=(n * r,)).reshape(n, r).copy()
+
+    @property
+    def eigenvalues(self) -> np.ndarray:
+        k = lib.divscope_embedding_eigenvalues(self._h, None, 0)
+        out = np.zeros(max(k, 1))
+        lib.divscope_embedding_eigenvalues(self._h, out.ctypes.data_as(_dp), k)
+        return out[:k].copy()
+
+    @property
+    def dropped_negative_mass(self) -> float:
+        return lib.divscope_embedding_dropped_negative_mass(self._h)
+
+    @property
+    def truncated(self) -> bool:
+        return bool(lib.divscope_embedding_truncated(self._h))
+
+    @property
+    def resid(self) -> float:
+        return lib.divscope_embedding_resid(self._h)
+
+    def write(self, tsv_path, meta_path=None) -> None:
+        _check(lib.divscope_embedding_write(self._h, str(tsv_path).encode(),
+                                            None if meta_path is None else str(meta_path).encode()))
+
+
+def embed(g: Matrix, rank=None, oversampling=None, power_iters=None, seed=None, opts=None,
+          ids: Sequence[str] | None = None, threads: int = 1) -> Embedding:
+    """ref divscope_embed (capi.cpp:337-354)."""
+    o = _opts(rank, oversampling, power_iters, seed, opts)
+    rs = _vp()
+    try:
+        if ids is not None:
+            arr = (C.c_char_p * len(ids))(*[s.encode() for s in ids])
+            _check(lib.divscope_readset_from_ids(arr, len(ids), C.byref(rs)))
+        h = _vp()
+        _check(lib.divscope_embed(g.handle, C.byref(o), threads, rs, C.byref(h)))
+        return Embedding(h.value)
+    finally:
+        if rs.value:
+            lib.divscope_readset_free(rs)
+
+
+def embedding_load(path) -> Embedding:
+    h = _vp()
+    _check(lib.divscope_embedding_load(str(path).encode(), C.byref(h)))
+    return Embedding(h.value)
+
+
+def synth_points(config: int, n: int, seed: int) -> np.ndarray:
+    dims = {1: 20, 2: 50, 3: 100, 4: 64}
+    out = np.empty((n, dims[config]), np.float64)
+    d = _sz(0)
+    _check(lib.divscope_synth_points(config, n, seed, out.ctypes.data_as(_dp), C.byref(d)))
+    return out
+
+
+def synth_reads(count: int, length: int = 400, ancestors: int = 50, sub_rate: float = 0.05,
+                seed: int = 0) -> list[bytes]:
+    buf = C.create_string_buffer(count * length)
+    _check(lib.divscope_synth_reads(count, length, ancestors, sub_rate, seed, buf))
+    raw = buf.raw
+    return [raw[i * length:(i + 1) * length] for i in range(count)]
+
+
+def set_device(device: int) -> None:
+    _check(lib.divscope_set_device(device))
+
+
+def stats_enable_timing(on: bool = True) -> None:
+    lib.divscope_stats_enable_timing(int(on))
+
+
+def stats_reset() -> None:
+    lib.divscope_stats_reset()
+
+
+def stats_get() -> Stats:
+    s = Stats()
+    lib.divscope_stats_get(C.byref(s))
+    return s

@@ -1,0 +1,492 @@
+// C ABI of divscope-b200 (include/divscope.h). Mirrors the reference's MDS
+// section of the C API (ref src/capi.cpp:37-103, :286-414): status mapping,
+// thread-local last error, `wrap` semantics (nothing throws across the ABI),
+// NULL checks, out-handles written only on success, option defaults and the
+// clamp / error precedence of divscope_eigs / divscope_embed.
+#include "divscope.h"
+
+#include <charconv>
+#include <cstring>
+#include <fstream>
+#include <new>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "solver.hpp"
+
+using dsb::errc;
+using dsb::Error;
+
+struct divscope_readset {
+    std::vector<std::string> ids;
+};
+struct divscope_matrix {
+    dsb::Matrix m;
+};
+struct divscope_embedding {
+    std::vector<std::string> ids;
+    dsb::Embedding emb;
+};
+
+namespace {
+
+thread_local std::string g_last_error;  // ref capi.cpp:39
+
+divscope_status map_errc(errc c) { return static_cast<divscope_status>(static_cast<int>(c)); }
+
+template <typename F>
+divscope_status wrap(F&& f) noexcept {  // ref capi.cpp:66-82
+    try {
+        f();
+        g_last_error.clear();
+        return DIVSCOPE_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return map_errc(e.code());
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of memory";
+        return DIVSCOPE_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return DIVSCOPE_ERR_INTERNAL;
+    }
+}
+
+divscope_status fail_invalid(const char* msg) {  // ref capi.cpp:84-87
+    g_last_error = msg;
+    return DIVSCOPE_ERR_INVALID_ARGUMENT;
+}
+
+dsb::SolverOptions to_options(const divscope_solver_options* o) {  // ref capi.cpp:94-103
+    dsb::SolverOptions opts;
+    if (o) {
+        opts.rank = o->rank;
+        opts.oversampling = o->oversampling;
+        opts.power_iters = o->power_iters;
+        opts.seed = o->seed;
+    }
+    return opts;
+}
+
+std::vector<std::string> index_ids(size_t n) {
+    std::vector<std::string> ids;
+    ids.reserve(n);
+    for (size_t i = 0; i < n; ++i) ids.push_back(std::to_string(i));
+    return ids;
+}
+
+// ref src/mds.cpp:152-188
+void write_embedding_tsv(const dsb::Embedding& e, const std::vector<std::string>& ids,
+                         const std::string& path) {
+    if (ids.size() != e.n) throw Error(errc::shape_mismatch, "id count does not match embedding");
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error(errc::io_error, "cannot open " + path + " for writing");
+    out << "id";
+    for (size_t c = 0; c < e.r; ++c) out << "\tdim" << (c + 1);
+    out << '\n';
+    for (size_t i = 0; i < e.n; ++i) {
+        out << ids[i];
+        for (size_t c = 0; c < e.r; ++c) out << '\t' << dsb::format_double(e.coords[i * e.r + c]);
+        out << '\n';
+    }
+    if (!out.flush()) throw Error(errc::io_error, "failed writing " + path);
+}
+
+void write_embedding_meta(const dsb::Embedding& e, const std::string& path) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error(errc::io_error, "cannot open " + path + " for writing");
+    out << "rank=" << e.r << '\n';
+    out << "truncated=" << (e.truncated ? 1 : 0) << '\n';
+    out << "eigenvalues=";
+    for (size_t i = 0; i < e.eigenvalues.size(); ++i) {
+        if (i) out << ',';
+        out << dsb::format_double(e.eigenvalues[i]);
+    }
+    out << '\n';
+    out << "dropped_negative_mass=" << dsb::format_double(e.dropped_negative_mass) << '\n';
+    if (!out.flush()) throw Error(errc::io_error, "failed writing " + path);
+}
+
+// ref src/mds.cpp:190-238
+void load_embedding_tsv(const std::string& path, std::vector<std::string>& ids, size_t& dims,
+                        std::vector<double>& coords) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw Error(errc::io_error, "cannot open " + path);
+    std::string line;
+    if (!std::getline(in, line)) throw Error(errc::bad_format, path + ": empty embedding table");
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    dims = 0;
+    {
+        std::istringstream header(line);
+        std::string tok;
+        if (!std::getline(header, tok, '\t') || tok != "id")
+            throw Error(errc::bad_format, path + ": missing id header column");
+        while (std::getline(header, tok, '\t')) ++dims;
+        if (dims == 0) throw Error(errc::bad_format, path + ": no dimension columns");
+    }
+    size_t lineno = 1;
+    while (std::getline(in, line)) {
+        ++lineno;
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        if (line.empty()) continue;
+        std::istringstream row(line);
+        std::string tok;
+        if (!std::getline(row, tok, '\t') || tok.empty())
+            throw Error(errc::bad_format, path + ": missing id on line " + std::to_string(lineno));
+        ids.push_back(tok);
+        size_t got = 0;
+        while (std::getline(row, tok, '\t')) {
+            char* endp = nullptr;
+            const double v = std::strtod(tok.c_str(), &endp);
+            if (endp == tok.c_str() || *endp != '\0')
+                throw Error(errc::bad_format, path + ": bad number '" + tok + "' on line " +
+                                                  std::to_string(lineno));
+            coords.push_back(v);
+            ++got;
+        }
+        if (got != dims)
+            throw Error(errc::bad_format, path + ": expected " + std::to_string(dims) +
+                                              " coordinates on line " + std::to_string(lineno));
+    }
+    if (ids.empty()) throw Error(errc::empty_input, path + ": no embedding rows");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* divscope_status_name(divscope_status s) {  // ref capi.cpp:116-139
+    switch (s) {
+        case DIVSCOPE_OK: return "ok";
+        case DIVSCOPE_ERR_IO: return "io_error";
+        case DIVSCOPE_ERR_EMPTY_INPUT: return "empty_input";
+        case DIVSCOPE_ERR_INVALID_CHARACTER: return "invalid_character";
+        case DIVSCOPE_ERR_DUPLICATE_ID: return "duplicate_id";
+        case DIVSCOPE_ERR_SAMPLE_TOO_LARGE: return "sample_too_large";
+        case DIVSCOPE_ERR_EMPTY_SEQUENCE: return "empty_sequence";
+        case DIVSCOPE_ERR_BAD_FORMAT: return "bad_format";
+        case DIVSCOPE_ERR_TRUNCATED: return "truncated";
+        case DIVSCOPE_ERR_NOT_SYMMETRIC: return "not_symmetric";
+        case DIVSCOPE_ERR_RANK_TOO_LARGE: return "rank_too_large";
+        case DIVSCOPE_ERR_ZERO_MATRIX: return "zero_matrix";
+        case DIVSCOPE_ERR_BAD_GAP: return "bad_gap";
+        case DIVSCOPE_ERR_SHAPE_MISMATCH: return "shape_mismatch";
+        case DIVSCOPE_ERR_MISSING_LABEL: return "missing_label";
+        case DIVSCOPE_ERR_JOIN_ERROR: return "join_error";
+        case DIVSCOPE_ERR_BAD_AXIS: return "bad_axis";
+        case DIVSCOPE_ERR_INVALID_ARGUMENT: return "invalid_argument";
+        case DIVSCOPE_ERR_INTERNAL: return "internal";
+    }
+    return "internal";
+}
+
+const char* divscope_last_error(void) { return g_last_error.c_str(); }
+
+const char* divscope_version(void) { return "1.0.0-b200"; }
+
+/* ---- readsets (ids only) ---- */
+
+divscope_status divscope_readset_from_ids(const char* const* ids, size_t count,
+                                          divscope_readset** out) {
+    if ((!ids && count) || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        auto* rs = new divscope_readset;
+        for (size_t i = 0; i < count; ++i) {
+            if (!ids[i]) {
+                delete rs;
+                throw Error(errc::invalid_argument, "null id");
+            }
+            rs->ids.emplace_back(ids[i]);
+        }
+        *out = rs;
+    });
+}
+
+size_t divscope_readset_size(const divscope_readset* rs) { return rs ? rs->ids.size() : 0; }
+
+const char* divscope_readset_id(const divscope_readset* rs, size_t i) {
+    if (!rs || i >= rs->ids.size()) return nullptr;
+    return rs->ids[i].c_str();
+}
+
+void divscope_readset_free(divscope_readset* rs) { delete rs; }
+
+/* ---- matrices ---- */
+
+divscope_status divscope_matrix_from_host(const double* values, size_t rows, size_t cols,
+                                          int symmetric, divscope_matrix** out) {
+    if ((!values && rows * cols != 0) || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m = dsb::matrix_from_host(values, rows, cols, symmetric != 0, dsb::DType::F64);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+divscope_status divscope_matrix_from_host_f32(const float* values, size_t rows, size_t cols,
+                                              int symmetric, divscope_matrix** out) {
+    if ((!values && rows * cols != 0) || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m = dsb::matrix_from_host(values, rows, cols, symmetric != 0, dsb::DType::F32);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+size_t divscope_matrix_rows(const divscope_matrix* m) { return m ? m->m.store->rows : 0; }
+size_t divscope_matrix_cols(const divscope_matrix* m) { return m ? m->m.store->cols : 0; }
+int divscope_matrix_symmetric(const divscope_matrix* m) {
+    return m && m->m.store->symmetric ? 1 : 0;
+}
+
+double divscope_matrix_get(const divscope_matrix* m, size_t i, size_t j) {
+    if (!m || i >= m->m.store->rows || j >= m->m.store->cols) return 0.0;
+    double v = 0.0;
+    const divscope_status st = wrap([&] { v = dsb::matrix_get(m->m, i, j); });
+    return st == DIVSCOPE_OK ? v : 0.0;
+}
+
+divscope_status divscope_matrix_copy_to_host(const divscope_matrix* m, double* out) {
+    if (!m || (!out && m->m.store->rows * m->m.store->cols != 0)) return fail_invalid("null argument");
+    return wrap([&] { dsb::matrix_to_host(m->m, out); });
+}
+
+divscope_status divscope_matrix_write(const divscope_matrix* m, const char* dvs_path) {
+    if (!m || !dvs_path) return fail_invalid("null argument");
+    return wrap([&] {
+        const dsb::Store& s = *m->m.store;
+        std::vector<double> host(s.rows * s.cols);
+        dsb::matrix_to_host(m->m, host.data());
+        dsb::write_dvs(dvs_path, s.rows, s.cols, m->m.gram ? true : s.symmetric, host.data());
+    });
+}
+
+divscope_status divscope_matrix_read(const char* dvs_path, divscope_matrix** out) {
+    if (!dvs_path || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        size_t rows = 0, cols = 0;
+        bool sym = false;
+        const std::vector<double> v = dsb::read_dvs(dvs_path, rows, cols, sym);
+        dsb::Matrix m = dsb::matrix_from_host(v.data(), rows, cols, sym, dsb::DType::F64);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+void divscope_matrix_free(divscope_matrix* m) { delete m; }
+
+divscope_status divscope_matrix_euclidean(const double* points, size_t n, size_t dim,
+                                          int store_f32, divscope_matrix** out) {
+    if (!points || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m = dsb::matrix_euclidean(points, n, dim, store_f32 != 0);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+divscope_status divscope_matrix_hamming(const char* reads, size_t count, size_t length,
+                                        divscope_matrix** out) {
+    if (!reads || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m = dsb::matrix_hamming(reads, count, length);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+divscope_status divscope_hamming_counts(const char* reads, size_t count, size_t length,
+                                        uint32_t* out) {
+    if (!reads || !out) return fail_invalid("null argument");
+    return wrap([&] { dsb::hamming_counts(reads, count, length, out); });
+}
+
+/* ---- spectra and embeddings ---- */
+
+void divscope_solver_options_init(divscope_solver_options* o) {  // ref capi.cpp:288-294
+    if (!o) return;
+    o->rank = 50;
+    o->oversampling = 10;
+    o->power_iters = 2;
+    o->seed = 0;
+}
+
+divscope_status divscope_gram(const divscope_matrix* dist, unsigned threads,
+                              divscope_matrix** out) {  // ref capi.cpp:296-307
+    (void)threads;
+    if (!dist || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix g = dsb::gram_from_distances(dist->m);
+        *out = new divscope_matrix{std::move(g)};
+    });
+}
+
+divscope_status divscope_eigs(const divscope_matrix* gram, const divscope_solver_options* opts,
+                              unsigned threads, double* eigenvalues, size_t* count,
+                              double* resid) {  // ref capi.cpp:309-325
+    (void)threads;
+    if (!gram || !opts || !eigenvalues) return fail_invalid("null argument");
+    return wrap([&] {
+        if (gram->m.store->rows != gram->m.store->cols)
+            throw Error(errc::not_symmetric, "matrix is not square");
+        const dsb::Spectrum s = dsb::eigs_sym(gram->m, to_options(opts));
+        for (size_t i = 0; i < s.eigenvalues.size(); ++i) eigenvalues[i] = s.eigenvalues[i];
+        if (count) *count = s.eigenvalues.size();
+        if (resid) *resid = s.resid;
+    });
+}
+
+divscope_status divscope_stable_rank(const divscope_matrix* gram, unsigned threads,
+                                     double* out) {  // ref capi.cpp:327-335
+    (void)threads;
+    if (!gram || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        if (gram->m.store->rows != gram->m.store->cols)
+            throw Error(errc::not_symmetric, "matrix is not square");
+        *out = dsb::stable_rank(gram->m);
+    });
+}
+
+divscope_status divscope_embed(const divscope_matrix* gram, const divscope_solver_options* opts,
+                               unsigned threads, const divscope_readset* ids,
+                               divscope_embedding** out) {  // ref capi.cpp:337-354
+    (void)threads;
+    if (!gram || !opts || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        if (gram->m.store->rows != gram->m.store->cols)
+            throw Error(errc::not_symmetric, "matrix is not square");
+        if (ids && ids->ids.size() != gram->m.store->rows)
+            throw Error(errc::shape_mismatch, "id count does not match matrix");
+        dsb::Embedding e = dsb::embed(gram->m, opts->rank, to_options(opts));
+        auto* handle = new divscope_embedding;
+        handle->ids = ids ? ids->ids : index_ids(e.n);
+        handle->emb = std::move(e);
+        *out = handle;
+    });
+}
+
+divscope_status divscope_randomized_range(const divscope_matrix* gram,
+                                          const divscope_solver_options* opts, double* q_out) {
+    if (!gram || !opts || !q_out) return fail_invalid("null argument");
+    return wrap([&] {
+        if (gram->m.store->rows != gram->m.store->cols)
+            throw Error(errc::not_symmetric, "matrix is not square");
+        dsb::randomized_range(gram->m, to_options(opts), q_out);
+    });
+}
+
+size_t divscope_embedding_rows(const divscope_embedding* e) { return e ? e->emb.n : 0; }
+size_t divscope_embedding_dims(const divscope_embedding* e) { return e ? e->emb.r : 0; }
+
+const char* divscope_embedding_id(const divscope_embedding* e, size_t i) {
+    if (!e || i >= e->ids.size()) return nullptr;
+    return e->ids[i].c_str();
+}
+
+double divscope_embedding_get(const divscope_embedding* e, size_t i, size_t c) {
+    if (!e || i >= e->emb.n || c >= e->emb.r) return 0.0;
+    return e->emb.coords[i * e->emb.r + c];
+}
+
+size_t divscope_embedding_eigenvalues(const divscope_embedding* e, double* out, size_t cap) {
+    if (!e) return 0;
+    if (out)
+        for (size_t i = 0; i < e->emb.eigenvalues.size() && i < cap; ++i)
+            out[i] = e->emb.eigenvalues[i];
+    return e->emb.eigenvalues.size();
+}
+
+double divscope_embedding_dropped_negative_mass(const divscope_embedding* e) {
+    return e ? e->emb.dropped_negative_mass : 0.0;
+}
+
+int divscope_embedding_truncated(const divscope_embedding* e) {
+    return e && e->emb.truncated ? 1 : 0;
+}
+
+const double* divscope_embedding_coords(const divscope_embedding* e) {
+    if (!e || e->emb.coords.empty()) return nullptr;
+    return e->emb.coords.data();
+}
+
+double divscope_embedding_resid(const divscope_embedding* e) { return e ? e->emb.resid : 0.0; }
+
+divscope_status divscope_embedding_write(const divscope_embedding* e, const char* tsv_path,
+                                         const char* meta_path) {
+    if (!e || !tsv_path) return fail_invalid("null argument");
+    return wrap([&] {
+        write_embedding_tsv(e->emb, e->ids, tsv_path);
+        if (meta_path) write_embedding_meta(e->emb, meta_path);
+    });
+}
+
+divscope_status divscope_embedding_load(const char* tsv_path, divscope_embedding** out) {
+    if (!tsv_path || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        auto* handle = new divscope_embedding;
+        try {
+            size_t dims = 0;
+            load_embedding_tsv(tsv_path, handle->ids, dims, handle->emb.coords);
+            handle->emb.n = handle->ids.size();
+            handle->emb.r = dims;
+        } catch (...) {
+            delete handle;
+            throw;
+        }
+        *out = handle;
+    });
+}
+
+void divscope_embedding_free(divscope_embedding* e) { delete e; }
+
+/* ---- device / instrumentation ---- */
+
+divscope_status divscope_set_device(int device) {
+    return wrap([&] { dsb::Ctx::get().set_device(device); });
+}
+
+void divscope_stats_enable_timing(int on) {
+    try {
+        dsb::Ctx& c = dsb::Ctx::get();
+        std::lock_guard<std::recursive_mutex> lk(c.mu);
+        c.timing = on != 0;
+    } catch (...) {
+    }
+}
+
+void divscope_stats_reset(void) {
+    try {
+        dsb::Ctx& c = dsb::Ctx::get();
+        std::lock_guard<std::recursive_mutex> lk(c.mu);
+        c.drain_timing();
+        c.k2_ms = c.k1_ms = 0.0;
+        c.k2_launches = c.k1_launches = 0;
+        c.h2d = c.d2h = 0;
+        c.launches_base = dsb::kernel_launch_count();
+    } catch (...) {
+    }
+}
+
+void divscope_stats_get(divscope_stats* out) {
+    if (!out) return;
+    std::memset(out, 0, sizeof(*out));
+    try {
+        dsb::Ctx& c = dsb::Ctx::get();
+        std::lock_guard<std::recursive_mutex> lk(c.mu);
+        c.drain_timing();
+        out->kernel_launches = dsb::kernel_launch_count() - c.launches_base;
+        out->product_launches = c.k2_launches;
+        out->product_ms = c.k2_ms;
+        out->stats_launches = c.k1_launches;
+        out->stats_ms = c.k1_ms;
+        out->h2d_bytes = c.h2d;
+        out->d2h_bytes = c.d2h;
+    } catch (...) {
+    }
+}
+
+void* divscope_stream(void) {
+    try {
+        return dsb::Ctx::get().stream;
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+}  // extern "C"

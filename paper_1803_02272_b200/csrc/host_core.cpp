@@ -1,0 +1,281 @@
+// Host runtime of divscope-b200 (see host_core.hpp).
+#include "host_core.hpp"
+
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <charconv>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+
+namespace dsb {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+
+void count_launch(int k) { g_launches.fetch_add(static_cast<uint64_t>(k)); }
+uint64_t kernel_launch_count() { return g_launches.load(); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(errc::internal, std::string("CUDA error: ") + cudaGetErrorString(e) + " (" +
+                                        what + ")");
+}
+
+DevBuf::DevBuf(size_t b) : bytes(b) {
+    if (b == 0) return;
+    const cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        throw Error(errc::internal, "device out of memory allocating " + std::to_string(b) +
+                                        " bytes: " + cudaGetErrorString(e));
+    }
+}
+
+DevBuf::~DevBuf() {
+    if (p) cudaFree(p);
+}
+
+Ctx::Ctx() = default;
+
+Ctx& Ctx::get() {
+    static Ctx* c = new Ctx();  // never destroyed: avoids teardown-order issues with the driver
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (!c->inited_) c->init();
+    return *c;
+}
+
+void Ctx::init() {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw Error(errc::internal,
+                    "no usable CUDA device (divscope-b200 has no CPU fallback): " +
+                        std::string(cudaGetErrorString(e)));
+    int dev = 0;
+    DSB_CUDA(cudaGetDevice(&dev));
+    device = dev;
+    DSB_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    DSB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        throw Error(errc::internal, std::string("divscope-b200 needs an sm_100 device, found ") +
+                                        prop.name);
+    sms = prop.multiProcessorCount;
+    DSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    DSB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+        throw Error(errc::internal, "cuTensorMapEncodeTiled unavailable");
+    encode_fn_ = fn;
+    inited_ = true;
+}
+
+void Ctx::set_device(int dev) {
+    std::lock_guard<std::recursive_mutex> lk(mu);
+    DSB_CUDA(cudaSetDevice(dev));
+    if (inited_ && dev != device) {
+        arena_.clear();
+        if (stream) cudaStreamDestroy(stream);
+        stream = nullptr;
+        inited_ = false;
+    }
+    if (!inited_) init();
+}
+
+void* Ctx::scratch(const std::string& slot, size_t bytes) {
+    auto& b = arena_[slot];
+    if (!b || b->bytes < bytes) {
+        if (b) {
+            DSB_CUDA(cudaStreamSynchronize(stream));
+            b.reset();
+        }
+        b = std::make_unique<DevBuf>(std::max<size_t>(bytes, 256));
+    }
+    return b->p;
+}
+
+void Ctx::begin_timed(int kind, cudaEvent_t* a) {
+    (void)kind;
+    *a = nullptr;
+    if (!timing) return;
+    DSB_CUDA(cudaEventCreate(a));
+    DSB_CUDA(cudaEventRecord(*a, stream));
+}
+
+void Ctx::end_timed(int kind, cudaEvent_t a) {
+    if (kind == 1) ++k2_launches;
+    else ++k1_launches;
+    if (!timing || !a) return;
+    cudaEvent_t b;
+    DSB_CUDA(cudaEventCreate(&b));
+    DSB_CUDA(cudaEventRecord(b, stream));
+    pending.push_back({a, b, kind});
+}
+
+void Ctx::drain_timing() {
+    if (pending.empty()) return;
+    DSB_CUDA(cudaStreamSynchronize(stream));
+    for (auto& t : pending) {
+        float ms = 0.0f;
+        DSB_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+        (t.kind == 1 ? k2_ms : k1_ms) += ms;
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    pending.clear();
+}
+
+void Ctx::h2d_copy(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    DSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    h2d += bytes;
+}
+
+void Ctx::d2h_copy(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    DSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+    DSB_CUDA(cudaStreamSynchronize(stream));
+    d2h += bytes;
+}
+
+void Ctx::sync() {
+    DSB_CUDA(cudaStreamSynchronize(stream));
+    DSB_CUDA(cudaGetLastError());
+}
+
+bool Ctx::encode_tmap(CUtensorMap* map, const void* base, DType dt, size_t rows, size_t cols,
+                      size_t ld_elems) {
+    auto fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(encode_fn_);
+    const size_t esz = dt == DType::F64 ? 8 : 4;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems * esz)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(kBM)};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r =
+        fn(map, dt == DType::F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+           2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+std::shared_ptr<Store> make_store(size_t rows, size_t cols, bool symmetric, DType dt) {
+    auto s = std::make_shared<Store>();
+    s->rows = rows;
+    s->cols = cols;
+    s->symmetric = symmetric;
+    s->dt = dt;
+    // TMA needs 16-byte row pitch; keep rows 256-byte aligned
+    s->ld = round_up(std::max<size_t>(cols, 1), dt == DType::F64 ? 32 : 64);
+    const size_t esz = dt == DType::F64 ? 8 : 4;
+    s->buf = std::make_shared<DevBuf>(std::max<size_t>(rows, 1) * s->ld * esz);
+    return s;
+}
+
+void upload_rows(Store& s, const void* host, size_t host_ld_elems) {
+    Ctx& c = Ctx::get();
+    const size_t esz = s.dt == DType::F64 ? 8 : 4;
+    if (s.rows == 0 || s.cols == 0) return;
+    DSB_CUDA(cudaMemcpy2DAsync(s.buf->p, s.ld * esz, host, host_ld_elems * esz, s.cols * esz,
+                               s.rows, cudaMemcpyHostToDevice, c.stream));
+    c.h2d += s.rows * s.cols * esz;
+    if (s.ld > s.cols)  // zero the pitch padding so full-row reads stay clean
+        DSB_CUDA(cudaMemset2DAsync(static_cast<char*>(s.buf->p) + s.cols * esz, s.ld * esz, 0,
+                                   (s.ld - s.cols) * esz, s.rows, c.stream));
+}
+
+// ---- RNG: restatement of ref src/rng.hpp:16-48 ------------------------------
+double uniform_open_closed(std::mt19937_64& eng) {
+    return static_cast<double>((eng() >> 11) + 1) * 0x1.0p-53;
+}
+double uniform_closed_open(std::mt19937_64& eng) {
+    return static_cast<double>(eng() >> 11) * 0x1.0p-53;
+}
+uint64_t bounded_uint64(std::mt19937_64& eng, uint64_t bound) {
+    const uint64_t threshold = -bound % bound;
+    for (;;) {
+        const uint64_t x = eng();
+        if (x >= threshold) return x % bound;
+    }
+}
+void fill_gaussian(std::mt19937_64& eng, double* out, size_t n) {
+    const double two_pi = 6.283185307179586476925286766559;
+    size_t i = 0;
+    while (i < n) {
+        const double u1 = uniform_open_closed(eng);
+        const double u2 = uniform_closed_open(eng);
+        const double radius = std::sqrt(-2.0 * std::log(u1));
+        out[i++] = radius * std::cos(two_pi * u2);
+        if (i < n) out[i++] = radius * std::sin(two_pi * u2);
+    }
+}
+
+// ---- DVS1 (ref src/distmat.cpp:132-222; format ref distmat.hpp:42-44) -----
+namespace {
+constexpr char kMagic[4] = {'D', 'V', 'S', '1'};
+void put_le(std::string& b, uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) b.push_back(static_cast<char>((v >> (8 * i)) & 0xff));
+}
+uint64_t get_le(const unsigned char* p, int bytes) {
+    uint64_t v = 0;
+    for (int i = bytes - 1; i >= 0; --i) v = (v << 8) | p[i];
+    return v;
+}
+}  // namespace
+
+void write_dvs(const std::string& path, size_t rows, size_t cols, bool symmetric,
+               const double* values) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error(errc::io_error, "cannot open " + path + " for writing");
+    std::string header(kMagic, 4);
+    put_le(header, 1, 4);
+    put_le(header, rows, 8);
+    put_le(header, cols, 8);
+    put_le(header, symmetric ? 1u : 0u, 8);
+    out.write(header.data(), static_cast<std::streamsize>(header.size()));
+    // x86-64 is little-endian: the payload is the raw IEEE bytes
+    static_assert(sizeof(double) == 8, "");
+    out.write(reinterpret_cast<const char*>(values),
+              static_cast<std::streamsize>(rows * cols * sizeof(double)));
+    out.flush();
+    if (!out) throw Error(errc::io_error, "write failed for " + path);
+}
+
+std::vector<double> read_dvs(const std::string& path, size_t& rows, size_t& cols,
+                             bool& symmetric) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw Error(errc::io_error, "cannot open " + path);
+    unsigned char header[32];
+    in.read(reinterpret_cast<char*>(header), 32);
+    if (in.gcount() != 32) throw Error(errc::truncated, path + ": header truncated");
+    if (std::memcmp(header, kMagic, 4) != 0) throw Error(errc::bad_format, path + ": bad magic");
+    const uint64_t version = get_le(header + 4, 4);
+    if (version != 1)
+        throw Error(errc::bad_format, path + ": unsupported version " + std::to_string(version));
+    rows = get_le(header + 8, 8);
+    cols = get_le(header + 16, 8);
+    symmetric = (get_le(header + 24, 8) & 1) != 0;
+    if (symmetric && rows != cols)
+        throw Error(errc::bad_format, path + ": symmetric flag on non-square matrix");
+    const uint64_t count = rows * cols;
+    std::vector<double> v(count);
+    in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(count * 8));
+    if (static_cast<uint64_t>(in.gcount()) != count * 8)
+        throw Error(errc::truncated, path + ": payload truncated");
+    return v;
+}
+
+// ref src/textio.hpp:11-16 (shortest round-trip form)
+std::string format_double(double v) {
+    char buf[64];
+    auto res = std::to_chars(buf, buf + sizeof(buf), v);
+    return std::string(buf, res.ptr);
+}
+
+}  // namespace dsb

@@ -1,0 +1,156 @@
+// Host runtime of divscope-b200: error model, device context (stream,
+// workspace arena, instrumentation), device-resident matrix handles.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace dsb {
+
+// error codes: mirror of ref src/error.hpp:10-30 (and the C enum)
+enum class errc {
+    ok = 0,
+    io_error,
+    empty_input,
+    invalid_character,
+    duplicate_id,
+    sample_too_large,
+    empty_sequence,
+    bad_format,
+    truncated,
+    not_symmetric,
+    rank_too_large,
+    zero_matrix,
+    bad_gap,
+    shape_mismatch,
+    missing_label,
+    join_error,
+    bad_axis,
+    invalid_argument,
+    internal,
+};
+
+class Error : public std::runtime_error {
+public:
+    Error(errc code, const std::string& msg) : std::runtime_error(msg), code_(code) {}
+    errc code() const noexcept { return code_; }
+
+private:
+    errc code_;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define DSB_CUDA(call) ::dsb::cuda_check((call), #call)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    explicit DevBuf(size_t b);
+    ~DevBuf();
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct TimedPair {
+    cudaEvent_t a, b;
+    int kind;  // 0 = K1, 1 = K2
+};
+
+class Ctx {
+public:
+    static Ctx& get();
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    std::recursive_mutex mu;  // one solver at a time per process
+
+    // grow-only workspace arena
+    void* scratch(const std::string& slot, size_t bytes);
+
+    // instrumentation
+    bool timing = false;
+    uint64_t launches_base = 0;
+    uint64_t k2_launches = 0, k1_launches = 0, h2d = 0, d2h = 0;
+    double k2_ms = 0.0, k1_ms = 0.0;
+    std::vector<TimedPair> pending;
+    void begin_timed(int kind, cudaEvent_t* a);
+    void end_timed(int kind, cudaEvent_t a);
+    void drain_timing();
+
+    void h2d_copy(void* dst, const void* src, size_t bytes);
+    void d2h_copy(void* dst, const void* src, size_t bytes);
+    void sync();
+
+    bool encode_tmap(CUtensorMap* map, const void* base, DType dt, size_t rows, size_t cols,
+                     size_t ld_elems);
+
+    void set_device(int dev);
+
+private:
+    Ctx();
+    void init();
+    bool inited_ = false;
+    std::map<std::string, std::unique_ptr<DevBuf>> arena_;
+    void* encode_fn_ = nullptr;
+};
+
+// Device-resident dense matrix (row-major, leading dimension ld elements).
+struct Store {
+    size_t rows = 0, cols = 0, ld = 0;
+    bool symmetric = false;
+    DType dt = DType::F64;
+    std::shared_ptr<DevBuf> buf;
+    // cached TMA descriptor for the K2 streaming read
+    bool tmap_ok = false;
+    CUtensorMap tmap{};
+    // cached K1 results when used as an explicit symmetric matrix
+    bool stats_ok = false;
+    double stats[S_COUNT] = {};
+    std::shared_ptr<DevBuf> stats_dev;
+    std::mutex mu;
+};
+
+// Lazy gram: the distance store plus the centering terms of
+// gram_from_distances (ref mds.cpp:29-41). G itself is never formed.
+struct GramInfo {
+    size_t n = 0;
+    std::shared_ptr<DevBuf> row_mean;     // [n]
+    std::vector<double> row_mean_h;       // host copy (for _get / _write)
+    std::shared_ptr<DevBuf> scalars;      // [S_COUNT]
+    double sc[S_COUNT] = {};
+};
+
+size_t round_up(size_t x, size_t m);
+std::shared_ptr<Store> make_store(size_t rows, size_t cols, bool symmetric, DType dt);
+void upload_rows(Store& s, const void* host, size_t host_ld_elems);
+
+// reference RNG conventions (ref src/rng.hpp:16-48)
+double uniform_open_closed(std::mt19937_64& eng);
+double uniform_closed_open(std::mt19937_64& eng);
+uint64_t bounded_uint64(std::mt19937_64& eng, uint64_t bound);
+void fill_gaussian(std::mt19937_64& eng, double* out, size_t n);
+
+// DVS1 container (ref src/distmat.cpp:132-222)
+void write_dvs(const std::string& path, size_t rows, size_t cols, bool symmetric,
+               const double* values);
+std::vector<double> read_dvs(const std::string& path, size_t& rows, size_t& cols,
+                             bool& symmetric);
+
+std::string format_double(double v);
+
+}  // namespace dsb

@@ -1,0 +1,262 @@
+// K1 — pass 0 over the distance matrix (replaces the validation / row-mean
+// part of gram_from_distances, ref src/mds.cpp:14-41, and frobenius_sq,
+// ref src/rsvd.cpp:64-79).
+//
+// One read of D. The grid walks the upper-triangular pairs of 64x64 tiles
+// (I <= J); each CTA loads tile (I,J) and its mirror (J,I) with coalesced
+// 16-byte loads and produces, from that single read:
+//   * partial row sums of d^2 of both tiles -> part[J][rows of I] and
+//     part[I][rows of J] (disjoint slots, so no atomics; k1_rowmeans sums the
+//     slots of a row in tile order => deterministic),
+//   * sum of d^4 (closed-form ||G||_F^2), max |d| (all entries and the upper
+//     triangle), and max |d_ij - d_ji| by comparing the tile with the
+//     transposed mirror through shared memory.
+// HBM roofline: n^2 * sizeof(T) bytes read once (+ n^2/64 * 8 partial bytes).
+#include <cfloat>
+
+#include "device_utils.cuh"
+#include "kernels.cuh"
+
+namespace dsb {
+
+namespace {
+
+constexpr int kT = 64;          // tile edge
+constexpr int kK1Threads = 256; // 8 warps, 8 rows each
+
+template <typename T>
+struct Pair2;
+template <>
+struct Pair2<double> {
+    using V = double2;
+};
+template <>
+struct Pair2<float> {
+    using V = float2;
+};
+
+// load d[row][col], d[row][col+1] (zeros outside [0,n)), widened to double
+template <typename T>
+__device__ __forceinline__ void load2(const T* __restrict__ d, size_t ld, size_t n, size_t row,
+                                      size_t col, double& a0, double& a1) {
+    a0 = 0.0;
+    a1 = 0.0;
+    if (row >= n || col >= n) return;
+    const T* p = d + row * ld + col;
+    if (col + 1 < n) {
+        const typename Pair2<T>::V v = __ldg(reinterpret_cast<const typename Pair2<T>::V*>(p));
+        a0 = static_cast<double>(v.x);
+        a1 = static_cast<double>(v.y);
+    } else {
+        a0 = static_cast<double>(__ldg(p));
+    }
+}
+
+// (I, J) with I <= J from the linear index over the upper triangle, row-major
+__device__ __forceinline__ void pair_of(long long p, int nbt, int& I, int& J) {
+    const double nf = static_cast<double>(nbt);
+    double g = (2.0 * nf + 1.0 - sqrt((2.0 * nf + 1.0) * (2.0 * nf + 1.0) - 8.0 * (double)p)) / 2.0;
+    long long i = g <= 0.0 ? 0 : static_cast<long long>(g);
+    if (i > nbt - 1) i = nbt - 1;
+    auto off = [&](long long r) { return r * nbt - r * (r - 1) / 2; };
+    while (i > 0 && off(i) > p) --i;
+    while (i + 1 < nbt && off(i + 1) <= p) ++i;
+    I = static_cast<int>(i);
+    J = static_cast<int>(i + (p - off(i)));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kK1Threads) k1_tile_pairs(const T* __restrict__ d, size_t ld,
+                                                            int n, int nbt,
+                                                            double* __restrict__ part,
+                                                            size_t part_ld,
+                                                            double* __restrict__ cta_stats) {
+    __shared__ double mirror[kT][kT + 1];
+    __shared__ double red[4][kK1Threads / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long npairs = static_cast<long long>(nbt) * (nbt + 1) / 2;
+    double sum4 = 0.0, maxabs = 0.0, maxabs_up = 0.0, maxasym = 0.0;
+
+    for (long long p = blockIdx.x; p < npairs; p += gridDim.x) {
+        int I, J;
+        pair_of(p, nbt, I, J);
+        const size_t r0 = static_cast<size_t>(I) * kT, c0 = static_cast<size_t>(J) * kT;
+        // tile A = D[I rows][J cols]: warp handles rows warp + 8t, lane cols 2*lane..+1
+        double a[8][2];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            load2(d, ld, n, r0 + warp + 8 * t, c0 + 2 * lane, a[t][0], a[t][1]);
+        double b[8][2];
+        if (I != J) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                load2(d, ld, n, c0 + warp + 8 * t, r0 + 2 * lane, b[t][0], b[t][1]);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int r = warp + 8 * t;
+            const double s0 = a[t][0] * a[t][0], s1 = a[t][1] * a[t][1];
+            const double rs = warp_sum(s0 + s1);
+            if (lane == 0 && r0 + r < static_cast<size_t>(n)) part[J * part_ld + r0 + r] = rs;
+            sum4 += s0 * s0 + s1 * s1;
+            maxabs = fmax(maxabs, fmax(fabs(a[t][0]), fabs(a[t][1])));
+            const int cA = 2 * lane;
+            if (I != J || r <= cA) maxabs_up = fmax(maxabs_up, fabs(a[t][0]));
+            if (I != J || r <= cA + 1) maxabs_up = fmax(maxabs_up, fabs(a[t][1]));
+        }
+        if (I != J) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int r = warp + 8 * t;
+                const double s0 = b[t][0] * b[t][0], s1 = b[t][1] * b[t][1];
+                const double rs = warp_sum(s0 + s1);
+                if (lane == 0 && c0 + r < static_cast<size_t>(n)) part[I * part_ld + c0 + r] = rs;
+                sum4 += s0 * s0 + s1 * s1;
+                maxabs = fmax(maxabs, fmax(fabs(b[t][0]), fabs(b[t][1])));
+                mirror[r][2 * lane] = b[t][0];
+                mirror[r][2 * lane + 1] = b[t][1];
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int r = warp + 8 * t;
+                mirror[r][2 * lane] = a[t][0];
+                mirror[r][2 * lane + 1] = a[t][1];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int r = warp + 8 * t;
+            maxasym = fmax(maxasym, fabs(a[t][0] - mirror[2 * lane][r]));
+            maxasym = fmax(maxasym, fabs(a[t][1] - mirror[2 * lane + 1][r]));
+        }
+        __syncthreads();
+    }
+    // fixed-order block reduction (deterministic for a fixed grid)
+    sum4 = warp_sum(sum4);
+    maxabs = warp_max(maxabs);
+    maxabs_up = warp_max(maxabs_up);
+    maxasym = warp_max(maxasym);
+    if (lane == 0) {
+        red[0][warp] = sum4;
+        red[1][warp] = maxabs;
+        red[2][warp] = maxabs_up;
+        red[3][warp] = maxasym;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+        for (int w = 0; w < kK1Threads / 32; ++w) {
+            s += red[0][w];
+            m1 = fmax(m1, red[1][w]);
+            m2 = fmax(m2, red[2][w]);
+            m3 = fmax(m3, red[3][w]);
+        }
+        cta_stats[blockIdx.x * 4 + 0] = s;
+        cta_stats[blockIdx.x * 4 + 1] = m1;
+        cta_stats[blockIdx.x * 4 + 2] = m2;
+        cta_stats[blockIdx.x * 4 + 3] = m3;
+    }
+}
+
+// r_i = (sum over tile columns of part[J][i]) / n, plus per-block sums of
+// the raw row sums, r and r^2.
+__global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ part, size_t part_ld,
+                                                   int nbt, int n, double* __restrict__ row_mean,
+                                                   double* __restrict__ blk_stats) {
+    __shared__ double red[3][8];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double rowsum = 0.0, r = 0.0;
+    if (i < n) {
+        for (int J = 0; J < nbt; ++J) rowsum += part[static_cast<size_t>(J) * part_ld + i];
+        r = rowsum / static_cast<double>(n);
+        row_mean[i] = r;
+    }
+    double v0 = warp_sum(rowsum), v1 = warp_sum(r), v2 = warp_sum(r * r);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red[0][warp] = v0;
+        red[1][warp] = v1;
+        red[2][warp] = v2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0, s1 = 0, s2 = 0;
+        for (int w = 0; w < 8; ++w) {
+            s0 += red[0][w];
+            s1 += red[1][w];
+            s2 += red[2][w];
+        }
+        blk_stats[blockIdx.x * 3 + 0] = s0;
+        blk_stats[blockIdx.x * 3 + 1] = s1;
+        blk_stats[blockIdx.x * 3 + 2] = s2;
+    }
+}
+
+__global__ void k1_finalize(const double* __restrict__ cta_stats, int ncta,
+                            const double* __restrict__ blk_stats, int nblk, int n,
+                            double* __restrict__ scalars) {
+    if (threadIdx.x != 0) return;
+    double sum4 = 0, m1 = 0, m2 = 0, m3 = 0;
+    for (int c = 0; c < ncta; ++c) {
+        sum4 += cta_stats[c * 4 + 0];
+        m1 = fmax(m1, cta_stats[c * 4 + 1]);
+        m2 = fmax(m2, cta_stats[c * 4 + 2]);
+        m3 = fmax(m3, cta_stats[c * 4 + 3]);
+    }
+    double rows = 0, sr = 0, sr2 = 0;
+    for (int b = 0; b < nblk; ++b) {
+        rows += blk_stats[b * 3 + 0];
+        sr += blk_stats[b * 3 + 1];
+        sr2 += blk_stats[b * 3 + 2];
+    }
+    const double nf = static_cast<double>(n);
+    const double grand = sr / nf;
+    scalars[S_GRAND] = grand;
+    scalars[S_FRO2_LAZY] = 0.25 * (sum4 - 2.0 * nf * sr2 + nf * nf * grand * grand);
+    scalars[S_FRO2_EXPL] = rows;
+    scalars[S_MAXABS] = m1;
+    scalars[S_MAXABS_UP] = m2;
+    scalars[S_MAXASYM] = m3;
+    scalars[S_SUM4] = sum4;
+    scalars[S_SUMR] = sr;
+    scalars[S_SUMR2] = sr2;
+}
+
+}  // namespace
+
+size_t k1_part_elems(size_t n) {
+    const size_t nbt = (n + kT - 1) / kT;
+    return nbt * nbt * kT;
+}
+
+int k1_grid(size_t n, int sms) {
+    const long long nbt = static_cast<long long>((n + kT - 1) / kT);
+    const long long npairs = nbt * (nbt + 1) / 2;
+    const long long cap = static_cast<long long>(sms) * 6;
+    return static_cast<int>(npairs < cap ? npairs : cap);
+}
+
+void launch_k1(const void* d, DType dt, size_t ld, size_t n, const K1Work& w, double* row_mean,
+               double* scalars, int sms, cudaStream_t st) {
+    (void)sms;
+    const int nbt = static_cast<int>((n + kT - 1) / kT);
+    const size_t part_ld = static_cast<size_t>(nbt) * kT;
+    if (dt == DType::F64)
+        k1_tile_pairs<double><<<w.grid, kK1Threads, 0, st>>>(static_cast<const double*>(d), ld,
+                                                             static_cast<int>(n), nbt, w.part,
+                                                             part_ld, w.cta_stats);
+    else
+        k1_tile_pairs<float><<<w.grid, kK1Threads, 0, st>>>(static_cast<const float*>(d), ld,
+                                                            static_cast<int>(n), nbt, w.part,
+                                                            part_ld, w.cta_stats);
+    const int nblk = static_cast<int>((n + 255) / 256);
+    k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, part_ld, nbt, static_cast<int>(n), row_mean,
+                                      w.blk_stats);
+    k1_finalize<<<1, 32, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),
+                                  scalars);
+    count_launch(3);
+}
+
+}  // namespace dsb

@@ -1,0 +1,327 @@
+// K2 — the centered tall-skinny product Y = G X that replaces multiply_sym
+// over the materialized gram (ref src/rsvd.cpp:18-36, called 2q+2 times by
+// randomized_range / eigs_sym, rsvd.cpp:94-98 and :108; G built by
+// gram_from_distances, ref src/mds.cpp:43-58).
+//
+// G is never formed. With S = D o D, r the row means of S and g the grand
+// mean,  G X = -1/2 [ S X - r (1^T X) - 1 (r^T X) + g 1 (1^T X) ],  so the
+// streaming part is S X: D is read once per pass, squared in registers
+// (fp32 D is widened first, so d^2 is exact), and multiplied into the panel
+// on the FP64 tensor cores (mma.sync m8n8k4 f64 -> DMMA, measured 37.1 TF/s
+// vs 33.6 for DFMA on this B200; see profiles/).
+//
+// Structure (one CTA per SM, persistent, stream-K):
+//  * warp 8 = producer: one elected lane issues, per (row block, k tile)
+//    iteration, a TMA 2D load of the 128 x 128-byte D tile (SWIZZLE_128B) and
+//    a cp.async.bulk of the matching contiguous k4-interleaved panel chunk,
+//    both completing on the stage's mbarrier; a ring of `stages` buffers.
+//  * warps 0-7 = consumers: each owns 16 rows x WP columns of the 128-row
+//    block; per k4 step it reads 2 A fragments (swizzled smem, squared) and
+//    WP/8 B fragments (one contiguous 256-byte smem read each) and issues
+//    2*WP/8 DMMAs into register accumulators.
+//  * the flattened iteration space (row blocks x k tiles) is split evenly
+//    over the grid with the reference's own chunk rule (parallel.hpp:33-34),
+//    so every SM streams the same number of D bytes; a CTA flushes its
+//    accumulators to a private partial slot whenever its range crosses a row
+//    block. k2_reduce sums the slots of a block in CTA order (deterministic,
+//    run-to-run bit-identical) and applies the rank-3 centering.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "device_utils.cuh"
+#include "kernels.cuh"
+
+namespace dsb {
+
+namespace {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kTileBytes = kBM * 128;  // one D stage: 128 rows x 128 bytes
+
+template <typename TD>
+constexpr int kt_cols() {
+    return 128 / static_cast<int>(sizeof(TD));
+}
+
+template <int WP, typename TD>
+constexpr int stage_bytes() {
+    // D tile (1024-aligned for the 128B swizzle) + panel chunk, rounded to 1024
+    return ((kTileBytes + kt_cols<TD>() * WP * 8) + 1023) / 1024 * 1024;
+}
+
+__device__ __forceinline__ long long chunk_begin(long long total, long long c, long long P) {
+    return total * c / P;
+}
+
+// A(row r, col k) inside a TMA SWIZZLE_128B tile with 128-byte rows
+template <typename TD>
+__device__ __forceinline__ double load_a(const unsigned char* tile, int r, int k) {
+    if constexpr (sizeof(TD) == 8) {
+        const int off = r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3);
+        return *reinterpret_cast<const double*>(tile + off);
+    } else {
+        const int off = r * 128 + ((((k >> 2) ^ (r & 7))) << 4) + ((k & 3) << 2);
+        return static_cast<double>(*reinterpret_cast<const float*>(tile + off));
+    }
+}
+
+template <int WP, typename TD, bool SQUARE>
+__global__ void __launch_bounds__(kThreads, 1)
+    k2_product(const __grid_constant__ CUtensorMap tmD, const double* __restrict__ X, int nk,
+               long long total, double* __restrict__ part, int maxseg, int stages) {
+    constexpr int KT = kt_cols<TD>();
+    constexpr int K4 = KT / 4;
+    constexpr int NF = WP / 8;
+    constexpr int XB = KT * WP * 8;
+    constexpr int SB = stage_bytes<WP, TD>();
+
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * SB);
+    uint64_t* empty = full + stages;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long P = gridDim.x, c = blockIdx.x;
+    const long long t0 = chunk_begin(total, c, P), t1 = chunk_begin(total, c + 1, P);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            prefetch_tmap(&tmD);
+            int s = 0;
+            uint32_t ph = 0;
+            for (long long t = t0; t < t1; ++t) {
+                if (t - t0 >= stages) mbar_wait(&empty[s], ph ^ 1);
+                const int b = static_cast<int>(t / nk), kt = static_cast<int>(t % nk);
+                unsigned char* st = smem + static_cast<size_t>(s) * SB;
+                mbar_arrive_expect_tx(&full[s], kTileBytes + XB);
+                tma_load_2d(st, &tmD, kt * KT, b * kBM, &full[s]);
+                bulk_load(st + kTileBytes, X + static_cast<size_t>(kt) * KT * WP, XB, &full[s]);
+                if (++s == stages) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    double acc[2][NF][2];
+#pragma unroll
+    for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < NF; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+
+    const int m0 = warp * 16;
+    const int rq = lane >> 2, kq = lane & 3;
+    auto flush = [&](int seg) {
+        double* dst = part + (static_cast<size_t>(c) * maxseg + seg) * kBM * WP;
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm) {
+            const int row = m0 + 8 * fm + rq;
+#pragma unroll
+            for (int fn = 0; fn < NF; ++fn) {
+                double2 v;
+                v.x = acc[fm][fn][0];
+                v.y = acc[fm][fn][1];
+                *reinterpret_cast<double2*>(dst + row * WP + 8 * fn + 2 * kq) = v;
+                acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+            }
+        }
+    };
+
+    if (t0 < t1) {
+        int cur_b = static_cast<int>(t0 / nk);
+        int seg = 0;
+        int s = 0;
+        uint32_t ph = 0;
+        for (long long t = t0; t < t1; ++t) {
+            const int b = static_cast<int>(t / nk);
+            if (b != cur_b) {
+                flush(seg);
+                ++seg;
+                cur_b = b;
+            }
+            mbar_wait(&full[s], ph);
+            const unsigned char* tile = smem + static_cast<size_t>(s) * SB;
+            const double* xs = reinterpret_cast<const double*>(tile + kTileBytes);
+#pragma unroll
+            for (int kk = 0; kk < K4; ++kk) {
+                double a[2];
+#pragma unroll
+                for (int fm = 0; fm < 2; ++fm) {
+                    const double v = load_a<TD>(tile, m0 + 8 * fm + rq, 4 * kk + kq);
+                    a[fm] = SQUARE ? v * v : v;
+                }
+#pragma unroll
+                for (int fn = 0; fn < NF; ++fn) {
+                    const double bv = xs[(kk * WP + 8 * fn + rq) * 4 + kq];
+                    dmma884(acc[0][fn][0], acc[0][fn][1], a[0], bv);
+                    dmma884(acc[1][fn][0], acc[1][fn][1], a[1], bv);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        flush(seg);
+    }
+}
+
+__device__ __forceinline__ long long cta_of(long long t, long long total, long long P) {
+    long long c = static_cast<long long>((static_cast<double>(t) * P) / static_cast<double>(total));
+    if (c > P - 1) c = P - 1;
+    if (c < 0) c = 0;
+    while (c + 1 < P && chunk_begin(total, c + 1, P) <= t) ++c;
+    while (c > 0 && chunk_begin(total, c, P) > t) --c;
+    return c;
+}
+
+// Sum the partial slots of each row block in CTA order, then
+//   mode 1: y = -1/2 (y - r_i s_c - t_c + g s_c)   (rank-3 centering)
+//   mode 0: y as is.
+// Rows >= n are written as zero. Output in the k4-interleaved panel layout.
+template <int WP>
+__global__ void __launch_bounds__(256)
+    k2_reduce(const double* __restrict__ part, int maxseg, int nk, long long total, int P, int n,
+              int mode, const double* __restrict__ row_mean, const double* __restrict__ scalars,
+              const double* __restrict__ colsums, double* __restrict__ y) {
+    const int b = blockIdx.x;
+    const long long c_lo = cta_of(static_cast<long long>(b) * nk, total, P);
+    const long long c_hi = cta_of(static_cast<long long>(b + 1) * nk - 1, total, P);
+    const double g = mode ? scalars[S_GRAND] : 0.0;
+    for (int e = threadIdx.x; e < kBM * WP; e += blockDim.x) {
+        const int r = e / WP, col = e % WP;
+        double v = 0.0;
+        for (long long cc = c_lo; cc <= c_hi; ++cc) {
+            const int seg = b - static_cast<int>(chunk_begin(total, cc, P) / nk);
+            v += part[(static_cast<size_t>(cc) * maxseg + seg) * kBM * WP + e];
+        }
+        const size_t i = static_cast<size_t>(b) * kBM + r;
+        if (i >= static_cast<size_t>(n)) {
+            v = 0.0;
+        } else if (mode) {
+            const double s = colsums[col], t = colsums[WP + col];
+            v = -0.5 * (v - row_mean[i] * s - t + g * s);
+        }
+        y[pidx(i, col, WP)] = v;
+    }
+}
+
+template <int WP, typename TD, bool SQ>
+void set_smem_attr(size_t smem) {
+    static bool done = false;  // per instantiation
+    static size_t max_set = 0;
+    if (!done || smem > max_set) {
+        cudaFuncSetAttribute(k2_product<WP, TD, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        done = true;
+        max_set = smem;
+    }
+}
+
+template <int WP>
+void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
+               double* part, const double* row_mean, const double* scalars,
+               const double* colsums, double* y, cudaStream_t st) {
+    if (dt == DType::F64) {
+        if (mode) {
+            set_smem_attr<WP, double, true>(p.smem);
+            k2_product<WP, double, true><<<p.grid, kThreads, p.smem, st>>>(
+                *tmap, x, p.nk, p.total, part, p.maxseg, p.stages);
+        } else {
+            set_smem_attr<WP, double, false>(p.smem);
+            k2_product<WP, double, false><<<p.grid, kThreads, p.smem, st>>>(
+                *tmap, x, p.nk, p.total, part, p.maxseg, p.stages);
+        }
+    } else if (mode) {
+        set_smem_attr<WP, float, true>(p.smem);
+        k2_product<WP, float, true><<<p.grid, kThreads, p.smem, st>>>(*tmap, x, p.nk, p.total,
+                                                                        part, p.maxseg, p.stages);
+    } else {
+        set_smem_attr<WP, float, false>(p.smem);
+        k2_product<WP, float, false><<<p.grid, kThreads, p.smem, st>>>(*tmap, x, p.nk, p.total,
+                                                                         part, p.maxseg, p.stages);
+    }
+    k2_reduce<WP><<<p.nb, 256, 0, st>>>(part, p.maxseg, p.nk, p.total, p.grid, p.n, mode,
+                                        row_mean, scalars, colsums, y);
+}
+
+}  // namespace
+
+K2Plan k2_plan(size_t n, int wp, DType dt, int sms) {
+    K2Plan p;
+    p.wp = wp;
+    p.n = static_cast<int>(n);
+    p.nb = static_cast<int>((n + kBM - 1) / kBM);
+    const int kt = dt == DType::F64 ? 16 : 32;
+    p.nk = static_cast<int>((n + kt - 1) / kt);
+    p.total = static_cast<long long>(p.nb) * p.nk;
+    p.grid = static_cast<int>(std::min<long long>(sms, p.total));
+    const int sb = ((kTileBytes + kt * wp * 8) + 1023) / 1024 * 1024;
+    const size_t budget = 220 * 1024;
+    int stages = static_cast<int>((budget - 1024 - 256) / sb);
+    stages = std::max(2, std::min(stages, 8));
+    p.stages = stages;
+    p.smem = static_cast<size_t>(stages) * sb + 1024 + 2 * 8 * stages;
+    // max row blocks a CTA range touches
+    int maxseg = 1;
+    for (long long c = 0; c < p.grid; ++c) {
+        const long long a = p.total * c / p.grid, b = p.total * (c + 1) / p.grid;
+        if (b > a) maxseg = std::max<int>(maxseg, static_cast<int>((b - 1) / p.nk - a / p.nk + 1));
+    }
+    p.maxseg = maxseg;
+    p.part_elems = static_cast<size_t>(p.grid) * maxseg * kBM * wp;
+    return p;
+}
+
+void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
+               double* part, const double* row_mean, const double* scalars,
+               const double* colsums, double* y, size_t n_pad, cudaStream_t st) {
+    (void)n_pad;
+    switch (p.wp) {
+#define DSB_WP(W)                                                                              \
+    case W:                                                                                    \
+        launch_wp<W>(tmap, dt, mode, p, x, part, row_mean, scalars, colsums, y, st);           \
+        break;
+        DSB_WP(8)
+        DSB_WP(16)
+        DSB_WP(24)
+        DSB_WP(32)
+        DSB_WP(40)
+        DSB_WP(48)
+        DSB_WP(56)
+        DSB_WP(64)
+        DSB_WP(72)
+        DSB_WP(80)
+        DSB_WP(88)
+        DSB_WP(96)
+        DSB_WP(104)
+        DSB_WP(112)
+        DSB_WP(120)
+        DSB_WP(128)
+#undef DSB_WP
+        default:
+            throw std::invalid_argument("unsupported panel width");
+    }
+    count_launch(2);
+}
+
+}  // namespace dsb

@@ -1,0 +1,107 @@
+// Launch interface of the divscope-b200 kernels (host side). Every launcher
+// enqueues on the given stream and never synchronizes.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace dsb {
+
+constexpr int kBM = 128;      // K2 row-block height (rows of D per CTA tile)
+constexpr int kMaxWP = 128;   // widest panel (rank + oversampling, padded to 8)
+
+// indices into the K1 scalar block (double[16])
+enum Scalar : int {
+    S_GRAND = 0,       // grand mean of d^2 (mds.cpp:39-41)
+    S_FRO2_LAZY = 1,   // ||G||_F^2 by the closed form 1/4 (sum d^4 - 2 n |r|^2 + n^2 g^2)
+    S_FRO2_EXPL = 2,   // sum_ij a_ij^2 (explicit matrices, rsvd.cpp:64-79)
+    S_MAXABS = 3,      // max |a_ij| over all entries (mds.cpp:21-22)
+    S_MAXABS_UP = 4,   // max |a_ij| over i <= j (rsvd.cpp:50-54)
+    S_MAXASYM = 5,     // max |a_ij - a_ji|
+    S_SUM4 = 6,        // sum a^4
+    S_SUMR = 7,        // sum_i r_i
+    S_SUMR2 = 8,       // sum_i r_i^2
+    S_COUNT = 16,
+};
+
+enum class DType { F64 = 0, F32 = 1 };
+
+// ---- K1: one streaming pass over D (tile pairs): row sums of squares,
+// sum of fourth powers, max |d| and max |d_ij - d_ji| -----------------------
+struct K1Work {
+    double* part;        // [nbt][n_pad64] per-tile-column row partial sums
+    double* cta_stats;   // [grid][4]
+    double* blk_stats;   // [nblk][3]
+    int grid;
+};
+size_t k1_part_elems(size_t n);
+int k1_grid(size_t n, int sms);
+void launch_k1(const void* d, DType dt, size_t ld, size_t n, const K1Work& w, double* row_mean,
+               double* scalars, int sms, cudaStream_t st);
+
+// ---- K2: centered skinny product Y = G X (stream-K, DMMA f64) -------------
+struct K2Plan {
+    int wp = 0;
+    int n = 0, nb = 0, nk = 0;
+    long long total = 0;
+    int grid = 0, maxseg = 0, stages = 0;
+    size_t smem = 0;
+    size_t part_elems = 0;   // doubles needed for the partial workspace
+};
+K2Plan k2_plan(size_t n, int wp, DType dt, int sms);
+// mode: 0 = explicit matrix (Y = A X), 1 = gram of D (D squared on the fly,
+// then rank-3 centering).
+void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
+               double* part, const double* row_mean, const double* scalars,
+               const double* colsums, double* y, size_t n_pad, cudaStream_t st);
+
+// ---- panel kernels (n_pad x WP, k4-interleaved) -----------------------------
+int panel_grid(size_t n_pad, int sms);
+void launch_panel_from_rowmajor(const double* src, size_t n, int w, int wp, size_t n_pad,
+                                double* dst, cudaStream_t st);
+void launch_panel_to_rowmajor(const double* src, size_t n, int w, int wp, double* dst,
+                              cudaStream_t st);
+// colsums[0..wp) = 1^T X, colsums[wp..2wp) = r^T X (deterministic 2-level)
+void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_pad, int wp,
+                    double* partial, double* colsums, int sms, cudaStream_t st);
+// out (wp x wp) = A^T B (deterministic 2-level)
+void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, double* partial,
+                      double* out, int sms, cudaStream_t st);
+// CholQR step on W = Y^T Y: rinv = R^{-1} with breakdown handling (shift /
+// drop, K3); flags[0] |= 1 when shifted.
+void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shift, double* rinv,
+                     int* flags, cudaStream_t st);
+// q = y * rinv (row-wise, upper-triangular rinv)
+void launch_panel_apply(const double* y, const double* rinv, size_t n_pad, int wp, double* q,
+                        cudaStream_t st);
+
+// ---- K5: Rayleigh-Ritz EVD + |lambda| ordering + embed filter (1 CTA) -----
+struct EvdOut {
+    double* vals;      // [w] eigenvalues in reference order (|lambda| desc, + first)
+    double* vkeep;     // [w][r] eigenvectors of the embed-kept eigenvalues
+    double* kept_vals; // [r]
+    double* dmeta;     // [0]=resid [1]=dropped_negative_mass [2]=sum lambda^2
+    int* imeta;        // [0]=keep [1]=r [2]=truncated [3]=sweeps [4]=converged
+};
+void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
+                const double* scalars, int fro_index, const EvdOut& o, cudaStream_t st);
+
+// ---- K6: lift U = Q V_keep, sign rule (mds.cpp:65-77), scale by sqrt(lambda)
+void launch_lift(const double* q, size_t n, int wp, int w, const double* vkeep,
+                 const double* kept_vals, const int* imeta, int rmax, double* coords,
+                 double* partial, int sms, cudaStream_t st);
+
+// ---- K9 / K7: distance builders --------------------------------------------
+void launch_euclid(const double* pts, size_t n, int dim, void* d, DType dt, size_t ld,
+                   cudaStream_t st);
+void launch_hamming(const unsigned long long* packed, size_t count, int words, int length,
+                    double* d, size_t ld, uint32_t* counts, cudaStream_t st);
+
+// ---- misc ------------------------------------------------------------------
+uint64_t kernel_launch_count();
+void count_launch(int k = 1);
+
+}  // namespace dsb

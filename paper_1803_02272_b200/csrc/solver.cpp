@@ -1,0 +1,530 @@
+// Host orchestration of the B200 MDS path: K1 (pass 0) at gram time, then
+// the randomized range finder, Rayleigh-Ritz and the embedding, all
+// enqueued on the library stream with no host round trip until the final
+// read-back (ref src/rsvd.cpp:81-145, src/mds.cpp:14-124).
+#include "solver.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <thread>
+#include <tuple>
+
+namespace dsb {
+
+namespace {
+
+struct StatsOut {
+    double sc[S_COUNT];
+    std::shared_ptr<DevBuf> scalars;
+    std::shared_ptr<DevBuf> row_mean;
+};
+
+// K1 over a store; returns scalars (host) plus device scalars/row means.
+StatsOut run_k1(const Store& s) {
+    Ctx& c = Ctx::get();
+    const size_t n = s.rows;
+    K1Work w;
+    w.grid = k1_grid(n, c.sms);
+    w.part = static_cast<double*>(c.scratch("k1_part", k1_part_elems(n) * sizeof(double)));
+    w.cta_stats = static_cast<double*>(c.scratch("k1_cta", static_cast<size_t>(w.grid) * 4 * 8));
+    w.blk_stats = static_cast<double*>(c.scratch("k1_blk", ((n + 255) / 256) * 3 * 8 + 64));
+    StatsOut o;
+    o.row_mean = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * sizeof(double));
+    o.scalars = std::make_shared<DevBuf>(S_COUNT * sizeof(double));
+    DSB_CUDA(cudaMemsetAsync(o.scalars->p, 0, S_COUNT * sizeof(double), c.stream));
+    cudaEvent_t ev;
+    c.begin_timed(0, &ev);
+    launch_k1(s.buf->p, s.dt, s.ld, n, w, o.row_mean->as<double>(), o.scalars->as<double>(), c.sms,
+              c.stream);
+    c.end_timed(0, ev);
+    DSB_CUDA(cudaGetLastError());
+    c.d2h_copy(o.sc, o.scalars->p, S_COUNT * sizeof(double));
+    return o;
+}
+
+void ensure_tmap(Store& s) {
+    std::lock_guard<std::mutex> lk(s.mu);
+    if (s.tmap_ok) return;
+    if (!Ctx::get().encode_tmap(&s.tmap, s.buf->p, s.dt, s.rows, s.cols, s.ld))
+        throw Error(errc::internal, "cuTensorMapEncodeTiled failed");
+    s.tmap_ok = true;
+}
+
+// check_symmetric (ref rsvd.cpp:46-60) for explicit matrices, cached
+void ensure_explicit_stats(Store& s) {
+    {
+        std::lock_guard<std::mutex> lk(s.mu);
+        if (s.stats_ok) return;
+    }
+    StatsOut o = run_k1(s);
+    std::lock_guard<std::mutex> lk(s.mu);
+    std::memcpy(s.stats, o.sc, sizeof(s.stats));
+    s.stats_dev = o.scalars;
+    s.stats_ok = true;
+}
+
+// Omega = fill_gaussian(mt19937_64(seed)) as n x w row-major (rsvd.cpp:90-92),
+// memoized for the most recent shapes (a pure function of (seed, n, w)).
+const std::vector<double>& omega_host(uint64_t seed, size_t n, size_t w) {
+    static std::deque<std::tuple<uint64_t, size_t, size_t, std::vector<double>>> cache;
+    for (auto& e : cache)
+        if (std::get<0>(e) == seed && std::get<1>(e) == n && std::get<2>(e) == w)
+            return std::get<3>(e);
+    std::vector<double> om(n * w);
+    std::mt19937_64 eng(seed);
+    fill_gaussian(eng, om.data(), om.size());
+    if (cache.size() >= 2) cache.pop_front();
+    cache.emplace_back(seed, n, w, std::move(om));
+    return std::get<3>(cache.back());
+}
+
+struct RunOut {
+    std::vector<double> vals;  // w values, reference order
+    size_t keep = 0;
+    double resid = 0.0;
+    Embedding emb;
+};
+
+enum class What { Eigs, Embed, Range };
+
+RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What what,
+           size_t requested, double* range_out) {
+    Ctx& c = Ctx::get();
+    Store& s = *g.store;
+    const size_t n = s.rows;
+    const bool lazy = static_cast<bool>(g.gram);
+    const double* scal_dev = nullptr;
+    const double* row_mean = nullptr;
+    int fro_index;
+    if (lazy) {
+        scal_dev = g.gram->scalars->as<double>();
+        row_mean = g.gram->row_mean->as<double>();
+        fro_index = S_FRO2_LAZY;
+    } else {
+        // ref rsvd.cpp:46-60: n == 0 -> invalid_argument; asymmetry -> not_symmetric
+        if (n == 0) throw Error(errc::invalid_argument, "empty matrix");
+        ensure_explicit_stats(s);
+        if (s.stats[S_MAXASYM] > 1e-10 * std::max(1.0, s.stats[S_MAXABS_UP]))
+            throw Error(errc::not_symmetric, "matrix is not symmetric");
+        scal_dev = s.stats_dev->as<double>();
+        fro_index = S_FRO2_EXPL;
+    }
+    // ref rsvd.cpp:83-88
+    if (rank < 1) throw Error(errc::invalid_argument, "rank must be >= 1");
+    const size_t w = rank + p;
+    if (w > n) throw Error(errc::rank_too_large, "rank + oversampling exceeds matrix order");
+    if (w > static_cast<size_t>(kMaxWP))
+        throw Error(errc::invalid_argument,
+                    "rank + oversampling > 128 is not supported by the GPU path");
+    const int wi = static_cast<int>(w);
+    const int wp = static_cast<int>(round_up(w, 8));
+    const size_t n_pad = round_up(n, kBM);
+    const int mode = lazy ? 1 : 0;
+
+    ensure_tmap(s);
+    const K2Plan plan = k2_plan(n, wp, s.dt, c.sms);
+    const size_t pbytes = n_pad * wp * sizeof(double);
+    double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
+    double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));
+    double* P2 = static_cast<double*>(c.scratch("panel2", pbytes));
+    double* part = static_cast<double*>(c.scratch("k2_part", plan.part_elems * sizeof(double)));
+    const int pg = panel_grid(n_pad, c.sms);
+    const size_t part_small =
+        std::max<size_t>(static_cast<size_t>(pg) * wp * wp, static_cast<size_t>(pg) * 2 * wp);
+    double* psmall = static_cast<double*>(c.scratch("panel_part", part_small * sizeof(double)));
+    double* colsums = static_cast<double*>(c.scratch("colsums", 2 * wp * sizeof(double)));
+    double* wmat = static_cast<double*>(c.scratch("wmat", wp * wp * sizeof(double)));
+    double* rinv = static_cast<double*>(c.scratch("rinv", wp * wp * sizeof(double)));
+    int* flags = static_cast<int*>(c.scratch("flags", 64));
+    DSB_CUDA(cudaMemsetAsync(flags, 0, 64, c.stream));
+
+    // Omega: host-generated (bit-identical to the reference), relayout on device
+    {
+        const std::vector<double>& om = omega_host(seed, n, w);
+        double* stage = static_cast<double*>(c.scratch("omega_rm", n * w * sizeof(double)));
+        c.h2d_copy(stage, om.data(), n * w * sizeof(double));
+        launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, P0, c.stream);
+    }
+
+    auto product = [&](const double* x, double* y) {
+        if (mode) launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
+        cudaEvent_t ev;
+        c.begin_timed(1, &ev);
+        launch_k2(&s.tmap, s.dt, mode, plan, x, part, row_mean, scal_dev, colsums, y, n_pad,
+                  c.stream);
+        c.end_timed(1, ev);
+    };
+    // CholeskyQR3 with shift/drop handling: y -> t -> y -> out
+    auto orth = [&](double* y, double* t, double* out) {
+        launch_panel_dot(y, y, n_pad, wp, psmall, wmat, c.sms, c.stream);
+        launch_chol_inv(wmat, wp, wi, n, 1, rinv, flags, c.stream);
+        launch_panel_apply(y, rinv, n_pad, wp, t, c.stream);
+        launch_panel_dot(t, t, n_pad, wp, psmall, wmat, c.sms, c.stream);
+        launch_chol_inv(wmat, wp, wi, n, 0, rinv, flags, c.stream);
+        launch_panel_apply(t, rinv, n_pad, wp, y, c.stream);
+        launch_panel_dot(y, y, n_pad, wp, psmall, wmat, c.sms, c.stream);
+        launch_chol_inv(wmat, wp, wi, n, 0, rinv, flags, c.stream);
+        launch_panel_apply(y, rinv, n_pad, wp, out, c.stream);
+    };
+
+    // ref rsvd.cpp:94-98
+    product(P0, P1);
+    orth(P1, P2, P0);
+    for (size_t it = 0; it < q; ++it) {
+        product(P0, P1);
+        orth(P1, P2, P0);
+        product(P0, P1);
+        orth(P1, P2, P0);
+    }
+    RunOut out;
+    if (what == What::Range) {
+        double* rm = static_cast<double*>(c.scratch("range_rm", n * w * sizeof(double)));
+        launch_panel_to_rowmajor(P0, n, wi, wp, rm, c.stream);
+        DSB_CUDA(cudaGetLastError());
+        c.d2h_copy(range_out, rm, n * w * sizeof(double));
+        return out;
+    }
+    // ref rsvd.cpp:108-110: GQ, B = Q^T GQ (symmetrized inside K5)
+    product(P0, P1);
+    launch_panel_dot(P0, P1, n_pad, wp, psmall, wmat, c.sms, c.stream);
+    const size_t req = what == What::Embed ? requested : std::min(rank, w);
+    EvdOut eo;
+    eo.vals = static_cast<double*>(c.scratch("evd_vals", kMaxWP * sizeof(double)));
+    eo.vkeep = static_cast<double*>(c.scratch("evd_vkeep", w * std::max<size_t>(req, 1) * 8));
+    eo.kept_vals = static_cast<double*>(c.scratch("evd_kept", kMaxWP * sizeof(double)));
+    eo.dmeta = static_cast<double*>(c.scratch("evd_dmeta", 8 * sizeof(double)));
+    eo.imeta = static_cast<int*>(c.scratch("evd_imeta", 8 * sizeof(int)));
+    launch_evd(wmat, wp, wi, static_cast<int>(rank), static_cast<int>(req), scal_dev, fro_index,
+               eo, c.stream);
+    double* coords = nullptr;
+    if (what == What::Embed) {
+        coords = static_cast<double*>(c.scratch("coords", n * std::max<size_t>(req, 1) * 8));
+        const int P = static_cast<int>(std::min<size_t>(static_cast<size_t>(c.sms) * 2,
+                                                        std::max<size_t>(n / 64, 1)));
+        double* lp = static_cast<double*>(
+            c.scratch("lift_part", static_cast<size_t>(P) * std::max<size_t>(req, 1) * 2 * 8));
+        launch_lift(P0, n, wp, wi, eo.vkeep, eo.kept_vals, eo.imeta, static_cast<int>(req),
+                    coords, lp, c.sms, c.stream);
+    }
+    DSB_CUDA(cudaGetLastError());
+    // read back (one sync for all of it)
+    struct Meta {
+        double vals[kMaxWP];
+        double kept[kMaxWP];
+        double dmeta[8];
+        int imeta[8];
+    } meta{};
+    DSB_CUDA(cudaMemcpyAsync(meta.vals, eo.vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
+    DSB_CUDA(cudaMemcpyAsync(meta.kept, eo.kept_vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
+    DSB_CUDA(cudaMemcpyAsync(meta.dmeta, eo.dmeta, 8 * 8, cudaMemcpyDeviceToHost, c.stream));
+    c.d2h_copy(meta.imeta, eo.imeta, 8 * sizeof(int));
+    c.d2h += w * 16 + 64;
+    if (!meta.imeta[4])
+        throw Error(errc::internal, "small eigensolve failed");  // ref rsvd.cpp:113-114
+    out.vals.assign(meta.vals, meta.vals + w);
+    out.keep = static_cast<size_t>(meta.imeta[0]);
+    out.resid = meta.dmeta[0];
+    if (what == What::Embed) {
+        Embedding& e = out.emb;
+        e.n = n;
+        e.r = static_cast<size_t>(meta.imeta[1]);
+        e.truncated = meta.imeta[2] != 0;
+        e.dropped_negative_mass = meta.dmeta[1];
+        e.resid = meta.dmeta[0];
+        e.eigenvalues.assign(meta.kept, meta.kept + e.r);
+        e.coords.resize(n * e.r);
+        if (e.r) c.d2h_copy(e.coords.data(), coords, n * e.r * sizeof(double));
+    }
+    return out;
+}
+
+}  // namespace
+
+Matrix matrix_from_host(const void* values, size_t rows, size_t cols, bool symmetric, DType dt) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    Matrix m;
+    m.store = make_store(rows, cols, symmetric, dt);
+    upload_rows(*m.store, values, cols);
+    c.sync();  // the caller may release its buffer on return
+    return m;
+}
+
+Matrix gram_from_distances(const Matrix& d) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const Store& s = *d.store;
+    // ref mds.cpp:15-20
+    if (s.rows != s.cols || !s.symmetric)
+        throw Error(errc::not_symmetric, "gram matrix requires a symmetric distance matrix");
+    const size_t n = s.rows;
+    if (n == 0) throw Error(errc::empty_input, "empty distance matrix");
+    StatsOut o = run_k1(s);
+    // ref mds.cpp:21-27
+    if (o.sc[S_MAXASYM] > 1e-12 * std::max(1.0, o.sc[S_MAXABS]))
+        throw Error(errc::not_symmetric, "distance matrix values are not symmetric");
+    Matrix g;
+    g.store = d.store;
+    g.gram = std::make_shared<GramInfo>();
+    g.gram->n = n;
+    g.gram->row_mean = o.row_mean;
+    g.gram->scalars = o.scalars;
+    std::memcpy(g.gram->sc, o.sc, sizeof(o.sc));
+    g.gram->row_mean_h.resize(n);
+    c.d2h_copy(g.gram->row_mean_h.data(), o.row_mean->p, n * sizeof(double));
+    return g;
+}
+
+Spectrum eigs_sym(const Matrix& g, const SolverOptions& opts) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    RunOut r = run(g, opts.rank, opts.oversampling, opts.power_iters, opts.seed, What::Eigs,
+                   opts.rank, nullptr);
+    Spectrum s;
+    s.eigenvalues.assign(r.vals.begin(), r.vals.begin() + r.keep);
+    s.resid = r.resid;
+    return s;
+}
+
+Embedding embed(const Matrix& g, size_t rank, SolverOptions opts) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const size_t n = g.n();
+    // ref mds.cpp:118-121
+    if (rank < 1 || rank > n) throw Error(errc::rank_too_large, "rank must be in [1, n]");
+    opts.rank = rank;
+    opts.oversampling = std::min(opts.oversampling, n - rank);
+    RunOut r = run(g, opts.rank, opts.oversampling, opts.power_iters, opts.seed, What::Embed, rank,
+                   nullptr);
+    return std::move(r.emb);
+}
+
+void randomized_range(const Matrix& g, const SolverOptions& opts, double* q_out) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    run(g, opts.rank, opts.oversampling, opts.power_iters, opts.seed, What::Range, opts.rank,
+        q_out);
+}
+
+double matrix_get(const Matrix& m, size_t i, size_t j) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const Store& s = *m.store;
+    const size_t esz = s.dt == DType::F64 ? 8 : 4;
+    auto fetch = [&](size_t a, size_t b) {
+        unsigned char buf[8];
+        c.d2h_copy(buf, static_cast<const char*>(s.buf->p) + (a * s.ld + b) * esz, esz);
+        if (esz == 8) {
+            double v;
+            std::memcpy(&v, buf, 8);
+            return v;
+        }
+        float f;
+        std::memcpy(&f, buf, 4);
+        return static_cast<double>(f);
+    };
+    if (!m.gram) return fetch(i, j);
+    // ref mds.cpp:50-51 (upper) and :57-58 (mirror)
+    const auto& rm = m.gram->row_mean_h;
+    const double grand = m.gram->sc[S_GRAND];
+    if (i <= j) {
+        const double dij = fetch(i, j);
+        return -0.5 * (dij * dij - rm[i] - rm[j] + grand);
+    }
+    const double dji = fetch(j, i);
+    return -0.5 * (dji * dji - rm[j] - rm[i] + grand);
+}
+
+void matrix_to_host(const Matrix& m, double* out) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const Store& s = *m.store;
+    const size_t esz = s.dt == DType::F64 ? 8 : 4;
+    std::vector<unsigned char> raw(s.rows * s.cols * esz);
+    if (!raw.empty()) {
+        DSB_CUDA(cudaMemcpy2DAsync(raw.data(), s.cols * esz, s.buf->p, s.ld * esz, s.cols * esz,
+                                   s.rows, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        c.d2h += raw.size();
+    }
+    const size_t rows = s.rows, cols = s.cols;
+    auto at = [&](size_t a, size_t b) {
+        if (esz == 8) {
+            double v;
+            std::memcpy(&v, &raw[(a * cols + b) * 8], 8);
+            return v;
+        }
+        float f;
+        std::memcpy(&f, &raw[(a * cols + b) * 4], 4);
+        return static_cast<double>(f);
+    };
+    if (!m.gram) {
+        for (size_t a = 0; a < rows; ++a)
+            for (size_t b = 0; b < cols; ++b) out[a * cols + b] = at(a, b);
+        return;
+    }
+    const auto& rm = m.gram->row_mean_h;
+    const double grand = m.gram->sc[S_GRAND];
+    for (size_t a = 0; a < rows; ++a)
+        for (size_t b = a; b < cols; ++b) {
+            const double dab = at(a, b);
+            const double v = -0.5 * (dab * dab - rm[a] - rm[b] + grand);
+            out[a * cols + b] = v;
+            out[b * cols + a] = v;
+        }
+}
+
+double stable_rank(const Matrix& g) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    Store& s = *g.store;
+    const size_t n = s.rows;
+    const bool lazy = static_cast<bool>(g.gram);
+    double fro2;
+    const double* scal_dev;
+    const double* row_mean = nullptr;
+    if (lazy) {
+        fro2 = g.gram->sc[S_FRO2_LAZY];
+        scal_dev = g.gram->scalars->as<double>();
+        row_mean = g.gram->row_mean->as<double>();
+    } else {
+        if (n == 0) throw Error(errc::invalid_argument, "empty matrix");
+        ensure_explicit_stats(s);
+        if (s.stats[S_MAXASYM] > 1e-10 * std::max(1.0, s.stats[S_MAXABS_UP]))
+            throw Error(errc::not_symmetric, "matrix is not symmetric");
+        fro2 = s.stats[S_FRO2_EXPL];
+        scal_dev = s.stats_dev->as<double>();
+    }
+    if (fro2 == 0.0) throw Error(errc::zero_matrix, "stable rank undefined for zero matrix");
+    const int mode = lazy ? 1 : 0;
+    const int wp = 8;
+    const size_t n_pad = round_up(n, kBM);
+    ensure_tmap(s);
+    const K2Plan plan = k2_plan(n, wp, s.dt, c.sms);
+    double* X = static_cast<double*>(c.scratch("sr_x", n_pad * wp * 8));
+    double* Y = static_cast<double*>(c.scratch("sr_y", n_pad * wp * 8));
+    double* part = static_cast<double*>(c.scratch("k2_part", plan.part_elems * 8));
+    const int pg = panel_grid(n_pad, c.sms);
+    double* psmall = static_cast<double*>(c.scratch("panel_part", static_cast<size_t>(pg) * wp * wp * 8 + 64));
+    double* colsums = static_cast<double*>(c.scratch("colsums", 2 * wp * 8));
+    double* wmat = static_cast<double*>(c.scratch("wmat", wp * wp * 8));
+    double* scale = static_cast<double*>(c.scratch("sr_scale", wp * wp * 8));
+    double* stage = static_cast<double*>(c.scratch("sr_stage", n * 8));
+    // ref rsvd.cpp:157-176: v ~ fill_gaussian(mt19937_64(0x5eed)), normalized
+    std::mt19937_64 eng(0x5eedULL);
+    std::vector<double> v(n);
+    auto load_v = [&](bool from_engine) {
+        if (from_engine) {
+            fill_gaussian(eng, v.data(), n);
+            double ss = 0.0;
+            for (double a : v) ss += a * a;
+            const double nrm = std::sqrt(ss);
+            for (double& a : v) a /= nrm;
+        }
+        c.h2d_copy(stage, v.data(), n * 8);
+        launch_panel_from_rowmajor(stage, n, 1, wp, n_pad, X, c.stream);
+    };
+    load_v(true);
+    std::vector<double> hs(wp * wp, 0.0);
+    double sigma = 0.0;
+    for (int it = 0; it < 20000; ++it) {
+        if (mode) launch_colsums(X, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
+        cudaEvent_t ev;
+        c.begin_timed(1, &ev);
+        launch_k2(&s.tmap, s.dt, mode, plan, X, part, row_mean, scal_dev, colsums, Y, n_pad,
+                  c.stream);
+        c.end_timed(1, ev);
+        launch_panel_dot(Y, Y, n_pad, wp, psmall, wmat, c.sms, c.stream);
+        double w00 = 0.0;
+        c.d2h_copy(&w00, wmat, 8);
+        const double norm = std::sqrt(w00);
+        if (norm == 0.0) {
+            load_v(true);
+            sigma = 0.0;
+            continue;
+        }
+        // v = w / norm
+        hs[0] = 1.0 / norm;
+        c.h2d_copy(scale, hs.data(), wp * wp * 8);
+        launch_panel_apply(Y, scale, n_pad, wp, X, c.stream);
+        if (sigma != 0.0 && std::abs(norm - sigma) <= 1e-13 * norm) {
+            sigma = norm;
+            break;
+        }
+        sigma = norm;
+    }
+    c.sync();
+    return fro2 / (sigma * sigma);
+}
+
+Matrix matrix_euclidean(const double* pts, size_t n, size_t dim, bool f32) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    if (n == 0 || dim == 0) throw Error(errc::empty_input, "no points");
+    if (dim > 256) throw Error(errc::invalid_argument, "dimension > 256 not supported");
+    Matrix m;
+    m.store = make_store(n, n, true, f32 ? DType::F32 : DType::F64);
+    DevBuf dp(n * dim * sizeof(double));
+    c.h2d_copy(dp.p, pts, n * dim * sizeof(double));
+    launch_euclid(dp.as<double>(), n, static_cast<int>(dim), m.store->buf->p, m.store->dt,
+                  m.store->ld, c.stream);
+    c.sync();
+    return m;
+}
+
+namespace {
+std::vector<unsigned long long> pack_reads(const char* reads, size_t count, size_t length,
+                                           int& words) {
+    if (count == 0 || length == 0) throw Error(errc::empty_input, "no reads");
+    words = static_cast<int>((length + 31) / 32);
+    std::vector<unsigned long long> packed(count * words, 0ull);
+    for (size_t i = 0; i < count; ++i)
+        for (size_t t = 0; t < length; ++t) {
+            unsigned long long code;
+            switch (reads[i * length + t]) {
+                case 'A': code = 0; break;
+                case 'C': code = 1; break;
+                case 'G': code = 2; break;
+                case 'T': code = 3; break;
+                default:
+                    throw Error(errc::invalid_character,
+                                "read " + std::to_string(i) + ": base " + std::to_string(t + 1) +
+                                    " is not A/C/G/T");
+            }
+            packed[i * words + t / 32] |= code << (2 * (t % 32));
+        }
+    return packed;
+}
+}  // namespace
+
+Matrix matrix_hamming(const char* reads, size_t count, size_t length) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    int words = 0;
+    const auto packed = pack_reads(reads, count, length, words);
+    Matrix m;
+    m.store = make_store(count, count, true, DType::F64);
+    DevBuf dp(packed.size() * 8);
+    c.h2d_copy(dp.p, packed.data(), packed.size() * 8);
+    launch_hamming(dp.as<unsigned long long>(), count, words, static_cast<int>(length),
+                   m.store->buf->as<double>(), m.store->ld, nullptr, c.stream);
+    c.sync();
+    return m;
+}
+
+void hamming_counts(const char* reads, size_t count, size_t length, uint32_t* out) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    int words = 0;
+    const auto packed = pack_reads(reads, count, length, words);
+    DevBuf dp(packed.size() * 8);
+    DevBuf dc(count * count * sizeof(uint32_t));
+    c.h2d_copy(dp.p, packed.data(), packed.size() * 8);
+    launch_hamming(dp.as<unsigned long long>(), count, words, static_cast<int>(length), nullptr, 0,
+                   dc.as<uint32_t>(), c.stream);
+    c.d2h_copy(out, dc.p, count * count * sizeof(uint32_t));
+}
+
+}  // namespace dsb

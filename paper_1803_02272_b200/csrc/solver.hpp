@@ -1,0 +1,69 @@
+// C++ API of the B200 MDS path — the host-side mirror of the reference's
+// C++ entry points (ref src/mds.hpp:34-59, src/rsvd.hpp:20-62) over
+// device-resident handles. The C ABI (capi.cpp) is a thin wrapper.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host_core.hpp"
+
+namespace dsb {
+
+// ref src/rsvd.hpp:20-25 (C++ defaults; the C API defaults differ)
+struct SolverOptions {
+    size_t rank = 1;
+    size_t oversampling = 10;
+    size_t power_iters = 2;
+    uint64_t seed = 0;
+};
+
+// A matrix handle: device store + optional lazy-gram terms.
+struct Matrix {
+    std::shared_ptr<Store> store;
+    std::shared_ptr<GramInfo> gram;  // non-null => this handle denotes G(store)
+    size_t n() const { return store->rows; }
+};
+
+// ref src/rsvd.hpp:29-33 (vectors omitted: the C ABI never returns them)
+struct Spectrum {
+    std::vector<double> eigenvalues;  // keep = min(rank, w), reference order
+    double resid = 0.0;
+};
+
+// ref src/mds.hpp:21-28
+struct Embedding {
+    size_t n = 0, r = 0;
+    std::vector<double> coords;       // n x r row-major
+    std::vector<double> eigenvalues;  // retained, descending
+    double dropped_negative_mass = 0.0;
+    bool truncated = false;
+    double resid = 0.0;
+};
+
+// ref src/mds.cpp:14-60 (validation + centering terms; G not materialized)
+Matrix gram_from_distances(const Matrix& d);
+
+// ref src/rsvd.cpp:102-145
+Spectrum eigs_sym(const Matrix& g, const SolverOptions& opts);
+
+// ref src/mds.cpp:116-124 (rank overrides opts.rank, p clamped to n - rank)
+Embedding embed(const Matrix& g, size_t rank, SolverOptions opts);
+
+// ref src/rsvd.cpp:81-100 (basis written n x w row-major)
+void randomized_range(const Matrix& g, const SolverOptions& opts, double* q_out);
+
+// ref src/rsvd.cpp:147-178
+double stable_rank(const Matrix& g);
+
+// G_ij of a handle (lazy gram evaluated like ref mds.cpp:50-58)
+double matrix_get(const Matrix& m, size_t i, size_t j);
+void matrix_to_host(const Matrix& m, double* out);
+
+Matrix matrix_from_host(const void* values, size_t rows, size_t cols, bool symmetric, DType dt);
+Matrix matrix_euclidean(const double* pts, size_t n, size_t dim, bool f32);
+Matrix matrix_hamming(const char* reads, size_t count, size_t length);
+void hamming_counts(const char* reads, size_t count, size_t length, uint32_t* out);
+
+}  // namespace dsb

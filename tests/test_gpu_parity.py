@@ -1,0 +1,360 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle
+and the reference's own known-answer tests.
+
+Reference KATs ported from /root/reference/proj/tests/test_mds.cpp,
+test_rsvd.cpp, test_capi.cpp and acceptance.cpp (cited per test).
+Tolerances: eigenvalues relative 1e-10 (fp64 D) / 1e-4 (fp32 D) per
+BASELINE.json north_star; coordinates per column up to sign; integer Hamming
+counts and Euclidean distances bit-exact.
+"""
+import numpy as np
+import pytest
+
+from helpers import coords_match_up_to_sign, rel_err, sin_subspace, with_spectrum
+
+pytestmark = pytest.mark.gpu
+
+
+def err(ds, fn, *a, **k):
+    with pytest.raises(ds.DivscopeError) as ei:
+        fn(*a, **k)
+    return ei.value.status
+
+
+# ---------------------------------------------------------------- builders
+
+def test_euclid_bit_exact_vs_oracle(ds, oracle):
+    pts = ds.synth_points(1, 301, 11)
+    d_gpu = ds.matrix_euclidean(pts).to_numpy()
+    d_cpu = oracle.euclidean_matrix(pts)
+    assert np.array_equal(d_gpu, d_cpu)
+    d32 = ds.matrix_euclidean(pts, store_f32=True).to_numpy()
+    assert np.array_equal(d32, d_cpu.astype(np.float32).astype(np.float64))
+
+
+def test_euclid_matches_reference_fixture(ds, ref):
+    # ref tests/testdata.cpp:157-184 compiled from the reference sources
+    pts = ref.uniform_box(97, 5, 303)
+    assert np.array_equal(ds.matrix_euclidean(pts).to_numpy(), ref.euclidean_matrix(pts))
+
+
+def test_hamming_counts_bit_exact(ds, oracle):
+    reads = ds.synth_reads(203, 400, 7, 0.05, 5)
+    h = ds.hamming_counts(reads)
+    st, h_cpu = oracle.hamming_counts(b"".join(reads), len(reads), 400)
+    assert st == 0
+    assert np.array_equal(h, h_cpu)
+    d = ds.matrix_hamming(reads).to_numpy()
+    assert np.array_equal(d, h_cpu.astype(np.float64) / 400.0)
+
+
+def test_hamming_edge_cases(ds, oracle):
+    # odd length (partial last word), identical reads, single read
+    reads = [b"ACGTA", b"ACGTA", b"TTTTT"]
+    h = ds.hamming_counts(reads)
+    assert h.tolist() == [[0, 0, 4], [0, 0, 4], [4, 4, 0]]
+    assert ds.hamming_counts([b"A" * 33]).tolist() == [[0]]
+    assert err(ds, ds.hamming_counts, [b"ACGN"]) == ds.Status.ERR_INVALID_CHARACTER
+
+
+# ---------------------------------------------------------------- gram
+
+def test_gram_two_point_exact(ds):
+    # ref tests/test_mds.cpp:27-34
+    g = ds.gram(ds.matrix_from_host(np.array([[0.0, 2.0], [2.0, 0.0]])))
+    assert g.to_numpy().tolist() == [[1.0, -1.0], [-1.0, 1.0]]
+    assert g.get(1, 0) == -1.0 and g.symmetric
+
+
+def test_gram_zero(ds):
+    # ref tests/test_mds.cpp:36-39
+    g = ds.gram(ds.matrix_from_host(np.zeros((3, 3))))
+    assert not np.any(g.to_numpy())
+
+
+def test_gram_matches_oracle(ds, oracle):
+    pts = ds.synth_points(2, 513, 3)
+    d = oracle.euclidean_matrix(pts)
+    st, g_cpu = oracle.gram(d)
+    assert st == 0
+    g_gpu = ds.gram(ds.matrix_from_host(d)).to_numpy()
+    assert np.max(np.abs(g_gpu - g_cpu)) <= 1e-13 * np.max(np.abs(g_cpu))
+    assert np.array_equal(g_gpu, g_gpu.T)
+    # double-centering: rows sum to ~0 (ref tests/test_mds.cpp:41-55)
+    assert np.max(np.abs(g_gpu.sum(1))) < 1e-9 * np.max(np.abs(g_gpu)) * 513
+
+
+def test_gram_validation(ds):
+    # ref tests/test_mds.cpp:76-101
+    rect = ds.matrix_from_host(np.zeros((2, 3)), symmetric=False)
+    assert err(ds, ds.gram, rect) == ds.Status.ERR_NOT_SYMMETRIC
+    lie = ds.matrix_from_host(np.array([[0.0, 1.0], [2.0, 0.0]]))
+    assert err(ds, ds.gram, lie) == ds.Status.ERR_NOT_SYMMETRIC
+    empty = ds.matrix_from_host(np.zeros((0, 0)))
+    assert err(ds, ds.gram, empty) == ds.Status.ERR_EMPTY_INPUT
+    unflagged = ds.matrix_from_host(np.zeros((2, 2)), symmetric=False)
+    assert err(ds, ds.gram, unflagged) == ds.Status.ERR_NOT_SYMMETRIC
+
+
+def test_gram_tolerance_boundary(ds):
+    # |d_ij - d_ji| <= 1e-12 max(1, max|d|) passes (ref mds.cpp:23-27)
+    d = np.array([[0.0, 3.0], [3.0 + 2e-12, 0.0]])
+    ds.gram(ds.matrix_from_host(d))
+    d[1, 0] = 3.0 + 8e-12
+    assert err(ds, ds.gram, ds.matrix_from_host(d)) == ds.Status.ERR_NOT_SYMMETRIC
+
+
+# ---------------------------------------------------------------- eigs KATs
+
+def test_eigs_signed_diagonal(ds):
+    # ref tests/test_rsvd.cpp:103-118
+    g = ds.matrix_from_host(np.diag([3.0, -2.0, 1.0]))
+    vals, _ = ds.eigs(g, rank=2, oversampling=1, power_iters=2, seed=0)
+    assert vals.shape == (2,)
+    assert vals[0] == pytest.approx(3.0, rel=1e-12)
+    assert vals[1] == pytest.approx(-2.0, rel=1e-12)
+
+
+def test_eigs_magnitude_order_positive_first(ds):
+    # ref tests/test_rsvd.cpp:120-130
+    g = ds.matrix_from_host(np.diag([2.0, -2.0, 1.0]))
+    vals, _ = ds.eigs(g, rank=3, oversampling=0, power_iters=2, seed=0)
+    assert vals == pytest.approx([2.0, -2.0, 1.0], rel=1e-12)
+
+
+def test_eigs_rank_one(ds, oracle):
+    # ref tests/test_rsvd.cpp:132-156
+    x = oracle.fill_gaussian(3, 40)
+    x /= np.linalg.norm(x)
+    vals, resid = ds.eigs(ds.matrix_from_host(np.outer(x, x)), rank=1, oversampling=10,
+                          power_iters=2, seed=0)
+    assert vals[0] == pytest.approx(1.0, rel=1e-10)
+    assert resid < 1e-6
+
+
+def test_eigs_vs_dense(ds, oracle):
+    # ref tests/test_rsvd.cpp:158-183
+    w = [100.0 * 0.7 ** i for i in range(20)] + [0.0] * 40
+    g = with_spectrum(w, 12345, oracle)
+    vals, _ = ds.eigs(ds.matrix_from_host(g), rank=10, oversampling=10, power_iters=3, seed=0)
+    dense = np.sort(np.linalg.eigvalsh(g))[::-1][:10]
+    assert rel_err(vals, dense) < 1e-6
+
+
+def test_eigs_residual_tail(ds, oracle):
+    # ref tests/test_rsvd.cpp:202-216
+    g = ds.matrix_from_host(with_spectrum([6, 5, 4, 0, 0, 0, 0, 0], 8, oracle))
+    _, r3 = ds.eigs(g, rank=3, oversampling=5, power_iters=2, seed=0)
+    assert r3 < 1e-6
+    _, r2 = ds.eigs(g, rank=2, oversampling=0, power_iters=6, seed=0)
+    assert r2 == pytest.approx(4.0, rel=0.02)
+
+
+def test_eigs_errors(ds):
+    # ref tests/test_rsvd.cpp:218-250, test_capi.cpp:254-260
+    g = ds.matrix_from_host(np.diag([1.0, 2.0, 3.0]))
+    assert err(ds, ds.eigs, g, rank=3, oversampling=1) == ds.Status.ERR_RANK_TOO_LARGE
+    assert err(ds, ds.eigs, g, rank=0, oversampling=1) == ds.Status.ERR_INVALID_ARGUMENT
+    asym = ds.matrix_from_host(np.array([[0.0, 1.0], [2.0, 0.0]]))
+    assert err(ds, ds.eigs, asym, rank=1, oversampling=0) == ds.Status.ERR_NOT_SYMMETRIC
+    rect = ds.matrix_from_host(np.zeros((2, 3)), symmetric=False)
+    assert err(ds, ds.eigs, rect, rank=1, oversampling=0) == ds.Status.ERR_NOT_SYMMETRIC
+    empty = ds.matrix_from_host(np.zeros((0, 0)))
+    assert err(ds, ds.eigs, empty, rank=1, oversampling=0) == ds.Status.ERR_INVALID_ARGUMENT
+
+
+def test_eigs_matches_oracle_explicit(ds, oracle):
+    w = [50, 20, 10, 5, 2, 1, 0.5, 0.1] + [0.0] * 52
+    g = with_spectrum(w, 321, oracle)
+    vals, resid = ds.eigs(ds.matrix_from_host(g), rank=5, oversampling=5, power_iters=2, seed=9)
+    st, v_cpu, _, r_cpu = oracle.eigs(5, 5, 2, 9, g=g)
+    assert st == 0
+    assert rel_err(vals, v_cpu) < 1e-10
+    fro2 = float(np.sum(g * g))
+    assert abs(resid ** 2 - r_cpu ** 2) <= 1e-12 * fro2
+
+
+# ---------------------------------------------------------------- range
+
+def test_range_orthonormal(ds, oracle):
+    # ref tests/test_rsvd.cpp:50-62
+    g = ds.matrix_from_host(with_spectrum([9, 7, 5, 3, 1, 0.5, 0.1, 0.05], 4, oracle))
+    q = ds.randomized_range(g, rank=3, oversampling=2, power_iters=2, seed=0)
+    assert q.shape == (8, 5)
+    assert np.max(np.abs(q.T @ q - np.eye(5))) < 1e-8
+
+
+def test_range_captures_diagonal_subspace(ds):
+    # ref tests/test_rsvd.cpp:64-79
+    g = ds.matrix_from_host(np.diag([10.0, 5.0, 1.0] + [0.0] * 7))
+    q = ds.randomized_range(g, rank=3, oversampling=5, power_iters=2, seed=0)
+    for axis in range(3):
+        e = np.zeros(10)
+        e[axis] = 1.0
+        assert np.linalg.norm(q @ (q.T @ e) - e) < 1e-10
+
+
+# ---------------------------------------------------------------- embed KATs
+
+def test_embed_two_points(ds):
+    # ref tests/test_mds.cpp:103-114
+    g = ds.gram(ds.matrix_from_host(np.array([[0.0, 2.0], [2.0, 0.0]])))
+    e = ds.embed(g, rank=1, oversampling=10, power_iters=2, seed=0)
+    assert (e.rows, e.dims) == (2, 1)
+    assert e.eigenvalues[0] == pytest.approx(2.0, rel=1e-12)
+    c = e.coords
+    assert c[0, 0] == pytest.approx(1.0, rel=1e-10)
+    assert c[1, 0] == pytest.approx(-1.0, rel=1e-10)
+    assert e.dropped_negative_mass == 0.0 and not e.truncated
+
+
+def test_embed_zero_gram(ds):
+    # ref tests/test_mds.cpp:116-126
+    e = ds.embed(ds.matrix_from_host(np.zeros((3, 3))), rank=2, oversampling=10, seed=0)
+    assert e.rows == 3 and e.dims == 0 and e.truncated and e.dropped_negative_mass == 0.0
+
+
+def test_embed_euclidean_round_trip(ds, oracle):
+    # ref tests/test_mds.cpp:128-147 (and acceptance #3, acceptance.cpp:97-123)
+    pts = oracle.fill_gaussian(21, 40 * 3).reshape(40, 3)
+    d = oracle.euclidean_matrix(pts)
+    g = ds.gram(ds.matrix_from_host(d))
+    e = ds.embed(g, rank=3, oversampling=10, power_iters=2, seed=1)
+    assert e.dims == 3
+    x = e.coords
+    dd = np.sqrt(((x[:, None, :] - x[None, :, :]) ** 2).sum(-1))
+    iu = np.triu_indices(40, 1)
+    assert np.max(np.abs(dd[iu] - d[iu]) / d[iu]) < 1e-8
+
+
+def test_embed_truncation(ds, oracle):
+    # ref tests/test_mds.cpp:149-159
+    pts = oracle.fill_gaussian(33, 20 * 3).reshape(20, 3)
+    g = ds.gram(ds.matrix_from_host(oracle.euclidean_matrix(pts)))
+    e = ds.embed(g, rank=5, oversampling=10, power_iters=2, seed=0)
+    assert e.dims == 3 and e.truncated and len(e.eigenvalues) == 3
+
+
+def test_embed_column_norms_and_sign(ds, oracle):
+    # ref tests/test_mds.cpp:161-195
+    pts = oracle.fill_gaussian(44, 30 * 4).reshape(30, 4)
+    g = ds.gram(ds.matrix_from_host(oracle.euclidean_matrix(pts)))
+    e = ds.embed(g, rank=4, oversampling=10, power_iters=2, seed=0)
+    assert e.dims == 4
+    ev, x = e.eigenvalues, e.coords
+    assert np.all(ev > 0) and np.all(np.diff(ev) <= 0)
+    assert np.allclose((x * x).sum(0), ev, rtol=1e-6)
+    for c in range(4):
+        assert x[np.argmax(np.abs(x[:, c])), c] > 0
+
+
+def test_embed_negative_mass(ds):
+    # ref tests/test_mds.cpp:197-214, acceptance.cpp:191-217
+    d = np.ones((4, 4)) - np.eye(4)
+    d[2, 3] = d[3, 2] = 2.0
+    e = ds.embed(ds.gram(ds.matrix_from_host(d)), rank=4, oversampling=10, seed=5)
+    assert e.dropped_negative_mass > 0.0 and e.truncated and e.dims >= 2
+    assert np.all(e.eigenvalues > 0)
+
+
+def test_embed_rank_bounds(ds):
+    # ref tests/test_mds.cpp:216-225, test_capi.cpp:281-285
+    g = ds.gram(ds.matrix_from_host(np.array([[0.0, 2.0], [2.0, 0.0]])))
+    assert err(ds, ds.embed, g, rank=0) == ds.Status.ERR_RANK_TOO_LARGE
+    assert err(ds, ds.embed, g, rank=3) == ds.Status.ERR_RANK_TOO_LARGE
+    assert err(ds, ds.embed, g, rank=1, ids=["a", "b", "c"]) == ds.Status.ERR_SHAPE_MISMATCH
+
+
+def test_embed_ids_and_files(ds, tmp_path):
+    # ref tests/test_capi.cpp:255-278 (write / load round trip)
+    g = ds.gram(ds.matrix_from_host(np.array([[0.0, 2.0], [2.0, 0.0]])))
+    e = ds.embed(g, rank=1, ids=["a", "b"])
+    assert e.id(0) == "a" and e.id(2) is None
+    e.write(tmp_path / "e.tsv", tmp_path / "e.meta")
+    back = ds.embedding_load(tmp_path / "e.tsv")
+    assert back.rows == 2 and back.dims == 1 and back.get(1, 0) == e.get(1, 0)
+    assert len(back.eigenvalues) == 0
+    meta = (tmp_path / "e.meta").read_text().splitlines()
+    assert meta[0] == "rank=1" and meta[1] == "truncated=0"
+
+
+# ---------------------------------------------------------------- parity at scale
+
+def _parity(ds, oracle, d, k, p, q, seed, eig_tol, d_host=None, f32=False):
+    """embed through the GPU vs the oracle restatement on the same D and Omega."""
+    dm = ds.matrix_from_host_f32(d) if f32 else ds.matrix_from_host(d)
+    e = ds.embed(ds.gram(dm), rank=k, oversampling=p, power_iters=q, seed=seed)
+    dh = d_host if d_host is not None else d
+    st, rm, grand = oracle.gram_stats(dh)
+    assert st == 0
+    ref = oracle.embed(k, p, q, seed, d=dh, row_mean=rm, grand=grand)
+    assert ref["status"] == 0
+    return e, ref
+
+
+def test_c1_parity(ds, oracle):
+    # BASELINE config 1 at full size: n=2000, k=10, p=10, q=1
+    pts = ds.synth_points(1, 2000, 1)
+    d = oracle.euclidean_matrix(pts)
+    e, ref = _parity(ds, oracle, d, 10, 10, 1, 1, 1e-10)
+    assert e.dims == ref["r"] == 10 and e.truncated == ref["truncated"]
+    assert rel_err(e.eigenvalues, ref["eigenvalues"]) < 1e-10
+    lam = ref["eigenvalues"]
+    # coordinates: per column up to sign, scaled by sqrt(lambda_k)
+    assert coords_match_up_to_sign(e.coords, ref["coords"]) < 1e-8 * np.sqrt(lam[0])
+    assert sin_subspace(e.coords, ref["coords"]) < 1e-9
+    fro2 = float(np.sum(oracle.gram(d)[1] ** 2))
+    assert abs(e.resid ** 2 - ref["resid"] ** 2) <= 1e-11 * fro2
+
+
+def test_c5_like_hamming_parity(ds, oracle):
+    reads = ds.synth_reads(1500, 400, 50, 0.05, 5)
+    d = ds.matrix_hamming(reads).to_numpy()
+    e, ref = _parity(ds, oracle, d, 30, 20, 2, 5, 1e-10)
+    assert e.dims == ref["r"]
+    assert rel_err(e.eigenvalues, ref["eigenvalues"]) < 1e-10
+    assert abs(e.dropped_negative_mass - ref["dropped_negative_mass"]) <= 1e-10 * max(
+        1.0, abs(ref["eigenvalues"][0]))
+
+
+def test_c4_like_f32_parity(ds, oracle):
+    # fp32-stored D, fp64 arithmetic; w = 70 > dim 64: rank-deficient panel
+    pts = ds.synth_points(4, 1500, 7)
+    d32 = oracle.euclidean_matrix(pts).astype(np.float32)
+    d_wide = d32.astype(np.float64)
+    e, ref = _parity(ds, oracle, d32, 50, 20, 3, 7, 1e-4, d_host=d_wide, f32=True)
+    top = min(40, ref["r"])
+    assert rel_err(e.eigenvalues[:top], ref["eigenvalues"][:top]) < 1e-4
+
+
+def test_deterministic(ds):
+    pts = ds.synth_points(2, 700, 2)
+    g = ds.gram(ds.matrix_euclidean(pts))
+    a = ds.embed(g, rank=20, oversampling=10, power_iters=2, seed=3)
+    b = ds.embed(g, rank=20, oversampling=10, power_iters=2, seed=3)
+    assert np.array_equal(a.coords, b.coords) and np.array_equal(a.eigenvalues, b.eigenvalues)
+
+
+# ---------------------------------------------------------------- stable rank
+
+def test_stable_rank(ds):
+    # ref tests/test_rsvd.cpp:252-279, acceptance.cpp:219-238
+    assert ds.stable_rank(ds.matrix_from_host(np.diag([10.0, 5.0, 1.0]))) == pytest.approx(
+        1.26, rel=1e-11)
+    x = np.array([0.5, -1.25, 2.0, 0.75])
+    assert ds.stable_rank(ds.matrix_from_host(np.outer(x, x))) == pytest.approx(1.0, rel=1e-9)
+    assert ds.stable_rank(ds.matrix_from_host(np.eye(7))) == pytest.approx(7.0, rel=1e-9)
+    assert err(ds, ds.stable_rank, ds.matrix_from_host(np.zeros((3, 3)))) == \
+        ds.Status.ERR_ZERO_MATRIX
+
+
+# ---------------------------------------------------------------- DVS
+
+def test_dvs_round_trip(ds, tmp_path):
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((5, 7))
+    m = ds.matrix_from_host(a, symmetric=False)
+    m.write(tmp_path / "a.dvs")
+    b = ds.matrix_read(tmp_path / "a.dvs")
+    assert (b.rows, b.cols, b.symmetric) == (5, 7, False)
+    assert np.array_equal(b.to_numpy(), a)
