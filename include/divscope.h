@@ -226,6 +226,9 @@ void divscope_stats_reset(void);
 void divscope_stats_get(divscope_stats* out);
 /* stream the library enqueues on (cudaStream_t as void*) */
 void* divscope_stream(void);
+/* measured FP64 tensor-core (DMMA) throughput of this device in TFLOP/s
+ * (roofline denominator of the FP64-bound product pass); < 0 on failure */
+double divscope_fp64_tensor_peak_tflops(int iters);
 
 #ifdef __cplusplus
 }

@@ -523,6 +523,28 @@ void orc_euclidean_matrix(const double* pts, std::size_t n, std::size_t dim, dou
         }
 }
 
+// same, rows chunked over threads (parallel.hpp:17-46); each row's values do
+// not depend on the chunking, so the output is identical
+void orc_euclidean_matrix_mt(const double* pts, std::size_t n, std::size_t dim, unsigned threads,
+                             double* out) {
+    chunks(n, threads, [&](std::size_t begin, std::size_t end) {
+        for (std::size_t i = begin; i < end; ++i)
+            for (std::size_t j = 0; j < n; ++j) {
+                if (i == j) {
+                    out[i * n + j] = 0.0;
+                    continue;
+                }
+                const std::size_t a = std::min(i, j), b = std::max(i, j);
+                double sq = 0.0;
+                for (std::size_t c = 0; c < dim; ++c) {
+                    const double diff = pts[a * dim + c] - pts[b * dim + c];
+                    sq += diff * diff;
+                }
+                out[i * n + j] = std::sqrt(sq);
+            }
+    });
+}
+
 // sum_i sum_j of the explicit reconstruction error (mds.cpp:126-150)
 double orc_reconstruction_error(const double* g, std::size_t n, const double* coords,
                                 std::size_t r) {

@@ -30,6 +30,7 @@ __all__ = [
     "matrix_hamming", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
     "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
     "stats_enable_timing", "stats_reset", "stats_get", "set_device", "LIB_PATH",
+    "fp64_tensor_peak_tflops", "stream_ptr",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libdivscope_b200.so"
@@ -136,6 +137,7 @@ def _load() -> C.CDLL:
         "divscope_stats_reset": ([], None),
         "divscope_stats_get": ([C.POINTER(Stats)], None),
         "divscope_stream": ([], _vp),
+        "divscope_fp64_tensor_peak_tflops": ([C.c_int], C.c_double),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -145,10 +147,6 @@ def _load() -> C.CDLL:
 
 
 lib = _load()
-
-#: every symbol include/divscope.h declares (checked by the CPU test-suite)
-EXPORTED = sorted(n for n in dir(lib) if n.startswith("divscope_"))
-
 
 def _check(status: int) -> None:
     if status != 0:
@@ -414,6 +412,14 @@ def stats_enable_timing(on: bool = True) -> None:
 
 def stats_reset() -> None:
     lib.divscope_stats_reset()
+
+
+def fp64_tensor_peak_tflops(iters: int = 20000) -> float:
+    return lib.divscope_fp64_tensor_peak_tflops(iters)
+
+
+def stream_ptr() -> int:
+    return lib.divscope_stream() or 0
 
 
 def stats_get() -> Stats:

@@ -58,6 +58,7 @@ class Oracle:
                                 _dp, _dp, C.POINTER(_sz), _dp, C.POINTER(C.c_int), _dp]
         L.orc_hamming_counts.argtypes = [C.c_char_p, _sz, _sz, C.POINTER(C.c_uint32)]
         L.orc_euclidean_matrix.argtypes = [_dp, _sz, _sz, _dp]
+        L.orc_euclidean_matrix_mt.argtypes = [_dp, _sz, _sz, C.c_uint, _dp]
         L.orc_reconstruction_error.argtypes = [_dp, _sz, _dp, _sz]
         L.orc_reconstruction_error.restype = C.c_double
         L.orc_stable_rank.argtypes = [_dp, _sz, C.c_uint, _dp]
@@ -141,6 +142,13 @@ class Oracle:
         n, dim = pts.shape
         out = np.empty((n, n))
         self.lib.orc_euclidean_matrix(_ptr(np.ascontiguousarray(pts)), n, dim, _ptr(out))
+        return out
+
+    def euclidean_matrix_mt(self, pts: np.ndarray, threads: int | None = None) -> np.ndarray:
+        n, dim = pts.shape
+        out = np.empty((n, n))
+        self.lib.orc_euclidean_matrix_mt(_ptr(np.ascontiguousarray(pts)), n, dim,
+                                         threads or _threads(), _ptr(out))
         return out
 
     def reconstruction_error(self, g, coords):
