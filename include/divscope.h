@@ -218,6 +218,8 @@ typedef struct divscope_stats {
     double stats_ms;            /* summed K1 device time, when timing on */
     uint64_t h2d_bytes;
     uint64_t d2h_bytes;
+    int32_t last_evd_sweeps;    /* Jacobi sweeps of the last Rayleigh-Ritz EVD */
+    int32_t last_orth_shifted;  /* 1 if a shifted CholeskyQR step was needed */
 } divscope_stats;
 
 /* timing on => CUDA events are recorded around K1/K2 on the library stream */

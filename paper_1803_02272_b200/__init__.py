@@ -75,7 +75,8 @@ class SolverOptions(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("product_launches", C.c_uint64),
                 ("product_ms", C.c_double), ("stats_launches", C.c_uint64),
-                ("stats_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("stats_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("last_evd_sweeps", C.c_int32), ("last_orth_shifted", C.c_int32)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -138,6 +139,8 @@ def _load() -> C.CDLL:
         "divscope_stats_get": ([C.POINTER(Stats)], None),
         "divscope_stream": ([], _vp),
         "divscope_fp64_tensor_peak_tflops": ([C.c_int], C.c_double),
+        "divscope_bench_product": ([_vp, C.c_int, C.c_int, C.c_int], C.c_double),
+        "divscope_bench_product": ([_vp, C.c_int, C.c_int, C.c_int], C.c_double),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -416,6 +419,16 @@ def stats_reset() -> None:
 
 def fp64_tensor_peak_tflops(iters: int = 20000) -> float:
     return lib.divscope_fp64_tensor_peak_tflops(iters)
+
+
+def bench_product(m: "Matrix", wp: int, mode: int = 1, iters: int = 5) -> float:
+    """mean device ms of one K2 streaming-product launch (kernel tuning aid)"""
+    return lib.divscope_bench_product(m.handle, wp, mode, iters)
+
+
+def bench_product(m: "Matrix", wp: int, mode: int = 1, iters: int = 5) -> float:
+    """mean device ms of one K2 streaming-product launch (kernel tuning aid)"""
+    return lib.divscope_bench_product(m.handle, wp, mode, iters)
 
 
 def stream_ptr() -> int:

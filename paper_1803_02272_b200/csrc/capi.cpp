@@ -422,7 +422,9 @@ divscope_status divscope_embedding_load(const char* tsv_path, divscope_embedding
         auto* handle = new divscope_embedding;
         try {
             size_t dims = 0;
-            load_embedding_tsv(tsv_path, handle->ids, dims, handle->emb.coords);
+            std::vector<double> coords;
+            load_embedding_tsv(tsv_path, handle->ids, dims, coords);
+            handle->emb.coords.assign(coords);
             handle->emb.n = handle->ids.size();
             handle->emb.r = dims;
         } catch (...) {
@@ -477,6 +479,8 @@ void divscope_stats_get(divscope_stats* out) {
         out->stats_ms = c.k1_ms;
         out->h2d_bytes = c.h2d;
         out->d2h_bytes = c.d2h;
+        out->last_evd_sweeps = c.last_evd_sweeps;
+        out->last_orth_shifted = c.last_orth_shifted;
     } catch (...) {
     }
 }

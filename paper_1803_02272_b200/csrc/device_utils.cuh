@@ -96,6 +96,17 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 
+// D(16x8) += A(16x4) * B(4x8): a0/a1 = A[l/4][l%4], A[l/4+8][l%4]; b = B[l%4][l/4];
+// c0,c1 = C[l/4][2(l%4)+0/1], c2,c3 = C[l/4+8][2(l%4)+0/1]
+__device__ __forceinline__ void dmma1684(double& c0, double& c1, double& c2, double& c3, double a0,
+                                         double a1, double b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};"
+        : "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+        : "d"(a0), "d"(a1), "d"(b));
+}
+
 // ---- warp helpers -----------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -28,144 +28,89 @@ __device__ __forceinline__ int pk(int a, int b, int w) {
     return a * w - (a * (a - 1)) / 2 + (b - a);
 }
 
-constexpr int kEvdThreads = 512;
-
-__global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ bmat, int wp, int w,
-                                                     int rank, int requested,
-                                                     const double* __restrict__ scalars,
-                                                     int fro_index, EvdOut o) {
-    extern __shared__ double sm[];
-    const int npk = w * (w + 1) / 2;
-    double* A = sm;            // packed upper triangle
-    double* V = A + npk;       // [w][w]
-    __shared__ double cs[kMaxWP / 2 + 1], sn[kMaxWP / 2 + 1];
-    __shared__ int pp[kMaxWP / 2 + 1], qq[kMaxWP / 2 + 1];
-    __shared__ double red[2][kEvdThreads / 32];
-    __shared__ int done;
-    __shared__ int order[kMaxWP];
-    __shared__ int kept[kMaxWP];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int warp = tid >> 5, lane = tid & 31;
-
-    for (int a = tid; a < w; a += nt)
-        for (int b = a; b < w; ++b)
-            A[pk(a, b, w)] = 0.5 * (bmat[a * wp + b] + bmat[b * wp + a]);
-    for (int e = tid; e < w * w; e += nt) V[e] = (e / w == e % w) ? 1.0 : 0.0;
-    if (tid == 0) done = (w <= 1);
-    __syncthreads();
-
-    const int m = w + (w & 1);  // players (w odd -> one dummy)
-    const int h = m / 2;
-    const int nblk = h * (h + 1) / 2;
-    int sweeps = 0;
-    for (; sweeps < 60 && !done; ++sweeps) {
-        for (int r = 0; r < m - 1; ++r) {
-            // phase 1: rotations of this round's pairs
-            for (int k = tid; k < h; k += nt) {
-                const int x = (k == 0) ? 0 : 1 + ((k - 1 + r) % (m - 1));
-                const int kk = m - 1 - k;
-                const int y = 1 + ((kk - 1 + r) % (m - 1));
-                const int p = min(x, y), q = max(x, y);
-                double c = 1.0, s = 0.0;
-                if (q < w) {
-                    const double apq = A[pk(p, q, w)];
-                    if (fabs(apq) >= 1e-300) {
-                        const double app = A[pk(p, p, w)], aqq = A[pk(q, q, w)];
-                        const double theta = (aqq - app) / (2.0 * apq);
-                        const double t = (theta >= 0.0 ? 1.0 : -1.0) /
-                                         (fabs(theta) + sqrt(theta * theta + 1.0));
-                        c = 1.0 / sqrt(t * t + 1.0);
-                        s = t * c;
-                    }
-                }
-                pp[k] = p;
-                qq[k] = q;
-                cs[k] = c;
-                sn[k] = s;
-            }
-            __syncthreads();
-            // phase 2a: 2x2 blocks of A (J_i^T A J_j)
-            for (int e = tid; e < nblk; e += nt) {
-                // decode e -> (i, j), i <= j over h pairs (row-major upper)
-                int i = 0, rem = e;
-                while (rem >= h - i) {
-                    rem -= h - i;
-                    ++i;
-                }
-                const int j = i + rem;
-                const int pi = pp[i], qi = qq[i], pj = pp[j], qj = qq[j];
-                const double ci = cs[i], si = sn[i], cj = cs[j], sj = sn[j];
-                const bool vqi = qi < w, vqj = qj < w;
-                const double a11 = A[pk(pi, pj, w)];
-                const double a12 = vqj ? A[pk(pi, qj, w)] : 0.0;
-                const double a21 = vqi ? A[pk(qi, pj, w)] : 0.0;
-                const double a22 = (vqi && vqj) ? A[pk(qi, qj, w)] : 0.0;
-                const double b11 = cj * a11 - sj * a12, b12 = sj * a11 + cj * a12;
-                const double b21 = cj * a21 - sj * a22, b22 = sj * a21 + cj * a22;
-                const double n11 = ci * b11 - si * b21, n21 = si * b11 + ci * b21;
-                const double n12 = ci * b12 - si * b22, n22 = si * b12 + ci * b22;
-                if (i == j) {
-                    A[pk(pi, pi, w)] = n11;
-                    if (vqi) {
-                        A[pk(qi, qi, w)] = n22;
-                        A[pk(pi, qi, w)] = 0.0;
-                    }
-                } else {
-                    A[pk(pi, pj, w)] = n11;
-                    if (vqj) A[pk(pi, qj, w)] = n12;
-                    if (vqi) A[pk(qi, pj, w)] = n21;
-                    if (vqi && vqj) A[pk(qi, qj, w)] = n22;
-                }
-            }
-            // phase 2b: columns of V
-            for (int e = tid; e < w * h; e += nt) {
-                const int k = e / h, i = e % h;
-                const int p = pp[i], q = qq[i];
-                if (q < w) {
-                    const double c = cs[i], s = sn[i];
-                    const double vp = V[k * w + p], vq = V[k * w + q];
-                    V[k * w + p] = c * vp - s * vq;
-                    V[k * w + q] = s * vp + c * vq;
-                }
-            }
-            __syncthreads();
-        }
-        // convergence: off-diagonal energy vs diagonal energy
-        double off = 0.0, dg = 0.0;
-        for (int e = tid; e < npk; e += nt) {
-            // decode packed index e -> (a, b)
-            int a = 0, rem = e;
-            while (rem >= w - a) {
-                rem -= w - a;
-                ++a;
-            }
-            const double v = A[e];
-            if (rem == 0)
-                dg += v * v;
-            else
-                off += v * v;
-        }
-        off = warp_sum(off);
-        dg = warp_sum(dg);
-        if (lane == 0) {
-            red[0][warp] = off;
-            red[1][warp] = dg;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            double so = 0.0, sd = 0.0;
-            for (int k = 0; k < nt / 32; ++k) {
-                so += red[0][k];
-                sd += red[1][k];
-            }
-            done = (so == 0.0 || so <= 1e-34 * sd) ? 1 : 0;
-        }
-        __syncthreads();
+// Rotation of pair (p, q) annihilating a_pq (Rutishauser's formulas, as the
+// oracle's Jacobi): returns c, s with J = [[c, s], [-s, c]] on (p, q).
+__device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, double& c,
+                                           double& s) {
+    c = 1.0;
+    s = 0.0;
+    if (fabs(apq) >= 1e-300) {
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        c = 1.0 / sqrt(t * t + 1.0);
+        s = t * c;
     }
+}
 
+// (i, j) block of J_i^T A J_j for the 2x2 blocks of the round's pairs
+__device__ __forceinline__ void block_update(const double* __restrict__ Ain, double* __restrict__ Aout,
+                                             int w, int pi, int qi, int pj, int qj, double ci,
+                                             double si, double cj, double sj, bool diag) {
+    const bool vqi = qi < w, vqj = qj < w;
+    const double a11 = Ain[pk(pi, pj, w)];
+    const double a12 = vqj ? Ain[pk(pi, qj, w)] : 0.0;
+    const double a21 = vqi ? Ain[pk(qi, pj, w)] : 0.0;
+    const double a22 = (vqi && vqj) ? Ain[pk(qi, qj, w)] : 0.0;
+    const double b11 = cj * a11 - sj * a12, b12 = sj * a11 + cj * a12;
+    const double b21 = cj * a21 - sj * a22, b22 = sj * a21 + cj * a22;
+    const double n11 = ci * b11 - si * b21, n21 = si * b11 + ci * b21;
+    const double n12 = ci * b12 - si * b22, n22 = si * b12 + ci * b22;
+    if (diag) {
+        Aout[pk(pi, pi, w)] = n11;
+        if (vqi) {
+            Aout[pk(qi, qi, w)] = n22;
+            Aout[pk(pi, qi, w)] = 0.0;
+        }
+    } else {
+        Aout[pk(pi, pj, w)] = n11;
+        if (vqj) Aout[pk(pi, qj, w)] = n12;
+        if (vqi) Aout[pk(qi, pj, w)] = n21;
+        if (vqi && vqj) Aout[pk(qi, qj, w)] = n22;
+    }
+}
+
+// round-robin tournament: players 0..m-1, player 0 fixed
+__device__ __forceinline__ void pair_at(int r, int k, int m, int& p, int& q) {
+    const int x = (k == 0) ? 0 : 1 + ((k - 1 + r) % (m - 1));
+    const int y = 1 + ((m - 2 - k + r) % (m - 1));
+    p = min(x, y);
+    q = max(x, y);
+}
+
+// off-diagonal / diagonal energy of packed A -> done flag (block reduce)
+__device__ int jacobi_converged(const double* __restrict__ A, int w, double* red) {
+    const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
+    double off = 0.0, dg = 0.0;
+    for (int a = tid; a < w; a += nt) {
+        const double* row = A + pk(a, a, w);
+        dg += row[0] * row[0];
+        for (int b = 1; b < w - a; ++b) off += row[b] * row[b];
+    }
+    off = warp_sum(off);
+    dg = warp_sum(dg);
+    if (lane == 0) {
+        red[warp] = off;
+        red[32 + warp] = dg;
+    }
+    __syncthreads();
+    double so = 0.0, sd = 0.0;
+    for (int k = 0; k < nt / 32; ++k) {
+        so += red[k];
+        sd += red[32 + k];
+    }
+    __syncthreads();
+    return (so == 0.0 || so <= 1e-34 * sd) ? 1 : 0;
+}
+
+// Shared tail: reference ordering (rsvd.cpp:118-127), keep / resid
+// (rsvd.cpp:129-142), embed filter (mds.cpp:85-99), V_keep.
+__device__ void evd_finish(const double* __restrict__ A, const double* __restrict__ V, int w,
+                           int rank, int requested, const double* __restrict__ scalars,
+                           int fro_index, const EvdOut& o, int sweeps, int done,
+                           int* __restrict__ order, int* __restrict__ kept) {
+    const int tid = threadIdx.x, nt = blockDim.x;
     if (tid == 0) {
         // ascending (stable on index), then stable by |lambda| desc, + first
-        // (the reference sorts Eigen's ascending output, rsvd.cpp:118-127)
         for (int a = 0; a < w; ++a) order[a] = a;
         for (int a = 1; a < w; ++a) {
             const int x = order[a];
@@ -183,8 +128,7 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
             int b = a - 1;
             while (b >= 0) {
                 const double vb = A[pk(order[b], order[b], w)];
-                const bool x_before =
-                    (fabs(vx) != fabs(vb)) ? (fabs(vx) > fabs(vb)) : (vx > vb);
+                const bool x_before = (fabs(vx) != fabs(vb)) ? (fabs(vx) > fabs(vb)) : (vx > vb);
                 if (!x_before) break;
                 order[b + 1] = order[b];
                 --b;
@@ -221,35 +165,197 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
         for (int c = 0; c < cnt; ++c) o.kept_vals[c] = A[pk(kept[c], kept[c], w)];
     }
     __syncthreads();
-    // V_keep [w][requested]
-    int r = o.imeta[1];
+    const int r = o.imeta[1];
     for (int e = tid; e < w * requested; e += nt) {
         const int x = e / requested, c = e % requested;
         o.vkeep[e] = c < r ? V[x * w + kept[c]] : 0.0;
     }
 }
 
-// U = Q V_keep for a CTA-contiguous row range, written to coords (n x r),
-// plus the CTA's per-column (|u| max, first index) partial.
+constexpr int kEvdThreads = 512;
+
+// General kernel (any w <= 128): packed A single-buffered, rotations of a
+// round computed first (barrier), then all 2x2 blocks and V row pairs.
+__global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ bmat, int wp, int w,
+                                                     int rank, int requested,
+                                                     const double* __restrict__ scalars,
+                                                     int fro_index, EvdOut o) {
+    extern __shared__ double sm[];
+    const int npk = w * (w + 1) / 2;
+    double* A = sm;       // packed upper triangle
+    double* V = A + npk;  // [w][w]
+    __shared__ double cs[kMaxWP / 2 + 1], sn[kMaxWP / 2 + 1];
+    __shared__ int pp[kMaxWP / 2 + 1], qq[kMaxWP / 2 + 1];
+    __shared__ double red[64];
+    __shared__ int order[kMaxWP], kept[kMaxWP];
+    __shared__ unsigned char blk_i[(kMaxWP / 2) * (kMaxWP / 2 + 1) / 2];
+    __shared__ unsigned char blk_j[(kMaxWP / 2) * (kMaxWP / 2 + 1) / 2];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int a = tid; a < w; a += nt)
+        for (int b = a; b < w; ++b) A[pk(a, b, w)] = 0.5 * (bmat[a * wp + b] + bmat[b * wp + a]);
+    for (int e = tid; e < w * w; e += nt) V[e] = (e / w == e % w) ? 1.0 : 0.0;
+    const int m = w + (w & 1), h = m / 2, nblk = h * (h + 1) / 2;
+    for (int i = tid; i < h; i += nt) {
+        const int base = i * h - (i * (i - 1)) / 2;
+        for (int j = i; j < h; ++j) {
+            blk_i[base + j - i] = static_cast<unsigned char>(i);
+            blk_j[base + j - i] = static_cast<unsigned char>(j);
+        }
+    }
+    __syncthreads();
+    int done = (w <= 1), sweeps = 0;
+    for (; sweeps < 60 && !done; ++sweeps) {
+        for (int r = 0; r < m - 1; ++r) {
+            for (int k = tid; k < h; k += nt) {
+                int p, q;
+                pair_at(r, k, m, p, q);
+                double c = 1.0, s = 0.0;
+                if (q < w) jacobi_rot(A[pk(p, p, w)], A[pk(q, q, w)], A[pk(p, q, w)], c, s);
+                pp[k] = p;
+                qq[k] = q;
+                cs[k] = c;
+                sn[k] = s;
+            }
+            __syncthreads();
+            for (int e = tid; e < nblk; e += nt) {
+                const int i = blk_i[e], j = blk_j[e];
+                block_update(A, A, w, pp[i], qq[i], pp[j], qq[j], cs[i], sn[i], cs[j], sn[j], i == j);
+            }
+            for (int e = tid; e < w * h; e += nt) {
+                const int k = e / h, i = e % h;
+                const int p = pp[i], q = qq[i];
+                if (q < w) {
+                    const double c = cs[i], s = sn[i];
+                    const double vp = V[k * w + p], vq = V[k * w + q];
+                    V[k * w + p] = c * vp - s * vq;
+                    V[k * w + q] = s * vp + c * vq;
+                }
+            }
+            __syncthreads();
+        }
+        done = jacobi_converged(A, w, red);
+    }
+    evd_finish(A, V, w, rank, requested, scalars, fro_index, o, sweeps, done, order, kept);
+}
+
+// Small-w kernel (w <= 64): A double-buffered, so every thread computes the
+// (redundant, identical) rotations it needs from the previous round's A and
+// a round costs ONE barrier; V is rotated one round behind with the
+// rotations the diagonal-block threads published.
+__global__ void __launch_bounds__(kEvdThreads) k_evd_small(const double* __restrict__ bmat, int wp,
+                                                           int w, int rank, int requested,
+                                                           const double* __restrict__ scalars,
+                                                           int fro_index, EvdOut o) {
+    extern __shared__ double sm[];
+    const int npk = w * (w + 1) / 2;
+    double* Abuf[2] = {sm, sm + npk};
+    double* V = sm + 2 * npk;  // [w][w]
+    __shared__ double cs[2][33], sn[2][33];
+    __shared__ unsigned char pp[2][33], qq[2][33];
+    __shared__ double red[64];
+    __shared__ int order[kMaxWP], kept[kMaxWP];
+    __shared__ unsigned char blk_i[32 * 33 / 2], blk_j[32 * 33 / 2];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int a = tid; a < w; a += nt)
+        for (int b = a; b < w; ++b)
+            Abuf[0][pk(a, b, w)] = 0.5 * (bmat[a * wp + b] + bmat[b * wp + a]);
+    for (int e = tid; e < w * w; e += nt) V[e] = (e / w == e % w) ? 1.0 : 0.0;
+    const int m = w + (w & 1), h = m / 2, nblk = h * (h + 1) / 2;
+    for (int i = tid; i < h; i += nt) {
+        const int base = i * h - (i * (i - 1)) / 2;
+        for (int j = i; j < h; ++j) {
+            blk_i[base + j - i] = static_cast<unsigned char>(i);
+            blk_j[base + j - i] = static_cast<unsigned char>(j);
+        }
+    }
+    if (tid < 33) {
+        cs[0][tid] = cs[1][tid] = 1.0;
+        sn[0][tid] = sn[1][tid] = 0.0;
+        pp[0][tid] = pp[1][tid] = 0;
+        qq[0][tid] = qq[1][tid] = 255;
+    }
+    __syncthreads();
+    int cur = 0, slot = 0, done = (w <= 1), sweeps = 0;
+    for (; sweeps < 60 && !done; ++sweeps) {
+        for (int r = 0; r < m - 1; ++r) {
+            const double* Ain = Abuf[cur];
+            double* Aout = Abuf[cur ^ 1];
+            for (int e = tid; e < nblk; e += nt) {
+                const int i = blk_i[e], j = blk_j[e];
+                int pi, qi, pj, qj;
+                pair_at(r, i, m, pi, qi);
+                pair_at(r, j, m, pj, qj);
+                double ci = 1.0, si = 0.0, cj = 1.0, sj = 0.0;
+                if (qi < w) jacobi_rot(Ain[pk(pi, pi, w)], Ain[pk(qi, qi, w)], Ain[pk(pi, qi, w)], ci, si);
+                if (i == j) {
+                    cj = ci;
+                    sj = si;
+                    cs[slot][i] = ci;
+                    sn[slot][i] = si;
+                    pp[slot][i] = static_cast<unsigned char>(pi);
+                    qq[slot][i] = static_cast<unsigned char>(qi);
+                } else if (qj < w) {
+                    jacobi_rot(Ain[pk(pj, pj, w)], Ain[pk(qj, qj, w)], Ain[pk(pj, qj, w)], cj, sj);
+                }
+                block_update(Ain, Aout, w, pi, qi, pj, qj, ci, si, cj, sj, i == j);
+            }
+            // V with the previous round's rotations (slot ^ 1)
+            for (int e = tid; e < w * h; e += nt) {
+                const int k = e / h, i = e % h;
+                const int p = pp[slot ^ 1][i], q = qq[slot ^ 1][i];
+                if (q < w) {
+                    const double c = cs[slot ^ 1][i], s = sn[slot ^ 1][i];
+                    const double vp = V[k * w + p], vq = V[k * w + q];
+                    V[k * w + p] = c * vp - s * vq;
+                    V[k * w + q] = s * vp + c * vq;
+                }
+            }
+            __syncthreads();
+            cur ^= 1;
+            slot ^= 1;
+        }
+        done = jacobi_converged(Abuf[cur], w, red);
+    }
+    // last round's rotations still owe V
+    for (int e = tid; e < w * h; e += nt) {
+        const int k = e / h, i = e % h;
+        const int p = pp[slot ^ 1][i], q = qq[slot ^ 1][i];
+        if (q < w) {
+            const double c = cs[slot ^ 1][i], s = sn[slot ^ 1][i];
+            const double vp = V[k * w + p], vq = V[k * w + q];
+            V[k * w + p] = c * vp - s * vq;
+            V[k * w + q] = s * vp + c * vq;
+        }
+    }
+    __syncthreads();
+    evd_finish(Abuf[cur], V, w, rank, requested, scalars, fro_index, o, sweeps, done, order, kept);
+}
+
+// U = Q V_keep (n x r, row-major into coords). CTA c owns rows
+// [n c / P, n (c+1) / P); thread t owns column t % r and rows t / r + k * (256 / r),
+// keeping a running (value at max |u|, first index) that is merged in thread
+// (= row) order into the CTA partial — the sign rule of ref mds.cpp:65-77.
 __global__ void __launch_bounds__(256) k_lift(const double* __restrict__ q, int n, int wp, int w,
                                               const double* __restrict__ vkeep,
                                               const int* __restrict__ imeta, int rmax,
                                               double* __restrict__ coords,
                                               double* __restrict__ partial) {
-    extern __shared__ double sv[];  // [w][rmax] then [4 * wp] staging
+    extern __shared__ double sv[];  // [w][rmax]
+    __shared__ double best_v[256];
+    __shared__ int best_i[256];
     const int r = imeta[1];
+    if (r == 0) return;
     for (int e = threadIdx.x; e < w * rmax; e += blockDim.x) sv[e] = vkeep[e];
     __syncthreads();
     const int row0 = static_cast<int>(static_cast<long long>(n) * blockIdx.x / gridDim.x);
     const int row1 = static_cast<int>(static_cast<long long>(n) * (blockIdx.x + 1) / gridDim.x);
-    // per column: threads stride over the CTA's rows keeping a running
-    // (value at max |u|, first index); merged in thread order below
-    __shared__ double best_v[256];
-    __shared__ int best_i[256];
-    for (int c = 0; c < r; ++c) {
-        double bv = 0.0;
-        int bi = -1;
-        for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+    const int per = 256 / r;  // rows in flight per sweep (r <= 128)
+    const int t = threadIdx.x;
+    double bv = 0.0;
+    int bi = -1;
+    if (t < per * r) {
+        const int c = t % r;
+        for (int i = row0 + t / r; i < row1; i += per) {
             double s = 0.0;
             for (int k = 0; k < w; ++k) s += q[pidx(i, k, wp)] * sv[k * rmax + c];
             coords[static_cast<size_t>(i) * r + c] = s;
@@ -258,50 +364,65 @@ __global__ void __launch_bounds__(256) k_lift(const double* __restrict__ q, int 
                 bi = i;
             }
         }
-        best_v[threadIdx.x] = bv;
-        best_i[threadIdx.x] = bi;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double v = 0.0;
-            int ix = -1;
-            for (int t = 0; t < blockDim.x; ++t) {
-                const int ti = best_i[t];
-                if (ti < 0) continue;
-                const double tv = best_v[t];
-                if (ix < 0 || fabs(tv) > fabs(v) || (fabs(tv) == fabs(v) && ti < ix)) {
-                    v = tv;
-                    ix = ti;
-                }
-            }
-            partial[(static_cast<size_t>(blockIdx.x) * rmax + c) * 2 + 0] = v;
-            partial[(static_cast<size_t>(blockIdx.x) * rmax + c) * 2 + 1] = static_cast<double>(ix);
-        }
-        __syncthreads();
     }
-}
-
-__global__ void k_lift_scale(int n, const int* __restrict__ imeta, int P, int rmax,
-                             const double* __restrict__ kept_vals,
-                             const double* __restrict__ partial, double* __restrict__ coords) {
-    __shared__ double scale[kMaxWP];
-    const int r = imeta[1];
-    if (threadIdx.x < r) {
-        const int c = threadIdx.x;
+    best_v[t] = bv;
+    best_i[t] = bi;
+    __syncthreads();
+    if (t < r) {
         double v = 0.0;
-        long long ix = -1;
-        for (int b = 0; b < P; ++b) {
-            const double iv = partial[(static_cast<size_t>(b) * rmax + c) * 2 + 1];
-            if (iv < 0) continue;
-            const double tv = partial[(static_cast<size_t>(b) * rmax + c) * 2 + 0];
-            const long long ti = static_cast<long long>(iv);
+        int ix = -1;
+        for (int k = 0; k < per; ++k) {  // threads t + k r own column t, rows in order
+            const int ti = best_i[t + k * r];
+            if (ti < 0) continue;
+            const double tv = best_v[t + k * r];
             if (ix < 0 || fabs(tv) > fabs(v) || (fabs(tv) == fabs(v) && ti < ix)) {
                 v = tv;
                 ix = ti;
             }
         }
-        const double sg = (v < 0.0) ? -1.0 : 1.0;
-        scale[c] = sg * sqrt(kept_vals[c]);
+        partial[(static_cast<size_t>(blockIdx.x) * rmax + t) * 2 + 0] = v;
+        partial[(static_cast<size_t>(blockIdx.x) * rmax + t) * 2 + 1] = static_cast<double>(ix);
     }
+}
+
+// per column: merge the CTA partials (warp per column, any order gives the
+// same winner: larger |u|, then smaller index), scale = sign * sqrt(lambda)
+__global__ void __launch_bounds__(256) k_lift_signs(const int* __restrict__ imeta, int P, int rmax,
+                                                    const double* __restrict__ kept_vals,
+                                                    const double* __restrict__ partial,
+                                                    double* __restrict__ scale) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int r = imeta[1];
+    if (warp >= r) return;
+    double v = 0.0;
+    long long ix = -1;
+    for (int b = lane; b < P; b += 32) {
+        const double iv = partial[(static_cast<size_t>(b) * rmax + warp) * 2 + 1];
+        if (iv < 0) continue;
+        const double tv = partial[(static_cast<size_t>(b) * rmax + warp) * 2 + 0];
+        const long long ti = static_cast<long long>(iv);
+        if (ix < 0 || fabs(tv) > fabs(v) || (fabs(tv) == fabs(v) && ti < ix)) {
+            v = tv;
+            ix = ti;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (oi >= 0 && (ix < 0 || fabs(ov) > fabs(v) || (fabs(ov) == fabs(v) && oi < ix))) {
+            v = ov;
+            ix = oi;
+        }
+    }
+    if (lane == 0) scale[warp] = (v < 0.0 ? -1.0 : 1.0) * sqrt(kept_vals[warp]);
+}
+
+__global__ void k_lift_scale(int n, const int* __restrict__ imeta,
+                             const double* __restrict__ scale_g, double* __restrict__ coords) {
+    __shared__ double scale[kMaxWP];
+    const int r = imeta[1];
+    if (threadIdx.x < r) scale[threadIdx.x] = scale_g[threadIdx.x];
     __syncthreads();
     const size_t total = static_cast<size_t>(n) * r;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
@@ -313,15 +434,28 @@ __global__ void k_lift_scale(int n, const int* __restrict__ imeta, int P, int rm
 
 void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
                 const double* scalars, int fro_index, const EvdOut& o, cudaStream_t st) {
-    const size_t smem = (static_cast<size_t>(w) * (w + 1) / 2 + static_cast<size_t>(w) * w) *
-                        sizeof(double);
-    static size_t set_for = 0;
-    if (smem > 48 * 1024 && smem > set_for) {
-        cudaFuncSetAttribute(k_evd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        set_for = smem;
+    if (w <= 64) {
+        const size_t smem = (static_cast<size_t>(w) * (w + 1) + static_cast<size_t>(w) * w) *
+                            sizeof(double);
+        static size_t set_small = 0;
+        if (smem > 48 * 1024 && smem > set_small) {
+            cudaFuncSetAttribute(k_evd_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            set_small = smem;
+        }
+        const int threads = w <= 32 ? 128 : 512;
+        k_evd_small<<<1, threads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
+    } else {
+        const size_t smem = (static_cast<size_t>(w) * (w + 1) / 2 + static_cast<size_t>(w) * w) *
+                            sizeof(double);
+        static size_t set_for = 0;
+        if (smem > 48 * 1024 && smem > set_for) {
+            cudaFuncSetAttribute(k_evd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            set_for = smem;
+        }
+        k_evd<<<1, kEvdThreads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
     }
-    k_evd<<<1, kEvdThreads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
     count_launch();
 }
 
@@ -339,9 +473,12 @@ void launch_lift(const double* q, size_t n, int wp, int w, const double* vkeep,
     }
     k_lift<<<P, 256, smem, st>>>(q, static_cast<int>(n), wp, w, vkeep, imeta, rmax, coords,
                                  partial);
-    k_lift_scale<<<std::min(P, 1024), 256, 0, st>>>(static_cast<int>(n), imeta, P, rmax,
-                                                    kept_vals, partial, coords);
-    count_launch(2);
+    double* scale = partial + static_cast<size_t>(P) * rmax * 2;
+    k_lift_signs<<<(rmax * 32 + 255) / 256, 256, 0, st>>>(imeta, P, rmax, kept_vals, partial,
+                                                         scale);
+    const int sg = static_cast<int>(std::min<size_t>((n * rmax + 255) / 256, 148 * 8));
+    k_lift_scale<<<std::max(sg, 1), 256, 0, st>>>(static_cast<int>(n), imeta, scale, coords);
+    count_launch(3);
 }
 
 }  // namespace dsb

@@ -7,7 +7,10 @@
 #include <charconv>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <fstream>
+#include <map>
+#include <mutex>
 
 namespace dsb {
 
@@ -116,6 +119,19 @@ void Ctx::end_timed(int kind, cudaEvent_t a) {
     pending.push_back({a, b, kind});
 }
 
+void Ctx::make_events(cudaEvent_t* a, cudaEvent_t* b) {
+    *a = *b = nullptr;
+    if (!timing) return;
+    DSB_CUDA(cudaEventCreate(a));
+    DSB_CUDA(cudaEventCreate(b));
+}
+
+void Ctx::add_timed(int kind, cudaEvent_t a, cudaEvent_t b) {
+    if (kind == 1) ++k2_launches;
+    else ++k1_launches;
+    if (a && b) pending.push_back({a, b, kind});
+}
+
 void Ctx::drain_timing() {
     if (pending.empty()) return;
     DSB_CUDA(cudaStreamSynchronize(stream));
@@ -148,12 +164,12 @@ void Ctx::sync() {
 }
 
 bool Ctx::encode_tmap(CUtensorMap* map, const void* base, DType dt, size_t rows, size_t cols,
-                      size_t ld_elems) {
+                      size_t ld_elems, int box_rows) {
     auto fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(encode_fn_);
     const size_t esz = dt == DType::F64 ? 8 : 4;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems * esz)};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(kBM)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
     const CUresult r =
         fn(map, dt == DType::F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
@@ -164,6 +180,70 @@ bool Ctx::encode_tmap(CUtensorMap* map, const void* base, DType dt, size_t rows,
 }
 
 size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+namespace {
+std::mutex g_pool_mu;
+std::multimap<size_t, void*> g_pool;  // capacity (bytes) -> free pinned block
+size_t g_pool_bytes = 0;
+constexpr size_t kPoolCap = size_t(4) << 30;
+}  // namespace
+
+void PinnedVec::resize(size_t n) {
+    if (n <= cap_) {
+        n_ = n;
+        return;
+    }
+    release();
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(double);
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        auto it = g_pool.lower_bound(bytes);
+        if (it != g_pool.end() && it->first <= 2 * bytes) {
+            p_ = static_cast<double*>(it->second);
+            cap_ = it->first / sizeof(double);
+            g_pool_bytes -= it->first;
+            g_pool.erase(it);
+            pinned_ = true;
+            n_ = n;
+            return;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) == cudaSuccess) {
+        pinned_ = true;
+    } else {
+        cudaGetLastError();
+        p = std::malloc(bytes);
+        if (!p) throw std::bad_alloc();
+        pinned_ = false;
+    }
+    p_ = static_cast<double*>(p);
+    cap_ = bytes / sizeof(double);
+    n_ = n;
+}
+
+void PinnedVec::assign(const std::vector<double>& v) {
+    resize(v.size());
+    if (!v.empty()) std::memcpy(p_, v.data(), v.size() * sizeof(double));
+}
+
+void PinnedVec::release() {
+    if (!p_) return;
+    if (pinned_) {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        const size_t bytes = cap_ * sizeof(double);
+        if (g_pool_bytes + bytes <= kPoolCap) {
+            g_pool.emplace(bytes, p_);
+            g_pool_bytes += bytes;
+        } else {
+            cudaFreeHost(p_);
+        }
+    } else {
+        std::free(p_);
+    }
+    p_ = nullptr;
+    n_ = cap_ = 0;
+}
 
 std::shared_ptr<Store> make_store(size_t rows, size_t cols, bool symmetric, DType dt) {
     auto s = std::make_shared<Store>();

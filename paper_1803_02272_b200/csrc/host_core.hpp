@@ -87,9 +87,13 @@ public:
     uint64_t launches_base = 0;
     uint64_t k2_launches = 0, k1_launches = 0, h2d = 0, d2h = 0;
     double k2_ms = 0.0, k1_ms = 0.0;
+    int last_evd_sweeps = 0, last_orth_shifted = 0;
     std::vector<TimedPair> pending;
     void begin_timed(int kind, cudaEvent_t* a);
     void end_timed(int kind, cudaEvent_t a);
+    // events created (when timing) for a caller that records them itself
+    void make_events(cudaEvent_t* a, cudaEvent_t* b);
+    void add_timed(int kind, cudaEvent_t a, cudaEvent_t b);
     void drain_timing();
 
     void h2d_copy(void* dst, const void* src, size_t bytes);
@@ -97,7 +101,7 @@ public:
     void sync();
 
     bool encode_tmap(CUtensorMap* map, const void* base, DType dt, size_t rows, size_t cols,
-                     size_t ld_elems);
+                     size_t ld_elems, int box_rows);
 
     void set_device(int dev);
 
@@ -117,7 +121,8 @@ struct Store {
     std::shared_ptr<DevBuf> buf;
     // cached TMA descriptor for the K2 streaming read
     bool tmap_ok = false;
-    CUtensorMap tmap{};
+    CUtensorMap tmap128{}, tmap256{};  // box heights of the two K2 tile shapes
+    const CUtensorMap* tmap_for(int bm) const { return bm == 256 ? &tmap256 : &tmap128; }
     // cached K1 results when used as an explicit symmetric matrix
     bool stats_ok = false;
     double stats[S_COUNT] = {};
@@ -133,6 +138,45 @@ struct GramInfo {
     std::vector<double> row_mean_h;       // host copy (for _get / _write)
     std::shared_ptr<DevBuf> scalars;      // [S_COUNT]
     double sc[S_COUNT] = {};
+    std::mutex mu;
+};
+
+// Host array of doubles in pinned (page-locked) memory drawn from a recycling
+// pool, so device->host result copies run at full PCIe / C2C speed without
+// paying cudaMallocHost per call. Falls back to pageable memory when pinning
+// is unavailable.
+class PinnedVec {
+public:
+    PinnedVec() = default;
+    explicit PinnedVec(size_t n) { resize(n); }
+    PinnedVec(const PinnedVec&) = delete;
+    PinnedVec& operator=(const PinnedVec&) = delete;
+    PinnedVec(PinnedVec&& o) noexcept { swap(o); }
+    PinnedVec& operator=(PinnedVec&& o) noexcept {
+        swap(o);
+        return *this;
+    }
+    ~PinnedVec() { release(); }
+    void resize(size_t n);
+    void assign(const std::vector<double>& v);
+    double* data() { return p_; }
+    const double* data() const { return p_; }
+    size_t size() const { return n_; }
+    bool empty() const { return n_ == 0; }
+    double& operator[](size_t i) { return p_[i]; }
+    double operator[](size_t i) const { return p_[i]; }
+
+private:
+    void release();
+    void swap(PinnedVec& o) noexcept {
+        std::swap(p_, o.p_);
+        std::swap(n_, o.n_);
+        std::swap(cap_, o.cap_);
+        std::swap(pinned_, o.pinned_);
+    }
+    double* p_ = nullptr;
+    size_t n_ = 0, cap_ = 0;
+    bool pinned_ = false;
 };
 
 size_t round_up(size_t x, size_t m);

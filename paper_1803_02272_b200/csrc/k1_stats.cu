@@ -194,34 +194,53 @@ __global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ pa
     }
 }
 
-__global__ void k1_finalize(const double* __restrict__ cta_stats, int ncta,
-                            const double* __restrict__ blk_stats, int nblk, int n,
-                            double* __restrict__ scalars) {
-    if (threadIdx.x != 0) return;
-    double sum4 = 0, m1 = 0, m2 = 0, m3 = 0;
-    for (int c = 0; c < ncta; ++c) {
+// One block: thread t reduces entries t, t+256, ... (fixed order), then a
+// fixed-order tree over the 256 threads — deterministic.
+__global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ cta_stats, int ncta,
+                                                   const double* __restrict__ blk_stats, int nblk,
+                                                   int n, double* __restrict__ scalars) {
+    __shared__ double sh[7][256];
+    const int t = threadIdx.x;
+    double sum4 = 0, m1 = 0, m2 = 0, m3 = 0, rows = 0, sr = 0, sr2 = 0;
+    for (int c = t; c < ncta; c += 256) {
         sum4 += cta_stats[c * 4 + 0];
         m1 = fmax(m1, cta_stats[c * 4 + 1]);
         m2 = fmax(m2, cta_stats[c * 4 + 2]);
         m3 = fmax(m3, cta_stats[c * 4 + 3]);
     }
-    double rows = 0, sr = 0, sr2 = 0;
-    for (int b = 0; b < nblk; ++b) {
+    for (int b = t; b < nblk; b += 256) {
         rows += blk_stats[b * 3 + 0];
         sr += blk_stats[b * 3 + 1];
         sr2 += blk_stats[b * 3 + 2];
     }
-    const double nf = static_cast<double>(n);
-    const double grand = sr / nf;
-    scalars[S_GRAND] = grand;
-    scalars[S_FRO2_LAZY] = 0.25 * (sum4 - 2.0 * nf * sr2 + nf * nf * grand * grand);
-    scalars[S_FRO2_EXPL] = rows;
-    scalars[S_MAXABS] = m1;
-    scalars[S_MAXABS_UP] = m2;
-    scalars[S_MAXASYM] = m3;
-    scalars[S_SUM4] = sum4;
-    scalars[S_SUMR] = sr;
-    scalars[S_SUMR2] = sr2;
+    sh[0][t] = sum4; sh[1][t] = m1; sh[2][t] = m2; sh[3][t] = m3;
+    sh[4][t] = rows; sh[5][t] = sr; sh[6][t] = sr2;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (t < off) {
+            sh[0][t] += sh[0][t + off];
+            sh[1][t] = fmax(sh[1][t], sh[1][t + off]);
+            sh[2][t] = fmax(sh[2][t], sh[2][t + off]);
+            sh[3][t] = fmax(sh[3][t], sh[3][t + off]);
+            sh[4][t] += sh[4][t + off];
+            sh[5][t] += sh[5][t + off];
+            sh[6][t] += sh[6][t + off];
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        const double nf = static_cast<double>(n);
+        const double grand = sh[5][0] / nf;
+        scalars[S_GRAND] = grand;
+        scalars[S_FRO2_LAZY] = 0.25 * (sh[0][0] - 2.0 * nf * sh[6][0] + nf * nf * grand * grand);
+        scalars[S_FRO2_EXPL] = sh[4][0];
+        scalars[S_MAXABS] = sh[1][0];
+        scalars[S_MAXABS_UP] = sh[2][0];
+        scalars[S_MAXASYM] = sh[3][0];
+        scalars[S_SUM4] = sh[0][0];
+        scalars[S_SUMR] = sh[5][0];
+        scalars[S_SUMR2] = sh[6][0];
+    }
 }
 
 }  // namespace
@@ -254,7 +273,7 @@ void launch_k1(const void* d, DType dt, size_t ld, size_t n, const K1Work& w, do
     const int nblk = static_cast<int>((n + 255) / 256);
     k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, part_ld, nbt, static_cast<int>(n), row_mean,
                                       w.blk_stats);
-    k1_finalize<<<1, 32, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),
+    k1_finalize<<<1, 256, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),
                                   scalars);
     count_launch(3);
 }

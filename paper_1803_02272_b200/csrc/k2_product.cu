@@ -37,19 +37,25 @@ namespace dsb {
 
 namespace {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kTileBytes = kBM * 128;  // one D stage: 128 rows x 128 bytes
+// CW consumer warps own 16 rows each: BM = 16 CW rows of D per tile.
+template <int CW>
+constexpr int bm_of() {
+    return 16 * CW;
+}
+template <int CW>
+constexpr int tile_bytes() {
+    return bm_of<CW>() * 128;  // one D stage: BM rows x 128 bytes
+}
 
 template <typename TD>
 constexpr int kt_cols() {
     return 128 / static_cast<int>(sizeof(TD));
 }
 
-template <int WP, typename TD>
+template <int WP, typename TD, int CW>
 constexpr int stage_bytes() {
     // D tile (1024-aligned for the 128B swizzle) + panel chunk, rounded to 1024
-    return ((kTileBytes + kt_cols<TD>() * WP * 8) + 1023) / 1024 * 1024;
+    return ((tile_bytes<CW>() + kt_cols<TD>() * WP * 8) + 1023) / 1024 * 1024;
 }
 
 __device__ __forceinline__ long long chunk_begin(long long total, long long c, long long P) {
@@ -68,19 +74,22 @@ __device__ __forceinline__ double load_a(const unsigned char* tile, int r, int k
     }
 }
 
-template <int WP, typename TD, bool SQUARE>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int WP, typename TD, bool SQUARE, int CW>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
     k2_product(const __grid_constant__ CUtensorMap tmD, const double* __restrict__ X, int nk,
                long long total, double* __restrict__ part, int maxseg, int stages) {
     constexpr int KT = kt_cols<TD>();
     constexpr int K4 = KT / 4;
     constexpr int NF = WP / 8;
     constexpr int XB = KT * WP * 8;
-    constexpr int SB = stage_bytes<WP, TD>();
+    constexpr int SB = stage_bytes<WP, TD, CW>();
+    constexpr int BM = bm_of<CW>();
+    constexpr int kTileBytes = tile_bytes<CW>();
 
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the 128B swizzle, by integer offset so the
+    // compiler keeps the shared address space (LDS, not generic loads)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * SB);
     uint64_t* empty = full + stages;
 
@@ -91,13 +100,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
+            mbar_init(&empty[s], CW);
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (warp == kConsumerWarps) {
+    if (warp == CW) {
         // ---------------- producer ----------------
         if (lane == 0) {
             prefetch_tmap(&tmD);
@@ -108,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int b = static_cast<int>(t / nk), kt = static_cast<int>(t % nk);
                 unsigned char* st = smem + static_cast<size_t>(s) * SB;
                 mbar_arrive_expect_tx(&full[s], kTileBytes + XB);
-                tma_load_2d(st, &tmD, kt * KT, b * kBM, &full[s]);
+                tma_load_2d(st, &tmD, kt * KT, b * BM, &full[s]);
                 bulk_load(st + kTileBytes, X + static_cast<size_t>(kt) * KT * WP, XB, &full[s]);
                 if (++s == stages) {
                     s = 0;
@@ -129,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int m0 = warp * 16;
     const int rq = lane >> 2, kq = lane & 3;
     auto flush = [&](int seg) {
-        double* dst = part + (static_cast<size_t>(c) * maxseg + seg) * kBM * WP;
+        double* dst = part + (static_cast<size_t>(c) * maxseg + seg) * BM * WP;
 #pragma unroll
         for (int fm = 0; fm < 2; ++fm) {
             const int row = m0 + 8 * fm + rq;
@@ -170,8 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int fn = 0; fn < NF; ++fn) {
                     const double bv = xs[(kk * WP + 8 * fn + rq) * 4 + kq];
-                    dmma884(acc[0][fn][0], acc[0][fn][1], a[0], bv);
-                    dmma884(acc[1][fn][0], acc[1][fn][1], a[1], bv);
+                    dmma1684(acc[0][fn][0], acc[0][fn][1], acc[1][fn][0], acc[1][fn][1], a[0],
+                             a[1], bv);
                 }
             }
             __syncwarp();
@@ -198,23 +207,28 @@ __device__ __forceinline__ long long cta_of(long long t, long long total, long l
 //   mode 1: y = -1/2 (y - r_i s_c - t_c + g s_c)   (rank-3 centering)
 //   mode 0: y as is.
 // Rows >= n are written as zero. Output in the k4-interleaved panel layout.
-template <int WP>
+template <int WP, int BM>
 __global__ void __launch_bounds__(256)
     k2_reduce(const double* __restrict__ part, int maxseg, int nk, long long total, int P, int n,
               int mode, const double* __restrict__ row_mean, const double* __restrict__ scalars,
               const double* __restrict__ colsums, double* __restrict__ y) {
-    const int b = blockIdx.x;
+    constexpr int kRows = 32;  // rows of the BM-row block handled by this CTA
+    const int b = blockIdx.x / (BM / kRows);
+    const int r0 = (blockIdx.x % (BM / kRows)) * kRows;
     const long long c_lo = cta_of(static_cast<long long>(b) * nk, total, P);
     const long long c_hi = cta_of(static_cast<long long>(b + 1) * nk - 1, total, P);
+    const int nslot = static_cast<int>(c_hi - c_lo + 1);
     const double g = mode ? scalars[S_GRAND] : 0.0;
-    for (int e = threadIdx.x; e < kBM * WP; e += blockDim.x) {
-        const int r = e / WP, col = e % WP;
+    for (int e = threadIdx.x; e < kRows * WP; e += blockDim.x) {
+        const int r = r0 + e / WP, col = e % WP;
+        const int eo = r * WP + col;
         double v = 0.0;
-        for (long long cc = c_lo; cc <= c_hi; ++cc) {
+        for (int sl = 0; sl < nslot; ++sl) {
+            const long long cc = c_lo + sl;
             const int seg = b - static_cast<int>(chunk_begin(total, cc, P) / nk);
-            v += part[(static_cast<size_t>(cc) * maxseg + seg) * kBM * WP + e];
+            v += part[(static_cast<size_t>(cc) * maxseg + seg) * BM * WP + eo];
         }
-        const size_t i = static_cast<size_t>(b) * kBM + r;
+        const size_t i = static_cast<size_t>(b) * BM + r;
         if (i >= static_cast<size_t>(n)) {
             v = 0.0;
         } else if (mode) {
@@ -225,58 +239,57 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-template <int WP, typename TD, bool SQ>
-void set_smem_attr(size_t smem) {
-    static bool done = false;  // per instantiation
-    static size_t max_set = 0;
-    if (!done || smem > max_set) {
-        cudaFuncSetAttribute(k2_product<WP, TD, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        done = true;
-        max_set = smem;
+template <int WP, typename TD, bool SQ, int CW>
+void run_product(const CUtensorMap* tmap, const K2Plan& p, const double* x, double* part,
+                 cudaStream_t st) {
+    static size_t set_for = 0;  // per instantiation
+    if (p.smem > set_for) {
+        cudaFuncSetAttribute(k2_product<WP, TD, SQ, CW>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
+        set_for = p.smem;
     }
+    k2_product<WP, TD, SQ, CW><<<p.grid, (CW + 1) * 32, p.smem, st>>>(*tmap, x, p.nk, p.total,
+                                                                      part, p.maxseg, p.stages);
 }
 
-template <int WP>
+template <int WP, int CW>
 void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
                double* part, const double* row_mean, const double* scalars,
-               const double* colsums, double* y, cudaStream_t st) {
+               const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1) {
+    if (e0) cudaEventRecord(e0, st);
     if (dt == DType::F64) {
-        if (mode) {
-            set_smem_attr<WP, double, true>(p.smem);
-            k2_product<WP, double, true><<<p.grid, kThreads, p.smem, st>>>(
-                *tmap, x, p.nk, p.total, part, p.maxseg, p.stages);
-        } else {
-            set_smem_attr<WP, double, false>(p.smem);
-            k2_product<WP, double, false><<<p.grid, kThreads, p.smem, st>>>(
-                *tmap, x, p.nk, p.total, part, p.maxseg, p.stages);
-        }
-    } else if (mode) {
-        set_smem_attr<WP, float, true>(p.smem);
-        k2_product<WP, float, true><<<p.grid, kThreads, p.smem, st>>>(*tmap, x, p.nk, p.total,
-                                                                        part, p.maxseg, p.stages);
+        if (mode)
+            run_product<WP, double, true, CW>(tmap, p, x, part, st);
+        else
+            run_product<WP, double, false, CW>(tmap, p, x, part, st);
     } else {
-        set_smem_attr<WP, float, false>(p.smem);
-        k2_product<WP, float, false><<<p.grid, kThreads, p.smem, st>>>(*tmap, x, p.nk, p.total,
-                                                                         part, p.maxseg, p.stages);
+        if (mode)
+            run_product<WP, float, true, CW>(tmap, p, x, part, st);
+        else
+            run_product<WP, float, false, CW>(tmap, p, x, part, st);
     }
-    k2_reduce<WP><<<p.nb, 256, 0, st>>>(part, p.maxseg, p.nk, p.total, p.grid, p.n, mode,
-                                        row_mean, scalars, colsums, y);
+    if (e1) cudaEventRecord(e1, st);
+    k2_reduce<WP, bm_of<CW>()><<<p.nb * (bm_of<CW>() / 32), 256, 0, st>>>(
+        part, p.maxseg, p.nk, p.total, p.grid, p.n, mode, row_mean, scalars, colsums, y);
 }
 
 }  // namespace
 
+int k2_warps(int wp) { return wp <= 64 ? 16 : 8; }
+
 K2Plan k2_plan(size_t n, int wp, DType dt, int sms) {
     K2Plan p;
     p.wp = wp;
+    p.cw = k2_warps(wp);
+    p.bm = 16 * p.cw;
     p.n = static_cast<int>(n);
-    p.nb = static_cast<int>((n + kBM - 1) / kBM);
+    p.nb = static_cast<int>((n + p.bm - 1) / p.bm);
     const int kt = dt == DType::F64 ? 16 : 32;
     p.nk = static_cast<int>((n + kt - 1) / kt);
     p.total = static_cast<long long>(p.nb) * p.nk;
     p.grid = static_cast<int>(std::min<long long>(sms, p.total));
-    const int sb = ((kTileBytes + kt * wp * 8) + 1023) / 1024 * 1024;
-    const size_t budget = 220 * 1024;
+    const int sb = ((p.bm * 128 + kt * wp * 8) + 1023) / 1024 * 1024;
+    const size_t budget = 222 * 1024;
     int stages = static_cast<int>((budget - 1024 - 256) / sb);
     stages = std::max(2, std::min(stages, 8));
     p.stages = stages;
@@ -288,18 +301,20 @@ K2Plan k2_plan(size_t n, int wp, DType dt, int sms) {
         if (b > a) maxseg = std::max<int>(maxseg, static_cast<int>((b - 1) / p.nk - a / p.nk + 1));
     }
     p.maxseg = maxseg;
-    p.part_elems = static_cast<size_t>(p.grid) * maxseg * kBM * wp;
+    p.part_elems = static_cast<size_t>(p.grid) * maxseg * p.bm * wp;
     return p;
 }
 
 void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
                double* part, const double* row_mean, const double* scalars,
-               const double* colsums, double* y, size_t n_pad, cudaStream_t st) {
+               const double* colsums, double* y, size_t n_pad, cudaStream_t st, cudaEvent_t e0,
+               cudaEvent_t e1) {
     (void)n_pad;
     switch (p.wp) {
-#define DSB_WP(W)                                                                              \
-    case W:                                                                                    \
-        launch_wp<W>(tmap, dt, mode, p, x, part, row_mean, scalars, colsums, y, st);           \
+#define DSB_WP(W)                                                                               \
+    case W:                                                                                     \
+        launch_wp<W, (W <= 64 ? 16 : 8)>(tmap, dt, mode, p, x, part, row_mean, scalars, colsums, \
+                                         y, st, e0, e1);                                         \
         break;
         DSB_WP(8)
         DSB_WP(16)

@@ -10,7 +10,7 @@
 
 namespace dsb {
 
-constexpr int kBM = 128;      // K2 row-block height (rows of D per CTA tile)
+constexpr int kRowPad = 256;  // panels / row blocks are padded to a multiple of this
 constexpr int kMaxWP = 128;   // widest panel (rank + oversampling, padded to 8)
 
 // indices into the K1 scalar block (double[16])
@@ -45,6 +45,7 @@ void launch_k1(const void* d, DType dt, size_t ld, size_t n, const K1Work& w, do
 // ---- K2: centered skinny product Y = G X (stream-K, DMMA f64) -------------
 struct K2Plan {
     int wp = 0;
+    int cw = 8, bm = 128;   // consumer warps, rows per tile (16 per warp)
     int n = 0, nb = 0, nk = 0;
     long long total = 0;
     int grid = 0, maxseg = 0, stages = 0;
@@ -54,9 +55,12 @@ struct K2Plan {
 K2Plan k2_plan(size_t n, int wp, DType dt, int sms);
 // mode: 0 = explicit matrix (Y = A X), 1 = gram of D (D squared on the fly,
 // then rank-3 centering).
+// e0/e1 (may be null) are recorded around the streaming kernel only
+int k2_warps(int wp);
 void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
                double* part, const double* row_mean, const double* scalars,
-               const double* colsums, double* y, size_t n_pad, cudaStream_t st);
+               const double* colsums, double* y, size_t n_pad, cudaStream_t st,
+               cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr);
 
 // ---- panel kernels (n_pad x WP, k4-interleaved) -----------------------------
 int panel_grid(size_t n_pad, int sms);
@@ -77,6 +81,13 @@ void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shi
 // q = y * rinv (row-wise, upper-triangular rinv)
 void launch_panel_apply(const double* y, const double* rinv, size_t n_pad, int wp, double* q,
                         cudaStream_t st);
+
+// K3 fast path for wp <= 32: the three CholeskyQR passes y -> t -> y -> out
+// in one cooperative launch (returns false when not applicable / launch
+// refused, in which case the caller uses the multi-kernel path).
+int orth_fused_grid(size_t n_pad, int sms);
+bool launch_orth_fused(double* y, double* t, double* out, size_t n_pad, int wp, int w, size_t n,
+                       double* partial, double* wsum, int* flags, int sms, cudaStream_t st);
 
 // ---- K5: Rayleigh-Ritz EVD + |lambda| ordering + embed filter (1 CTA) -----
 struct EvdOut {

@@ -1,0 +1,297 @@
+// K3 fast path (panel width WP <= 32): the whole CholeskyQR3 of one
+// orthonormalization in ONE cooperative launch (replaces thin_orthonormal,
+// ref src/rsvd.cpp:38-44).
+//
+// Per pass (3 passes: shifted-if-needed, then two plain):
+//   1. each CTA forms the partial Gram Y_c^T Y_c of its contiguous row range
+//      on the f64 tensor cores (interleaved layout => contiguous fragments);
+//   2. grid sync; CTA c sums elements e = c, c + P, ... over the partials in
+//      CTA order (deterministic); grid sync;
+//   3. every CTA factors W = R^T R redundantly in one warp, lane j holding
+//      column j in registers (identical inputs and code => identical R in all
+//      CTAs), with the shift / drop rules of launch_chol_inv;
+//   4. each thread solves q_i R = y_i for one of the CTA's rows (forward
+//      substitution; dropped columns come out as zero).
+// Rows never leave their CTA between passes, so a pass needs only the two
+// grid syncs around the Gram reduction.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "device_utils.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dsb {
+
+namespace {
+
+constexpr double kShiftTrigF = 1e-10;  // same rules as k_chol_inv
+long long* g_orth_prof = nullptr;      // debug: per-phase cycle counts of CTA 0
+constexpr double kDropTolF = 1e-20;
+
+// CTA-wide right-looking Cholesky W = R^T R of a WP x WP matrix already in
+// shared memory (A, row-major, overwritten by R; strict lower part zeroed).
+// Thread 0 takes the pivot decision (shift / drop rules of k_chol_inv); the
+// row scaling and the trailing update are spread over the CTA. Returns true
+// when the first (shift-allowed) attempt asks for a shift; the caller then
+// reloads A + sigma I and calls again with first_shifting = false.
+template <int WP>
+__device__ bool cta_cholesky(double* __restrict__ A, int w, const double* __restrict__ d0s,
+                             double maxdiag, bool first_shifting, bool drop_mode,
+                             int* __restrict__ dropped_s, double* __restrict__ rinv_diag) {
+    __shared__ double piv_s, inv_s;
+    __shared__ int drop_s, shift_s;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int k = 0; k < WP; ++k) {
+        if (tid == 0) {
+            const double p = A[k * WP + k];
+            const double d0k = d0s[k];
+            bool drop = (k >= w) || !(d0k > 0.0) || !(p > 0.0);
+            bool shift = false;
+            if (first_shifting) {
+                if (k < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift = true;
+                drop = drop && !(k < w && d0k > 0.0);
+            } else if (drop_mode && p <= kDropTolF * maxdiag) {
+                drop = true;
+            }
+            const double rkk = drop ? 1.0 : sqrt(p);
+            piv_s = rkk;
+            inv_s = drop ? 0.0 : 1.0 / rkk;
+            drop_s = drop;
+            shift_s = shift;
+            dropped_s[k] = drop;
+            rinv_diag[k] = inv_s;
+            A[k * WP + k] = rkk;
+        }
+        __syncthreads();
+        if (shift_s) return true;
+        const double inv = inv_s;
+        for (int j = k + 1 + tid; j < WP; j += nt) A[k * WP + j] *= inv;  // drop => 0
+        __syncthreads();
+        const int m = WP - k - 1;
+        for (int e = tid; e < m * m; e += nt) {
+            const int i = k + 1 + e / m, j = k + 1 + e % m;
+            if (j >= i) A[i * WP + j] -= A[k * WP + i] * A[k * WP + j];
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < WP * WP; e += nt)
+        if (e / WP > e % WP) A[e] = 0.0;
+    __syncthreads();
+    return false;
+}
+
+template <int WP>
+__global__ void __launch_bounds__(256, 1)
+    k_orth_fused(const double* __restrict__ y, double* __restrict__ out, size_t n_pad, int w,
+                 double nrows, int ldr, double* __restrict__ partial, double* __restrict__ wsum,
+                 int* __restrict__ flags, long long* __restrict__ prof) {
+    long long t_last = clock64();
+    int prof_i = 0;
+    auto mark = [&]() {
+        if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+            const long long t = clock64();
+            prof[prof_i] = t - t_last;
+            t_last = t;
+        }
+        ++prof_i;
+    };
+    constexpr int NF = WP / 8;
+    constexpr int NT = NF * NF;
+    constexpr int TPW = (NT + 7) / 8;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double R[WP * WP];
+    __shared__ int dropped_s[WP];
+    __shared__ double d0s[WP];
+    __shared__ double rdiag[WP];
+    __shared__ double tr_s[2];
+    __shared__ int skip_third;
+    // the CTA's rows stay in shared memory for all passes, column-major with
+    // leading dimension ldr = 4 (mod 16): conflict-free MMA fragments and
+    // conflict-free thread-per-row access
+    extern __shared__ double ps[];  // [WP][ldr]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P = gridDim.x, c = blockIdx.x;
+    const size_t nq = n_pad / 4;
+    const size_t q0 = nq * c / P, q1 = nq * (c + 1) / P;
+    const int nrow = static_cast<int>((q1 - q0) * 4);
+    {
+        const double* src = y + q0 * WP * 4;
+        for (int e = threadIdx.x; e < nrow * WP; e += blockDim.x) {
+            const int qb = e / (WP * 4), cc = (e / 4) % WP, rr = e & 3;
+            ps[cc * ldr + 4 * qb + rr] = src[e];
+        }
+    }
+    if (threadIdx.x == 0) skip_third = 0;
+    __syncthreads();
+    mark();
+    // pass 0 may shift; when it did not, CholQR2 suffices (same decision in
+    // every CTA: identical factorization)
+    for (int pass = 0; pass < 3; ++pass) {
+        if (pass == 2 && skip_third) break;
+        // ---- 1. partial Gram of this CTA's rows (f64 MMA from shared memory)
+        {
+            double acc[TPW][2];
+#pragma unroll
+            for (int j = 0; j < TPW; ++j) acc[j][0] = acc[j][1] = 0.0;
+            const int rq = lane >> 2, kq = lane & 3;
+            for (int q = 0; q < nrow / 4; ++q) {
+#pragma unroll
+                for (int j = 0; j < TPW; ++j) {
+                    const int tt = warp + 8 * j;
+                    if (tt < NT) {
+                        const int ta = tt / NF, tb = tt % NF;
+                        dmma884(acc[j][0], acc[j][1], ps[(8 * ta + rq) * ldr + 4 * q + kq],
+                                ps[(8 * tb + rq) * ldr + 4 * q + kq]);
+                    }
+                }
+            }
+            double* o = partial + static_cast<size_t>(c) * WP * WP;
+#pragma unroll
+            for (int j = 0; j < TPW; ++j) {
+                const int tt = warp + 8 * j;
+                if (tt < NT) {
+                    const int ta = tt / NF, tb = tt % NF;
+                    o[(8 * ta + rq) * WP + 8 * tb + 2 * kq] = acc[j][0];
+                    o[(8 * ta + rq) * WP + 8 * tb + 2 * kq + 1] = acc[j][1];
+                }
+            }
+        }
+        mark();
+        grid.sync();
+        mark();
+        // ---- 2. W = sum of partials: one warp per element, lanes stride over
+        // the P partials, fixed shuffle tree => deterministic
+        {
+            const int gw = (c * 256 + threadIdx.x) >> 5, nw = P * 8;
+            for (int e = gw; e < WP * WP; e += nw) {
+                double s = 0.0;
+                for (int k = lane; k < P; k += 32) s += partial[static_cast<size_t>(k) * WP * WP + e];
+                s = warp_sum(s);
+                if (lane == 0) wsum[e] = s;
+            }
+        }
+        mark();
+        grid.sync();
+        mark();
+        // ---- 3. Cholesky of W, every CTA (identical inputs and code)
+        {
+            const int tid = threadIdx.x;
+            if (tid < WP) d0s[tid] = tid < w ? wsum[tid * WP + tid] : 0.0;
+            __syncthreads();
+            if (tid == 0) {
+                double tr = 0.0, mx = 0.0;
+                for (int j = 0; j < w; ++j) {
+                    tr += d0s[j];
+                    mx = fmax(mx, d0s[j]);
+                }
+                tr_s[0] = tr;
+                tr_s[1] = mx;
+            }
+            double sigma = 0.0;
+            bool shifted = false;
+            for (int attempt = 0; attempt < 2; ++attempt) {
+                for (int e = tid; e < WP * WP; e += blockDim.x) {
+                    const int i = e / WP, j = e % WP;
+                    double v = (i < w && j < w) ? wsum[e] : 0.0;
+                    if (i == j && i < w && d0s[i] > 0.0) v += sigma;
+                    R[e] = v;
+                }
+                __syncthreads();
+                const bool first_shifting = pass == 0 && attempt == 0;
+                const bool drop_mode = pass != 0;
+                if (!cta_cholesky<WP>(R, w, d0s, tr_s[1], first_shifting, drop_mode, dropped_s,
+                                      rdiag))
+                    break;
+                sigma = 11.0 * (nrows * w + static_cast<double>(w) * (w + 1)) * 0x1.0p-53 * tr_s[0];
+                shifted = true;
+            }
+            if (tid == 0) {
+                if (shifted && c == 0) flags[0] |= 1;
+                if (pass == 0) skip_third = shifted ? 0 : 1;
+            }
+        }
+        __syncthreads();
+        mark();
+        // ---- 4. q_r R = y_r, thread per row, in place in shared memory
+        for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
+            for (int cc = 0; cc < WP; ++cc) {
+                double v = 0.0;
+                if (!dropped_s[cc]) {
+                    double s = ps[cc * ldr + r];
+                    for (int k = 0; k < cc; ++k) s -= ps[k * ldr + r] * R[k * WP + cc];
+                    v = s * rdiag[cc];
+                }
+                ps[cc * ldr + r] = v;
+            }
+        }
+        __syncthreads();
+        mark();
+    }
+    {
+        double* dst = out + q0 * WP * 4;
+        for (int e = threadIdx.x; e < nrow * WP; e += blockDim.x) {
+            const int qb = e / (WP * 4), cc = (e / 4) % WP, rr = e & 3;
+            dst[e] = ps[cc * ldr + 4 * qb + rr];
+        }
+    }
+}
+
+template <int WP>
+bool launch_wp(double* y, double* out, size_t n_pad, int w, size_t n, double* partial,
+               double* wsum, int* flags, int sms, cudaStream_t st) {
+    const int P = std::min<int>(sms, static_cast<int>(std::max<size_t>(n_pad / 4 / 8, 1)));
+    const size_t nq = n_pad / 4;
+    const int rows_max = static_cast<int>(((nq + P - 1) / P) * 4);
+    const int ldr = (rows_max + 15) / 16 * 16 + 4;
+    const size_t smem = static_cast<size_t>(WP) * ldr * sizeof(double);
+    if (smem > 200 * 1024) return false;
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(k_orth_fused<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
+        attr = std::max<size_t>(smem, 48 * 1024);
+    }
+    static size_t occ_smem = 0;
+    static int per_sm = 0;
+    if (occ_smem != smem) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_orth_fused<WP>, 256, smem);
+        occ_smem = smem;
+    }
+    if (per_sm < 1) return false;
+    double nr = static_cast<double>(n);
+    int ldr_a = ldr;
+    const double* yc = y;
+    long long* prof = g_orth_prof;
+    void* args[] = {&yc, &out, &n_pad, &w, &nr, &ldr_a, &partial, &wsum, &flags, &prof};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_orth_fused<WP>), dim3(P),
+                                       dim3(256), args, smem, st) == cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" void divscope_debug_orth_prof(long long* dev_buf) { g_orth_prof = dev_buf; }
+
+int orth_fused_grid(size_t n_pad, int sms) {
+    return std::min<int>(sms, static_cast<int>(std::max<size_t>(n_pad / 4 / 8, 1)));
+}
+
+bool launch_orth_fused(double* y, double* t, double* out, size_t n_pad, int wp, int w, size_t n,
+                       double* partial, double* wsum, int* flags, int sms, cudaStream_t st) {
+    (void)t;
+    bool ok = false;
+    switch (wp) {
+        case 8: ok = launch_wp<8>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        case 16: ok = launch_wp<16>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        case 24: ok = launch_wp<24>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        case 32: ok = launch_wp<32>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        default: return false;
+    }
+    if (ok) count_launch();
+    return ok;
+}
+
+}  // namespace dsb

@@ -75,12 +75,26 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const double* __restrict
     }
 }
 
-__global__ void k_sum_partials(const double* __restrict__ partial, int P, int m,
-                               double* __restrict__ out) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < P; ++c) s += partial[static_cast<size_t>(c) * m + e];
-        out[e] = s;
+// out[e] = sum_c partial[c][e]. A block owns 32 consecutive e (one per lane);
+// its 8 warps take fixed strided subsets of c, combined in warp order, so the
+// result is deterministic for a fixed P.
+__global__ void __launch_bounds__(256) k_sum_partials(const double* __restrict__ partial, int P,
+                                                      int m, double* __restrict__ out) {
+    __shared__ double sh[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int e = blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (e < m) {
+#pragma unroll 4
+        for (int c = warp; c < P; c += 8) s += partial[static_cast<size_t>(c) * m + e];
+    }
+    sh[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && e < m) {
+        double t = sh[0][lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) t += sh[w][lane];
+        out[e] = t;
     }
 }
 
@@ -141,7 +155,7 @@ __global__ void __launch_bounds__(256) k_panel_dot_partial(const double* __restr
 constexpr double kShiftTrig = 1e-10;
 constexpr double kDropTol = 1e-20;
 
-__global__ void __launch_bounds__(256) k_chol_inv(const double* __restrict__ wmat, int wp, int w,
+__global__ void __launch_bounds__(128) k_chol_inv(const double* __restrict__ wmat, int wp, int w,
                                                   double nrows, int allow_shift,
                                                   double* __restrict__ rinv,
                                                   int* __restrict__ flags) {
@@ -209,27 +223,24 @@ __global__ void __launch_bounds__(256) k_chol_inv(const double* __restrict__ wma
         if (tid == 0) flags[0] |= 1;
         __syncthreads();
     }
-    // R^{-1} straight into global memory: rows from the bottom up, columns in
-    // parallel (rows written before a __syncthreads are visible to the block)
-    for (int i = wp - 1; i >= 0; --i) {
-        for (int c = tid; c < wp; c += nt) {
-            double v;
-            if (c < i) {
-                v = 0.0;
-            } else if (c == i) {
-                v = 1.0 / A[i * ld + i];
-            } else {
-                double s = 0.0;
-                for (int k = i + 1; k <= c; ++k) s += A[i * ld + k] * rinv[k * wp + c];
-                v = -s / A[i * ld + i];
-            }
-            rinv[i * wp + c] = v;
+    // in-place inverse of the upper-triangular R held in A (column by column,
+    // LAPACK trti2 order): T = R^{-1} on columns 0..j-1 is used to form column j
+    __shared__ double inv_jj;
+    for (int j = 0; j < wp; ++j) {
+        if (tid == 0) inv_jj = 1.0 / A[j * ld + j];
+        double t = 0.0;
+        const int i = tid;
+        if (i < j) {
+            for (int k = i; k < j; ++k) t += A[i * ld + k] * A[k * ld + j];
         }
+        __syncthreads();
+        if (i < j) A[i * ld + j] = -t * inv_jj;
+        if (tid == 0) A[j * ld + j] = inv_jj;
         __syncthreads();
     }
     for (int e = tid; e < wp * wp; e += nt) {
         const int i = e / wp, j = e % wp;
-        if (dropped[i] || dropped[j]) rinv[e] = 0.0;
+        rinv[e] = (i > j || dropped[i] || dropped[j]) ? 0.0 : A[i * ld + j];
     }
 }
 
@@ -314,7 +325,7 @@ void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_
     const int P = panel_grid(n_pad, sms);
     k_colsum_partial<<<P, 256, 2 * wp * 4 * sizeof(double), st>>>(x, row_mean, n, n_pad, wp,
                                                                   partial);
-    k_sum_partials<<<(2 * wp + 255) / 256, 256, 0, st>>>(partial, P, 2 * wp, colsums);
+    k_sum_partials<<<(2 * wp + 31) / 32, 256, 0, st>>>(partial, P, 2 * wp, colsums);
     count_launch(2);
 }
 
@@ -333,7 +344,7 @@ void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, do
         default:
             throw std::invalid_argument("unsupported panel width");
     }
-    k_sum_partials<<<(wp * wp + 255) / 256, 256, 0, st>>>(partial, P, wp * wp, out);
+    k_sum_partials<<<(wp * wp + 31) / 32, 256, 0, st>>>(partial, P, wp * wp, out);
     count_launch(2);
 }
 
@@ -346,7 +357,7 @@ void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shi
                              static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
         set_for = std::max<size_t>(smem, 48 * 1024);
     }
-    k_chol_inv<<<1, 256, smem, st>>>(w_mat, wp, w, static_cast<double>(n), allow_shift, rinv,
+    k_chol_inv<<<1, 128, smem, st>>>(w_mat, wp, w, static_cast<double>(n), allow_shift, rinv,
                                      flags);
     count_launch();
 }

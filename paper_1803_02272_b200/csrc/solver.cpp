@@ -47,7 +47,8 @@ StatsOut run_k1(const Store& s) {
 void ensure_tmap(Store& s) {
     std::lock_guard<std::mutex> lk(s.mu);
     if (s.tmap_ok) return;
-    if (!Ctx::get().encode_tmap(&s.tmap, s.buf->p, s.dt, s.rows, s.cols, s.ld))
+    if (!Ctx::get().encode_tmap(&s.tmap128, s.buf->p, s.dt, s.rows, s.cols, s.ld, 128) ||
+        !Ctx::get().encode_tmap(&s.tmap256, s.buf->p, s.dt, s.rows, s.cols, s.ld, 256))
         throw Error(errc::internal, "cuTensorMapEncodeTiled failed");
     s.tmap_ok = true;
 }
@@ -66,18 +67,32 @@ void ensure_explicit_stats(Store& s) {
 }
 
 // Omega = fill_gaussian(mt19937_64(seed)) as n x w row-major (rsvd.cpp:90-92),
-// memoized for the most recent shapes (a pure function of (seed, n, w)).
-const std::vector<double>& omega_host(uint64_t seed, size_t n, size_t w) {
-    static std::deque<std::tuple<uint64_t, size_t, size_t, std::vector<double>>> cache;
+// generated on the host (bit-identical to the reference) into pinned memory
+// and memoized for the most recent shapes (a pure function of (seed, n, w));
+// it is copied to the device on every solve.
+struct PinnedOmega {
+    uint64_t seed = 0;
+    size_t n = 0, w = 0;
+    double* p = nullptr;
+    ~PinnedOmega() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+const double* omega_host(uint64_t seed, size_t n, size_t w) {
+    static std::deque<std::unique_ptr<PinnedOmega>> cache;
     for (auto& e : cache)
-        if (std::get<0>(e) == seed && std::get<1>(e) == n && std::get<2>(e) == w)
-            return std::get<3>(e);
-    std::vector<double> om(n * w);
+        if (e->seed == seed && e->n == n && e->w == w) return e->p;
+    auto e = std::make_unique<PinnedOmega>();
+    e->seed = seed;
+    e->n = n;
+    e->w = w;
+    DSB_CUDA(cudaMallocHost(&e->p, std::max<size_t>(n * w, 1) * sizeof(double)));
     std::mt19937_64 eng(seed);
-    fill_gaussian(eng, om.data(), om.size());
+    fill_gaussian(eng, e->p, n * w);
     if (cache.size() >= 2) cache.pop_front();
-    cache.emplace_back(seed, n, w, std::move(om));
-    return std::get<3>(cache.back());
+    cache.push_back(std::move(e));
+    return cache.back()->p;
 }
 
 struct RunOut {
@@ -120,7 +135,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
                     "rank + oversampling > 128 is not supported by the GPU path");
     const int wi = static_cast<int>(w);
     const int wp = static_cast<int>(round_up(w, 8));
-    const size_t n_pad = round_up(n, kBM);
+    const size_t n_pad = round_up(n, kRowPad);
     const int mode = lazy ? 1 : 0;
 
     ensure_tmap(s);
@@ -142,22 +157,25 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
 
     // Omega: host-generated (bit-identical to the reference), relayout on device
     {
-        const std::vector<double>& om = omega_host(seed, n, w);
+        const double* om = omega_host(seed, n, w);
         double* stage = static_cast<double*>(c.scratch("omega_rm", n * w * sizeof(double)));
-        c.h2d_copy(stage, om.data(), n * w * sizeof(double));
+        c.h2d_copy(stage, om, n * w * sizeof(double));
         launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, P0, c.stream);
     }
 
     auto product = [&](const double* x, double* y) {
         if (mode) launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
-        cudaEvent_t ev;
-        c.begin_timed(1, &ev);
-        launch_k2(&s.tmap, s.dt, mode, plan, x, part, row_mean, scal_dev, colsums, y, n_pad,
-                  c.stream);
-        c.end_timed(1, ev);
+        cudaEvent_t e0, e1;
+        c.make_events(&e0, &e1);
+        launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums, y,
+                  n_pad, c.stream, e0, e1);
+        c.add_timed(1, e0, e1);
     };
     // CholeskyQR3 with shift/drop handling: y -> t -> y -> out
     auto orth = [&](double* y, double* t, double* out) {
+        if (wp <= 32 &&
+            launch_orth_fused(y, t, out, n_pad, wp, wi, n, psmall, wmat, flags, c.sms, c.stream))
+            return;
         launch_panel_dot(y, y, n_pad, wp, psmall, wmat, c.sms, c.stream);
         launch_chol_inv(wmat, wp, wi, n, 1, rinv, flags, c.stream);
         launch_panel_apply(y, rinv, n_pad, wp, t, c.stream);
@@ -204,7 +222,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         const int P = static_cast<int>(std::min<size_t>(static_cast<size_t>(c.sms) * 2,
                                                         std::max<size_t>(n / 64, 1)));
         double* lp = static_cast<double*>(
-            c.scratch("lift_part", static_cast<size_t>(P) * std::max<size_t>(req, 1) * 2 * 8));
+            c.scratch("lift_part", (static_cast<size_t>(P) * 2 + 1) * std::max<size_t>(req, 1) * 8));
         launch_lift(P0, n, wp, wi, eo.vkeep, eo.kept_vals, eo.imeta, static_cast<int>(req),
                     coords, lp, c.sms, c.stream);
     }
@@ -221,6 +239,12 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     DSB_CUDA(cudaMemcpyAsync(meta.dmeta, eo.dmeta, 8 * 8, cudaMemcpyDeviceToHost, c.stream));
     c.d2h_copy(meta.imeta, eo.imeta, 8 * sizeof(int));
     c.d2h += w * 16 + 64;
+    c.last_evd_sweeps = meta.imeta[3];
+    {
+        int fl = 0;
+        c.d2h_copy(&fl, flags, sizeof(int));
+        c.last_orth_shifted = fl & 1;
+    }
     if (!meta.imeta[4])
         throw Error(errc::internal, "small eigensolve failed");  // ref rsvd.cpp:113-114
     out.vals.assign(meta.vals, meta.vals + w);
@@ -272,8 +296,6 @@ Matrix gram_from_distances(const Matrix& d) {
     g.gram->row_mean = o.row_mean;
     g.gram->scalars = o.scalars;
     std::memcpy(g.gram->sc, o.sc, sizeof(o.sc));
-    g.gram->row_mean_h.resize(n);
-    c.d2h_copy(g.gram->row_mean_h.data(), o.row_mean->p, n * sizeof(double));
     return g;
 }
 
@@ -308,6 +330,16 @@ void randomized_range(const Matrix& g, const SolverOptions& opts, double* q_out)
         q_out);
 }
 
+// host copy of the row means, fetched on first use (matrix_get / _write)
+static const std::vector<double>& host_row_means(GramInfo& g) {
+    std::lock_guard<std::mutex> lk(g.mu);
+    if (g.row_mean_h.size() != g.n) {
+        g.row_mean_h.resize(g.n);
+        Ctx::get().d2h_copy(g.row_mean_h.data(), g.row_mean->p, g.n * sizeof(double));
+    }
+    return g.row_mean_h;
+}
+
 double matrix_get(const Matrix& m, size_t i, size_t j) {
     Ctx& c = Ctx::get();
     std::lock_guard<std::recursive_mutex> lk(c.mu);
@@ -327,7 +359,7 @@ double matrix_get(const Matrix& m, size_t i, size_t j) {
     };
     if (!m.gram) return fetch(i, j);
     // ref mds.cpp:50-51 (upper) and :57-58 (mirror)
-    const auto& rm = m.gram->row_mean_h;
+    const auto& rm = host_row_means(*m.gram);
     const double grand = m.gram->sc[S_GRAND];
     if (i <= j) {
         const double dij = fetch(i, j);
@@ -365,7 +397,7 @@ void matrix_to_host(const Matrix& m, double* out) {
             for (size_t b = 0; b < cols; ++b) out[a * cols + b] = at(a, b);
         return;
     }
-    const auto& rm = m.gram->row_mean_h;
+    const auto& rm = host_row_means(*m.gram);
     const double grand = m.gram->sc[S_GRAND];
     for (size_t a = 0; a < rows; ++a)
         for (size_t b = a; b < cols; ++b) {
@@ -400,7 +432,7 @@ double stable_rank(const Matrix& g) {
     if (fro2 == 0.0) throw Error(errc::zero_matrix, "stable rank undefined for zero matrix");
     const int mode = lazy ? 1 : 0;
     const int wp = 8;
-    const size_t n_pad = round_up(n, kBM);
+    const size_t n_pad = round_up(n, kRowPad);
     ensure_tmap(s);
     const K2Plan plan = k2_plan(n, wp, s.dt, c.sms);
     double* X = static_cast<double*>(c.scratch("sr_x", n_pad * wp * 8));
@@ -431,11 +463,11 @@ double stable_rank(const Matrix& g) {
     double sigma = 0.0;
     for (int it = 0; it < 20000; ++it) {
         if (mode) launch_colsums(X, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
-        cudaEvent_t ev;
-        c.begin_timed(1, &ev);
-        launch_k2(&s.tmap, s.dt, mode, plan, X, part, row_mean, scal_dev, colsums, Y, n_pad,
-                  c.stream);
-        c.end_timed(1, ev);
+        cudaEvent_t e0, e1;
+        c.make_events(&e0, &e1);
+        launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, X, part, row_mean, scal_dev, colsums, Y,
+                  n_pad, c.stream, e0, e1);
+        c.add_timed(1, e0, e1);
         launch_panel_dot(Y, Y, n_pad, wp, psmall, wmat, c.sms, c.stream);
         double w00 = 0.0;
         c.d2h_copy(&w00, wmat, 8);

@@ -35,7 +35,7 @@ struct Spectrum {
 // ref src/mds.hpp:21-28
 struct Embedding {
     size_t n = 0, r = 0;
-    std::vector<double> coords;       // n x r row-major
+    PinnedVec coords;                 // n x r row-major (pinned)
     std::vector<double> eigenvalues;  // retained, descending
     double dropped_negative_mass = 0.0;
     bool truncated = false;

@@ -20,4 +20,5 @@ ds.set_device(0)
 D = ds.matrix_euclidean(ds.synth_points(cfg, n, seed), store_f32=f32)
 for _ in range(a.warmup + a.steps):
     e = ds.embed(ds.gram(D), rank=k, oversampling=p, power_iters=q, seed=seed)
-print("dims", e.dims, "lambda1", e.eigenvalues[0] if e.dims else None)
+st = ds.stats_get()
+print("dims", e.dims, "lambda1", e.eigenvalues[0] if e.dims else None, "evd_sweeps", st.last_evd_sweeps, "shifted", st.last_orth_shifted)
