@@ -105,6 +105,12 @@ divscope_status divscope_matrix_write(const divscope_matrix* m, const char* dvs_
 divscope_status divscope_matrix_read(const char* dvs_path, divscope_matrix** out);
 /* ref divscope.h:128 */
 void divscope_matrix_free(divscope_matrix* m);
+/* NEW: host-only DVS1 header / payload check (no device needed): shape and
+ * symmetric flag of a DVS file, with read_matrix's error codes
+ * (ref src/distmat.cpp:189-222). If values != NULL it receives rows*cols
+ * doubles. */
+divscope_status divscope_dvs_read_host(const char* dvs_path, size_t* rows, size_t* cols,
+                                       int* symmetric, double* values);
 
 /* ---- distance builders that feed the path (no reference equivalent) ----- */
 

@@ -110,6 +110,8 @@ def _load() -> C.CDLL:
         "divscope_matrix_write": ([_vp, C.c_char_p], _st),
         "divscope_matrix_read": ([C.c_char_p, C.POINTER(_vp)], _st),
         "divscope_matrix_free": ([_vp], None),
+        "divscope_dvs_read_host": ([C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int),
+                                    _dp], _st),
         "divscope_matrix_euclidean": ([_dp, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
         "divscope_matrix_hamming": ([C.c_char_p, _sz, _sz, C.POINTER(_vp)], _st),
         "divscope_hamming_counts": ([C.c_char_p, _sz, _sz, C.POINTER(C.c_uint32)], _st),
@@ -242,6 +244,17 @@ def matrix_from_host_f32(values: np.ndarray, symmetric: bool = True) -> Matrix:
 
 def matrix_read(path) -> Matrix:
     return _new_matrix(lib.divscope_matrix_read, str(path).encode())
+
+
+def dvs_read_host(path) -> tuple[np.ndarray, bool]:
+    """DVS1 file -> (values, symmetric) on the host (no device needed)."""
+    rows, cols, sym = _sz(0), _sz(0), C.c_int(0)
+    _check(lib.divscope_dvs_read_host(str(path).encode(), C.byref(rows), C.byref(cols),
+                                      C.byref(sym), None))
+    out = np.empty((rows.value, cols.value), np.float64)
+    _check(lib.divscope_dvs_read_host(str(path).encode(), C.byref(rows), C.byref(cols),
+                                      C.byref(sym), out.ctypes.data_as(_dp)))
+    return out, bool(sym.value)
 
 
 def matrix_euclidean(points: np.ndarray, store_f32: bool = False) -> Matrix:

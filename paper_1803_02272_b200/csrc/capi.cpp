@@ -273,6 +273,20 @@ divscope_status divscope_matrix_read(const char* dvs_path, divscope_matrix** out
 
 void divscope_matrix_free(divscope_matrix* m) { delete m; }
 
+divscope_status divscope_dvs_read_host(const char* dvs_path, size_t* rows, size_t* cols,
+                                       int* symmetric, double* values) {
+    if (!dvs_path || !rows || !cols || !symmetric) return fail_invalid("null argument");
+    return wrap([&] {
+        size_t r = 0, c = 0;
+        bool sym = false;
+        const std::vector<double> v = dsb::read_dvs(dvs_path, r, c, sym);
+        *rows = r;
+        *cols = c;
+        *symmetric = sym ? 1 : 0;
+        if (values && !v.empty()) std::memcpy(values, v.data(), v.size() * sizeof(double));
+    });
+}
+
 divscope_status divscope_matrix_euclidean(const double* points, size_t n, size_t dim,
                                           int store_f32, divscope_matrix** out) {
     if (!points || !out) return fail_invalid("null argument");

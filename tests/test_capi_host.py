@@ -1,0 +1,150 @@
+"""CPU tests of the C ABI boundary (no GPU): the library loads, exports every
+symbol include/divscope.h declares, and keeps the reference's status codes,
+defaults, NULL handling and host-side file formats (ref include/divscope.h,
+src/capi.cpp:37-139, src/distmat.cpp:132-222, src/mds.cpp:152-238)."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+G = Path(__file__).resolve().parent / "golden"
+
+
+def declared_functions():
+    text = (ROOT / "include" / "divscope.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(divscope_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(ds):
+    names = declared_functions()
+    assert len(names) >= 45
+    missing = [n for n in names if not hasattr(ds.lib, n)]
+    assert not missing, missing
+
+
+def test_reference_functions_all_declared():
+    # the MDS section of the reference C API (ref include/divscope.h:114-185)
+    ref_names = """divscope_status_name divscope_last_error divscope_version divscope_readset_size
+    divscope_readset_id divscope_readset_free divscope_matrix_rows divscope_matrix_cols
+    divscope_matrix_symmetric divscope_matrix_get divscope_matrix_write divscope_matrix_read
+    divscope_matrix_free divscope_solver_options_init divscope_gram divscope_eigs
+    divscope_stable_rank divscope_embed divscope_embedding_rows divscope_embedding_dims
+    divscope_embedding_id divscope_embedding_get divscope_embedding_eigenvalues
+    divscope_embedding_dropped_negative_mass divscope_embedding_truncated
+    divscope_embedding_write divscope_embedding_load divscope_embedding_free""".split()
+    assert set(ref_names) <= set(declared_functions())
+
+
+def test_status_names_mirror_reference(ds):
+    names = ["ok", "io_error", "empty_input", "invalid_character", "duplicate_id",
+             "sample_too_large", "empty_sequence", "bad_format", "truncated", "not_symmetric",
+             "rank_too_large", "zero_matrix", "bad_gap", "shape_mismatch", "missing_label",
+             "join_error", "bad_axis", "invalid_argument", "internal"]
+    for code, name in enumerate(names):
+        assert ds.lib.divscope_status_name(code).decode() == name
+        assert ds.Status(code).value == code
+
+
+def test_solver_options_defaults(ds):
+    o = ds.solver_options_init()  # ref capi.cpp:288-294
+    assert (o.rank, o.oversampling, o.power_iters, o.seed) == (50, 10, 2, 0)
+
+
+def test_null_arguments(ds):
+    out = C.c_void_p()
+    assert ds.lib.divscope_gram(None, 1, C.byref(out)) == ds.Status.ERR_INVALID_ARGUMENT
+    assert ds.lib.divscope_last_error() == b"null argument"
+    assert out.value is None  # out-handles written only on success
+    assert ds.lib.divscope_embed(None, None, 1, None, C.byref(out)) == ds.Status.ERR_INVALID_ARGUMENT
+    assert ds.lib.divscope_matrix_rows(None) == 0 and ds.lib.divscope_embedding_dims(None) == 0
+    assert ds.lib.divscope_embedding_id(None, 0) is None
+    assert ds.lib.divscope_matrix_get(None, 0, 0) == 0.0
+
+
+def test_no_gpu_fails_loudly(ds):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.matrix_from_host(np.eye(2))
+    assert ei.value.status == ds.Status.ERR_INTERNAL
+    assert "no usable CUDA device" in ei.value.message
+
+
+def test_dvs_reads_reference_files(ds):
+    a, sym = ds.dvs_read_host(G / "rect5x7.dvs")
+    assert not sym and np.array_equal(a, np.load(G / "rect5x7.npy"))
+    d, sym = ds.dvs_read_host(G / "euclid64.dvs")
+    assert sym and np.array_equal(d, np.load(G / "euclid.npz")["d"])
+
+
+def test_dvs_errors(ds, tmp_path):
+    # ref src/distmat.cpp:189-222 error classes
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.dvs_read_host(tmp_path / "missing.dvs")
+    assert ei.value.status == ds.Status.ERR_IO
+    raw = (G / "rect5x7.dvs").read_bytes()
+    (tmp_path / "short.dvs").write_bytes(raw[:20])
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.dvs_read_host(tmp_path / "short.dvs")
+    assert ei.value.status == ds.Status.ERR_TRUNCATED
+    (tmp_path / "magic.dvs").write_bytes(b"XVS1" + raw[4:])
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.dvs_read_host(tmp_path / "magic.dvs")
+    assert ei.value.status == ds.Status.ERR_BAD_FORMAT
+    (tmp_path / "cut.dvs").write_bytes(raw[:-8])
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.dvs_read_host(tmp_path / "cut.dvs")
+    assert ei.value.status == ds.Status.ERR_TRUNCATED
+    bad = bytearray(raw)
+    bad[24] = 1  # symmetric flag on a 5 x 7 matrix
+    (tmp_path / "symrect.dvs").write_bytes(bytes(bad))
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.dvs_read_host(tmp_path / "symrect.dvs")
+    assert ei.value.status == ds.Status.ERR_BAD_FORMAT
+
+
+def test_embedding_tsv_load(ds, tmp_path):
+    # ref src/mds.cpp:190-238
+    (tmp_path / "e.tsv").write_text("id\tdim1\tdim2\na\t1.5\t-2\nb\t0\t3e-5\n")
+    e = ds.embedding_load(tmp_path / "e.tsv")
+    assert (e.rows, e.dims) == (2, 2) and e.id(1) == "b"
+    assert e.coords.tolist() == [[1.5, -2.0], [0.0, 3e-5]]
+    assert len(e.eigenvalues) == 0
+    e.write(tmp_path / "f.tsv")
+    assert (tmp_path / "f.tsv").read_text() == "id\tdim1\tdim2\na\t1.5\t-2\nb\t0\t3e-05\n"
+    (tmp_path / "bad.tsv").write_text("id\tdim1\na\tnotanumber\n")
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.embedding_load(tmp_path / "bad.tsv")
+    assert ei.value.status == ds.Status.ERR_BAD_FORMAT
+
+
+def test_synth_is_deterministic(ds):
+    a = ds.synth_points(2, 300, 5)
+    b = ds.synth_points(2, 300, 5)
+    assert np.array_equal(a, b) and a.shape == (300, 50)
+    reads = ds.synth_reads(300, 400, 50, 0.05, 1)
+    assert len(reads) == 300 and all(len(r) == 400 for r in reads)
+    assert set(b"".join(reads)) <= set(b"ACGT")
+    assert reads == ds.synth_reads(300, 400, 50, 0.05, 1)
+
+
+def test_synth_reads_substitution_rate(ds, oracle):
+    # same-ancestor reads differ at ~2 * 5% of positions (independent noise)
+    reads = ds.synth_reads(400, 400, 2, 0.05, 3)
+    st, h = oracle.hamming_counts(b"".join(reads), 400, 400)
+    small = h[h < 100]
+    small = small[small > 0]
+    assert 25 < np.median(small) < 55  # E = 400 * (1 - 0.95^2 - 0.05^2/3) ~ 38.7
+
+
+def test_synth_points_cluster_structure(ds):
+    pts = ds.synth_points(1, 2000, 1)  # 5 clusters, centers N(0, 100 I)
+    from numpy.linalg import eigvalsh
+    c = np.cov(pts.T)
+    ev = np.sort(eigvalsh(c))[::-1]
+    assert ev[:4].min() > 20 and ev[5:].max() < 2  # 4 between-cluster directions + unit noise
