@@ -184,10 +184,15 @@ def b200_arm(args, wl):
     import paper_1803_02272_b200 as ds
     ds.set_device(torch.cuda.current_device())
     cfg, n, k, p, q, seed, f32 = WORKLOADS[wl]
-    seed = seed + 1000 * rank  # independent replica per rank (DESIGN.md multi-GPU)
     w = k + min(p, n - k)
     passes = 2 * q + 3
     stream = torch.cuda.ExternalStream(ds.stream_ptr())
+    sharded = world > 1
+    if sharded:
+        # one NCCL communicator over the box; D row-sharded (strong scaling)
+        obj = [ds.comm_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        ds.comm_init(world, rank, obj[0])
 
     def barrier():
         if world > 1:
@@ -195,10 +200,13 @@ def b200_arm(args, wl):
 
     # ---- inputs: D built on the device (K9), host copy for the e2e leg
     pts = ds.synth_points(cfg, n, seed)
-    D = ds.matrix_euclidean(pts, store_f32=f32)
-    d_host = torch.empty((n, n), dtype=torch.float32 if f32 else torch.float64, pin_memory=True)
+    rb, re_ = ds.shard_range(n, world, rank) if sharded else (0, n)
+    D = ds.matrix_euclidean_rows(pts, rb, re_, store_f32=f32) if sharded else \
+        ds.matrix_euclidean(pts, store_f32=f32)
+    d_host = torch.empty((re_ - rb, n), dtype=torch.float32 if f32 else torch.float64,
+                         pin_memory=True)
     d_np = d_host.numpy()
-    d_np[...] = D.to_numpy().astype(d_np.dtype)
+    d_np[...] = D.to_numpy().astype(d_np.dtype)  # this rank's rows
     fp64_peak = ds.fp64_tensor_peak_tflops(20000)
     peaks = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -209,7 +217,11 @@ def b200_arm(args, wl):
         return e
 
     def step_e2e():
-        m = ds.matrix_from_host_f32(d_np) if f32 else ds.matrix_from_host(d_np)
+        if sharded:
+            m = (ds.matrix_from_host_rows_f32 if f32 else ds.matrix_from_host_rows)(
+                d_np, n, rb, re_)
+        else:
+            m = ds.matrix_from_host_f32(d_np) if f32 else ds.matrix_from_host(d_np)
         g = ds.gram(m)
         e = ds.embed(g, rank=k, oversampling=p, power_iters=q, seed=seed)
         c = e.coords  # result on the host
@@ -239,12 +251,13 @@ def b200_arm(args, wl):
         tt = torch.tensor([t_ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_ms = float(tt.item())
-    value = world * n * n * passes * args.steps / (t_ms * 1e-3)
+    value = n * n * passes * args.steps / (t_ms * 1e-3)
 
     # ---- roofline of the dominant kernel (K2, the centered product pass)
     k2_ms = st.product_ms / max(st.product_launches, 1)
-    bytes_per_launch = n * n * (4 if f32 else 8) + 2 * n * w * 8 + n * 8
-    flops_per_launch = 2.0 * n * n * w
+    m_rows = re_ - rb  # rows of D this rank streams per product pass
+    bytes_per_launch = m_rows * n * (4 if f32 else 8) + n * w * 8 + m_rows * w * 8 + m_rows * 8
+    flops_per_launch = 2.0 * m_rows * n * w
     tflops = flops_per_launch / (k2_ms * 1e-3) / 1e12
     gbs = bytes_per_launch / (k2_ms * 1e-3) / 1e9
     traffic = None
@@ -265,7 +278,7 @@ def b200_arm(args, wl):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
                 else "fallback 6650 GB/s (B200_PROFILING.md)"},
         "pass0": {"k1_avg_ms": st.stats_ms / max(st.stats_launches, 1),
-                  "achieved_gbs": n * n * (4 if f32 else 8) /
+                  "achieved_gbs": m_rows * n * (4 if f32 else 8) /
                   (st.stats_ms / max(st.stats_launches, 1) * 1e-3) / 1e9},
     }
 
@@ -288,7 +301,7 @@ def b200_arm(args, wl):
         tt = torch.tensor([te_ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         te_ms = float(tt.item())
-    e2e_value = world * n * n * passes * args.steps / (te_ms * 1e-3)
+    e2e_value = n * n * passes * args.steps / (te_ms * 1e-3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -304,13 +317,15 @@ def b200_arm(args, wl):
         line = {
             "metric": "MDS distance entries/s per streaming pass", "value": value,
             "unit": "entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, reference RNG conventions; D built on the GPU)",
             "config": {"workload": wl, "n": n, "k": k, "p": p, "q": q, "seed": seed,
                        "d_dtype": "f32" if f32 else "f64", "streaming_passes_per_step": passes,
                        "l2": "inputs larger than L2 (D = %.1f GB)" % (n * n * (4 if f32 else 8) / 1e9),
-                       "parallelism": "replicas" if world > 1 else "single"},
+                       "parallelism": (f"dp{world} (D row-sharded, panel all-gather + Gram "
+                                       "all-reduce over NCCL)") if world > 1 else "single"},
             "e2e": {"value": e2e_value, "unit": "entries/s",
                     "h2d_bytes_per_step": int(st2.h2d_bytes // max(args.steps, 1)),
                     "d2h_bytes_per_step": int(st2.d2h_bytes // max(args.steps, 1))},
@@ -323,6 +338,7 @@ def b200_arm(args, wl):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        ds.comm_destroy()
         torch.distributed.destroy_process_group()
     return 0
 

@@ -197,6 +197,30 @@ void divscope_embedding_free(divscope_embedding* e);
 divscope_status divscope_randomized_range(const divscope_matrix* gram,
                                           const divscope_solver_options* opts, double* q_out);
 
+/* ---- multi-GPU: one process per GPU, NCCL over NVLink (NEW) ------------ */
+
+/* 128-byte NCCL unique id (create on rank 0, share out of band). */
+divscope_status divscope_comm_unique_id(void* id128);
+/* Join the communicator (collective over all ranks). While active, gram /
+ * eigs / embed on row-sharded handles run the distributed algorithm. */
+divscope_status divscope_comm_init(int world, int rank, const void* id128);
+divscope_status divscope_comm_destroy(void);
+/* Row shard [begin, end) of `rank` for an n x n matrix: the reference chunk
+ * formula (ref src/parallel.hpp:33-34) over 256-row blocks. Host-only. */
+divscope_status divscope_shard_range(size_t n, int world, int rank, size_t* begin, size_t* end);
+/* This rank's rows [row_begin, row_end) of an n x n symmetric distance matrix
+ * (row-major host buffer of (row_end-row_begin) x n). */
+divscope_status divscope_matrix_from_host_rows(const double* rows, size_t n, size_t row_begin,
+                                               size_t row_end, int symmetric,
+                                               divscope_matrix** out);
+divscope_status divscope_matrix_from_host_rows_f32(const float* rows, size_t n, size_t row_begin,
+                                                   size_t row_end, int symmetric,
+                                                   divscope_matrix** out);
+/* This rank's rows of the exact Euclidean distance matrix of all n points. */
+divscope_status divscope_matrix_euclidean_rows(const double* points, size_t n, size_t dim,
+                                               int store_f32, size_t row_begin, size_t row_end,
+                                               divscope_matrix** out);
+
 /* ---- seeded workload synthesis (NEW; BASELINE.json configs) ------------ */
 
 /* Points of BASELINE config `config` (1..4), n x dim row-major into `out`

@@ -136,6 +136,13 @@ def _load() -> C.CDLL:
         "divscope_synth_points": ([C.c_int, _sz, C.c_uint64, _dp, C.POINTER(_sz)], _st),
         "divscope_synth_reads": ([_sz, _sz, _sz, C.c_double, C.c_uint64, C.c_char_p], _st),
         "divscope_set_device": ([C.c_int], _st),
+        "divscope_comm_unique_id": ([_vp], _st),
+        "divscope_comm_init": ([C.c_int, C.c_int, _vp], _st),
+        "divscope_comm_destroy": ([], _st),
+        "divscope_shard_range": ([_sz, C.c_int, C.c_int, C.POINTER(_sz), C.POINTER(_sz)], _st),
+        "divscope_matrix_from_host_rows": ([_dp, _sz, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
+        "divscope_matrix_from_host_rows_f32": ([_fp, _sz, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
+        "divscope_matrix_euclidean_rows": ([_dp, _sz, _sz, C.c_int, _sz, _sz, C.POINTER(_vp)], _st),
         "divscope_stats_enable_timing": ([C.c_int], None),
         "divscope_stats_reset": ([], None),
         "divscope_stats_get": ([C.POINTER(Stats)], None),
@@ -416,6 +423,51 @@ def synth_reads(count: int, length: int = 400, ancestors: int = 50, sub_rate: fl
     _check(lib.divscope_synth_reads(count, length, ancestors, sub_rate, seed, buf))
     raw = buf.raw
     return [raw[i * length:(i + 1) * length] for i in range(count)]
+
+
+# ---- multi-GPU -----------------------------------------------------------
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib.divscope_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_init(world: int, rank: int, uid: bytes) -> None:
+    buf = C.create_string_buffer(bytes(uid), 128)
+    _check(lib.divscope_comm_init(world, rank, buf))
+
+
+def comm_destroy() -> None:
+    _check(lib.divscope_comm_destroy())
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    b, e = _sz(0), _sz(0)
+    _check(lib.divscope_shard_range(n, world, rank, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def matrix_from_host_rows(rows: np.ndarray, n: int, row_begin: int, row_end: int,
+                          symmetric: bool = True) -> Matrix:
+    a = _f64(rows)
+    return _new_matrix(lib.divscope_matrix_from_host_rows, a.ctypes.data_as(_dp), n, row_begin,
+                       row_end, int(symmetric))
+
+
+def matrix_from_host_rows_f32(rows: np.ndarray, n: int, row_begin: int, row_end: int,
+                              symmetric: bool = True) -> Matrix:
+    a = np.ascontiguousarray(rows, dtype=np.float32)
+    return _new_matrix(lib.divscope_matrix_from_host_rows_f32, a.ctypes.data_as(_fp), n,
+                       row_begin, row_end, int(symmetric))
+
+
+def matrix_euclidean_rows(points: np.ndarray, row_begin: int, row_end: int,
+                          store_f32: bool = False) -> Matrix:
+    p = _f64(points)
+    n, dim = p.shape
+    return _new_matrix(lib.divscope_matrix_euclidean_rows, p.ctypes.data_as(_dp), n, dim,
+                       int(store_f32), row_begin, row_end)
 
 
 def set_device(device: int) -> None:

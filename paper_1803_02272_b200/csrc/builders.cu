@@ -20,15 +20,17 @@ constexpr int kET = 64;  // output tile edge
 
 template <bool F32>
 __global__ void __launch_bounds__(256) k_euclid(const double* __restrict__ pts, int n, int dim,
-                                                void* __restrict__ dout, size_t ld) {
+                                                void* __restrict__ dout, size_t ld, int row0,
+                                                int nrows) {
     extern __shared__ double sp[];
     const int ldp = dim + 1;  // odd stride: conflict-free column reads
     double* ri = sp;               // [64][ldp]
     double* cj = sp + kET * ldp;   // [64][ldp]
-    const int i0 = blockIdx.y * kET, j0 = blockIdx.x * kET;
+    const int i0 = row0 + blockIdx.y * kET, j0 = blockIdx.x * kET;
+    const int iend = row0 + nrows;
     for (int e = threadIdx.x; e < kET * dim; e += blockDim.x) {
         const int r = e / dim, c = e % dim;
-        ri[r * ldp + c] = (i0 + r < n) ? pts[static_cast<size_t>(i0 + r) * dim + c] : 0.0;
+        ri[r * ldp + c] = (i0 + r < iend) ? pts[static_cast<size_t>(i0 + r) * dim + c] : 0.0;
         cj[r * ldp + c] = (j0 + r < n) ? pts[static_cast<size_t>(j0 + r) * dim + c] : 0.0;
     }
     __syncthreads();
@@ -55,16 +57,17 @@ __global__ void __launch_bounds__(256) k_euclid(const double* __restrict__ pts, 
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int i = i0 + ty + 16 * a;
-        if (i >= n) continue;
+        if (i >= iend) continue;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int j = j0 + tx + 16 * b;
             if (j >= n) continue;
             const double dist = (i == j) ? 0.0 : __dsqrt_rn(acc[a][b]);
+            const size_t li = static_cast<size_t>(i - row0);
             if (F32)
-                static_cast<float*>(dout)[static_cast<size_t>(i) * ld + j] = __double2float_rn(dist);
+                static_cast<float*>(dout)[li * ld + j] = __double2float_rn(dist);
             else
-                static_cast<double*>(dout)[static_cast<size_t>(i) * ld + j] = dist;
+                static_cast<double*>(dout)[li * ld + j] = dist;
         }
     }
 }
@@ -119,17 +122,24 @@ __global__ void __launch_bounds__(256) k_hamming(const unsigned long long* __res
 
 void launch_euclid(const double* pts, size_t n, int dim, void* d, DType dt, size_t ld,
                    cudaStream_t st) {
-    const int nb = static_cast<int>((n + kET - 1) / kET);
+    launch_euclid_rows(pts, n, dim, d, dt, ld, 0, n, st);
+}
+
+void launch_euclid_rows(const double* pts, size_t n, int dim, void* d, DType dt, size_t ld,
+                        size_t row0, size_t nrows, cudaStream_t st) {
+    if (nrows == 0) return;
     const size_t smem = 2 * static_cast<size_t>(kET) * (dim + 1) * sizeof(double);
-    dim3 grid(nb, nb);
+    dim3 grid(static_cast<unsigned>((n + kET - 1) / kET), static_cast<unsigned>((nrows + kET - 1) / kET));
     if (dt == DType::F32) {
         cudaFuncSetAttribute(k_euclid<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
-        k_euclid<true><<<grid, 256, smem, st>>>(pts, static_cast<int>(n), dim, d, ld);
+        k_euclid<true><<<grid, 256, smem, st>>>(pts, static_cast<int>(n), dim, d, ld,
+                                                static_cast<int>(row0), static_cast<int>(nrows));
     } else {
         cudaFuncSetAttribute(k_euclid<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
-        k_euclid<false><<<grid, 256, smem, st>>>(pts, static_cast<int>(n), dim, d, ld);
+        k_euclid<false><<<grid, 256, smem, st>>>(pts, static_cast<int>(n), dim, d, ld,
+                                                 static_cast<int>(row0), static_cast<int>(nrows));
     }
     count_launch();
 }

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.hpp"
 #include "solver.hpp"
 
 using dsb::errc;
@@ -326,7 +327,8 @@ divscope_status divscope_gram(const divscope_matrix* dist, unsigned threads,
     (void)threads;
     if (!dist || !out) return fail_invalid("null argument");
     return wrap([&] {
-        dsb::Matrix g = dsb::gram_from_distances(dist->m);
+        dsb::Matrix g = dist->m.store->sharded ? dsb::gram_sharded(dist->m)
+                                               : dsb::gram_from_distances(dist->m);
         *out = new divscope_matrix{std::move(g)};
     });
 }
@@ -337,9 +339,10 @@ divscope_status divscope_eigs(const divscope_matrix* gram, const divscope_solver
     (void)threads;
     if (!gram || !opts || !eigenvalues) return fail_invalid("null argument");
     return wrap([&] {
-        if (gram->m.store->rows != gram->m.store->cols)
+        if (!gram->m.store->square())
             throw Error(errc::not_symmetric, "matrix is not square");
-        const dsb::Spectrum s = dsb::eigs_sym(gram->m, to_options(opts));
+        const dsb::Spectrum s = gram->m.store->sharded ? dsb::eigs_sharded(gram->m, to_options(opts))
+                                                       : dsb::eigs_sym(gram->m, to_options(opts));
         for (size_t i = 0; i < s.eigenvalues.size(); ++i) eigenvalues[i] = s.eigenvalues[i];
         if (count) *count = s.eigenvalues.size();
         if (resid) *resid = s.resid;
@@ -351,7 +354,7 @@ divscope_status divscope_stable_rank(const divscope_matrix* gram, unsigned threa
     (void)threads;
     if (!gram || !out) return fail_invalid("null argument");
     return wrap([&] {
-        if (gram->m.store->rows != gram->m.store->cols)
+        if (!gram->m.store->square())
             throw Error(errc::not_symmetric, "matrix is not square");
         *out = dsb::stable_rank(gram->m);
     });
@@ -363,11 +366,13 @@ divscope_status divscope_embed(const divscope_matrix* gram, const divscope_solve
     (void)threads;
     if (!gram || !opts || !out) return fail_invalid("null argument");
     return wrap([&] {
-        if (gram->m.store->rows != gram->m.store->cols)
+        if (!gram->m.store->square())
             throw Error(errc::not_symmetric, "matrix is not square");
-        if (ids && ids->ids.size() != gram->m.store->rows)
+        if (ids && ids->ids.size() != gram->m.store->order())
             throw Error(errc::shape_mismatch, "id count does not match matrix");
-        dsb::Embedding e = dsb::embed(gram->m, opts->rank, to_options(opts));
+        dsb::Embedding e = gram->m.store->sharded
+                               ? dsb::embed_sharded(gram->m, opts->rank, to_options(opts))
+                               : dsb::embed(gram->m, opts->rank, to_options(opts));
         auto* handle = new divscope_embedding;
         handle->ids = ids ? ids->ids : index_ids(e.n);
         handle->emb = std::move(e);
@@ -379,7 +384,7 @@ divscope_status divscope_randomized_range(const divscope_matrix* gram,
                                           const divscope_solver_options* opts, double* q_out) {
     if (!gram || !opts || !q_out) return fail_invalid("null argument");
     return wrap([&] {
-        if (gram->m.store->rows != gram->m.store->cols)
+        if (!gram->m.store->square())
             throw Error(errc::not_symmetric, "matrix is not square");
         dsb::randomized_range(gram->m, to_options(opts), q_out);
     });
@@ -450,6 +455,67 @@ divscope_status divscope_embedding_load(const char* tsv_path, divscope_embedding
 }
 
 void divscope_embedding_free(divscope_embedding* e) { delete e; }
+
+/* ---- multi-GPU ---- */
+
+divscope_status divscope_comm_unique_id(void* id128) {
+    if (!id128) return fail_invalid("null argument");
+    return wrap([&] { dsb::Comm::get().unique_id(id128); });
+}
+
+divscope_status divscope_comm_init(int world, int rank, const void* id128) {
+    if (!id128) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Ctx& c = dsb::Ctx::get();
+        std::lock_guard<std::recursive_mutex> lk(c.mu);
+        dsb::Comm::get().init(world, rank, id128, c.stream);
+    });
+}
+
+divscope_status divscope_comm_destroy(void) {
+    return wrap([&] { dsb::Comm::get().destroy(); });
+}
+
+divscope_status divscope_shard_range(size_t n, int world, int rank, size_t* begin, size_t* end) {
+    if (!begin || !end) return fail_invalid("null argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail_invalid("bad world/rank");
+    dsb::shard_rows(n, world, rank, *begin, *end);
+    g_last_error.clear();
+    return DIVSCOPE_OK;
+}
+
+divscope_status divscope_matrix_from_host_rows(const double* rows, size_t n, size_t row_begin,
+                                               size_t row_end, int symmetric,
+                                               divscope_matrix** out) {
+    if ((!rows && row_end > row_begin) || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m = dsb::matrix_from_host_rows(rows, n, row_begin, row_end, symmetric != 0,
+                                                   dsb::DType::F64);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+divscope_status divscope_matrix_from_host_rows_f32(const float* rows, size_t n, size_t row_begin,
+                                                   size_t row_end, int symmetric,
+                                                   divscope_matrix** out) {
+    if ((!rows && row_end > row_begin) || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m = dsb::matrix_from_host_rows(rows, n, row_begin, row_end, symmetric != 0,
+                                                   dsb::DType::F32);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+divscope_status divscope_matrix_euclidean_rows(const double* points, size_t n, size_t dim,
+                                               int store_f32, size_t row_begin, size_t row_end,
+                                               divscope_matrix** out) {
+    if (!points || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m =
+            dsb::matrix_euclidean_rows(points, n, dim, store_f32 != 0, row_begin, row_end);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
 
 /* ---- device / instrumentation ---- */
 

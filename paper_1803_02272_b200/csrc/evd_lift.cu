@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256) k_lift(const double* __restrict__ q, int 
                                               const double* __restrict__ vkeep,
                                               const int* __restrict__ imeta, int rmax,
                                               double* __restrict__ coords,
-                                              double* __restrict__ partial) {
+                                              double* __restrict__ partial, long long row_off) {
     extern __shared__ double sv[];  // [w][rmax]
     __shared__ double best_v[256];
     __shared__ int best_i[256];
@@ -381,7 +381,8 @@ __global__ void __launch_bounds__(256) k_lift(const double* __restrict__ q, int 
             }
         }
         partial[(static_cast<size_t>(blockIdx.x) * rmax + t) * 2 + 0] = v;
-        partial[(static_cast<size_t>(blockIdx.x) * rmax + t) * 2 + 1] = static_cast<double>(ix);
+        partial[(static_cast<size_t>(blockIdx.x) * rmax + t) * 2 + 1] =
+            ix < 0 ? -1.0 : static_cast<double>(ix + row_off);
     }
 }
 
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(256) k_lift_signs(const int* __restrict__ imet
     long long ix = -1;
     for (int b = lane; b < P; b += 32) {
         const double iv = partial[(static_cast<size_t>(b) * rmax + warp) * 2 + 1];
-        if (iv < 0) continue;
+        if (!(iv >= 0.0)) continue;  // empty CTA / rank (or NaN fill)
         const double tv = partial[(static_cast<size_t>(b) * rmax + warp) * 2 + 0];
         const long long ti = static_cast<long long>(iv);
         if (ix < 0 || fabs(tv) > fabs(v) || (fabs(tv) == fabs(v) && ti < ix)) {
@@ -462,8 +463,19 @@ void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
 void launch_lift(const double* q, size_t n, int wp, int w, const double* vkeep,
                  const double* kept_vals, const int* imeta, int rmax, double* coords,
                  double* partial, int sms, cudaStream_t st) {
-    const int P = static_cast<int>(std::min<size_t>(static_cast<size_t>(sms) * 2,
-                                                    std::max<size_t>(n / 64, 1)));
+    const int P = lift_grid(n, sms);
+    launch_lift_partial(q, n, wp, w, vkeep, imeta, rmax, coords, partial, 0, P, st);
+    double* scale = partial + static_cast<size_t>(P) * rmax * 2;
+    launch_lift_finish(n, imeta, P, rmax, kept_vals, partial, scale, coords, st);
+}
+
+int lift_grid(size_t n, int sms) {
+    return static_cast<int>(std::min<size_t>(static_cast<size_t>(sms) * 2, std::max<size_t>(n / 64, 1)));
+}
+
+void launch_lift_partial(const double* q, size_t n, int wp, int w, const double* vkeep,
+                         const int* imeta, int rmax, double* coords, double* partial,
+                         long long row_off, int P, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(w) * rmax * sizeof(double);
     static size_t set_for = 0;
     if (smem > 48 * 1024 && smem > set_for) {
@@ -472,13 +484,19 @@ void launch_lift(const double* q, size_t n, int wp, int w, const double* vkeep,
         set_for = smem;
     }
     k_lift<<<P, 256, smem, st>>>(q, static_cast<int>(n), wp, w, vkeep, imeta, rmax, coords,
-                                 partial);
-    double* scale = partial + static_cast<size_t>(P) * rmax * 2;
+                                 partial, row_off);
+    count_launch();
+}
+
+// signs from `P` partials (any number of CTAs / ranks, merged order-free),
+// then coords (n local rows) *= sign * sqrt(lambda); scale -> rmax doubles
+void launch_lift_finish(size_t n, const int* imeta, int P, int rmax, const double* kept_vals,
+                        const double* partial, double* scale, double* coords, cudaStream_t st) {
     k_lift_signs<<<(rmax * 32 + 255) / 256, 256, 0, st>>>(imeta, P, rmax, kept_vals, partial,
                                                          scale);
     const int sg = static_cast<int>(std::min<size_t>((n * rmax + 255) / 256, 148 * 8));
     k_lift_scale<<<std::max(sg, 1), 256, 0, st>>>(static_cast<int>(n), imeta, scale, coords);
-    count_launch(3);
+    count_launch(2);
 }
 
 }  // namespace dsb

@@ -116,6 +116,12 @@ private:
 // Device-resident dense matrix (row-major, leading dimension ld elements).
 struct Store {
     size_t rows = 0, cols = 0, ld = 0;
+    // row shard of a distributed matrix (multi-GPU): this store holds rows
+    // [row_begin, row_begin + rows) of an n_global x cols matrix
+    bool sharded = false;
+    size_t n_global = 0, row_begin = 0;
+    size_t order() const { return sharded ? n_global : rows; }
+    bool square() const { return sharded ? n_global == cols : rows == cols; }
     bool symmetric = false;
     DType dt = DType::F64;
     std::shared_ptr<DevBuf> buf;

@@ -277,7 +277,9 @@ void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
 
 int k2_warps(int wp) { return wp <= 64 ? 16 : 8; }
 
-K2Plan k2_plan(size_t n, int wp, DType dt, int sms) {
+K2Plan k2_plan(size_t n, int wp, DType dt, int sms) { return k2_plan_rect(n, n, wp, dt, sms); }
+
+K2Plan k2_plan_rect(size_t n, size_t ncols, int wp, DType dt, int sms) {
     K2Plan p;
     p.wp = wp;
     p.cw = k2_warps(wp);
@@ -285,7 +287,7 @@ K2Plan k2_plan(size_t n, int wp, DType dt, int sms) {
     p.n = static_cast<int>(n);
     p.nb = static_cast<int>((n + p.bm - 1) / p.bm);
     const int kt = dt == DType::F64 ? 16 : 32;
-    p.nk = static_cast<int>((n + kt - 1) / kt);
+    p.nk = static_cast<int>((ncols + kt - 1) / kt);
     p.total = static_cast<long long>(p.nb) * p.nk;
     p.grid = static_cast<int>(std::min<long long>(sms, p.total));
     const int sb = ((p.bm * 128 + kt * wp * 8) + 1023) / 1024 * 1024;

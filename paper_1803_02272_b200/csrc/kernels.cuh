@@ -42,6 +42,16 @@ int k1_grid(size_t n, int sms);
 void launch_k1(const void* d, DType dt, size_t ld, size_t n, const K1Work& w, double* row_mean,
                double* scalars, int sms, cudaStream_t st);
 
+// ---- K1 for a row shard (rectangular rows x cols block): row sums of d^2,
+// sum d^4 and max |d| (deterministic per-CTA partials -> finalize on host)
+int k1_rows_grid(size_t rows, int sms);
+void launch_k1_rows(const void* d, DType dt, size_t ld, size_t rows, size_t cols, double* rowsum,
+                    double* cta_stats, int grid, cudaStream_t st);
+// max |A[i][j] - B[j][i]| over an m x p block A (lda) and p x m block B (ldb),
+// atomically max-ed (non-negative doubles as u64) into *out
+void launch_asym_block(const void* a, size_t lda, const void* b, size_t ldb, DType dt, size_t m,
+                       size_t p, double* out, cudaStream_t st);
+
 // ---- K2: centered skinny product Y = G X (stream-K, DMMA f64) -------------
 struct K2Plan {
     int wp = 0;
@@ -53,6 +63,8 @@ struct K2Plan {
     size_t part_elems = 0;   // doubles needed for the partial workspace
 };
 K2Plan k2_plan(size_t n, int wp, DType dt, int sms);
+// rows (output rows, D rows) != ncols (reduction length = panel rows used)
+K2Plan k2_plan_rect(size_t rows, size_t ncols, int wp, DType dt, int sms);
 // mode: 0 = explicit matrix (Y = A X), 1 = gram of D (D squared on the fly,
 // then rank-3 centering).
 // e0/e1 (may be null) are recorded around the streaming kernel only
@@ -104,10 +116,20 @@ void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
 void launch_lift(const double* q, size_t n, int wp, int w, const double* vkeep,
                  const double* kept_vals, const int* imeta, int rmax, double* coords,
                  double* partial, int sms, cudaStream_t st);
+int lift_grid(size_t n, int sms);
+// partial: P x rmax x (value, global row index); row_off = global index of local row 0
+void launch_lift_partial(const double* q, size_t n, int wp, int w, const double* vkeep,
+                         const int* imeta, int rmax, double* coords, double* partial,
+                         long long row_off, int P, cudaStream_t st);
+void launch_lift_finish(size_t n, const int* imeta, int P, int rmax, const double* kept_vals,
+                        const double* partial, double* scale, double* coords, cudaStream_t st);
 
 // ---- K9 / K7: distance builders --------------------------------------------
 void launch_euclid(const double* pts, size_t n, int dim, void* d, DType dt, size_t ld,
                    cudaStream_t st);
+// rows [row0, row0 + nrows) of the n x n matrix into d (row-major, local rows)
+void launch_euclid_rows(const double* pts, size_t n, int dim, void* d, DType dt, size_t ld,
+                        size_t row0, size_t nrows, cudaStream_t st);
 void launch_hamming(const unsigned long long* packed, size_t count, int words, int length,
                     double* d, size_t ld, uint32_t* counts, cudaStream_t st);
 

@@ -1,0 +1,443 @@
+// Multi-GPU MDS path: D row-sharded over the ranks of one box
+// (one process per GPU), NCCL over NVLink only for the exchange steps.
+//
+//   gram   : K1 over the local rows (row sums / sum d^4 / max |d| — the
+//            reference's row means use full rows, mds.cpp:31-38, which a row
+//            shard has); the symmetry check exchanges the off-diagonal blocks
+//            pairwise (ring shift, send D[R_g, C_h], compare with the local
+//            D[R_g, C_h] transposed against the received D[R_h, C_g]); row
+//            means are all-gathered (every rank keeps the full r) and the
+//            scalars (grand mean, ||G||_F^2 closed form) are reduced in index
+//            order on the host, so they do not depend on the rank count.
+//   solve  : the panel X (n x w) is replicated; each pass computes the local
+//            rows Y_g = G[R_g, :] X with K2, CholeskyQR all-reduces the w x w
+//            Gram, applies R^{-1} to the local rows and all-gathers the panel
+//            (grouped broadcasts: shards differ by at most one block); the
+//            Ritz Gram Q^T GQ is all-reduced and every rank solves the same
+//            EVD; the sign rule gathers the per-CTA (max |u|, first index)
+//            partials of all ranks; the coordinates are all-gathered.
+// With one rank the same code runs with every collective a no-op.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+
+#include "comm.hpp"
+#include "solver.hpp"
+
+namespace dsb {
+
+namespace {
+
+struct Layout {
+    int world = 1, rank = 0;
+    std::vector<size_t> rb, re;  // row ranges of every rank
+};
+
+Layout layout_of(size_t n) {
+    Comm& cm = Comm::get();
+    Layout L;
+    L.world = cm.active() ? cm.world() : 1;
+    L.rank = cm.active() ? cm.rank() : 0;
+    L.rb.resize(L.world);
+    L.re.resize(L.world);
+    for (int r = 0; r < L.world; ++r) shard_rows(n, L.world, r, L.rb[r], L.re[r]);
+    return L;
+}
+
+// interleaved-panel chunk of rank r: rows [rb_r, re_r) padded to the block
+// (last rank to n_pad)
+void panel_chunks(const Layout& L, size_t n_pad, int wp, std::vector<size_t>& cnt,
+                  std::vector<size_t>& off) {
+    cnt.resize(L.world);
+    off.resize(L.world);
+    for (int r = 0; r < L.world; ++r) {
+        const size_t b = L.rb[r];
+        const size_t e = (r == L.world - 1) ? n_pad : L.rb[r + 1];
+        off[r] = b * wp;
+        cnt[r] = (e > b ? e - b : 0) * wp;
+    }
+}
+
+void check_shard(const Store& s) {
+    Layout L = layout_of(s.n_global);
+    if (s.row_begin != L.rb[L.rank] || s.row_begin + s.rows != L.re[L.rank])
+        throw Error(errc::shape_mismatch,
+                    "row shard does not match this rank's range (divscope_shard_range)");
+}
+
+}  // namespace
+
+Matrix matrix_from_host_rows(const void* rows, size_t n, size_t row_begin, size_t row_end,
+                             bool symmetric, DType dt) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    if (row_end < row_begin || row_end > n) throw Error(errc::invalid_argument, "bad row range");
+    Matrix m;
+    m.store = make_store(row_end - row_begin, n, symmetric, dt);
+    m.store->sharded = true;
+    m.store->n_global = n;
+    m.store->row_begin = row_begin;
+    upload_rows(*m.store, rows, n);
+    c.sync();
+    return m;
+}
+
+Matrix matrix_euclidean_rows(const double* pts, size_t n, size_t dim, bool f32, size_t row_begin,
+                             size_t row_end) {
+    // K9 on this shard's row window only (every (i, j) is computed
+    // independently, so the shard has exactly the bits of the full matrix)
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    if (row_end < row_begin || row_end > n) throw Error(errc::invalid_argument, "bad row range");
+    if (n == 0 || dim == 0) throw Error(errc::empty_input, "no points");
+    if (dim > 256) throw Error(errc::invalid_argument, "dimension > 256 not supported");
+    Matrix m;
+    m.store = make_store(row_end - row_begin, n, true, f32 ? DType::F32 : DType::F64);
+    m.store->sharded = true;
+    m.store->n_global = n;
+    m.store->row_begin = row_begin;
+    DevBuf dp(n * dim * sizeof(double));
+    c.h2d_copy(dp.p, pts, n * dim * sizeof(double));
+    launch_euclid_rows(dp.as<double>(), n, static_cast<int>(dim), m.store->buf->p, m.store->dt,
+                       m.store->ld, row_begin, row_end - row_begin, c.stream);
+    c.sync();
+    return m;
+}
+
+Matrix gram_sharded(const Matrix& d) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    Comm& cm = Comm::get();
+    const Store& s = *d.store;
+    if (!s.square() || !s.symmetric)
+        throw Error(errc::not_symmetric, "gram matrix requires a symmetric distance matrix");
+    const size_t n = s.n_global;
+    if (n == 0) throw Error(errc::empty_input, "empty distance matrix");
+    check_shard(s);
+    Layout L = layout_of(n);
+    const size_t m = s.rows, rb = s.row_begin;
+    const size_t esz = s.dt == DType::F64 ? 8 : 4;
+    // ---- local row statistics
+    const int grid = k1_rows_grid(m, c.sms);
+    auto row_mean = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * 8);  // full r
+    double* rowsum = static_cast<double*>(c.scratch("sh_rowsum", std::max<size_t>(m, 1) * 8));
+    double* cta = static_cast<double*>(c.scratch("sh_cta", static_cast<size_t>(grid) * 2 * 8));
+    double* red = static_cast<double*>(c.scratch("sh_red", 8 * 8));
+    DSB_CUDA(cudaMemsetAsync(red, 0, 8 * 8, c.stream));
+    cudaEvent_t e0, e1;
+    c.make_events(&e0, &e1);
+    if (e0) DSB_CUDA(cudaEventRecord(e0, c.stream));
+    if (m) launch_k1_rows(s.buf->p, s.dt, s.ld, m, n, rowsum, cta, grid, c.stream);
+    // ---- symmetry: local diagonal block, then ring-shift block exchange
+    launch_asym_block(static_cast<const char*>(s.buf->p) + rb * esz, s.ld,
+                      static_cast<const char*>(s.buf->p) + rb * esz, s.ld, s.dt, m, m, red + 2,
+                      c.stream);
+    if (L.world > 1) {
+        size_t maxm = 0;
+        for (int r = 0; r < L.world; ++r) maxm = std::max(maxm, L.re[r] - L.rb[r]);
+        // staging in f64 element units (f32 blocks travel as raw bytes)
+        const size_t stage_elems = (maxm * maxm * esz + 7) / 8;
+        double* sbuf = static_cast<double*>(c.scratch("sh_send", stage_elems * 8 + 64));
+        double* rbuf = static_cast<double*>(c.scratch("sh_recv", stage_elems * 8 + 64));
+        for (int sft = 1; sft < L.world; ++sft) {
+            const int ps = (L.rank + sft) % L.world, pr = (L.rank - sft + L.world) % L.world;
+            const size_t ms = L.re[ps] - L.rb[ps], mr = L.re[pr] - L.rb[pr];
+            // send D[R_g, C_ps] packed (m x ms)
+            if (m && ms)
+                DSB_CUDA(cudaMemcpy2DAsync(sbuf, ms * esz,
+                                           static_cast<const char*>(s.buf->p) + L.rb[ps] * esz,
+                                           s.ld * esz, ms * esz, m, cudaMemcpyDeviceToDevice,
+                                           c.stream));
+            cm.sendrecv(sbuf, (m * ms * esz + 7) / 8, ps, rbuf, (mr * m * esz + 7) / 8, pr,
+                        c.stream);
+            // received D[R_pr, C_g] (mr x m) vs local D[R_g, C_pr] (m x mr)
+            launch_asym_block(static_cast<const char*>(s.buf->p) + L.rb[pr] * esz, s.ld, rbuf, m,
+                              s.dt, m, mr, red + 2, c.stream);
+        }
+    }
+    // ---- scalars: sum d^4 (fixed-order partials), max |d|, max asym
+    {
+        // fold the CTA partials into red[0] (sum), red[1] (max) on the host
+        std::vector<double> h(static_cast<size_t>(grid) * 2);
+        if (m) {
+            DSB_CUDA(cudaMemcpyAsync(h.data(), cta, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+        }
+        double sum4 = 0.0, mx = 0.0;
+        for (int b = 0; b < (m ? grid : 0); ++b) {
+            sum4 += h[b * 2];
+            mx = std::max(mx, h[b * 2 + 1]);
+        }
+        double hv[2] = {sum4, mx};
+        DSB_CUDA(cudaMemcpyAsync(red, hv, 16, cudaMemcpyHostToDevice, c.stream));
+    }
+    cm.allreduce_sum(red, 1, c.stream);
+    cm.allreduce_max(red + 1, 2, c.stream);
+    // ---- row means: local, then all-gathered
+    {
+        std::vector<double> hs(m);
+        if (m) c.d2h_copy(hs.data(), rowsum, m * 8);
+        for (double& v : hs) v /= static_cast<double>(n);
+        if (m) c.h2d_copy(row_mean->as<double>() + rb, hs.data(), m * 8);
+        std::vector<size_t> cnt(L.world), off(L.world);
+        for (int r = 0; r < L.world; ++r) {
+            off[r] = L.rb[r];
+            cnt[r] = L.re[r] - L.rb[r];
+        }
+        cm.allgatherv(row_mean->as<double>(), cnt.data(), off.data(), c.stream);
+    }
+    if (e1) DSB_CUDA(cudaEventRecord(e1, c.stream));
+    c.add_timed(0, e0, e1);
+    double hred[3];
+    c.d2h_copy(hred, red, 24);
+    const double maxabs = hred[1];
+    double maxasym = 0.0;
+    {
+        uint64_t bits;
+        std::memcpy(&bits, &hred[2], 8);
+        std::memcpy(&maxasym, &bits, 8);
+    }
+    if (maxasym > 1e-12 * std::max(1.0, maxabs))  // ref mds.cpp:23-27
+        throw Error(errc::not_symmetric, "distance matrix values are not symmetric");
+    Matrix g;
+    g.store = d.store;
+    g.gram = std::make_shared<GramInfo>();
+    GramInfo& gi = *g.gram;
+    gi.n = n;
+    gi.row_mean = row_mean;
+    gi.row_mean_h.resize(n);
+    c.d2h_copy(gi.row_mean_h.data(), row_mean->p, n * 8);
+    // grand mean and ||G||_F^2 in index order on the host (rank-count independent)
+    double sr = 0.0, sr2 = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        sr += gi.row_mean_h[i];
+        sr2 += gi.row_mean_h[i] * gi.row_mean_h[i];
+    }
+    const double nf = static_cast<double>(n);
+    gi.sc[S_GRAND] = sr / nf;
+    gi.sc[S_FRO2_LAZY] = 0.25 * (hred[0] - 2.0 * nf * sr2 + nf * nf * gi.sc[S_GRAND] * gi.sc[S_GRAND]);
+    gi.sc[S_MAXABS] = maxabs;
+    gi.sc[S_MAXASYM] = maxasym;
+    gi.sc[S_SUM4] = hred[0];
+    gi.sc[S_SUMR] = sr;
+    gi.sc[S_SUMR2] = sr2;
+    gi.scalars = std::make_shared<DevBuf>(S_COUNT * 8);
+    c.h2d_copy(gi.scalars->p, gi.sc, S_COUNT * 8);
+    c.sync();
+    return g;
+}
+
+namespace {
+
+const double* omega_pinned(uint64_t seed, size_t n, size_t w) {
+    static std::deque<std::tuple<uint64_t, size_t, size_t, PinnedVec>> cache;
+    for (auto& e : cache)
+        if (std::get<0>(e) == seed && std::get<1>(e) == n && std::get<2>(e) == w)
+            return std::get<3>(e).data();
+    PinnedVec v(std::max<size_t>(n * w, 1));
+    std::mt19937_64 eng(seed);
+    fill_gaussian(eng, v.data(), n * w);
+    if (cache.size() >= 2) cache.pop_front();
+    cache.emplace_back(seed, n, w, std::move(v));
+    return std::get<3>(cache.back()).data();
+}
+
+struct ShardOut {
+    std::vector<double> vals;
+    size_t keep = 0;
+    double resid = 0.0;
+    Embedding emb;
+};
+
+ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed,
+                     bool embed_mode, size_t requested) {
+    Ctx& c = Ctx::get();
+    Comm& cm = Comm::get();
+    Store& s = *g.store;
+    if (!g.gram) throw Error(errc::invalid_argument, "sharded solve needs a gram handle");
+    const size_t n = s.n_global, m = s.rows, rb = s.row_begin;
+    check_shard(s);
+    Layout L = layout_of(n);
+    if (rank < 1) throw Error(errc::invalid_argument, "rank must be >= 1");
+    const size_t w = rank + p;
+    if (w > n) throw Error(errc::rank_too_large, "rank + oversampling exceeds matrix order");
+    if (w > static_cast<size_t>(kMaxWP))
+        throw Error(errc::invalid_argument,
+                    "rank + oversampling > 128 is not supported by the GPU path");
+    const int wi = static_cast<int>(w), wp = static_cast<int>(round_up(w, 8));
+    const size_t n_pad = round_up(n, kRowPad);
+    // local panel rows: block-aligned, last rank up to n_pad
+    const size_t m_pad = (L.rank == L.world - 1) ? n_pad - rb : (L.re[L.rank] - rb);
+    const double* r_full = g.gram->row_mean->as<double>();
+    const double* scal = g.gram->scalars->as<double>();
+    {
+        std::lock_guard<std::mutex> lk(s.mu);
+        if (!s.tmap_ok) {
+            if (!c.encode_tmap(&s.tmap128, s.buf->p, s.dt, std::max<size_t>(m, 1), s.cols, s.ld,
+                               128) ||
+                !c.encode_tmap(&s.tmap256, s.buf->p, s.dt, std::max<size_t>(m, 1), s.cols, s.ld,
+                               256))
+                throw Error(errc::internal, "cuTensorMapEncodeTiled failed");
+            s.tmap_ok = true;
+        }
+    }
+    const K2Plan plan = k2_plan_rect(std::max<size_t>(m, 1), n, wp, s.dt, c.sms);
+    const size_t pbytes = n_pad * wp * 8;
+    double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
+    double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));
+    double* P2 = static_cast<double*>(c.scratch("panel2", pbytes));
+    double* part = static_cast<double*>(c.scratch("k2_part", plan.part_elems * 8 + 64));
+    const int pg = panel_grid(std::max<size_t>(m_pad, 4), c.sms);
+    const int pgf = panel_grid(n_pad, c.sms);
+    double* psmall = static_cast<double*>(c.scratch(
+        "panel_part", static_cast<size_t>(std::max(pg, pgf)) * std::max(wp * wp, 2 * wp) * 8));
+    double* colsums = static_cast<double*>(c.scratch("colsums", 2 * wp * 8));
+    double* wmat = static_cast<double*>(c.scratch("wmat", wp * wp * 8));
+    double* rinv = static_cast<double*>(c.scratch("rinv", wp * wp * 8));
+    int* flags = static_cast<int*>(c.scratch("flags", 64));
+    DSB_CUDA(cudaMemsetAsync(flags, 0, 64, c.stream));
+    DSB_CUDA(cudaMemsetAsync(P1, 0, pbytes, c.stream));
+    std::vector<size_t> cnt, off;
+    panel_chunks(L, n_pad, wp, cnt, off);
+    {
+        const double* om = omega_pinned(seed, n, w);
+        double* stage = static_cast<double*>(c.scratch("omega_rm", n * w * 8));
+        c.h2d_copy(stage, om, n * w * 8);
+        launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, P0, c.stream);
+    }
+    const size_t lo = rb * wp;  // local chunk offset in a panel
+    auto product = [&](const double* x_full, double* y_full) {
+        // s = 1^T X, t = r^T X over the full replicated panel
+        launch_colsums(x_full, r_full, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
+        cudaEvent_t e0, e1;
+        c.make_events(&e0, &e1);
+        if (m)
+            launch_k2(s.tmap_for(plan.bm), s.dt, 1, plan, x_full, part, r_full + rb, scal, colsums,
+                      y_full + lo, m_pad, c.stream, e0, e1);
+        c.add_timed(1, e0, e1);
+    };
+    auto orth_local = [&](double* y_full, double* t_full, double* out_full) {
+        double* y = y_full + lo;
+        double* t = t_full + lo;
+        double* o = out_full + lo;
+        double* bufs[3][2] = {{y, t}, {t, y}, {y, o}};
+        for (int ps = 0; ps < 3; ++ps) {
+            launch_panel_dot(bufs[ps][0], bufs[ps][0], m_pad, wp, psmall, wmat, c.sms, c.stream);
+            cm.allreduce_sum(wmat, static_cast<size_t>(wp) * wp, c.stream);
+            launch_chol_inv(wmat, wp, wi, n, ps == 0 ? 1 : 0, rinv, flags, c.stream);
+            launch_panel_apply(bufs[ps][0], rinv, m_pad, wp, bufs[ps][1], c.stream);
+        }
+        cm.allgatherv(out_full, cnt.data(), off.data(), c.stream);
+    };
+    product(P0, P1);
+    orth_local(P1, P2, P0);
+    for (size_t it = 0; it < q; ++it) {
+        product(P0, P1);
+        orth_local(P1, P2, P0);
+        product(P0, P1);
+        orth_local(P1, P2, P0);
+    }
+    product(P0, P1);
+    launch_panel_dot(P0 + lo, P1 + lo, m_pad, wp, psmall, wmat, c.sms, c.stream);
+    cm.allreduce_sum(wmat, static_cast<size_t>(wp) * wp, c.stream);
+    const size_t req = embed_mode ? requested : std::min(rank, w);
+    EvdOut eo;
+    eo.vals = static_cast<double*>(c.scratch("evd_vals", kMaxWP * 8));
+    eo.vkeep = static_cast<double*>(c.scratch("evd_vkeep", w * std::max<size_t>(req, 1) * 8));
+    eo.kept_vals = static_cast<double*>(c.scratch("evd_kept", kMaxWP * 8));
+    eo.dmeta = static_cast<double*>(c.scratch("evd_dmeta", 64));
+    eo.imeta = static_cast<int*>(c.scratch("evd_imeta", 64));
+    launch_evd(wmat, wp, wi, static_cast<int>(rank), static_cast<int>(req), scal, S_FRO2_LAZY, eo,
+               c.stream);
+    ShardOut out;
+    double* coords = nullptr;
+    if (embed_mode) {
+        const size_t rq = std::max<size_t>(req, 1);
+        coords = static_cast<double*>(c.scratch("coords", n * rq * 8));
+        const int P = lift_grid(std::max<size_t>(m, 1), c.sms);
+        // all ranks' CTA partials side by side: [world][P][rmax][2]
+        double* lp = static_cast<double*>(
+            c.scratch("lift_part_all", (static_cast<size_t>(L.world) * P * 2 + 1) * rq * 8));
+        DSB_CUDA(cudaMemsetAsync(lp, 0xff, static_cast<size_t>(L.world) * P * 2 * rq * 8,
+                                 c.stream));  // -NaN index => ignored
+        // local rows written at their global row positions (r-wide rows
+        // once r is known on the device: the lift writes row-major n_local x r)
+        double* my_coords = static_cast<double*>(c.scratch("coords_local", std::max<size_t>(m, 1) * rq * 8));
+        if (m)
+            launch_lift_partial(P0 + lo, m, wp, wi, eo.vkeep, eo.imeta, static_cast<int>(req),
+                                my_coords, lp + static_cast<size_t>(L.rank) * P * 2 * rq,
+                                static_cast<long long>(rb), P, c.stream);
+        std::vector<size_t> pc(L.world, static_cast<size_t>(P) * 2 * rq), po(L.world);
+        for (int r = 0; r < L.world; ++r) po[r] = static_cast<size_t>(r) * P * 2 * rq;
+        cm.allgatherv(lp, pc.data(), po.data(), c.stream);
+        double* scale = lp + static_cast<size_t>(L.world) * P * 2 * rq;
+        launch_lift_finish(m, eo.imeta, L.world * P, static_cast<int>(req), eo.kept_vals, lp, scale,
+                           my_coords, c.stream);
+        DSB_CUDA(cudaGetLastError());
+        int im[8];
+        c.d2h_copy(im, eo.imeta, sizeof(im));
+        const size_t r = static_cast<size_t>(im[1]);
+        // gather n x r coordinates (row chunks are contiguous in row-major)
+        if (r) {
+            DSB_CUDA(cudaMemcpyAsync(coords + rb * r, my_coords, m * r * 8,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+            std::vector<size_t> cc(L.world), co(L.world);
+            for (int k = 0; k < L.world; ++k) {
+                co[k] = L.rb[k] * r;
+                cc[k] = (L.re[k] - L.rb[k]) * r;
+            }
+            cm.allgatherv(coords, cc.data(), co.data(), c.stream);
+        }
+    }
+    DSB_CUDA(cudaGetLastError());
+    double vals[kMaxWP], kept[kMaxWP], dmeta[8];
+    int imeta[8];
+    DSB_CUDA(cudaMemcpyAsync(vals, eo.vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
+    DSB_CUDA(cudaMemcpyAsync(kept, eo.kept_vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
+    DSB_CUDA(cudaMemcpyAsync(dmeta, eo.dmeta, 64, cudaMemcpyDeviceToHost, c.stream));
+    c.d2h_copy(imeta, eo.imeta, sizeof(imeta));
+    c.last_evd_sweeps = imeta[3];
+    if (!imeta[4]) throw Error(errc::internal, "small eigensolve failed");
+    out.vals.assign(vals, vals + w);
+    out.keep = static_cast<size_t>(imeta[0]);
+    out.resid = dmeta[0];
+    if (embed_mode) {
+        Embedding& e = out.emb;
+        e.n = n;
+        e.r = static_cast<size_t>(imeta[1]);
+        e.truncated = imeta[2] != 0;
+        e.dropped_negative_mass = dmeta[1];
+        e.resid = dmeta[0];
+        e.eigenvalues.assign(kept, kept + e.r);
+        e.coords.resize(n * e.r);
+        if (e.r) c.d2h_copy(e.coords.data(), coords, n * e.r * 8);
+    }
+    return out;
+}
+
+}  // namespace
+
+Embedding embed_sharded(const Matrix& g, size_t rank, SolverOptions opts) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    const size_t n = g.n();
+    if (rank < 1 || rank > n) throw Error(errc::rank_too_large, "rank must be in [1, n]");
+    opts.rank = rank;
+    opts.oversampling = std::min(opts.oversampling, n - rank);
+    ShardOut r = run_sharded(g, opts.rank, opts.oversampling, opts.power_iters, opts.seed, true, rank);
+    return std::move(r.emb);
+}
+
+Spectrum eigs_sharded(const Matrix& g, const SolverOptions& opts) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    ShardOut r = run_sharded(g, opts.rank, opts.oversampling, opts.power_iters, opts.seed, false,
+                             opts.rank);
+    Spectrum s;
+    s.eigenvalues.assign(r.vals.begin(), r.vals.begin() + r.keep);
+    s.resid = r.resid;
+    return s;
+}
+
+}  // namespace dsb

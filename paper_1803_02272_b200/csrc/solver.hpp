@@ -23,7 +23,7 @@ struct SolverOptions {
 struct Matrix {
     std::shared_ptr<Store> store;
     std::shared_ptr<GramInfo> gram;  // non-null => this handle denotes G(store)
-    size_t n() const { return store->rows; }
+    size_t n() const { return store->order(); }
 };
 
 // ref src/rsvd.hpp:29-33 (vectors omitted: the C ABI never returns them)
@@ -62,6 +62,16 @@ double matrix_get(const Matrix& m, size_t i, size_t j);
 void matrix_to_host(const Matrix& m, double* out);
 
 Matrix matrix_from_host(const void* values, size_t rows, size_t cols, bool symmetric, DType dt);
+
+// ---- multi-GPU (sharded.cpp): one process per GPU, NCCL ----------------
+// rows [row_begin, row_end) of an n x n matrix, uploaded by this rank
+Matrix matrix_from_host_rows(const void* rows, size_t n, size_t row_begin, size_t row_end,
+                             bool symmetric, DType dt);
+Matrix matrix_euclidean_rows(const double* pts, size_t n, size_t dim, bool f32,
+                             size_t row_begin, size_t row_end);
+Matrix gram_sharded(const Matrix& d);
+Embedding embed_sharded(const Matrix& g, size_t rank, SolverOptions opts);
+Spectrum eigs_sharded(const Matrix& g, const SolverOptions& opts);
 Matrix matrix_euclidean(const double* pts, size_t n, size_t dim, bool f32);
 Matrix matrix_hamming(const char* reads, size_t count, size_t length);
 void hamming_counts(const char* reads, size_t count, size_t length, uint32_t* out);

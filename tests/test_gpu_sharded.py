@@ -1,0 +1,72 @@
+"""GPU tests of the row-sharded (multi-GPU) path, run with one rank: the same
+code as N ranks with every collective over a single-rank NCCL communicator.
+(One GPU per box here; ranks that wait on each other must not share a GPU.)"""
+import numpy as np
+import pytest
+
+from helpers import coords_match_up_to_sign, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm1(ds):
+    uid = ds.comm_unique_id()
+    ds.comm_init(1, 0, uid)
+    yield
+    ds.comm_destroy()
+
+
+def test_sharded_embed_matches_oracle(ds, oracle, comm1):
+    pts = ds.synth_points(2, 1800, 4)
+    n = pts.shape[0]
+    b, e = ds.shard_range(n, 1, 0)
+    assert (b, e) == (0, n)
+    d_sh = ds.matrix_euclidean_rows(pts, b, e)
+    g = ds.gram(d_sh)
+    emb = ds.embed(g, rank=20, oversampling=10, power_iters=2, seed=9)
+    d = oracle.euclidean_matrix(pts)
+    st, rm, grand = oracle.gram_stats(d)
+    ref = oracle.embed(20, 10, 2, 9, d=d, row_mean=rm, grand=grand)
+    assert emb.dims == ref["r"]
+    assert rel_err(emb.eigenvalues, ref["eigenvalues"]) < 1e-10
+    assert coords_match_up_to_sign(emb.coords, ref["coords"]) < 1e-8 * np.sqrt(ref["eigenvalues"][0])
+    vals, resid = ds.eigs(g, rank=20, oversampling=10, power_iters=2, seed=9)
+    assert rel_err(vals, ref["eigenvalues"][: len(vals)]) < 1e-10
+
+
+def test_sharded_matches_unsharded(ds, comm1):
+    pts = ds.synth_points(1, 1000, 2)
+    a = ds.embed(ds.gram(ds.matrix_euclidean(pts)), rank=10, oversampling=10, power_iters=1, seed=1)
+    b = ds.embed(ds.gram(ds.matrix_euclidean_rows(pts, 0, 1000)), rank=10, oversampling=10,
+                 power_iters=1, seed=1)
+    assert rel_err(b.eigenvalues, a.eigenvalues) < 1e-12
+    assert coords_match_up_to_sign(b.coords, a.coords) < 1e-9 * np.sqrt(a.eigenvalues[0])
+
+
+def test_sharded_host_rows_and_validation(ds, oracle, comm1):
+    pts = ds.synth_points(1, 300, 3)
+    d = oracle.euclidean_matrix(pts)
+    m = ds.matrix_from_host_rows(d, 300, 0, 300)
+    assert (m.rows, m.cols) == (300, 300)
+    emb = ds.embed(ds.gram(m), rank=5, oversampling=5, power_iters=1, seed=2)
+    assert emb.dims == 5
+    lie = d.copy()
+    lie[3, 7] += 1e-6
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.gram(ds.matrix_from_host_rows(lie, 300, 0, 300))
+    assert ei.value.status == ds.Status.ERR_NOT_SYMMETRIC
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.gram(ds.matrix_from_host_rows(d[:100], 300, 0, 100))  # not this rank's range
+    assert ei.value.status == ds.Status.ERR_SHAPE_MISMATCH
+
+
+def test_sharded_f32(ds, oracle, comm1):
+    pts = ds.synth_points(4, 1200, 5)
+    d32 = oracle.euclidean_matrix(pts).astype(np.float32)
+    m = ds.matrix_from_host_rows_f32(d32, 1200, 0, 1200)
+    emb = ds.embed(ds.gram(m), rank=30, oversampling=10, power_iters=2, seed=3)
+    dw = d32.astype(np.float64)
+    st, rm, grand = oracle.gram_stats(dw)
+    ref = oracle.embed(30, 10, 2, 3, d=dw, row_mean=rm, grand=grand)
+    assert rel_err(emb.eigenvalues[:30], ref["eigenvalues"][:30]) < 1e-4
