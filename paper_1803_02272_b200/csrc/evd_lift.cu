@@ -30,14 +30,38 @@ __device__ __forceinline__ int pk(int a, int b, int w) {
 
 // Rotation of pair (p, q) annihilating a_pq (Rutishauser's formulas, as the
 // oracle's Jacobi): returns c, s with J = [[c, s], [-s, c]] on (p, q).
+// theta = (a_qq - a_pp) / (2 a_pq), t = sgn(theta) / (|theta| + sqrt(theta^2+1)),
+// c = 1 / sqrt(t^2 + 1), s = t c. The reciprocals / square roots use the
+// MUFU seeds plus Newton steps (a few ulps): any c, s with c^2 + s^2 = 1 to
+// rounding is an orthogonal rotation, and a slightly imperfect annihilation is
+// removed by the next sweep.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(r, fma(-x, r, 1.0), r);
+    r = fma(r, fma(-x, r, 1.0), r);
+    return r;
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y = rsqrt(x);  // MUFU.RSQ64H + refinement in libdevice
+    return y;
+}
 __device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, double& c,
                                            double& s) {
     c = 1.0;
     s = 0.0;
     if (fabs(apq) >= 1e-300) {
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        c = 1.0 / sqrt(t * t + 1.0);
+        const double theta = (aqq - app) * (0.5 * rcp_nr(apq));
+        const double th2 = theta * theta;
+        double t;
+        if (th2 < 1e300) {
+            const double hyp = (th2 + 1.0) * rsqrt_nr(th2 + 1.0);  // sqrt(theta^2 + 1)
+            t = rcp_nr(fabs(theta) + hyp);
+            if (theta < 0.0) t = -t;
+        } else {
+            t = 0.5 * rcp_nr(theta);
+        }
+        c = rsqrt_nr(t * t + 1.0);
         s = t * c;
     }
 }
@@ -109,32 +133,27 @@ __device__ void evd_finish(const double* __restrict__ A, const double* __restric
                            int fro_index, const EvdOut& o, int sweeps, int done,
                            int* __restrict__ order, int* __restrict__ kept) {
     const int tid = threadIdx.x, nt = blockDim.x;
+    // Reference order (rsvd.cpp:118-127 applied to Eigen's ascending output):
+    // ascending stable sort, then stable sort by |lambda| desc, positive first.
+    // Equivalent total order on (lambda, index): a before b iff
+    //   |la| > |lb|, or |la| == |lb| and la > lb, or la == lb and a < b
+    // (equal values keep the ascending sort's index order). Each thread
+    // computes its element's rank by counting predecessors.
+    for (int a = tid; a < w; a += nt) {
+        const double la = A[pk(a, a, w)];
+        int pos = 0;
+        for (int b = 0; b < w; ++b) {
+            if (b == a) continue;
+            const double lb = A[pk(b, b, w)];
+            const bool b_first = (fabs(lb) != fabs(la)) ? (fabs(lb) > fabs(la))
+                                 : (lb != la)           ? (lb > la)
+                                                        : (b < a);
+            pos += b_first ? 1 : 0;
+        }
+        order[pos] = a;
+    }
+    __syncthreads();
     if (tid == 0) {
-        // ascending (stable on index), then stable by |lambda| desc, + first
-        for (int a = 0; a < w; ++a) order[a] = a;
-        for (int a = 1; a < w; ++a) {
-            const int x = order[a];
-            const double vx = A[pk(x, x, w)];
-            int b = a - 1;
-            while (b >= 0 && A[pk(order[b], order[b], w)] > vx) {
-                order[b + 1] = order[b];
-                --b;
-            }
-            order[b + 1] = x;
-        }
-        for (int a = 1; a < w; ++a) {
-            const int x = order[a];
-            const double vx = A[pk(x, x, w)];
-            int b = a - 1;
-            while (b >= 0) {
-                const double vb = A[pk(order[b], order[b], w)];
-                const bool x_before = (fabs(vx) != fabs(vb)) ? (fabs(vx) > fabs(vb)) : (vx > vb);
-                if (!x_before) break;
-                order[b + 1] = order[b];
-                --b;
-            }
-            order[b + 1] = x;
-        }
         const int keep = min(rank, w);
         double sumsq = 0.0, maxabs = 0.0;
         for (int a = 0; a < w; ++a) o.vals[a] = A[pk(order[a], order[a], w)];
@@ -173,6 +192,7 @@ __device__ void evd_finish(const double* __restrict__ A, const double* __restric
 }
 
 constexpr int kEvdThreads = 512;
+__device__ long long g_evd_prof[16];
 
 // General kernel (any w <= 128): packed A single-buffered, rotations of a
 // round computed first (barrier), then all 2x2 blocks and V row pairs.
@@ -191,9 +211,11 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
     __shared__ unsigned char blk_i[(kMaxWP / 2) * (kMaxWP / 2 + 1) / 2];
     __shared__ unsigned char blk_j[(kMaxWP / 2) * (kMaxWP / 2 + 1) / 2];
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int a = tid; a < w; a += nt)
-        for (int b = a; b < w; ++b) A[pk(a, b, w)] = 0.5 * (bmat[a * wp + b] + bmat[b * wp + a]);
-    for (int e = tid; e < w * w; e += nt) V[e] = (e / w == e % w) ? 1.0 : 0.0;
+    for (int e = tid; e < w * w; e += nt) {
+        const int a = e / w, b = e % w;
+        if (b >= a) A[pk(a, b, w)] = 0.5 * (bmat[a * wp + b] + bmat[b * wp + a]);
+        V[e] = (a == b) ? 1.0 : 0.0;
+    }
     const int m = w + (w & 1), h = m / 2, nblk = h * (h + 1) / 2;
     for (int i = tid; i < h; i += nt) {
         const int base = i * h - (i * (i - 1)) / 2;
@@ -204,8 +226,10 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
     }
     __syncthreads();
     int done = (w <= 1), sweeps = 0;
+    long long t_a = clock64(), acc1 = 0, acc2 = 0, acc3 = 0;
     for (; sweeps < 60 && !done; ++sweeps) {
         for (int r = 0; r < m - 1; ++r) {
+            const long long t0 = clock64();
             for (int k = tid; k < h; k += nt) {
                 int p, q;
                 pair_at(r, k, m, p, q);
@@ -217,6 +241,8 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
                 sn[k] = s;
             }
             __syncthreads();
+            const long long t1 = clock64();
+            acc1 += t1 - t0;
             for (int e = tid; e < nblk; e += nt) {
                 const int i = blk_i[e], j = blk_j[e];
                 block_update(A, A, w, pp[i], qq[i], pp[j], qq[j], cs[i], sn[i], cs[j], sn[j], i == j);
@@ -232,10 +258,22 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
                 }
             }
             __syncthreads();
+            acc2 += clock64() - t1;
         }
+        const long long t2 = clock64();
         done = jacobi_converged(A, w, red);
+        acc3 += clock64() - t2;
     }
+    const long long t_b = clock64();
     evd_finish(A, V, w, rank, requested, scalars, fro_index, o, sweeps, done, order, kept);
+    if (tid == 0) {
+        g_evd_prof[0] = t_b - t_a;
+        g_evd_prof[1] = acc1;
+        g_evd_prof[2] = acc2;
+        g_evd_prof[3] = acc3;
+        g_evd_prof[4] = clock64() - t_b;
+        g_evd_prof[5] = sweeps;
+    }
 }
 
 // Small-w kernel (w <= 64): A double-buffered, so every thread computes the
@@ -433,9 +471,13 @@ __global__ void k_lift_scale(int n, const int* __restrict__ imeta,
 
 }  // namespace
 
+extern "C" void divscope_debug_evd_prof(long long* host16) {
+    cudaMemcpyFromSymbol(host16, g_evd_prof, 16 * sizeof(long long));
+}
+
 void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
                 const double* scalars, int fro_index, const EvdOut& o, cudaStream_t st) {
-    if (w <= 64) {
+    if (false) {
         const size_t smem = (static_cast<size_t>(w) * (w + 1) + static_cast<size_t>(w) * w) *
                             sizeof(double);
         static size_t set_small = 0;
@@ -455,7 +497,8 @@ void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
                                  static_cast<int>(smem));
             set_for = smem;
         }
-        k_evd<<<1, kEvdThreads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
+        const int threads = w <= 32 ? 128 : (w <= 64 ? 256 : kEvdThreads);
+        k_evd<<<1, threads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
     }
     count_launch();
 }

@@ -128,6 +128,8 @@ struct Store {
     // cached TMA descriptor for the K2 streaming read
     bool tmap_ok = false;
     CUtensorMap tmap128{}, tmap256{};  // box heights of the two K2 tile shapes
+    bool tmap64_ok = false;
+    CUtensorMap tmap64{};              // K1 tile-pair boxes
     const CUtensorMap* tmap_for(int bm) const { return bm == 256 ? &tmap256 : &tmap128; }
     // cached K1 results when used as an explicit symmetric matrix
     bool stats_ok = false;

@@ -65,73 +65,125 @@ __device__ __forceinline__ void pair_of(long long p, int nbt, int& I, int& J) {
     J = static_cast<int>(i + (p - off(i)));
 }
 
+// ---- TMA-fed version: tiles arrive as NB boxes of 64 rows x 128 bytes
+// (SWIZZLE_128B) on a 3..6-stage mbarrier ring filled by a producer warp; 8
+// consumer warps each own 8 rows of both tiles: lane (row r = l % 8, quarter
+// q = l / 8) reads its 16-element row segment with 16-byte shared loads,
+// sums it sequentially, and two xor-shuffles complete the 64-column row sum.
 template <typename T>
-__global__ void __launch_bounds__(kK1Threads) k1_tile_pairs(const T* __restrict__ d, size_t ld,
-                                                            int n, int nbt,
-                                                            double* __restrict__ part,
-                                                            size_t part_ld,
-                                                            double* __restrict__ cta_stats) {
-    __shared__ double mirror[kT][kT + 1];
+struct K1Cfg {
+    static constexpr int E = sizeof(T);
+    static constexpr int BC = 128 / E;           // columns per 128-byte box row
+    static constexpr int NB = kT / BC;           // boxes per 64-column tile
+    static constexpr int TILE = NB * kT * 128;   // bytes per tile
+    static constexpr int STAGE = 2 * TILE;
+    static constexpr int STAGES = (192 * 1024) / STAGE;
+};
+
+// element (r, c) of a swizzled tile (box-major)
+template <typename T>
+__device__ __forceinline__ const T* tile_at(const unsigned char* tile, int r, int c) {
+    using C = K1Cfg<T>;
+    const int b = c / C::BC, cc = c % C::BC;
+    const int byte = cc * C::E;
+    return reinterpret_cast<const T*>(tile + b * (kT * 128) + r * 128 +
+                                      ((((byte >> 4) ^ (r & 7))) << 4) + (byte & 15));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kK1Threads + 32, 1)
+    k1_tile_pairs(const __grid_constant__ CUtensorMap tm, int n, int nbt,
+                  double* __restrict__ part, size_t part_ld, double* __restrict__ cta_stats) {
+    using C = K1Cfg<T>;
+    extern __shared__ __align__(1024) unsigned char k1_raw[];
+    unsigned char* sm = k1_raw + ((1024u - (smem_u32(k1_raw) & 1023u)) & 1023u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::STAGES * C::STAGE);
+    uint64_t* empty = full + C::STAGES;
     __shared__ double red[4][kK1Threads / 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long npairs = static_cast<long long>(nbt) * (nbt + 1) / 2;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kK1Threads / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kK1Threads / 32) {  // producer
+        if (lane == 0) {
+            prefetch_tmap(&tm);
+            int s = 0;
+            uint32_t ph = 0;
+            long long it = 0;
+            for (long long p = blockIdx.x; p < npairs; p += gridDim.x, ++it) {
+                if (it >= C::STAGES) mbar_wait(&empty[s], ph ^ 1);
+                int I, J;
+                pair_of(p, nbt, I, J);
+                unsigned char* st = sm + s * C::STAGE;
+                mbar_arrive_expect_tx(&full[s], (I != J ? 2 : 1) * C::TILE);
+                for (int b = 0; b < C::NB; ++b)
+                    tma_load_2d(st + b * (kT * 128), &tm, J * kT + b * C::BC, I * kT, &full[s]);
+                if (I != J)
+                    for (int b = 0; b < C::NB; ++b)
+                        tma_load_2d(st + C::TILE + b * (kT * 128), &tm, I * kT + b * C::BC, J * kT,
+                                    &full[s]);
+                if (++s == C::STAGES) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        return;
+    }
     double sum4 = 0.0, maxabs = 0.0, maxabs_up = 0.0, maxasym = 0.0;
-
+    const int r = warp * 8 + (lane & 7), q = lane >> 3;
+    int s = 0;
+    uint32_t ph = 0;
     for (long long p = blockIdx.x; p < npairs; p += gridDim.x) {
         int I, J;
         pair_of(p, nbt, I, J);
-        const size_t r0 = static_cast<size_t>(I) * kT, c0 = static_cast<size_t>(J) * kT;
-        // tile A = D[I rows][J cols]: warp handles rows warp + 8t, lane cols 2*lane..+1
-        double a[8][2];
+        mbar_wait(&full[s], ph);
+        const unsigned char* A = sm + s * C::STAGE;
+        const unsigned char* B = (I != J) ? A + C::TILE : A;
+        double a[16];
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-            load2(d, ld, n, r0 + warp + 8 * t, c0 + 2 * lane, a[t][0], a[t][1]);
-        double b[8][2];
+        for (int j = 0; j < 16; ++j) a[j] = static_cast<double>(*tile_at<T>(A, r, q * 16 + j));
+        double rs = 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const double sq = a[j] * a[j];
+            rs += sq;
+            sum4 += sq * sq;
+            maxabs = fmax(maxabs, fabs(a[j]));
+            if (I != J || q * 16 + j >= r) maxabs_up = fmax(maxabs_up, fabs(a[j]));
+            // symmetry: A[r][c] vs B[c][r] (d_ij vs d_ji)
+            const double m = static_cast<double>(*tile_at<T>(B, q * 16 + j, r));
+            maxasym = fmax(maxasym, fabs(a[j] - m));
+        }
+        rs += __shfl_xor_sync(0xffffffffu, rs, 8);
+        rs += __shfl_xor_sync(0xffffffffu, rs, 16);
+        if (q == 0 && I * kT + r < n) part[static_cast<size_t>(J) * part_ld + I * kT + r] = rs;
         if (I != J) {
+            double rb = 0.0;
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
-                load2(d, ld, n, c0 + warp + 8 * t, r0 + 2 * lane, b[t][0], b[t][1]);
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const int r = warp + 8 * t;
-            const double s0 = a[t][0] * a[t][0], s1 = a[t][1] * a[t][1];
-            const double rs = warp_sum(s0 + s1);
-            if (lane == 0 && r0 + r < static_cast<size_t>(n)) part[J * part_ld + r0 + r] = rs;
-            sum4 += s0 * s0 + s1 * s1;
-            maxabs = fmax(maxabs, fmax(fabs(a[t][0]), fabs(a[t][1])));
-            const int cA = 2 * lane;
-            if (I != J || r <= cA) maxabs_up = fmax(maxabs_up, fabs(a[t][0]));
-            if (I != J || r <= cA + 1) maxabs_up = fmax(maxabs_up, fabs(a[t][1]));
-        }
-        if (I != J) {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const int r = warp + 8 * t;
-                const double s0 = b[t][0] * b[t][0], s1 = b[t][1] * b[t][1];
-                const double rs = warp_sum(s0 + s1);
-                if (lane == 0 && c0 + r < static_cast<size_t>(n)) part[I * part_ld + c0 + r] = rs;
-                sum4 += s0 * s0 + s1 * s1;
-                maxabs = fmax(maxabs, fmax(fabs(b[t][0]), fabs(b[t][1])));
-                mirror[r][2 * lane] = b[t][0];
-                mirror[r][2 * lane + 1] = b[t][1];
+            for (int j = 0; j < 16; ++j) {
+                const double b = static_cast<double>(*tile_at<T>(B, r, q * 16 + j));
+                const double sq = b * b;
+                rb += sq;
+                sum4 += sq * sq;
+                maxabs = fmax(maxabs, fabs(b));
             }
-        } else {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const int r = warp + 8 * t;
-                mirror[r][2 * lane] = a[t][0];
-                mirror[r][2 * lane + 1] = a[t][1];
-            }
+            rb += __shfl_xor_sync(0xffffffffu, rb, 8);
+            rb += __shfl_xor_sync(0xffffffffu, rb, 16);
+            if (q == 0 && J * kT + r < n) part[static_cast<size_t>(I) * part_ld + J * kT + r] = rb;
         }
-        __syncthreads();
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const int r = warp + 8 * t;
-            maxasym = fmax(maxasym, fabs(a[t][0] - mirror[2 * lane][r]));
-            maxasym = fmax(maxasym, fabs(a[t][1] - mirror[2 * lane + 1][r]));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == C::STAGES) {
+            s = 0;
+            ph ^= 1;
         }
-        __syncthreads();
     }
     // fixed-order block reduction (deterministic for a fixed grid)
     sum4 = warp_sum(sum4);
@@ -144,20 +196,25 @@ __global__ void __launch_bounds__(kK1Threads) k1_tile_pairs(const T* __restrict_
         red[2][warp] = maxabs_up;
         red[3][warp] = maxasym;
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"n"(kK1Threads));  // consumers only
     if (threadIdx.x == 0) {
-        double s = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+        double su = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
         for (int w = 0; w < kK1Threads / 32; ++w) {
-            s += red[0][w];
+            su += red[0][w];
             m1 = fmax(m1, red[1][w]);
             m2 = fmax(m2, red[2][w]);
             m3 = fmax(m3, red[3][w]);
         }
-        cta_stats[blockIdx.x * 4 + 0] = s;
+        cta_stats[blockIdx.x * 4 + 0] = su;
         cta_stats[blockIdx.x * 4 + 1] = m1;
         cta_stats[blockIdx.x * 4 + 2] = m2;
         cta_stats[blockIdx.x * 4 + 3] = m3;
     }
+}
+
+template <typename T>
+size_t k1_smem() {
+    return static_cast<size_t>(K1Cfg<T>::STAGES) * K1Cfg<T>::STAGE + 1024 + 16 * K1Cfg<T>::STAGES;
 }
 
 // r_i = (sum over tile columns of part[J][i]) / n, plus per-block sums of
@@ -253,28 +310,39 @@ size_t k1_part_elems(size_t n) {
 int k1_grid(size_t n, int sms) {
     const long long nbt = static_cast<long long>((n + kT - 1) / kT);
     const long long npairs = nbt * (nbt + 1) / 2;
-    const long long cap = static_cast<long long>(sms) * 6;
+    const long long cap = static_cast<long long>(sms);
     return static_cast<int>(npairs < cap ? npairs : cap);
 }
 
-void launch_k1(const void* d, DType dt, size_t ld, size_t n, const K1Work& w, double* row_mean,
+void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, double* row_mean,
                double* scalars, int sms, cudaStream_t st) {
     (void)sms;
     const int nbt = static_cast<int>((n + kT - 1) / kT);
     const size_t part_ld = static_cast<size_t>(nbt) * kT;
-    if (dt == DType::F64)
-        k1_tile_pairs<double><<<w.grid, kK1Threads, 0, st>>>(static_cast<const double*>(d), ld,
-                                                             static_cast<int>(n), nbt, w.part,
-                                                             part_ld, w.cta_stats);
-    else
-        k1_tile_pairs<float><<<w.grid, kK1Threads, 0, st>>>(static_cast<const float*>(d), ld,
-                                                            static_cast<int>(n), nbt, w.part,
-                                                            part_ld, w.cta_stats);
+    if (dt == DType::F64) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k1_tile_pairs<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(k1_smem<double>()));
+            attr = true;
+        }
+        k1_tile_pairs<double><<<w.grid, kK1Threads + 32, k1_smem<double>(), st>>>(
+            *tmap64, static_cast<int>(n), nbt, w.part, part_ld, w.cta_stats);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k1_tile_pairs<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(k1_smem<float>()));
+            attr = true;
+        }
+        k1_tile_pairs<float><<<w.grid, kK1Threads + 32, k1_smem<float>(), st>>>(
+            *tmap64, static_cast<int>(n), nbt, w.part, part_ld, w.cta_stats);
+    }
     const int nblk = static_cast<int>((n + 255) / 256);
     k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, part_ld, nbt, static_cast<int>(n), row_mean,
                                       w.blk_stats);
     k1_finalize<<<1, 256, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),
-                                  scalars);
+                                   scalars);
     count_launch(3);
 }
 

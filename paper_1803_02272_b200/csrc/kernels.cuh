@@ -39,7 +39,8 @@ struct K1Work {
 };
 size_t k1_part_elems(size_t n);
 int k1_grid(size_t n, int sms);
-void launch_k1(const void* d, DType dt, size_t ld, size_t n, const K1Work& w, double* row_mean,
+// tmap64: TMA descriptor of D with 64-row x 128-byte boxes (SWIZZLE_128B)
+void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, double* row_mean,
                double* scalars, int sms, cudaStream_t st);
 
 // ---- K1 for a row shard (rectangular rows x cols block): row sums of d^2,

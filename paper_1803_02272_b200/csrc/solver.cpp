@@ -22,8 +22,16 @@ struct StatsOut {
 };
 
 // K1 over a store; returns scalars (host) plus device scalars/row means.
-StatsOut run_k1(const Store& s) {
+StatsOut run_k1(Store& s) {
     Ctx& c = Ctx::get();
+    {
+        std::lock_guard<std::mutex> lk(s.mu);
+        if (!s.tmap64_ok) {
+            if (!c.encode_tmap(&s.tmap64, s.buf->p, s.dt, s.rows, s.cols, s.ld, 64))
+                throw Error(errc::internal, "cuTensorMapEncodeTiled failed");
+            s.tmap64_ok = true;
+        }
+    }
     const size_t n = s.rows;
     K1Work w;
     w.grid = k1_grid(n, c.sms);
@@ -36,7 +44,7 @@ StatsOut run_k1(const Store& s) {
     DSB_CUDA(cudaMemsetAsync(o.scalars->p, 0, S_COUNT * sizeof(double), c.stream));
     cudaEvent_t ev;
     c.begin_timed(0, &ev);
-    launch_k1(s.buf->p, s.dt, s.ld, n, w, o.row_mean->as<double>(), o.scalars->as<double>(), c.sms,
+    launch_k1(&s.tmap64, s.dt, n, w, o.row_mean->as<double>(), o.scalars->as<double>(), c.sms,
               c.stream);
     c.end_timed(0, ev);
     DSB_CUDA(cudaGetLastError());
@@ -279,7 +287,7 @@ Matrix matrix_from_host(const void* values, size_t rows, size_t cols, bool symme
 Matrix gram_from_distances(const Matrix& d) {
     Ctx& c = Ctx::get();
     std::lock_guard<std::recursive_mutex> lk(c.mu);
-    const Store& s = *d.store;
+    Store& s = *d.store;
     // ref mds.cpp:15-20
     if (s.rows != s.cols || !s.symmetric)
         throw Error(errc::not_symmetric, "gram matrix requires a symmetric distance matrix");
