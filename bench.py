@@ -46,6 +46,7 @@ WORKLOADS = {
     "C2": (2, 20000, 20, 10, 2, 2, False),
     "C3": (3, 100000, 50, 20, 2, 3, False),
     "C4": (4, 200000, 100, 20, 3, 4, True),
+    "C5": (5, 50000, 30, 20, 2, 5, False),   # Hamming D of 50k reads (L=400, 50 ancestors)
 }
 FP64_FALLBACK_TFLOPS = 37.1  # DMMA microbenchmark on this pool (profiles/fp64_peak_r01.txt)
 
@@ -199,14 +200,21 @@ def b200_arm(args, wl):
             torch.distributed.barrier()
 
     # ---- inputs: D built on the device (K9), host copy for the e2e leg
-    pts = ds.synth_points(cfg, n, seed)
     rb, re_ = ds.shard_range(n, world, rank) if sharded else (0, n)
-    D = ds.matrix_euclidean_rows(pts, rb, re_, store_f32=f32) if sharded else \
-        ds.matrix_euclidean(pts, store_f32=f32)
-    d_host = torch.empty((re_ - rb, n), dtype=torch.float32 if f32 else torch.float64,
-                         pin_memory=True)
-    d_np = d_host.numpy()
-    d_np[...] = D.to_numpy().astype(d_np.dtype)  # this rank's rows
+    if cfg == 5:
+        reads = ds.synth_reads(n, 400, 50, 0.05, seed)
+        D = ds.matrix_hamming(reads)
+        if sharded:
+            D = ds.matrix_from_host_rows(D.to_numpy()[rb:re_], n, rb, re_)
+    else:
+        pts = ds.synth_points(cfg, n, seed)
+        D = ds.matrix_euclidean_rows(pts, rb, re_, store_f32=f32) if sharded else \
+            ds.matrix_euclidean(pts, store_f32=f32)
+    if not args.no_e2e:
+        d_host = torch.empty((re_ - rb, n), dtype=torch.float32 if f32 else torch.float64,
+                             pin_memory=True)
+        d_np = d_host.numpy()
+        d_np[...] = D.to_numpy().astype(d_np.dtype)  # this rank's rows
     fp64_peak = ds.fp64_tensor_peak_tflops(20000)
     peaks = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -283,31 +291,35 @@ def b200_arm(args, wl):
     }
 
     # ---- e2e leg through the C ABI from pinned host memory
-    step_e2e()
-    torch.cuda.synchronize()
-    barrier()
-    ds.stats_reset()
-    ev2 = torch.cuda.Event(enable_timing=True)
-    ev3 = torch.cuda.Event(enable_timing=True)
-    ev2.record(stream)
-    for _ in range(args.steps):
+    e2e = None
+    if not args.no_e2e:
         step_e2e()
-    ev3.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    te_ms = ev2.elapsed_time(ev3)
-    st2 = ds.stats_get()
-    if world > 1:
-        tt = torch.tensor([te_ms], device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        te_ms = float(tt.item())
-    e2e_value = n * n * passes * args.steps / (te_ms * 1e-3)
+        torch.cuda.synchronize()
+        barrier()
+        ds.stats_reset()
+        ev2 = torch.cuda.Event(enable_timing=True)
+        ev3 = torch.cuda.Event(enable_timing=True)
+        ev2.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        ev3.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        te_ms = ev2.elapsed_time(ev3)
+        st2 = ds.stats_get()
+        if world > 1:
+            tt = torch.tensor([te_ms], device="cuda")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te_ms = float(tt.item())
+        e2e = {"value": n * n * passes * args.steps / (te_ms * 1e-3), "unit": "entries/s",
+               "h2d_bytes_per_step": int(st2.h2d_bytes // max(args.steps, 1)),
+               "d2h_bytes_per_step": int(st2.d2h_bytes // max(args.steps, 1))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle_bindings import Oracle
         omega = Oracle().fill_gaussian(seed, n * w).reshape(n, w)
-        dd = d_np.astype(np.float64)
+        dd = D.to_numpy()
         times, kind, cores = cpu_reference_pass(dd, omega, 1, 0)
         cpu = {"value": n * n / times[0], "unit": "entries/s", "cores": cores, "kind": kind,
                "sample": f"one multiply_sym pass (ref src/rsvd.cpp:18-36) over the materialized "
@@ -326,9 +338,7 @@ def b200_arm(args, wl):
                        "l2": "inputs larger than L2 (D = %.1f GB)" % (n * n * (4 if f32 else 8) / 1e9),
                        "parallelism": (f"dp{world} (D row-sharded, panel all-gather + Gram "
                                        "all-reduce over NCCL)") if world > 1 else "single"},
-            "e2e": {"value": e2e_value, "unit": "entries/s",
-                    "h2d_bytes_per_step": int(st2.h2d_bytes // max(args.steps, 1)),
-                    "d2h_bytes_per_step": int(st2.d2h_bytes // max(args.steps, 1))},
+            "e2e": e2e,
             "gpu_launches": int(st.kernel_launches),
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -351,6 +361,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (huge D)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args, args.workload)

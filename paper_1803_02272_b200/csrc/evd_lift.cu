@@ -154,6 +154,17 @@ __device__ void evd_finish(const double* __restrict__ A, const double* __restric
     }
     __syncthreads();
     if (tid == 0) {
+        // "positive first on equal |lambda|" (rsvd.cpp:118-127) also for twins
+        // equal to rounding (|la| and |lb| within 4 ulps): the reference's
+        // exact tie comes out of Eigen's EVD; ours can differ in the last bit.
+        for (int a = 0; a + 1 < w; ++a) {
+            const double x = A[pk(order[a], order[a], w)], y = A[pk(order[a + 1], order[a + 1], w)];
+            if (x < 0.0 && y > 0.0 && fabs(fabs(x) - y) <= 4.0 * 0x1.0p-52 * fabs(x)) {
+                const int t = order[a];
+                order[a] = order[a + 1];
+                order[a + 1] = t;
+            }
+        }
         const int keep = min(rank, w);
         double sumsq = 0.0, maxabs = 0.0;
         for (int a = 0; a < w; ++a) o.vals[a] = A[pk(order[a], order[a], w)];

@@ -32,55 +32,59 @@ constexpr double kShiftTrigF = 1e-10;  // same rules as k_chol_inv
 long long* g_orth_prof = nullptr;      // debug: per-phase cycle counts of CTA 0
 constexpr double kDropTolF = 1e-20;
 
-// CTA-wide right-looking Cholesky W = R^T R of a WP x WP matrix already in
-// shared memory (A, row-major, overwritten by R; strict lower part zeroed).
-// Thread 0 takes the pivot decision (shift / drop rules of k_chol_inv); the
-// row scaling and the trailing update are spread over the CTA. Returns true
-// when the first (shift-allowed) attempt asks for a shift; the caller then
-// reloads A + sigma I and calls again with first_shifting = false.
+// CTA-wide elimination W = L D L^T (A in shared memory, upper triangle used)
+// that also carries E = L^{-1} along (Gauss-Jordan style, same steps), so the
+// inverse Cholesky factor T = R^{-1} = L^{-T} D^{-1/2} comes out without a
+// second sequential sweep; the apply Q = Y T is then a small GEMM.
+// Step k: thread 0 takes the pivot decision (shift / drop rules of
+// k_chol_inv); one barrier; the trailing update of A and the new column
+// entries of E are spread over the CTA; one barrier.
+// Returns true when the first (shift-allowed) attempt asks for a shift.
 template <int WP>
-__device__ bool cta_cholesky(double* __restrict__ A, int w, const double* __restrict__ d0s,
-                             double maxdiag, bool first_shifting, bool drop_mode,
-                             int* __restrict__ dropped_s, double* __restrict__ rinv_diag) {
-    __shared__ double piv_s, inv_s;
-    __shared__ int drop_s, shift_s;
+__device__ bool cta_chol_inverse(double* __restrict__ A, double* __restrict__ E, int w,
+                                 const double* __restrict__ d0s, double maxdiag,
+                                 bool first_shifting, bool drop_mode, int* __restrict__ dropped_s,
+                                 double* __restrict__ dpiv, const unsigned short* __restrict__ tri,
+                                 const int* __restrict__ tri_off) {
+    __shared__ double invp_s;
+    __shared__ int shift_s;
     const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < WP * WP; e += nt) E[e] = (e / WP == e % WP) ? 1.0 : 0.0;
+    if (tid == 0) shift_s = 0;
+    __syncthreads();
     for (int k = 0; k < WP; ++k) {
         if (tid == 0) {
             const double p = A[k * WP + k];
             const double d0k = d0s[k];
             bool drop = (k >= w) || !(d0k > 0.0) || !(p > 0.0);
-            bool shift = false;
             if (first_shifting) {
-                if (k < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift = true;
+                if (k < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift_s = 1;
                 drop = drop && !(k < w && d0k > 0.0);
             } else if (drop_mode && p <= kDropTolF * maxdiag) {
                 drop = true;
             }
-            const double rkk = drop ? 1.0 : sqrt(p);
-            piv_s = rkk;
-            inv_s = drop ? 0.0 : 1.0 / rkk;
-            drop_s = drop;
-            shift_s = shift;
             dropped_s[k] = drop;
-            rinv_diag[k] = inv_s;
-            A[k * WP + k] = rkk;
+            dpiv[k] = drop ? 0.0 : p;
+            invp_s = drop ? 0.0 : 1.0 / p;
         }
         __syncthreads();
         if (shift_s) return true;
-        const double inv = inv_s;
-        for (int j = k + 1 + tid; j < WP; j += nt) A[k * WP + j] *= inv;  // drop => 0
-        __syncthreads();
-        const int m = WP - k - 1;
-        for (int e = tid; e < m * m; e += nt) {
-            const int i = k + 1 + e / m, j = k + 1 + e % m;
-            if (j >= i) A[i * WP + j] -= A[k * WP + i] * A[k * WP + j];
+        const double invp = invp_s;  // 0 for a dropped column: no elimination with it
+        const double* rowk = A + k * WP;
+        // trailing upper triangle {(i, j): k < i <= j}: a suffix of `tri`
+        const int t0 = tri_off[k + 1], t1 = tri_off[WP];
+        for (int t = t0 + tid; t < t1; t += nt) {
+            const int i = tri[t] >> 8, j = tri[t] & 0xff;
+            A[i * WP + j] -= rowk[i] * rowk[j] * invp;
+        }
+        // E rows i > k, columns c <= k: E[i][c] -= l_ik E[k][c], l_ik = a_ki / d_k
+        const int cols = k + 1, nrow = WP - k - 1;
+        for (int e = tid; e < nrow * cols; e += nt) {
+            const int i = k + 1 + e / cols, cc = e % cols;
+            E[i * WP + cc] -= rowk[i] * invp * E[k * WP + cc];
         }
         __syncthreads();
     }
-    for (int e = tid; e < WP * WP; e += nt)
-        if (e / WP > e % WP) A[e] = 0.0;
-    __syncthreads();
     return false;
 }
 
@@ -103,11 +107,14 @@ __global__ void __launch_bounds__(256, 1)
     constexpr int NT = NF * NF;
     constexpr int TPW = (NT + 7) / 8;
     cg::grid_group grid = cg::this_grid();
-    __shared__ double R[WP * WP];
+    __shared__ double R[WP * WP];   // W, eliminated in place
+    __shared__ double E[WP * WP];   // L^{-1}, then T = R^{-1}
     __shared__ int dropped_s[WP];
     __shared__ double d0s[WP];
-    __shared__ double rdiag[WP];
+    __shared__ double dpiv[WP];
     __shared__ double tr_s[2];
+    __shared__ unsigned short tri[WP * (WP + 1) / 2];
+    __shared__ int tri_off[WP + 1];
     __shared__ int skip_third;
     // the CTA's rows stay in shared memory for all passes, column-major with
     // leading dimension ldr = 4 (mod 16): conflict-free MMA fragments and
@@ -126,6 +133,12 @@ __global__ void __launch_bounds__(256, 1)
         }
     }
     if (threadIdx.x == 0) skip_third = 0;
+    for (int i = threadIdx.x; i <= WP; i += blockDim.x) {  // upper-triangle list sorted by row
+        const int off = i * WP - (i * (i - 1)) / 2;
+        tri_off[i] = off;
+        for (int j = i; j < WP && i < WP; ++j)
+            tri[off + j - i] = static_cast<unsigned short>((i << 8) | j);
+    }
     __syncthreads();
     mark();
     // pass 0 may shift; when it did not, CholQR2 suffices (same decision in
@@ -203,8 +216,8 @@ __global__ void __launch_bounds__(256, 1)
                 __syncthreads();
                 const bool first_shifting = pass == 0 && attempt == 0;
                 const bool drop_mode = pass != 0;
-                if (!cta_cholesky<WP>(R, w, d0s, tr_s[1], first_shifting, drop_mode, dropped_s,
-                                      rdiag))
+                if (!cta_chol_inverse<WP>(R, E, w, d0s, tr_s[1], first_shifting, drop_mode,
+                                          dropped_s, dpiv, tri, tri_off))
                     break;
                 sigma = 11.0 * (nrows * w + static_cast<double>(w) * (w + 1)) * 0x1.0p-53 * tr_s[0];
                 shifted = true;
@@ -216,16 +229,51 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncthreads();
         mark();
-        // ---- 4. q_r R = y_r, thread per row, in place in shared memory
-        for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
-            for (int cc = 0; cc < WP; ++cc) {
-                double v = 0.0;
-                if (!dropped_s[cc]) {
-                    double s = ps[cc * ldr + r];
-                    for (int k = 0; k < cc; ++k) s -= ps[k * ldr + r] * R[k * WP + cc];
-                    v = s * rdiag[cc];
+        // ---- 4. T = R^{-1} = L^{-T} D^{-1/2} (into R), then Q = Y T for this
+        // CTA's rows: outputs kept in registers until every thread has read
+        // its inputs, then written back in place
+        for (int e = threadIdx.x; e < WP * WP; e += blockDim.x) {
+            const int i = e / WP, j = e % WP;
+            const double dj = dpiv[j];
+            R[e] = (i <= j && dj > 0.0) ? E[j * WP + i] * rsqrt(dj) : 0.0;
+        }
+        __syncthreads();
+        {
+            // Q = Y T on the f64 tensor cores: 8x8 output tiles (row tile tm,
+            // column tile tn) spread over the warps, K = WP in steps of 4;
+            // fragments straight from shared memory (ps column-major with
+            // ldr = 4 mod 16: conflict-free A fragments)
+            constexpr int NFT = WP / 8;
+            constexpr int kMaxT = 16;  // tiles per warp: ceil(rows/8) * NFT / 8 <= 16
+            const int ntm = (nrow + 7) / 8, ntile = ntm * NFT;
+            double acc[kMaxT][2];
+            const int rq = lane >> 2, kq = lane & 3;
+#pragma unroll
+            for (int j = 0; j < kMaxT; ++j) {
+                acc[j][0] = acc[j][1] = 0.0;
+                const int t = warp + 8 * j;
+                if (t < ntile) {
+                    const int tm = t / NFT, tn = t % NFT;
+#pragma unroll
+                    for (int kk = 0; kk < WP / 4; ++kk) {
+                        const double av = ps[(4 * kk + kq) * ldr + 8 * tm + rq];
+                        const double bv = R[(4 * kk + kq) * WP + 8 * tn + rq];
+                        dmma884(acc[j][0], acc[j][1], av, bv);
+                    }
                 }
-                ps[cc * ldr + r] = v;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < kMaxT; ++j) {
+                const int t = warp + 8 * j;
+                if (t < ntile) {
+                    const int tm = t / NFT, tn = t % NFT;
+                    const int row = 8 * tm + rq, col = 8 * tn + 2 * kq;
+                    if (row < nrow) {
+                        ps[col * ldr + row] = acc[j][0];
+                        ps[(col + 1) * ldr + row] = acc[j][1];
+                    }
+                }
             }
         }
         __syncthreads();
@@ -248,7 +296,8 @@ bool launch_wp(double* y, double* out, size_t n_pad, int w, size_t n, double* pa
     const int rows_max = static_cast<int>(((nq + P - 1) / P) * 4);
     const int ldr = (rows_max + 15) / 16 * 16 + 4;
     const size_t smem = static_cast<size_t>(WP) * ldr * sizeof(double);
-    if (smem > 200 * 1024) return false;
+    // DMMA apply: ceil(rows / 8) * (WP / 8) tiles over 8 warps, <= 16 per warp
+    if (smem > 200 * 1024 || ((rows_max + 7) / 8) * (WP / 8) > 8 * 16) return false;
     static size_t attr = 0;
     if (smem > attr) {
         cudaFuncSetAttribute(k_orth_fused<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
