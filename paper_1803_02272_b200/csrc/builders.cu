@@ -131,13 +131,11 @@ void launch_euclid_rows(const double* pts, size_t n, int dim, void* d, DType dt,
     const size_t smem = 2 * static_cast<size_t>(kET) * (dim + 1) * sizeof(double);
     dim3 grid(static_cast<unsigned>((n + kET - 1) / kET), static_cast<unsigned>((nrows + kET - 1) / kET));
     if (dt == DType::F32) {
-        cudaFuncSetAttribute(k_euclid<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
+        allow_dyn_smem(reinterpret_cast<const void*>(k_euclid<true>));
         k_euclid<true><<<grid, 256, smem, st>>>(pts, static_cast<int>(n), dim, d, ld,
                                                 static_cast<int>(row0), static_cast<int>(nrows));
     } else {
-        cudaFuncSetAttribute(k_euclid<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
+        allow_dyn_smem(reinterpret_cast<const void*>(k_euclid<false>));
         k_euclid<false><<<grid, 256, smem, st>>>(pts, static_cast<int>(n), dim, d, ld,
                                                  static_cast<int>(row0), static_cast<int>(nrows));
     }
@@ -148,8 +146,7 @@ void launch_hamming(const unsigned long long* packed, size_t count, int words, i
                     double* d, size_t ld, uint32_t* counts, cudaStream_t st) {
     const int nb = static_cast<int>((count + kET - 1) / kET);
     const size_t smem = 2 * static_cast<size_t>(kET) * words * sizeof(unsigned long long);
-    cudaFuncSetAttribute(k_hamming, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
+    allow_dyn_smem(reinterpret_cast<const void*>(k_hamming));
     dim3 grid(nb, nb);
     k_hamming<<<grid, 256, smem, st>>>(packed, static_cast<int>(count), words, length, d, ld,
                                        counts);

@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
     __shared__ int order[kMaxWP], kept[kMaxWP];
     __shared__ unsigned char blk_i[(kMaxWP / 2) * (kMaxWP / 2 + 1) / 2];
     __shared__ unsigned char blk_j[(kMaxWP / 2) * (kMaxWP / 2 + 1) / 2];
+    __shared__ unsigned short sched[(kMaxWP - 1) * (kMaxWP / 2)];
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int e = tid; e < w * w; e += nt) {
         const int a = e / w, b = e % w;
@@ -235,6 +236,16 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
             blk_j[base + j - i] = static_cast<unsigned char>(j);
         }
     }
+    // tournament schedule of every round, precomputed (no modulo in the loop)
+    for (int e = tid; e < (m - 1) * h; e += nt) {
+        const int r = e / h, k = e % h;
+        int p, q;
+        pair_at(r, k, m, p, q);
+        sched[e] = static_cast<unsigned short>((p << 8) | q);
+    }
+    // V rotation mapping: thread -> (pair vi, first row vk0), rows stride vks
+    const int vact = (nt / h) * h;  // active threads in the V phase
+    const int vi = tid % h, vk0 = tid / h, vks = nt / h;
     __syncthreads();
     int done = (w <= 1), sweeps = 0;
     long long t_a = clock64(), acc1 = 0, acc2 = 0, acc3 = 0;
@@ -242,8 +253,8 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
         for (int r = 0; r < m - 1; ++r) {
             const long long t0 = clock64();
             for (int k = tid; k < h; k += nt) {
-                int p, q;
-                pair_at(r, k, m, p, q);
+                const int pq = sched[r * h + k];
+                const int p = pq >> 8, q = pq & 0xff;
                 double c = 1.0, s = 0.0;
                 if (q < w) jacobi_rot(A[pk(p, p, w)], A[pk(q, q, w)], A[pk(p, q, w)], c, s);
                 pp[k] = p;
@@ -258,11 +269,10 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
                 const int i = blk_i[e], j = blk_j[e];
                 block_update(A, A, w, pp[i], qq[i], pp[j], qq[j], cs[i], sn[i], cs[j], sn[j], i == j);
             }
-            for (int e = tid; e < w * h; e += nt) {
-                const int k = e / h, i = e % h;
-                const int p = pp[i], q = qq[i];
-                if (q < w) {
-                    const double c = cs[i], s = sn[i];
+            if (tid < vact && qq[vi] < w) {
+                const int p = pp[vi], q = qq[vi];
+                const double c = cs[vi], s = sn[vi];
+                for (int k = vk0; k < w; k += vks) {
                     const double vp = V[k * w + p], vq = V[k * w + q];
                     V[k * w + p] = c * vp - s * vq;
                     V[k * w + q] = s * vp + c * vq;
@@ -491,23 +501,13 @@ void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
     if (false) {
         const size_t smem = (static_cast<size_t>(w) * (w + 1) + static_cast<size_t>(w) * w) *
                             sizeof(double);
-        static size_t set_small = 0;
-        if (smem > 48 * 1024 && smem > set_small) {
-            cudaFuncSetAttribute(k_evd_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-            set_small = smem;
-        }
+        allow_dyn_smem(reinterpret_cast<const void*>(k_evd_small));
         const int threads = w <= 32 ? 128 : 512;
         k_evd_small<<<1, threads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
     } else {
         const size_t smem = (static_cast<size_t>(w) * (w + 1) / 2 + static_cast<size_t>(w) * w) *
                             sizeof(double);
-        static size_t set_for = 0;
-        if (smem > 48 * 1024 && smem > set_for) {
-            cudaFuncSetAttribute(k_evd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-            set_for = smem;
-        }
+        allow_dyn_smem(reinterpret_cast<const void*>(k_evd));
         const int threads = w <= 32 ? 128 : (w <= 64 ? 256 : kEvdThreads);
         k_evd<<<1, threads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
     }
@@ -531,12 +531,7 @@ void launch_lift_partial(const double* q, size_t n, int wp, int w, const double*
                          const int* imeta, int rmax, double* coords, double* partial,
                          long long row_off, int P, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(w) * rmax * sizeof(double);
-    static size_t set_for = 0;
-    if (smem > 48 * 1024 && smem > set_for) {
-        cudaFuncSetAttribute(k_lift, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        set_for = smem;
-    }
+    allow_dyn_smem(reinterpret_cast<const void*>(k_lift));
     k_lift<<<P, 256, smem, st>>>(q, static_cast<int>(n), wp, w, vkeep, imeta, rmax, coords,
                                  partial, row_off);
     count_launch();

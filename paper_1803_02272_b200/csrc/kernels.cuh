@@ -135,6 +135,10 @@ void launch_hamming(const unsigned long long* packed, size_t count, int words, i
                     double* d, size_t ld, uint32_t* counts, cudaStream_t st);
 
 // ---- misc ------------------------------------------------------------------
+// Opt a kernel into the full shared-memory carve-out once (dynamic limit =
+// 227 KB minus its static shared memory), so static + dynamic may exceed the
+// 48 KB default.
+void allow_dyn_smem(const void* kernel);
 uint64_t kernel_launch_count();
 void count_launch(int k = 1);
 

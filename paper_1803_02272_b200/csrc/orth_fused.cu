@@ -298,12 +298,7 @@ bool launch_wp(double* y, double* out, size_t n_pad, int w, size_t n, double* pa
     const size_t smem = static_cast<size_t>(WP) * ldr * sizeof(double);
     // DMMA apply: ceil(rows / 8) * (WP / 8) tiles over 8 warps, <= 16 per warp
     if (smem > 200 * 1024 || ((rows_max + 7) / 8) * (WP / 8) > 8 * 16) return false;
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(k_orth_fused<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
-        attr = std::max<size_t>(smem, 48 * 1024);
-    }
+    allow_dyn_smem(reinterpret_cast<const void*>(k_orth_fused<WP>));
     static size_t occ_smem = 0;
     static int per_sm = 0;
     if (occ_smem != smem) {

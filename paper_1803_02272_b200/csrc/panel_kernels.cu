@@ -287,12 +287,7 @@ template <int WP>
 void panel_apply_wp(const double* y, const double* rinv, size_t n_pad, double* q, int grid,
                     cudaStream_t st) {
     constexpr size_t smem = static_cast<size_t>(WP) * WP * sizeof(double);
-    static bool set = false;
-    if (!set && smem > 48 * 1024) {
-        cudaFuncSetAttribute(k_panel_apply<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        set = true;
-    }
+    allow_dyn_smem(reinterpret_cast<const void*>(k_panel_apply<WP>));
     k_panel_apply<WP><<<grid, 256, smem, st>>>(y, rinv, n_pad, q);
 }
 
@@ -351,12 +346,7 @@ void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, do
 void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shift, double* rinv,
                      int* flags, cudaStream_t st) {
     const size_t smem = (static_cast<size_t>(wp) * (wp + 1) + wp) * sizeof(double);
-    static size_t set_for = 0;
-    if (smem > set_for) {
-        cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(std::max<size_t>(smem, 48 * 1024)));
-        set_for = std::max<size_t>(smem, 48 * 1024);
-    }
+    allow_dyn_smem(reinterpret_cast<const void*>(k_chol_inv));
     k_chol_inv<<<1, 128, smem, st>>>(w_mat, wp, w, static_cast<double>(n), allow_shift, rinv,
                                      flags);
     count_launch();
