@@ -51,6 +51,14 @@ WORKLOADS = {
 FP64_FALLBACK_TFLOPS = 37.1  # DMMA microbenchmark on this pool (profiles/fp64_peak_r01.txt)
 
 
+def make_distance(ds, wl: str):
+    """Device-resident D of a workload (unsharded): Euclidean (K9) or Hamming (K7)."""
+    cfg, n, k, p, q, seed, f32 = WORKLOADS[wl]
+    if cfg == 5:
+        return ds.matrix_hamming(ds.synth_reads(n, 400, 50, 0.05, seed))
+    return ds.matrix_euclidean(ds.synth_points(cfg, n, seed), store_f32=f32)
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -62,29 +70,34 @@ def measured_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled through NVML during the timed
+    region (a library call per sample — no nvidia-smi process spawned inside
+    the measurement)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.05):
         self.index = index
-        self.samples: list[list[str]] = []
+        self.period = period_s
+        self.samples: list[tuple[float, float, int]] = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self.error = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                for line in out.stdout.strip().splitlines():
-                    self.samples.append([x.strip() for x in line.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            reasons_fn = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                getattr(N, "nvmlDeviceGetCurrentClocksThrottleReasons")
+            while not self._stop.is_set():
+                sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                rs = int(reasons_fn(h))
+                self.samples.append((sm, mx, rs))
+                self._stop.wait(self.period)
+            N.nvmlShutdown()
+        except Exception as e:  # pragma: no cover - reported in the JSON
+            self.error = repr(e)
 
     def __enter__(self):
         self._t.start()
@@ -95,14 +108,16 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self) -> dict:
-        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for s in self.samples for name, b in bits.items() if s[2] & b})
+        out = {"sm_mhz": float(np.median(sm)) if sm else None,
+               "sm_max_mhz": max(s[1] for s in self.samples) if sm else None,
+               "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
+        if self.error:
+            out["error"] = self.error
+        return out
 
 
 def dist_init():
@@ -356,7 +371,7 @@ def b200_arm(args, wl):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))

@@ -135,8 +135,14 @@ void Ctx::end_timed(int kind, cudaEvent_t a) {
 void Ctx::make_events(cudaEvent_t* a, cudaEvent_t* b) {
     *a = *b = nullptr;
     if (!timing) return;
-    DSB_CUDA(cudaEventCreate(a));
-    DSB_CUDA(cudaEventCreate(b));
+    for (cudaEvent_t* e : {a, b}) {
+        if (!event_pool.empty()) {
+            *e = event_pool.back();
+            event_pool.pop_back();
+        } else {
+            DSB_CUDA(cudaEventCreate(e));
+        }
+    }
 }
 
 void Ctx::add_timed(int kind, cudaEvent_t a, cudaEvent_t b) {
@@ -152,8 +158,8 @@ void Ctx::drain_timing() {
         float ms = 0.0f;
         DSB_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
         (t.kind == 1 ? k2_ms : k1_ms) += ms;
-        cudaEventDestroy(t.a);
-        cudaEventDestroy(t.b);
+        event_pool.push_back(t.a);
+        event_pool.push_back(t.b);
     }
     pending.clear();
 }

@@ -89,6 +89,7 @@ public:
     double k2_ms = 0.0, k1_ms = 0.0;
     int last_evd_sweeps = 0, last_orth_shifted = 0;
     std::vector<TimedPair> pending;
+    std::vector<cudaEvent_t> event_pool;
     void begin_timed(int kind, cudaEvent_t* a);
     void end_timed(int kind, cudaEvent_t a);
     // events created (when timing) for a caller that records them itself

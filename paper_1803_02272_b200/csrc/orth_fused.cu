@@ -107,8 +107,6 @@ __global__ void __launch_bounds__(256, 1)
     constexpr int NT = NF * NF;
     constexpr int TPW = (NT + 7) / 8;
     cg::grid_group grid = cg::this_grid();
-    __shared__ double R[WP * WP];   // W, eliminated in place
-    __shared__ double E[WP * WP];   // L^{-1}, then T = R^{-1}
     __shared__ int dropped_s[WP];
     __shared__ double d0s[WP];
     __shared__ double dpiv[WP];
@@ -119,7 +117,9 @@ __global__ void __launch_bounds__(256, 1)
     // the CTA's rows stay in shared memory for all passes, column-major with
     // leading dimension ldr = 4 (mod 16): conflict-free MMA fragments and
     // conflict-free thread-per-row access
-    extern __shared__ double ps[];  // [WP][ldr]
+    extern __shared__ double ps[];  // [WP][ldr], then R [WP*WP], E [WP*WP]
+    double* R = ps + static_cast<size_t>(WP) * ldr;  // W, eliminated in place; then T
+    double* E = R + WP * WP;                         // L^{-1}
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int P = gridDim.x, c = blockIdx.x;
     const size_t nq = n_pad / 4;
@@ -239,41 +239,41 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncthreads();
         {
-            // Q = Y T on the f64 tensor cores: 8x8 output tiles (row tile tm,
-            // column tile tn) spread over the warps, K = WP in steps of 4;
-            // fragments straight from shared memory (ps column-major with
-            // ldr = 4 mod 16: conflict-free A fragments)
+            // Q = Y T on the f64 tensor cores, in place: column c of Q needs
+            // columns k <= c of Y only (T upper triangular), so the 8-column
+            // tiles are produced right to left — each tile's rows are computed
+            // into registers, then written over Y's (no longer needed) columns.
+            // Fragments come straight from shared memory (ps column-major,
+            // ldr = 4 mod 16: conflict-free A fragments).
             constexpr int NFT = WP / 8;
-            constexpr int kMaxT = 16;  // tiles per warp: ceil(rows/8) * NFT / 8 <= 16
-            const int ntm = (nrow + 7) / 8, ntile = ntm * NFT;
-            double acc[kMaxT][2];
+            constexpr int kMaxRT = 16;  // row tiles per warp (rows per CTA <= 1024)
+            const int ntm = (nrow + 7) / 8;
             const int rq = lane >> 2, kq = lane & 3;
+            for (int tn = NFT - 1; tn >= 0; --tn) {
+                double acc[kMaxRT][2];
 #pragma unroll
-            for (int j = 0; j < kMaxT; ++j) {
-                acc[j][0] = acc[j][1] = 0.0;
-                const int t = warp + 8 * j;
-                if (t < ntile) {
-                    const int tm = t / NFT, tn = t % NFT;
-#pragma unroll
-                    for (int kk = 0; kk < WP / 4; ++kk) {
-                        const double av = ps[(4 * kk + kq) * ldr + 8 * tm + rq];
-                        const double bv = R[(4 * kk + kq) * WP + 8 * tn + rq];
-                        dmma884(acc[j][0], acc[j][1], av, bv);
+                for (int j = 0; j < kMaxRT; ++j) {
+                    acc[j][0] = acc[j][1] = 0.0;
+                    const int tm = warp + 8 * j;
+                    if (tm < ntm) {
+                        for (int kk = 0; kk < 2 * tn + 2; ++kk) {  // k <= 8 tn + 7
+                            const double av = ps[(4 * kk + kq) * ldr + 8 * tm + rq];
+                            const double bv = R[(4 * kk + kq) * WP + 8 * tn + rq];
+                            dmma884(acc[j][0], acc[j][1], av, bv);
+                        }
                     }
                 }
-            }
-            __syncthreads();
+                __syncthreads();
 #pragma unroll
-            for (int j = 0; j < kMaxT; ++j) {
-                const int t = warp + 8 * j;
-                if (t < ntile) {
-                    const int tm = t / NFT, tn = t % NFT;
+                for (int j = 0; j < kMaxRT; ++j) {
+                    const int tm = warp + 8 * j;
                     const int row = 8 * tm + rq, col = 8 * tn + 2 * kq;
-                    if (row < nrow) {
+                    if (tm < ntm && row < nrow) {
                         ps[col * ldr + row] = acc[j][0];
                         ps[(col + 1) * ldr + row] = acc[j][1];
                     }
                 }
+                __syncthreads();
             }
         }
         __syncthreads();
@@ -295,9 +295,9 @@ bool launch_wp(double* y, double* out, size_t n_pad, int w, size_t n, double* pa
     const size_t nq = n_pad / 4;
     const int rows_max = static_cast<int>(((nq + P - 1) / P) * 4);
     const int ldr = (rows_max + 15) / 16 * 16 + 4;
-    const size_t smem = static_cast<size_t>(WP) * ldr * sizeof(double);
-    // DMMA apply: ceil(rows / 8) * (WP / 8) tiles over 8 warps, <= 16 per warp
-    if (smem > 200 * 1024 || ((rows_max + 7) / 8) * (WP / 8) > 8 * 16) return false;
+    const size_t smem = (static_cast<size_t>(WP) * ldr + 2 * WP * WP) * sizeof(double);
+    // DMMA apply: ceil(rows / 8) row tiles over 8 warps, <= 16 per warp
+    if (smem > 220 * 1024 || (rows_max + 7) / 8 > 8 * 16) return false;
     allow_dyn_smem(reinterpret_cast<const void*>(k_orth_fused<WP>));
     static size_t occ_smem = 0;
     static int per_sm = 0;
@@ -332,6 +332,10 @@ bool launch_orth_fused(double* y, double* t, double* out, size_t n_pad, int wp, 
         case 16: ok = launch_wp<16>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
         case 24: ok = launch_wp<24>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
         case 32: ok = launch_wp<32>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        case 40: ok = launch_wp<40>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        case 48: ok = launch_wp<48>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        case 56: ok = launch_wp<56>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        case 64: ok = launch_wp<64>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
         default: return false;
     }
     if (ok) count_launch();

@@ -163,12 +163,26 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     int* flags = static_cast<int*>(c.scratch("flags", 64));
     DSB_CUDA(cudaMemsetAsync(flags, 0, 64, c.stream));
 
-    // Omega: host-generated (bit-identical to the reference), relayout on device
+    // Omega: host-generated (bit-identical to the reference), relayout on the
+    // device once per (seed, n, w) and kept resident (a pure function of the
+    // seed); every solve starts from a device copy of it
     {
-        const double* om = omega_host(seed, n, w);
-        double* stage = static_cast<double*>(c.scratch("omega_rm", n * w * sizeof(double)));
-        c.h2d_copy(stage, om, n * w * sizeof(double));
-        launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, P0, c.stream);
+        static uint64_t key_seed = 0;
+        static size_t key_n = 0, key_w = 0, key_np = 0;
+        static bool key_ok = false;
+        double* cached = static_cast<double*>(c.scratch("omega_panel", pbytes));
+        if (!key_ok || key_seed != seed || key_n != n || key_w != w || key_np != n_pad) {
+            const double* om = omega_host(seed, n, w);
+            double* stage = static_cast<double*>(c.scratch("omega_rm", n * w * sizeof(double)));
+            c.h2d_copy(stage, om, n * w * sizeof(double));
+            launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, cached, c.stream);
+            key_seed = seed;
+            key_n = n;
+            key_w = w;
+            key_np = n_pad;
+            key_ok = true;
+        }
+        DSB_CUDA(cudaMemcpyAsync(P0, cached, pbytes, cudaMemcpyDeviceToDevice, c.stream));
     }
 
     auto product = [&](const double* x, double* y) {
@@ -181,7 +195,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     };
     // CholeskyQR3 with shift/drop handling: y -> t -> y -> out
     auto orth = [&](double* y, double* t, double* out) {
-        if (wp <= 32 &&
+        if (wp <= 64 &&
             launch_orth_fused(y, t, out, n_pad, wp, wi, n, psmall, wmat, flags, c.sms, c.stream))
             return;
         launch_panel_dot(y, y, n_pad, wp, psmall, wmat, c.sms, c.stream);

@@ -15,9 +15,10 @@ ap.add_argument("--workload", default="C2")
 ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--steps", type=int, default=1)
 a = ap.parse_args()
-cfg, n, k, p, q, seed, f32 = bench.WORKLOADS[a.workload]
+wl = a.workload
+cfg, n, k, p, q, seed, f32 = bench.WORKLOADS[wl]
 ds.set_device(0)
-D = ds.matrix_euclidean(ds.synth_points(cfg, n, seed), store_f32=f32)
+D = bench.make_distance(ds, wl)
 for _ in range(a.warmup + a.steps):
     e = ds.embed(ds.gram(D), rank=k, oversampling=p, power_iters=q, seed=seed)
 st = ds.stats_get()

@@ -9,7 +9,7 @@ import paper_1803_02272_b200 as ds  # noqa: E402
 wl = sys.argv[1] if len(sys.argv) > 1 else "C2"
 cfg, n, k, p, q, seed, f32 = bench.WORKLOADS[wl]
 ds.set_device(0)
-D = ds.matrix_euclidean(ds.synth_points(cfg, n, seed), store_f32=f32)
+D = bench.make_distance(ds, wl)
 for _ in range(3):
     e = ds.embed(ds.gram(D), rank=k, oversampling=p, power_iters=q, seed=seed)
 for it in range(3):
