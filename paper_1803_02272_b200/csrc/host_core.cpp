@@ -281,9 +281,36 @@ void upload_rows(Store& s, const void* host, size_t host_ld_elems) {
     Ctx& c = Ctx::get();
     const size_t esz = s.dt == DType::F64 ? 8 : 4;
     if (s.rows == 0 || s.cols == 0) return;
-    DSB_CUDA(cudaMemcpy2DAsync(s.buf->p, s.ld * esz, host, host_ld_elems * esz, s.cols * esz,
-                               s.rows, cudaMemcpyHostToDevice, c.stream));
-    c.h2d += s.rows * s.cols * esz;
+    // Large uploads are split into row chunks alternated over the library
+    // stream and a side stream (two DMA engines in flight), then joined.
+    const size_t bytes = s.rows * s.cols * esz;
+    const size_t nchunk = bytes >= (size_t(64) << 20) ? 8 : 1;
+    if (nchunk == 1) {
+        DSB_CUDA(cudaMemcpy2DAsync(s.buf->p, s.ld * esz, host, host_ld_elems * esz, s.cols * esz,
+                                   s.rows, cudaMemcpyHostToDevice, c.stream));
+    } else {
+        static cudaStream_t side = nullptr;
+        static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+        if (!side) {
+            DSB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            DSB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+            DSB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        }
+        DSB_CUDA(cudaEventRecord(ev_fork, c.stream));
+        DSB_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+        for (size_t k = 0; k < nchunk; ++k) {
+            const size_t r0 = s.rows * k / nchunk, r1 = s.rows * (k + 1) / nchunk;
+            if (r1 == r0) continue;
+            cudaStream_t st = (k & 1) ? side : c.stream;
+            DSB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(s.buf->p) + r0 * s.ld * esz, s.ld * esz,
+                                       static_cast<const char*>(host) + r0 * host_ld_elems * esz,
+                                       host_ld_elems * esz, s.cols * esz, r1 - r0,
+                                       cudaMemcpyHostToDevice, st));
+        }
+        DSB_CUDA(cudaEventRecord(ev_join, side));
+        DSB_CUDA(cudaStreamWaitEvent(c.stream, ev_join, 0));
+    }
+    c.h2d += bytes;
     if (s.ld > s.cols)  // zero the pitch padding so full-row reads stay clean
         DSB_CUDA(cudaMemset2DAsync(static_cast<char*>(s.buf->p) + s.cols * esz, s.ld * esz, 0,
                                    (s.ld - s.cols) * esz, s.rows, c.stream));
