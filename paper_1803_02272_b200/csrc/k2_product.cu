@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "device_utils.cuh"
@@ -52,10 +53,12 @@ constexpr int kt_cols() {
     return 128 / static_cast<int>(sizeof(TD));
 }
 
-template <int WP, typename TD, int CW>
+// A stage holds KS boxes of D (BM rows x 128 bytes each, KS*kt columns) and
+// the matching KS*kt-row panel chunk.
+template <int WP, typename TD, int CW, int KS>
 constexpr int stage_bytes() {
-    // D tile (1024-aligned for the 128B swizzle) + panel chunk, rounded to 1024
-    return ((tile_bytes<CW>() + kt_cols<TD>() * WP * 8) + 1023) / 1024 * 1024;
+    // D boxes (1024-aligned for the 128B swizzle) + panel chunk, rounded to 1024
+    return ((KS * tile_bytes<CW>() + KS * kt_cols<TD>() * WP * 8) + 1023) / 1024 * 1024;
 }
 
 __device__ __forceinline__ long long chunk_begin(long long total, long long c, long long P) {
@@ -74,15 +77,15 @@ __device__ __forceinline__ double load_a(const unsigned char* tile, int r, int k
     }
 }
 
-template <int WP, typename TD, bool SQUARE, int CW>
+template <int WP, typename TD, bool SQUARE, int CW, int KS>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
     k2_product(const __grid_constant__ CUtensorMap tmD, const double* __restrict__ X, int nk,
                long long total, double* __restrict__ part, int maxseg, int stages) {
     constexpr int KT = kt_cols<TD>();
     constexpr int K4 = KT / 4;
     constexpr int NF = WP / 8;
-    constexpr int XB = KT * WP * 8;
-    constexpr int SB = stage_bytes<WP, TD, CW>();
+    constexpr int XB = KS * KT * WP * 8;
+    constexpr int SB = stage_bytes<WP, TD, CW, KS>();
     constexpr int BM = bm_of<CW>();
     constexpr int kTileBytes = tile_bytes<CW>();
 
@@ -116,9 +119,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
                 if (t - t0 >= stages) mbar_wait(&empty[s], ph ^ 1);
                 const int b = static_cast<int>(t / nk), kt = static_cast<int>(t % nk);
                 unsigned char* st = smem + static_cast<size_t>(s) * SB;
-                mbar_arrive_expect_tx(&full[s], kTileBytes + XB);
-                tma_load_2d(st, &tmD, kt * KT, b * BM, &full[s]);
-                bulk_load(st + kTileBytes, X + static_cast<size_t>(kt) * KT * WP, XB, &full[s]);
+                mbar_arrive_expect_tx(&full[s], KS * kTileBytes + XB);
+#pragma unroll
+                for (int kb = 0; kb < KS; ++kb)
+                    tma_load_2d(st + kb * kTileBytes, &tmD, (kt * KS + kb) * KT, b * BM, &full[s]);
+                bulk_load(st + KS * kTileBytes, X + static_cast<size_t>(kt) * KS * KT * WP, XB,
+                          &full[s]);
                 if (++s == stages) {
                     s = 0;
                     ph ^= 1;
@@ -167,13 +173,14 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
             }
             mbar_wait(&full[s], ph);
             const unsigned char* tile = smem + static_cast<size_t>(s) * SB;
-            const double* xs = reinterpret_cast<const double*>(tile + kTileBytes);
+            const double* xs = reinterpret_cast<const double*>(tile + KS * kTileBytes);
 #pragma unroll
-            for (int kk = 0; kk < K4; ++kk) {
+            for (int kk = 0; kk < KS * K4; ++kk) {
                 double a[2];
 #pragma unroll
                 for (int fm = 0; fm < 2; ++fm) {
-                    const double v = load_a<TD>(tile, m0 + 8 * fm + rq, 4 * kk + kq);
+                    const double v = load_a<TD>(tile + (kk / K4) * kTileBytes, m0 + 8 * fm + rq,
+                                                4 * (kk % K4) + kq);
                     a[fm] = SQUARE ? v * v : v;
                 }
 #pragma unroll
@@ -239,17 +246,26 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-template <int WP, typename TD, bool SQ, int CW>
-void run_product(const CUtensorMap* tmap, const K2Plan& p, const double* x, double* part,
-                 cudaStream_t st) {
+template <int WP, typename TD, bool SQ, int CW, int KS>
+void run_product_ks(const CUtensorMap* tmap, const K2Plan& p, const double* x, double* part,
+                    cudaStream_t st) {
     static size_t set_for = 0;  // per instantiation
     if (p.smem > set_for) {
-        cudaFuncSetAttribute(k2_product<WP, TD, SQ, CW>,
+        cudaFuncSetAttribute(k2_product<WP, TD, SQ, CW, KS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
         set_for = p.smem;
     }
-    k2_product<WP, TD, SQ, CW><<<p.grid, (CW + 1) * 32, p.smem, st>>>(*tmap, x, p.nk, p.total,
-                                                                      part, p.maxseg, p.stages);
+    k2_product<WP, TD, SQ, CW, KS><<<p.grid, (CW + 1) * 32, p.smem, st>>>(
+        *tmap, x, p.nk, p.total, part, p.maxseg, p.stages);
+}
+
+template <int WP, typename TD, bool SQ, int CW>
+void run_product(const CUtensorMap* tmap, const K2Plan& p, const double* x, double* part,
+                 cudaStream_t st) {
+    if (p.ks == 2)
+        run_product_ks<WP, TD, SQ, CW, 2>(tmap, p, x, part, st);
+    else
+        run_product_ks<WP, TD, SQ, CW, 1>(tmap, p, x, part, st);
 }
 
 template <int WP, int CW>
@@ -277,6 +293,18 @@ void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
 
 int k2_warps(int wp) { return wp <= 64 ? 16 : 8; }
 
+// 128-byte D boxes per pipeline stage (DSB_K2_KS overrides, for sweeps)
+int k2_ks(int wp, DType dt) {
+    (void)wp;
+    (void)dt;
+    static const int env = [] {
+        const char* e = std::getenv("DSB_K2_KS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (env == 1 || env == 2) return env;
+    return 2;  // halves the per-stage barrier work; +1-4 % DMMA util (tools/k2_sweep.py)
+}
+
 K2Plan k2_plan(size_t n, int wp, DType dt, int sms) { return k2_plan_rect(n, n, wp, dt, sms); }
 
 K2Plan k2_plan_rect(size_t n, size_t ncols, int wp, DType dt, int sms) {
@@ -286,11 +314,12 @@ K2Plan k2_plan_rect(size_t n, size_t ncols, int wp, DType dt, int sms) {
     p.bm = 16 * p.cw;
     p.n = static_cast<int>(n);
     p.nb = static_cast<int>((n + p.bm - 1) / p.bm);
-    const int kt = dt == DType::F64 ? 16 : 32;
+    p.ks = k2_ks(wp, dt);
+    const int kt = (dt == DType::F64 ? 16 : 32) * p.ks;  // columns per stage
     p.nk = static_cast<int>((ncols + kt - 1) / kt);
     p.total = static_cast<long long>(p.nb) * p.nk;
     p.grid = static_cast<int>(std::min<long long>(sms, p.total));
-    const int sb = ((p.bm * 128 + kt * wp * 8) + 1023) / 1024 * 1024;
+    const int sb = ((p.ks * p.bm * 128 + kt * wp * 8) + 1023) / 1024 * 1024;
     const size_t budget = 222 * 1024;
     int stages = static_cast<int>((budget - 1024 - 256) / sb);
     stages = std::max(2, std::min(stages, 8));

@@ -60,6 +60,7 @@ struct K2Plan {
     int n = 0, nb = 0, nk = 0;
     long long total = 0;
     int grid = 0, maxseg = 0, stages = 0;
+    int ks = 1;             // 128-byte D boxes per stage
     size_t smem = 0;
     size_t part_elems = 0;   // doubles needed for the partial workspace
 };
@@ -70,6 +71,7 @@ K2Plan k2_plan_rect(size_t rows, size_t ncols, int wp, DType dt, int sms);
 // then rank-3 centering).
 // e0/e1 (may be null) are recorded around the streaming kernel only
 int k2_warps(int wp);
+int k2_ks(int wp, DType dt);
 void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
                double* part, const double* row_mean, const double* scalars,
                const double* colsums, double* y, size_t n_pad, cudaStream_t st,
