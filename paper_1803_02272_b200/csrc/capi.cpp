@@ -561,6 +561,8 @@ void divscope_stats_get(divscope_stats* out) {
         out->d2h_bytes = c.d2h;
         out->last_evd_sweeps = c.last_evd_sweeps;
         out->last_orth_shifted = c.last_orth_shifted;
+        out->last_power_iters = c.last_power_iters;
+        out->reserved0 = 0;
     } catch (...) {
     }
 }

@@ -80,7 +80,9 @@ __device__ __forceinline__ double load_a(const unsigned char* tile, int r, int k
 template <int WP, typename TD, bool SQUARE, int CW, int KS>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
     k2_product(const __grid_constant__ CUtensorMap tmD, const double* __restrict__ X, int nk,
-               long long total, double* __restrict__ part, int maxseg, int stages) {
+               long long total, double* __restrict__ part, int maxseg, int stages,
+               const int* __restrict__ skip) {
+    if (skip && *skip) return;  // power-iteration batches past convergence
     constexpr int KT = kt_cols<TD>();
     constexpr int K4 = KT / 4;
     constexpr int NF = WP / 8;
@@ -218,7 +220,9 @@ template <int WP, int BM>
 __global__ void __launch_bounds__(256)
     k2_reduce(const double* __restrict__ part, int maxseg, int nk, long long total, int P, int n,
               int mode, const double* __restrict__ row_mean, const double* __restrict__ scalars,
-              const double* __restrict__ colsums, double* __restrict__ y) {
+              const double* __restrict__ colsums, double* __restrict__ y,
+              const int* __restrict__ skip) {
+    if (skip && *skip) return;
     constexpr int kRows = 32;  // rows of the BM-row block handled by this CTA
     const int b = blockIdx.x / (BM / kRows);
     const int r0 = (blockIdx.x % (BM / kRows)) * kRows;
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(256)
 
 template <int WP, typename TD, bool SQ, int CW, int KS>
 void run_product_ks(const CUtensorMap* tmap, const K2Plan& p, const double* x, double* part,
-                    cudaStream_t st) {
+                    cudaStream_t st, const int* skip) {
     static size_t set_for = 0;  // per instantiation
     if (p.smem > set_for) {
         cudaFuncSetAttribute(k2_product<WP, TD, SQ, CW, KS>,
@@ -256,37 +260,38 @@ void run_product_ks(const CUtensorMap* tmap, const K2Plan& p, const double* x, d
         set_for = p.smem;
     }
     k2_product<WP, TD, SQ, CW, KS><<<p.grid, (CW + 1) * 32, p.smem, st>>>(
-        *tmap, x, p.nk, p.total, part, p.maxseg, p.stages);
+        *tmap, x, p.nk, p.total, part, p.maxseg, p.stages, skip);
 }
 
 template <int WP, typename TD, bool SQ, int CW>
 void run_product(const CUtensorMap* tmap, const K2Plan& p, const double* x, double* part,
-                 cudaStream_t st) {
+                 cudaStream_t st, const int* skip) {
     if (p.ks == 2)
-        run_product_ks<WP, TD, SQ, CW, 2>(tmap, p, x, part, st);
+        run_product_ks<WP, TD, SQ, CW, 2>(tmap, p, x, part, st, skip);
     else
-        run_product_ks<WP, TD, SQ, CW, 1>(tmap, p, x, part, st);
+        run_product_ks<WP, TD, SQ, CW, 1>(tmap, p, x, part, st, skip);
 }
 
 template <int WP, int CW>
 void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
                double* part, const double* row_mean, const double* scalars,
-               const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1) {
+               const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
+               const int* skip) {
     if (e0) cudaEventRecord(e0, st);
     if (dt == DType::F64) {
         if (mode)
-            run_product<WP, double, true, CW>(tmap, p, x, part, st);
+            run_product<WP, double, true, CW>(tmap, p, x, part, st, skip);
         else
-            run_product<WP, double, false, CW>(tmap, p, x, part, st);
+            run_product<WP, double, false, CW>(tmap, p, x, part, st, skip);
     } else {
         if (mode)
-            run_product<WP, float, true, CW>(tmap, p, x, part, st);
+            run_product<WP, float, true, CW>(tmap, p, x, part, st, skip);
         else
-            run_product<WP, float, false, CW>(tmap, p, x, part, st);
+            run_product<WP, float, false, CW>(tmap, p, x, part, st, skip);
     }
     if (e1) cudaEventRecord(e1, st);
     k2_reduce<WP, bm_of<CW>()><<<p.nb * (bm_of<CW>() / 32), 256, 0, st>>>(
-        part, p.maxseg, p.nk, p.total, p.grid, p.n, mode, row_mean, scalars, colsums, y);
+        part, p.maxseg, p.nk, p.total, p.grid, p.n, mode, row_mean, scalars, colsums, y, skip);
 }
 
 }  // namespace
@@ -339,13 +344,13 @@ K2Plan k2_plan_rect(size_t n, size_t ncols, int wp, DType dt, int sms) {
 void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
                double* part, const double* row_mean, const double* scalars,
                const double* colsums, double* y, size_t n_pad, cudaStream_t st, cudaEvent_t e0,
-               cudaEvent_t e1) {
+               cudaEvent_t e1, const int* skip) {
     (void)n_pad;
     switch (p.wp) {
 #define DSB_WP(W)                                                                               \
     case W:                                                                                     \
         launch_wp<W, (W <= 64 ? 16 : 8)>(tmap, dt, mode, p, x, part, row_mean, scalars, colsums, \
-                                         y, st, e0, e1);                                         \
+                                         y, st, e0, e1, skip);                                   \
         break;
         DSB_WP(8)
         DSB_WP(16)

@@ -75,7 +75,7 @@ int k2_ks(int wp, DType dt);
 void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, const double* x,
                double* part, const double* row_mean, const double* scalars,
                const double* colsums, double* y, size_t n_pad, cudaStream_t st,
-               cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr);
+               cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr, const int* skip = nullptr);
 
 // ---- panel kernels (n_pad x WP, k4-interleaved) -----------------------------
 int panel_grid(size_t n_pad, int sms);
@@ -89,6 +89,16 @@ void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_
 // out (wp x wp) = A^T B (deterministic 2-level)
 void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, double* partial,
                       double* out, int sms, cudaStream_t st);
+// stable_rank power iteration, device side (ref rsvd.cpp:160-176): state =
+// {sigma, norm, done, zero, iters, active}; norm of Y column 0, v = w / norm,
+// convergence |norm - sigma| <= 1e-13 norm.
+struct SrState {
+    double sigma, norm;
+    int done, zero, iters, active;
+};
+void launch_sr_step(const double* y, size_t n, int wp, double* partial, SrState* state, double* x,
+                    int sms, cudaStream_t st);
+
 // CholQR step on W = Y^T Y: rinv = R^{-1} with breakdown handling (shift /
 // drop, K3); flags[0] |= 1 when shifted.
 void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shift, double* rinv,

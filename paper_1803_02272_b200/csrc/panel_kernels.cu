@@ -291,6 +291,62 @@ void panel_apply_wp(const double* y, const double* rinv, size_t n_pad, double* q
     k_panel_apply<WP><<<grid, 256, smem, st>>>(y, rinv, n_pad, q);
 }
 
+
+// ---- stable_rank power iteration step (ref rsvd.cpp:160-176) --------------
+// partial[b] = sum of y(i,0)^2 over CTA b's rows (fixed order)
+__global__ void __launch_bounds__(256) k_sr_norm_partial(const double* __restrict__ y, size_t n,
+                                                         int wp, const SrState* __restrict__ st,
+                                                         double* __restrict__ partial) {
+    if (st->done) return;
+    __shared__ double red[8];
+    const size_t i0 = n * blockIdx.x / gridDim.x, i1 = n * (blockIdx.x + 1) / gridDim.x;
+    double s = 0.0;
+    for (size_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const double v = y[pidx(i, 0, wp)];
+        s += v * v;
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += red[k];
+        partial[blockIdx.x] = t;
+    }
+}
+
+// one thread: norm, restart flag, convergence (same tests as the reference)
+__global__ void k_sr_update(const double* __restrict__ partial, int P, SrState* __restrict__ st) {
+    if (st->done) {
+        st->active = 0;
+        return;
+    }
+    double ss = 0.0;
+    for (int b = 0; b < P; ++b) ss += partial[b];
+    const double norm = sqrt(ss);
+    st->active = 1;
+    st->iters += 1;
+    st->norm = norm;
+    if (norm == 0.0) {  // start vector in the kernel: the host redraws it
+        st->zero = 1;
+        st->done = 1;
+        return;
+    }
+    if (st->sigma != 0.0 && fabs(norm - st->sigma) <= 1e-13 * norm) st->done = 1;
+    st->sigma = norm;
+}
+
+// v = w / norm (column 0; the other panel columns stay zero)
+__global__ void __launch_bounds__(256) k_sr_scale(const double* __restrict__ y, size_t n, int wp,
+                                                  const SrState* __restrict__ st,
+                                                  double* __restrict__ x) {
+    if (!st->active || st->zero) return;
+    const double norm = st->norm;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        x[pidx(i, 0, wp)] = y[pidx(i, 0, wp)] / norm;
+}
+
 }  // namespace
 
 int panel_grid(size_t n_pad, int sms) {
@@ -371,4 +427,15 @@ void launch_panel_apply(const double* y, const double* rinv, size_t n_pad, int w
     count_launch();
 }
 
+}  // namespace dsb
+
+namespace dsb {
+void launch_sr_step(const double* y, size_t n, int wp, double* partial, SrState* state, double* x,
+                    int sms, cudaStream_t st) {
+    const int P = sms;
+    k_sr_norm_partial<<<P, 256, 0, st>>>(y, n, wp, state, partial);
+    k_sr_update<<<1, 1, 0, st>>>(partial, P, state);
+    k_sr_scale<<<sms, 256, 0, st>>>(y, n, wp, state, x);
+    count_launch(3);
+}
 }  // namespace dsb

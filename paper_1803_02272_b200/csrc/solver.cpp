@@ -430,6 +430,8 @@ void matrix_to_host(const Matrix& m, double* out) {
         }
 }
 
+constexpr int kSrMaxIters = 20000;  // ref rsvd.cpp:160
+
 double stable_rank(const Matrix& g) {
     Ctx& c = Ctx::get();
     std::lock_guard<std::recursive_mutex> lk(c.mu);
@@ -463,8 +465,6 @@ double stable_rank(const Matrix& g) {
     const int pg = panel_grid(n_pad, c.sms);
     double* psmall = static_cast<double*>(c.scratch("panel_part", static_cast<size_t>(pg) * wp * wp * 8 + 64));
     double* colsums = static_cast<double*>(c.scratch("colsums", 2 * wp * 8));
-    double* wmat = static_cast<double*>(c.scratch("wmat", wp * wp * 8));
-    double* scale = static_cast<double*>(c.scratch("sr_scale", wp * wp * 8));
     double* stage = static_cast<double*>(c.scratch("sr_stage", n * 8));
     // ref rsvd.cpp:157-176: v ~ fill_gaussian(mt19937_64(0x5eed)), normalized
     std::mt19937_64 eng(0x5eedULL);
@@ -480,35 +480,46 @@ double stable_rank(const Matrix& g) {
         c.h2d_copy(stage, v.data(), n * 8);
         launch_panel_from_rowmajor(stage, n, 1, wp, n_pad, X, c.stream);
     };
+    // The loop runs on the device in batches: K2 (skipped once converged),
+    // then launch_sr_step (norm, restart flag, convergence test, v = w/norm).
+    // The host reads the state once per batch.
+    SrState* dstate = static_cast<SrState*>(c.scratch("sr_state", sizeof(SrState)));
+    static SrState* hstate = nullptr;
+    if (!hstate) DSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hstate), sizeof(SrState)));
+    double* npart = static_cast<double*>(c.scratch("sr_part", static_cast<size_t>(c.sms) * 8));
+    auto reset_state = [&](int iters) {
+        *hstate = SrState{0.0, 0.0, 0, 0, iters, 0};
+        DSB_CUDA(cudaMemcpyAsync(dstate, hstate, sizeof(SrState), cudaMemcpyHostToDevice, c.stream));
+        DSB_CUDA(cudaStreamSynchronize(c.stream));
+    };
     load_v(true);
-    std::vector<double> hs(wp * wp, 0.0);
+    reset_state(0);
     double sigma = 0.0;
-    for (int it = 0; it < 20000; ++it) {
-        if (mode) launch_colsums(X, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
-        cudaEvent_t e0, e1;
-        c.make_events(&e0, &e1);
-        launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, X, part, row_mean, scal_dev, colsums, Y,
-                  n_pad, c.stream, e0, e1);
-        c.add_timed(1, e0, e1);
-        launch_panel_dot(Y, Y, n_pad, wp, psmall, wmat, c.sms, c.stream);
-        double w00 = 0.0;
-        c.d2h_copy(&w00, wmat, 8);
-        const double norm = std::sqrt(w00);
-        if (norm == 0.0) {
+    int batch = 8;
+    for (;;) {
+        const int todo = std::min(batch, kSrMaxIters - hstate->iters);
+        if (todo <= 0) break;
+        for (int k = 0; k < todo; ++k) {
+            if (mode) launch_colsums(X, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            c.make_events(&e0, &e1);
+            launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, X, part, row_mean, scal_dev, colsums,
+                      Y, n_pad, c.stream, e0, e1, &dstate->done);
+            c.add_timed(1, e0, e1);
+            launch_sr_step(Y, n, wp, npart, dstate, X, c.sms, c.stream);
+        }
+        DSB_CUDA(cudaMemcpyAsync(hstate, dstate, sizeof(SrState), cudaMemcpyDeviceToHost, c.stream));
+        DSB_CUDA(cudaStreamSynchronize(c.stream));
+        if (hstate->zero) {  // ref rsvd.cpp:163-168: redraw, sigma = 0, continue
             load_v(true);
-            sigma = 0.0;
+            reset_state(hstate->iters);
             continue;
         }
-        // v = w / norm
-        hs[0] = 1.0 / norm;
-        c.h2d_copy(scale, hs.data(), wp * wp * 8);
-        launch_panel_apply(Y, scale, n_pad, wp, X, c.stream);
-        if (sigma != 0.0 && std::abs(norm - sigma) <= 1e-13 * norm) {
-            sigma = norm;
-            break;
-        }
-        sigma = norm;
+        sigma = hstate->sigma;
+        if (hstate->done) break;
+        batch = 32;
     }
+    c.last_power_iters = hstate->iters;
     c.sync();
     return fro2 / (sigma * sigma);
 }

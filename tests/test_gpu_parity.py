@@ -348,6 +348,27 @@ def test_stable_rank(ds):
         ds.Status.ERR_ZERO_MATRIX
 
 
+def test_stable_rank_lazy_gram_matches_oracle(ds, oracle):
+    # device-side power iteration (batched, convergence on the device) on a
+    # lazy gram vs the reference loop over the materialized gram
+    pts = ds.synth_points(1, 300, 11)
+    d = oracle.euclidean_matrix(pts)
+    st, g = oracle.gram(d)
+    assert st == 0
+    st, want = oracle.stable_rank(g)
+    assert st == 0
+    got = ds.stable_rank(ds.gram(ds.matrix_from_host(d)))
+    assert got == pytest.approx(want, rel=1e-10)
+    # explicit matrix with a slowly converging spectrum (many batches)
+    lam = np.linspace(1.0, 0.9, 40)
+    q, _ = np.linalg.qr(np.random.default_rng(5).standard_normal((40, 40)))
+    a = (q * lam) @ q.T
+    a = 0.5 * (a + a.T)
+    st, want = oracle.stable_rank(a)
+    assert st == 0
+    assert ds.stable_rank(ds.matrix_from_host(a)) == pytest.approx(want, rel=1e-8)
+
+
 # ---------------------------------------------------------------- DVS
 
 def test_dvs_round_trip(ds, tmp_path):
