@@ -1,0 +1,100 @@
+// tcgen05 (5th-generation tensor core) helpers for sm_100a: TMEM allocation,
+// shared-memory matrix descriptors, the kind::i8 MMA, commit and TMEM loads.
+//
+// Operand tiles are stored K-major without swizzle ("interleaved" canonical
+// layout): a core matrix is 8 rows x 16 bytes (128 contiguous bytes); the two
+// 16-byte K halves of a 32-byte K slice are LBO = 128 bytes apart and
+// consecutive 8-row groups SBO = 256 bytes apart, i.e. a (rows x 32 byte)
+// tile is [rows/8][2][8][16] bytes. Row r, byte k of a tile lives at
+//   (r / 8) * 256 + (k / 16) * 128 + (r % 8) * 16 + k % 16.
+#pragma once
+
+#include <cstdint>
+
+#include "device_utils.cuh"
+
+namespace dsb {
+
+__host__ __device__ __forceinline__ uint32_t umma_tile_off(uint32_t r, uint32_t k) {
+    return (r >> 3) * 256u + (k >> 4) * 128u + (r & 7u) * 16u + (k & 15u);
+}
+
+// Shared-memory descriptor, K-major, SWIZZLE_NONE, LBO 128 B, SBO 256 B,
+// descriptor version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc_k_interleave(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>(128u >> 4) << 16;  // leading byte offset (K direction)
+    d |= static_cast<uint64_t>(256u >> 4) << 32;  // stride byte offset (8-row groups)
+    d |= static_cast<uint64_t>(1) << 46;          // version
+    return d;                                     // base offset 0, layout type 0
+}
+
+// Instruction descriptor for kind::i8: D s32, A u8 (a_signed = 0) or s8,
+// B s8, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t umma_idesc_i8(int n, bool a_signed, bool b_signed) {
+    return (2u << 4)                                  // c_format = S32
+           | ((a_signed ? 1u : 0u) << 7)              // a_format
+           | ((b_signed ? 1u : 0u) << 10)             // b_format
+           | (static_cast<uint32_t>(n >> 3) << 17)    // N >> 3
+           | (static_cast<uint32_t>(128 >> 4) << 24); // M >> 4
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, int accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// All prior tcgen05 ops of this thread arrive on `bar` when complete.
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// one full warp; writes the TMEM base address to *dst (shared)
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+                 : "memory");
+}
+
+// 32 consecutive 32-bit columns of this thread's TMEM lane (warp w reads
+// lanes 32 (w % 4) .. +31; taddr carries the lane in bits 16..31).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+}  // namespace dsb
