@@ -237,6 +237,11 @@ divscope_status divscope_synth_reads(size_t count, size_t length, size_t ancesto
 
 /* ---- device / instrumentation (NEW) ------------------------------------- */
 
+/* NEW. Product-pass kernel: 0 = auto (int8 slice product on the integer
+ * tensor cores for lazy grams with rank + oversampling <= 64 and n >= 4096,
+ * else fp64 DMMA), 1 = fp64 DMMA only, 2 = int8 whenever supported. */
+divscope_status divscope_set_product_path(int mode);
+
 /* Select the CUDA device used by this process (default: current device). */
 divscope_status divscope_set_device(int device);
 

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from pathlib import Path
 from typing import Sequence
 
@@ -29,11 +30,11 @@ __all__ = [
     "matrix_from_host", "matrix_from_host_f32", "matrix_read", "matrix_euclidean",
     "matrix_hamming", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
     "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
-    "stats_enable_timing", "stats_reset", "stats_get", "set_device", "LIB_PATH",
+    "stats_enable_timing", "stats_reset", "set_product_path", "stats_get", "set_device", "LIB_PATH",
     "fp64_tensor_peak_tflops", "stream_ptr",
 ]
 
-LIB_PATH = Path(__file__).resolve().parent / "libdivscope_b200.so"
+LIB_PATH = Path(os.environ.get("DSB_LIB_OVERRIDE") or Path(__file__).resolve().parent / "libdivscope_b200.so")
 
 
 class Status(enum.IntEnum):
@@ -145,6 +146,7 @@ def _load() -> C.CDLL:
         "divscope_matrix_from_host_rows_f32": ([_fp, _sz, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
         "divscope_matrix_euclidean_rows": ([_dp, _sz, _sz, C.c_int, _sz, _sz, C.POINTER(_vp)], _st),
         "divscope_stats_enable_timing": ([C.c_int], None),
+        "divscope_set_product_path": ([C.c_int], C.c_int),
         "divscope_stats_reset": ([], None),
         "divscope_stats_get": ([C.POINTER(Stats)], None),
         "divscope_stream": ([], _vp),
@@ -473,6 +475,11 @@ def matrix_euclidean_rows(points: np.ndarray, row_begin: int, row_end: int,
 
 def set_device(device: int) -> None:
     _check(lib.divscope_set_device(device))
+
+
+def set_product_path(mode: int) -> None:
+    """0 auto, 1 fp64 DMMA only, 2 int8 slice product whenever supported."""
+    _check(lib.divscope_set_product_path(int(mode)))
 
 
 def stats_enable_timing(on: bool = True) -> None:

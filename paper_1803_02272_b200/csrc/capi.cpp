@@ -519,6 +519,12 @@ divscope_status divscope_matrix_euclidean_rows(const double* points, size_t n, s
 
 /* ---- device / instrumentation ---- */
 
+divscope_status divscope_set_product_path(int mode) {
+    if (mode < 0 || mode > 2) return fail_invalid("mode must be 0, 1 or 2");
+    dsb::set_product_path(mode);
+    return DIVSCOPE_OK;
+}
+
 divscope_status divscope_set_device(int device) {
     return wrap([&] { dsb::Ctx::get().set_device(device); });
 }

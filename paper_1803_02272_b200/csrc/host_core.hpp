@@ -144,6 +144,7 @@ struct Store {
 struct GramInfo {
     size_t n = 0;
     std::shared_ptr<DevBuf> row_mean;     // [n]
+    std::shared_ptr<DevBuf> row_exp;      // [n] int, K1 (unsharded grams only; else null)
     std::vector<double> row_mean_h;       // host copy (for _get / _write)
     std::shared_ptr<DevBuf> scalars;      // [S_COUNT]
     double sc[S_COUNT] = {};

@@ -90,10 +90,21 @@ __device__ __forceinline__ const T* tile_at(const unsigned char* tile, int r, in
                                       ((((byte >> 4) ^ (r & 7))) << 4) + (byte & 15));
 }
 
+// Smallest e with x < 2^e for x > 0 (the frexp exponent); kExpZero for 0.
+constexpr int kExpZero = -1100;
+__device__ __forceinline__ int exp_above(double x) {
+    if (!(x > 0.0)) return kExpZero;
+    const long long b = __double_as_longlong(x);
+    const int be = static_cast<int>((b >> 52) & 0x7ff);
+    if (be == 0) return -1022;  // subnormal: x < 2^-1022
+    return be - 1022;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kK1Threads + 32, 1)
     k1_tile_pairs(const __grid_constant__ CUtensorMap tm, int n, int nbt,
-                  double* __restrict__ part, size_t part_ld, double* __restrict__ cta_stats) {
+                  double* __restrict__ part, int* __restrict__ pexp, size_t part_ld,
+                  double* __restrict__ cta_stats) {
     using C = K1Cfg<T>;
     extern __shared__ __align__(1024) unsigned char k1_raw[];
     unsigned char* sm = k1_raw + ((1024u - (smem_u32(k1_raw) & 1023u)) & 1023u);
@@ -149,11 +160,12 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
         double a[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = static_cast<double>(*tile_at<T>(A, r, q * 16 + j));
-        double rs = 0.0;
+        double rs = 0.0, rmx = 0.0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const double sq = a[j] * a[j];
             rs += sq;
+            rmx = fmax(rmx, sq);
             sum4 += sq * sq;
             maxabs = fmax(maxabs, fabs(a[j]));
             if (I != J || q * 16 + j >= r) maxabs_up = fmax(maxabs_up, fabs(a[j]));
@@ -163,20 +175,31 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
         }
         rs += __shfl_xor_sync(0xffffffffu, rs, 8);
         rs += __shfl_xor_sync(0xffffffffu, rs, 16);
-        if (q == 0 && I * kT + r < n) part[static_cast<size_t>(J) * part_ld + I * kT + r] = rs;
+        rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, 8));
+        rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, 16));
+        if (q == 0 && I * kT + r < n) {
+            part[static_cast<size_t>(J) * part_ld + I * kT + r] = rs;
+            pexp[static_cast<size_t>(J) * part_ld + I * kT + r] = exp_above(rmx);
+        }
         if (I != J) {
-            double rb = 0.0;
+            double rb = 0.0, bmx = 0.0;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const double b = static_cast<double>(*tile_at<T>(B, r, q * 16 + j));
                 const double sq = b * b;
                 rb += sq;
+                bmx = fmax(bmx, sq);
                 sum4 += sq * sq;
                 maxabs = fmax(maxabs, fabs(b));
             }
             rb += __shfl_xor_sync(0xffffffffu, rb, 8);
             rb += __shfl_xor_sync(0xffffffffu, rb, 16);
-            if (q == 0 && J * kT + r < n) part[static_cast<size_t>(I) * part_ld + J * kT + r] = rb;
+            bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, 8));
+            bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, 16));
+            if (q == 0 && J * kT + r < n) {
+                part[static_cast<size_t>(I) * part_ld + J * kT + r] = rb;
+                pexp[static_cast<size_t>(I) * part_ld + J * kT + r] = exp_above(bmx);
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -218,36 +241,49 @@ size_t k1_smem() {
 }
 
 // r_i = (sum over tile columns of part[J][i]) / n, plus per-block sums of
-// the raw row sums, r and r^2.
-__global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ part, size_t part_ld,
+// the raw row sums, r and r^2. Also the row exponent e_i (max over the tile
+// partials: every d_ij^2 of row i is < 2^e_i) and the block max of the
+// dynamic-range bound 2^e_i / r_i used to admit the int8 slice product.
+__global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ part,
+                                                   const int* __restrict__ pexp, size_t part_ld,
                                                    int nbt, int n, double* __restrict__ row_mean,
+                                                   int* __restrict__ row_exp,
                                                    double* __restrict__ blk_stats) {
-    __shared__ double red[3][8];
+    __shared__ double red[4][8];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double rowsum = 0.0, r = 0.0;
+    double rowsum = 0.0, r = 0.0, ratio = 0.0;
     if (i < n) {
-        for (int J = 0; J < nbt; ++J) rowsum += part[static_cast<size_t>(J) * part_ld + i];
+        int e = kExpZero;
+        for (int J = 0; J < nbt; ++J) {
+            rowsum += part[static_cast<size_t>(J) * part_ld + i];
+            e = max(e, pexp[static_cast<size_t>(J) * part_ld + i]);
+        }
         r = rowsum / static_cast<double>(n);
         row_mean[i] = r;
+        row_exp[i] = e;
+        if (e > kExpZero) ratio = (r > 0.0) ? ldexp(1.0, e) / r : 1e300;
     }
-    double v0 = warp_sum(rowsum), v1 = warp_sum(r), v2 = warp_sum(r * r);
+    double v0 = warp_sum(rowsum), v1 = warp_sum(r), v2 = warp_sum(r * r), v3 = warp_max(ratio);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
         red[0][warp] = v0;
         red[1][warp] = v1;
         red[2][warp] = v2;
+        red[3][warp] = v3;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double s0 = 0, s1 = 0, s2 = 0;
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
         for (int w = 0; w < 8; ++w) {
             s0 += red[0][w];
             s1 += red[1][w];
             s2 += red[2][w];
+            s3 = fmax(s3, red[3][w]);
         }
-        blk_stats[blockIdx.x * 3 + 0] = s0;
-        blk_stats[blockIdx.x * 3 + 1] = s1;
-        blk_stats[blockIdx.x * 3 + 2] = s2;
+        blk_stats[blockIdx.x * 4 + 0] = s0;
+        blk_stats[blockIdx.x * 4 + 1] = s1;
+        blk_stats[blockIdx.x * 4 + 2] = s2;
+        blk_stats[blockIdx.x * 4 + 3] = s3;
     }
 }
 
@@ -256,9 +292,9 @@ __global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ pa
 __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ cta_stats, int ncta,
                                                    const double* __restrict__ blk_stats, int nblk,
                                                    int n, double* __restrict__ scalars) {
-    __shared__ double sh[7][256];
+    __shared__ double sh[8][256];
     const int t = threadIdx.x;
-    double sum4 = 0, m1 = 0, m2 = 0, m3 = 0, rows = 0, sr = 0, sr2 = 0;
+    double sum4 = 0, m1 = 0, m2 = 0, m3 = 0, rows = 0, sr = 0, sr2 = 0, rr = 0;
     for (int c = t; c < ncta; c += 256) {
         sum4 += cta_stats[c * 4 + 0];
         m1 = fmax(m1, cta_stats[c * 4 + 1]);
@@ -266,12 +302,13 @@ __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ ct
         m3 = fmax(m3, cta_stats[c * 4 + 3]);
     }
     for (int b = t; b < nblk; b += 256) {
-        rows += blk_stats[b * 3 + 0];
-        sr += blk_stats[b * 3 + 1];
-        sr2 += blk_stats[b * 3 + 2];
+        rows += blk_stats[b * 4 + 0];
+        sr += blk_stats[b * 4 + 1];
+        sr2 += blk_stats[b * 4 + 2];
+        rr = fmax(rr, blk_stats[b * 4 + 3]);
     }
     sh[0][t] = sum4; sh[1][t] = m1; sh[2][t] = m2; sh[3][t] = m3;
-    sh[4][t] = rows; sh[5][t] = sr; sh[6][t] = sr2;
+    sh[4][t] = rows; sh[5][t] = sr; sh[6][t] = sr2; sh[7][t] = rr;
     __syncthreads();
     for (int off = 128; off > 0; off >>= 1) {
         if (t < off) {
@@ -282,6 +319,7 @@ __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ ct
             sh[4][t] += sh[4][t + off];
             sh[5][t] += sh[5][t + off];
             sh[6][t] += sh[6][t + off];
+            sh[7][t] = fmax(sh[7][t], sh[7][t + off]);
         }
         __syncthreads();
     }
@@ -297,6 +335,7 @@ __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ ct
         scalars[S_SUM4] = sh[0][0];
         scalars[S_SUMR] = sh[5][0];
         scalars[S_SUMR2] = sh[6][0];
+        scalars[S_ROWRATIO] = sh[7][0];
     }
 }
 
@@ -315,7 +354,7 @@ int k1_grid(size_t n, int sms) {
 }
 
 void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, double* row_mean,
-               double* scalars, int sms, cudaStream_t st) {
+               int* row_exp, double* scalars, int sms, cudaStream_t st) {
     (void)sms;
     const int nbt = static_cast<int>((n + kT - 1) / kT);
     const size_t part_ld = static_cast<size_t>(nbt) * kT;
@@ -327,7 +366,7 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
             attr = true;
         }
         k1_tile_pairs<double><<<w.grid, kK1Threads + 32, k1_smem<double>(), st>>>(
-            *tmap64, static_cast<int>(n), nbt, w.part, part_ld, w.cta_stats);
+            *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
     } else {
         static bool attr = false;
         if (!attr) {
@@ -336,11 +375,11 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
             attr = true;
         }
         k1_tile_pairs<float><<<w.grid, kK1Threads + 32, k1_smem<float>(), st>>>(
-            *tmap64, static_cast<int>(n), nbt, w.part, part_ld, w.cta_stats);
+            *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
     }
     const int nblk = static_cast<int>((n + 255) / 256);
-    k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, part_ld, nbt, static_cast<int>(n), row_mean,
-                                      w.blk_stats);
+    k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, w.pexp, part_ld, nbt, static_cast<int>(n),
+                                      row_mean, row_exp, w.blk_stats);
     k1_finalize<<<1, 256, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),
                                    scalars);
     count_launch(3);

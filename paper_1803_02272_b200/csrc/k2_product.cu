@@ -296,6 +296,24 @@ void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
 
 }  // namespace
 
+void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, long long total,
+                      int P, int n, int mode, const double* row_mean, const double* scalars,
+                      const double* colsums, double* y, cudaStream_t st, const int* skip) {
+    const int nb = (n + bm - 1) / bm;
+    switch (wp * 1000 + bm) {
+#define DSB_RED(W, B)                                                                          \
+    case W * 1000 + B:                                                                         \
+        k2_reduce<W, B><<<nb * (B / 32), 256, 0, st>>>(part, maxseg, nk, total, P, n, mode,   \
+                                                       row_mean, scalars, colsums, y, skip);   \
+        break;
+        DSB_RED(8, 128) DSB_RED(16, 128) DSB_RED(24, 128) DSB_RED(32, 128) DSB_RED(40, 128)
+        DSB_RED(48, 128) DSB_RED(56, 128) DSB_RED(64, 128)
+#undef DSB_RED
+        default:
+            throw std::invalid_argument("unsupported reduce shape");
+    }
+}
+
 int k2_warps(int wp) { return wp <= 64 ? 16 : 8; }
 
 // 128-byte D boxes per pipeline stage (DSB_K2_KS overrides, for sweeps)

@@ -1,0 +1,841 @@
+// K2 on the integer tensor cores — the centered product Y = G X of
+// multiply_sym (ref src/rsvd.cpp:18-36 over the gram of mds.cpp:43-58) as an
+// exact-integer slice product (Ozaki-style splitting) on tcgen05 kind::i8.
+//
+// Why: in fp64 the pass is bounded by the FP64 tensor rate (2 n^2 w flops at
+// ~37 TF/s: 0.65 ms at C2), above the HBM time of reading D once (0.49 ms).
+// Integer MMAs run ~60x faster, so the pass becomes HBM-bound again.
+//
+// Splitting (all scalings are exact powers of two):
+//   S_ij = d_ij^2 = 2^e_i  * sum_{t=1..7} a_t 2^-8t,  a_t in [0,255]  (e_i: K1 row
+//          exponent, d^2 < 2^e_i; the 56-bit fixed-point value is truncated)
+//   X_jc = 2^f_c  * sum_{u=1..7} b_u 2^-8u,  b_u in [-128,127] (balanced digits
+//          of round(X 2^(56-f_c)), |X| 2^-f_c < 1/4)
+//   (S X)_ic = 2^(e_i+f_c) sum_{d=2..8} 2^-8d acc_d,  acc_d = sum_j sum_{t+u=d} a_t b_u
+// The terms with t+u >= 9 (weight <= 2^-72) are dropped; each acc_d is an
+// exact int32 sum over at most 8192 columns (7 * 255 * 128 * 8192 < 2^31),
+// after which it is flushed to fp64. Digits of S are produced on the fly in
+// shared memory from the fp64 (or fp32) D tile, so HBM traffic is exactly
+// one read of D per pass, as in the fp64 kernel.
+//
+// MMA structure (one CTA per SM, persistent, stream-K over (128-row block x
+// 32-column k-step) like the fp64 kernel): for each A digit t one
+// tcgen05.mma (M=128, K=32) against the CONCATENATION of B digits
+// 1..8-t (N' = (8-t) NB <= 256, else split), writing TMEM columns
+// (t-1) NB.. — so digit pair (t, u) lands on the accumulator of its
+// diagonal d = t+u. 7 MMAs per k-step, 28 digit products.
+//
+// Warp roles: warp 0 TMA producer of D tiles (128 rows x 128 B boxes,
+// SWIZZLE_128B); warp 1 TMEM owner + single-thread MMA issuer; warps 2-17
+// converters (8 tile rows each) (d -> d^2 -> 56-bit fixed point -> 7 byte planes written in the
+// UMMA K-major interleaved layout; converter 0 also bulk-copies the k-step's
+// B digits), converters 0-3 double as the epilogue (tcgen05.ld of the 7
+// diagonals, fp64 combine, exact 2^(e+f) scaling, partial slot RMW).
+// k2_reduce sums the partial slots in CTA order and applies the centering.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <stdexcept>
+
+#include "device_utils.cuh"
+#include "kernels.cuh"
+#include "umma.cuh"
+
+namespace dsb {
+
+namespace {
+
+constexpr int kRowsI8 = 128;   // M
+constexpr int kKStep = 32;     // int8 MMA K
+constexpr int kDig = 7;        // digits of S and of X
+constexpr int kChunk = 256;    // k-steps per int32 accumulation chunk (8192 columns)
+constexpr int kConv = 16;      // converter warps (8 rows each)
+constexpr int kThreadsI8 = (2 + kConv) * 32;
+constexpr int kExpZeroI8 = -1100;  // matches K1's exponent of an all-zero row
+constexpr int kABytes = kDig * kRowsI8 * kKStep;  // 28 KB of A digit tiles per k-step
+
+template <int NB>
+constexpr int b_bytes() {
+    return kDig * NB * kKStep;
+}
+template <typename TD>
+constexpr int d_bytes() {
+    return kRowsI8 * kKStep * static_cast<int>(sizeof(TD));
+}
+template <int NB>
+constexpr int g_bytes() {
+    return (kABytes + b_bytes<NB>() + 1023) / 1024 * 1024;
+}
+#ifndef DSB_I8_DSTAGES
+#define DSB_I8_DSTAGES 2
+#endif
+template <typename TD>
+constexpr int d_stages_req() {
+    return DSB_I8_DSTAGES * (sizeof(TD) == 8 ? 1 : 2);
+}
+template <int NB, typename TD>
+constexpr int g_stages() {
+    // digit stages fill the shared memory left after the D ring
+    return std::min(6, (212 * 1024 - d_stages_req<TD>() * d_bytes<TD>()) / g_bytes<NB>());
+}
+template <int NB, typename TD>
+constexpr int d_stages() {
+    return d_stages_req<TD>();
+}
+template <int NB, typename TD>
+constexpr size_t i8_smem() {
+    return 1024 + static_cast<size_t>(d_stages<NB, TD>()) * d_bytes<TD>() +
+           g_stages<NB, TD>() * g_bytes<NB>() + 256 + NB * 8;
+}
+
+// Walks a CTA's stream-K range [t0, t1) of (row block, k-step) items without
+// divisions: row block, k-step, segment index and position in the int32
+// accumulation chunk (chunks restart at every row block).
+struct Walk {
+    int it, t1, nks, rb, ks, seg, pos;
+    bool seg_first;  // the current chunk is the first one of its segment
+    __device__ Walk(int t0_, int t1_, int nks_)
+        : it(t0_), t1(t1_), nks(nks_), rb(t0_ / nks_), ks(t0_ % nks_), seg(0), pos(0),
+          seg_first(true) {}
+    __device__ bool more() const { return it < t1; }
+    __device__ bool first() const { return pos == 0; }
+    __device__ bool last() const { return it + 1 == t1 || ks + 1 == nks || pos + 1 == kChunk; }
+    __device__ void next() {
+        ++it;
+        ++ks;
+        ++pos;
+        if (ks == nks) {
+            ks = 0;
+            ++rb;
+            ++seg;
+            pos = 0;
+            seg_first = true;
+        } else if (pos == kChunk) {
+            pos = 0;
+            seg_first = false;
+        }
+    }
+};
+
+// 4 consecutive d values of row `row`, columns k0..k0+3 of the k-step tile
+template <typename TD>
+__device__ __forceinline__ void load4(const unsigned char* tile, int row, int k0, double (&d)[4]) {
+    if constexpr (sizeof(TD) == 8) {
+        // two 128-byte boxes (16 columns each), 16-byte chunk c at (c ^ row%8)
+        const unsigned char* box = tile + (k0 >> 4) * (kRowsI8 * 128) + row * 128;
+        const int c = (k0 & 15) >> 1;
+        const double2 v0 = *reinterpret_cast<const double2*>(box + (((c) ^ (row & 7)) << 4));
+        const double2 v1 = *reinterpret_cast<const double2*>(box + (((c + 1) ^ (row & 7)) << 4));
+        d[0] = v0.x;
+        d[1] = v0.y;
+        d[2] = v1.x;
+        d[3] = v1.y;
+    } else {
+        const unsigned char* rp = tile + row * 128;
+        const float4 v = *reinterpret_cast<const float4*>(rp + (((k0 >> 2) ^ (row & 7)) << 4));
+        d[0] = v.x;
+        d[1] = v.y;
+        d[2] = v.z;
+        d[3] = v.w;
+    }
+}
+
+// m = floor(s 2^(56 - e)) for 0 <= s < 2^e, as (hi, lo) 32-bit words, on
+// the FP64 pipe only (the integer conversion F2I.U64.F64 issues on the
+// narrow XU pipe and was the converter bottleneck). With C = 1.5 2^52, the
+// low word of the bits of C + v is v for an integer 0 <= v < 2^32:
+//   x  = s 2^(56-e)                      (exact power-of-two scaling)
+//   yh = C + floor(x 2^-32)              (fma, round toward -inf)  -> hi
+//   l  = x - floor(x 2^-32) 2^32 in [0, 2^32)   (exact fma)
+//   yl = C + floor(l)                    (add, round toward -inf)  -> lo
+__device__ __forceinline__ void fixed56(double s, double sc, uint32_t& lo, uint32_t& hi) {
+    constexpr double kC = 6755399441055744.0;  // 1.5 * 2^52
+    const double x = s * sc;
+    const double yh = __fma_rd(x, 0x1p-32, kC);
+    const double hf = yh - kC;
+    const double l = fma(-hf, 0x1p32, x);
+    const double yl = __dadd_rd(l, kC);
+    hi = static_cast<uint32_t>(__double_as_longlong(yh));
+    lo = static_cast<uint32_t>(__double_as_longlong(yl));
+}
+
+template <int NB, typename TD>
+__global__ void __launch_bounds__(kThreadsI8, 1)
+    k2i_product(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
+                const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
+                int nks, int total, double* __restrict__ part, int maxseg, int wp,
+                const int* __restrict__ skip, int dbg) {
+    if (skip && *skip) return;
+    constexpr int ND = d_stages<NB, TD>();
+    constexpr int NG = g_stages<NB, TD>();
+    constexpr int DB = d_bytes<TD>();
+    constexpr int GB = g_bytes<NB>();
+    constexpr int BB = b_bytes<NB>();
+    constexpr uint32_t NCOL = (kDig * NB <= 256) ? 256u : 512u;
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* dring = sm;
+    unsigned char* gring = sm + ND * DB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gring + NG * GB);
+    uint64_t* full_d = bars;
+    uint64_t* empty_d = full_d + ND;
+    uint64_t* full_g = empty_d + ND;
+    uint64_t* empty_g = full_g + NG;
+    uint64_t* acc_full = empty_g + NG;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    double* colscale = reinterpret_cast<double*>(bars + 32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cta = blockIdx.x;
+    const int t0 = static_cast<int>(static_cast<long long>(total) * cta / gridDim.x);
+    const int t1 = static_cast<int>(static_cast<long long>(total) * (cta + 1) / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ND; ++s) {
+            mbar_init(&full_d[s], 1);
+            mbar_init(&empty_d[s], kConv);
+        }
+        for (int s = 0; s < NG; ++s) {
+            mbar_init(&full_g[s], kConv + 1);
+            mbar_init(&empty_g[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 4);
+        fence_mbar_init();
+    }
+    for (int c = threadIdx.x; c < NB; c += blockDim.x) {
+        const int f = col_exp[c];
+        colscale[c] = (c < wp && f > kExpZeroI8) ? ldexp(1.0, f) : 0.0;
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, NCOL);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            prefetch_tmap(&tmD);
+            int s = 0, k = 0;
+            uint32_t ph = 0;
+            for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
+                if (k >= ND) mbar_wait(&empty_d[s], ph ^ 1);
+                unsigned char* dst = dring + s * DB;
+                mbar_arrive_expect_tx(&full_d[s], DB);
+                if constexpr (sizeof(TD) == 8) {
+                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[s]);
+                    tma_load_2d(dst + kRowsI8 * 128, &tmD, w.ks * kKStep + 16, w.rb * kRowsI8,
+                                &full_d[s]);
+                } else {
+                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[s]);
+                }
+                if (++s == ND) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            int s = 0, nflush = 0;
+            uint32_t ph = 0;
+            bool started = false;
+            for (Walk w(t0, t1, nks); w.more(); w.next()) {
+                mbar_wait(&full_g[s], ph);
+                tc_fence_after();
+                const bool first = w.first();
+                if (first && started) {
+                    mbar_wait(acc_empty, static_cast<uint32_t>((nflush - 1) & 1));
+                    tc_fence_after();
+                }
+                started = true;
+                const unsigned char* g = gring + s * GB;
+                const uint32_t abase = smem_u32(g), bbase = smem_u32(g + kABytes);
+#pragma unroll
+                for (int t = 1; t <= (dbg == 2 ? 0 : kDig); ++t) {
+                    const uint64_t ad = umma_desc_k_interleave(abase + (t - 1) * (kRowsI8 * kKStep));
+                    constexpr int per = 256 / NB;
+                    const int umax = 8 - t;
+#pragma unroll
+                    for (int u0 = 1; u0 <= umax; u0 += per) {
+                        const int nu = (umax - u0 + 1 < per) ? (umax - u0 + 1) : per;
+                        const uint64_t bd = umma_desc_k_interleave(bbase + (u0 - 1) * (NB * kKStep));
+                        umma_i8(tmem + static_cast<uint32_t>((t + u0 - 2) * NB), ad, bd,
+                                umma_idesc_i8(nu * NB, false, true), (first && t == 1) ? 0 : 1);
+                    }
+                }
+                umma_commit(&empty_g[s]);
+                if (w.last()) {
+                    umma_commit(acc_full);
+                    ++nflush;
+                }
+                if (++s == NG) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- converters (+ epilogue on 0..3) ----------------
+        const int cw = warp - 2;
+        const int row = cw * 8 + (lane >> 2);  // tile row converted by this lane
+        const int kq = lane & 3;
+        int cur_rb = -1;
+        double sc = 0.0;
+        int sd = 0, sg = 0, k = 0, nflush = 0;
+        uint32_t pd = 0, pg = 0;
+        for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
+            if (w.rb != cur_rb) {
+                cur_rb = w.rb;
+                const int grow = w.rb * kRowsI8 + row;
+                const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
+                sc = e > kExpZeroI8 ? ldexp(1.0, 56 - e) : 0.0;
+            }
+            mbar_wait(&full_d[sd], pd);
+            if (k >= NG) mbar_wait(&empty_g[sg], pg ^ 1);
+            unsigned char* g = gring + sg * GB;
+            if (cw == 0 && lane == 0) {
+                mbar_arrive_expect_tx(&full_g[sg], BB);
+                bulk_load(g + kABytes, bdig + static_cast<size_t>(w.ks) * BB, BB, &full_g[sg]);
+            }
+            const unsigned char* tile = dring + sd * DB;
+#pragma unroll
+            for (int h = 0; h < (dbg == 1 ? 0 : 2); ++h) {
+                const int k0 = h * 16 + kq * 4;
+                double d[4];
+                load4<TD>(tile, row, k0, d);
+                uint32_t lo[4], hi[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) fixed56(d[j] * d[j], sc, lo[j], hi[j]);
+                const uint32_t off = umma_tile_off(row, k0);
+                // digit t = byte (7 - t) of the 56-bit value
+#pragma unroll
+                for (int t = 1; t <= kDig; ++t) {
+                    const int byte = 7 - t;
+                    const uint32_t* src = byte >= 4 ? hi : lo;
+                    const uint32_t b = static_cast<uint32_t>(byte & 3);
+                    const uint32_t sel = b | ((b + 4) << 4);
+                    const uint32_t p01 = __byte_perm(src[0], src[1], sel);
+                    const uint32_t p23 = __byte_perm(src[2], src[3], sel);
+                    *reinterpret_cast<uint32_t*>(g + (t - 1) * (kRowsI8 * kKStep) + off) =
+                        __byte_perm(p01, p23, 0x5410);
+                }
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty_d[sd]);
+                mbar_arrive(&full_g[sg]);
+            }
+            if (++sd == ND) {
+                sd = 0;
+                pd ^= 1;
+            }
+            if (++sg == NG) {
+                sg = 0;
+                pg ^= 1;
+            }
+            if (cw < 4 && w.last()) {
+                // ---- epilogue: this warp's 32 TMEM lanes ----
+                const int q = warp & 3;
+                mbar_wait(acc_full, static_cast<uint32_t>(nflush & 1));
+                tc_fence_after();
+                const int rloc = q * 32 + lane;
+                const int grow = w.rb * kRowsI8 + rloc;
+                const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
+                const double rscale = e > kExpZeroI8 ? ldexp(1.0, e) : 0.0;
+                double* prow = part +
+                               (static_cast<size_t>(cta) * maxseg + w.seg) * kRowsI8 * wp +
+                               static_cast<size_t>(rloc) * wp;
+#pragma unroll
+                for (int cb = 0; cb < NB / 16; ++cb) {
+                    double v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = 0.0;
+#pragma unroll
+                    for (int dd = 2; dd <= 8; ++dd) {
+                        int32_t iv[16];
+                        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) +
+                                      static_cast<uint32_t>((dd - 2) * NB + cb * 16),
+                                  iv);
+                        tmem_ld_wait();
+                        const double wgt = ldexp(1.0, -8 * dd);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(iv[j]) * wgt;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int col = cb * 16 + j;
+                        if (col < wp) {
+                            const double val = v[j] * rscale * colscale[col];
+                            prow[col] = w.seg_first ? val : prow[col] + val;
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty);
+                ++nflush;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, NCOL);
+}
+
+// ---- NB = 32: A digits in tensor memory ------------------------------------
+// An MMA whose A operand comes from shared memory costs at least ~128 cycles
+// (the 4 KB A tile is read at ~32 B/clk; tools/microbench/umma_i8_rate.cu),
+// so the 7 digit MMAs of a k-step with N' = 224..32 ran at half the tensor
+// rate. With A in TMEM (written by the converters with tcgen05.st) the same
+// 7 MMAs take N'/2 cycles each: 448 cycles per k-step, well under the
+// ~1400-cycle HBM time of the k-step's 32 KB of D.
+// TMEM: columns [0, 224) the 7 diagonal accumulators, [256 + 64 s, +56) the
+// 7 x 8-column A digit planes of stage s (row = lane, byte k at column k/4).
+// Converter warp w (2..17) handles tile rows 32 (w % 4) + lane (its TMEM lane
+// quadrant) and columns 8 p .. 8 p + 7 of the k-step, p = (w - 2) / 4.
+constexpr int kAStagesTs = 4;
+constexpr int kNbTs = 32;
+
+template <typename TD>
+constexpr int d_stages_ts() {
+    return std::min(8, (208 * 1024 - kAStagesTs * b_bytes<kNbTs>()) / d_bytes<TD>());
+}
+template <typename TD>
+constexpr size_t ts_smem() {
+    return 1024 + static_cast<size_t>(d_stages_ts<TD>()) * d_bytes<TD>() +
+           kAStagesTs * b_bytes<kNbTs>() + 256 + kNbTs * 8;
+}
+
+// 8 consecutive d values of row `row`, columns c0..c0+7 of the k-step tile
+template <typename TD>
+__device__ __forceinline__ void load8(const unsigned char* tile, int row, int c0, double (&d)[8]) {
+    if constexpr (sizeof(TD) == 8) {
+        const unsigned char* box = tile + (c0 >> 4) * (kRowsI8 * 128) + row * 128;
+        const int c = (c0 & 15) >> 1;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 v = *reinterpret_cast<const double2*>(box + (((c + h) ^ (row & 7)) << 4));
+            d[2 * h] = v.x;
+            d[2 * h + 1] = v.y;
+        }
+    } else {
+        const unsigned char* rp = tile + row * 128;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float4 v =
+                *reinterpret_cast<const float4*>(rp + ((((c0 >> 2) + h) ^ (row & 7)) << 4));
+            d[4 * h] = v.x;
+            d[4 * h + 1] = v.y;
+            d[4 * h + 2] = v.z;
+            d[4 * h + 3] = v.w;
+        }
+    }
+}
+
+template <typename TD>
+__global__ void __launch_bounds__(kThreadsI8, 1)
+    k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
+                   const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
+                   int nks, int total, double* __restrict__ part, int maxseg, int wp,
+                   const int* __restrict__ skip, int dbg) {
+    if (skip && *skip) return;
+    constexpr int NB = kNbTs;
+    constexpr int ND = d_stages_ts<TD>();
+    constexpr int NA = kAStagesTs;
+    constexpr int DB = d_bytes<TD>();
+    constexpr int BB = b_bytes<NB>();
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* dring = sm;
+    unsigned char* bring = sm + ND * DB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NA * BB);
+    uint64_t* full_d = bars;
+    uint64_t* empty_d = full_d + ND;
+    uint64_t* full_a = empty_d + ND;
+    uint64_t* empty_a = full_a + NA;
+    uint64_t* acc_full = empty_a + NA;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    double* colscale = reinterpret_cast<double*>(bars + 32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cta = blockIdx.x;
+    const int t0 = static_cast<int>(static_cast<long long>(total) * cta / gridDim.x);
+    const int t1 = static_cast<int>(static_cast<long long>(total) * (cta + 1) / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ND; ++s) {
+            mbar_init(&full_d[s], 1);
+            mbar_init(&empty_d[s], kConv);
+        }
+        for (int s = 0; s < NA; ++s) {
+            mbar_init(&full_a[s], kConv + 1);
+            mbar_init(&empty_a[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 4);
+        fence_mbar_init();
+    }
+    for (int c = threadIdx.x; c < NB; c += blockDim.x) {
+        const int f = col_exp[c];
+        colscale[c] = (c < wp && f > kExpZeroI8) ? ldexp(1.0, f) : 0.0;
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem_a = tmem + 256;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            prefetch_tmap(&tmD);
+            int s = 0, k = 0;
+            uint32_t ph = 0;
+            for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
+                if (k >= ND) mbar_wait(&empty_d[s], ph ^ 1);
+                unsigned char* dst = dring + s * DB;
+                mbar_arrive_expect_tx(&full_d[s], DB);
+                if constexpr (sizeof(TD) == 8) {
+                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[s]);
+                    tma_load_2d(dst + kRowsI8 * 128, &tmD, w.ks * kKStep + 16, w.rb * kRowsI8,
+                                &full_d[s]);
+                } else {
+                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[s]);
+                }
+                if (++s == ND) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            int s = 0, nflush = 0;
+            uint32_t ph = 0;
+            bool started = false;
+            for (Walk w(t0, t1, nks); w.more(); w.next()) {
+                mbar_wait(&full_a[s], ph);
+                tc_fence_after();
+                const bool first = w.first();
+                if (first && started) {
+                    mbar_wait(acc_empty, static_cast<uint32_t>((nflush - 1) & 1));
+                    tc_fence_after();
+                }
+                started = true;
+                const uint64_t bd = umma_desc_k_interleave(smem_u32(bring + s * BB));
+                const uint32_t ta = tmem_a + static_cast<uint32_t>(s * 64);
+                if (dbg != 2) {
+#pragma unroll
+                    for (int t = 1; t <= kDig; ++t)
+                        umma_i8_ts(tmem + static_cast<uint32_t>((t - 1) * NB),
+                                   ta + static_cast<uint32_t>((t - 1) * 8), bd,
+                                   umma_idesc_i8((8 - t) * NB, false, true),
+                                   (first && t == 1) ? 0 : 1);
+                }
+                umma_commit(&empty_a[s]);
+                if (w.last()) {
+                    umma_commit(acc_full);
+                    ++nflush;
+                }
+                if (++s == NA) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- converters (+ epilogue on p == 0) ----------------
+        const int q = warp & 3;
+        const int part_k = (warp - 2) >> 2;
+        const int row = q * 32 + lane;
+        const int c0 = part_k * 8;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        int cur_rb = -1;
+        double sc = 0.0;
+        int sd = 0, sa = 0, k = 0, nflush = 0;
+        uint32_t pd = 0, pa = 0;
+        for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
+            if (w.rb != cur_rb) {
+                cur_rb = w.rb;
+                const int grow = w.rb * kRowsI8 + row;
+                const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
+                sc = e > kExpZeroI8 ? ldexp(1.0, 56 - e) : 0.0;
+            }
+            mbar_wait(&full_d[sd], pd);
+            if (k >= NA) {
+                mbar_wait(&empty_a[sa], pa ^ 1);
+                tc_fence_after();
+            }
+            if (warp == 2 && lane == 0) {
+                mbar_arrive_expect_tx(&full_a[sa], BB);
+                bulk_load(bring + sa * BB, bdig + static_cast<size_t>(w.ks) * BB, BB, &full_a[sa]);
+            }
+            if (dbg != 1) {
+                double d[8];
+                load8<TD>(dring + sd * DB, row, c0, d);
+                uint32_t lo[8], hi[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);
+                    lo[j] = static_cast<uint32_t>(m);
+                    hi[j] = static_cast<uint32_t>(m >> 32);
+                }
+                const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64) + lane_off;
+#pragma unroll
+                for (int t = 1; t <= kDig; ++t) {
+                    const int byte = 7 - t;
+                    const uint32_t* src = byte >= 4 ? hi : lo;
+                    const uint32_t b = static_cast<uint32_t>(byte & 3);
+                    const uint32_t sel = b | ((b + 4) << 4);
+                    const uint32_t w0 = __byte_perm(__byte_perm(src[0], src[1], sel),
+                                                    __byte_perm(src[2], src[3], sel), 0x5410);
+                    const uint32_t w1 = __byte_perm(__byte_perm(src[4], src[5], sel),
+                                                    __byte_perm(src[6], src[7], sel), 0x5410);
+                    tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2), w0, w1);
+                }
+                tmem_st_wait();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty_d[sd]);
+                mbar_arrive(&full_a[sa]);
+            }
+            if (++sd == ND) {
+                sd = 0;
+                pd ^= 1;
+            }
+            if (++sa == NA) {
+                sa = 0;
+                pa ^= 1;
+            }
+            if (part_k == 0 && w.last()) {
+                // ---- epilogue: this warp's 32 TMEM lanes ----
+                mbar_wait(acc_full, static_cast<uint32_t>(nflush & 1));
+                tc_fence_after();
+                const int grow = w.rb * kRowsI8 + row;
+                const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
+                const double rscale = e > kExpZeroI8 ? ldexp(1.0, e) : 0.0;
+                double* prow = part +
+                               (static_cast<size_t>(cta) * maxseg + w.seg) * kRowsI8 * wp +
+                               static_cast<size_t>(row) * wp;
+#pragma unroll
+                for (int cb = 0; cb < NB / 16; ++cb) {
+                    double v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = 0.0;
+#pragma unroll
+                    for (int dd = 2; dd <= 8; ++dd) {
+                        int32_t iv[16];
+                        tmem_ld16(tmem + lane_off + static_cast<uint32_t>((dd - 2) * NB + cb * 16),
+                                  iv);
+                        tmem_ld_wait();
+                        const double wgt = ldexp(1.0, -8 * dd);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(iv[j]) * wgt;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int col = cb * 16 + j;
+                        if (col < wp) {
+                            const double val = v[j] * rscale * colscale[col];
+                            prow[col] = w.seg_first ? val : prow[col] + val;
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty);
+                ++nflush;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// ---- B digits of the panel (per pass) --------------------------------------
+// column max |X| partials (k4-interleaved panel, rows [n_pad*b/P, ...))
+__global__ void __launch_bounds__(256) k_colmax_partial(const double* __restrict__ x, size_t n_pad,
+                                                        int wp, double* __restrict__ pmax) {
+    extern __shared__ double shm[];  // [wp * 4]
+    const size_t nq = n_pad / 4;
+    const size_t q0 = nq * blockIdx.x / gridDim.x, q1 = nq * (blockIdx.x + 1) / gridDim.x;
+    const int per = wp * 4;
+    for (int e = threadIdx.x; e < per; e += blockDim.x) {
+        double m = 0.0;
+        for (size_t q = q0; q < q1; ++q) m = fmax(m, fabs(x[q * per + e]));
+        shm[e] = m;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < wp; c += blockDim.x)
+        pmax[static_cast<size_t>(blockIdx.x) * wp + c] =
+            fmax(fmax(shm[c * 4], shm[c * 4 + 1]), fmax(shm[c * 4 + 2], shm[c * 4 + 3]));
+}
+
+// f_c with max |X_c| 2^-f_c < 1/4
+__global__ void k_colexp(const double* __restrict__ pmax, int P, int wp, int nb,
+                         int* __restrict__ col_exp) {
+    for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+        double m = 0.0;
+        if (c < wp)
+            for (int b = 0; b < P; ++b) m = fmax(m, pmax[static_cast<size_t>(b) * wp + c]);
+        int f = kExpZeroI8;
+        if (m > 0.0) {
+            int e;
+            frexp(m, &e);  // m < 2^e
+            f = e + 2;
+        }
+        col_exp[c] = f;
+    }
+}
+
+// one thread per (k-step, column, 4 rows): balanced base-256 digits of
+// round(X 2^(56 - f_c)), written as 7 byte planes in the UMMA layout
+__global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__ x, int nks, int wp,
+                                                      int nb, const int* __restrict__ col_exp,
+                                                      unsigned char* __restrict__ bdig) {
+    const long long total = static_cast<long long>(nks) * nb * 8;
+    const int bb = kDig * nb * kKStep;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int kq = static_cast<int>(e & 7);
+        const int c = static_cast<int>((e >> 3) % nb);
+        const long long ks = (e >> 3) / nb;
+        uint32_t word[kDig];
+#pragma unroll
+        for (int u = 0; u < kDig; ++u) word[u] = 0;
+        const int f = col_exp[c];
+        if (c < wp && f > kExpZeroI8) {
+            const double scale = ldexp(1.0, 56 - f);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const size_t j = static_cast<size_t>(ks) * kKStep + kq * 4 + jj;
+                long long m = __double2ll_rn(x[pidx(j, c, wp)] * scale);
+                int dig[kDig];
+#pragma unroll
+                for (int u = kDig - 1; u >= 1; --u) {
+                    const int b = static_cast<int>((m + 128) & 255) - 128;
+                    dig[u] = b;
+                    m = (m - b) >> 8;
+                }
+                dig[0] = static_cast<int>(m);
+#pragma unroll
+                for (int u = 0; u < kDig; ++u)
+                    word[u] |= (static_cast<uint32_t>(dig[u]) & 0xffu) << (8 * jj);
+            }
+        }
+        unsigned char* dst = bdig + static_cast<size_t>(ks) * bb;
+        const uint32_t off = umma_tile_off(static_cast<uint32_t>(c), static_cast<uint32_t>(kq * 4));
+#pragma unroll
+        for (int u = 0; u < kDig; ++u)
+            *reinterpret_cast<uint32_t*>(dst + u * (nb * kKStep) + off) = word[u];
+    }
+}
+
+// DSB_K2I_DEBUG: 1 = skip the digit conversion, 2 = skip the MMAs (timing
+// experiments only; results are wrong)
+int k2i_debug_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("DSB_K2I_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return m;
+}
+
+template <int NB, typename TD>
+void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
+            const int* row_exp, const int* col_exp, double* part, cudaStream_t st,
+            const int* skip) {
+    if constexpr (NB == kNbTs) {
+        static bool attr_ts = false;
+        if (!attr_ts) {
+            cudaFuncSetAttribute(k2i_product_ts<TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ts_smem<TD>()));
+            attr_ts = true;
+        }
+        k2i_product_ts<TD><<<p.grid, kThreadsI8, ts_smem<TD>(), st>>>(
+            *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
+            p.maxseg, wp, skip, k2i_debug_mode());
+        return;
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k2i_product<NB, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(i8_smem<NB, TD>()));
+        attr = true;
+    }
+    k2i_product<NB, TD><<<p.grid, kThreadsI8, i8_smem<NB, TD>(), st>>>(
+        *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part, p.maxseg,
+        wp, skip, k2i_debug_mode());
+}
+
+}  // namespace
+
+K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms) {
+    K2iPlan p;
+    p.nb = wp <= 32 ? 32 : 64;
+    p.nrows = static_cast<int>(nrows);
+    p.nblk = static_cast<int>((nrows + kRowsI8 - 1) / kRowsI8);
+    p.nks = static_cast<int>((ncols + kKStep - 1) / kKStep);
+    p.total = static_cast<long long>(p.nblk) * p.nks;
+    p.grid = static_cast<int>(std::min<long long>(sms, p.total));
+    int maxseg = 1;
+    for (long long c = 0; c < p.grid; ++c) {
+        const long long a = p.total * c / p.grid, b = p.total * (c + 1) / p.grid;
+        if (b > a) maxseg = std::max<int>(maxseg, static_cast<int>((b - 1) / p.nks - a / p.nks + 1));
+    }
+    p.maxseg = maxseg;
+    p.part_elems = static_cast<size_t>(p.grid) * maxseg * kRowsI8 * wp;
+    p.bdig_bytes = static_cast<size_t>(p.nks) * kDig * p.nb * kKStep;
+    p.colmax_grid = sms;
+    return p;
+}
+
+bool k2i_supported(int wp) { return wp >= 8 && wp <= 64; }
+
+void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, const double* x,
+                size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
+                unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
+                const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
+                const int* skip) {
+    k_colmax_partial<<<p.colmax_grid, 256, wp * 4 * sizeof(double), st>>>(x, x_rows_pad, wp, pmax);
+    k_colexp<<<1, 64, 0, st>>>(pmax, p.colmax_grid, wp, p.nb, col_exp);
+    {
+        const long long items = static_cast<long long>(p.nks) * p.nb * 8;
+        const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
+        k_panel_digits<<<grid, 256, 0, st>>>(x, p.nks, wp, p.nb, col_exp, bdig);
+    }
+    if (e0) cudaEventRecord(e0, st);
+    if (dt == DType::F64) {
+        if (p.nb == 32)
+            run_i8<32, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, st, skip);
+        else
+            run_i8<64, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, st, skip);
+    } else {
+        if (p.nb == 32)
+            run_i8<32, float>(tmap128, p, wp, bdig, row_exp, col_exp, part, st, skip);
+        else
+            run_i8<64, float>(tmap128, p, wp, bdig, row_exp, col_exp, part, st, skip);
+    }
+    if (e1) cudaEventRecord(e1, st);
+    launch_k2_reduce(wp, kRowsI8, part, p.maxseg, p.nks, p.total, p.grid, p.nrows, 1, row_mean,
+                     scalars, colsums, y, st, skip);
+    count_launch(5);
+}
+
+}  // namespace dsb

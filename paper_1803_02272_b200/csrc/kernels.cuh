@@ -24,6 +24,7 @@ enum Scalar : int {
     S_SUM4 = 6,        // sum a^4
     S_SUMR = 7,        // sum_i r_i
     S_SUMR2 = 8,       // sum_i r_i^2
+    S_ROWRATIO = 9,    // max_i 2^e_i / r_i (row max of d^2 over row mean, bound)
     S_COUNT = 16,
 };
 
@@ -33,15 +34,17 @@ enum class DType { F64 = 0, F32 = 1 };
 // sum of fourth powers, max |d| and max |d_ij - d_ji| -----------------------
 struct K1Work {
     double* part;        // [nbt][n_pad64] per-tile-column row partial sums
+    int* pexp;           // [nbt][n_pad64] per-tile-column row exponents of max d^2
     double* cta_stats;   // [grid][4]
-    double* blk_stats;   // [nblk][3]
+    double* blk_stats;   // [nblk][4]
     int grid;
 };
 size_t k1_part_elems(size_t n);
 int k1_grid(size_t n, int sms);
 // tmap64: TMA descriptor of D with 64-row x 128-byte boxes (SWIZZLE_128B)
+// row_exp[i]: smallest e with d_ij^2 < 2^e for all j (the int8 slice scale)
 void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, double* row_mean,
-               double* scalars, int sms, cudaStream_t st);
+               int* row_exp, double* scalars, int sms, cudaStream_t st);
 
 // ---- K1 for a row shard (rectangular rows x cols block): row sums of d^2,
 // sum d^4 and max |d| (deterministic per-CTA partials -> finalize on host)
@@ -76,6 +79,31 @@ void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
                double* part, const double* row_mean, const double* scalars,
                const double* colsums, double* y, size_t n_pad, cudaStream_t st,
                cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr, const int* skip = nullptr);
+
+// k2_reduce for an explicit row-block height (bm = 128 or 256)
+void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, long long total,
+                      int P, int n, int mode, const double* row_mean, const double* scalars,
+                      const double* colsums, double* y, cudaStream_t st, const int* skip);
+
+// ---- K2 on the integer tensor cores (k2i_product.cu): exact 7x7-digit
+// slice product of D o D and the panel on tcgen05 kind::i8 (lazy grams,
+// WP <= 64). row_exp from K1.
+struct K2iPlan {
+    int nb = 32;            // MMA N per digit (32 or 64 >= WP)
+    int nrows = 0, nblk = 0, nks = 0;
+    long long total = 0;
+    int grid = 0, maxseg = 0, colmax_grid = 0;
+    size_t part_elems = 0;  // doubles
+    size_t bdig_bytes = 0;  // panel digit planes
+};
+bool k2i_supported(int wp);
+K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms);
+// pmax: colmax_grid * wp doubles; col_exp: nb ints; bdig: bdig_bytes
+void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, const double* x,
+                size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
+                unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
+                const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0 = nullptr,
+                cudaEvent_t e1 = nullptr, const int* skip = nullptr);
 
 // ---- panel kernels (n_pad x WP, k4-interleaved) -----------------------------
 int panel_grid(size_t n_pad, int sms);

@@ -5,10 +5,14 @@
 #include "solver.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <deque>
 #include <thread>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
 #include <tuple>
 
 namespace dsb {
@@ -19,6 +23,7 @@ struct StatsOut {
     double sc[S_COUNT];
     std::shared_ptr<DevBuf> scalars;
     std::shared_ptr<DevBuf> row_mean;
+    std::shared_ptr<DevBuf> row_exp;
 };
 
 // K1 over a store; returns scalars (host) plus device scalars/row means.
@@ -37,15 +42,17 @@ StatsOut run_k1(Store& s) {
     w.grid = k1_grid(n, c.sms);
     w.part = static_cast<double*>(c.scratch("k1_part", k1_part_elems(n) * sizeof(double)));
     w.cta_stats = static_cast<double*>(c.scratch("k1_cta", static_cast<size_t>(w.grid) * 4 * 8));
-    w.blk_stats = static_cast<double*>(c.scratch("k1_blk", ((n + 255) / 256) * 3 * 8 + 64));
+    w.pexp = static_cast<int*>(c.scratch("k1_pexp", k1_part_elems(n) * sizeof(int)));
+    w.blk_stats = static_cast<double*>(c.scratch("k1_blk", ((n + 255) / 256) * 4 * 8 + 64));
     StatsOut o;
     o.row_mean = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * sizeof(double));
+    o.row_exp = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * sizeof(int));
     o.scalars = std::make_shared<DevBuf>(S_COUNT * sizeof(double));
     DSB_CUDA(cudaMemsetAsync(o.scalars->p, 0, S_COUNT * sizeof(double), c.stream));
     cudaEvent_t ev;
     c.begin_timed(0, &ev);
-    launch_k1(&s.tmap64, s.dt, n, w, o.row_mean->as<double>(), o.scalars->as<double>(), c.sms,
-              c.stream);
+    launch_k1(&s.tmap64, s.dt, n, w, o.row_mean->as<double>(), o.row_exp->as<int>(),
+              o.scalars->as<double>(), c.sms, c.stream);
     c.end_timed(0, ev);
     DSB_CUDA(cudaGetLastError());
     c.d2h_copy(o.sc, o.scalars->p, S_COUNT * sizeof(double));
@@ -103,6 +110,39 @@ const double* omega_host(uint64_t seed, size_t n, size_t w) {
     return cache.back()->p;
 }
 
+// The int8 slice product keeps ~53 bits relative to the ROW maximum of d^2;
+// accept it when every row's max / mean ratio is bounded (so the error stays
+// at the fp64 level relative to the row's own magnitude) and the data are
+// finite. DSB_K2_INT8=0 forces the fp64 kernel (parity comparisons).
+std::atomic<int> g_product_path{-1};  // -1: not yet read from DSB_K2_INT8
+
+}  // namespace
+
+void set_product_path(int mode) { g_product_path.store(mode); }
+
+namespace {
+
+int product_path() {
+    int m = g_product_path.load();
+    if (m < 0) {
+        // DSB_K2_INT8: unset/1 -> auto, 0 -> fp64 only, 2 -> int8 whenever supported
+        const char* e = std::getenv("DSB_K2_INT8");
+        const int v = e ? std::atoi(e) : 1;
+        m = v == 0 ? 1 : (v == 2 ? 2 : 0);
+        g_product_path.store(m);
+    }
+    return m;  // 0 auto, 1 fp64 only, 2 int8 whenever supported
+}
+
+bool use_int8_product(const GramInfo& gi, int wp) {
+    const int mode = product_path();
+    if (mode == 1 || !gi.row_exp || !k2i_supported(wp)) return false;
+    // small (L2-resident) problems: the extra digit launches outweigh the gain
+    if (gi.n < 4096 && mode != 2) return false;
+    const double ratio = gi.sc[S_ROWRATIO], s4 = gi.sc[S_SUM4];
+    return std::isfinite(s4) && std::isfinite(ratio) && ratio <= 4096.0;
+}
+
 struct RunOut {
     std::vector<double> vals;  // w values, reference order
     size_t keep = 0;
@@ -148,11 +188,26 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
 
     ensure_tmap(s);
     const K2Plan plan = k2_plan(n, wp, s.dt, c.sms);
+    // integer-tensor-core product (k2i_product.cu) for lazy grams of moderate
+    // dynamic range; the fp64 DMMA kernel otherwise
+    const bool use_i8 = lazy && use_int8_product(*g.gram, wp);
+    K2iPlan iplan;
+    double* pmax = nullptr;
+    int* col_exp = nullptr;
+    unsigned char* bdig = nullptr;
+    if (use_i8) {
+        iplan = k2i_plan(n, n, wp, c.sms);
+        pmax = static_cast<double*>(
+            c.scratch("i8_pmax", static_cast<size_t>(iplan.colmax_grid) * wp * sizeof(double)));
+        col_exp = static_cast<int*>(c.scratch("i8_colexp", 64 * sizeof(int)));
+        bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
+    }
     const size_t pbytes = n_pad * wp * sizeof(double);
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
     double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));
     double* P2 = static_cast<double*>(c.scratch("panel2", pbytes));
-    double* part = static_cast<double*>(c.scratch("k2_part", plan.part_elems * sizeof(double)));
+    double* part = static_cast<double*>(c.scratch(
+        "k2_part", std::max(plan.part_elems, use_i8 ? iplan.part_elems : 0) * sizeof(double)));
     const int pg = panel_grid(n_pad, c.sms);
     const size_t part_small =
         std::max<size_t>(static_cast<size_t>(pg) * wp * wp, static_cast<size_t>(pg) * 2 * wp);
@@ -189,8 +244,12 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         if (mode) launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
         cudaEvent_t e0, e1;
         c.make_events(&e0, &e1);
-        launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums, y,
-                  n_pad, c.stream, e0, e1);
+        if (use_i8)
+            launch_k2i(s.tmap_for(128), s.dt, iplan, wp, x, n_pad, g.gram->row_exp->as<int>(), pmax,
+                       col_exp, bdig, part, row_mean, scal_dev, colsums, y, c.stream, e0, e1);
+        else
+            launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums,
+                      y, n_pad, c.stream, e0, e1);
         c.add_timed(1, e0, e1);
     };
     // CholeskyQR3 with shift/drop handling: y -> t -> y -> out
@@ -316,6 +375,7 @@ Matrix gram_from_distances(const Matrix& d) {
     g.gram = std::make_shared<GramInfo>();
     g.gram->n = n;
     g.gram->row_mean = o.row_mean;
+    g.gram->row_exp = o.row_exp;
     g.gram->scalars = o.scalars;
     std::memcpy(g.gram->sc, o.sc, sizeof(o.sc));
     return g;

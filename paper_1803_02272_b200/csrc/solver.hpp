@@ -56,6 +56,9 @@ void randomized_range(const Matrix& g, const SolverOptions& opts, double* q_out)
 
 // ref src/rsvd.cpp:147-178
 double stable_rank(const Matrix& g);
+// product kernel choice: 0 auto, 1 fp64 DMMA only, 2 int8 slice product
+// whenever supported (lazy grams, w <= 64)
+void set_product_path(int mode);
 
 // G_ij of a handle (lazy gram evaluated like ref mds.cpp:50-58)
 double matrix_get(const Matrix& m, size_t i, size_t j);

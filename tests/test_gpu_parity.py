@@ -23,6 +23,17 @@ def err(ds, fn, *a, **k):
 
 # ---------------------------------------------------------------- builders
 
+
+@pytest.fixture(autouse=True, params=["auto", "int8"])
+def product_path(request, ds):
+    """Every parity test runs twice: with the automatic product-kernel choice
+    (fp64 DMMA at these small n) and with the int8 slice product forced for
+    every lazy gram it supports (k2i_product.cu)."""
+    ds.set_product_path(2 if request.param == "int8" else 0)
+    yield request.param
+    ds.set_product_path(0)
+
+
 def test_euclid_bit_exact_vs_oracle(ds, oracle):
     pts = ds.synth_points(1, 301, 11)
     d_gpu = ds.matrix_euclidean(pts).to_numpy()

@@ -90,7 +90,11 @@ __global__ void k_test(const uint8_t* __restrict__ A, const int8_t* __restrict__
 }
 
 template <int N>
-int run(int ksteps) {
+__global__ void k_test_ts(const uint8_t* __restrict__ A, const int8_t* __restrict__ B, int ksteps,
+                          int32_t* __restrict__ out);
+
+template <int N>
+int run(int ksteps, bool ts = false) {
     const int K = ksteps * KSTEP;
     std::vector<uint8_t> A(static_cast<size_t>(T) * M * K);
     std::vector<int8_t> B(static_cast<size_t>(T) * N * K);
@@ -107,8 +111,13 @@ int run(int ksteps) {
     cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
     cudaMemset(dO, 0, sizeof(int32_t) * M * T * N);
     const int smem = T * M * KSTEP + T * N * KSTEP;
-    cudaFuncSetAttribute(k_test<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_test<N><<<1, 256, smem>>>(dA, dB, ksteps, dO);
+    if (ts) {
+        cudaFuncSetAttribute(k_test_ts<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_test_ts<N><<<1, 256, smem>>>(dA, dB, ksteps, dO);
+    } else {
+        cudaFuncSetAttribute(k_test<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_test<N><<<1, 256, smem>>>(dA, dB, ksteps, dO);
+    }
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         printf("N=%d: CUDA error %s\n", N, cudaGetErrorString(e));
@@ -135,11 +144,95 @@ int run(int ksteps) {
                     ++bad;
                 }
             }
-    printf("N=%d ksteps=%d: %s (%ld mismatches)\n", N, ksteps, bad ? "FAIL" : "OK", bad);
+    printf("%s N=%d ksteps=%d: %s (%ld mismatches)\n", ts ? "TS" : "SS", N, ksteps,
+           bad ? "FAIL" : "OK", bad);
     cudaFree(dA);
     cudaFree(dB);
     cudaFree(dO);
     return bad ? 1 : 0;
+}
+
+// Same product with the A digits in tensor memory (written by tcgen05.st,
+// row r = lane r, byte k of the 32-byte K slice in column k/4).
+template <int N>
+__global__ void k_test_ts(const uint8_t* __restrict__ A, const int8_t* __restrict__ B, int ksteps,
+                          int32_t* __restrict__ out) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    unsigned char* sb = sm;  // [T][N x 32]
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) tmem_alloc(&tbase, 512);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tbase;
+    const uint32_t ta = tmem + 256;  // A digits: 7 x 8 columns
+    uint32_t phase = 0;
+    for (int ks = 0; ks < ksteps; ++ks) {
+        if (warp < 4) {
+            const int r = threadIdx.x;
+            for (int t = 0; t < T; ++t)
+                for (int c = 0; c < 8; c += 2) {
+                    uint32_t w[2];
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t v = 0;
+                        for (int b = 0; b < 4; ++b)
+                            v |= static_cast<uint32_t>(
+                                     A[(static_cast<size_t>(t) * M + r) * (ksteps * KSTEP) +
+                                       ks * KSTEP + (c + h) * 4 + b])
+                                 << (8 * b);
+                        w[h] = v;
+                    }
+                    tmem_st2(ta + (static_cast<uint32_t>(warp * 32) << 16) + t * 8 + c, w[0], w[1]);
+                }
+            tmem_st_wait();
+        }
+        for (int e = threadIdx.x; e < T * N * KSTEP; e += blockDim.x) {
+            const int u = e / (N * KSTEP), c = (e / KSTEP) % N, k = e % KSTEP;
+            sb[u * N * KSTEP + umma_tile_off(c, k)] = static_cast<unsigned char>(
+                B[(static_cast<size_t>(u) * N + c) * (ksteps * KSTEP) + ks * KSTEP + k]);
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            tc_fence_after();
+            for (int t = 1; t <= T; ++t) {
+                const int umax = 8 - t;
+                const int per = 256 / N;
+                for (int u0 = 1; u0 <= umax; u0 += per) {
+                    const int nu = (umax - u0 + 1 < per) ? (umax - u0 + 1) : per;
+                    const uint64_t bd = umma_desc_k_interleave(smem_u32(sb + (u0 - 1) * N * KSTEP));
+                    umma_i8_ts(tmem + (t + u0 - 2) * N, ta + (t - 1) * 8, bd,
+                               umma_idesc_i8(nu * N, false, true), (ks > 0 || t > 1) ? 1 : 0);
+                }
+            }
+            umma_commit(&bar);
+        }
+        __syncwarp();
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        __syncthreads();
+    }
+    if (warp < 4) {
+        const int row = warp * 32 + (threadIdx.x & 31);
+        for (int c0 = 0; c0 < T * N; c0 += 32) {
+            int32_t v[32];
+            tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+            tmem_ld_wait();
+            for (int j = 0; j < 32; ++j)
+                if (c0 + j < T * N) out[row * (T * N) + c0 + j] = v[j];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
 int main() {
@@ -148,5 +241,7 @@ int main() {
     rc |= run<32>(3);
     rc |= run<64>(2);
     rc |= run<16>(2);
+    rc |= run<32>(1, true);
+    rc |= run<32>(3, true);
     return rc;
 }
