@@ -568,7 +568,7 @@ void divscope_stats_get(divscope_stats* out) {
         out->last_evd_sweeps = c.last_evd_sweeps;
         out->last_orth_shifted = c.last_orth_shifted;
         out->last_power_iters = c.last_power_iters;
-        out->reserved0 = 0;
+        out->last_product_kernel = c.last_product_kernel;
     } catch (...) {
     }
 }

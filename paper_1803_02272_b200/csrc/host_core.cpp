@@ -40,9 +40,13 @@ void cuda_check(cudaError_t e, const char* what) {
                                         what + ")");
 }
 
+// Device buffers come from the stream-ordered pool on the library stream
+// (release threshold unlimited, see Ctx::init): a matrix handle created and
+// freed per call (the e2e path) reuses its blocks instead of paying a
+// synchronizing cudaMalloc/cudaFree of gigabytes every time.
 DevBuf::DevBuf(size_t b) : bytes(b) {
     if (b == 0) return;
-    const cudaError_t e = cudaMalloc(&p, b);
+    const cudaError_t e = cudaMallocAsync(&p, b, Ctx::get().stream);
     if (e != cudaSuccess) {
         p = nullptr;
         throw Error(errc::internal, "device out of memory allocating " + std::to_string(b) +
@@ -51,7 +55,7 @@ DevBuf::DevBuf(size_t b) : bytes(b) {
 }
 
 DevBuf::~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, Ctx::get().stream);
 }
 
 Ctx::Ctx() = default;
@@ -81,6 +85,12 @@ void Ctx::init() {
                                         prop.name);
     sms = prop.multiProcessorCount;
     DSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    {
+        cudaMemPool_t pool;
+        DSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = ~0ull;
+        DSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     cudaDriverEntryPointQueryResult q{};
     void* fn = nullptr;
     DSB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));

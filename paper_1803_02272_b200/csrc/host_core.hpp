@@ -88,6 +88,7 @@ public:
     uint64_t k2_launches = 0, k1_launches = 0, h2d = 0, d2h = 0;
     double k2_ms = 0.0, k1_ms = 0.0;
     int last_evd_sweeps = 0, last_orth_shifted = 0, last_power_iters = 0;
+    int last_product_kernel = 0;  // 0 fp64 DMMA, 1 int8 slice product
     std::vector<TimedPair> pending;
     std::vector<cudaEvent_t> event_pool;
     void begin_timed(int kind, cudaEvent_t* a);

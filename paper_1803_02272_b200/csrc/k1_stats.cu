@@ -90,12 +90,17 @@ __device__ __forceinline__ const T* tile_at(const unsigned char* tile, int r, in
                                       ((((byte >> 4) ^ (r & 7))) << 4) + (byte & 15));
 }
 
-// Smallest e with x < 2^e for x > 0 (the frexp exponent); kExpZero for 0.
+// Smallest e with x < 2^e for the largest x >= 0 of a set, from the max of
+// the high 32 bits of the doubles (for non-negative doubles the bit patterns
+// order like the values; integer max keeps this off the FP64 pipe).
+// kExpZero when all are zero.
 constexpr int kExpZero = -1100;
-__device__ __forceinline__ int exp_above(double x) {
-    if (!(x > 0.0)) return kExpZero;
-    const long long b = __double_as_longlong(x);
-    const int be = static_cast<int>((b >> 52) & 0x7ff);
+__device__ __forceinline__ uint32_t hi_bits(double x) {
+    return static_cast<uint32_t>(__double2hiint(x));
+}
+__device__ __forceinline__ int exp_above_hi(uint32_t hmax) {
+    if (hmax == 0u) return kExpZero;
+    const int be = static_cast<int>((hmax >> 20) & 0x7ffu);
     if (be == 0) return -1022;  // subnormal: x < 2^-1022
     return be - 1022;
 }
@@ -160,12 +165,13 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
         double a[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = static_cast<double>(*tile_at<T>(A, r, q * 16 + j));
-        double rs = 0.0, rmx = 0.0;
+        double rs = 0.0;
+        uint32_t rmx = 0u;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const double sq = a[j] * a[j];
             rs += sq;
-            rmx = fmax(rmx, sq);
+            rmx = max(rmx, hi_bits(sq));
             sum4 += sq * sq;
             maxabs = fmax(maxabs, fabs(a[j]));
             if (I != J || q * 16 + j >= r) maxabs_up = fmax(maxabs_up, fabs(a[j]));
@@ -175,30 +181,31 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
         }
         rs += __shfl_xor_sync(0xffffffffu, rs, 8);
         rs += __shfl_xor_sync(0xffffffffu, rs, 16);
-        rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, 8));
-        rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, 16));
+        rmx = max(rmx, __shfl_xor_sync(0xffffffffu, rmx, 8));
+        rmx = max(rmx, __shfl_xor_sync(0xffffffffu, rmx, 16));
         if (q == 0 && I * kT + r < n) {
             part[static_cast<size_t>(J) * part_ld + I * kT + r] = rs;
-            pexp[static_cast<size_t>(J) * part_ld + I * kT + r] = exp_above(rmx);
+            pexp[static_cast<size_t>(J) * part_ld + I * kT + r] = exp_above_hi(rmx);
         }
         if (I != J) {
-            double rb = 0.0, bmx = 0.0;
+            double rb = 0.0;
+            uint32_t bmx = 0u;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const double b = static_cast<double>(*tile_at<T>(B, r, q * 16 + j));
                 const double sq = b * b;
                 rb += sq;
-                bmx = fmax(bmx, sq);
+                bmx = max(bmx, hi_bits(sq));
                 sum4 += sq * sq;
                 maxabs = fmax(maxabs, fabs(b));
             }
             rb += __shfl_xor_sync(0xffffffffu, rb, 8);
             rb += __shfl_xor_sync(0xffffffffu, rb, 16);
-            bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, 8));
-            bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, 16));
+            bmx = max(bmx, __shfl_xor_sync(0xffffffffu, bmx, 8));
+            bmx = max(bmx, __shfl_xor_sync(0xffffffffu, bmx, 16));
             if (q == 0 && J * kT + r < n) {
                 part[static_cast<size_t>(I) * part_ld + J * kT + r] = rb;
-                pexp[static_cast<size_t>(I) * part_ld + J * kT + r] = exp_above(bmx);
+                pexp[static_cast<size_t>(I) * part_ld + J * kT + r] = exp_above_hi(bmx);
             }
         }
         __syncwarp();
@@ -244,46 +251,50 @@ size_t k1_smem() {
 // the raw row sums, r and r^2. Also the row exponent e_i (max over the tile
 // partials: every d_ij^2 of row i is < 2^e_i) and the block max of the
 // dynamic-range bound 2^e_i / r_i used to admit the int8 slice product.
+// A block owns 32 rows; its 8 warps stride over the tile columns J (warp w:
+// J = w, w + 8, ...) and the 8 partials are added in warp order (fixed).
+constexpr int kRmRows = 32;
 __global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ part,
                                                    const int* __restrict__ pexp, size_t part_ld,
                                                    int nbt, int n, double* __restrict__ row_mean,
                                                    int* __restrict__ row_exp,
                                                    double* __restrict__ blk_stats) {
-    __shared__ double red[4][8];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double rowsum = 0.0, r = 0.0, ratio = 0.0;
+    __shared__ double ps[8][kRmRows];
+    __shared__ int pe[8][kRmRows];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * kRmRows + lane;
+    double acc = 0.0;
+    int e = kExpZero;
     if (i < n) {
-        int e = kExpZero;
-        for (int J = 0; J < nbt; ++J) {
-            rowsum += part[static_cast<size_t>(J) * part_ld + i];
+        for (int J = warp; J < nbt; J += 8) {
+            acc += part[static_cast<size_t>(J) * part_ld + i];
             e = max(e, pexp[static_cast<size_t>(J) * part_ld + i]);
         }
-        r = rowsum / static_cast<double>(n);
-        row_mean[i] = r;
-        row_exp[i] = e;
-        if (e > kExpZero) ratio = (r > 0.0) ? ldexp(1.0, e) / r : 1e300;
     }
-    double v0 = warp_sum(rowsum), v1 = warp_sum(r), v2 = warp_sum(r * r), v3 = warp_max(ratio);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        red[0][warp] = v0;
-        red[1][warp] = v1;
-        red[2][warp] = v2;
-        red[3][warp] = v3;
-    }
+    ps[warp][lane] = acc;
+    pe[warp][lane] = e;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-        for (int w = 0; w < 8; ++w) {
-            s0 += red[0][w];
-            s1 += red[1][w];
-            s2 += red[2][w];
-            s3 = fmax(s3, red[3][w]);
+    if (warp == 0) {
+        double rowsum = 0.0, r = 0.0, ratio = 0.0;
+        if (i < n) {
+            int ee = kExpZero;
+            for (int w = 0; w < 8; ++w) {
+                rowsum += ps[w][lane];
+                ee = max(ee, pe[w][lane]);
+            }
+            r = rowsum / static_cast<double>(n);
+            row_mean[i] = r;
+            row_exp[i] = ee;
+            if (ee > kExpZero) ratio = (r > 0.0) ? ldexp(1.0, ee) / r : 1e300;
         }
-        blk_stats[blockIdx.x * 4 + 0] = s0;
-        blk_stats[blockIdx.x * 4 + 1] = s1;
-        blk_stats[blockIdx.x * 4 + 2] = s2;
-        blk_stats[blockIdx.x * 4 + 3] = s3;
+        const double v0 = warp_sum(rowsum), v1 = warp_sum(r), v2 = warp_sum(r * r),
+                     v3 = warp_max(ratio);
+        if (lane == 0) {
+            blk_stats[blockIdx.x * 4 + 0] = v0;
+            blk_stats[blockIdx.x * 4 + 1] = v1;
+            blk_stats[blockIdx.x * 4 + 2] = v2;
+            blk_stats[blockIdx.x * 4 + 3] = v3;
+        }
     }
 }
 
@@ -377,7 +388,7 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
         k1_tile_pairs<float><<<w.grid, kK1Threads + 32, k1_smem<float>(), st>>>(
             *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
     }
-    const int nblk = static_cast<int>((n + 255) / 256);
+    const int nblk = static_cast<int>((n + kRmRows - 1) / kRmRows);
     k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, w.pexp, part_ld, nbt, static_cast<int>(n),
                                       row_mean, row_exp, w.blk_stats);
     k1_finalize<<<1, 256, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),

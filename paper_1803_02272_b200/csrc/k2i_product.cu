@@ -687,20 +687,24 @@ __global__ void __launch_bounds__(256) k_colmax_partial(const double* __restrict
             fmax(fmax(shm[c * 4], shm[c * 4 + 1]), fmax(shm[c * 4 + 2], shm[c * 4 + 3]));
 }
 
-// f_c with max |X_c| 2^-f_c < 1/4
-__global__ void k_colexp(const double* __restrict__ pmax, int P, int wp, int nb,
-                         int* __restrict__ col_exp) {
-    for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+// f_c with max |X_c| 2^-f_c < 1/4 (one warp per column, max is exact in any order)
+__global__ void __launch_bounds__(1024) k_colexp(const double* __restrict__ pmax, int P, int wp,
+                                                 int nb, int* __restrict__ col_exp) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < nb; c += blockDim.x >> 5) {
         double m = 0.0;
         if (c < wp)
-            for (int b = 0; b < P; ++b) m = fmax(m, pmax[static_cast<size_t>(b) * wp + c]);
-        int f = kExpZeroI8;
-        if (m > 0.0) {
-            int e;
-            frexp(m, &e);  // m < 2^e
-            f = e + 2;
+            for (int b = lane; b < P; b += 32) m = fmax(m, pmax[static_cast<size_t>(b) * wp + c]);
+        m = warp_max(m);
+        if (lane == 0) {
+            int f = kExpZeroI8;
+            if (m > 0.0) {
+                int e;
+                frexp(m, &e);  // m < 2^e
+                f = e + 2;
+            }
+            col_exp[c] = f;
         }
-        col_exp[c] = f;
     }
 }
 
@@ -814,7 +818,7 @@ void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, 
                 const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
                 const int* skip) {
     k_colmax_partial<<<p.colmax_grid, 256, wp * 4 * sizeof(double), st>>>(x, x_rows_pad, wp, pmax);
-    k_colexp<<<1, 64, 0, st>>>(pmax, p.colmax_grid, wp, p.nb, col_exp);
+    k_colexp<<<1, 1024, 0, st>>>(pmax, p.colmax_grid, wp, p.nb, col_exp);
     {
         const long long items = static_cast<long long>(p.nks) * p.nb * 8;
         const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));

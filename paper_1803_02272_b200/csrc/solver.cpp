@@ -43,7 +43,7 @@ StatsOut run_k1(Store& s) {
     w.part = static_cast<double*>(c.scratch("k1_part", k1_part_elems(n) * sizeof(double)));
     w.cta_stats = static_cast<double*>(c.scratch("k1_cta", static_cast<size_t>(w.grid) * 4 * 8));
     w.pexp = static_cast<int*>(c.scratch("k1_pexp", k1_part_elems(n) * sizeof(int)));
-    w.blk_stats = static_cast<double*>(c.scratch("k1_blk", ((n + 255) / 256) * 4 * 8 + 64));
+    w.blk_stats = static_cast<double*>(c.scratch("k1_blk", ((n + 31) / 32) * 4 * 8 + 64));
     StatsOut o;
     o.row_mean = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * sizeof(double));
     o.row_exp = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * sizeof(int));
@@ -191,6 +191,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     // integer-tensor-core product (k2i_product.cu) for lazy grams of moderate
     // dynamic range; the fp64 DMMA kernel otherwise
     const bool use_i8 = lazy && use_int8_product(*g.gram, wp);
+    c.last_product_kernel = use_i8 ? 1 : 0;
     K2iPlan iplan;
     double* pmax = nullptr;
     int* col_exp = nullptr;
