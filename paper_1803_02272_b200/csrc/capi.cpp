@@ -10,6 +10,7 @@
 #include <fstream>
 #include <new>
 #include <sstream>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -25,9 +26,24 @@ struct divscope_readset {
 struct divscope_matrix {
     dsb::Matrix m;
 };
-struct divscope_embedding {
+static std::vector<std::string> index_ids(size_t n) {
     std::vector<std::string> ids;
+    ids.reserve(n);
+    for (size_t i = 0; i < n; ++i) ids.push_back(std::to_string(i));
+    return ids;
+}
+
+struct divscope_embedding {
+    // default ids "0".."n-1" (ref capi.cpp:345-348) are materialized on first
+    // use: an embed call should not pay n string allocations it may not need
+    std::vector<std::string> ids;
+    bool default_ids = false;
+    std::once_flag ids_once;
     dsb::Embedding emb;
+    const std::vector<std::string>& id_list() {
+        if (default_ids) std::call_once(ids_once, [this] { ids = index_ids(emb.n); });
+        return ids;
+    }
 };
 
 namespace {
@@ -70,12 +86,6 @@ dsb::SolverOptions to_options(const divscope_solver_options* o) {  // ref capi.c
     return opts;
 }
 
-std::vector<std::string> index_ids(size_t n) {
-    std::vector<std::string> ids;
-    ids.reserve(n);
-    for (size_t i = 0; i < n; ++i) ids.push_back(std::to_string(i));
-    return ids;
-}
 
 // ref src/mds.cpp:152-188
 void write_embedding_tsv(const dsb::Embedding& e, const std::vector<std::string>& ids,
@@ -374,7 +384,10 @@ divscope_status divscope_embed(const divscope_matrix* gram, const divscope_solve
                                ? dsb::embed_sharded(gram->m, opts->rank, to_options(opts))
                                : dsb::embed(gram->m, opts->rank, to_options(opts));
         auto* handle = new divscope_embedding;
-        handle->ids = ids ? ids->ids : index_ids(e.n);
+        if (ids)
+            handle->ids = ids->ids;
+        else
+            handle->default_ids = true;
         handle->emb = std::move(e);
         *out = handle;
     });
@@ -394,8 +407,10 @@ size_t divscope_embedding_rows(const divscope_embedding* e) { return e ? e->emb.
 size_t divscope_embedding_dims(const divscope_embedding* e) { return e ? e->emb.r : 0; }
 
 const char* divscope_embedding_id(const divscope_embedding* e, size_t i) {
-    if (!e || i >= e->ids.size()) return nullptr;
-    return e->ids[i].c_str();
+    if (!e) return nullptr;
+    const auto& v = const_cast<divscope_embedding*>(e)->id_list();
+    if (i >= v.size()) return nullptr;
+    return v[i].c_str();
 }
 
 double divscope_embedding_get(const divscope_embedding* e, size_t i, size_t c) {
@@ -430,7 +445,7 @@ divscope_status divscope_embedding_write(const divscope_embedding* e, const char
                                          const char* meta_path) {
     if (!e || !tsv_path) return fail_invalid("null argument");
     return wrap([&] {
-        write_embedding_tsv(e->emb, e->ids, tsv_path);
+        write_embedding_tsv(e->emb, const_cast<divscope_embedding*>(e)->id_list(), tsv_path);
         if (meta_path) write_embedding_meta(e->emb, meta_path);
     });
 }

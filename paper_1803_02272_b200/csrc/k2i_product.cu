@@ -402,6 +402,12 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 // Converter warp w (2..17) handles tile rows 32 (w % 4) + lane (its TMEM lane
 // quadrant) and columns 8 p .. 8 p + 7 of the k-step, p = (w - 2) / 4.
 constexpr int kAStagesTs = 4;
+#ifndef DSB_I8_FIXED_FP64
+#define DSB_I8_FIXED_FP64 0
+#endif
+// split the fixed-point conversions between the XU pipe (F2I) and the FP64
+// pipe (fixed56): each alone saturates before the HBM rate
+constexpr bool kFixedFp64 = DSB_I8_FIXED_FP64;
 constexpr int kNbTs = 32;
 
 template <typename TD>
@@ -589,9 +595,13 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 uint32_t lo[8], hi[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);
-                    lo[j] = static_cast<uint32_t>(m);
-                    hi[j] = static_cast<uint32_t>(m >> 32);
+                    if (kFixedFp64 && (j & 1)) {
+                        fixed56(d[j] * d[j], sc, lo[j], hi[j]);  // FP64 pipe
+                    } else {
+                        const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);  // XU
+                        lo[j] = static_cast<uint32_t>(m);
+                        hi[j] = static_cast<uint32_t>(m >> 32);
+                    }
                 }
                 const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64) + lane_off;
 #pragma unroll
@@ -669,45 +679,6 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 }
 
 // ---- B digits of the panel (per pass) --------------------------------------
-// column max |X| partials (k4-interleaved panel, rows [n_pad*b/P, ...))
-__global__ void __launch_bounds__(256) k_colmax_partial(const double* __restrict__ x, size_t n_pad,
-                                                        int wp, double* __restrict__ pmax) {
-    extern __shared__ double shm[];  // [wp * 4]
-    const size_t nq = n_pad / 4;
-    const size_t q0 = nq * blockIdx.x / gridDim.x, q1 = nq * (blockIdx.x + 1) / gridDim.x;
-    const int per = wp * 4;
-    for (int e = threadIdx.x; e < per; e += blockDim.x) {
-        double m = 0.0;
-        for (size_t q = q0; q < q1; ++q) m = fmax(m, fabs(x[q * per + e]));
-        shm[e] = m;
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < wp; c += blockDim.x)
-        pmax[static_cast<size_t>(blockIdx.x) * wp + c] =
-            fmax(fmax(shm[c * 4], shm[c * 4 + 1]), fmax(shm[c * 4 + 2], shm[c * 4 + 3]));
-}
-
-// f_c with max |X_c| 2^-f_c < 1/4 (one warp per column, max is exact in any order)
-__global__ void __launch_bounds__(1024) k_colexp(const double* __restrict__ pmax, int P, int wp,
-                                                 int nb, int* __restrict__ col_exp) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int c = warp; c < nb; c += blockDim.x >> 5) {
-        double m = 0.0;
-        if (c < wp)
-            for (int b = lane; b < P; b += 32) m = fmax(m, pmax[static_cast<size_t>(b) * wp + c]);
-        m = warp_max(m);
-        if (lane == 0) {
-            int f = kExpZeroI8;
-            if (m > 0.0) {
-                int e;
-                frexp(m, &e);  // m < 2^e
-                f = e + 2;
-            }
-            col_exp[c] = f;
-        }
-    }
-}
-
 // one thread per (k-step, column, 4 rows): balanced base-256 digits of
 // round(X 2^(56 - f_c)), written as 7 byte planes in the UMMA layout
 __global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__ x, int nks, int wp,
@@ -817,8 +788,8 @@ void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, 
                 unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
                 const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
                 const int* skip) {
-    k_colmax_partial<<<p.colmax_grid, 256, wp * 4 * sizeof(double), st>>>(x, x_rows_pad, wp, pmax);
-    k_colexp<<<1, 1024, 0, st>>>(pmax, p.colmax_grid, wp, p.nb, col_exp);
+    (void)x_rows_pad;
+    (void)pmax;  // column exponents come from launch_colsums (same pass over X)
     {
         const long long items = static_cast<long long>(p.nks) * p.nb * 8;
         const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
@@ -839,7 +810,7 @@ void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, 
     if (e1) cudaEventRecord(e1, st);
     launch_k2_reduce(wp, kRowsI8, part, p.maxseg, p.nks, p.total, p.grid, p.nrows, 1, row_mean,
                      scalars, colsums, y, st, skip);
-    count_launch(5);
+    count_launch(3);
 }
 
 }  // namespace dsb

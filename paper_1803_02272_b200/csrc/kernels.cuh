@@ -112,8 +112,11 @@ void launch_panel_from_rowmajor(const double* src, size_t n, int w, int wp, size
 void launch_panel_to_rowmajor(const double* src, size_t n, int w, int wp, double* dst,
                               cudaStream_t st);
 // colsums[0..wp) = 1^T X, colsums[wp..2wp) = r^T X (deterministic 2-level)
+// With pmax/col_exp (int8 product): also the column max partials [P][wp] and
+// the column exponents col_exp[0..nb) of the panel digits.
 void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_pad, int wp,
-                    double* partial, double* colsums, int sms, cudaStream_t st);
+                    double* partial, double* colsums, int sms, cudaStream_t st,
+                    double* pmax = nullptr, int nb = 0, int* col_exp = nullptr);
 // out (wp x wp) = A^T B (deterministic 2-level)
 void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, double* partial,
                       double* out, int sms, cudaStream_t st);

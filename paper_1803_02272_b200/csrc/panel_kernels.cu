@@ -44,26 +44,30 @@ __global__ void k_panel_to_rowmajor(const double* __restrict__ src, size_t n, in
     }
 }
 
-// colsum partials: CTA c handles k4 row blocks [nq c / P, nq (c+1) / P)
+// colsum partials: CTA c handles k4 row blocks [nq c / P, nq (c+1) / P);
+// optionally also the column max |x| (int8 product: column exponents)
 __global__ void __launch_bounds__(256) k_colsum_partial(const double* __restrict__ x,
                                                         const double* __restrict__ row_mean,
                                                         size_t n, size_t n_pad, int wp,
-                                                        double* __restrict__ partial) {
-    extern __shared__ double sh[];  // [2][wp*4]
+                                                        double* __restrict__ partial,
+                                                        double* __restrict__ pmax) {
+    extern __shared__ double sh[];  // [3][wp*4]
     const size_t nq = n_pad / 4;
     const size_t q0 = nq * blockIdx.x / gridDim.x, q1 = nq * (blockIdx.x + 1) / gridDim.x;
     const int per = wp * 4;
     for (int e = threadIdx.x; e < per; e += blockDim.x) {
-        double s = 0.0, t = 0.0;
+        double s = 0.0, t = 0.0, m = 0.0;
         const int rr = e & 3;
         for (size_t q = q0; q < q1; ++q) {
             const double v = x[q * per + e];
             const size_t i = q * 4 + rr;
             s += v;
+            m = fmax(m, fabs(v));
             if (i < n) t += row_mean[i] * v;
         }
         sh[e] = s;
         sh[per + e] = t;
+        sh[2 * per + e] = m;
     }
     __syncthreads();
     for (int c = threadIdx.x; c < wp; c += blockDim.x) {
@@ -72,29 +76,57 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const double* __restrict
             ((sh[per + 4 * c] + sh[per + 4 * c + 1]) + sh[per + 4 * c + 2]) + sh[per + 4 * c + 3];
         partial[static_cast<size_t>(blockIdx.x) * 2 * wp + c] = s;
         partial[static_cast<size_t>(blockIdx.x) * 2 * wp + wp + c] = t;
+        if (pmax) {
+            const double* mm = sh + 2 * per + 4 * c;
+            pmax[static_cast<size_t>(blockIdx.x) * wp + c] =
+                fmax(fmax(mm[0], mm[1]), fmax(mm[2], mm[3]));
+        }
     }
 }
 
 // out[e] = sum_c partial[c][e]. A block owns 32 consecutive e (one per lane);
-// its 8 warps take fixed strided subsets of c, combined in warp order, so the
+// its 32 warps take fixed strided subsets of c, combined in warp order, so the
 // result is deterministic for a fixed P.
-__global__ void __launch_bounds__(256) k_sum_partials(const double* __restrict__ partial, int P,
-                                                      int m, double* __restrict__ out) {
-    __shared__ double sh[8][32];
+__global__ void __launch_bounds__(1024) k_sum_partials(const double* __restrict__ partial, int P,
+                                                       int m, double* __restrict__ out) {
+    __shared__ double sh[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * 32 + lane;
     double s = 0.0;
     if (e < m) {
 #pragma unroll 4
-        for (int c = warp; c < P; c += 8) s += partial[static_cast<size_t>(c) * m + e];
+        for (int c = warp; c < P; c += 32) s += partial[static_cast<size_t>(c) * m + e];
     }
     sh[warp][lane] = s;
     __syncthreads();
     if (warp == 0 && e < m) {
         double t = sh[0][lane];
 #pragma unroll
-        for (int w = 1; w < 8; ++w) t += sh[w][lane];
+        for (int w = 1; w < 32; ++w) t += sh[w][lane];
         out[e] = t;
+    }
+}
+
+// column exponents f_c for the int8 panel digits: max |X_c| 2^-f_c < 1/4
+// (one warp per column; max is exact in any order)
+__global__ void __launch_bounds__(1024) k_colexp_final(const double* __restrict__ pmax, int P,
+                                                       int wp, int nb, int* __restrict__ col_exp) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < nb; c += blockDim.x >> 5) {
+        double m = 0.0;
+        if (c < wp)
+    #pragma unroll 8
+            for (int b = lane; b < P; b += 32) m = fmax(m, pmax[static_cast<size_t>(b) * wp + c]);
+        m = warp_max(m);
+        if (lane == 0) {
+            int f = -1100;
+            if (m > 0.0) {
+                int e;
+                frexp(m, &e);  // m < 2^e
+                f = e + 2;
+            }
+            col_exp[c] = f;
+        }
     }
 }
 
@@ -372,12 +404,17 @@ void launch_panel_to_rowmajor(const double* src, size_t n, int w, int wp, double
 }
 
 void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_pad, int wp,
-                    double* partial, double* colsums, int sms, cudaStream_t st) {
+                    double* partial, double* colsums, int sms, cudaStream_t st, double* pmax,
+                    int nb, int* col_exp) {
     const int P = panel_grid(n_pad, sms);
-    k_colsum_partial<<<P, 256, 2 * wp * 4 * sizeof(double), st>>>(x, row_mean, n, n_pad, wp,
-                                                                  partial);
-    k_sum_partials<<<(2 * wp + 31) / 32, 256, 0, st>>>(partial, P, 2 * wp, colsums);
+    k_colsum_partial<<<P, 256, 3 * wp * 4 * sizeof(double), st>>>(x, row_mean, n, n_pad, wp,
+                                                                  partial, pmax);
+    k_sum_partials<<<(2 * wp + 31) / 32, 1024, 0, st>>>(partial, P, 2 * wp, colsums);
     count_launch(2);
+    if (pmax && col_exp) {
+        k_colexp_final<<<1, 1024, 0, st>>>(pmax, P, wp, nb, col_exp);
+        count_launch(1);
+    }
 }
 
 void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, double* partial,
@@ -395,7 +432,7 @@ void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, do
         default:
             throw std::invalid_argument("unsupported panel width");
     }
-    k_sum_partials<<<(wp * wp + 31) / 32, 256, 0, st>>>(partial, P, wp * wp, out);
+    k_sum_partials<<<(wp * wp + 31) / 32, 1024, 0, st>>>(partial, P, wp * wp, out);
     count_launch(2);
 }
 

@@ -6,12 +6,14 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <deque>
 #include <thread>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <tuple>
 
@@ -198,8 +200,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     unsigned char* bdig = nullptr;
     if (use_i8) {
         iplan = k2i_plan(n, n, wp, c.sms);
-        pmax = static_cast<double*>(
-            c.scratch("i8_pmax", static_cast<size_t>(iplan.colmax_grid) * wp * sizeof(double)));
+        pmax = static_cast<double*>(c.scratch(
+            "i8_pmax", static_cast<size_t>(panel_grid(n_pad, c.sms)) * wp * sizeof(double)));
         col_exp = static_cast<int*>(c.scratch("i8_colexp", 64 * sizeof(int)));
         bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
     }
@@ -241,8 +243,30 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         DSB_CUDA(cudaMemcpyAsync(P0, cached, pbytes, cudaMemcpyDeviceToDevice, c.stream));
     }
 
+    // DSB_TRACE=1: device timestamps between the stages of this solve (stderr)
+    static const bool trace = std::getenv("DSB_TRACE") != nullptr;
+    const auto h0 = std::chrono::steady_clock::now();
+    auto host_us = [&] {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0)
+            .count();
+    };
+    std::vector<std::pair<const char*, cudaEvent_t>> marks;
+    auto mark = [&](const char* what_) {
+        if (!trace) return;
+        std::fprintf(stderr, "[trace] host at %-10s %.1f us\n", what_, host_us());
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, c.stream);
+        marks.emplace_back(what_, e);
+    };
+    mark("start");
+    if (trace) std::fprintf(stderr, "[trace] host setup %.1f us\n", host_us());
     auto product = [&](const double* x, double* y) {
-        if (mode) launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
+        if (use_i8)
+            launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream, pmax,
+                           iplan.nb, col_exp);
+        else if (mode)
+            launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
         cudaEvent_t e0, e1;
         c.make_events(&e0, &e1);
         if (use_i8)
@@ -252,12 +276,15 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
             launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums,
                       y, n_pad, c.stream, e0, e1);
         c.add_timed(1, e0, e1);
+        mark("product");
     };
     // CholeskyQR3 with shift/drop handling: y -> t -> y -> out
     auto orth = [&](double* y, double* t, double* out) {
         if (wp <= 64 &&
-            launch_orth_fused(y, t, out, n_pad, wp, wi, n, psmall, wmat, flags, c.sms, c.stream))
+            launch_orth_fused(y, t, out, n_pad, wp, wi, n, psmall, wmat, flags, c.sms, c.stream)) {
+            mark("orth");
             return;
+        }
         launch_panel_dot(y, y, n_pad, wp, psmall, wmat, c.sms, c.stream);
         launch_chol_inv(wmat, wp, wi, n, 1, rinv, flags, c.stream);
         launch_panel_apply(y, rinv, n_pad, wp, t, c.stream);
@@ -296,8 +323,10 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     eo.kept_vals = static_cast<double*>(c.scratch("evd_kept", kMaxWP * sizeof(double)));
     eo.dmeta = static_cast<double*>(c.scratch("evd_dmeta", 8 * sizeof(double)));
     eo.imeta = static_cast<int*>(c.scratch("evd_imeta", 8 * sizeof(int)));
+    mark("ritz_gram");
     launch_evd(wmat, wp, wi, static_cast<int>(rank), static_cast<int>(req), scal_dev, fro_index,
                eo, c.stream);
+    mark("evd");
     double* coords = nullptr;
     if (what == What::Embed) {
         coords = static_cast<double*>(c.scratch("coords", n * std::max<size_t>(req, 1) * 8));
@@ -319,7 +348,18 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     DSB_CUDA(cudaMemcpyAsync(meta.vals, eo.vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
     DSB_CUDA(cudaMemcpyAsync(meta.kept, eo.kept_vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
     DSB_CUDA(cudaMemcpyAsync(meta.dmeta, eo.dmeta, 8 * 8, cudaMemcpyDeviceToHost, c.stream));
+    mark("lift");
+    if (trace) std::fprintf(stderr, "[trace] host enqueue done %.1f us\n", host_us());
     c.d2h_copy(meta.imeta, eo.imeta, 8 * sizeof(int));
+    if (trace) std::fprintf(stderr, "[trace] host meta synced %.1f us\n", host_us());
+    if (trace) {
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+            std::fprintf(stderr, "[trace] %-10s %8.1f us\n", marks[i].first, ms * 1e3);
+        }
+        for (auto& m : marks) cudaEventDestroy(m.second);
+    }
     c.d2h += w * 16 + 64;
     c.last_evd_sweeps = meta.imeta[3];
     {
@@ -343,6 +383,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         e.coords.resize(n * e.r);
         if (e.r) c.d2h_copy(e.coords.data(), coords, n * e.r * sizeof(double));
     }
+    if (trace) std::fprintf(stderr, "[trace] host coords done %.1f us\n", host_us());
     return out;
 }
 
