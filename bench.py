@@ -283,27 +283,39 @@ def b200_arm(args, wl):
     flops_per_launch = 2.0 * m_rows * n * w
     tflops = flops_per_launch / (k2_ms * 1e-3) / 1e12
     gbs = bytes_per_launch / (k2_ms * 1e-3) / 1e9
+    int8_path = int(st.last_product_kernel) == 1
+    kname = "k2i_product" if int8_path else "k2_product"
     traffic = None
     tp = ROOT / "profiles" / "k2_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(wl)
+            tv = json.loads(tp.read_text()).get(wl)
+            traffic = tv.get(kname) if isinstance(tv, dict) else (None if int8_path else tv)
         except Exception:
             traffic = None
-    roofline = {
-        "bound": "tensor", "achieved": tflops, "peak": fp64_peak, "unit": "TFLOP/s",
-        "frac": tflops / fp64_peak, "traffic": traffic,
-        "kernel": "k2_product (DMMA f64) — FP64-bound at this w; HBM shown alongside",
-        "peak_source": "live f64 DMMA microbenchmark (divscope_fp64_tensor_peak_tflops)",
-        "k2_avg_ms": k2_ms, "k2_launches": int(st.product_launches),
-        "flops_per_launch": flops_per_launch, "bytes_per_launch": bytes_per_launch,
-        "hbm": {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
-                else "fallback 6650 GB/s (B200_PROFILING.md)"},
-        "pass0": {"k1_avg_ms": st.stats_ms / max(st.stats_launches, 1),
-                  "achieved_gbs": m_rows * n * (4 if f32 else 8) /
-                  (st.stats_ms / max(st.stats_launches, 1) * 1e-3) / 1e9},
-    }
+    hbm = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
+           else "fallback 6650 GB/s (B200_PROFILING.md)"}
+    common = {"k2_avg_ms": k2_ms, "k2_launches": int(st.product_launches),
+              "flops_per_launch": flops_per_launch, "bytes_per_launch": bytes_per_launch,
+              "pass0": {"k1_avg_ms": st.stats_ms / max(st.stats_launches, 1),
+                        "achieved_gbs": m_rows * n * (4 if f32 else 8) /
+                        (st.stats_ms / max(st.stats_launches, 1) * 1e-3) / 1e9}}
+    if int8_path:
+        # exact integer slice product on the int8 tensor cores: one read of D
+        # per pass, HBM-bound; the f64-equivalent flop rate shown alongside
+        roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": gbs / hbm_peak, "traffic": traffic,
+                    "kernel": "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)",
+                    "peak_source": hbm["peak_source"],
+                    "fp64_equiv": {"achieved": tflops, "unit": "TFLOP/s",
+                                   "fp64_dmma_peak": fp64_peak}, **common}
+    else:
+        roofline = {"bound": "tensor", "achieved": tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": tflops / fp64_peak, "traffic": traffic,
+                    "kernel": "k2_product (DMMA f64) — FP64-bound at this w; HBM shown alongside",
+                    "peak_source": "live f64 DMMA microbenchmark (divscope_fp64_tensor_peak_tflops)",
+                    "hbm": hbm, **common}
 
     # ---- e2e leg through the C ABI from pinned host memory
     e2e = None

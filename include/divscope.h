@@ -256,7 +256,7 @@ typedef struct divscope_stats {
     int32_t last_evd_sweeps;    /* Jacobi sweeps of the last Rayleigh-Ritz EVD */
     int32_t last_orth_shifted;  /* 1 if a shifted CholeskyQR step was needed */
     int32_t last_power_iters;   /* power iterations of the last stable_rank */
-    int32_t reserved0;
+    int32_t last_product_kernel; /* 0 fp64 DMMA (k2_product), 1 int8 slice product */
 } divscope_stats;
 
 /* timing on => CUDA events are recorded around K1/K2 on the library stream */
