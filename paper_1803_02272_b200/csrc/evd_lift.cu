@@ -11,6 +11,7 @@
 // (round-robin tournament ordering), updating every 2x2 block of B and
 // every row pair of V independently — two barriers per round, no atomics.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_utils.cuh"
 #include "kernels.cuh"
@@ -128,10 +129,29 @@ __device__ int jacobi_converged(const double* __restrict__ A, int w, double* red
 
 // Shared tail: reference ordering (rsvd.cpp:118-127), keep / resid
 // (rsvd.cpp:129-142), embed filter (mds.cpp:85-99), V_keep.
+// dg: the w eigenvalues (diagonal of the converged A); V row-major with
+// leading dimension ldv
+__device__ void evd_finish_dg(const double* __restrict__ dg, const double* __restrict__ V,
+                              int ldv, int w, int rank, int requested,
+                              const double* __restrict__ scalars, int fro_index, const EvdOut& o,
+                              int sweeps, int done, int* __restrict__ order,
+                              int* __restrict__ kept);
+
 __device__ void evd_finish(const double* __restrict__ A, const double* __restrict__ V, int w,
                            int rank, int requested, const double* __restrict__ scalars,
                            int fro_index, const EvdOut& o, int sweeps, int done,
                            int* __restrict__ order, int* __restrict__ kept) {
+    __shared__ double dg[kMaxWP];
+    for (int a = threadIdx.x; a < w; a += blockDim.x) dg[a] = A[pk(a, a, w)];
+    __syncthreads();
+    evd_finish_dg(dg, V, w, w, rank, requested, scalars, fro_index, o, sweeps, done, order, kept);
+}
+
+__device__ void evd_finish_dg(const double* __restrict__ dg, const double* __restrict__ V,
+                              int ldv, int w, int rank, int requested,
+                              const double* __restrict__ scalars, int fro_index, const EvdOut& o,
+                              int sweeps, int done, int* __restrict__ order,
+                              int* __restrict__ kept) {
     const int tid = threadIdx.x, nt = blockDim.x;
     // Reference order (rsvd.cpp:118-127 applied to Eigen's ascending output):
     // ascending stable sort, then stable sort by |lambda| desc, positive first.
@@ -140,11 +160,11 @@ __device__ void evd_finish(const double* __restrict__ A, const double* __restric
     // (equal values keep the ascending sort's index order). Each thread
     // computes its element's rank by counting predecessors.
     for (int a = tid; a < w; a += nt) {
-        const double la = A[pk(a, a, w)];
+        const double la = dg[a];
         int pos = 0;
         for (int b = 0; b < w; ++b) {
             if (b == a) continue;
-            const double lb = A[pk(b, b, w)];
+            const double lb = dg[b];
             const bool b_first = (fabs(lb) != fabs(la)) ? (fabs(lb) > fabs(la))
                                  : (lb != la)           ? (lb > la)
                                                         : (b < a);
@@ -158,7 +178,7 @@ __device__ void evd_finish(const double* __restrict__ A, const double* __restric
         // equal to rounding (|la| and |lb| within 4 ulps): the reference's
         // exact tie comes out of Eigen's EVD; ours can differ in the last bit.
         for (int a = 0; a + 1 < w; ++a) {
-            const double x = A[pk(order[a], order[a], w)], y = A[pk(order[a + 1], order[a + 1], w)];
+            const double x = dg[order[a]], y = dg[order[a + 1]];
             if (x < 0.0 && y > 0.0 && fabs(fabs(x) - y) <= 4.0 * 0x1.0p-52 * fabs(x)) {
                 const int t = order[a];
                 order[a] = order[a + 1];
@@ -167,7 +187,7 @@ __device__ void evd_finish(const double* __restrict__ A, const double* __restric
         }
         const int keep = min(rank, w);
         double sumsq = 0.0, maxabs = 0.0;
-        for (int a = 0; a < w; ++a) o.vals[a] = A[pk(order[a], order[a], w)];
+        for (int a = 0; a < w; ++a) o.vals[a] = dg[order[a]];
         for (int a = 0; a < keep; ++a) {
             const double lam = o.vals[a];
             sumsq += lam * lam;
@@ -192,13 +212,13 @@ __device__ void evd_finish(const double* __restrict__ A, const double* __restric
         o.imeta[2] = cnt < requested ? 1 : 0;
         o.imeta[3] = sweeps;
         o.imeta[4] = done;
-        for (int c = 0; c < cnt; ++c) o.kept_vals[c] = A[pk(kept[c], kept[c], w)];
+        for (int c = 0; c < cnt; ++c) o.kept_vals[c] = dg[kept[c]];
     }
     __syncthreads();
     const int r = o.imeta[1];
     for (int e = tid; e < w * requested; e += nt) {
         const int x = e / requested, c = e % requested;
-        o.vkeep[e] = c < r ? V[x * w + kept[c]] : 0.0;
+        o.vkeep[e] = c < r ? V[x * ldv + kept[c]] : 0.0;
     }
 }
 
@@ -295,99 +315,6 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
         g_evd_prof[4] = clock64() - t_b;
         g_evd_prof[5] = sweeps;
     }
-}
-
-// Small-w kernel (w <= 64): A double-buffered, so every thread computes the
-// (redundant, identical) rotations it needs from the previous round's A and
-// a round costs ONE barrier; V is rotated one round behind with the
-// rotations the diagonal-block threads published.
-__global__ void __launch_bounds__(kEvdThreads) k_evd_small(const double* __restrict__ bmat, int wp,
-                                                           int w, int rank, int requested,
-                                                           const double* __restrict__ scalars,
-                                                           int fro_index, EvdOut o) {
-    extern __shared__ double sm[];
-    const int npk = w * (w + 1) / 2;
-    double* Abuf[2] = {sm, sm + npk};
-    double* V = sm + 2 * npk;  // [w][w]
-    __shared__ double cs[2][33], sn[2][33];
-    __shared__ unsigned char pp[2][33], qq[2][33];
-    __shared__ double red[64];
-    __shared__ int order[kMaxWP], kept[kMaxWP];
-    __shared__ unsigned char blk_i[32 * 33 / 2], blk_j[32 * 33 / 2];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int a = tid; a < w; a += nt)
-        for (int b = a; b < w; ++b)
-            Abuf[0][pk(a, b, w)] = 0.5 * (bmat[a * wp + b] + bmat[b * wp + a]);
-    for (int e = tid; e < w * w; e += nt) V[e] = (e / w == e % w) ? 1.0 : 0.0;
-    const int m = w + (w & 1), h = m / 2, nblk = h * (h + 1) / 2;
-    for (int i = tid; i < h; i += nt) {
-        const int base = i * h - (i * (i - 1)) / 2;
-        for (int j = i; j < h; ++j) {
-            blk_i[base + j - i] = static_cast<unsigned char>(i);
-            blk_j[base + j - i] = static_cast<unsigned char>(j);
-        }
-    }
-    if (tid < 33) {
-        cs[0][tid] = cs[1][tid] = 1.0;
-        sn[0][tid] = sn[1][tid] = 0.0;
-        pp[0][tid] = pp[1][tid] = 0;
-        qq[0][tid] = qq[1][tid] = 255;
-    }
-    __syncthreads();
-    int cur = 0, slot = 0, done = (w <= 1), sweeps = 0;
-    for (; sweeps < 60 && !done; ++sweeps) {
-        for (int r = 0; r < m - 1; ++r) {
-            const double* Ain = Abuf[cur];
-            double* Aout = Abuf[cur ^ 1];
-            for (int e = tid; e < nblk; e += nt) {
-                const int i = blk_i[e], j = blk_j[e];
-                int pi, qi, pj, qj;
-                pair_at(r, i, m, pi, qi);
-                pair_at(r, j, m, pj, qj);
-                double ci = 1.0, si = 0.0, cj = 1.0, sj = 0.0;
-                if (qi < w) jacobi_rot(Ain[pk(pi, pi, w)], Ain[pk(qi, qi, w)], Ain[pk(pi, qi, w)], ci, si);
-                if (i == j) {
-                    cj = ci;
-                    sj = si;
-                    cs[slot][i] = ci;
-                    sn[slot][i] = si;
-                    pp[slot][i] = static_cast<unsigned char>(pi);
-                    qq[slot][i] = static_cast<unsigned char>(qi);
-                } else if (qj < w) {
-                    jacobi_rot(Ain[pk(pj, pj, w)], Ain[pk(qj, qj, w)], Ain[pk(pj, qj, w)], cj, sj);
-                }
-                block_update(Ain, Aout, w, pi, qi, pj, qj, ci, si, cj, sj, i == j);
-            }
-            // V with the previous round's rotations (slot ^ 1)
-            for (int e = tid; e < w * h; e += nt) {
-                const int k = e / h, i = e % h;
-                const int p = pp[slot ^ 1][i], q = qq[slot ^ 1][i];
-                if (q < w) {
-                    const double c = cs[slot ^ 1][i], s = sn[slot ^ 1][i];
-                    const double vp = V[k * w + p], vq = V[k * w + q];
-                    V[k * w + p] = c * vp - s * vq;
-                    V[k * w + q] = s * vp + c * vq;
-                }
-            }
-            __syncthreads();
-            cur ^= 1;
-            slot ^= 1;
-        }
-        done = jacobi_converged(Abuf[cur], w, red);
-    }
-    // last round's rotations still owe V
-    for (int e = tid; e < w * h; e += nt) {
-        const int k = e / h, i = e % h;
-        const int p = pp[slot ^ 1][i], q = qq[slot ^ 1][i];
-        if (q < w) {
-            const double c = cs[slot ^ 1][i], s = sn[slot ^ 1][i];
-            const double vp = V[k * w + p], vq = V[k * w + q];
-            V[k * w + p] = c * vp - s * vq;
-            V[k * w + q] = s * vp + c * vq;
-        }
-    }
-    __syncthreads();
-    evd_finish(Abuf[cur], V, w, rank, requested, scalars, fro_index, o, sweeps, done, order, kept);
 }
 
 // U = Q V_keep (n x r, row-major into coords). CTA c owns rows
@@ -498,13 +425,7 @@ extern "C" void divscope_debug_evd_prof(long long* host16) {
 
 void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
                 const double* scalars, int fro_index, const EvdOut& o, cudaStream_t st) {
-    if (false) {
-        const size_t smem = (static_cast<size_t>(w) * (w + 1) + static_cast<size_t>(w) * w) *
-                            sizeof(double);
-        allow_dyn_smem(reinterpret_cast<const void*>(k_evd_small));
-        const int threads = w <= 32 ? 128 : 512;
-        k_evd_small<<<1, threads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
-    } else {
+    {
         const size_t smem = (static_cast<size_t>(w) * (w + 1) / 2 + static_cast<size_t>(w) * w) *
                             sizeof(double);
         allow_dyn_smem(reinterpret_cast<const void*>(k_evd));

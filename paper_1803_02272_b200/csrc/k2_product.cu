@@ -224,21 +224,26 @@ __global__ void __launch_bounds__(256)
               const int* __restrict__ skip) {
     if (skip && *skip) return;
     constexpr int kRows = 32;  // rows of the BM-row block handled by this CTA
+    constexpr int kMaxSlots = 256;  // >= grid + 1 (a row block spans <= grid CTAs)
+    __shared__ long long slot_base[kMaxSlots];
     const int b = blockIdx.x / (BM / kRows);
     const int r0 = (blockIdx.x % (BM / kRows)) * kRows;
+    // CTAs whose stream-K range touches row block b, and their slot offsets
     const long long c_lo = cta_of(static_cast<long long>(b) * nk, total, P);
     const long long c_hi = cta_of(static_cast<long long>(b + 1) * nk - 1, total, P);
     const int nslot = static_cast<int>(c_hi - c_lo + 1);
+    for (int k = threadIdx.x; k < nslot && k < kMaxSlots; k += blockDim.x) {
+        const long long cc = c_lo + k;
+        const int seg = b - static_cast<int>(chunk_begin(total, cc, P) / nk);
+        slot_base[k] = (cc * maxseg + seg) * static_cast<long long>(BM) * WP;
+    }
+    __syncthreads();
     const double g = mode ? scalars[S_GRAND] : 0.0;
     for (int e = threadIdx.x; e < kRows * WP; e += blockDim.x) {
         const int r = r0 + e / WP, col = e % WP;
         const int eo = r * WP + col;
         double v = 0.0;
-        for (int sl = 0; sl < nslot; ++sl) {
-            const long long cc = c_lo + sl;
-            const int seg = b - static_cast<int>(chunk_begin(total, cc, P) / nk);
-            v += part[(static_cast<size_t>(cc) * maxseg + seg) * BM * WP + eo];
-        }
+        for (int sl = 0; sl < nslot; ++sl) v += part[slot_base[sl] + eo];
         const size_t i = static_cast<size_t>(b) * BM + r;
         if (i >= static_cast<size_t>(n)) {
             v = 0.0;
