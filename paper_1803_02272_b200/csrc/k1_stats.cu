@@ -95,6 +95,7 @@ __device__ __forceinline__ const T* tile_at(const unsigned char* tile, int r, in
 // order like the values; integer max keeps this off the FP64 pipe).
 // kExpZero when all are zero.
 constexpr int kExpZero = -1100;
+__device__ __forceinline__ double max_keep(double m, double x) { return x > m ? x : m; }
 __device__ __forceinline__ uint32_t hi_bits(double x) {
     return static_cast<uint32_t>(__double2hiint(x));
 }
@@ -173,11 +174,16 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
             rs += sq;
             rmx = max(rmx, hi_bits(sq));
             sum4 += sq * sq;
-            maxabs = fmax(maxabs, fabs(a[j]));
-            if (I != J || q * 16 + j >= r) maxabs_up = fmax(maxabs_up, fabs(a[j]));
+            // (x > m ? x : m): NaN is never selected, as std::max(m, x) in the
+            // reference's scans (mds.cpp:21-27, rsvd.cpp:50-54); cheaper than fmax
+            if (I != J || q * 16 + j >= r) maxabs_up = max_keep(maxabs_up, fabs(a[j]));
             // symmetry: A[r][c] vs B[c][r] (d_ij vs d_ji)
             const double m = static_cast<double>(*tile_at<T>(B, q * 16 + j, r));
-            maxasym = fmax(maxasym, fabs(a[j] - m));
+            maxasym = max_keep(maxasym, fabs(a[j] - m));
+        }
+        if (I == J) {  // diagonal tile: maxabs_up saw only its upper part
+#pragma unroll
+            for (int j = 0; j < 16; ++j) maxabs = max_keep(maxabs, fabs(a[j]));
         }
         rs += __shfl_xor_sync(0xffffffffu, rs, 8);
         rs += __shfl_xor_sync(0xffffffffu, rs, 16);
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
                 rb += sq;
                 bmx = max(bmx, hi_bits(sq));
                 sum4 += sq * sq;
-                maxabs = fmax(maxabs, fabs(b));
+                maxabs = max_keep(maxabs, fabs(b));
             }
             rb += __shfl_xor_sync(0xffffffffu, rb, 8);
             rb += __shfl_xor_sync(0xffffffffu, rb, 16);
@@ -215,6 +221,9 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
             ph ^= 1;
         }
     }
+    // every off-diagonal A tile entry is an upper entry: max|a| over all
+    // entries = max(max over upper entries, B tiles, diagonal tiles)
+    maxabs = max_keep(maxabs, maxabs_up);
     // fixed-order block reduction (deterministic for a fixed grid)
     sum4 = warp_sum(sum4);
     maxabs = warp_max(maxabs);

@@ -401,6 +401,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 // 7 x 8-column A digit planes of stage s (row = lane, byte k at column k/4).
 // Converter warp w (2..17) handles tile rows 32 (w % 4) + lane (its TMEM lane
 // quadrant) and columns 8 p .. 8 p + 7 of the k-step, p = (w - 2) / 4.
+#ifndef DSB_TS_SMEM_KB
+#define DSB_TS_SMEM_KB 208
+#endif
 constexpr int kAStagesTs = 4;
 #ifndef DSB_I8_FIXED_FP64
 #define DSB_I8_FIXED_FP64 0
@@ -412,7 +415,7 @@ constexpr int kNbTs = 32;
 
 template <typename TD>
 constexpr int d_stages_ts() {
-    return std::min(8, (208 * 1024 - kAStagesTs * b_bytes<kNbTs>()) / d_bytes<TD>());
+    return std::min(8, (DSB_TS_SMEM_KB * 1024 - kAStagesTs * b_bytes<kNbTs>()) / d_bytes<TD>());
 }
 template <typename TD>
 constexpr size_t ts_smem() {
