@@ -26,7 +26,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, size_t ld,
                                                       size_t rows, size_t cols,
                                                       double* __restrict__ rowsum,
-                                                      double* __restrict__ cta_stats) {
+                                                      double* __restrict__ cta_stats,
+                                                      int* __restrict__ row_exp) {
     __shared__ double red[2][8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t gw = static_cast<size_t>(blockIdx.x) * 8 + warp;
@@ -35,6 +36,7 @@ __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, s
     for (size_t r = gw; r < rows; r += nw) {
         const T* row = d + r * ld;
         double s = 0.0;
+        uint32_t hmx = 0u;  // max over the row of the high word of d^2 (>= 0)
         size_t c = 2 * lane;
         // main body: 4 independent 2-element loads per lane per iteration
         for (; c + 192 + 1 < cols; c += 256) {
@@ -49,6 +51,8 @@ __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, s
                 s += s0 + s1;
                 sum4 += s0 * s0 + s1 * s1;
                 maxabs = fmax(maxabs, fmax(fabs(a0), fabs(a1)));
+                hmx = max(hmx, max(static_cast<uint32_t>(__double2hiint(s0)),
+                                   static_cast<uint32_t>(__double2hiint(s1))));
             }
         }
         for (; c < cols; c += 64) {
@@ -58,9 +62,18 @@ __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, s
             s += s0 + s1;
             sum4 += s0 * s0 + s1 * s1;
             maxabs = fmax(maxabs, fmax(fabs(a0), fabs(a1)));
+            hmx = max(hmx, max(static_cast<uint32_t>(__double2hiint(s0)),
+                               static_cast<uint32_t>(__double2hiint(s1))));
         }
         s = warp_sum(s);
-        if (lane == 0) rowsum[r] = s;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) hmx = max(hmx, __shfl_xor_sync(0xffffffffu, hmx, o));
+        if (lane == 0) {
+            rowsum[r] = s;
+            // smallest e with d^2 < 2^e over the row (int8 slice scale; K1 rule)
+            const int be = static_cast<int>((hmx >> 20) & 0x7ffu);
+            row_exp[r] = hmx == 0u ? -1100 : (be == 0 ? -1022 : be - 1022);
+        }
     }
     sum4 = warp_sum(sum4);
     maxabs = warp_max(maxabs);
@@ -111,13 +124,13 @@ int k1_rows_grid(size_t rows, int sms) {
 }
 
 void launch_k1_rows(const void* d, DType dt, size_t ld, size_t rows, size_t cols, double* rowsum,
-                    double* cta_stats, int grid, cudaStream_t st) {
+                    double* cta_stats, int grid, cudaStream_t st, int* row_exp) {
     if (dt == DType::F64)
         k1_rows_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(d), ld, rows, cols,
-                                                     rowsum, cta_stats);
+                                                     rowsum, cta_stats, row_exp);
     else
         k1_rows_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(d), ld, rows, cols,
-                                                    rowsum, cta_stats);
+                                                    rowsum, cta_stats, row_exp);
     count_launch();
 }
 

@@ -49,8 +49,9 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
 // ---- K1 for a row shard (rectangular rows x cols block): row sums of d^2,
 // sum d^4 and max |d| (deterministic per-CTA partials -> finalize on host)
 int k1_rows_grid(size_t rows, int sms);
+// row_exp[r]: smallest e with d_rj^2 < 2^e over the row (int8 slice product)
 void launch_k1_rows(const void* d, DType dt, size_t ld, size_t rows, size_t cols, double* rowsum,
-                    double* cta_stats, int grid, cudaStream_t st);
+                    double* cta_stats, int grid, cudaStream_t st, int* row_exp);
 // max |A[i][j] - B[j][i]| over an m x p block A (lda) and p x m block B (ldb),
 // atomically max-ed (non-negative doubles as u64) into *out
 void launch_asym_block(const void* a, size_t lda, const void* b, size_t ldb, DType dt, size_t m,

@@ -123,12 +123,13 @@ Matrix gram_sharded(const Matrix& d) {
     auto row_mean = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * 8);  // full r
     double* rowsum = static_cast<double*>(c.scratch("sh_rowsum", std::max<size_t>(m, 1) * 8));
     double* cta = static_cast<double*>(c.scratch("sh_cta", static_cast<size_t>(grid) * 2 * 8));
+    auto row_exp = std::make_shared<DevBuf>(std::max<size_t>(m, 1) * sizeof(int));  // local rows
     double* red = static_cast<double*>(c.scratch("sh_red", 8 * 8));
     DSB_CUDA(cudaMemsetAsync(red, 0, 8 * 8, c.stream));
     cudaEvent_t e0, e1;
     c.make_events(&e0, &e1);
     if (e0) DSB_CUDA(cudaEventRecord(e0, c.stream));
-    if (m) launch_k1_rows(s.buf->p, s.dt, s.ld, m, n, rowsum, cta, grid, c.stream);
+    if (m) launch_k1_rows(s.buf->p, s.dt, s.ld, m, n, rowsum, cta, grid, c.stream, row_exp->as<int>());
     // ---- symmetry: local diagonal block, then ring-shift block exchange
     launch_asym_block(static_cast<const char*>(s.buf->p) + rb * esz, s.ld,
                       static_cast<const char*>(s.buf->p) + rb * esz, s.ld, s.dt, m, m, red + 2,
@@ -169,11 +170,26 @@ Matrix gram_sharded(const Matrix& d) {
             sum4 += h[b * 2];
             mx = std::max(mx, h[b * 2 + 1]);
         }
+        // dynamic-range bound of the int8 product: max_i 2^e_i / r_i (K1 rule)
+        double ratio = 0.0;
+        if (m) {
+            std::vector<double> rs(m);
+            std::vector<int> ex(m);
+            c.d2h_copy(rs.data(), rowsum, m * 8);
+            c.d2h_copy(ex.data(), row_exp->p, m * sizeof(int));
+            for (size_t i = 0; i < m; ++i) {
+                if (ex[i] <= -1100) continue;
+                const double r = rs[i] / static_cast<double>(n);
+                ratio = std::max(ratio, r > 0.0 ? std::ldexp(1.0, ex[i]) / r : 1e300);
+            }
+        }
         double hv[2] = {sum4, mx};
         DSB_CUDA(cudaMemcpyAsync(red, hv, 16, cudaMemcpyHostToDevice, c.stream));
+        DSB_CUDA(cudaMemcpyAsync(red + 3, &ratio, 8, cudaMemcpyHostToDevice, c.stream));
+        c.sync();
     }
     cm.allreduce_sum(red, 1, c.stream);
-    cm.allreduce_max(red + 1, 2, c.stream);
+    cm.allreduce_max(red + 1, 3, c.stream);
     // ---- row means: local, then all-gathered
     {
         std::vector<double> hs(m);
@@ -189,8 +205,8 @@ Matrix gram_sharded(const Matrix& d) {
     }
     if (e1) DSB_CUDA(cudaEventRecord(e1, c.stream));
     c.add_timed(0, e0, e1);
-    double hred[3];
-    c.d2h_copy(hred, red, 24);
+    double hred[4];
+    c.d2h_copy(hred, red, 32);
     const double maxabs = hred[1];
     double maxasym = 0.0;
     {
@@ -206,6 +222,7 @@ Matrix gram_sharded(const Matrix& d) {
     GramInfo& gi = *g.gram;
     gi.n = n;
     gi.row_mean = row_mean;
+    gi.row_exp = row_exp;  // this rank's rows
     gi.row_mean_h.resize(n);
     c.d2h_copy(gi.row_mean_h.data(), row_mean->p, n * 8);
     // grand mean and ||G||_F^2 in index order on the host (rank-count independent)
@@ -222,6 +239,7 @@ Matrix gram_sharded(const Matrix& d) {
     gi.sc[S_SUM4] = hred[0];
     gi.sc[S_SUMR] = sr;
     gi.sc[S_SUMR2] = sr2;
+    gi.sc[S_ROWRATIO] = hred[3];
     gi.scalars = std::make_shared<DevBuf>(S_COUNT * 8);
     c.h2d_copy(gi.scalars->p, gi.sc, S_COUNT * 8);
     c.sync();
@@ -283,11 +301,26 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         }
     }
     const K2Plan plan = k2_plan_rect(std::max<size_t>(m, 1), n, wp, s.dt, c.sms);
+    // int8 slice product on this rank's rows (same admission rule as 1 GPU)
+    const bool use_i8 = m > 0 && use_int8_product(*g.gram, wp);
+    K2iPlan iplan;
+    double* pmax = nullptr;
+    int* col_exp = nullptr;
+    unsigned char* bdig = nullptr;
+    if (use_i8) {
+        iplan = k2i_plan(m, n, wp, c.sms);
+        pmax = static_cast<double*>(c.scratch(
+            "i8_pmax", static_cast<size_t>(panel_grid(n_pad, c.sms)) * wp * sizeof(double)));
+        col_exp = static_cast<int*>(c.scratch("i8_colexp", 64 * sizeof(int)));
+        bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
+    }
+    c.last_product_kernel = use_i8 ? 1 : 0;
     const size_t pbytes = n_pad * wp * 8;
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
     double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));
     double* P2 = static_cast<double*>(c.scratch("panel2", pbytes));
-    double* part = static_cast<double*>(c.scratch("k2_part", plan.part_elems * 8 + 64));
+    double* part = static_cast<double*>(c.scratch(
+        "k2_part", std::max(plan.part_elems, use_i8 ? iplan.part_elems : 0) * 8 + 64));
     const int pg = panel_grid(std::max<size_t>(m_pad, 4), c.sms);
     const int pgf = panel_grid(n_pad, c.sms);
     double* psmall = static_cast<double*>(c.scratch(
@@ -308,11 +341,20 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     }
     const size_t lo = rb * wp;  // local chunk offset in a panel
     auto product = [&](const double* x_full, double* y_full) {
-        // s = 1^T X, t = r^T X over the full replicated panel
-        launch_colsums(x_full, r_full, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
+        // s = 1^T X, t = r^T X over the full replicated panel (+ the int8
+        // column exponents: identical on every rank)
+        if (use_i8)
+            launch_colsums(x_full, r_full, n, n_pad, wp, psmall, colsums, c.sms, c.stream, pmax,
+                           iplan.nb, col_exp);
+        else
+            launch_colsums(x_full, r_full, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
         cudaEvent_t e0, e1;
         c.make_events(&e0, &e1);
-        if (m)
+        if (use_i8)
+            launch_k2i(s.tmap_for(128), s.dt, iplan, wp, x_full, n_pad, g.gram->row_exp->as<int>(),
+                       pmax, col_exp, bdig, part, r_full + rb, scal, colsums, y_full + lo,
+                       c.stream, e0, e1);
+        else if (m)
             launch_k2(s.tmap_for(plan.bm), s.dt, 1, plan, x_full, part, r_full + rb, scal, colsums,
                       y_full + lo, m_pad, c.stream, e0, e1);
         c.add_timed(1, e0, e1);

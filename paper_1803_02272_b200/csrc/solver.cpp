@@ -118,12 +118,6 @@ const double* omega_host(uint64_t seed, size_t n, size_t w) {
 // finite. DSB_K2_INT8=0 forces the fp64 kernel (parity comparisons).
 std::atomic<int> g_product_path{-1};  // -1: not yet read from DSB_K2_INT8
 
-}  // namespace
-
-void set_product_path(int mode) { g_product_path.store(mode); }
-
-namespace {
-
 int product_path() {
     int m = g_product_path.load();
     if (m < 0) {
@@ -136,6 +130,10 @@ int product_path() {
     return m;  // 0 auto, 1 fp64 only, 2 int8 whenever supported
 }
 
+}  // namespace
+
+void set_product_path(int mode) { g_product_path.store(mode); }
+
 bool use_int8_product(const GramInfo& gi, int wp) {
     const int mode = product_path();
     if (mode == 1 || !gi.row_exp || !k2i_supported(wp)) return false;
@@ -144,6 +142,8 @@ bool use_int8_product(const GramInfo& gi, int wp) {
     const double ratio = gi.sc[S_ROWRATIO], s4 = gi.sc[S_SUM4];
     return std::isfinite(s4) && std::isfinite(ratio) && ratio <= 4096.0;
 }
+
+namespace {
 
 struct RunOut {
     std::vector<double> vals;  // w values, reference order

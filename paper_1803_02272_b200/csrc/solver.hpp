@@ -59,6 +59,8 @@ double stable_rank(const Matrix& g);
 // product kernel choice: 0 auto, 1 fp64 DMMA only, 2 int8 slice product
 // whenever supported (lazy grams, w <= 64)
 void set_product_path(int mode);
+// whether a product pass on this gram uses the int8 slice product
+bool use_int8_product(const GramInfo& gi, int wp);
 
 // G_ij of a handle (lazy gram evaluated like ref mds.cpp:50-58)
 double matrix_get(const Matrix& m, size_t i, size_t j);

@@ -17,6 +17,15 @@ def comm1(ds):
     ds.comm_destroy()
 
 
+
+@pytest.fixture(autouse=True, params=["auto", "int8"])
+def product_path(request, ds):
+    """Sharded solves on both product kernels (fp64 DMMA at these n / forced int8)."""
+    ds.set_product_path(2 if request.param == "int8" else 0)
+    yield request.param
+    ds.set_product_path(0)
+
+
 def test_sharded_embed_matches_oracle(ds, oracle, comm1):
     pts = ds.synth_points(2, 1800, 4)
     n = pts.shape[0]
