@@ -103,6 +103,15 @@ divscope_status divscope_matrix_copy_to_host(const divscope_matrix* m, double* o
 /* ref divscope.h:118-121 (DVS1 container, ref src/distmat.hpp:42-44) */
 divscope_status divscope_matrix_write(const divscope_matrix* m, const char* dvs_path);
 divscope_status divscope_matrix_read(const char* dvs_path, divscope_matrix** out);
+
+/* NEW. Rows [row_begin, row_end) of a symmetric DVS1 file as a row-shard
+ * handle (the multi-GPU layout of divscope_shard_range): each rank reads only
+ * its own rows, streamed from the file through pinned staging buffers into
+ * HBM. Same errors as divscope_matrix_read; a non-symmetric file gives
+ * DIVSCOPE_ERR_NOT_SYMMETRIC. (ref src/distmat.cpp:189-222 reads the whole
+ * payload on one host.) */
+divscope_status divscope_matrix_read_rows(const char* dvs_path, size_t row_begin,
+                                          size_t row_end, divscope_matrix** out);
 /* ref divscope.h:128 */
 void divscope_matrix_free(divscope_matrix* m);
 /* NEW: host-only DVS1 header / payload check (no device needed): shape and

@@ -30,7 +30,7 @@ __all__ = [
     "matrix_from_host", "matrix_from_host_f32", "matrix_read", "matrix_euclidean",
     "matrix_hamming", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
     "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
-    "stats_enable_timing", "stats_reset", "set_product_path", "stats_get", "set_device", "LIB_PATH",
+    "stats_enable_timing", "stats_reset", "set_product_path", "matrix_read_rows", "stats_get", "set_device", "LIB_PATH",
     "fp64_tensor_peak_tflops", "stream_ptr",
 ]
 
@@ -111,6 +111,7 @@ def _load() -> C.CDLL:
         "divscope_matrix_copy_to_host": ([_vp, _dp], _st),
         "divscope_matrix_write": ([_vp, C.c_char_p], _st),
         "divscope_matrix_read": ([C.c_char_p, C.POINTER(_vp)], _st),
+        "divscope_matrix_read_rows": ([C.c_char_p, _sz, _sz, C.POINTER(_vp)], _st),
         "divscope_matrix_free": ([_vp], None),
         "divscope_dvs_read_host": ([C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int),
                                     _dp], _st),
@@ -254,6 +255,11 @@ def matrix_from_host_f32(values: np.ndarray, symmetric: bool = True) -> Matrix:
 
 def matrix_read(path) -> Matrix:
     return _new_matrix(lib.divscope_matrix_read, str(path).encode())
+
+
+def matrix_read_rows(path, row_begin: int, row_end: int) -> Matrix:
+    """Rows [row_begin, row_end) of a symmetric DVS1 file as a row-shard handle."""
+    return _new_matrix(lib.divscope_matrix_read_rows, str(path).encode(), row_begin, row_end)
 
 
 def dvs_read_host(path) -> tuple[np.ndarray, bool]:

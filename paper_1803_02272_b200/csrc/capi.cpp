@@ -274,10 +274,17 @@ divscope_status divscope_matrix_write(const divscope_matrix* m, const char* dvs_
 divscope_status divscope_matrix_read(const char* dvs_path, divscope_matrix** out) {
     if (!dvs_path || !out) return fail_invalid("null argument");
     return wrap([&] {
-        size_t rows = 0, cols = 0;
-        bool sym = false;
-        const std::vector<double> v = dsb::read_dvs(dvs_path, rows, cols, sym);
-        dsb::Matrix m = dsb::matrix_from_host(v.data(), rows, cols, sym, dsb::DType::F64);
+        // streaming ingest: pinned double-buffered pread -> H2D (dvs_stream.cpp)
+        dsb::Matrix m = dsb::matrix_read_dvs(dvs_path, false, 0, 0);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+divscope_status divscope_matrix_read_rows(const char* dvs_path, size_t row_begin,
+                                          size_t row_end, divscope_matrix** out) {
+    if (!dvs_path || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m = dsb::matrix_read_dvs(dvs_path, true, row_begin, row_end);
         *out = new divscope_matrix{std::move(m)};
     });
 }

@@ -70,6 +70,15 @@ Matrix matrix_from_host(const void* values, size_t rows, size_t cols, bool symme
 
 // ---- multi-GPU (sharded.cpp): one process per GPU, NCCL ----------------
 // rows [row_begin, row_end) of an n x n matrix, uploaded by this rank
+// DVS1 files (streaming ingest, dvs_stream.cpp)
+struct DvsHeader {
+    size_t rows = 0, cols = 0;
+    bool symmetric = false;
+};
+DvsHeader read_dvs_header(const std::string& path);
+// whole matrix, or (rows_only) rows [row_begin, row_end) as a row-shard handle
+Matrix matrix_read_dvs(const std::string& path, bool rows_only, size_t row_begin, size_t row_end);
+
 Matrix matrix_from_host_rows(const void* rows, size_t n, size_t row_begin, size_t row_end,
                              bool symmetric, DType dt);
 Matrix matrix_euclidean_rows(const double* pts, size_t n, size_t dim, bool f32,

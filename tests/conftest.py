@@ -5,6 +5,9 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
+# streaming DVS ingest in 1 MB chunks, so small test files span several
+# double-buffered chunks (read once when the library first reads a file)
+os.environ.setdefault("DSB_DVS_CHUNK_MB", "1")
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 

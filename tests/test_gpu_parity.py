@@ -390,3 +390,35 @@ def test_dvs_round_trip(ds, tmp_path):
     b = ds.matrix_read(tmp_path / "a.dvs")
     assert (b.rows, b.cols, b.symmetric) == (5, 7, False)
     assert np.array_equal(b.to_numpy(), a)
+
+
+def test_dvs_streaming_ingest_and_row_shards(ds, oracle, tmp_path):
+    # ref src/distmat.cpp:189-222 (DVS1), streamed in 1 MB chunks (conftest):
+    # a 700 x 700 f64 payload spans 4 double-buffered chunks
+    pts = ds.synth_points(1, 700, 5)
+    d = oracle.euclidean_matrix(pts)
+    f = tmp_path / "d.dvs"
+    ds.matrix_from_host(d).write(f)
+    full = ds.matrix_read(f)
+    assert (full.rows, full.cols, full.symmetric) == (700, 700, True)
+    assert np.array_equal(full.to_numpy(), d)
+    part = ds.matrix_read_rows(f, 256, 512)
+    assert (part.rows, part.cols) == (256, 700)
+    assert np.array_equal(part.to_numpy(), d[256:512])
+    empty = ds.matrix_read_rows(f, 300, 300)
+    assert empty.rows == 0
+    assert err(ds, ds.matrix_read_rows, f, 512, 256) == ds.Status.ERR_INVALID_ARGUMENT
+    assert err(ds, ds.matrix_read_rows, f, 0, 701) == ds.Status.ERR_INVALID_ARGUMENT
+    # non-symmetric file: no row shards
+    rect = tmp_path / "r.dvs"
+    ds.matrix_from_host(np.ones((3, 4)), symmetric=False).write(rect)
+    assert err(ds, ds.matrix_read_rows, rect, 0, 1) == ds.Status.ERR_NOT_SYMMETRIC
+    # truncated payload / header, bad magic (same codes as the reference)
+    raw = f.read_bytes()
+    (tmp_path / "t.dvs").write_bytes(raw[:-8])
+    assert err(ds, ds.matrix_read, tmp_path / "t.dvs") == ds.Status.ERR_TRUNCATED
+    (tmp_path / "h.dvs").write_bytes(raw[:20])
+    assert err(ds, ds.matrix_read, tmp_path / "h.dvs") == ds.Status.ERR_TRUNCATED
+    (tmp_path / "m.dvs").write_bytes(b"XXXX" + raw[4:64])
+    assert err(ds, ds.matrix_read, tmp_path / "m.dvs") == ds.Status.ERR_BAD_FORMAT
+    assert err(ds, ds.matrix_read, tmp_path / "missing.dvs") == ds.Status.ERR_IO

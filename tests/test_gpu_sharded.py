@@ -79,3 +79,18 @@ def test_sharded_f32(ds, oracle, comm1):
     st, rm, grand = oracle.gram_stats(dw)
     ref = oracle.embed(30, 10, 2, 3, d=dw, row_mean=rm, grand=grand)
     assert rel_err(emb.eigenvalues[:30], ref["eigenvalues"][:30]) < 1e-4
+
+
+def test_sharded_from_dvs_rows(ds, oracle, comm1, tmp_path):
+    # each rank streams only its rows of the DVS file (divscope_matrix_read_rows)
+    n, k, p, q, seed = 600, 8, 8, 1, 4
+    pts = ds.synth_points(2, n, seed)
+    d = oracle.euclidean_matrix(pts)
+    f = tmp_path / "d.dvs"
+    ds.matrix_from_host(d).write(f)
+    rb, re_ = ds.shard_range(n, 1, 0)
+    shard = ds.matrix_read_rows(f, rb, re_)
+    e = ds.embed(ds.gram(shard), rank=k, oversampling=p, power_iters=q, seed=seed)
+    ref = ds.embed(ds.gram(ds.matrix_from_host(d)), rank=k, oversampling=p, power_iters=q,
+                   seed=seed)
+    np.testing.assert_allclose(e.eigenvalues, ref.eigenvalues, rtol=1e-10)
