@@ -203,6 +203,14 @@ void divscope_embedding_free(divscope_embedding* e);
  * src/rsvd.hpp:43-44, for its orthonormality / subspace KATs): writes the
  * n x (rank + oversampling) basis, row-major. Numerically rank-deficient
  * directions come back as zero columns (K3). */
+/* NEW (the reference has it in C++ only, src/mds.hpp:54-58 / mds.cpp:126-150).
+ * sqrt(sum_ij (g_ij - x_i . x_j)^2) of an embedding against its gram (lazy:
+ * G evaluated on the fly from the upper triangle of D; explicit: stored
+ * entries). DIVSCOPE_ERR_SHAPE_MISMATCH when the sizes differ. */
+divscope_status divscope_reconstruction_error(const divscope_matrix* gram,
+                                              const divscope_embedding* e, unsigned threads,
+                                              double* out);
+
 divscope_status divscope_randomized_range(const divscope_matrix* gram,
                                           const divscope_solver_options* opts, double* q_out);
 

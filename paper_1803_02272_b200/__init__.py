@@ -30,7 +30,7 @@ __all__ = [
     "matrix_from_host", "matrix_from_host_f32", "matrix_read", "matrix_euclidean",
     "matrix_hamming", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
     "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
-    "stats_enable_timing", "stats_reset", "set_product_path", "matrix_read_rows", "stats_get", "set_device", "LIB_PATH",
+    "stats_enable_timing", "stats_reset", "set_product_path", "matrix_read_rows", "reconstruction_error", "stats_get", "set_device", "LIB_PATH",
     "fp64_tensor_peak_tflops", "stream_ptr",
 ]
 
@@ -112,6 +112,7 @@ def _load() -> C.CDLL:
         "divscope_matrix_write": ([_vp, C.c_char_p], _st),
         "divscope_matrix_read": ([C.c_char_p, C.POINTER(_vp)], _st),
         "divscope_matrix_read_rows": ([C.c_char_p, _sz, _sz, C.POINTER(_vp)], _st),
+        "divscope_reconstruction_error": ([_vp, _vp, C.c_uint, _dp], _st),
         "divscope_matrix_free": ([_vp], None),
         "divscope_dvs_read_host": ([C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int),
                                     _dp], _st),
@@ -410,6 +411,13 @@ def embed(g: Matrix, rank=None, oversampling=None, power_iters=None, seed=None, 
     finally:
         if rs.value:
             lib.divscope_readset_free(rs)
+
+
+def reconstruction_error(g: Matrix, e: "Embedding", threads: int = 1) -> float:
+    """ref mds.cpp:126-150 (sqrt of sum_ij (g_ij - x_i . x_j)^2)."""
+    out = C.c_double(0.0)
+    _check(lib.divscope_reconstruction_error(g.handle, e._h, threads, C.byref(out)))
+    return out.value
 
 
 def embedding_load(path) -> Embedding:

@@ -400,6 +400,14 @@ divscope_status divscope_embed(const divscope_matrix* gram, const divscope_solve
     });
 }
 
+divscope_status divscope_reconstruction_error(const divscope_matrix* gram,
+                                              const divscope_embedding* e, unsigned threads,
+                                              double* out) {  // ref mds.hpp:54-58
+    (void)threads;
+    if (!gram || !e || !out) return fail_invalid("null argument");
+    return wrap([&] { *out = dsb::reconstruction_error(gram->m, e->emb); });
+}
+
 divscope_status divscope_randomized_range(const divscope_matrix* gram,
                                           const divscope_solver_options* opts, double* q_out) {
     if (!gram || !opts || !q_out) return fail_invalid("null argument");

@@ -368,7 +368,11 @@ void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
                double* part, const double* row_mean, const double* scalars,
                const double* colsums, double* y, size_t n_pad, cudaStream_t st, cudaEvent_t e0,
                cudaEvent_t e1, const int* skip) {
-    (void)n_pad;
+    // rows beyond the last BM-row block up to the panel padding must read as
+    // zero (BM = 128 for WP > 64 leaves up to 128 rows unwritten)
+    const size_t r_done = static_cast<size_t>(p.nb) * p.bm;
+    if (n_pad > r_done)
+        cudaMemsetAsync(y + r_done * p.wp, 0, (n_pad - r_done) * p.wp * sizeof(double), st);
     switch (p.wp) {
 #define DSB_WP(W)                                                                               \
     case W:                                                                                     \

@@ -39,6 +39,7 @@
 #include <stdexcept>
 
 #include "device_utils.cuh"
+#include "host_core.hpp"
 #include "kernels.cuh"
 #include "umma.cuh"
 
@@ -789,8 +790,15 @@ bool k2i_supported(int wp) { return wp >= 8 && wp <= 64; }
 void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, const double* x,
                 size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
                 unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
-                const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
-                const int* skip) {
+                const double* colsums, double* y, size_t y_rows_pad, cudaStream_t st,
+                cudaEvent_t e0, cudaEvent_t e1, const int* skip) {
+    // k2_reduce writes the 128-row blocks; the panel rows beyond them (up to
+    // the 256-row padding) must read as zero, whatever an earlier, larger
+    // solve left in this workspace
+    const size_t r_done = static_cast<size_t>(p.nblk) * kRowsI8;
+    if (y_rows_pad > r_done)
+        DSB_CUDA(cudaMemsetAsync(y + r_done * wp, 0, (y_rows_pad - r_done) * wp * sizeof(double),
+                                 st));
     (void)x_rows_pad;
     (void)pmax;  // column exponents come from launch_colsums (same pass over X)
     {

@@ -103,8 +103,19 @@ K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms);
 void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, const double* x,
                 size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
                 unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
-                const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0 = nullptr,
-                cudaEvent_t e1 = nullptr, const int* skip = nullptr);
+                const double* colsums, double* y, size_t y_rows_pad, cudaStream_t st,
+                cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr, const int* skip = nullptr);
+
+// out[0] = sum of `count` doubles in a fixed order
+void launch_sum_fixed(const double* partial, size_t count, double* out, cudaStream_t st);
+
+// reconstruction_error (recon.cu, ref mds.cpp:126-150): out[0] = sum_ij
+// (g_ij - x_i . x_j)^2 over a lazy gram of D (upper tiles only) or an explicit
+// matrix; x: n x r row-major; partial: recon_blocks(n, lazy) doubles
+size_t recon_blocks(size_t n, bool lazy);
+void launch_recon(const void* d, DType dt, size_t ld, size_t n, bool lazy, const double* row_mean,
+                  const double* scalars, const double* x, int r, double* partial, double* out,
+                  cudaStream_t st);
 
 // ---- panel kernels (n_pad x WP, k4-interleaved) -----------------------------
 int panel_grid(size_t n_pad, int sms);

@@ -476,3 +476,11 @@ void launch_sr_step(const double* y, size_t n, int wp, double* partial, SrState*
     count_launch(3);
 }
 }  // namespace dsb
+
+namespace dsb {
+// out[0] = sum of count doubles, fixed order (deterministic)
+void launch_sum_fixed(const double* partial, size_t count, double* out, cudaStream_t st) {
+    k_sum_partials<<<1, 1024, 0, st>>>(partial, static_cast<int>(count), 1, out);
+    count_launch(1);
+}
+}  // namespace dsb

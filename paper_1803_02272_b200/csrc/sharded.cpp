@@ -352,7 +352,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         c.make_events(&e0, &e1);
         if (use_i8)
             launch_k2i(s.tmap_for(128), s.dt, iplan, wp, x_full, n_pad, g.gram->row_exp->as<int>(),
-                       pmax, col_exp, bdig, part, r_full + rb, scal, colsums, y_full + lo,
+                       pmax, col_exp, bdig, part, r_full + rb, scal, colsums, y_full + lo, m_pad,
                        c.stream, e0, e1);
         else if (m)
             launch_k2(s.tmap_for(plan.bm), s.dt, 1, plan, x_full, part, r_full + rb, scal, colsums,

@@ -271,7 +271,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         c.make_events(&e0, &e1);
         if (use_i8)
             launch_k2i(s.tmap_for(128), s.dt, iplan, wp, x, n_pad, g.gram->row_exp->as<int>(), pmax,
-                       col_exp, bdig, part, row_mean, scal_dev, colsums, y, c.stream, e0, e1);
+                       col_exp, bdig, part, row_mean, scal_dev, colsums, y, n_pad, c.stream, e0,
+                       e1);
         else
             launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums,
                       y, n_pad, c.stream, e0, e1);
@@ -445,6 +446,31 @@ Embedding embed(const Matrix& g, size_t rank, SolverOptions opts) {
     RunOut r = run(g, opts.rank, opts.oversampling, opts.power_iters, opts.seed, What::Embed, rank,
                    nullptr);
     return std::move(r.emb);
+}
+
+// ref src/mds.cpp:126-150 (shape check, then sqrt of the summed squares)
+double reconstruction_error(const Matrix& g, const Embedding& e) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    Store& s = *g.store;
+    if (s.sharded)
+        throw Error(errc::invalid_argument, "reconstruction_error on a row shard is not supported");
+    const size_t n = g.n();
+    if (e.n != n) throw Error(errc::shape_mismatch, "embedding/gram size mismatch");
+    if (n == 0) return 0.0;
+    const bool lazy = static_cast<bool>(g.gram);
+    const size_t r = e.r;
+    double* x = static_cast<double*>(c.scratch("recon_x", std::max<size_t>(n * r, 1) * 8));
+    if (r) c.h2d_copy(x, e.coords.data(), n * r * sizeof(double));
+    double* part = static_cast<double*>(c.scratch("recon_part", recon_blocks(n, lazy) * 8));
+    double* out = static_cast<double*>(c.scratch("recon_out", 64));
+    launch_recon(s.buf->p, s.dt, s.ld, n, lazy, lazy ? g.gram->row_mean->as<double>() : nullptr,
+                 lazy ? g.gram->scalars->as<double>() : nullptr, x, static_cast<int>(r), part,
+                 out, c.stream);
+    DSB_CUDA(cudaGetLastError());
+    double total = 0.0;
+    c.d2h_copy(&total, out, sizeof(double));
+    return std::sqrt(total);
 }
 
 void randomized_range(const Matrix& g, const SolverOptions& opts, double* q_out) {

@@ -56,6 +56,8 @@ void randomized_range(const Matrix& g, const SolverOptions& opts, double* q_out)
 
 // ref src/rsvd.cpp:147-178
 double stable_rank(const Matrix& g);
+// ref src/mds.cpp:126-150
+double reconstruction_error(const Matrix& g, const Embedding& e);
 // product kernel choice: 0 auto, 1 fp64 DMMA only, 2 int8 slice product
 // whenever supported (lazy grams, w <= 64)
 void set_product_path(int mode);

@@ -422,3 +422,51 @@ def test_dvs_streaming_ingest_and_row_shards(ds, oracle, tmp_path):
     (tmp_path / "m.dvs").write_bytes(b"XXXX" + raw[4:64])
     assert err(ds, ds.matrix_read, tmp_path / "m.dvs") == ds.Status.ERR_BAD_FORMAT
     assert err(ds, ds.matrix_read, tmp_path / "missing.dvs") == ds.Status.ERR_IO
+
+
+def test_reconstruction_error_matches_oracle(ds, oracle):
+    # ref src/mds.cpp:126-150 and tests/test_mds.cpp:128-147 (recon < 1e-8 ||G||_F
+    # for an exact low-rank cloud); lazy gram (upper tiles only) and explicit
+    for n, dim, seed in ((300, 3, 7), (517, 20, 8)):
+        rng = np.random.default_rng(seed)
+        pts = rng.standard_normal((n, dim))
+        d = oracle.euclidean_matrix(pts)
+        st, g = oracle.gram(d)
+        g_lazy = ds.gram(ds.matrix_from_host(d))
+        e = ds.embed(g_lazy, rank=min(dim, 10), oversampling=5, power_iters=2, seed=1)
+        want = oracle.reconstruction_error(g, e.coords)
+        fro = np.sqrt(np.sum(g * g))
+        got = ds.reconstruction_error(g_lazy, e)
+        assert abs(got - want) <= 1e-12 * fro
+        got_x = ds.reconstruction_error(ds.matrix_from_host(g), e)
+        assert abs(got_x - want) <= 1e-12 * fro
+        if dim <= 10:
+            assert got < 1e-8 * fro
+    # truncated embedding of a higher-dimensional cloud: a large error, still exact
+    pts = np.random.default_rng(3).standard_normal((400, 30))
+    d = oracle.euclidean_matrix(pts)
+    st, g = oracle.gram(d)
+    gl = ds.gram(ds.matrix_from_host(d))
+    e = ds.embed(gl, rank=4, oversampling=8, power_iters=2, seed=2)
+    want = oracle.reconstruction_error(g, e.coords)
+    assert ds.reconstruction_error(gl, e) == pytest.approx(want, rel=1e-12)
+    # size mismatch (ref mds.cpp:128-129)
+    other = ds.gram(ds.matrix_from_host(oracle.euclidean_matrix(pts[:100])))
+    assert err(ds, ds.reconstruction_error, other, e) == ds.Status.ERR_SHAPE_MISMATCH
+
+
+def test_workspace_reuse_large_then_small(ds, oracle):
+    # panel rows past the last product row block must read as zero even when a
+    # larger earlier solve left data in the reused workspace (BM = 128 for the
+    # int8 kernel and for w > 64 in fp64)
+    for w_rank, w_p in ((60, 10), (4, 4)):
+        big = oracle.euclidean_matrix(ds.synth_points(2, 900, 1))
+        ds.embed(ds.gram(ds.matrix_from_host(big)), rank=w_rank, oversampling=w_p, seed=3)
+        n = 300  # 300 mod 256 = 44: one 128-row block short of the 256-row padding
+        d = oracle.euclidean_matrix(ds.synth_points(2, n, 2))
+        st, rm, grand = oracle.gram_stats(d)
+        st, want, _, _ = oracle.eigs(w_rank, w_p, 2, 5, d=d, row_mean=rm, grand=grand,
+                                     vectors=False)
+        vals, _ = ds.eigs(ds.gram(ds.matrix_from_host(d)), rank=w_rank, oversampling=w_p,
+                          power_iters=2, seed=5)
+        np.testing.assert_allclose(vals[:8], want[:8], rtol=1e-9)
