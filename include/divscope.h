@@ -73,6 +73,14 @@ typedef struct divscope_readset divscope_readset;
 divscope_status divscope_readset_from_ids(const char* const* ids, size_t count,
                                           divscope_readset** out);
 /* ref divscope.h:62, :64, :71 */
+/* NEW. A readset with sequences (ids NULL -> "0".."count-1"); sequences are
+ * copied. (The reference builds readsets from FASTA, seqio.cpp; FASTA parsing
+ * is out of scope here.) */
+divscope_status divscope_readset_from_sequences(const char* const* ids,
+                                                const char* const* sequences, size_t count,
+                                                divscope_readset** out);
+/* ref divscope.h:65 (NULL for ids-only readsets) */
+const char* divscope_readset_sequence(const divscope_readset* rs, size_t i);
 size_t divscope_readset_size(const divscope_readset* rs);
 const char* divscope_readset_id(const divscope_readset* rs, size_t i);
 void divscope_readset_free(divscope_readset* rs);
@@ -80,7 +88,42 @@ void divscope_readset_free(divscope_readset* rs);
 /* ---- matrices ------------------------------------------------------------ */
 
 /* ref divscope.h:103 */
+/* ---- Smith-Waterman alignment distances, on the GPU (ref divscope.h:73-112;
+ * src/align.cpp:28-106, src/distmat.cpp:45-128): bit-exact distances, same
+ * error codes. `threads` is accepted and ignored. */
+typedef struct divscope_scoring {
+    int match;    /* > 0 */
+    int mismatch; /* < 0 */
+    int gap;      /* < 0 */
+} divscope_scoring;
+
+/* 1 / -1 / -2 */
+void divscope_scoring_init(divscope_scoring* s);
+
+typedef struct divscope_alignment {
+    int score;
+    int distance;
+    size_t a_begin, a_end; /* half-open spans of the locally aligned regions */
+    size_t b_begin, b_end;
+} divscope_alignment;
+
+/* scoring == NULL selects the defaults */
+divscope_status divscope_align(const char* a, const char* b, const divscope_scoring* scoring,
+                               divscope_alignment* out);
+/* Symmetric alignment distance (operands are ordered canonically first). */
+divscope_status divscope_distance(const char* a, const char* b, const divscope_scoring* scoring,
+                                  int* out);
+
 typedef struct divscope_matrix divscope_matrix;
+
+/* ref divscope.h:105-112: all pairs of a readset (symmetric n x n, zero
+ * diagonal) / queries x refs; readsets must carry sequences. */
+divscope_status divscope_pairwise_self(const divscope_readset* rs, const divscope_scoring* scoring,
+                                       unsigned threads, divscope_matrix** out);
+divscope_status divscope_pairwise_cross(const divscope_readset* queries,
+                                        const divscope_readset* refs,
+                                        const divscope_scoring* scoring, unsigned threads,
+                                        divscope_matrix** out);
 
 /* NEW (in-memory constructor a cgo/ctypes binding needs; the reference only
  * builds matrices via pairwise alignment or DVS files): copy a row-major

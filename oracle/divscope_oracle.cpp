@@ -23,6 +23,7 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <string_view>
 #include <vector>
 
 namespace {
@@ -31,6 +32,7 @@ namespace {
 enum Errc : int {
     OK = 0,
     EMPTY_INPUT = 2,
+    EMPTY_SEQUENCE = 6,
     NOT_SYMMETRIC = 9,
     RANK_TOO_LARGE = 10,
     ZERO_MATRIX = 11,
@@ -599,6 +601,75 @@ int orc_stable_rank(const double* g, std::size_t n, unsigned threads, double* ou
     }
     *out = fro2 / (sigma * sigma);
     return OK;
+}
+
+
+// ---- Smith-Waterman alignment distance: CPU restatement of src/align.cpp:28-106
+// (forward fill with the first maximal cell in row-major order, greedy
+// traceback preferring diagonal > up > left among the predecessors that
+// exactly account for the cell, zero cells walked through when accounted for;
+// distance = mismatch + gap steps) and the canonical operand order of
+// sw_distance (align.cpp:99-104: b < a lexicographically -> swap).
+// out6 = score, distance, a_begin, a_end, b_begin, b_end
+int orc_sw_align(const char* a, std::size_t na, const char* b, std::size_t nb, int match,
+                 int mismatch, int gap, long long* out6) {
+    if (!(match > 0 && mismatch < 0 && gap < 0)) return INVALID_ARGUMENT;
+    if (na == 0 || nb == 0) return EMPTY_SEQUENCE;
+    const std::size_t ld = nb + 1;
+    std::vector<int> h((na + 1) * ld, 0);
+    int best = 0;
+    std::size_t bi = 0, bj = 0;
+    auto sub = [&](std::size_t i, std::size_t j) {
+        return (a[i - 1] == b[j - 1] && a[i - 1] != 'N') ? match : mismatch;
+    };
+    for (std::size_t i = 1; i <= na; ++i)
+        for (std::size_t j = 1; j <= nb; ++j) {
+            int v = h[(i - 1) * ld + j - 1] + sub(i, j);
+            v = std::max(v, h[(i - 1) * ld + j] + gap);
+            v = std::max(v, h[i * ld + j - 1] + gap);
+            v = std::max(v, 0);
+            h[i * ld + j] = v;
+            if (v > best) {
+                best = v;
+                bi = i;
+                bj = j;
+            }
+        }
+    std::size_t i = bi, j = bj;
+    long long events = 0;
+    while (i > 0 && j > 0) {
+        const int v = h[i * ld + j], s = sub(i, j);
+        if (h[(i - 1) * ld + j - 1] + s == v) {
+            if (s != match) ++events;
+            --i;
+            --j;
+        } else if (h[(i - 1) * ld + j] + gap == v) {
+            ++events;
+            --i;
+        } else if (h[i * ld + j - 1] + gap == v) {
+            ++events;
+            --j;
+        } else {
+            break;
+        }
+    }
+    out6[0] = best;
+    out6[1] = events;
+    out6[2] = static_cast<long long>(i);
+    out6[3] = static_cast<long long>(bi);
+    out6[4] = static_cast<long long>(j);
+    out6[5] = static_cast<long long>(bj);
+    return 0;
+}
+
+int orc_sw_distance(const char* a, std::size_t na, const char* b, std::size_t nb, int match,
+                    int mismatch, int gap, int* out) {
+    const std::string_view va(a, na), vb(b, nb);
+    long long r[6];
+    const int st = (vb < va) ? orc_sw_align(b, nb, a, na, match, mismatch, gap, r)
+                             : orc_sw_align(a, na, b, nb, match, mismatch, gap, r);
+    if (st == 0) *out = static_cast<int>(r[1]);
+    return st;
 }
 
 }  // extern "C"

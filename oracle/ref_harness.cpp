@@ -18,6 +18,7 @@
 #include <cstring>
 #include <string>
 
+#include "align.hpp"
 #include "distmat.hpp"
 #include "error.hpp"
 #include "mds.hpp"
@@ -190,6 +191,60 @@ int ref_read_matrix(const char* path, double* v, std::size_t* rows, std::size_t*
         *cols = d.cols;
         *sym = d.symmetric ? 1 : 0;
         if (v) std::memcpy(v, d.values.data(), d.values.size() * sizeof(double));
+    });
+}
+
+
+// ---- Smith-Waterman distances (src/align.cpp:28-106, src/distmat.cpp:45-128)
+static ScoringScheme scheme_of(int match, int mismatch, int gap) {
+    ScoringScheme s;
+    s.match = match;
+    s.mismatch = mismatch;
+    s.gap = gap;
+    return s;
+}
+
+// out6 = score, distance, a_begin, a_end, b_begin, b_end
+int ref_sw_align(const char* a, const char* b, int match, int mismatch, int gap, long long* out6) {
+    return guarded([&] {
+        const AlignmentResult r = sw_align(a, b, scheme_of(match, mismatch, gap));
+        out6[0] = r.score;
+        out6[1] = r.distance;
+        out6[2] = static_cast<long long>(r.a_begin);
+        out6[3] = static_cast<long long>(r.a_end);
+        out6[4] = static_cast<long long>(r.b_begin);
+        out6[5] = static_cast<long long>(r.b_end);
+    });
+}
+
+int ref_sw_distance(const char* a, const char* b, int match, int mismatch, int gap, int* out) {
+    return guarded([&] { *out = sw_distance(a, b, scheme_of(match, mismatch, gap)); });
+}
+
+static ReadSet readset_of(const char* concat, const std::size_t* offs, std::size_t n) {
+    ReadSet rs;
+    for (std::size_t i = 0; i < n; ++i)
+        rs.reads.push_back({"r" + std::to_string(i), std::string(concat + offs[i], offs[i + 1] - offs[i])});
+    return rs;
+}
+
+// reads i: concat[offs[i], offs[i+1]); out n x n (row-major)
+int ref_pairwise_self(const char* concat, const std::size_t* offs, std::size_t n, int match,
+                      int mismatch, int gap, unsigned threads, double* out) {
+    return guarded([&] {
+        const DistanceMatrix d =
+            pairwise_self(readset_of(concat, offs, n), scheme_of(match, mismatch, gap), threads);
+        std::memcpy(out, d.values.data(), d.values.size() * sizeof(double));
+    });
+}
+
+int ref_pairwise_cross(const char* qc, const std::size_t* qo, std::size_t m, const char* rc,
+                       const std::size_t* ro, std::size_t n, int match, int mismatch, int gap,
+                       unsigned threads, double* out) {
+    return guarded([&] {
+        const DistanceMatrix d = pairwise_cross(readset_of(qc, qo, m), readset_of(rc, ro, n),
+                                                scheme_of(match, mismatch, gap), threads);
+        std::memcpy(out, d.values.data(), d.values.size() * sizeof(double));
     });
 }
 

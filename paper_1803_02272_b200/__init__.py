@@ -30,7 +30,8 @@ __all__ = [
     "matrix_from_host", "matrix_from_host_f32", "matrix_read", "matrix_euclidean",
     "matrix_hamming", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
     "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
-    "stats_enable_timing", "stats_reset", "set_product_path", "matrix_read_rows", "reconstruction_error", "stats_get", "set_device", "LIB_PATH",
+    "stats_enable_timing", "stats_reset", "set_product_path", "matrix_read_rows", "reconstruction_error", "Scoring", "Alignment",
+    "align", "distance", "pairwise_self", "pairwise_cross", "stats_get", "set_device", "LIB_PATH",
     "fp64_tensor_peak_tflops", "stream_ptr",
 ]
 
@@ -102,6 +103,14 @@ def _load() -> C.CDLL:
         "divscope_readset_size": ([_vp], _sz),
         "divscope_readset_id": ([_vp, _sz], C.c_char_p),
         "divscope_readset_free": ([_vp], None),
+        "divscope_readset_from_sequences": ([C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), _sz,
+                                             C.POINTER(_vp)], _st),
+        "divscope_readset_sequence": ([_vp, _sz], C.c_char_p),
+        "divscope_scoring_init": ([C.c_void_p], None),
+        "divscope_align": ([C.c_char_p, C.c_char_p, C.c_void_p, C.c_void_p], _st),
+        "divscope_distance": ([C.c_char_p, C.c_char_p, C.c_void_p, C.POINTER(C.c_int)], _st),
+        "divscope_pairwise_self": ([_vp, C.c_void_p, C.c_uint, C.POINTER(_vp)], _st),
+        "divscope_pairwise_cross": ([_vp, _vp, C.c_void_p, C.c_uint, C.POINTER(_vp)], _st),
         "divscope_matrix_from_host": ([_dp, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
         "divscope_matrix_from_host_f32": ([_fp, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
         "divscope_matrix_rows": ([_vp], _sz),
@@ -418,6 +427,68 @@ def reconstruction_error(g: Matrix, e: "Embedding", threads: int = 1) -> float:
     out = C.c_double(0.0)
     _check(lib.divscope_reconstruction_error(g.handle, e._h, threads, C.byref(out)))
     return out.value
+
+
+class Scoring(C.Structure):
+    """ref divscope_scoring (divscope.h:75-79); defaults 1 / -1 / -2."""
+    _fields_ = [("match", C.c_int), ("mismatch", C.c_int), ("gap", C.c_int)]
+
+    def __init__(self, match=1, mismatch=-1, gap=-2):
+        super().__init__(match, mismatch, gap)
+
+
+class Alignment(C.Structure):
+    _fields_ = [("score", C.c_int), ("distance", C.c_int), ("a_begin", _sz), ("a_end", _sz),
+                ("b_begin", _sz), ("b_end", _sz)]
+
+
+def _seq(s) -> bytes:
+    return s.encode() if isinstance(s, str) else bytes(s)
+
+
+def align(a, b, scoring: Scoring | None = None) -> Alignment:
+    """ref divscope_align: Smith-Waterman with the deterministic traceback (GPU)."""
+    out = Alignment()
+    _check(lib.divscope_align(_seq(a), _seq(b), C.byref(scoring) if scoring else None,
+                              C.byref(out)))
+    return out
+
+
+def distance(a, b, scoring: Scoring | None = None) -> int:
+    """ref divscope_distance (canonical operand order)."""
+    out = C.c_int(0)
+    _check(lib.divscope_distance(_seq(a), _seq(b), C.byref(scoring) if scoring else None,
+                                 C.byref(out)))
+    return out.value
+
+
+class _Readset:
+    def __init__(self, seqs, ids=None):
+        seqs = [_seq(s) for s in seqs]
+        sa = (C.c_char_p * len(seqs))(*seqs)
+        ia = None
+        if ids is not None:
+            ia = (C.c_char_p * len(ids))(*[_seq(i) for i in ids])
+        self.h = _vp()
+        _check(lib.divscope_readset_from_sequences(ia, sa, len(seqs), C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and lib is not None:
+            lib.divscope_readset_free(self.h)
+
+
+def pairwise_self(seqs, scoring: Scoring | None = None, ids=None) -> Matrix:
+    """ref divscope_pairwise_self: n x n Smith-Waterman distance matrix (GPU)."""
+    rs = _Readset(seqs, ids)
+    return _new_matrix(lib.divscope_pairwise_self, rs.h, C.byref(scoring) if scoring else None,
+                       1)
+
+
+def pairwise_cross(queries, refs, scoring: Scoring | None = None) -> Matrix:
+    """ref divscope_pairwise_cross: queries x refs distance matrix (GPU)."""
+    q, r = _Readset(queries), _Readset(refs)
+    return _new_matrix(lib.divscope_pairwise_cross, q.h, r.h,
+                       C.byref(scoring) if scoring else None, 1)
 
 
 def embedding_load(path) -> Embedding:

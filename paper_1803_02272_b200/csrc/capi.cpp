@@ -22,6 +22,7 @@ using dsb::Error;
 
 struct divscope_readset {
     std::vector<std::string> ids;
+    std::vector<std::string> seqs;  // empty for ids-only readsets
 };
 struct divscope_matrix {
     dsb::Matrix m;
@@ -214,6 +215,33 @@ divscope_status divscope_readset_from_ids(const char* const* ids, size_t count,
     });
 }
 
+divscope_status divscope_readset_from_sequences(const char* const* ids,
+                                                const char* const* sequences, size_t count,
+                                                divscope_readset** out) {
+    if ((!sequences && count) || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        auto* rs = new divscope_readset;
+        try {
+            rs->ids.reserve(count);
+            rs->seqs.reserve(count);
+            for (size_t i = 0; i < count; ++i) {
+                if (!sequences[i] || (ids && !ids[i])) throw Error(errc::invalid_argument, "null entry");
+                rs->ids.emplace_back(ids ? std::string(ids[i]) : std::to_string(i));
+                rs->seqs.emplace_back(sequences[i]);
+            }
+        } catch (...) {
+            delete rs;
+            throw;
+        }
+        *out = rs;
+    });
+}
+
+const char* divscope_readset_sequence(const divscope_readset* rs, size_t i) {
+    if (!rs || i >= rs->seqs.size()) return nullptr;
+    return rs->seqs[i].c_str();
+}
+
 size_t divscope_readset_size(const divscope_readset* rs) { return rs ? rs->ids.size() : 0; }
 
 const char* divscope_readset_id(const divscope_readset* rs, size_t i) {
@@ -327,6 +355,76 @@ divscope_status divscope_hamming_counts(const char* reads, size_t count, size_t 
                                         uint32_t* out) {
     if (!reads || !out) return fail_invalid("null argument");
     return wrap([&] { dsb::hamming_counts(reads, count, length, out); });
+}
+
+/* ---- Smith-Waterman distances on the GPU (ref capi.cpp:190-245) ---- */
+
+void divscope_scoring_init(divscope_scoring* s) {
+    if (!s) return;
+    s->match = 1;
+    s->mismatch = -1;
+    s->gap = -2;
+}
+
+static dsb::SwScheme to_scheme(const divscope_scoring* s) {
+    dsb::SwScheme x;
+    if (s) {
+        x.match = s->match;
+        x.mismatch = s->mismatch;
+        x.gap = s->gap;
+    }
+    return x;
+}
+
+divscope_status divscope_align(const char* a, const char* b, const divscope_scoring* scoring,
+                               divscope_alignment* out) {
+    if (!a || !b || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        const dsb::SwAlignment r = dsb::sw_align(a, b, to_scheme(scoring));
+        out->score = r.score;
+        out->distance = r.distance;
+        out->a_begin = r.a_begin;
+        out->a_end = r.a_end;
+        out->b_begin = r.b_begin;
+        out->b_end = r.b_end;
+    });
+}
+
+divscope_status divscope_distance(const char* a, const char* b, const divscope_scoring* scoring,
+                                  int* out) {
+    if (!a || !b || !out) return fail_invalid("null argument");
+    return wrap([&] { *out = dsb::sw_distance(a, b, to_scheme(scoring)); });
+}
+
+static void need_sequences(const divscope_readset* rs) {
+    if (rs->seqs.size() != rs->ids.size())
+        throw Error(errc::invalid_argument, "readset has no sequences (ids-only)");
+}
+
+divscope_status divscope_pairwise_self(const divscope_readset* rs, const divscope_scoring* scoring,
+                                       unsigned threads, divscope_matrix** out) {
+    (void)threads;
+    if (!rs || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        need_sequences(rs);
+        dsb::Matrix m = dsb::pairwise_self(rs->ids, rs->seqs, to_scheme(scoring));
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
+divscope_status divscope_pairwise_cross(const divscope_readset* queries,
+                                        const divscope_readset* refs,
+                                        const divscope_scoring* scoring, unsigned threads,
+                                        divscope_matrix** out) {
+    (void)threads;
+    if (!queries || !refs || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        need_sequences(queries);
+        need_sequences(refs);
+        dsb::Matrix m = dsb::pairwise_cross(queries->ids, queries->seqs, refs->ids, refs->seqs,
+                                            to_scheme(scoring));
+        *out = new divscope_matrix{std::move(m)};
+    });
 }
 
 /* ---- spectra and embeddings ---- */

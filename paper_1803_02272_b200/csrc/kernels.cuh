@@ -117,6 +117,21 @@ void launch_recon(const void* d, DType dt, size_t ld, size_t n, bool lazy, const
                   const double* scalars, const double* x, int r, double* partial, double* out,
                   cudaStream_t st);
 
+// ---- Smith-Waterman distances (sw.cu) ----------------------------------------
+struct SwPlan {
+    int nstr_max = 0;        // 8-column strips of the longest read
+    long long threads = 0;   // persistent threads (each owns scratch columns)
+    size_t dirs_elems = 0;   // u16 traceback codes
+    size_t hb_elems = 0;     // int boundary columns
+};
+SwPlan sw_plan(int max_len, int sms);
+// mode 0: pairs i < j of n_a reads (D symmetric, both halves written);
+// 1: n_a queries x n_b refs; 2: one pair (reads 0, 1) as given -> aux[6]
+void launch_sw(const unsigned char* seq, const long long* off, const int* len, int mode,
+               long long n_a, long long n_b, long long npairs, int match, int mismatch, int gap,
+               const SwPlan& p, unsigned short* dirs, int* hb, double* dout, size_t ld,
+               long long* aux, cudaStream_t st);
+
 // ---- panel kernels (n_pad x WP, k4-interleaved) -----------------------------
 int panel_grid(size_t n_pad, int sms);
 void launch_panel_from_rowmajor(const double* src, size_t n, int w, int wp, size_t n_pad,

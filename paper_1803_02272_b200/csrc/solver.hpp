@@ -72,6 +72,23 @@ Matrix matrix_from_host(const void* values, size_t rows, size_t cols, bool symme
 
 // ---- multi-GPU (sharded.cpp): one process per GPU, NCCL ----------------
 // rows [row_begin, row_end) of an n x n matrix, uploaded by this rank
+// Smith-Waterman distances on the GPU (sw.cu, pairwise.cpp; ref src/align.cpp,
+// src/distmat.cpp:45-128)
+struct SwScheme {
+    int match = 1, mismatch = -1, gap = -2;  // ref align.hpp:13-17
+};
+struct SwAlignment {
+    int score = 0, distance = 0;
+    size_t a_begin = 0, a_end = 0, b_begin = 0, b_end = 0;
+};
+SwAlignment sw_align(const std::string& a, const std::string& b, const SwScheme& s);
+int sw_distance(const std::string& a, const std::string& b, const SwScheme& s);
+Matrix pairwise_self(const std::vector<std::string>& ids, const std::vector<std::string>& seqs,
+                     const SwScheme& s);
+Matrix pairwise_cross(const std::vector<std::string>& qids, const std::vector<std::string>& q,
+                      const std::vector<std::string>& rids, const std::vector<std::string>& r,
+                      const SwScheme& s);
+
 // DVS1 files (streaming ingest, dvs_stream.cpp)
 struct DvsHeader {
     size_t rows = 0, cols = 0;

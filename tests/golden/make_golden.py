@@ -11,6 +11,8 @@ the reference code path; nothing is computed by the product or the oracle:
   kats.npz      eigs_sym / embed / stable_rank outputs on the reference KAT
                 matrices (ref tests/test_rsvd.cpp, tests/test_mds.cpp)
   reads.npz     testdata::random_reads (ref tests/testdata.cpp:28-37)
+  sw.npz        sw_align / pairwise_self over mutated read families (ref src/align.cpp,
+                src/distmat.cpp)
   *.dvs         DVS1 files written by write_matrix (ref src/distmat.cpp:169-187)
 
 Usage: python tests/golden/make_golden.py
@@ -95,6 +97,37 @@ def main():
     # --- reads
     raw = ref.random_reads(40, 100, 77)
     np.savez(HERE / "reads.npz", reads=np.frombuffer(raw, dtype=np.uint8).reshape(40, 100))
+    # --- Smith-Waterman (ref src/align.cpp:28-106, src/distmat.cpp:45-88):
+    # mutated families of the random reads (substitutions, N, indels), all
+    # pairs' alignments under two schemes + the pairwise_self matrix
+    rng = np.random.default_rng(11)
+    base = [bytes(r) for r in np.frombuffer(raw, dtype=np.uint8).reshape(40, 100)[:8]]
+    seqs = []
+    for k, s in enumerate(base):
+        for m in range(3):
+            b = bytearray(s)
+            for _ in range(rng.integers(0, 8)):
+                pos = int(rng.integers(0, len(b)))
+                op = int(rng.integers(0, 4))
+                if op == 0:
+                    b[pos] = b"ACGTN"[int(rng.integers(0, 5))]
+                elif op == 1 and len(b) > 10:
+                    del b[pos]
+                else:
+                    b.insert(pos, b"ACGT"[int(rng.integers(0, 4))])
+            seqs.append(bytes(b[: 60 + 15 * m]))
+    lens = np.array([len(s) for s in seqs])
+    cat = np.frombuffer(b"".join(seqs), dtype=np.uint8)
+    aln = []
+    for sch in ((1, -1, -2), (2, -3, -1)):
+        for i in range(len(seqs)):
+            for j in range(len(seqs)):
+                st, r6 = ref.sw_align(seqs[i], seqs[j], sch)
+                assert st == 0
+                aln.append((sch[0], sch[1], sch[2], i, j) + tuple(r6))
+    st, dself = ref.pairwise_self(seqs, (1, -1, -2), threads=1)
+    assert st == 0
+    np.savez(HERE / "sw.npz", cat=cat, lens=lens, aln=np.array(aln, dtype=np.int64), dself=dself)
     # --- DVS files
     rng = np.random.default_rng(3)
     a = rng.standard_normal((5, 7))

@@ -62,6 +62,10 @@ class Oracle:
         L.orc_reconstruction_error.argtypes = [_dp, _sz, _dp, _sz]
         L.orc_reconstruction_error.restype = C.c_double
         L.orc_stable_rank.argtypes = [_dp, _sz, C.c_uint, _dp]
+        L.orc_sw_align.argtypes = [C.c_char_p, _sz, C.c_char_p, _sz, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_longlong)]
+        L.orc_sw_distance.argtypes = [C.c_char_p, _sz, C.c_char_p, _sz, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(C.c_int)]
 
     def fill_gaussian(self, seed: int, count: int) -> np.ndarray:
         out = np.empty(count, np.float64)
@@ -155,6 +159,16 @@ class Oracle:
         n, r = coords.shape
         return self.lib.orc_reconstruction_error(_ptr(g), n, _ptr(np.ascontiguousarray(coords)), r)
 
+    def sw_align(self, a: bytes, b: bytes, scheme=(1, -1, -2)):
+        out = (C.c_longlong * 6)()
+        st = self.lib.orc_sw_align(a, len(a), b, len(b), *scheme, out)
+        return st, tuple(out)
+
+    def sw_distance(self, a: bytes, b: bytes, scheme=(1, -1, -2)):
+        out = C.c_int(0)
+        st = self.lib.orc_sw_distance(a, len(a), b, len(b), *scheme, C.byref(out))
+        return st, out.value
+
     def stable_rank(self, g):
         out = C.c_double(0)
         st = self.lib.orc_stable_rank(_ptr(g), g.shape[0], _threads(), C.byref(out))
@@ -183,6 +197,15 @@ class RefLib:
         L.ref_eigs_sym.argtypes = [_dp, _sz, _sz, _sz, _sz, _u64, C.c_uint, _dp, _dp,
                                    C.POINTER(_sz), _dp]
         L.ref_stable_rank.argtypes = [_dp, _sz, C.c_uint, _dp]
+        L.ref_sw_align.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_longlong)]
+        L.ref_sw_distance.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(C.c_int)]
+        L.ref_pairwise_self.argtypes = [C.c_char_p, C.POINTER(_sz), _sz, C.c_int, C.c_int,
+                                        C.c_int, C.c_uint, _dp]
+        L.ref_pairwise_cross.argtypes = [C.c_char_p, C.POINTER(_sz), _sz, C.c_char_p,
+                                         C.POINTER(_sz), _sz, C.c_int, C.c_int, C.c_int,
+                                         C.c_uint, _dp]
         L.ref_embed.argtypes = [_dp, _sz, _sz, _sz, _sz, _u64, C.c_uint, _dp, _dp,
                                 C.POINTER(_sz), _dp, C.POINTER(C.c_int)]
         L.ref_reconstruction_error.argtypes = [_dp, _sz, _dp, _sz, C.c_uint]
@@ -242,6 +265,38 @@ class RefLib:
                                    _ptr(vecs), C.byref(keep), C.byref(resid))
         k = keep.value
         return st, vals[:k].copy(), vecs[: n * k].reshape(n, k).copy(), resid.value
+
+    def sw_align(self, a: bytes, b: bytes, scheme=(1, -1, -2)):
+        out = (C.c_longlong * 6)()
+        st = self.lib.ref_sw_align(a, b, *scheme, out)
+        return st, tuple(out)
+
+    def sw_distance(self, a: bytes, b: bytes, scheme=(1, -1, -2)):
+        out = C.c_int(0)
+        st = self.lib.ref_sw_distance(a, b, *scheme, C.byref(out))
+        return st, out.value
+
+    @staticmethod
+    def _concat(seqs):
+        offs = [0]
+        for s in seqs:
+            offs.append(offs[-1] + len(s))
+        return b"".join(seqs), (C.c_size_t * len(offs))(*offs)
+
+    def pairwise_self(self, seqs, scheme=(1, -1, -2), threads=None):
+        cat, offs = self._concat(seqs)
+        out = np.zeros((len(seqs), len(seqs)))
+        st = self.lib.ref_pairwise_self(cat, offs, len(seqs), *scheme, threads or _threads(),
+                                        _ptr(out))
+        return st, out
+
+    def pairwise_cross(self, q, r, scheme=(1, -1, -2), threads=None):
+        qc, qo = self._concat(q)
+        rc, ro = self._concat(r)
+        out = np.zeros((len(q), len(r)))
+        st = self.lib.ref_pairwise_cross(qc, qo, len(q), rc, ro, len(r), *scheme,
+                                         threads or _threads(), _ptr(out))
+        return st, out
 
     def stable_rank(self, g):
         out = C.c_double(0)

@@ -13,6 +13,8 @@ import pytest
 
 from helpers import coords_match_up_to_sign, rel_err
 
+GOLDEN = G
+
 G = Path(__file__).resolve().parent / "golden"
 
 
@@ -127,3 +129,24 @@ def test_oracle_matches_ref_directly(oracle, ref):
     e = oracle.embed(6, 10, 2, 4, d=d, row_mean=rm, grand=grand)
     assert rel_err(e["eigenvalues"], e_ref["eigenvalues"]) < 1e-12
     assert coords_match_up_to_sign(e["coords"], e_ref["coords"]) < 1e-10
+
+
+def test_sw_oracle_matches_reference_fixture(oracle):
+    # tests/golden/sw.npz from the reference's sw_align / pairwise_self
+    z = np.load(GOLDEN / "sw.npz")
+    cat, lens = z["cat"].tobytes(), z["lens"]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    seqs = [cat[offs[i]:offs[i + 1]] for i in range(len(lens))]
+    for row in z["aln"]:
+        m, mm, g, i, j = (int(x) for x in row[:5])
+        st, r6 = oracle.sw_align(seqs[i], seqs[j], (m, mm, g))
+        assert st == 0 and r6 == tuple(int(x) for x in row[5:])
+    n = len(seqs)
+    for i in range(n):
+        for j in range(n):
+            if i != j:
+                st, dist = oracle.sw_distance(seqs[i], seqs[j])
+                assert st == 0 and dist == z["dself"][i, j]
+    # error precedence (ref align.cpp:33-35): scheme first, then empty operands
+    assert oracle.sw_align(b"", b"A")[0] == 6          # EMPTY_SEQUENCE
+    assert oracle.sw_align(b"AC", b"A", (0, -1, -1))[0] == 17  # INVALID_ARGUMENT
