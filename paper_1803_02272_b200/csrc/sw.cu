@@ -12,8 +12,9 @@
 // order diagonal > up > left, whose value exactly accounts for the cell (0,
 // 1, 2), else 3 (stop) — packed 2 bits per cell, 16 bits per strip row,
 // stored [row][strip][thread] (coalesced). The first maximal cell in
-// row-major order is tracked with a (value desc, i asc, j asc) rule, which is
-// visit-order independent, so the strip order finds the reference's cell.
+// row-major order (the reference's strict-greater scan) is found from the
+// strip visiting order: a tie can only improve on the current best from an
+// earlier row of a later strip, so `v > best || (v == best && i < bi)`.
 // The traceback then walks the codes from that cell exactly as
 // align.cpp:70-92 (the diagonal step counts when the substitution is not a
 // match; gap steps count), so distance, score and spans equal the
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(kSwThreads) k_sw(
 #pragma unroll
             for (int c = 0; c < kSwStrip; ++c) top[c] = 0;
             int diag_l = 0;  // H[i-1][j0-1]
+            const int valid = nb - j0 + 1;  // cells of this strip inside the matrix (>= 1)
             for (int i = 1; i <= na; ++i) {
                 const unsigned int ca = A[i - 1];
                 const bool ca_n = (ca == 'N');
@@ -119,15 +121,19 @@ __global__ void __launch_bounds__(kSwThreads) k_sw(
                     const int u = top[c] + gap;
                     const int l = (c == 0 ? left_l : cur[c - 1]) + gap;
                     int v = max(max(d, u), max(l, 0));
+                    // cells past column nb (last strip) are clamped to 0: they
+                    // feed only other padded cells and never become the maximum
+                    if (c >= valid) v = 0;
                     const unsigned int cd = (d == v) ? 0u : (u == v) ? 1u : (l == v) ? 2u : 3u;
                     code |= cd << (2 * c);
                     cur[c] = v;
-                    const int j = j0 + c;
-                    if (j <= nb && (v > best || (v == best && best > 0 &&
-                                                 (i < bi || (i == bi && j < bj))))) {
+                    // first maximum in row-major order: strips are visited left to
+                    // right and rows top-down within a strip, so a tie replaces the
+                    // current best only from an earlier row of a later strip
+                    if (v > best || (v == best && i < bi)) {
                         best = v;
                         bi = i;
-                        bj = j;
+                        bj = j0 + c;
                     }
                 }
                 hb[i * T + tid] = cur[kSwStrip - 1];
@@ -182,8 +188,8 @@ SwPlan sw_plan(int max_len, int sms) {
     p.nstr_max = (std::max(max_len, 1) + kSwStrip - 1) / kSwStrip;
     const size_t per_thread = (static_cast<size_t>(max_len) + 1) *
                               (static_cast<size_t>(p.nstr_max) * sizeof(unsigned short) + sizeof(int));
-    const size_t budget = size_t(4) << 30;  // traceback codes + boundary columns
-    size_t threads = static_cast<size_t>(sms) * 2 * kSwThreads;
+    const size_t budget = size_t(12) << 30;  // traceback codes + boundary columns
+    size_t threads = static_cast<size_t>(sms) * 8 * kSwThreads;
     threads = std::min(threads, std::max<size_t>(kSwThreads, budget / std::max<size_t>(per_thread, 1)));
     threads = std::max<size_t>(kSwThreads, threads / kSwThreads * kSwThreads);
     p.threads = static_cast<long long>(threads);

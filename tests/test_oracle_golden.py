@@ -13,9 +13,8 @@ import pytest
 
 from helpers import coords_match_up_to_sign, rel_err
 
-GOLDEN = G
-
 G = Path(__file__).resolve().parent / "golden"
+GOLDEN = G
 
 
 def test_fill_gaussian_bit_exact(oracle):
