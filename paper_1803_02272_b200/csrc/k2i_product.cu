@@ -391,37 +391,49 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     if (warp == 1) tmem_dealloc(tmem, NCOL);
 }
 
-// ---- NB = 32: A digits in tensor memory ------------------------------------
+// ---- A digits in tensor memory ---------------------------------------------
 // An MMA whose A operand comes from shared memory costs at least ~128 cycles
 // (the 4 KB A tile is read at ~32 B/clk; tools/microbench/umma_i8_rate.cu),
-// so the 7 digit MMAs of a k-step with N' = 224..32 ran at half the tensor
-// rate. With A in TMEM (written by the converters with tcgen05.st) the same
-// 7 MMAs take N'/2 cycles each: 448 cycles per k-step, well under the
-// ~1400-cycle HBM time of the k-step's 32 KB of D.
-// TMEM: columns [0, 224) the 7 diagonal accumulators, [256 + 64 s, +56) the
-// 7 x 8-column A digit planes of stage s (row = lane, byte k at column k/4).
+// so the digit MMAs of a k-step (N' = 224..32) ran at half the tensor rate or
+// worse. With A in TMEM (written by the converters with tcgen05.st) each MMA
+// takes N'/2 cycles: 448 (NB = 32) / 896 (NB = 64) cycles per k-step, under
+// the ~1400-cycle HBM time of the k-step's 32 KB of D.
+// TMEM: columns [0, 7 NB) the diagonal accumulators, then NA stages of the
+// 7 x 8-column A digit planes (row = lane, byte k at column k / 4): NA = 4
+// for NB = 32, NA = 1 for NB = 64 (448 + 56 columns). With one A stage the
+// converters overlap the next k-step's conversion (into registers) with the
+// MMAs of the current one and only the TMEM stores wait for the stage.
+// The panel digits stream through their own ring (the producer warp issues
+// them next to the D tiles; the MMA commits free both).
 // Converter warp w (2..17) handles tile rows 32 (w % 4) + lane (its TMEM lane
 // quadrant) and columns 8 p .. 8 p + 7 of the k-step, p = (w - 2) / 4.
 #ifndef DSB_TS_SMEM_KB
 #define DSB_TS_SMEM_KB 208
 #endif
-constexpr int kAStagesTs = 4;
-#ifndef DSB_I8_FIXED_FP64
-#define DSB_I8_FIXED_FP64 0
-#endif
-// split the fixed-point conversions between the XU pipe (F2I) and the FP64
-// pipe (fixed56): each alone saturates before the HBM rate
-constexpr bool kFixedFp64 = DSB_I8_FIXED_FP64;
-constexpr int kNbTs = 32;
 
-template <typename TD>
-constexpr int d_stages_ts() {
-    return std::min(8, (DSB_TS_SMEM_KB * 1024 - kAStagesTs * b_bytes<kNbTs>()) / d_bytes<TD>());
+constexpr int kBStagesTs = 4;
+
+
+template <int NB>
+constexpr int a_stages_ts() {
+    return NB <= 32 ? 4 : 1;
 }
-template <typename TD>
+template <int NB>
+constexpr uint32_t a_base_ts() {  // first TMEM column of the A stages
+    return NB <= 32 ? 256u : 448u;
+}
+template <int NB>
+constexpr int b_stages_ts() {
+    return a_stages_ts<NB>() == 1 ? kBStagesTs : a_stages_ts<NB>();
+}
+template <int NB, typename TD>
+constexpr int d_stages_ts() {
+    return std::min(8, (DSB_TS_SMEM_KB * 1024 - b_stages_ts<NB>() * b_bytes<NB>()) / d_bytes<TD>());
+}
+template <int NB, typename TD>
 constexpr size_t ts_smem() {
-    return 1024 + static_cast<size_t>(d_stages_ts<TD>()) * d_bytes<TD>() +
-           kAStagesTs * b_bytes<kNbTs>() + 256 + kNbTs * 8;
+    return 1024 + static_cast<size_t>(d_stages_ts<NB, TD>()) * d_bytes<TD>() +
+           b_stages_ts<NB>() * b_bytes<NB>() + 448 + NB * 8;
 }
 
 // 8 consecutive d values of row `row`, columns c0..c0+7 of the k-step tile
@@ -450,16 +462,20 @@ __device__ __forceinline__ void load8(const unsigned char* tile, int row, int c0
     }
 }
 
-template <typename TD>
+template <int NB, typename TD>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
                    const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
                    int nks, int total, double* __restrict__ part, int maxseg, int wp,
                    const int* __restrict__ skip, int dbg) {
     if (skip && *skip) return;
-    constexpr int NB = kNbTs;
-    constexpr int ND = d_stages_ts<TD>();
-    constexpr int NA = kAStagesTs;
+    constexpr int ND = d_stages_ts<NB, TD>();
+    constexpr int NA = a_stages_ts<NB>();
+    // panel digits: with several A stages they ride with the A stage (loaded
+    // by one converter lane when it claims the stage); with a single A stage
+    // they get their own ring filled ahead by the producer
+    constexpr bool kBProd = (NA == 1);
+    constexpr int NBR = kBProd ? kBStagesTs : NA;
     constexpr int DB = d_bytes<TD>();
     constexpr int BB = b_bytes<NB>();
 
@@ -467,15 +483,17 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* dring = sm;
     unsigned char* bring = sm + ND * DB;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NA * BB);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NBR * BB);
     uint64_t* full_d = bars;
     uint64_t* empty_d = full_d + ND;
     uint64_t* full_a = empty_d + ND;
     uint64_t* empty_a = full_a + NA;
-    uint64_t* acc_full = empty_a + NA;
+    uint64_t* full_b = empty_a + NA;
+    uint64_t* empty_b = full_b + NBR;
+    uint64_t* acc_full = empty_b + NBR;
     uint64_t* acc_empty = acc_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-    double* colscale = reinterpret_cast<double*>(bars + 32);
+    double* colscale = reinterpret_cast<double*>(bars + 56);  // <= 34 barriers + slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
@@ -488,9 +506,16 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             mbar_init(&empty_d[s], kConv);
         }
         for (int s = 0; s < NA; ++s) {
-            mbar_init(&full_a[s], kConv + 1);
+            // with the digits riding on the A stage, their expect_tx arrival
+            // is the stage's 17th
+            mbar_init(&full_a[s], kBProd ? kConv : kConv + 1);
             mbar_init(&empty_a[s], 1);
         }
+        for (int s = 0; s < NBR; ++s) {
+            mbar_init(&full_b[s], 1);
+            mbar_init(&empty_b[s], 1);
+        }
+        static_assert(kBProd || NBR == NA, "B ring rides with the A ring");
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 4);
         fence_mbar_init();
@@ -504,39 +529,50 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tmem_a = tmem + 256;
+    const uint32_t tmem_a = tmem + a_base_ts<NB>();
 
     if (warp == 0) {
-        // ---------------- TMA producer ----------------
+        // ---------------- TMA producer: D tiles and panel digits ----------------
         if (lane == 0) {
             prefetch_tmap(&tmD);
-            int s = 0, k = 0;
-            uint32_t ph = 0;
+            int sd = 0, sb = 0, k = 0;
+            uint32_t pd = 0, pb = 0;
             for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
-                if (k >= ND) mbar_wait(&empty_d[s], ph ^ 1);
-                unsigned char* dst = dring + s * DB;
-                mbar_arrive_expect_tx(&full_d[s], DB);
+                if (k >= ND) mbar_wait(&empty_d[sd], pd ^ 1);
+                unsigned char* dst = dring + sd * DB;
+                mbar_arrive_expect_tx(&full_d[sd], DB);
                 if constexpr (sizeof(TD) == 8) {
-                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[s]);
+                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[sd]);
                     tma_load_2d(dst + kRowsI8 * 128, &tmD, w.ks * kKStep + 16, w.rb * kRowsI8,
-                                &full_d[s]);
+                                &full_d[sd]);
                 } else {
-                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[s]);
+                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[sd]);
                 }
-                if (++s == ND) {
-                    s = 0;
-                    ph ^= 1;
+                if (++sd == ND) {
+                    sd = 0;
+                    pd ^= 1;
+                }
+                if constexpr (kBProd) {
+                    if (k >= NBR) mbar_wait(&empty_b[sb], pb ^ 1);
+                    mbar_arrive_expect_tx(&full_b[sb], BB);
+                    bulk_load(bring + sb * BB, bdig + static_cast<size_t>(w.ks) * BB, BB,
+                              &full_b[sb]);
+                    if (++sb == NBR) {
+                        sb = 0;
+                        pb ^= 1;
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            int s = 0, nflush = 0;
-            uint32_t ph = 0;
+            int sa = 0, sb = 0, nflush = 0;
+            uint32_t pa = 0, pb = 0;
             bool started = false;
             for (Walk w(t0, t1, nks); w.more(); w.next()) {
-                mbar_wait(&full_a[s], ph);
+                mbar_wait(&full_a[sa], pa);
+                if constexpr (kBProd) mbar_wait(&full_b[sb], pb);
                 tc_fence_after();
                 const bool first = w.first();
                 if (first && started) {
@@ -544,24 +580,38 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     tc_fence_after();
                 }
                 started = true;
-                const uint64_t bd = umma_desc_k_interleave(smem_u32(bring + s * BB));
-                const uint32_t ta = tmem_a + static_cast<uint32_t>(s * 64);
+                const uint32_t bbase = smem_u32(bring + sb * BB);
+                const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64);
                 if (dbg != 2) {
 #pragma unroll
-                    for (int t = 1; t <= kDig; ++t)
-                        umma_i8_ts(tmem + static_cast<uint32_t>((t - 1) * NB),
-                                   ta + static_cast<uint32_t>((t - 1) * 8), bd,
-                                   umma_idesc_i8((8 - t) * NB, false, true),
-                                   (first && t == 1) ? 0 : 1);
+                    for (int t = 1; t <= kDig; ++t) {
+                        constexpr int per = 256 / NB;
+                        const int umax = 8 - t;
+#pragma unroll
+                        for (int u0 = 1; u0 <= umax; u0 += per) {
+                            const int nu = (umax - u0 + 1 < per) ? (umax - u0 + 1) : per;
+                            const uint64_t bd =
+                                umma_desc_k_interleave(bbase + (u0 - 1) * (NB * kKStep));
+                            umma_i8_ts(tmem + static_cast<uint32_t>((t + u0 - 2) * NB),
+                                       ta + static_cast<uint32_t>((t - 1) * 8), bd,
+                                       umma_idesc_i8(nu * NB, false, true),
+                                       (first && t == 1) ? 0 : 1);
+                        }
+                    }
                 }
-                umma_commit(&empty_a[s]);
+                umma_commit(&empty_a[sa]);
+                if constexpr (kBProd) umma_commit(&empty_b[sb]);
                 if (w.last()) {
                     umma_commit(acc_full);
                     ++nflush;
                 }
-                if (++s == NA) {
-                    s = 0;
-                    ph ^= 1;
+                if (++sa == NA) {
+                    sa = 0;
+                    pa ^= 1;
+                }
+                if (++sb == NBR) {
+                    sb = 0;
+                    pb ^= 1;
                 }
             }
         }
@@ -585,48 +635,93 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 sc = e > kExpZeroI8 ? ldexp(1.0, 56 - e) : 0.0;
             }
             mbar_wait(&full_d[sd], pd);
-            if (k >= NA) {
-                mbar_wait(&empty_a[sa], pa ^ 1);
-                tc_fence_after();
-            }
-            if (warp == 2 && lane == 0) {
-                mbar_arrive_expect_tx(&full_a[sa], BB);
-                bulk_load(bring + sa * BB, bdig + static_cast<size_t>(w.ks) * BB, BB, &full_a[sa]);
-            }
-            if (dbg != 1) {
-                double d[8];
-                load8<TD>(dring + sd * DB, row, c0, d);
-                uint32_t lo[8], hi[8];
+            if constexpr (!kBProd) {
+                // several A stages: claim the stage (and load its panel
+                // digits) first, then convert and store digit by digit
+                if (k >= NA) {
+                    mbar_wait(&empty_a[sa], pa ^ 1);
+                    tc_fence_after();
+                }
+                if (warp == 2 && lane == 0) {
+                    mbar_arrive_expect_tx(&full_a[sa], BB);
+                    bulk_load(bring + sa * BB, bdig + static_cast<size_t>(w.ks) * BB, BB,
+                              &full_a[sa]);
+                }
+                if (dbg != 1) {
+                    double d[8];
+                    load8<TD>(dring + sd * DB, row, c0, d);
+                    uint32_t lo[8], hi[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (kFixedFp64 && (j & 1)) {
-                        fixed56(d[j] * d[j], sc, lo[j], hi[j]);  // FP64 pipe
-                    } else {
-                        const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);  // XU
+                    for (int j = 0; j < 8; ++j) {
+                        const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);
                         lo[j] = static_cast<uint32_t>(m);
                         hi[j] = static_cast<uint32_t>(m >> 32);
                     }
-                }
-                const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64) + lane_off;
+                    const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64) + lane_off;
 #pragma unroll
-                for (int t = 1; t <= kDig; ++t) {
-                    const int byte = 7 - t;
-                    const uint32_t* src = byte >= 4 ? hi : lo;
-                    const uint32_t b = static_cast<uint32_t>(byte & 3);
-                    const uint32_t sel = b | ((b + 4) << 4);
-                    const uint32_t w0 = __byte_perm(__byte_perm(src[0], src[1], sel),
-                                                    __byte_perm(src[2], src[3], sel), 0x5410);
-                    const uint32_t w1 = __byte_perm(__byte_perm(src[4], src[5], sel),
-                                                    __byte_perm(src[6], src[7], sel), 0x5410);
-                    tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2), w0, w1);
+                    for (int t = 1; t <= kDig; ++t) {
+                        const int byte = 7 - t;
+                        const uint32_t* src = byte >= 4 ? hi : lo;
+                        const uint32_t b = static_cast<uint32_t>(byte & 3);
+                        const uint32_t sel = b | ((b + 4) << 4);
+                        const uint32_t w0 = __byte_perm(__byte_perm(src[0], src[1], sel),
+                                                        __byte_perm(src[2], src[3], sel), 0x5410);
+                        const uint32_t w1 = __byte_perm(__byte_perm(src[4], src[5], sel),
+                                                        __byte_perm(src[6], src[7], sel), 0x5410);
+                        tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2), w0, w1);
+                    }
+                    tmem_st_wait();
                 }
-                tmem_st_wait();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&empty_d[sd]);
-                mbar_arrive(&full_a[sa]);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&empty_d[sd]);
+                    mbar_arrive(&full_a[sa]);
+                }
+            } else {
+                // single A stage: convert into registers while the MMAs of the
+                // previous k-step still read the stage, then store
+                uint32_t wd[kDig][2];
+                if (dbg != 1) {
+                    double d[8];
+                    load8<TD>(dring + sd * DB, row, c0, d);
+                    uint32_t lo[8], hi[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);
+                        lo[j] = static_cast<uint32_t>(m);
+                        hi[j] = static_cast<uint32_t>(m >> 32);
+                    }
+#pragma unroll
+                    for (int t = 1; t <= kDig; ++t) {
+                        const int byte = 7 - t;
+                        const uint32_t* src = byte >= 4 ? hi : lo;
+                        const uint32_t b = static_cast<uint32_t>(byte & 3);
+                        const uint32_t sel = b | ((b + 4) << 4);
+                        wd[t - 1][0] = __byte_perm(__byte_perm(src[0], src[1], sel),
+                                                   __byte_perm(src[2], src[3], sel), 0x5410);
+                        wd[t - 1][1] = __byte_perm(__byte_perm(src[4], src[5], sel),
+                                                   __byte_perm(src[6], src[7], sel), 0x5410);
+                    }
+                }
+                if (k >= NA) {
+                    mbar_wait(&empty_a[sa], pa ^ 1);
+                    tc_fence_after();
+                }
+                if (dbg != 1) {
+                    const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64) + lane_off;
+#pragma unroll
+                    for (int t = 1; t <= kDig; ++t)
+                        tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2),
+                                 wd[t - 1][0], wd[t - 1][1]);
+                    tmem_st_wait();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&empty_d[sd]);
+                    mbar_arrive(&full_a[sa]);
+                }
             }
             if (++sd == ND) {
                 sd = 0;
@@ -726,6 +821,15 @@ __global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__
     }
 }
 
+// DSB_K2I_SS=1: the shared-memory-A kernel instead of the TMEM-A one
+bool k2i_force_ss() {
+    static const bool f = [] {
+        const char* e = std::getenv("DSB_K2I_SS");
+        return e && std::atoi(e) == 1;
+    }();
+    return f;
+}
+
 // DSB_K2I_DEBUG: 1 = skip the digit conversion, 2 = skip the MMAs (timing
 // experiments only; results are wrong)
 int k2i_debug_mode() {
@@ -740,14 +844,15 @@ template <int NB, typename TD>
 void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
             const int* row_exp, const int* col_exp, double* part, cudaStream_t st,
             const int* skip) {
-    if constexpr (NB == kNbTs) {
+    if (!k2i_force_ss()) {
         static bool attr_ts = false;
         if (!attr_ts) {
-            cudaFuncSetAttribute(k2i_product_ts<TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(ts_smem<TD>()));
+            cudaFuncSetAttribute(k2i_product_ts<NB, TD>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ts_smem<NB, TD>()));
             attr_ts = true;
         }
-        k2i_product_ts<TD><<<p.grid, kThreadsI8, ts_smem<TD>(), st>>>(
+        k2i_product_ts<NB, TD><<<p.grid, kThreadsI8, ts_smem<NB, TD>(), st>>>(
             *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
             p.maxseg, wp, skip, k2i_debug_mode());
         return;
