@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "comm.hpp"
+#include "kernels.cuh"
 #include "solver.hpp"
 
 using dsb::errc;
@@ -710,3 +711,22 @@ void* divscope_stream(void) {
 }
 
 }  // extern "C"
+
+// test hook: fingerprint of columns [col0, col0 + ncols) of a matrix handle's
+// rows (the sharded symmetry check, sharded.cpp)
+extern "C" int divscope_debug_block_fingerprint(const divscope_matrix* m, size_t col0,
+                                                size_t ncols, int swap,
+                                                unsigned long long* out) {
+    if (!m || !out) return DIVSCOPE_ERR_INVALID_ARGUMENT;
+    return wrap([&] {
+        dsb::Ctx& c = dsb::Ctx::get();
+        const dsb::Store& st = *m->m.store;
+        if (col0 + ncols > st.cols) throw Error(errc::invalid_argument, "bad column range");
+        auto* d = static_cast<unsigned long long*>(c.scratch("dbg_fp", 8));
+        DSB_CUDA(cudaMemsetAsync(d, 0, 8, c.stream));
+        dsb::launch_block_fingerprint(st.buf->p, st.dt, st.ld, st.rows, col0, ncols,
+                                      st.sharded ? st.row_begin : 0, swap != 0, d, c.sms,
+                                      c.stream);
+        c.d2h_copy(out, d, 8);
+    });
+}

@@ -117,6 +117,42 @@ __global__ void __launch_bounds__(256) k_asym_block(const T* __restrict__ a, siz
     if (tx == 0 && mx > 0.0) atomicMax(out, __double_as_longlong(mx));
 }
 
+// Order-independent 64-bit fingerprint of a block of D: sum over its entries
+// of a mix of (value bits, global row, global column), exact mod 2^64 (so
+// the result does not depend on the launch shape). With swap the positions
+// enter as (column, row): the fingerprint of a block equals that of the
+// transposed partner block iff (up to a 2^-64 collision) they are transposes.
+__device__ __forceinline__ unsigned long long fp_mix(unsigned long long v, unsigned long long i,
+                                                     unsigned long long j) {
+    unsigned long long x = v ^ (i * 0x9E3779B97F4A7C15ull) ^ (j * 0xC2B2AE3D27D4EB4Full);
+    x ^= x >> 31;
+    x *= 0x7FB5D329728EA185ull;
+    x ^= x >> 27;
+    x *= 0x81DADEF4BC2DD44Dull;
+    x ^= x >> 33;
+    return x;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_block_fingerprint(const T* __restrict__ d, size_t ld,
+                                                           size_t m, size_t col0, size_t ncols,
+                                                           size_t row0, int swap,
+                                                           unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    const size_t total = m * ncols;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t r = e / ncols, c = e % ncols;
+        const double v = static_cast<double>(d[r * ld + col0 + c]);
+        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+        const unsigned long long gi = row0 + r, gj = col0 + c;
+        acc += swap ? fp_mix(bits, gj, gi) : fp_mix(bits, gi, gj);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 }  // namespace
 
 int k1_rows_grid(size_t rows, int sms) {
@@ -145,6 +181,20 @@ void launch_asym_block(const void* a, size_t lda, const void* b, size_t ldb, DTy
     else
         k_asym_block<float><<<grid, 256, 0, st>>>(static_cast<const float*>(a), lda,
                                                   static_cast<const float*>(b), ldb, m, p, o);
+    count_launch();
+}
+
+void launch_block_fingerprint(const void* d, DType dt, size_t ld, size_t m, size_t col0,
+                              size_t ncols, size_t row0, bool swap, unsigned long long* out,
+                              int sms, cudaStream_t st) {
+    if (m == 0 || ncols == 0) return;
+    const int grid = static_cast<int>(std::min<size_t>((m * ncols + 255) / 256, sms * 8));
+    if (dt == DType::F64)
+        k_block_fingerprint<double><<<grid, 256, 0, st>>>(static_cast<const double*>(d), ld, m, col0,
+                                                          ncols, row0, swap ? 1 : 0, out);
+    else
+        k_block_fingerprint<float><<<grid, 256, 0, st>>>(static_cast<const float*>(d), ld, m, col0,
+                                                         ncols, row0, swap ? 1 : 0, out);
     count_launch();
 }
 

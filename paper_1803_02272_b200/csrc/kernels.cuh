@@ -132,6 +132,13 @@ void launch_sw(const unsigned char* seq, const long long* off, const int* len, i
                const SwPlan& p, unsigned short* dirs, int* hb, double* dout, size_t ld,
                long long* aux, cudaStream_t st);
 
+// out += order-independent fingerprint of the m x ncols block of a row shard
+// starting at column col0 (row0 = global index of its first row); swap: hash
+// positions as (column, row), the transposed partner's convention
+void launch_block_fingerprint(const void* d, DType dt, size_t ld, size_t m, size_t col0,
+                              size_t ncols, size_t row0, bool swap, unsigned long long* out,
+                              int sms, cudaStream_t st);
+
 // ---- panel kernels (n_pad x WP, k4-interleaved) -----------------------------
 int panel_grid(size_t n_pad, int sms);
 void launch_panel_from_rowmajor(const double* src, size_t n, int w, int wp, size_t n_pad,

@@ -134,7 +134,34 @@ Matrix gram_sharded(const Matrix& d) {
     launch_asym_block(static_cast<const char*>(s.buf->p) + rb * esz, s.ld,
                       static_cast<const char*>(s.buf->p) + rb * esz, s.ld, s.dt, m, m, red + 2,
                       c.stream);
+    // cross-rank blocks: fingerprints first (one pass over the local rows, a
+    // world x world all-gather); the exact block exchange only runs when some
+    // block pair differs, to report the exact max |d_ij - d_ji|
+    bool need_exchange = false;
     if (L.world > 1) {
+        const int W = L.world;
+        auto* fp = static_cast<unsigned long long*>(
+            c.scratch("sh_fp", static_cast<size_t>(W) * W * sizeof(unsigned long long)));
+        DSB_CUDA(cudaMemsetAsync(fp, 0, static_cast<size_t>(W) * W * 8, c.stream));
+        unsigned long long* mine = fp + static_cast<size_t>(L.rank) * W;
+        for (int h = 0; h < W; ++h) {
+            if (h == L.rank) continue;
+            launch_block_fingerprint(s.buf->p, s.dt, s.ld, m, L.rb[h], L.re[h] - L.rb[h], rb,
+                                     L.rank > h, mine + h, c.sms, c.stream);
+        }
+        std::vector<size_t> cnt(W, static_cast<size_t>(W)), dsp(W);
+        for (int r = 0; r < W; ++r) dsp[r] = static_cast<size_t>(r) * W;
+        cm.allgatherv(reinterpret_cast<double*>(fp), cnt.data(), dsp.data(), c.stream);
+        std::vector<unsigned long long> hfp(static_cast<size_t>(W) * W);
+        c.d2h_copy(hfp.data(), fp, hfp.size() * 8);
+        for (int g = 0; g < W && !need_exchange; ++g)
+            for (int h = g + 1; h < W; ++h)
+                if (hfp[static_cast<size_t>(g) * W + h] != hfp[static_cast<size_t>(h) * W + g]) {
+                    need_exchange = true;
+                    break;
+                }
+    }
+    if (need_exchange) {
         size_t maxm = 0;
         for (int r = 0; r < L.world; ++r) maxm = std::max(maxm, L.re[r] - L.rb[r]);
         // staging in f64 element units (f32 blocks travel as raw bytes)

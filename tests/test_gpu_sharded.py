@@ -94,3 +94,48 @@ def test_sharded_from_dvs_rows(ds, oracle, comm1, tmp_path):
     ref = ds.embed(ds.gram(ds.matrix_from_host(d)), rank=k, oversampling=p, power_iters=q,
                    seed=seed)
     np.testing.assert_allclose(e.eigenvalues, ref.eigenvalues, rtol=1e-10)
+
+
+def _fp_np(block, row0, col0, swap):
+    """numpy restatement of fp_mix summed over a block (k1_shard.cu)."""
+    with np.errstate(over="ignore"):
+        v = np.ascontiguousarray(block, dtype=np.float64).view(np.uint64)
+        i = (np.arange(block.shape[0], dtype=np.uint64) + np.uint64(row0))[:, None]
+        j = (np.arange(block.shape[1], dtype=np.uint64) + np.uint64(col0))[None, :]
+        if swap:
+            i, j = j, i
+        x = v ^ (i * np.uint64(0x9E3779B97F4A7C15)) ^ (j * np.uint64(0xC2B2AE3D27D4EB4F))
+        x ^= x >> np.uint64(31)
+        x *= np.uint64(0x7FB5D329728EA185)
+        x ^= x >> np.uint64(27)
+        x *= np.uint64(0x81DADEF4BC2DD44D)
+        x ^= x >> np.uint64(33)
+        return int(np.sum(x, dtype=np.uint64))
+
+
+def test_block_fingerprints_pair_transposes(ds, oracle):
+    # the sharded symmetry check compares rank g's fingerprint of D[R_g, C_h]
+    # with rank h's swapped fingerprint of D[R_h, C_g] (sharded.cpp)
+    import ctypes as C
+    fn = ds.lib.divscope_debug_block_fingerprint
+    fn.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(C.c_uint64)]
+
+    def fp(m, c0, nc, swap):
+        out = C.c_uint64(0)
+        assert fn(m.handle, c0, nc, int(swap), C.byref(out)) == 0
+        return out.value
+
+    n = 700
+    d = oracle.euclidean_matrix(ds.synth_points(2, n, 9))
+    a = ds.matrix_from_host_rows(d[0:256], n, 0, 256)
+    b = ds.matrix_from_host_rows(d[256:700], n, 256, 700)
+    fa, fb = fp(a, 256, 444, False), fp(b, 0, 256, True)
+    assert fa == fb == _fp_np(d[0:256, 256:700], 0, 256, False)
+    assert fb == _fp_np(d[256:700, 0:256], 256, 0, True)
+    d2 = d.copy()
+    d2[300, 10] = np.nextafter(d2[300, 10], 1e9)  # one ulp off its mirror
+    b2 = ds.matrix_from_host_rows(d2[256:700], n, 256, 700)
+    assert fp(b2, 0, 256, True) != fa
+    # f32 storage hashes the widened values
+    af = ds.matrix_from_host_rows_f32(d[0:256].astype(np.float32), n, 0, 256)
+    assert fp(af, 256, 444, False) == _fp_np(d[0:256, 256:700].astype(np.float32), 0, 256, False)
