@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -184,7 +185,7 @@ def reference_arm(args, wl):
         "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -200,14 +201,20 @@ def b200_arm(args, wl):
     import paper_1803_02272_b200 as ds
     ds.set_device(torch.cuda.current_device())
     cfg, n, k, p, q, seed, f32 = WORKLOADS[wl]
+    n1 = n
+    sharded = world > 1 or args.force_sharded
+    if sharded and not args.strong:
+        # weak scaling: every GPU streams the same n1^2 entries of D per pass,
+        # the matrix grows as n = n1 sqrt(N) (row-sharded over the N GPUs)
+        n = int(round(n1 * math.sqrt(world)))
     w = k + min(p, n - k)
     passes = 2 * q + 3
     stream = torch.cuda.ExternalStream(ds.stream_ptr())
-    sharded = world > 1
     if sharded:
-        # one NCCL communicator over the box; D row-sharded (strong scaling)
+        # one NCCL communicator over the box; D row-sharded
         obj = [ds.comm_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(obj, src=0)
+        if world > 1:
+            torch.distributed.broadcast_object_list(obj, src=0)
         ds.comm_init(world, rank, obj[0])
 
     def barrier():
@@ -357,14 +364,15 @@ def b200_arm(args, wl):
             "metric": "MDS distance entries/s per streaming pass", "value": value,
             "unit": "entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak",
+            "scaling": "strong" if (sharded and args.strong) else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, reference RNG conventions; D built on the GPU)",
-            "config": {"workload": wl, "n": n, "k": k, "p": p, "q": q, "seed": seed,
+            "config": {"workload": wl, "n": n, "n_single_gpu": n1, "k": k, "p": p, "q": q,
+                       "seed": seed,
                        "d_dtype": "f32" if f32 else "f64", "streaming_passes_per_step": passes,
                        "l2": "inputs larger than L2 (D = %.1f GB)" % (n * n * (4 if f32 else 8) / 1e9),
                        "parallelism": (f"dp{world} (D row-sharded, panel all-gather + Gram "
-                                       "all-reduce over NCCL)") if world > 1 else "single"},
+                                       "all-reduce over NCCL)") if sharded else "single"},
             "e2e": e2e,
             "gpu_launches": int(st.kernel_launches),
             "roofline": roofline,
@@ -373,14 +381,33 @@ def b200_arm(args, wl):
             "result_check": {"dims": int(e.dims), "lambda_1": float(e.eigenvalues[0])
                              if e.dims else None},
         }
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        emit(line)
+    if sharded:
         ds.comm_destroy()
+    if world > 1:
         torch.distributed.destroy_process_group()
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line, on the process's original stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # stdout carries exactly one JSON line: keep a handle on the original
+    # stdout for it and send everything else written to fd 1 (NCCL's version
+    # banner and debug lines, library prints) to stderr
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -389,6 +416,11 @@ def main():
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (huge D)")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the row-sharded path even on one GPU (testing)")
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1: keep the workload's n (strong scaling); default grows n as "
+                         "n1 sqrt(N) so each GPU streams n1^2 entries per pass (weak scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args, args.workload)

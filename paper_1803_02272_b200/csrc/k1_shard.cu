@@ -1,5 +1,5 @@
 // K1 for a row shard of D (multi-GPU pass 0): a warp streams one full row at
-// a time (16-byte loads, 4 in flight per lane), giving the row sum of d^2 in a
+// a time (16-byte loads, 8 in flight per lane), giving the row sum of d^2 in a
 // fixed order, plus per-CTA sum d^4 / max |d|; and the cross-shard symmetry
 // check max |d_ij - d_ji| on exchanged blocks (ref src/mds.cpp:21-41).
 #include <algorithm>
@@ -38,19 +38,21 @@ __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, s
         double s = 0.0;
         uint32_t hmx = 0u;  // max over the row of the high word of d^2 (>= 0)
         size_t c = 2 * lane;
-        // main body: 4 independent 2-element loads per lane per iteration
-        for (; c + 192 + 1 < cols; c += 256) {
-            typename V2<T>::type v[4];
+        // main body: 8 independent 2-element loads per lane per iteration
+        for (; c + 448 + 1 < cols; c += 512) {
+            typename V2<T>::type v[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 8; ++u)
                 v[u] = __ldg(reinterpret_cast<const typename V2<T>::type*>(row + c + 64 * u));
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const double a0 = v[u].x, a1 = v[u].y;
                 const double s0 = a0 * a0, s1 = a1 * a1;
                 s += s0 + s1;
                 sum4 += s0 * s0 + s1 * s1;
-                maxabs = fmax(maxabs, fmax(fabs(a0), fabs(a1)));
+                // NaN-ignoring select, as the reference's std::max scan
+                const double m01 = fabs(a1) > fabs(a0) ? fabs(a1) : fabs(a0);
+                maxabs = m01 > maxabs ? m01 : maxabs;
                 hmx = max(hmx, max(static_cast<uint32_t>(__double2hiint(s0)),
                                    static_cast<uint32_t>(__double2hiint(s1))));
             }
@@ -61,7 +63,8 @@ __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, s
             const double s0 = a0 * a0, s1 = a1 * a1;
             s += s0 + s1;
             sum4 += s0 * s0 + s1 * s1;
-            maxabs = fmax(maxabs, fmax(fabs(a0), fabs(a1)));
+            const double m01 = fabs(a1) > fabs(a0) ? fabs(a1) : fabs(a0);
+            maxabs = m01 > maxabs ? m01 : maxabs;
             hmx = max(hmx, max(static_cast<uint32_t>(__double2hiint(s0)),
                                static_cast<uint32_t>(__double2hiint(s1))));
         }

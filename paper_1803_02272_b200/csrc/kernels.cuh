@@ -168,6 +168,11 @@ void launch_sr_step(const double* y, size_t n, int wp, double* partial, SrState*
 // drop, K3); flags[0] |= 1 when shifted.
 void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shift, double* rinv,
                      int* flags, cudaStream_t st);
+// the fused kernel's L D L^T elimination (carrying L^{-1}) as one CTA, WP <= 64:
+// rinv = R^{-1} with the shift (pass 0) / drop (later passes) rules; false
+// when WP is not supported (use launch_chol_inv)
+bool launch_chol_inv_elim(const double* w_mat, int wp, int w, size_t n, int pass, double* rinv,
+                          int* flags, cudaStream_t st);
 // q = y * rinv (row-wise, upper-triangular rinv)
 void launch_panel_apply(const double* y, const double* rinv, size_t n_pad, int wp, double* q,
                         cudaStream_t st);

@@ -1,19 +1,19 @@
-// K3 fast path (panel width WP <= 32): the whole CholeskyQR3 of one
+// K3 fast path (panel width WP <= 64): the whole CholeskyQR2/3 of one
 // orthonormalization in ONE cooperative launch (replaces thin_orthonormal,
 // ref src/rsvd.cpp:38-44).
 //
-// Per pass (3 passes: shifted-if-needed, then two plain):
+// Per pass (pass 0 may shift; a third pass only when it did):
 //   1. each CTA forms the partial Gram Y_c^T Y_c of its contiguous row range
-//      on the f64 tensor cores (interleaved layout => contiguous fragments);
-//   2. grid sync; CTA c sums elements e = c, c + P, ... over the partials in
-//      CTA order (deterministic); grid sync;
-//   3. every CTA factors W = R^T R redundantly in one warp, lane j holding
-//      column j in registers (identical inputs and code => identical R in all
-//      CTAs), with the shift / drop rules of launch_chol_inv;
-//   4. each thread solves q_i R = y_i for one of the CTA's rows (forward
-//      substitution; dropped columns come out as zero).
+//      (resident in shared memory) on the f64 tensor cores;
+//   2. grid sync; fixed-order reduction of the partials (warp per element);
+//      grid sync;
+//   3. every CTA factors W = L D L^T redundantly (identical inputs and code =>
+//      identical factors), carrying E = L^{-1} along the elimination, with
+//      the shift / drop rules of launch_chol_inv; T = L^{-T} D^{-1/2};
+//   4. Q = Y T on the f64 tensor cores, in place, right to left.
 // Rows never leave their CTA between passes, so a pass needs only the two
-// grid syncs around the Gram reduction.
+// grid syncs around the Gram reduction. The same single-CTA elimination is
+// exported for the multi-kernel (sharded) path: launch_chol_inv_elim.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -315,6 +315,64 @@ bool launch_wp(double* y, double* out, size_t n_pad, int w, size_t n, double* pa
                                        dim3(256), args, smem, st) == cudaSuccess;
 }
 
+// Single-CTA W -> T = R^{-1} for the multi-kernel / sharded CholeskyQR
+// (same elimination and pivot rules as the fused kernel's step 3 and 4a).
+template <int WP>
+__global__ void __launch_bounds__(256) k_chol_inv_elim(const double* __restrict__ wmat, int w,
+                                                       double nrows, int pass,
+                                                       double* __restrict__ rinv,
+                                                       int* __restrict__ flags) {
+    __shared__ int dropped_s[WP];
+    __shared__ double d0s[WP];
+    __shared__ double dpiv[WP];
+    __shared__ double tr_s[2];
+    __shared__ unsigned short tri[WP * (WP + 1) / 2];
+    __shared__ int tri_off[WP + 1];
+    extern __shared__ double ce[];  // R [WP*WP], E [WP*WP]
+    double* R = ce;
+    double* E = R + WP * WP;
+    const int tid = threadIdx.x;
+    for (int i = tid; i <= WP; i += blockDim.x) {
+        const int off = i * WP - (i * (i - 1)) / 2;
+        tri_off[i] = off;
+        for (int j = i; j < WP && i < WP; ++j)
+            tri[off + j - i] = static_cast<unsigned short>((i << 8) | j);
+    }
+    if (tid < WP) d0s[tid] = tid < w ? wmat[tid * WP + tid] : 0.0;
+    __syncthreads();
+    if (tid == 0) {
+        double tr = 0.0, mx = 0.0;
+        for (int j = 0; j < w; ++j) {
+            tr += d0s[j];
+            mx = fmax(mx, d0s[j]);
+        }
+        tr_s[0] = tr;
+        tr_s[1] = mx;
+    }
+    double sigma = 0.0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        for (int e = tid; e < WP * WP; e += blockDim.x) {
+            const int i = e / WP, j = e % WP;
+            double v = (i < w && j < w) ? wmat[e] : 0.0;
+            if (i == j && i < w && d0s[i] > 0.0) v += sigma;
+            R[e] = v;
+        }
+        __syncthreads();
+        if (!cta_chol_inverse<WP>(R, E, w, d0s, tr_s[1], pass == 0 && attempt == 0, pass != 0,
+                                  dropped_s, dpiv, tri, tri_off))
+            break;
+        sigma = 11.0 * (nrows * w + static_cast<double>(w) * (w + 1)) * 0x1.0p-53 * tr_s[0];
+        if (tid == 0) flags[0] |= 1;
+        __syncthreads();
+    }
+    __syncthreads();
+    for (int e = tid; e < WP * WP; e += blockDim.x) {
+        const int i = e / WP, j = e % WP;
+        const double dj = dpiv[j];
+        rinv[e] = (i <= j && dj > 0.0) ? E[j * WP + i] * rsqrt(dj) : 0.0;
+    }
+}
+
 }  // namespace
 
 extern "C" void divscope_debug_orth_prof(long long* dev_buf) { g_orth_prof = dev_buf; }
@@ -340,6 +398,25 @@ bool launch_orth_fused(double* y, double* t, double* out, size_t n_pad, int wp, 
     }
     if (ok) count_launch();
     return ok;
+}
+
+bool launch_chol_inv_elim(const double* w_mat, int wp, int w, size_t n, int pass, double* rinv,
+                          int* flags, cudaStream_t st) {
+    const size_t smem = static_cast<size_t>(2) * wp * wp * sizeof(double);
+    const double nr = static_cast<double>(n);
+    switch (wp) {
+#define DSB_CE(W)                                                                              \
+    case W:                                                                                    \
+        allow_dyn_smem(reinterpret_cast<const void*>(k_chol_inv_elim<W>));                     \
+        k_chol_inv_elim<W><<<1, 256, smem, st>>>(w_mat, w, nr, pass, rinv, flags);             \
+        break;
+        DSB_CE(8) DSB_CE(16) DSB_CE(24) DSB_CE(32) DSB_CE(40) DSB_CE(48) DSB_CE(56) DSB_CE(64)
+#undef DSB_CE
+        default:
+            return false;
+    }
+    count_launch();
+    return true;
 }
 
 }  // namespace dsb

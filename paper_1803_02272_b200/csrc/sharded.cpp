@@ -394,7 +394,8 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         for (int ps = 0; ps < 3; ++ps) {
             launch_panel_dot(bufs[ps][0], bufs[ps][0], m_pad, wp, psmall, wmat, c.sms, c.stream);
             cm.allreduce_sum(wmat, static_cast<size_t>(wp) * wp, c.stream);
-            launch_chol_inv(wmat, wp, wi, n, ps == 0 ? 1 : 0, rinv, flags, c.stream);
+            if (!launch_chol_inv_elim(wmat, wp, wi, n, ps, rinv, flags, c.stream))
+                launch_chol_inv(wmat, wp, wi, n, ps == 0 ? 1 : 0, rinv, flags, c.stream);
             launch_panel_apply(bufs[ps][0], rinv, m_pad, wp, bufs[ps][1], c.stream);
         }
         cm.allgatherv(out_full, cnt.data(), off.data(), c.stream);
