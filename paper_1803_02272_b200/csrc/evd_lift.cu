@@ -159,15 +159,23 @@ __device__ void evd_finish_dg(const double* __restrict__ dg, const double* __res
     //   |la| > |lb|, or |la| == |lb| and la > lb, or la == lb and a < b
     // (equal values keep the ascending sort's index order). Each thread
     // computes its element's rank by counting predecessors.
+    // NaN eigenvalues (non-finite input) sort last by index, so the ranks
+    // always form a permutation
     for (int a = tid; a < w; a += nt) {
         const double la = dg[a];
+        const bool na = isnan(la);
         int pos = 0;
         for (int b = 0; b < w; ++b) {
             if (b == a) continue;
             const double lb = dg[b];
-            const bool b_first = (fabs(lb) != fabs(la)) ? (fabs(lb) > fabs(la))
-                                 : (lb != la)           ? (lb > la)
-                                                        : (b < a);
+            const bool nb = isnan(lb);
+            bool b_first;
+            if (na || nb)
+                b_first = (na && nb) ? (b < a) : na;
+            else
+                b_first = (fabs(lb) != fabs(la)) ? (fabs(lb) > fabs(la))
+                          : (lb != la)           ? (lb > la)
+                                                 : (b < a);
             pos += b_first ? 1 : 0;
         }
         order[pos] = a;

@@ -470,3 +470,49 @@ def test_workspace_reuse_large_then_small(ds, oracle):
         vals, _ = ds.eigs(ds.gram(ds.matrix_from_host(d)), rank=w_rank, oversampling=w_p,
                           power_iters=2, seed=5)
         np.testing.assert_allclose(vals[:8], want[:8], rtol=1e-9)
+
+
+def test_int8_product_admission_and_f32(ds, oracle, product_path):
+    # K2i admission (solver.cpp use_int8_product): finite data with a row
+    # max/mean ratio <= 2^12 and w <= 64; otherwise the fp64 kernel runs
+    if product_path != "int8":
+        pytest.skip("int8-specific")
+    n = 600
+    pts = ds.synth_points(2, n, 4)
+    d = oracle.euclidean_matrix(pts)
+    k, p = 12, 8
+    e8_d = ds.embed(ds.gram(ds.matrix_from_host(d)), rank=k, oversampling=p, seed=2)
+    assert ds.stats_get().last_product_kernel == 1
+    # f32 storage on the int8 path vs the fp64 kernel on the same f32 D
+    d32 = d.astype(np.float32)
+    e8 = ds.embed(ds.gram(ds.matrix_from_host_f32(d32)), rank=k, oversampling=p, seed=2)
+    assert ds.stats_get().last_product_kernel == 1
+    ds.set_product_path(1)
+    e64 = ds.embed(ds.gram(ds.matrix_from_host_f32(d32)), rank=k, oversampling=p, seed=2)
+    assert ds.stats_get().last_product_kernel == 0
+    ds.set_product_path(2)
+    np.testing.assert_allclose(e8.eigenvalues, e64.eigenvalues, rtol=1e-12)
+    # the ratio bound 2^e_i / r_i is <= 2 n, so rejection needs n > 2048: a
+    # tight cluster plus one far point gives rows with max d^2 ~ n * mean
+    rng = np.random.default_rng(6)
+    clu = rng.standard_normal((5000, 3)) * 1e-3
+    clu[0] = (1e3, 0.0, 0.0)
+    dfar = oracle.euclidean_matrix(clu)
+    ds.embed(ds.gram(ds.matrix_from_host(dfar)), rank=k, oversampling=p, seed=2)
+    assert ds.stats_get().last_product_kernel == 0
+    # the same cluster without the outlier is admitted
+    dclu = oracle.euclidean_matrix(clu[1:])
+    ds.embed(ds.gram(ds.matrix_from_host(dclu)), rank=k, oversampling=p, seed=2)
+    assert ds.stats_get().last_product_kernel == 1
+    # non-finite data -> fp64 kernel; the NaN Ritz matrix fails the small
+    # eigensolve like Eigen's (ref rsvd.cpp:113-114), without corrupting state
+    dn = d.copy()
+    dn[3, 5] = dn[5, 3] = np.inf
+    assert err(ds, ds.embed, ds.gram(ds.matrix_from_host(dn)), rank=k, oversampling=p,
+               seed=2) == ds.Status.ERR_INTERNAL
+    assert ds.stats_get().last_product_kernel == 0
+    again = ds.embed(ds.gram(ds.matrix_from_host(d)), rank=k, oversampling=p, seed=2)
+    np.testing.assert_allclose(again.eigenvalues, e8_d.eigenvalues, rtol=1e-12)
+    # w > 64 -> fp64
+    ds.embed(ds.gram(ds.matrix_from_host(d)), rank=60, oversampling=10, seed=2)
+    assert ds.stats_get().last_product_kernel == 0
