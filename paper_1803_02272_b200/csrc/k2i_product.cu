@@ -414,13 +414,37 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 constexpr int kBStagesTs = 4;
 
 
+#ifndef DSB_TS_NB64_HYBRID
+#define DSB_TS_NB64_HYBRID 1
+#endif
+// NB = 64 hybrid: digits 1..4 of each A stage in TMEM (4 x 8 columns, two
+// stages in the 64 columns left after the 448 accumulator columns), digits
+// 5..7 — whose MMAs are narrow (N' <= 192) and so pay the shared-memory
+// A floor anyway — from shared memory. Two stages let the conversion of the
+// next k-step proceed while the MMAs of the current one run.
+template <int NB>
+constexpr bool hybrid_ts() {
+    return NB > 32 && DSB_TS_NB64_HYBRID;
+}
+template <int NB>
+constexpr int tmem_digits_ts() {
+    return hybrid_ts<NB>() ? 4 : kDig;
+}
 template <int NB>
 constexpr int a_stages_ts() {
-    return NB <= 32 ? 4 : 1;
+    return NB <= 32 ? 4 : (hybrid_ts<NB>() ? 2 : 1);
+}
+template <int NB>
+constexpr uint32_t a_stage_cols_ts() {
+    return hybrid_ts<NB>() ? 32u : 64u;
 }
 template <int NB>
 constexpr uint32_t a_base_ts() {  // first TMEM column of the A stages
     return NB <= 32 ? 256u : 448u;
+}
+template <int NB>
+constexpr int a_smem_stage_ts() {  // bytes of shared-memory A digits per stage
+    return (kDig - tmem_digits_ts<NB>()) * kRowsI8 * kKStep;
 }
 template <int NB>
 constexpr int b_stages_ts() {
@@ -428,12 +452,15 @@ constexpr int b_stages_ts() {
 }
 template <int NB, typename TD>
 constexpr int d_stages_ts() {
-    return std::min(8, (DSB_TS_SMEM_KB * 1024 - b_stages_ts<NB>() * b_bytes<NB>()) / d_bytes<TD>());
+    return std::min(8, (DSB_TS_SMEM_KB * 1024 - b_stages_ts<NB>() * b_bytes<NB>() -
+                        a_stages_ts<NB>() * a_smem_stage_ts<NB>()) /
+                           d_bytes<TD>());
 }
 template <int NB, typename TD>
 constexpr size_t ts_smem() {
     return 1024 + static_cast<size_t>(d_stages_ts<NB, TD>()) * d_bytes<TD>() +
-           b_stages_ts<NB>() * b_bytes<NB>() + 448 + NB * 8;
+           b_stages_ts<NB>() * b_bytes<NB>() + a_stages_ts<NB>() * a_smem_stage_ts<NB>() + 448 +
+           NB * 8;
 }
 
 // 8 consecutive d values of row `row`, columns c0..c0+7 of the k-step tile
@@ -478,12 +505,16 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     constexpr int NBR = kBProd ? kBStagesTs : NA;
     constexpr int DB = d_bytes<TD>();
     constexpr int BB = b_bytes<NB>();
+    constexpr int TD_DIG = tmem_digits_ts<NB>();  // digits 1..TD_DIG in TMEM
+    constexpr int ASB = a_smem_stage_ts<NB>();     // the rest in shared memory
+    constexpr uint32_t ACOLS = a_stage_cols_ts<NB>();
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* dring = sm;
     unsigned char* bring = sm + ND * DB;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NBR * BB);
+    unsigned char* aring = bring + NBR * BB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(aring + NA * ASB);
     uint64_t* full_d = bars;
     uint64_t* empty_d = full_d + ND;
     uint64_t* full_a = empty_d + ND;
@@ -581,7 +612,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 }
                 started = true;
                 const uint32_t bbase = smem_u32(bring + sb * BB);
-                const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64);
+                const uint32_t ta = tmem_a + static_cast<uint32_t>(sa) * ACOLS;
+                const uint32_t asm_base = smem_u32(aring + sa * ASB);
                 if (dbg != 2) {
 #pragma unroll
                     for (int t = 1; t <= kDig; ++t) {
@@ -592,10 +624,17 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                             const int nu = (umax - u0 + 1 < per) ? (umax - u0 + 1) : per;
                             const uint64_t bd =
                                 umma_desc_k_interleave(bbase + (u0 - 1) * (NB * kKStep));
-                            umma_i8_ts(tmem + static_cast<uint32_t>((t + u0 - 2) * NB),
-                                       ta + static_cast<uint32_t>((t - 1) * 8), bd,
-                                       umma_idesc_i8(nu * NB, false, true),
-                                       (first && t == 1) ? 0 : 1);
+                            const uint32_t dcol = tmem + static_cast<uint32_t>((t + u0 - 2) * NB);
+                            const uint32_t idesc = umma_idesc_i8(nu * NB, false, true);
+                            const int acc = (first && t == 1) ? 0 : 1;
+                            if (t <= TD_DIG)
+                                umma_i8_ts(dcol, ta + static_cast<uint32_t>((t - 1) * 8), bd,
+                                           idesc, acc);
+                            else
+                                umma_i8(dcol,
+                                        umma_desc_k_interleave(
+                                            asm_base + (t - TD_DIG - 1) * (kRowsI8 * kKStep)),
+                                        bd, idesc, acc);
                         }
                     }
                 }
@@ -657,7 +696,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                         lo[j] = static_cast<uint32_t>(m);
                         hi[j] = static_cast<uint32_t>(m >> 32);
                     }
-                    const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64) + lane_off;
+                    const uint32_t ta = tmem_a + static_cast<uint32_t>(sa) * ACOLS + lane_off;
+                    unsigned char* as = aring + sa * ASB + umma_tile_off(row, c0);
 #pragma unroll
                     for (int t = 1; t <= kDig; ++t) {
                         const int byte = 7 - t;
@@ -668,9 +708,14 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                                                         __byte_perm(src[2], src[3], sel), 0x5410);
                         const uint32_t w1 = __byte_perm(__byte_perm(src[4], src[5], sel),
                                                         __byte_perm(src[6], src[7], sel), 0x5410);
-                        tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2), w0, w1);
+                        if (t <= TD_DIG)
+                            tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2), w0, w1);
+                        else
+                            *reinterpret_cast<uint2*>(as + (t - TD_DIG - 1) * (kRowsI8 * kKStep)) =
+                                make_uint2(w0, w1);
                     }
                     tmem_st_wait();
+                    if constexpr (TD_DIG < kDig) fence_proxy_async();
                 }
                 tc_fence_before();
                 __syncwarp();

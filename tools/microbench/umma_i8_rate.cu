@@ -34,6 +34,23 @@ __global__ void k_rate(int iters, int pattern, int nb, unsigned long long* cycle
                     umma_i8_ts(tmem + (t - 1) * nb, tmem + 256 + (t - 1) * 8,
                                umma_desc_k_interleave(smem_u32(sb)),
                                umma_idesc_i8((8 - t) * nb, false, true), 1);
+            } else if (pattern == 3 || pattern == 4) {
+                // NB = 64: digits 1..4 from TMEM (pattern 3: 5..7 from smem;
+                // pattern 4: all from TMEM), N' split at 256
+                for (int t = 1; t <= 7; ++t) {
+                    const int per = 256 / nb, umax = 8 - t;
+                    for (int u0 = 1; u0 <= umax; u0 += per) {
+                        const int nu = (umax - u0 + 1 < per) ? (umax - u0 + 1) : per;
+                        const uint64_t bd = umma_desc_k_interleave(smem_u32(sb + (u0 - 1) * nb * 32));
+                        if (t <= 4 || pattern == 4)
+                            umma_i8_ts(tmem + (t + u0 - 2) * nb, tmem + 448, bd,
+                                       umma_idesc_i8(nu * nb, false, true), 1);
+                        else
+                            umma_i8(tmem + (t + u0 - 2) * nb,
+                                    umma_desc_k_interleave(smem_u32(sa + (t - 1) * 4096)), bd,
+                                    umma_idesc_i8(nu * nb, false, true), 1);
+                    }
+                }
             } else if (pattern == 0) {
                 for (int t = 1; t <= 7; ++t) {
                     const int per = 256 / nb, umax = 8 - t;
@@ -76,7 +93,9 @@ int main() {
     const Cfg cfgs[] = {{0, 32, 28 * 32, "digit pattern NB=32 (7 MMAs, N'=224..32)"},
                         {0, 64, 28 * 64, "digit pattern NB=64 (10 MMAs)"},
                         {1, 32, 4 * 224, "4 x N=224"},
-                        {2, 32, 28 * 32, "digit pattern NB=32, A in TMEM"}};
+                        {2, 32, 28 * 32, "digit pattern NB=32, A in TMEM"},
+                        {3, 64, 28 * 64, "NB=64 hybrid (digits 1-4 TMEM, 5-7 smem)"},
+                        {4, 64, 28 * 64, "NB=64 all digits in TMEM"}};
     for (const Cfg& c : cfgs) {
         const int iters = 4000;
         k_rate<<<sms, 128, smem>>>(10, c.pattern, c.nb, dc);
