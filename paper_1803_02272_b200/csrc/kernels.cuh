@@ -181,8 +181,16 @@ void launch_panel_apply(const double* y, const double* rinv, size_t n_pad, int w
 // in one cooperative launch (returns false when not applicable / launch
 // refused, in which case the caller uses the multi-kernel path).
 int orth_fused_grid(size_t n_pad, int sms);
+// cstat (nullable): per CTA [3][WP] column statistics of the result for the
+// next product pass (1^T Q, r^T Q with row_mean (nullable -> 0), max |Q|);
+// reduce with launch_colstats_final over orth_fused_grid() CTAs
 bool launch_orth_fused(double* y, double* t, double* out, size_t n_pad, int wp, int w, size_t n,
-                       double* partial, double* wsum, int* flags, int sms, cudaStream_t st);
+                       double* partial, double* wsum, int* flags, int sms, cudaStream_t st,
+                       const double* row_mean = nullptr, double* cstat = nullptr);
+// colsums[0..wp) = sum_c s, [wp..2wp) = sum_c t; col_exp (nullable) from the
+// maxima (int8 panel digits), over P per-CTA [3][wp] statistics
+void launch_colstats_final(const double* cstat, int P, int wp, int nb, double* colsums,
+                           int* col_exp, cudaStream_t st);
 
 // ---- K5: Rayleigh-Ritz EVD + |lambda| ordering + embed filter (1 CTA) -----
 struct EvdOut {

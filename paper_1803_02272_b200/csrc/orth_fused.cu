@@ -92,7 +92,8 @@ template <int WP>
 __global__ void __launch_bounds__(256, 1)
     k_orth_fused(const double* __restrict__ y, double* __restrict__ out, size_t n_pad, int w,
                  double nrows, int ldr, double* __restrict__ partial, double* __restrict__ wsum,
-                 int* __restrict__ flags, long long* __restrict__ prof) {
+                 int* __restrict__ flags, long long* __restrict__ prof,
+                 const double* __restrict__ row_mean, double* __restrict__ cstat) {
     long long t_last = clock64();
     int prof_i = 0;
     auto mark = [&]() {
@@ -286,11 +287,31 @@ __global__ void __launch_bounds__(256, 1)
             dst[e] = ps[cc * ldr + 4 * qb + rr];
         }
     }
+    if (cstat) {
+        // the next product pass's column statistics of this CTA's rows:
+        // 1^T Q, r^T Q (centering) and max |Q| (int8 column exponents),
+        // rows in order; reduced over the CTAs by launch_colstats_final
+        const size_t i0 = q0 * 4;
+        for (int cc = threadIdx.x; cc < WP; cc += blockDim.x) {
+            double sv = 0.0, tv = 0.0, mv = 0.0;
+            for (int r = 0; r < nrow; ++r) {
+                const double v = ps[cc * ldr + r];
+                sv += v;
+                if (row_mean && i0 + r < static_cast<size_t>(nrows)) tv += row_mean[i0 + r] * v;
+                mv = fmax(mv, fabs(v));
+            }
+            double* o = cstat + static_cast<size_t>(c) * 3 * WP;
+            o[cc] = sv;
+            o[WP + cc] = tv;
+            o[2 * WP + cc] = mv;
+        }
+    }
 }
 
 template <int WP>
 bool launch_wp(double* y, double* out, size_t n_pad, int w, size_t n, double* partial,
-               double* wsum, int* flags, int sms, cudaStream_t st) {
+               double* wsum, int* flags, int sms, cudaStream_t st, const double* row_mean,
+               double* cstat) {
     const int P = std::min<int>(sms, static_cast<int>(std::max<size_t>(n_pad / 4 / 8, 1)));
     const size_t nq = n_pad / 4;
     const int rows_max = static_cast<int>(((nq + P - 1) / P) * 4);
@@ -310,7 +331,8 @@ bool launch_wp(double* y, double* out, size_t n_pad, int w, size_t n, double* pa
     int ldr_a = ldr;
     const double* yc = y;
     long long* prof = g_orth_prof;
-    void* args[] = {&yc, &out, &n_pad, &w, &nr, &ldr_a, &partial, &wsum, &flags, &prof};
+    void* args[] = {&yc,   &out,   &n_pad, &w,    &nr,       &ldr_a,
+                    &partial, &wsum, &flags, &prof, &row_mean, &cstat};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_orth_fused<WP>), dim3(P),
                                        dim3(256), args, smem, st) == cudaSuccess;
 }
@@ -382,18 +404,19 @@ int orth_fused_grid(size_t n_pad, int sms) {
 }
 
 bool launch_orth_fused(double* y, double* t, double* out, size_t n_pad, int wp, int w, size_t n,
-                       double* partial, double* wsum, int* flags, int sms, cudaStream_t st) {
+                       double* partial, double* wsum, int* flags, int sms, cudaStream_t st,
+                       const double* row_mean, double* cstat) {
     (void)t;
     bool ok = false;
     switch (wp) {
-        case 8: ok = launch_wp<8>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
-        case 16: ok = launch_wp<16>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
-        case 24: ok = launch_wp<24>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
-        case 32: ok = launch_wp<32>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
-        case 40: ok = launch_wp<40>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
-        case 48: ok = launch_wp<48>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
-        case 56: ok = launch_wp<56>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
-        case 64: ok = launch_wp<64>(y, out, n_pad, w, n, partial, wsum, flags, sms, st); break;
+        case 8: ok = launch_wp<8>(y, out, n_pad, w, n, partial, wsum, flags, sms, st, row_mean, cstat); break;
+        case 16: ok = launch_wp<16>(y, out, n_pad, w, n, partial, wsum, flags, sms, st, row_mean, cstat); break;
+        case 24: ok = launch_wp<24>(y, out, n_pad, w, n, partial, wsum, flags, sms, st, row_mean, cstat); break;
+        case 32: ok = launch_wp<32>(y, out, n_pad, w, n, partial, wsum, flags, sms, st, row_mean, cstat); break;
+        case 40: ok = launch_wp<40>(y, out, n_pad, w, n, partial, wsum, flags, sms, st, row_mean, cstat); break;
+        case 48: ok = launch_wp<48>(y, out, n_pad, w, n, partial, wsum, flags, sms, st, row_mean, cstat); break;
+        case 56: ok = launch_wp<56>(y, out, n_pad, w, n, partial, wsum, flags, sms, st, row_mean, cstat); break;
+        case 64: ok = launch_wp<64>(y, out, n_pad, w, n, partial, wsum, flags, sms, st, row_mean, cstat); break;
         default: return false;
     }
     if (ok) count_launch();

@@ -379,6 +379,38 @@ __global__ void __launch_bounds__(256) k_sr_scale(const double* __restrict__ y, 
         x[pidx(i, 0, wp)] = y[pidx(i, 0, wp)] / norm;
 }
 
+// one warp per output: e < 2 wp sums (s, then t), e >= 2 wp the column
+// exponents from the maxima; lanes stride over the P CTA statistics in a
+// fixed order, xor-tree combine => deterministic
+__global__ void __launch_bounds__(256) k_colstats_final(const double* __restrict__ cstat, int P,
+                                                        int wp, int nb, double* __restrict__ colsums,
+                                                        int* __restrict__ col_exp) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nsum = 2 * wp;
+    if (gw < nsum) {
+        double v = 0.0;
+        for (int b = lane; b < P; b += 32) v += cstat[static_cast<size_t>(b) * 3 * wp + gw];
+        v = warp_sum(v);
+        if (lane == 0) colsums[gw] = v;
+    } else if (col_exp && gw < nsum + nb) {
+        const int c = gw - nsum;
+        double m = 0.0;
+        if (c < wp)
+            for (int b = lane; b < P; b += 32)
+                m = fmax(m, cstat[static_cast<size_t>(b) * 3 * wp + 2 * wp + c]);
+        m = warp_max(m);
+        if (lane == 0) {
+            int f = -1100;
+            if (m > 0.0) {
+                int e;
+                frexp(m, &e);  // m < 2^e
+                f = e + 2;
+            }
+            col_exp[c] = f;
+        }
+    }
+}
+
 }  // namespace
 
 int panel_grid(size_t n_pad, int sms) {
@@ -481,6 +513,15 @@ namespace dsb {
 // out[0] = sum of count doubles, fixed order (deterministic)
 void launch_sum_fixed(const double* partial, size_t count, double* out, cudaStream_t st) {
     k_sum_partials<<<1, 1024, 0, st>>>(partial, static_cast<int>(count), 1, out);
+    count_launch(1);
+}
+}  // namespace dsb
+
+namespace dsb {
+void launch_colstats_final(const double* cstat, int P, int wp, int nb, double* colsums,
+                           int* col_exp, cudaStream_t st) {
+    const int warps = 2 * wp + (col_exp ? nb : 0);
+    k_colstats_final<<<(warps * 32 + 255) / 256, 256, 0, st>>>(cstat, P, wp, nb, colsums, col_exp);
     count_launch(1);
 }
 }  // namespace dsb

@@ -261,12 +261,23 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     };
     mark("start");
     if (trace) std::fprintf(stderr, "[trace] host setup %.1f us\n", host_us());
+    // per-CTA column statistics left by the fused orth kernel for the next
+    // product pass (saves its separate column-statistics pass)
+    double* cstat = static_cast<double*>(c.scratch(
+        "orth_cstat", static_cast<size_t>(orth_fused_grid(n_pad, c.sms)) * 3 * wp * sizeof(double)));
+    bool stats_ready = false;
     auto product = [&](const double* x, double* y) {
-        if (use_i8)
+        if (stats_ready) {
+            // the orth kernel that produced x left its column statistics
+            launch_colstats_final(cstat, orth_fused_grid(n_pad, c.sms), wp, use_i8 ? iplan.nb : 0,
+                                  colsums, use_i8 ? col_exp : nullptr, c.stream);
+        } else if (use_i8) {
             launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream, pmax,
                            iplan.nb, col_exp);
-        else if (mode)
+        } else if (mode) {
             launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
+        }
+        stats_ready = false;
         cudaEvent_t e0, e1;
         c.make_events(&e0, &e1);
         if (use_i8)
@@ -282,10 +293,13 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     // CholeskyQR3 with shift/drop handling: y -> t -> y -> out
     auto orth = [&](double* y, double* t, double* out) {
         if (wp <= 64 &&
-            launch_orth_fused(y, t, out, n_pad, wp, wi, n, psmall, wmat, flags, c.sms, c.stream)) {
+            launch_orth_fused(y, t, out, n_pad, wp, wi, n, psmall, wmat, flags, c.sms, c.stream,
+                              mode ? row_mean : nullptr, (mode || use_i8) ? cstat : nullptr)) {
+            stats_ready = mode || use_i8;
             mark("orth");
             return;
         }
+        stats_ready = false;
         launch_panel_dot(y, y, n_pad, wp, psmall, wmat, c.sms, c.stream);
         launch_chol_inv(wmat, wp, wi, n, 1, rinv, flags, c.stream);
         launch_panel_apply(y, rinv, n_pad, wp, t, c.stream);
