@@ -489,6 +489,35 @@ __device__ __forceinline__ void load8(const unsigned char* tile, int row, int c0
     }
 }
 
+// Digit planes of 8 fixed-point values (lo/hi 32-bit halves): w[t-1][g] holds
+// digit t (byte 7 - t of the 56-bit value) of elements 4g..4g+3, byte j =
+// element 4g+j. Two bytes of two planes are gathered per first-level
+// byte_perm, so a pair of planes costs 4 permutes instead of 6.
+__device__ __forceinline__ void pack_digits(const uint32_t (&lo)[8], const uint32_t (&hi)[8],
+                                            uint32_t (&w)[kDig][2]) {
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        const int e = 4 * g;
+        // lo bytes 3,2 -> digits 4,5 ; lo bytes 1,0 -> digits 6,7
+        const uint32_t p45 = __byte_perm(lo[e], lo[e + 1], 0x6273);
+        const uint32_t q45 = __byte_perm(lo[e + 2], lo[e + 3], 0x6273);
+        w[3][g] = __byte_perm(p45, q45, 0x5410);
+        w[4][g] = __byte_perm(p45, q45, 0x7632);
+        const uint32_t p67 = __byte_perm(lo[e], lo[e + 1], 0x4051);
+        const uint32_t q67 = __byte_perm(lo[e + 2], lo[e + 3], 0x4051);
+        w[5][g] = __byte_perm(p67, q67, 0x5410);
+        w[6][g] = __byte_perm(p67, q67, 0x7632);
+        // hi bytes 2,1 -> digits 1,2 ; hi byte 0 -> digit 3
+        const uint32_t p12 = __byte_perm(hi[e], hi[e + 1], 0x5162);
+        const uint32_t q12 = __byte_perm(hi[e + 2], hi[e + 3], 0x5162);
+        w[0][g] = __byte_perm(p12, q12, 0x5410);
+        w[1][g] = __byte_perm(p12, q12, 0x7632);
+        const uint32_t p3 = __byte_perm(hi[e], hi[e + 1], 0x0040);
+        const uint32_t q3 = __byte_perm(hi[e + 2], hi[e + 3], 0x0040);
+        w[2][g] = __byte_perm(p3, q3, 0x5410);
+    }
+}
+
 template <int NB, typename TD>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
@@ -698,16 +727,11 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     }
                     const uint32_t ta = tmem_a + static_cast<uint32_t>(sa) * ACOLS + lane_off;
                     unsigned char* as = aring + sa * ASB + umma_tile_off(row, c0);
+                    uint32_t wd[kDig][2];
+                    pack_digits(lo, hi, wd);
 #pragma unroll
                     for (int t = 1; t <= kDig; ++t) {
-                        const int byte = 7 - t;
-                        const uint32_t* src = byte >= 4 ? hi : lo;
-                        const uint32_t b = static_cast<uint32_t>(byte & 3);
-                        const uint32_t sel = b | ((b + 4) << 4);
-                        const uint32_t w0 = __byte_perm(__byte_perm(src[0], src[1], sel),
-                                                        __byte_perm(src[2], src[3], sel), 0x5410);
-                        const uint32_t w1 = __byte_perm(__byte_perm(src[4], src[5], sel),
-                                                        __byte_perm(src[6], src[7], sel), 0x5410);
+                        const uint32_t w0 = wd[t - 1][0], w1 = wd[t - 1][1];
                         if (t <= TD_DIG)
                             tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2), w0, w1);
                         else
@@ -737,17 +761,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                         lo[j] = static_cast<uint32_t>(m);
                         hi[j] = static_cast<uint32_t>(m >> 32);
                     }
-#pragma unroll
-                    for (int t = 1; t <= kDig; ++t) {
-                        const int byte = 7 - t;
-                        const uint32_t* src = byte >= 4 ? hi : lo;
-                        const uint32_t b = static_cast<uint32_t>(byte & 3);
-                        const uint32_t sel = b | ((b + 4) << 4);
-                        wd[t - 1][0] = __byte_perm(__byte_perm(src[0], src[1], sel),
-                                                   __byte_perm(src[2], src[3], sel), 0x5410);
-                        wd[t - 1][1] = __byte_perm(__byte_perm(src[4], src[5], sel),
-                                                   __byte_perm(src[6], src[7], sel), 0x5410);
-                    }
+                    pack_digits(lo, hi, wd);
                 }
                 if (k >= NA) {
                     mbar_wait(&empty_a[sa], pa ^ 1);
