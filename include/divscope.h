@@ -145,6 +145,10 @@ double divscope_matrix_get(const divscope_matrix* m, size_t i, size_t j);
 divscope_status divscope_matrix_copy_to_host(const divscope_matrix* m, double* out);
 /* ref divscope.h:118-121 (DVS1 container, ref src/distmat.hpp:42-44) */
 divscope_status divscope_matrix_write(const divscope_matrix* m, const char* dvs_path);
+/* ref divscope.h:122-128: tab-separated export with an id header row; ids
+ * from the given readsets (NULL -> 0-based index ids); a gram handle writes G */
+divscope_status divscope_matrix_write_tsv(const divscope_matrix* m, const divscope_readset* row_ids,
+                                          const divscope_readset* col_ids, const char* tsv_path);
 divscope_status divscope_matrix_read(const char* dvs_path, divscope_matrix** out);
 
 /* NEW. Rows [row_begin, row_end) of a symmetric DVS1 file as a row-shard

@@ -248,4 +248,16 @@ int ref_pairwise_cross(const char* qc, const std::size_t* qo, std::size_t m, con
     });
 }
 
+
+// src/distmat.cpp:224-244 (index ids)
+int ref_write_matrix_tsv(const char* path, const double* v, std::size_t rows, std::size_t cols,
+                         int sym) {
+    return guarded([&] {
+        std::vector<std::string> r, c;
+        for (std::size_t i = 0; i < rows; ++i) r.push_back(std::to_string(i));
+        for (std::size_t j = 0; j < cols; ++j) c.push_back(std::to_string(j));
+        write_matrix_tsv(make_matrix(v, rows, cols, sym), r, c, path);
+    });
+}
+
 }  // extern "C"

@@ -121,6 +121,7 @@ def _load() -> C.CDLL:
         "divscope_matrix_write": ([_vp, C.c_char_p], _st),
         "divscope_matrix_read": ([C.c_char_p, C.POINTER(_vp)], _st),
         "divscope_matrix_read_rows": ([C.c_char_p, _sz, _sz, C.POINTER(_vp)], _st),
+        "divscope_matrix_write_tsv": ([_vp, _vp, _vp, C.c_char_p], _st),
         "divscope_reconstruction_error": ([_vp, _vp, C.c_uint, _dp], _st),
         "divscope_matrix_free": ([_vp], None),
         "divscope_dvs_read_host": ([C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int),
@@ -241,6 +242,23 @@ class Matrix:
 
     def write(self, path) -> None:
         _check(lib.divscope_matrix_write(self._h, str(path).encode()))
+
+    def write_tsv(self, path, row_ids=None, col_ids=None) -> None:
+        """ref divscope_matrix_write_tsv (ids default to 0-based indices)."""
+        def rs(ids):
+            if ids is None:
+                return None, None
+            arr = (C.c_char_p * len(ids))(*[str(i).encode() for i in ids])
+            h = _vp()
+            _check(lib.divscope_readset_from_ids(arr, len(ids), C.byref(h)))
+            return h, arr
+        (rh, ra), (ch, ca) = rs(row_ids), rs(col_ids)
+        try:
+            _check(lib.divscope_matrix_write_tsv(self._h, rh, ch, str(path).encode()))
+        finally:
+            for h in (rh, ch):
+                if h is not None and h.value:
+                    lib.divscope_readset_free(h)
 
 
 def _new_matrix(fn, *args) -> Matrix:

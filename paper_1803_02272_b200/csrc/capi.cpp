@@ -300,6 +300,39 @@ divscope_status divscope_matrix_write(const divscope_matrix* m, const char* dvs_
     });
 }
 
+divscope_status divscope_matrix_write_tsv(const divscope_matrix* m, const divscope_readset* row_ids,
+                                          const divscope_readset* col_ids,
+                                          const char* tsv_path) {  // ref capi.cpp:270-282
+    if (!m || !tsv_path) return fail_invalid("null argument");
+    return wrap([&] {
+        const dsb::Store& s = *m->m.store;
+        const std::vector<std::string> rows = row_ids ? row_ids->ids : index_ids(s.rows);
+        const std::vector<std::string> cols = col_ids ? col_ids->ids : index_ids(s.cols);
+        // ref distmat.cpp:224-244
+        if (rows.size() != s.rows || cols.size() != s.cols)
+            throw Error(errc::shape_mismatch, "id lists do not match matrix shape");
+        std::vector<double> host(s.rows * s.cols);
+        dsb::matrix_to_host(m->m, host.data());
+        std::ofstream out(tsv_path, std::ios::binary);
+        if (!out) throw Error(errc::io_error, std::string("cannot open ") + tsv_path + " for writing");
+        std::string line = "id";
+        for (const std::string& id : cols) line += '\t' + id;
+        line += '\n';
+        out << line;
+        for (size_t i = 0; i < s.rows; ++i) {
+            line = rows[i];
+            for (size_t j = 0; j < s.cols; ++j) {
+                line += '\t';
+                line += dsb::format_double(host[i * s.cols + j]);
+            }
+            line += '\n';
+            out << line;
+        }
+        out.flush();
+        if (!out) throw Error(errc::io_error, std::string("write failed for ") + tsv_path);
+    });
+}
+
 divscope_status divscope_matrix_read(const char* dvs_path, divscope_matrix** out) {
     if (!dvs_path || !out) return fail_invalid("null argument");
     return wrap([&] {

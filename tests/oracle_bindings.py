@@ -197,6 +197,7 @@ class RefLib:
         L.ref_eigs_sym.argtypes = [_dp, _sz, _sz, _sz, _sz, _u64, C.c_uint, _dp, _dp,
                                    C.POINTER(_sz), _dp]
         L.ref_stable_rank.argtypes = [_dp, _sz, C.c_uint, _dp]
+        L.ref_write_matrix_tsv.argtypes = [C.c_char_p, _dp, _sz, _sz, C.c_int]
         L.ref_sw_align.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(C.c_longlong)]
         L.ref_sw_distance.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int,
@@ -265,6 +266,11 @@ class RefLib:
                                    _ptr(vecs), C.byref(keep), C.byref(resid))
         k = keep.value
         return st, vals[:k].copy(), vecs[: n * k].reshape(n, k).copy(), resid.value
+
+    def write_matrix_tsv(self, path, v, sym=True):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        return self.lib.ref_write_matrix_tsv(str(path).encode(), _ptr(v), v.shape[0], v.shape[1],
+                                             int(sym))
 
     def sw_align(self, a: bytes, b: bytes, scheme=(1, -1, -2)):
         out = (C.c_longlong * 6)()

@@ -516,3 +516,21 @@ def test_int8_product_admission_and_f32(ds, oracle, product_path):
     # w > 64 -> fp64
     ds.embed(ds.gram(ds.matrix_from_host(d)), rank=60, oversampling=10, seed=2)
     assert ds.stats_get().last_product_kernel == 0
+
+
+def test_matrix_write_tsv_byte_identical(ds, oracle, ref, tmp_path):
+    # ref src/distmat.cpp:224-244 through capi.cpp:270-282: index ids, the
+    # shortest round-trip number format (textio.hpp:11-16)
+    d = oracle.euclidean_matrix(ds.synth_points(1, 37, 3))
+    ds.matrix_from_host(d).write_tsv(tmp_path / "ours.tsv")
+    assert ref.write_matrix_tsv(tmp_path / "ref.tsv", d) == 0
+    assert (tmp_path / "ours.tsv").read_bytes() == (tmp_path / "ref.tsv").read_bytes()
+    # a gram handle writes G (as matrix_get / _write do)
+    g = ds.gram(ds.matrix_from_host(d))
+    g.write_tsv(tmp_path / "g.tsv", row_ids=[f"r{i}" for i in range(37)])
+    lines = (tmp_path / "g.tsv").read_text().splitlines()
+    assert lines[0].split("\t")[:3] == ["id", "0", "1"] and lines[1].startswith("r0\t")
+    st, gref = oracle.gram(d)
+    vals = np.array([[float(x) for x in ln.split("\t")[1:]] for ln in lines[1:]])
+    assert np.max(np.abs(vals - gref)) <= 1e-13 * np.max(np.abs(gref))
+    assert err(ds, g.write_tsv, tmp_path / "x.tsv", row_ids=["a"]) == ds.Status.ERR_SHAPE_MISMATCH
