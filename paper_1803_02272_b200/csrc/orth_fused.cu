@@ -289,16 +289,36 @@ __global__ void __launch_bounds__(256, 1)
     }
     if (cstat) {
         // the next product pass's column statistics of this CTA's rows:
-        // 1^T Q, r^T Q (centering) and max |Q| (int8 column exponents),
-        // rows in order; reduced over the CTAs by launch_colstats_final
+        // 1^T Q, r^T Q (centering) and max |Q| (int8 column exponents).
+        // Thread (slice, column): rows slice, slice + S, ...; the S slice
+        // partials are combined in slice order (fixed) in shared memory
+        // (reusing the Gram scratch R, free after the last pass).
+        // S slices per column, bounded by the threads and by the 2 WP^2
+        // doubles of R and E that hold the [3][S][WP] partials
+        constexpr int S = (256 / WP < (2 * WP) / 3) ? 256 / WP : (2 * WP) / 3;
         const size_t i0 = q0 * 4;
-        for (int cc = threadIdx.x; cc < WP; cc += blockDim.x) {
+        double* red = R;
+        const int cc = threadIdx.x % WP, sl = threadIdx.x / WP;
+        static_assert(3 * S * WP <= 2 * WP * WP && S >= 1, "partials fit in R and E");
+        if (sl < S) {
             double sv = 0.0, tv = 0.0, mv = 0.0;
-            for (int r = 0; r < nrow; ++r) {
+            for (int r = sl; r < nrow; r += S) {
                 const double v = ps[cc * ldr + r];
                 sv += v;
                 if (row_mean && i0 + r < static_cast<size_t>(nrows)) tv += row_mean[i0 + r] * v;
                 mv = fmax(mv, fabs(v));
+            }
+            red[(0 * S + sl) * WP + cc] = sv;
+            red[(1 * S + sl) * WP + cc] = tv;
+            red[(2 * S + sl) * WP + cc] = mv;
+        }
+        __syncthreads();
+        if (threadIdx.x < WP) {
+            double sv = 0.0, tv = 0.0, mv = 0.0;
+            for (int k = 0; k < S; ++k) {
+                sv += red[(0 * S + k) * WP + cc];
+                tv += red[(1 * S + k) * WP + cc];
+                mv = fmax(mv, red[(2 * S + k) * WP + cc]);
             }
             double* o = cstat + static_cast<size_t>(c) * 3 * WP;
             o[cc] = sv;
