@@ -14,23 +14,23 @@
 //   (S X)_ic = 2^(e_i+f_c) sum_{d=2..8} 2^-8d acc_d,  acc_d = sum_j sum_{t+u=d} a_t b_u
 // The terms with t+u >= 9 (weight <= 2^-72) are dropped; each acc_d is an
 // exact int32 sum over at most 8192 columns (7 * 255 * 128 * 8192 < 2^31),
-// after which it is flushed to fp64. Digits of S are produced on the fly in
-// shared memory from the fp64 (or fp32) D tile, so HBM traffic is exactly
-// one read of D per pass, as in the fp64 kernel.
+// after which it is flushed to fp64. Digits of S are produced on the fly from
+// the fp64 (or fp32) D tile, so HBM traffic is exactly one read of D per
+// pass, as in the fp64 kernel.
 //
 // MMA structure (one CTA per SM, persistent, stream-K over (128-row block x
 // 32-column k-step) like the fp64 kernel): for each A digit t one
 // tcgen05.mma (M=128, K=32) against the CONCATENATION of B digits
 // 1..8-t (N' = (8-t) NB <= 256, else split), writing TMEM columns
 // (t-1) NB.. — so digit pair (t, u) lands on the accumulator of its
-// diagonal d = t+u. 7 MMAs per k-step, 28 digit products.
+// diagonal d = t+u: 28 digit products per k-step.
 //
 // Warp roles: warp 0 TMA producer of D tiles (128 rows x 128 B boxes,
-// SWIZZLE_128B); warp 1 TMEM owner + single-thread MMA issuer; warps 2-17
-// converters (8 tile rows each) (d -> d^2 -> 56-bit fixed point -> 7 byte planes written in the
-// UMMA K-major interleaved layout; converter 0 also bulk-copies the k-step's
-// B digits), converters 0-3 double as the epilogue (tcgen05.ld of the 7
-// diagonals, fp64 combine, exact 2^(e+f) scaling, partial slot RMW).
+// SWIZZLE_128B) (and, with a single A stage, of the panel digits); warp 1
+// TMEM owner + single-thread MMA issuer; warps 2-17 converters (d -> d^2 ->
+// 56-bit fixed point -> byte planes, written into TMEM with tcgen05.st, see
+// k2i_product_ts below), converters 0-3 double as the epilogue (tcgen05.ld
+// of the 7 diagonals, fp64 combine, exact 2^(e+f) scaling, partial slot RMW).
 // k2_reduce sums the partial slots in CTA order and applies the centering.
 #include <cudaTypedefs.h>
 
@@ -54,7 +54,6 @@ constexpr int kChunk = 256;    // k-steps per int32 accumulation chunk (8192 col
 constexpr int kConv = 16;      // converter warps (8 rows each)
 constexpr int kThreadsI8 = (2 + kConv) * 32;
 constexpr int kExpZeroI8 = -1100;  // matches K1's exponent of an all-zero row
-constexpr int kABytes = kDig * kRowsI8 * kKStep;  // 28 KB of A digit tiles per k-step
 
 template <int NB>
 constexpr int b_bytes() {
@@ -64,32 +63,6 @@ template <typename TD>
 constexpr int d_bytes() {
     return kRowsI8 * kKStep * static_cast<int>(sizeof(TD));
 }
-template <int NB>
-constexpr int g_bytes() {
-    return (kABytes + b_bytes<NB>() + 1023) / 1024 * 1024;
-}
-#ifndef DSB_I8_DSTAGES
-#define DSB_I8_DSTAGES 2
-#endif
-template <typename TD>
-constexpr int d_stages_req() {
-    return DSB_I8_DSTAGES * (sizeof(TD) == 8 ? 1 : 2);
-}
-template <int NB, typename TD>
-constexpr int g_stages() {
-    // digit stages fill the shared memory left after the D ring
-    return std::min(6, (212 * 1024 - d_stages_req<TD>() * d_bytes<TD>()) / g_bytes<NB>());
-}
-template <int NB, typename TD>
-constexpr int d_stages() {
-    return d_stages_req<TD>();
-}
-template <int NB, typename TD>
-constexpr size_t i8_smem() {
-    return 1024 + static_cast<size_t>(d_stages<NB, TD>()) * d_bytes<TD>() +
-           g_stages<NB, TD>() * g_bytes<NB>() + 256 + NB * 8;
-}
-
 // Walks a CTA's stream-K range [t0, t1) of (row block, k-step) items without
 // divisions: row block, k-step, segment index and position in the int32
 // accumulation chunk (chunks restart at every row block).
@@ -118,278 +91,6 @@ struct Walk {
         }
     }
 };
-
-// 4 consecutive d values of row `row`, columns k0..k0+3 of the k-step tile
-template <typename TD>
-__device__ __forceinline__ void load4(const unsigned char* tile, int row, int k0, double (&d)[4]) {
-    if constexpr (sizeof(TD) == 8) {
-        // two 128-byte boxes (16 columns each), 16-byte chunk c at (c ^ row%8)
-        const unsigned char* box = tile + (k0 >> 4) * (kRowsI8 * 128) + row * 128;
-        const int c = (k0 & 15) >> 1;
-        const double2 v0 = *reinterpret_cast<const double2*>(box + (((c) ^ (row & 7)) << 4));
-        const double2 v1 = *reinterpret_cast<const double2*>(box + (((c + 1) ^ (row & 7)) << 4));
-        d[0] = v0.x;
-        d[1] = v0.y;
-        d[2] = v1.x;
-        d[3] = v1.y;
-    } else {
-        const unsigned char* rp = tile + row * 128;
-        const float4 v = *reinterpret_cast<const float4*>(rp + (((k0 >> 2) ^ (row & 7)) << 4));
-        d[0] = v.x;
-        d[1] = v.y;
-        d[2] = v.z;
-        d[3] = v.w;
-    }
-}
-
-// m = floor(s 2^(56 - e)) for 0 <= s < 2^e, as (hi, lo) 32-bit words, on
-// the FP64 pipe only (the integer conversion F2I.U64.F64 issues on the
-// narrow XU pipe and was the converter bottleneck). With C = 1.5 2^52, the
-// low word of the bits of C + v is v for an integer 0 <= v < 2^32:
-//   x  = s 2^(56-e)                      (exact power-of-two scaling)
-//   yh = C + floor(x 2^-32)              (fma, round toward -inf)  -> hi
-//   l  = x - floor(x 2^-32) 2^32 in [0, 2^32)   (exact fma)
-//   yl = C + floor(l)                    (add, round toward -inf)  -> lo
-__device__ __forceinline__ void fixed56(double s, double sc, uint32_t& lo, uint32_t& hi) {
-    constexpr double kC = 6755399441055744.0;  // 1.5 * 2^52
-    const double x = s * sc;
-    const double yh = __fma_rd(x, 0x1p-32, kC);
-    const double hf = yh - kC;
-    const double l = fma(-hf, 0x1p32, x);
-    const double yl = __dadd_rd(l, kC);
-    hi = static_cast<uint32_t>(__double_as_longlong(yh));
-    lo = static_cast<uint32_t>(__double_as_longlong(yl));
-}
-
-template <int NB, typename TD>
-__global__ void __launch_bounds__(kThreadsI8, 1)
-    k2i_product(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
-                const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
-                int nks, int total, double* __restrict__ part, int maxseg, int wp,
-                const int* __restrict__ skip, int dbg) {
-    if (skip && *skip) return;
-    constexpr int ND = d_stages<NB, TD>();
-    constexpr int NG = g_stages<NB, TD>();
-    constexpr int DB = d_bytes<TD>();
-    constexpr int GB = g_bytes<NB>();
-    constexpr int BB = b_bytes<NB>();
-    constexpr uint32_t NCOL = (kDig * NB <= 256) ? 256u : 512u;
-
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    unsigned char* dring = sm;
-    unsigned char* gring = sm + ND * DB;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gring + NG * GB);
-    uint64_t* full_d = bars;
-    uint64_t* empty_d = full_d + ND;
-    uint64_t* full_g = empty_d + ND;
-    uint64_t* empty_g = full_g + NG;
-    uint64_t* acc_full = empty_g + NG;
-    uint64_t* acc_empty = acc_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-    double* colscale = reinterpret_cast<double*>(bars + 32);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cta = blockIdx.x;
-    const int t0 = static_cast<int>(static_cast<long long>(total) * cta / gridDim.x);
-    const int t1 = static_cast<int>(static_cast<long long>(total) * (cta + 1) / gridDim.x);
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < ND; ++s) {
-            mbar_init(&full_d[s], 1);
-            mbar_init(&empty_d[s], kConv);
-        }
-        for (int s = 0; s < NG; ++s) {
-            mbar_init(&full_g[s], kConv + 1);
-            mbar_init(&empty_g[s], 1);
-        }
-        mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 4);
-        fence_mbar_init();
-    }
-    for (int c = threadIdx.x; c < NB; c += blockDim.x) {
-        const int f = col_exp[c];
-        colscale[c] = (c < wp && f > kExpZeroI8) ? ldexp(1.0, f) : 0.0;
-    }
-    if (warp == 1) tmem_alloc(tmem_slot, NCOL);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        // ---------------- TMA producer ----------------
-        if (lane == 0) {
-            prefetch_tmap(&tmD);
-            int s = 0, k = 0;
-            uint32_t ph = 0;
-            for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
-                if (k >= ND) mbar_wait(&empty_d[s], ph ^ 1);
-                unsigned char* dst = dring + s * DB;
-                mbar_arrive_expect_tx(&full_d[s], DB);
-                if constexpr (sizeof(TD) == 8) {
-                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[s]);
-                    tma_load_2d(dst + kRowsI8 * 128, &tmD, w.ks * kKStep + 16, w.rb * kRowsI8,
-                                &full_d[s]);
-                } else {
-                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[s]);
-                }
-                if (++s == ND) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            int s = 0, nflush = 0;
-            uint32_t ph = 0;
-            bool started = false;
-            for (Walk w(t0, t1, nks); w.more(); w.next()) {
-                mbar_wait(&full_g[s], ph);
-                tc_fence_after();
-                const bool first = w.first();
-                if (first && started) {
-                    mbar_wait(acc_empty, static_cast<uint32_t>((nflush - 1) & 1));
-                    tc_fence_after();
-                }
-                started = true;
-                const unsigned char* g = gring + s * GB;
-                const uint32_t abase = smem_u32(g), bbase = smem_u32(g + kABytes);
-#pragma unroll
-                for (int t = 1; t <= (dbg == 2 ? 0 : kDig); ++t) {
-                    const uint64_t ad = umma_desc_k_interleave(abase + (t - 1) * (kRowsI8 * kKStep));
-                    constexpr int per = 256 / NB;
-                    const int umax = 8 - t;
-#pragma unroll
-                    for (int u0 = 1; u0 <= umax; u0 += per) {
-                        const int nu = (umax - u0 + 1 < per) ? (umax - u0 + 1) : per;
-                        const uint64_t bd = umma_desc_k_interleave(bbase + (u0 - 1) * (NB * kKStep));
-                        umma_i8(tmem + static_cast<uint32_t>((t + u0 - 2) * NB), ad, bd,
-                                umma_idesc_i8(nu * NB, false, true), (first && t == 1) ? 0 : 1);
-                    }
-                }
-                umma_commit(&empty_g[s]);
-                if (w.last()) {
-                    umma_commit(acc_full);
-                    ++nflush;
-                }
-                if (++s == NG) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-        }
-        __syncwarp();
-    } else {
-        // ---------------- converters (+ epilogue on 0..3) ----------------
-        const int cw = warp - 2;
-        const int row = cw * 8 + (lane >> 2);  // tile row converted by this lane
-        const int kq = lane & 3;
-        int cur_rb = -1;
-        double sc = 0.0;
-        int sd = 0, sg = 0, k = 0, nflush = 0;
-        uint32_t pd = 0, pg = 0;
-        for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
-            if (w.rb != cur_rb) {
-                cur_rb = w.rb;
-                const int grow = w.rb * kRowsI8 + row;
-                const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
-                sc = e > kExpZeroI8 ? ldexp(1.0, 56 - e) : 0.0;
-            }
-            mbar_wait(&full_d[sd], pd);
-            if (k >= NG) mbar_wait(&empty_g[sg], pg ^ 1);
-            unsigned char* g = gring + sg * GB;
-            if (cw == 0 && lane == 0) {
-                mbar_arrive_expect_tx(&full_g[sg], BB);
-                bulk_load(g + kABytes, bdig + static_cast<size_t>(w.ks) * BB, BB, &full_g[sg]);
-            }
-            const unsigned char* tile = dring + sd * DB;
-#pragma unroll
-            for (int h = 0; h < (dbg == 1 ? 0 : 2); ++h) {
-                const int k0 = h * 16 + kq * 4;
-                double d[4];
-                load4<TD>(tile, row, k0, d);
-                uint32_t lo[4], hi[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) fixed56(d[j] * d[j], sc, lo[j], hi[j]);
-                const uint32_t off = umma_tile_off(row, k0);
-                // digit t = byte (7 - t) of the 56-bit value
-#pragma unroll
-                for (int t = 1; t <= kDig; ++t) {
-                    const int byte = 7 - t;
-                    const uint32_t* src = byte >= 4 ? hi : lo;
-                    const uint32_t b = static_cast<uint32_t>(byte & 3);
-                    const uint32_t sel = b | ((b + 4) << 4);
-                    const uint32_t p01 = __byte_perm(src[0], src[1], sel);
-                    const uint32_t p23 = __byte_perm(src[2], src[3], sel);
-                    *reinterpret_cast<uint32_t*>(g + (t - 1) * (kRowsI8 * kKStep) + off) =
-                        __byte_perm(p01, p23, 0x5410);
-                }
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&empty_d[sd]);
-                mbar_arrive(&full_g[sg]);
-            }
-            if (++sd == ND) {
-                sd = 0;
-                pd ^= 1;
-            }
-            if (++sg == NG) {
-                sg = 0;
-                pg ^= 1;
-            }
-            if (cw < 4 && w.last()) {
-                // ---- epilogue: this warp's 32 TMEM lanes ----
-                const int q = warp & 3;
-                mbar_wait(acc_full, static_cast<uint32_t>(nflush & 1));
-                tc_fence_after();
-                const int rloc = q * 32 + lane;
-                const int grow = w.rb * kRowsI8 + rloc;
-                const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
-                const double rscale = e > kExpZeroI8 ? ldexp(1.0, e) : 0.0;
-                double* prow = part +
-                               (static_cast<size_t>(cta) * maxseg + w.seg) * kRowsI8 * wp +
-                               static_cast<size_t>(rloc) * wp;
-#pragma unroll
-                for (int cb = 0; cb < NB / 16; ++cb) {
-                    double v[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = 0.0;
-#pragma unroll
-                    for (int dd = 2; dd <= 8; ++dd) {
-                        int32_t iv[16];
-                        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) +
-                                      static_cast<uint32_t>((dd - 2) * NB + cb * 16),
-                                  iv);
-                        tmem_ld_wait();
-                        const double wgt = ldexp(1.0, -8 * dd);
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(iv[j]) * wgt;
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int col = cb * 16 + j;
-                        if (col < wp) {
-                            const double val = v[j] * rscale * colscale[col];
-                            prow[col] = w.seg_first ? val : prow[col] + val;
-                        }
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(acc_empty);
-                ++nflush;
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, NCOL);
-}
 
 // ---- A digits in tensor memory ---------------------------------------------
 // An MMA whose A operand comes from shared memory costs at least ~128 cycles
@@ -880,15 +581,6 @@ __global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__
     }
 }
 
-// DSB_K2I_SS=1: the shared-memory-A kernel instead of the TMEM-A one
-bool k2i_force_ss() {
-    static const bool f = [] {
-        const char* e = std::getenv("DSB_K2I_SS");
-        return e && std::atoi(e) == 1;
-    }();
-    return f;
-}
-
 // DSB_K2I_DEBUG: 1 = skip the digit conversion, 2 = skip the MMAs (timing
 // experiments only; results are wrong)
 int k2i_debug_mode() {
@@ -903,28 +595,15 @@ template <int NB, typename TD>
 void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
             const int* row_exp, const int* col_exp, double* part, cudaStream_t st,
             const int* skip) {
-    if (!k2i_force_ss()) {
-        static bool attr_ts = false;
-        if (!attr_ts) {
-            cudaFuncSetAttribute(k2i_product_ts<NB, TD>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(ts_smem<NB, TD>()));
-            attr_ts = true;
-        }
-        k2i_product_ts<NB, TD><<<p.grid, kThreadsI8, ts_smem<NB, TD>(), st>>>(
-            *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
-            p.maxseg, wp, skip, k2i_debug_mode());
-        return;
-    }
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k2i_product<NB, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(i8_smem<NB, TD>()));
+        cudaFuncSetAttribute(k2i_product_ts<NB, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(ts_smem<NB, TD>()));
         attr = true;
     }
-    k2i_product<NB, TD><<<p.grid, kThreadsI8, i8_smem<NB, TD>(), st>>>(
-        *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part, p.maxseg,
-        wp, skip, k2i_debug_mode());
+    k2i_product_ts<NB, TD><<<p.grid, kThreadsI8, ts_smem<NB, TD>(), st>>>(
+        *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
+        p.maxseg, wp, skip, k2i_debug_mode());
 }
 
 }  // namespace
