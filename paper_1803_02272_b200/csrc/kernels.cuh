@@ -123,8 +123,9 @@ struct SwPlan {
     long long threads = 0;   // persistent threads (each owns scratch columns)
     size_t dirs_elems = 0;   // u16 traceback codes
     size_t hb_elems = 0;     // int boundary columns
+    bool forward_only = false;  // k_sw_e: events carried forward, no traceback codes
 };
-SwPlan sw_plan(int max_len, int sms);
+SwPlan sw_plan(int max_len, int sms, int mode, int match, int mismatch, int gap);
 // mode 0: pairs i < j of n_a reads (D symmetric, both halves written);
 // 1: n_a queries x n_b refs; 2: one pair (reads 0, 1) as given -> aux[6]
 void launch_sw(const unsigned char* seq, const long long* off, const int* len, int mode,

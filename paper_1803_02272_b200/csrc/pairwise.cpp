@@ -58,7 +58,7 @@ Packed pack(const std::vector<const std::string*>& seqs) {
 void run(const Packed& p, int mode, long long na, long long nb, long long npairs,
          const SwScheme& s, double* dout, size_t ld, long long* aux) {
     Ctx& c = Ctx::get();
-    const SwPlan plan = sw_plan(p.max_len, c.sms);
+    const SwPlan plan = sw_plan(p.max_len, c.sms, mode, s.match, s.mismatch, s.gap);
     auto* dirs = static_cast<unsigned short*>(c.scratch("sw_dirs", plan.dirs_elems * 2));
     int* hb = static_cast<int*>(c.scratch("sw_hb", plan.hb_elems * 4));
     launch_sw(p.bytes->as<unsigned char>(), p.off->as<long long>(), p.len->as<int>(), mode, na, nb,

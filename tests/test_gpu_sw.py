@@ -85,3 +85,19 @@ def test_sw_errors(ds):
     assert (r.score, r.distance, r.a_begin, r.a_end) == (0, 0, 0, 0)
     # 'N' never matches, itself included
     assert ds.align(b"NNNN", b"NNNN").score == 0
+
+
+@pytest.mark.parametrize("scheme", [(81, -90, -60),     # forward-only kernel, |H| near 2^15
+                                    (100, -150, -120),  # scores past 2^15: traceback kernel
+                                    (1, -1, -1)])
+def test_both_sw_kernels_vs_reference(ds, ref, scheme):
+    # sw_plan picks k_sw_e (events carried forward) while every key fits
+    # 32 bits and k_sw (stored traceback codes) otherwise; both bit-exact
+    reads = ds.synth_reads(40, 400, 3, 0.08, 11)
+    seqs = [bytes(r) if k % 3 else bytes(r[: 150 + 5 * k]) for k, r in enumerate(reads)]
+    st, want = ref.pairwise_self(seqs, scheme)
+    assert st == 0
+    assert np.array_equal(ds.pairwise_self(seqs, ds.Scoring(*scheme)).to_numpy(), want)
+    st, wx = ref.pairwise_cross(seqs[:9], seqs[9:], scheme)
+    assert st == 0
+    assert np.array_equal(ds.pairwise_cross(seqs[:9], seqs[9:], ds.Scoring(*scheme)).to_numpy(), wx)
