@@ -113,6 +113,18 @@ struct Walk {
 #endif
 
 constexpr int kBStagesTs = 4;
+#ifndef DSB_K2I_WARP_ISSUE
+#define DSB_K2I_WARP_ISSUE 1
+#endif
+constexpr bool kWarpIssue = DSB_K2I_WARP_ISSUE != 0;
+// panel digits get their own producer-filled ring when the A ring is this
+// shallow or shallower: riding on a 2-deep A stage, the 14 KB digit load is
+// issued only one MMA group ahead and its L2 latency stalls the MMA thread
+#ifndef DSB_TS_BPROD_NA
+#define DSB_TS_BPROD_NA 2
+#endif
+template <int NB>
+constexpr bool bprod_ts();
 
 
 #ifndef DSB_TS_NB64_HYBRID
@@ -149,7 +161,11 @@ constexpr int a_smem_stage_ts() {  // bytes of shared-memory A digits per stage
 }
 template <int NB>
 constexpr int b_stages_ts() {
-    return a_stages_ts<NB>() == 1 ? kBStagesTs : a_stages_ts<NB>();
+    return bprod_ts<NB>() ? kBStagesTs : a_stages_ts<NB>();
+}
+template <int NB>
+constexpr bool bprod_ts() {
+    return a_stages_ts<NB>() <= DSB_TS_BPROD_NA;
 }
 template <int NB, typename TD>
 constexpr int d_stages_ts() {
@@ -231,7 +247,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     // panel digits: with several A stages they ride with the A stage (loaded
     // by one converter lane when it claims the stage); with a single A stage
     // they get their own ring filled ahead by the producer
-    constexpr bool kBProd = (NA == 1);
+    constexpr bool kBProd = bprod_ts<NB>();
     constexpr int NBR = kBProd ? kBStagesTs : NA;
     constexpr int DB = d_bytes<TD>();
     constexpr int BB = b_bytes<NB>();
@@ -277,6 +293,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             mbar_init(&empty_b[s], 1);
         }
         static_assert(kBProd || NBR == NA, "B ring rides with the A ring");
+        static_assert(kBProd || NA > 1, "a single A stage needs the producer's B ring");
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 4);
         fence_mbar_init();
@@ -327,7 +344,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0) {
+        // the whole warp runs the issuer loop (warp-uniform operands, one
+        // elected lane issues); DSB_K2I_WARP_ISSUE=0 restores the lane-0 loop
+        if (kWarpIssue || lane == 0) {
             int sa = 0, sb = 0, nflush = 0;
             uint32_t pa = 0, pb = 0;
             bool started = false;
@@ -357,21 +376,35 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                             const uint32_t dcol = tmem + static_cast<uint32_t>((t + u0 - 2) * NB);
                             const uint32_t idesc = umma_idesc_i8(nu * NB, false, true);
                             const int acc = (first && t == 1) ? 0 : 1;
-                            if (t <= TD_DIG)
-                                umma_i8_ts(dcol, ta + static_cast<uint32_t>((t - 1) * 8), bd,
-                                           idesc, acc);
-                            else
-                                umma_i8(dcol,
-                                        umma_desc_k_interleave(
-                                            asm_base + (t - TD_DIG - 1) * (kRowsI8 * kKStep)),
-                                        bd, idesc, acc);
+                            if (t <= TD_DIG) {
+                                const uint32_t ta_t = ta + static_cast<uint32_t>((t - 1) * 8);
+                                if constexpr (kWarpIssue)
+                                    umma_i8_ts_w(dcol, ta_t, bd, idesc, acc);
+                                else
+                                    umma_i8_ts(dcol, ta_t, bd, idesc, acc);
+                            } else {
+                                const uint64_t ad = umma_desc_k_interleave(
+                                    asm_base + (t - TD_DIG - 1) * (kRowsI8 * kKStep));
+                                if constexpr (kWarpIssue)
+                                    umma_i8_w(dcol, ad, bd, idesc, acc);
+                                else
+                                    umma_i8(dcol, ad, bd, idesc, acc);
+                            }
                         }
                     }
                 }
-                umma_commit(&empty_a[sa]);
-                if constexpr (kBProd) umma_commit(&empty_b[sb]);
+                if constexpr (kWarpIssue) {
+                    umma_commit_w(&empty_a[sa]);
+                    if constexpr (kBProd) umma_commit_w(&empty_b[sb]);
+                } else {
+                    umma_commit(&empty_a[sa]);
+                    if constexpr (kBProd) umma_commit(&empty_b[sb]);
+                }
                 if (w.last()) {
-                    umma_commit(acc_full);
+                    if constexpr (kWarpIssue)
+                        umma_commit_w(acc_full);
+                    else
+                        umma_commit(acc_full);
                     ++nflush;
                 }
                 if (++sa == NA) {
@@ -404,14 +437,15 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 sc = e > kExpZeroI8 ? ldexp(1.0, 56 - e) : 0.0;
             }
             mbar_wait(&full_d[sd], pd);
-            if constexpr (!kBProd) {
+            if constexpr (NA > 1) {
                 // several A stages: claim the stage (and load its panel
-                // digits) first, then convert and store digit by digit
+                // digits, unless the producer streams them) first, then
+                // convert and store digit by digit
                 if (k >= NA) {
                     mbar_wait(&empty_a[sa], pa ^ 1);
                     tc_fence_after();
                 }
-                if (warp == 2 && lane == 0) {
+                if (!kBProd && warp == 2 && lane == 0) {
                     mbar_arrive_expect_tx(&full_a[sa], BB);
                     bulk_load(bring + sa * BB, bdig + static_cast<size_t>(w.ks) * BB, BB,
                               &full_a[sa]);

@@ -51,6 +51,34 @@ __global__ void k_rate(int iters, int pattern, int nb, unsigned long long* cycle
                                     umma_idesc_i8(nu * nb, false, true), 1);
                     }
                 }
+            } else if (pattern == 5 || pattern == 7) {
+                // NB = 64, all digits in TMEM, N' split at 128 (5) or the
+                // digit loop order reversed, largest-N last (7)
+                for (int tt = 1; tt <= 7; ++tt) {
+                    const int t = pattern == 7 ? 8 - tt : tt;
+                    const int per = (pattern == 5 ? 128 : 256) / nb, umax = 8 - t;
+                    for (int u0 = 1; u0 <= umax; u0 += per) {
+                        const int nu = (umax - u0 + 1 < per) ? (umax - u0 + 1) : per;
+                        const uint64_t bd = umma_desc_k_interleave(smem_u32(sb + (u0 - 1) * nb * 32));
+                        umma_i8_ts(tmem + (t + u0 - 2) * nb, tmem + 448, bd,
+                                   umma_idesc_i8(nu * nb, false, true), 1);
+                    }
+                }
+            } else if (pattern == 6) {
+                // 7 x N = 256 from TMEM (same accumulator region, 1792 columns)
+                for (int t = 0; t < 7; ++t)
+                    umma_i8_ts(tmem + (t & 1) * 192, tmem + 448, umma_desc_k_interleave(smem_u32(sb)),
+                               umma_idesc_i8(256, false, true), 1);
+            } else if (pattern == 8) {
+                // 14 x N = 128 from TMEM (1792 columns)
+                for (int t = 0; t < 14; ++t)
+                    umma_i8_ts(tmem + (t % 3) * 128, tmem + 448, umma_desc_k_interleave(smem_u32(sb)),
+                               umma_idesc_i8(128, false, true), 1);
+            } else if (pattern == 9) {
+                // 28 x N = 64 from TMEM (1792 columns)
+                for (int t = 0; t < 28; ++t)
+                    umma_i8_ts(tmem + (t % 6) * 64, tmem + 448, umma_desc_k_interleave(smem_u32(sb)),
+                               umma_idesc_i8(64, false, true), 1);
             } else if (pattern == 0) {
                 for (int t = 1; t <= 7; ++t) {
                     const int per = 256 / nb, umax = 8 - t;
@@ -95,7 +123,12 @@ int main() {
                         {1, 32, 4 * 224, "4 x N=224"},
                         {2, 32, 28 * 32, "digit pattern NB=32, A in TMEM"},
                         {3, 64, 28 * 64, "NB=64 hybrid (digits 1-4 TMEM, 5-7 smem)"},
-                        {4, 64, 28 * 64, "NB=64 all digits in TMEM"}};
+                        {4, 64, 28 * 64, "NB=64 all digits in TMEM"},
+                        {5, 64, 28 * 64, "NB=64 all TMEM, N split at 128"},
+                        {7, 64, 28 * 64, "NB=64 all TMEM, t reversed"},
+                        {6, 64, 28 * 64, "7 x N=256 TS"},
+                        {8, 64, 28 * 64, "14 x N=128 TS"},
+                        {9, 64, 28 * 64, "28 x N=64 TS"}};
     for (const Cfg& c : cfgs) {
         const int iters = 4000;
         k_rate<<<sms, 128, smem>>>(10, c.pattern, c.nb, dc);
