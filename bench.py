@@ -310,11 +310,15 @@ def b200_arm(args, wl):
                         (st.stats_ms / max(st.stats_launches, 1) * 1e-3) / 1e9}}
     if int8_path:
         # exact integer slice product on the int8 tensor cores: one read of D
-        # per pass, HBM-bound; the f64-equivalent flop rate shown alongside
+        # per column group (w <= 64: one group), HBM-bound; `achieved` counts
+        # the pass's algorithmic bytes (D once), `streamed_gbs` every read
+        groups = max(int(st.last_product_groups), 1)
         roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": gbs / hbm_peak, "traffic": traffic,
                     "kernel": "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)",
                     "peak_source": hbm["peak_source"],
+                    "column_groups": groups,
+                    "streamed_gbs": gbs * groups if groups > 1 else gbs,
                     "fp64_equiv": {"achieved": tflops, "unit": "TFLOP/s",
                                    "fp64_dmma_peak": fp64_peak}, **common}
     else:

@@ -89,6 +89,7 @@ public:
     double k2_ms = 0.0, k1_ms = 0.0;
     int last_evd_sweeps = 0, last_orth_shifted = 0, last_power_iters = 0;
     int last_product_kernel = 0;  // 0 fp64 DMMA, 1 int8 slice product
+    int last_product_groups = 1;  // int8 column groups (reads of D per pass)
     std::vector<TimedPair> pending;
     std::vector<cudaEvent_t> event_pool;
     void begin_timed(int kind, cudaEvent_t* a);

@@ -312,7 +312,9 @@ void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, lo
                                                        row_mean, scalars, colsums, y, skip);   \
         break;
         DSB_RED(8, 128) DSB_RED(16, 128) DSB_RED(24, 128) DSB_RED(32, 128) DSB_RED(40, 128)
-        DSB_RED(48, 128) DSB_RED(56, 128) DSB_RED(64, 128)
+        DSB_RED(48, 128) DSB_RED(56, 128) DSB_RED(64, 128) DSB_RED(72, 128) DSB_RED(80, 128)
+        DSB_RED(88, 128) DSB_RED(96, 128) DSB_RED(104, 128) DSB_RED(112, 128)
+        DSB_RED(120, 128) DSB_RED(128, 128)
 #undef DSB_RED
         default:
             throw std::invalid_argument("unsupported reduce shape");

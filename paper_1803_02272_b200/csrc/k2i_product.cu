@@ -118,10 +118,10 @@ constexpr int kBStagesTs = 4;
 #endif
 constexpr bool kWarpIssue = DSB_K2I_WARP_ISSUE != 0;
 // panel digits get their own producer-filled ring when the A ring is this
-// shallow or shallower: riding on a 2-deep A stage, the 14 KB digit load is
-// issued only one MMA group ahead and its L2 latency stalls the MMA thread
+// shallow or shallower (a single A stage); riding on the 2-deep NB = 64 A
+// ring measured as fast as a separate ring (DSB_TS_BPROD_NA=2)
 #ifndef DSB_TS_BPROD_NA
-#define DSB_TS_BPROD_NA 2
+#define DSB_TS_BPROD_NA 1
 #endif
 template <int NB>
 constexpr bool bprod_ts();
@@ -239,7 +239,7 @@ template <int NB, typename TD>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
                    const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
-                   int nks, int total, double* __restrict__ part, int maxseg, int wp,
+                   int nks, int total, double* __restrict__ part, int maxseg, int wp, int cg0,
                    const int* __restrict__ skip, int dbg) {
     if (skip && *skip) return;
     constexpr int ND = d_stages_ts<NB, TD>();
@@ -298,9 +298,10 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         mbar_init(acc_empty, 4);
         fence_mbar_init();
     }
+    // this launch's column group: panel columns cg0 .. cg0 + NB - 1
     for (int c = threadIdx.x; c < NB; c += blockDim.x) {
-        const int f = col_exp[c];
-        colscale[c] = (c < wp && f > kExpZeroI8) ? ldexp(1.0, f) : 0.0;
+        const int f = cg0 + c < wp ? col_exp[cg0 + c] : kExpZeroI8;
+        colscale[c] = f > kExpZeroI8 ? ldexp(1.0, f) : 0.0;
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
@@ -552,9 +553,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     }
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const int col = cb * 16 + j;
+                        const int col = cg0 + cb * 16 + j;
                         if (col < wp) {
-                            const double val = v[j] * rscale * colscale[col];
+                            const double val = v[j] * rscale * colscale[col - cg0];
                             prow[col] = w.seg_first ? val : prow[col] + val;
                         }
                     }
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 // one thread per (k-step, column, 4 rows): balanced base-256 digits of
 // round(X 2^(56 - f_c)), written as 7 byte planes in the UMMA layout
 __global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__ x, int nks, int wp,
-                                                      int nb, const int* __restrict__ col_exp,
+                                                      int nb, int cg0, const int* __restrict__ col_exp,
                                                       unsigned char* __restrict__ bdig) {
     const long long total = static_cast<long long>(nks) * nb * 8;
     const int bb = kDig * nb * kKStep;
@@ -587,13 +588,14 @@ __global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__
         uint32_t word[kDig];
 #pragma unroll
         for (int u = 0; u < kDig; ++u) word[u] = 0;
-        const int f = col_exp[c];
-        if (c < wp && f > kExpZeroI8) {
+        const int gc = cg0 + c;
+        const int f = gc < wp ? col_exp[gc] : kExpZeroI8;
+        if (f > kExpZeroI8) {
             const double scale = ldexp(1.0, 56 - f);
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
                 const size_t j = static_cast<size_t>(ks) * kKStep + kq * 4 + jj;
-                long long m = __double2ll_rn(x[pidx(j, c, wp)] * scale);
+                long long m = __double2ll_rn(x[pidx(j, gc, wp)] * scale);
                 int dig[kDig];
 #pragma unroll
                 for (int u = kDig - 1; u >= 1; --u) {
@@ -627,7 +629,7 @@ int k2i_debug_mode() {
 
 template <int NB, typename TD>
 void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
-            const int* row_exp, const int* col_exp, double* part, cudaStream_t st,
+            const int* row_exp, const int* col_exp, double* part, int cg0, cudaStream_t st,
             const int* skip) {
     static bool attr = false;
     if (!attr) {
@@ -637,14 +639,25 @@ void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned ch
     }
     k2i_product_ts<NB, TD><<<p.grid, kThreadsI8, ts_smem<NB, TD>(), st>>>(
         *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
-        p.maxseg, wp, skip, k2i_debug_mode());
+        p.maxseg, wp, cg0, skip, k2i_debug_mode());
 }
 
 }  // namespace
 
 K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms) {
     K2iPlan p;
-    p.nb = wp <= 32 ? 32 : 64;
+    // column groups, one full pass over D each: NB = 64 groups while more
+    // than 32 columns remain, then one NB = 32 or 64 group for the rest
+    for (int c0 = 0; c0 < wp && p.ngroups < K2iPlan::kMaxGroups; ++p.ngroups) {
+        const int rest = wp - c0;
+        const int nb = rest <= 32 ? 32 : 64;
+        p.gc0[p.ngroups] = c0;
+        p.gnb[p.ngroups] = nb;
+        p.bdig_bytes = std::max(p.bdig_bytes, static_cast<size_t>((ncols + kKStep - 1) / kKStep) *
+                                                  kDig * nb * kKStep);
+        c0 += nb;
+        p.nb = c0;
+    }
     p.nrows = static_cast<int>(nrows);
     p.nblk = static_cast<int>((nrows + kRowsI8 - 1) / kRowsI8);
     p.nks = static_cast<int>((ncols + kKStep - 1) / kKStep);
@@ -657,12 +670,11 @@ K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms) {
     }
     p.maxseg = maxseg;
     p.part_elems = static_cast<size_t>(p.grid) * maxseg * kRowsI8 * wp;
-    p.bdig_bytes = static_cast<size_t>(p.nks) * kDig * p.nb * kKStep;
     p.colmax_grid = sms;
     return p;
 }
 
-bool k2i_supported(int wp) { return wp >= 8 && wp <= 64; }
+bool k2i_supported(int wp) { return wp >= 8 && wp <= 128; }
 
 void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, const double* x,
                 size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
@@ -678,27 +690,30 @@ void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, 
                                  st));
     (void)x_rows_pad;
     (void)pmax;  // column exponents come from launch_colsums (same pass over X)
-    {
-        const long long items = static_cast<long long>(p.nks) * p.nb * 8;
-        const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
-        k_panel_digits<<<grid, 256, 0, st>>>(x, p.nks, wp, p.nb, col_exp, bdig);
-    }
-    if (e0) cudaEventRecord(e0, st);
-    if (dt == DType::F64) {
-        if (p.nb == 32)
-            run_i8<32, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, st, skip);
-        else
-            run_i8<64, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, st, skip);
-    } else {
-        if (p.nb == 32)
-            run_i8<32, float>(tmap128, p, wp, bdig, row_exp, col_exp, part, st, skip);
-        else
-            run_i8<64, float>(tmap128, p, wp, bdig, row_exp, col_exp, part, st, skip);
+    for (int g = 0; g < p.ngroups; ++g) {
+        const int nb = p.gnb[g], cg0 = p.gc0[g];
+        {
+            const long long items = static_cast<long long>(p.nks) * nb * 8;
+            const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
+            k_panel_digits<<<grid, 256, 0, st>>>(x, p.nks, wp, nb, cg0, col_exp, bdig);
+        }
+        if (g == 0 && e0) cudaEventRecord(e0, st);
+        if (dt == DType::F64) {
+            if (nb == 32)
+                run_i8<32, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
+            else
+                run_i8<64, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
+        } else {
+            if (nb == 32)
+                run_i8<32, float>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
+            else
+                run_i8<64, float>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
+        }
     }
     if (e1) cudaEventRecord(e1, st);
     launch_k2_reduce(wp, kRowsI8, part, p.maxseg, p.nks, p.total, p.grid, p.nrows, 1, row_mean,
                      scalars, colsums, y, st, skip);
-    count_launch(3);
+    count_launch(2 * p.ngroups + 1);
 }
 
 }  // namespace dsb

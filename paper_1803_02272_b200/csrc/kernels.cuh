@@ -90,7 +90,11 @@ void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, lo
 // slice product of D o D and the panel on tcgen05 kind::i8 (lazy grams,
 // WP <= 64). row_exp from K1.
 struct K2iPlan {
-    int nb = 32;            // MMA N per digit (32 or 64 >= WP)
+    static constexpr int kMaxGroups = 4;
+    int nb = 0;             // padded panel width covered by the column groups (>= WP)
+    int ngroups = 0;        // launches per pass (each streams D once)
+    int gc0[kMaxGroups] = {};  // first panel column of each group
+    int gnb[kMaxGroups] = {};  // MMA N per digit of each group (32 or 64)
     int nrows = 0, nblk = 0, nks = 0;
     long long total = 0;
     int grid = 0, maxseg = 0, colmax_grid = 0;
@@ -99,7 +103,7 @@ struct K2iPlan {
 };
 bool k2i_supported(int wp);
 K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms);
-// pmax: colmax_grid * wp doubles; col_exp: nb ints; bdig: bdig_bytes
+// pmax: colmax_grid * wp doubles; col_exp: nb ints (<= 128); bdig: bdig_bytes
 void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, const double* x,
                 size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
                 unsigned char* bdig, double* part, const double* row_mean, const double* scalars,

@@ -338,10 +338,11 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         iplan = k2i_plan(m, n, wp, c.sms);
         pmax = static_cast<double*>(c.scratch(
             "i8_pmax", static_cast<size_t>(panel_grid(n_pad, c.sms)) * wp * sizeof(double)));
-        col_exp = static_cast<int*>(c.scratch("i8_colexp", 64 * sizeof(int)));
+        col_exp = static_cast<int*>(c.scratch("i8_colexp", 128 * sizeof(int)));
         bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
     }
     c.last_product_kernel = use_i8 ? 1 : 0;
+    c.last_product_groups = use_i8 ? iplan.ngroups : 1;
     const size_t pbytes = n_pad * wp * 8;
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
     double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));

@@ -474,7 +474,7 @@ def test_workspace_reuse_large_then_small(ds, oracle):
 
 def test_int8_product_admission_and_f32(ds, oracle, product_path):
     # K2i admission (solver.cpp use_int8_product): finite data with a row
-    # max/mean ratio <= 2^12 and w <= 64; otherwise the fp64 kernel runs
+    # max/mean ratio <= 2^12 and w <= 128; otherwise the fp64 kernel runs
     if product_path != "int8":
         pytest.skip("int8-specific")
     n = 600
@@ -513,9 +513,33 @@ def test_int8_product_admission_and_f32(ds, oracle, product_path):
     assert ds.stats_get().last_product_kernel == 0
     again = ds.embed(ds.gram(ds.matrix_from_host(d)), rank=k, oversampling=p, seed=2)
     np.testing.assert_allclose(again.eigenvalues, e8_d.eigenvalues, rtol=1e-12)
-    # w > 64 -> fp64
-    ds.embed(ds.gram(ds.matrix_from_host(d)), rank=60, oversampling=10, seed=2)
-    assert ds.stats_get().last_product_kernel == 0
+    # 64 < w <= 128 (the GPU path's limit): int8 in two column groups
+    ds.embed(ds.gram(ds.matrix_from_host(d)), rank=100, oversampling=20, seed=2)
+    assert (ds.stats_get().last_product_kernel, ds.stats_get().last_product_groups) == (1, 2)
+
+
+@pytest.mark.parametrize("rank,over", [(60, 10), (100, 20), (100, 28)])
+def test_int8_column_groups_match_fp64(ds, oracle, rank, over):
+    # w = 70 -> groups of 64 + 32 columns (wp 72); w = 120, 128 -> 64 + 64
+    n = 900
+    d = oracle.euclidean_matrix(ds.synth_points(3, n, 7))
+    g = ds.gram(ds.matrix_from_host(d))
+    ds.set_product_path(2)
+    try:
+        e8 = ds.embed(g, rank=rank, oversampling=over, power_iters=2, seed=4)
+        st = ds.stats_get()
+        assert (st.last_product_kernel, st.last_product_groups) == (1, 2)
+        ds.set_product_path(1)
+        e64 = ds.embed(g, rank=rank, oversampling=over, power_iters=2, seed=4)
+        assert ds.stats_get().last_product_kernel == 0
+    finally:
+        ds.set_product_path(0)
+    assert e8.dims == e64.dims
+    np.testing.assert_allclose(e8.eigenvalues[:40], e64.eigenvalues[:40], rtol=1e-10)
+    np.testing.assert_allclose(e8.eigenvalues, e64.eigenvalues, rtol=1e-6)
+    st_, rm, grand = oracle.gram_stats(d)
+    want = oracle.embed(rank, over, 2, 4, d=d, row_mean=rm, grand=grand)
+    np.testing.assert_allclose(e8.eigenvalues[:20], want["eigenvalues"][:20], rtol=1e-10)
 
 
 def test_matrix_write_tsv_byte_identical(ds, oracle, ref, tmp_path):
