@@ -143,17 +143,29 @@ template <int NB>
 constexpr int tmem_digits_ts() {
     return hybrid_ts<NB>() ? 4 : kDig;
 }
+// NB = 32: four 64-column A stages after the 224 accumulator columns (a
+// fifth 56-column stage fits — DSB_TS_NA32=5 DSB_TS_ACOLS32=56
+// DSB_TS_ABASE32=224 — and measured no faster)
+#ifndef DSB_TS_NA32
+#define DSB_TS_NA32 4
+#endif
 template <int NB>
 constexpr int a_stages_ts() {
-    return NB <= 32 ? 4 : (hybrid_ts<NB>() ? 2 : 1);
+    return NB <= 32 ? DSB_TS_NA32 : (hybrid_ts<NB>() ? 2 : 1);
 }
+#ifndef DSB_TS_ACOLS32
+#define DSB_TS_ACOLS32 64
+#endif
+#ifndef DSB_TS_ABASE32
+#define DSB_TS_ABASE32 256
+#endif
 template <int NB>
 constexpr uint32_t a_stage_cols_ts() {
-    return hybrid_ts<NB>() ? 32u : 64u;
+    return hybrid_ts<NB>() ? 32u : (NB <= 32 ? DSB_TS_ACOLS32 : 64u);
 }
 template <int NB>
 constexpr uint32_t a_base_ts() {  // first TMEM column of the A stages
-    return NB <= 32 ? 256u : 448u;
+    return NB <= 32 ? DSB_TS_ABASE32 : 448u;
 }
 template <int NB>
 constexpr int a_smem_stage_ts() {  // bytes of shared-memory A digits per stage
@@ -294,6 +306,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         }
         static_assert(kBProd || NBR == NA, "B ring rides with the A ring");
         static_assert(kBProd || NA > 1, "a single A stage needs the producer's B ring");
+        static_assert(a_base_ts<NB>() + NA * ACOLS <= 512 && a_base_ts<NB>() >= 7 * NB,
+                      "A stages fit in TMEM after the accumulators");
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 4);
         fence_mbar_init();
