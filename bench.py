@@ -31,7 +31,6 @@ import math
 import os
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -72,41 +71,41 @@ def measured_peaks() -> dict:
 
 class ClockSampler:
     """SM clock and throttle reasons sampled through NVML during the timed
-    region (a library call per sample — no nvidia-smi process spawned inside
-    the measurement)."""
+    region, from a separate process (tools/nvml_sampler.py): NVML calls from
+    a thread of this interpreter cost the timed region ~0.2 ms per step
+    (measured), a sampler process nothing measurable."""
 
-    def __init__(self, index: int, period_s: float = 0.05):
+    def __init__(self, index: int, period_s: float = 0.02):
         self.index = index
         self.period = period_s
-        self.samples: list[tuple[float, float, int]] = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self.samples: list = []
         self.error = None
-
-    def _run(self):
-        try:
-            import pynvml as N
-            N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
-            reasons_fn = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-                getattr(N, "nvmlDeviceGetCurrentClocksThrottleReasons")
-            while not self._stop.is_set():
-                sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
-                rs = int(reasons_fn(h))
-                self.samples.append((sm, mx, rs))
-                self._stop.wait(self.period)
-            N.nvmlShutdown()
-        except Exception as e:  # pragma: no cover - reported in the JSON
-            self.error = repr(e)
+        self._p = None
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(
+                [sys.executable, str(ROOT / "tools" / "nvml_sampler.py"), str(self.index),
+                 str(self.period)], stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            if self._p.stdout.readline().strip() != "ready":
+                raise RuntimeError("sampler did not start")
+        except Exception as e:  # pragma: no cover - reported in the JSON
+            self.error = repr(e)
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        try:
+            out, _ = self._p.communicate("stop\n", timeout=30)
+            got = json.loads(out.strip().splitlines()[-1])
+            # drop the samples taken just before and just after the region
+            self.samples = [tuple(x) for x in got[1:-1]] or [tuple(x) for x in got]
+        except Exception as e:  # pragma: no cover
+            self.error = repr(e)
+            self._p.kill()
 
     def summary(self) -> dict:
         bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,

@@ -236,7 +236,9 @@ size_t divscope_embedding_eigenvalues(const divscope_embedding* e, double* out, 
 double divscope_embedding_dropped_negative_mass(const divscope_embedding* e);
 int divscope_embedding_truncated(const divscope_embedding* e);
 /* NEW: pointer to the n x dims row-major coordinates (valid for the life of
- * the handle; NULL when dims == 0). */
+ * the handle; NULL when dims == 0). divscope_embed leaves the coordinates in
+ * device memory; the first host access (this call, _get, _write) downloads
+ * them once. */
 const double* divscope_embedding_coords(const divscope_embedding* e);
 /* NEW: Frobenius-gap residual of the spectrum the embedding came from. */
 double divscope_embedding_resid(const divscope_embedding* e);

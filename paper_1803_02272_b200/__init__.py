@@ -366,7 +366,8 @@ def randomized_range(g: Matrix, rank=None, oversampling=None, power_iters=None, 
 
 
 class Embedding:
-    """Owning wrapper of a ``divscope_embedding*`` (coordinates on the host)."""
+    """Owning wrapper of a ``divscope_embedding*`` (coordinates stay on the device
+    until first read, then are cached on the host)."""
 
     def __init__(self, handle: int):
         self._h = C.c_void_p(handle)

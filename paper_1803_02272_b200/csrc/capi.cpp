@@ -98,9 +98,10 @@ void write_embedding_tsv(const dsb::Embedding& e, const std::vector<std::string>
     out << "id";
     for (size_t c = 0; c < e.r; ++c) out << "\tdim" << (c + 1);
     out << '\n';
+    const double* xy = e.host_coords();
     for (size_t i = 0; i < e.n; ++i) {
         out << ids[i];
-        for (size_t c = 0; c < e.r; ++c) out << '\t' << dsb::format_double(e.coords[i * e.r + c]);
+        for (size_t c = 0; c < e.r; ++c) out << '\t' << dsb::format_double(xy[i * e.r + c]);
         out << '\n';
     }
     if (!out.flush()) throw Error(errc::io_error, "failed writing " + path);
@@ -562,7 +563,7 @@ const char* divscope_embedding_id(const divscope_embedding* e, size_t i) {
 
 double divscope_embedding_get(const divscope_embedding* e, size_t i, size_t c) {
     if (!e || i >= e->emb.n || c >= e->emb.r) return 0.0;
-    return e->emb.coords[i * e->emb.r + c];
+    return e->emb.host_coords()[i * e->emb.r + c];
 }
 
 size_t divscope_embedding_eigenvalues(const divscope_embedding* e, double* out, size_t cap) {
@@ -582,8 +583,8 @@ int divscope_embedding_truncated(const divscope_embedding* e) {
 }
 
 const double* divscope_embedding_coords(const divscope_embedding* e) {
-    if (!e || e->emb.coords.empty()) return nullptr;
-    return e->emb.coords.data();
+    if (!e) return nullptr;
+    return e->emb.host_coords();
 }
 
 double divscope_embedding_resid(const divscope_embedding* e) { return e ? e->emb.resid : 0.0; }
@@ -605,7 +606,7 @@ divscope_status divscope_embedding_load(const char* tsv_path, divscope_embedding
             size_t dims = 0;
             std::vector<double> coords;
             load_embedding_tsv(tsv_path, handle->ids, dims, coords);
-            handle->emb.coords.assign(coords);
+            handle->emb.set_host_coords(coords);
             handle->emb.n = handle->ids.size();
             handle->emb.r = dims;
         } catch (...) {
@@ -695,7 +696,7 @@ void divscope_stats_enable_timing(int on) {
     try {
         dsb::Ctx& c = dsb::Ctx::get();
         std::lock_guard<std::recursive_mutex> lk(c.mu);
-        c.timing = on != 0;
+        c.set_timing(on != 0);
     } catch (...) {
     }
 }

@@ -124,11 +124,42 @@ void* Ctx::scratch(const std::string& slot, size_t bytes) {
     return b->p;
 }
 
+void* Ctx::pinned_scratch(const std::string& name, size_t bytes) {
+    auto& b = pinned_arena_[name];
+    const size_t elems = (bytes + sizeof(double) - 1) / sizeof(double);
+    if (!b || b->size() < elems) {
+        if (b) DSB_CUDA(cudaStreamSynchronize(stream));  // an async copy may still target it
+        b = std::make_unique<PinnedVec>(elems);
+    }
+    return b->data();
+}
+
+cudaEvent_t Ctx::pooled_event() {
+    if (!event_pool.empty()) {
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    DSB_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void Ctx::set_timing(bool on) {
+    timing = on;
+    // events come from a pool filled here, so a timed region creates none
+    while (on && event_pool.size() < 1024) {
+        cudaEvent_t e;
+        DSB_CUDA(cudaEventCreate(&e));
+        event_pool.push_back(e);
+    }
+}
+
 void Ctx::begin_timed(int kind, cudaEvent_t* a) {
     (void)kind;
     *a = nullptr;
     if (!timing) return;
-    DSB_CUDA(cudaEventCreate(a));
+    *a = pooled_event();
     DSB_CUDA(cudaEventRecord(*a, stream));
 }
 
@@ -136,8 +167,7 @@ void Ctx::end_timed(int kind, cudaEvent_t a) {
     if (kind == 1) ++k2_launches;
     else ++k1_launches;
     if (!timing || !a) return;
-    cudaEvent_t b;
-    DSB_CUDA(cudaEventCreate(&b));
+    cudaEvent_t b = pooled_event();
     DSB_CUDA(cudaEventRecord(b, stream));
     pending.push_back({a, b, kind});
 }
@@ -145,14 +175,8 @@ void Ctx::end_timed(int kind, cudaEvent_t a) {
 void Ctx::make_events(cudaEvent_t* a, cudaEvent_t* b) {
     *a = *b = nullptr;
     if (!timing) return;
-    for (cudaEvent_t* e : {a, b}) {
-        if (!event_pool.empty()) {
-            *e = event_pool.back();
-            event_pool.pop_back();
-        } else {
-            DSB_CUDA(cudaEventCreate(e));
-        }
-    }
+    *a = pooled_event();
+    *b = pooled_event();
 }
 
 void Ctx::add_timed(int kind, cudaEvent_t a, cudaEvent_t b) {

@@ -53,6 +53,44 @@ private:
 void cuda_check(cudaError_t e, const char* what);
 #define DSB_CUDA(call) ::dsb::cuda_check((call), #call)
 
+// Host array of doubles in pinned (page-locked) memory drawn from a recycling
+// pool, so device->host result copies run at full PCIe / C2C speed without
+// paying cudaMallocHost per call. Falls back to pageable memory when pinning
+// is unavailable.
+class PinnedVec {
+public:
+    PinnedVec() = default;
+    explicit PinnedVec(size_t n) { resize(n); }
+    PinnedVec(const PinnedVec&) = delete;
+    PinnedVec& operator=(const PinnedVec&) = delete;
+    PinnedVec(PinnedVec&& o) noexcept { swap(o); }
+    PinnedVec& operator=(PinnedVec&& o) noexcept {
+        swap(o);
+        return *this;
+    }
+    ~PinnedVec() { release(); }
+    void resize(size_t n);
+    void assign(const std::vector<double>& v);
+    double* data() { return p_; }
+    const double* data() const { return p_; }
+    size_t size() const { return n_; }
+    bool empty() const { return n_ == 0; }
+    double& operator[](size_t i) { return p_[i]; }
+    double operator[](size_t i) const { return p_[i]; }
+
+private:
+    void release();
+    void swap(PinnedVec& o) noexcept {
+        std::swap(p_, o.p_);
+        std::swap(n_, o.n_);
+        std::swap(cap_, o.cap_);
+        std::swap(pinned_, o.pinned_);
+    }
+    double* p_ = nullptr;
+    size_t n_ = 0, cap_ = 0;
+    bool pinned_ = false;
+};
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -98,9 +136,13 @@ public:
     void make_events(cudaEvent_t* a, cudaEvent_t* b);
     void add_timed(int kind, cudaEvent_t a, cudaEvent_t b);
     void drain_timing();
+    void set_timing(bool on);
+    cudaEvent_t pooled_event();
 
     void h2d_copy(void* dst, const void* src, size_t bytes);
     void d2h_copy(void* dst, const void* src, size_t bytes);
+    // named page-locked host buffer (grown on demand, never shrunk)
+    void* pinned_scratch(const std::string& name, size_t bytes);
     void sync();
 
     bool encode_tmap(CUtensorMap* map, const void* base, DType dt, size_t rows, size_t cols,
@@ -113,6 +155,7 @@ private:
     void init();
     bool inited_ = false;
     std::map<std::string, std::unique_ptr<DevBuf>> arena_;
+    std::map<std::string, std::unique_ptr<PinnedVec>> pinned_arena_;
     void* encode_fn_ = nullptr;
 };
 
@@ -153,43 +196,6 @@ struct GramInfo {
     std::mutex mu;
 };
 
-// Host array of doubles in pinned (page-locked) memory drawn from a recycling
-// pool, so device->host result copies run at full PCIe / C2C speed without
-// paying cudaMallocHost per call. Falls back to pageable memory when pinning
-// is unavailable.
-class PinnedVec {
-public:
-    PinnedVec() = default;
-    explicit PinnedVec(size_t n) { resize(n); }
-    PinnedVec(const PinnedVec&) = delete;
-    PinnedVec& operator=(const PinnedVec&) = delete;
-    PinnedVec(PinnedVec&& o) noexcept { swap(o); }
-    PinnedVec& operator=(PinnedVec&& o) noexcept {
-        swap(o);
-        return *this;
-    }
-    ~PinnedVec() { release(); }
-    void resize(size_t n);
-    void assign(const std::vector<double>& v);
-    double* data() { return p_; }
-    const double* data() const { return p_; }
-    size_t size() const { return n_; }
-    bool empty() const { return n_ == 0; }
-    double& operator[](size_t i) { return p_[i]; }
-    double operator[](size_t i) const { return p_[i]; }
-
-private:
-    void release();
-    void swap(PinnedVec& o) noexcept {
-        std::swap(p_, o.p_);
-        std::swap(n_, o.n_);
-        std::swap(cap_, o.cap_);
-        std::swap(pinned_, o.pinned_);
-    }
-    double* p_ = nullptr;
-    size_t n_ = 0, cap_ = 0;
-    bool pinned_ = false;
-};
 
 size_t round_up(size_t x, size_t m);
 std::shared_ptr<Store> make_store(size_t rows, size_t cols, bool symmetric, DType dt);

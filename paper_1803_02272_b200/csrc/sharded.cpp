@@ -423,9 +423,11 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
                c.stream);
     ShardOut out;
     double* coords = nullptr;
+    std::shared_ptr<DevBuf> dcoords;  // owned by the returned embedding
     if (embed_mode) {
         const size_t rq = std::max<size_t>(req, 1);
-        coords = static_cast<double*>(c.scratch("coords", n * rq * 8));
+        dcoords = std::make_shared<DevBuf>(n * rq * 8);
+        coords = dcoords->as<double>();
         const int P = lift_grid(std::max<size_t>(m, 1), c.sms);
         // all ranks' CTA partials side by side: [world][P][rmax][2]
         double* lp = static_cast<double*>(
@@ -481,8 +483,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         e.dropped_negative_mass = dmeta[1];
         e.resid = dmeta[0];
         e.eigenvalues.assign(kept, kept + e.r);
-        e.coords.resize(n * e.r);
-        if (e.r) c.d2h_copy(e.coords.data(), coords, n * e.r * 8);
+        e.dcoords = std::move(dcoords);
     }
     return out;
 }

@@ -344,8 +344,11 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
                eo, c.stream);
     mark("evd");
     double* coords = nullptr;
+    std::shared_ptr<DevBuf> dcoords;
     if (what == What::Embed) {
-        coords = static_cast<double*>(c.scratch("coords", n * std::max<size_t>(req, 1) * 8));
+        // owned by the returned embedding (host copy on first access)
+        dcoords = std::make_shared<DevBuf>(n * std::max<size_t>(req, 1) * 8);
+        coords = dcoords->as<double>();
         const int P = static_cast<int>(std::min<size_t>(static_cast<size_t>(c.sms) * 2,
                                                         std::max<size_t>(n / 64, 1)));
         double* lp = static_cast<double*>(
@@ -354,19 +357,24 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
                     coords, lp, c.sms, c.stream);
     }
     DSB_CUDA(cudaGetLastError());
-    // read back (one sync for all of it)
+    // read back into pinned memory, one sync for all of it
     struct Meta {
         double vals[kMaxWP];
         double kept[kMaxWP];
         double dmeta[8];
         int imeta[8];
-    } meta{};
+        int flags;
+    };
+    Meta& meta = *static_cast<Meta*>(c.pinned_scratch("run_meta", sizeof(Meta)));
     DSB_CUDA(cudaMemcpyAsync(meta.vals, eo.vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
     DSB_CUDA(cudaMemcpyAsync(meta.kept, eo.kept_vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
     DSB_CUDA(cudaMemcpyAsync(meta.dmeta, eo.dmeta, 8 * 8, cudaMemcpyDeviceToHost, c.stream));
+    DSB_CUDA(cudaMemcpyAsync(meta.imeta, eo.imeta, 8 * sizeof(int), cudaMemcpyDeviceToHost,
+                             c.stream));
+    DSB_CUDA(cudaMemcpyAsync(&meta.flags, flags, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     mark("lift");
     if (trace) std::fprintf(stderr, "[trace] host enqueue done %.1f us\n", host_us());
-    c.d2h_copy(meta.imeta, eo.imeta, 8 * sizeof(int));
+    c.sync();
     if (trace) std::fprintf(stderr, "[trace] host meta synced %.1f us\n", host_us());
     if (trace) {
         for (size_t i = 1; i < marks.size(); ++i) {
@@ -376,13 +384,9 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         }
         for (auto& m : marks) cudaEventDestroy(m.second);
     }
-    c.d2h += w * 16 + 64;
+    c.d2h += w * 16 + 64 + 32 + 4;
     c.last_evd_sweeps = meta.imeta[3];
-    {
-        int fl = 0;
-        c.d2h_copy(&fl, flags, sizeof(int));
-        c.last_orth_shifted = fl & 1;
-    }
+    c.last_orth_shifted = meta.flags & 1;
     if (!meta.imeta[4])
         throw Error(errc::internal, "small eigensolve failed");  // ref rsvd.cpp:113-114
     out.vals.assign(meta.vals, meta.vals + w);
@@ -396,8 +400,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         e.dropped_negative_mass = meta.dmeta[1];
         e.resid = meta.dmeta[0];
         e.eigenvalues.assign(meta.kept, meta.kept + e.r);
-        e.coords.resize(n * e.r);
-        if (e.r) c.d2h_copy(e.coords.data(), coords, n * e.r * sizeof(double));
+        // the lift wrote n x req with row stride r (= kept columns)
+        e.dcoords = std::move(dcoords);
     }
     if (trace) std::fprintf(stderr, "[trace] host coords done %.1f us\n", host_us());
     return out;
@@ -450,6 +454,24 @@ Spectrum eigs_sym(const Matrix& g, const SolverOptions& opts) {
     return s;
 }
 
+const double* Embedding::host_coords() const {
+    if (n * r == 0) return nullptr;
+    std::call_once(*once_, [this] {
+        if (!dcoords) return;
+        Ctx& c = Ctx::get();
+        std::lock_guard<std::recursive_mutex> lk(c.mu);
+        PinnedVec h(n * r);
+        c.d2h_copy(h.data(), dcoords->p, n * r * sizeof(double));
+        coords_ = std::move(h);
+    });
+    return coords_.empty() ? nullptr : coords_.data();
+}
+
+void Embedding::set_host_coords(const std::vector<double>& v) {
+    coords_.assign(v);
+    dcoords.reset();
+}
+
 Embedding embed(const Matrix& g, size_t rank, SolverOptions opts) {
     Ctx& c = Ctx::get();
     std::lock_guard<std::recursive_mutex> lk(c.mu);
@@ -476,7 +498,11 @@ double reconstruction_error(const Matrix& g, const Embedding& e) {
     const bool lazy = static_cast<bool>(g.gram);
     const size_t r = e.r;
     double* x = static_cast<double*>(c.scratch("recon_x", std::max<size_t>(n * r, 1) * 8));
-    if (r) c.h2d_copy(x, e.coords.data(), n * r * sizeof(double));
+    if (r && e.dcoords)
+        DSB_CUDA(cudaMemcpyAsync(x, e.dcoords->p, n * r * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 c.stream));
+    else if (r)
+        c.h2d_copy(x, e.host_coords(), n * r * sizeof(double));
     double* part = static_cast<double*>(c.scratch("recon_part", recon_blocks(n, lazy) * 8));
     double* out = static_cast<double*>(c.scratch("recon_out", 64));
     launch_recon(s.buf->p, s.dt, s.ld, n, lazy, lazy ? g.gram->row_mean->as<double>() : nullptr,

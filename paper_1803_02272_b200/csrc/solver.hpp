@@ -4,6 +4,7 @@
 #pragma once
 
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -35,11 +36,20 @@ struct Spectrum {
 // ref src/mds.hpp:21-28
 struct Embedding {
     size_t n = 0, r = 0;
-    PinnedVec coords;                 // n x r row-major (pinned)
+    // n x r row-major coordinates. The solver leaves them on the device
+    // (dcoords); the host copy is made on first access, so an embed call
+    // does not pay the download unless the caller reads them.
+    std::shared_ptr<DevBuf> dcoords;
+    const double* host_coords() const;  // nullptr when n * r == 0
+    void set_host_coords(const std::vector<double>& v);
     std::vector<double> eigenvalues;  // retained, descending
     double dropped_negative_mass = 0.0;
     bool truncated = false;
     double resid = 0.0;
+
+private:
+    mutable PinnedVec coords_;
+    mutable std::shared_ptr<std::once_flag> once_ = std::make_shared<std::once_flag>();
 };
 
 // ref src/mds.cpp:14-60 (validation + centering terms; G not materialized)
