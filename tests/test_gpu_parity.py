@@ -558,3 +558,26 @@ def test_matrix_write_tsv_byte_identical(ds, oracle, ref, tmp_path):
     vals = np.array([[float(x) for x in ln.split("\t")[1:]] for ln in lines[1:]])
     assert np.max(np.abs(vals - gref)) <= 1e-13 * np.max(np.abs(gref))
     assert err(ds, g.write_tsv, tmp_path / "x.tsv", row_ids=["a"]) == ds.Status.ERR_SHAPE_MISMATCH
+
+
+@pytest.mark.parametrize("n,rank,over", [(4095, 6, 2), (4096, 22, 10), (4097, 30, 3),
+                                         (4225, 40, 25), (2049, 60, 5), (1153, 90, 38)])
+def test_int8_tile_boundaries_match_fp64(ds, n, rank, over):
+    # row counts around the 128-row block / 32-column k-step / 256-row padding
+    # and panel widths around the 32 / 64 column-group edges (wp 8..128)
+    d = ds.matrix_euclidean(ds.synth_points(2, n, n % 97))
+    g = ds.gram(d)
+    ds.set_product_path(2)
+    try:
+        e8 = ds.embed(g, rank=rank, oversampling=over, power_iters=1, seed=n)
+        assert ds.stats_get().last_product_kernel == 1
+        ds.set_product_path(1)
+        e64 = ds.embed(g, rank=rank, oversampling=over, power_iters=1, seed=n)
+    finally:
+        ds.set_product_path(0)
+    assert e8.dims == e64.dims
+    top = min(e8.dims, 12)
+    np.testing.assert_allclose(e8.eigenvalues[:top], e64.eigenvalues[:top], rtol=1e-10)
+    from helpers import coords_match_up_to_sign
+    assert coords_match_up_to_sign(e8.coords[:, :top], e64.coords[:, :top]) < \
+        1e-7 * np.sqrt(e64.eigenvalues[0])

@@ -139,3 +139,21 @@ def test_block_fingerprints_pair_transposes(ds, oracle):
     # f32 storage hashes the widened values
     af = ds.matrix_from_host_rows_f32(d[0:256].astype(np.float32), n, 0, 256)
     assert fp(af, 256, 444, False) == _fp_np(d[0:256, 256:700].astype(np.float32), 0, 256, False)
+
+
+@pytest.mark.parametrize("rank,over,f32", [(60, 10, False), (100, 20, True)])
+def test_sharded_wide_panel_matches_unsharded(ds, comm1, product_path, rank, over, f32):
+    # w > 64: the int8 product runs in two column groups on each rank's rows
+    # (forced int8) or the fp64 DMMA kernel at WP > 64 (auto at this n)
+    pts = ds.synth_points(3, 1500, 6)
+    n = pts.shape[0]
+    a = ds.embed(ds.gram(ds.matrix_euclidean(pts, store_f32=f32)), rank=rank, oversampling=over,
+                 power_iters=2, seed=3)
+    b = ds.embed(ds.gram(ds.matrix_euclidean_rows(pts, 0, n, store_f32=f32)), rank=rank,
+                 oversampling=over, power_iters=2, seed=3)
+    st = ds.stats_get()
+    if product_path == "int8":
+        assert (st.last_product_kernel, st.last_product_groups) == (1, 2)
+    assert b.dims == a.dims
+    np.testing.assert_allclose(b.eigenvalues[:30], a.eigenvalues[:30], rtol=1e-10)
+    np.testing.assert_allclose(b.eigenvalues, a.eigenvalues, rtol=1e-6)
