@@ -46,30 +46,31 @@ __device__ bool cta_chol_inverse(double* __restrict__ A, double* __restrict__ E,
                                  bool first_shifting, bool drop_mode, int* __restrict__ dropped_s,
                                  double* __restrict__ dpiv, const unsigned short* __restrict__ tri,
                                  const int* __restrict__ tri_off) {
-    __shared__ double invp_s;
-    __shared__ int shift_s;
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int e = tid; e < WP * WP; e += nt) E[e] = (e / WP == e % WP) ? 1.0 : 0.0;
-    if (tid == 0) shift_s = 0;
     __syncthreads();
     for (int k = 0; k < WP; ++k) {
+        // every thread takes the (identical) pivot decision from the same
+        // shared values: no barrier between the decision and the update
+        const double p = A[k * WP + k];
+        const double d0k = d0s[k];
+        bool drop = (k >= w) || !(d0k > 0.0) || !(p > 0.0);
+        bool shift = false;
+        if (first_shifting) {
+            if (k < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift = true;
+            drop = drop && !(k < w && d0k > 0.0);
+        } else if (drop_mode && p <= kDropTolF * maxdiag) {
+            drop = true;
+        }
+        if (shift) {  // uniform across the CTA; the caller rewrites A next
+            __syncthreads();
+            return true;
+        }
         if (tid == 0) {
-            const double p = A[k * WP + k];
-            const double d0k = d0s[k];
-            bool drop = (k >= w) || !(d0k > 0.0) || !(p > 0.0);
-            if (first_shifting) {
-                if (k < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift_s = 1;
-                drop = drop && !(k < w && d0k > 0.0);
-            } else if (drop_mode && p <= kDropTolF * maxdiag) {
-                drop = true;
-            }
             dropped_s[k] = drop;
             dpiv[k] = drop ? 0.0 : p;
-            invp_s = drop ? 0.0 : 1.0 / p;
         }
-        __syncthreads();
-        if (shift_s) return true;
-        const double invp = invp_s;  // 0 for a dropped column: no elimination with it
+        const double invp = drop ? 0.0 : 1.0 / p;  // 0 for a dropped column: no elimination
         const double* rowk = A + k * WP;
         // trailing upper triangle {(i, j): k < i <= j}: a suffix of `tri`
         const int t0 = tri_off[k + 1], t1 = tri_off[WP];
