@@ -581,3 +581,32 @@ def test_int8_tile_boundaries_match_fp64(ds, n, rank, over):
     from helpers import coords_match_up_to_sign
     assert coords_match_up_to_sign(e8.coords[:, :top], e64.coords[:, :top]) < \
         1e-7 * np.sqrt(e64.eigenvalues[0])
+
+
+def test_handles_shared_across_threads(ds):
+    # ref include/divscope.h:5-9: handles are immutable and shareable across
+    # threads; the library serializes device work on its context and every
+    # thread gets the same answer (ctypes drops the GIL inside the calls)
+    import threading
+    g = ds.gram(ds.matrix_euclidean(ds.synth_points(2, 3000, 8)))
+    want = ds.embed(g, rank=8, oversampling=6, power_iters=2, seed=5)
+    shared = ds.embed(g, rank=8, oversampling=6, power_iters=2, seed=5)
+    out, errs = {}, []
+
+    def work(t):
+        try:
+            e = ds.embed(g, rank=8, oversampling=6, power_iters=2, seed=5)
+            out[t] = (e.eigenvalues.copy(), e.coords.copy(), shared.coords.copy())
+        except Exception as ex:  # pragma: no cover - reported below
+            errs.append(repr(ex))
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for vals, coords, sh in out.values():
+        assert np.array_equal(vals, want.eigenvalues)
+        assert np.array_equal(coords, want.coords)
+        assert np.array_equal(sh, want.coords)  # first-access download raced by 6 threads
