@@ -747,21 +747,28 @@ void* divscope_stream(void) {
 
 }  // extern "C"
 
-// test hook: fingerprint of columns [col0, col0 + ncols) of a matrix handle's
-// rows (the sharded symmetry check, sharded.cpp)
-extern "C" int divscope_debug_block_fingerprint(const divscope_matrix* m, size_t col0,
-                                                size_t ncols, int swap,
-                                                unsigned long long* out) {
+// test hook: the antisymmetric symmetry fingerprint of a matrix handle's rows
+// (the sharded gram's one-pass symmetry check, k1_shard.cu / sharded.cpp):
+// out[0], out[1] = its two 32-bit halves
+extern "C" int divscope_debug_sym_fingerprint(const divscope_matrix* m, unsigned long long* out) {
     if (!m || !out) return DIVSCOPE_ERR_INVALID_ARGUMENT;
     return wrap([&] {
         dsb::Ctx& c = dsb::Ctx::get();
+        std::lock_guard<std::recursive_mutex> lk(c.mu);
         const dsb::Store& st = *m->m.store;
-        if (col0 + ncols > st.cols) throw Error(errc::invalid_argument, "bad column range");
-        auto* d = static_cast<unsigned long long*>(c.scratch("dbg_fp", 8));
-        DSB_CUDA(cudaMemsetAsync(d, 0, 8, c.stream));
-        dsb::launch_block_fingerprint(st.buf->p, st.dt, st.ld, st.rows, col0, ncols,
-                                      st.sharded ? st.row_begin : 0, swap != 0, d, c.sms,
-                                      c.stream);
-        c.d2h_copy(out, d, 8);
+        const size_t rows = st.rows;
+        const int grid = dsb::k1_rows_grid(rows, c.sms);
+        auto* d = static_cast<unsigned long long*>(c.scratch("dbg_fp", 16));
+        double* rs = static_cast<double*>(c.scratch("dbg_fp_rs", std::max<size_t>(rows, 1) * 8));
+        double* cta = static_cast<double*>(c.scratch("dbg_fp_cta", static_cast<size_t>(grid) * 24));
+        int* ex = static_cast<int*>(c.scratch("dbg_fp_ex", std::max<size_t>(rows, 1) * 4));
+        DSB_CUDA(cudaMemsetAsync(d, 0, 16, c.stream));
+        if (rows)
+            dsb::launch_k1_rows(st.buf->p, st.dt, st.ld, rows, st.cols,
+                                st.sharded ? st.row_begin : 0, rs, nullptr, cta, grid, c.stream,
+                                ex, d);
+        c.d2h_copy(out, d, 16);
+        out[0] &= 0xFFFFFFFFull;
+        out[1] &= 0xFFFFFFFFull;
     });
 }

@@ -83,6 +83,11 @@ void Comm::allreduce_max(double* buf, size_t count, cudaStream_t st) {
     check(allReduce_(buf, buf, count, ncclFloat64, ncclMax, comm_, st), "ncclAllReduce");
 }
 
+void Comm::allreduce_sum_u64(unsigned long long* buf, size_t count, cudaStream_t st) {
+    if (!comm_) return;
+    check(allReduce_(buf, buf, count, ncclUint64, ncclSum, comm_, st), "ncclAllReduce");
+}
+
 void Comm::allgatherv(double* buf, const size_t* counts, const size_t* displs, cudaStream_t st) {
     if (!comm_ || world_ == 1) return;
     check(groupStart_(), "ncclGroupStart");

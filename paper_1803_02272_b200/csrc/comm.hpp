@@ -25,6 +25,8 @@ public:
     // collectives on the library stream (double elements)
     void allreduce_sum(double* buf, size_t count, cudaStream_t st);
     void allreduce_max(double* buf, size_t count, cudaStream_t st);
+    // sum of unsigned 64-bit integers (wraps mod 2^64)
+    void allreduce_sum_u64(unsigned long long* buf, size_t count, cudaStream_t st);
     // rank r contributes counts[r] elements at displs[r] of buf (in place)
     void allgatherv(double* buf, const size_t* counts, const size_t* displs, cudaStream_t st);
     // pairwise exchange: send `count_send` to peer_send, receive `count_recv` from peer_recv

@@ -22,19 +22,47 @@ struct V2<float> {
     using type = float2;
 };
 
+// Antisymmetric fingerprint of D: sum over (i, j) of sgn(j - i) h(d_ij, {i, j})
+// where h mixes the value bits with the UNORDERED position through a
+// bijection of each 32-bit half of the value (two independent 32-bit sums,
+// `lo` and `hi`). Over a whole matrix both sums are zero (mod 2^32) iff every
+// mirrored pair has identical bits: one differing pair is always detected,
+// several cancel only by a ~2^-64 accident. Each rank sums over its own rows
+// inside the K1 pass (32-bit integer ops only, ~12 per element, so the pass
+// stays HBM-bound) and one all-reduce decides the symmetry of the whole
+// sharded matrix.
+struct SymFp {
+    uint32_t lo = 0, hi = 0;
+    __device__ __forceinline__ void add(double v, uint32_t i, uint32_t j) {
+        const uint32_t key = j > i ? i * 0x9E3779B1u + j * 0x85EBCA77u
+                                   : j * 0x9E3779B1u + i * 0x85EBCA77u;
+        const uint32_t s = j > i ? 1u : (j < i ? 0xFFFFFFFFu : 0u);
+        const uint32_t vl = static_cast<uint32_t>(__double2loint(v));
+        const uint32_t vh = static_cast<uint32_t>(__double2hiint(v));
+        lo += ((vl ^ key) * 0xC2B2AE3Du) * s;
+        hi += ((vh ^ key ^ 0x165667B1u) * 0x27D4EB2Fu) * s;
+    }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, size_t ld,
-                                                      size_t rows, size_t cols,
+                                                      size_t rows, size_t cols, size_t row0,
                                                       double* __restrict__ rowsum,
+                                                      double* __restrict__ row_mean,
                                                       double* __restrict__ cta_stats,
-                                                      int* __restrict__ row_exp) {
-    __shared__ double red[2][8];
+                                                      int* __restrict__ row_exp,
+                                                      unsigned long long* __restrict__ fp_out) {
+    __shared__ double red[3][8];
+    __shared__ uint32_t fred[2][8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t gw = static_cast<size_t>(blockIdx.x) * 8 + warp;
     const size_t nw = static_cast<size_t>(gridDim.x) * 8;
-    double sum4 = 0.0, maxabs = 0.0;
+    double sum4 = 0.0, maxabs = 0.0, ratio = 0.0;
+    const double nf = static_cast<double>(cols);
+    SymFp fp;
     for (size_t r = gw; r < rows; r += nw) {
         const T* row = d + r * ld;
+        const uint32_t gi = static_cast<uint32_t>(row0 + r);
         double s = 0.0;
         uint32_t hmx = 0u;  // max over the row of the high word of d^2 (>= 0)
         size_t c = 2 * lane;
@@ -47,6 +75,9 @@ __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, s
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const double a0 = v[u].x, a1 = v[u].y;
+                const uint32_t j = static_cast<uint32_t>(c + 64 * u);
+                fp.add(a0, gi, j);
+                fp.add(a1, gi, j + 1);
                 const double s0 = a0 * a0, s1 = a1 * a1;
                 s += s0 + s1;
                 sum4 += s0 * s0 + s1 * s1;
@@ -60,6 +91,8 @@ __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, s
         for (; c < cols; c += 64) {
             const double a0 = static_cast<double>(row[c]);
             const double a1 = (c + 1 < cols) ? static_cast<double>(row[c + 1]) : 0.0;
+            fp.add(a0, gi, static_cast<uint32_t>(c));
+            if (c + 1 < cols) fp.add(a1, gi, static_cast<uint32_t>(c + 1));
             const double s0 = a0 * a0, s1 = a1 * a1;
             s += s0 + s1;
             sum4 += s0 * s0 + s1 * s1;
@@ -73,26 +106,97 @@ __global__ void __launch_bounds__(256) k1_rows_kernel(const T* __restrict__ d, s
         for (int o = 16; o > 0; o >>= 1) hmx = max(hmx, __shfl_xor_sync(0xffffffffu, hmx, o));
         if (lane == 0) {
             rowsum[r] = s;
+            const double rm = s / nf;
+            if (row_mean) row_mean[r] = rm;
             // smallest e with d^2 < 2^e over the row (int8 slice scale; K1 rule)
             const int be = static_cast<int>((hmx >> 20) & 0x7ffu);
-            row_exp[r] = hmx == 0u ? -1100 : (be == 0 ? -1022 : be - 1022);
+            const int e = hmx == 0u ? -1100 : (be == 0 ? -1022 : be - 1022);
+            row_exp[r] = e;
+            // int8 admission bound 2^e_i / r_i (K1 rule)
+            if (e > -1100) ratio = fmax(ratio, rm > 0.0 ? ldexp(1.0, e) / rm : 1e300);
         }
     }
     sum4 = warp_sum(sum4);
     maxabs = warp_max(maxabs);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        fp.lo += __shfl_xor_sync(0xffffffffu, fp.lo, o);
+        fp.hi += __shfl_xor_sync(0xffffffffu, fp.hi, o);
+    }
     if (lane == 0) {
         red[0][warp] = sum4;
         red[1][warp] = maxabs;
+        red[2][warp] = ratio;
+        fred[0][warp] = fp.lo;
+        fred[1][warp] = fp.hi;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double a = 0.0, m = 0.0;
+        double a = 0.0, m = 0.0, q = 0.0;
+        uint32_t fl = 0, fh = 0;
         for (int w = 0; w < 8; ++w) {
             a += red[0][w];
             m = fmax(m, red[1][w]);
+            q = fmax(q, red[2][w]);
+            fl += fred[0][w];
+            fh += fred[1][w];
         }
-        cta_stats[blockIdx.x * 2 + 0] = a;
-        cta_stats[blockIdx.x * 2 + 1] = m;
+        cta_stats[blockIdx.x * 3 + 0] = a;
+        cta_stats[blockIdx.x * 3 + 1] = m;
+        cta_stats[blockIdx.x * 3 + 2] = q;
+        // each half as a 64-bit addend (< 2^32): the sums stay exact, the
+        // verdict reads them mod 2^32
+        if (fp_out) {
+            if (fl) atomicAdd(fp_out, static_cast<unsigned long long>(fl));
+            if (fh) atomicAdd(fp_out + 1, static_cast<unsigned long long>(fh));
+        }
+    }
+}
+
+// Fold of the K1-rows CTA partials, fixed order: red[0] = sum d^4,
+// red[1] = max |d|, red[3] = max_i 2^e_i / r_i (int8 admission bound).
+__global__ void __launch_bounds__(32) k_shard_fold(const double* __restrict__ cta, int grid,
+                                                   double* __restrict__ red) {
+    const int lane = threadIdx.x;
+    double a = 0.0, m = 0.0, q = 0.0;
+    for (int b = lane; b < grid; b += 32) {  // lane-strided, then a fixed tree
+        a += cta[3 * b];
+        m = fmax(m, cta[3 * b + 1]);
+        q = fmax(q, cta[3 * b + 2]);
+    }
+    a = warp_sum(a);
+    m = warp_max(m);
+    q = warp_max(q);
+    if (lane == 0) {
+        red[0] = a;
+        red[1] = m;
+        red[3] = q;
+    }
+}
+
+// Grand mean terms over the full (all-gathered) row means in a fixed order
+// independent of the rank count: sums[0] = sum r_i, sums[1] = sum r_i^2.
+__global__ void __launch_bounds__(1024) k_rowmean_sums(const double* __restrict__ r, size_t n,
+                                                       double* __restrict__ sums) {
+    __shared__ double a[1024], b[1024];
+    double s = 0.0, s2 = 0.0;
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) {
+        s += r[i];
+        s2 += r[i] * r[i];
+    }
+    a[threadIdx.x] = s;
+    b[threadIdx.x] = s2;
+    __syncthreads();
+    for (int o = 512; o > 0; o >>= 1) {
+        if (static_cast<int>(threadIdx.x) < o) {
+            a[threadIdx.x] += a[threadIdx.x + o];
+            b[threadIdx.x] += b[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        sums[0] = a[0];
+        sums[1] = b[0];
     }
 }
 
@@ -120,56 +224,33 @@ __global__ void __launch_bounds__(256) k_asym_block(const T* __restrict__ a, siz
     if (tx == 0 && mx > 0.0) atomicMax(out, __double_as_longlong(mx));
 }
 
-// Order-independent 64-bit fingerprint of a block of D: sum over its entries
-// of a mix of (value bits, global row, global column), exact mod 2^64 (so
-// the result does not depend on the launch shape). With swap the positions
-// enter as (column, row): the fingerprint of a block equals that of the
-// transposed partner block iff (up to a 2^-64 collision) they are transposes.
-__device__ __forceinline__ unsigned long long fp_mix(unsigned long long v, unsigned long long i,
-                                                     unsigned long long j) {
-    unsigned long long x = v ^ (i * 0x9E3779B97F4A7C15ull) ^ (j * 0xC2B2AE3D27D4EB4Full);
-    x ^= x >> 31;
-    x *= 0x7FB5D329728EA185ull;
-    x ^= x >> 27;
-    x *= 0x81DADEF4BC2DD44Dull;
-    x ^= x >> 33;
-    return x;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) k_block_fingerprint(const T* __restrict__ d, size_t ld,
-                                                           size_t m, size_t col0, size_t ncols,
-                                                           size_t row0, int swap,
-                                                           unsigned long long* __restrict__ out) {
-    unsigned long long acc = 0;
-    const size_t total = m * ncols;
-    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t r = e / ncols, c = e % ncols;
-        const double v = static_cast<double>(d[r * ld + col0 + c]);
-        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
-        const unsigned long long gi = row0 + r, gj = col0 + c;
-        acc += swap ? fp_mix(bits, gj, gi) : fp_mix(bits, gi, gj);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
-}
-
 }  // namespace
 
 int k1_rows_grid(size_t rows, int sms) {
     return static_cast<int>(std::max<size_t>(1, std::min<size_t>((rows + 7) / 8, sms * 8)));
 }
 
-void launch_k1_rows(const void* d, DType dt, size_t ld, size_t rows, size_t cols, double* rowsum,
-                    double* cta_stats, int grid, cudaStream_t st, int* row_exp) {
+void launch_k1_rows(const void* d, DType dt, size_t ld, size_t rows, size_t cols, size_t row0,
+                    double* rowsum, double* row_mean, double* cta_stats, int grid,
+                    cudaStream_t st, int* row_exp, unsigned long long* sym_fp) {
     if (dt == DType::F64)
         k1_rows_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(d), ld, rows, cols,
-                                                     rowsum, cta_stats, row_exp);
+                                                     row0, rowsum, row_mean, cta_stats, row_exp,
+                                                     sym_fp);
     else
         k1_rows_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(d), ld, rows, cols,
-                                                    rowsum, cta_stats, row_exp);
+                                                    row0, rowsum, row_mean, cta_stats, row_exp,
+                                                    sym_fp);
+    count_launch();
+}
+
+void launch_shard_fold(const double* cta, int grid, double* red, cudaStream_t st) {
+    k_shard_fold<<<1, 32, 0, st>>>(cta, grid, red);
+    count_launch();
+}
+
+void launch_rowmean_sums(const double* row_mean, size_t n, double* sums, cudaStream_t st) {
+    k_rowmean_sums<<<1, 1024, 0, st>>>(row_mean, n, sums);
     count_launch();
 }
 
@@ -187,18 +268,5 @@ void launch_asym_block(const void* a, size_t lda, const void* b, size_t ldb, DTy
     count_launch();
 }
 
-void launch_block_fingerprint(const void* d, DType dt, size_t ld, size_t m, size_t col0,
-                              size_t ncols, size_t row0, bool swap, unsigned long long* out,
-                              int sms, cudaStream_t st) {
-    if (m == 0 || ncols == 0) return;
-    const int grid = static_cast<int>(std::min<size_t>((m * ncols + 255) / 256, sms * 8));
-    if (dt == DType::F64)
-        k_block_fingerprint<double><<<grid, 256, 0, st>>>(static_cast<const double*>(d), ld, m, col0,
-                                                          ncols, row0, swap ? 1 : 0, out);
-    else
-        k_block_fingerprint<float><<<grid, 256, 0, st>>>(static_cast<const float*>(d), ld, m, col0,
-                                                         ncols, row0, swap ? 1 : 0, out);
-    count_launch();
-}
 
 }  // namespace dsb

@@ -47,11 +47,19 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
                int* row_exp, double* scalars, int sms, cudaStream_t st);
 
 // ---- K1 for a row shard (rectangular rows x cols block): row sums of d^2,
-// sum d^4 and max |d| (deterministic per-CTA partials -> finalize on host)
+// sum d^4 and max |d| (deterministic per-CTA partials), plus the shard's
+// antisymmetric symmetry fingerprint (atomically added into *sym_fp; the
+// sum over all shards is zero iff D is exactly symmetric)
 int k1_rows_grid(size_t rows, int sms);
 // row_exp[r]: smallest e with d_rj^2 < 2^e over the row (int8 slice product)
-void launch_k1_rows(const void* d, DType dt, size_t ld, size_t rows, size_t cols, double* rowsum,
-                    double* cta_stats, int grid, cudaStream_t st, int* row_exp);
+void launch_k1_rows(const void* d, DType dt, size_t ld, size_t rows, size_t cols, size_t row0,
+                    double* rowsum, double* row_mean, double* cta_stats, int grid,
+                    cudaStream_t st, int* row_exp, unsigned long long* sym_fp);
+// fold of the K1-rows CTA partials (3 per CTA): red[0] sum d^4, red[1] max |d|,
+// red[3] int8 admission ratio
+void launch_shard_fold(const double* cta, int grid, double* red, cudaStream_t st);
+// sums[0] = sum r_i, sums[1] = sum r_i^2 over the full row means (fixed order)
+void launch_rowmean_sums(const double* row_mean, size_t n, double* sums, cudaStream_t st);
 // max |A[i][j] - B[j][i]| over an m x p block A (lda) and p x m block B (ldb),
 // atomically max-ed (non-negative doubles as u64) into *out
 void launch_asym_block(const void* a, size_t lda, const void* b, size_t ldb, DType dt, size_t m,
@@ -136,13 +144,6 @@ void launch_sw(const unsigned char* seq, const long long* off, const int* len, i
                long long n_a, long long n_b, long long npairs, int match, int mismatch, int gap,
                const SwPlan& p, unsigned short* dirs, int* hb, double* dout, size_t ld,
                long long* aux, cudaStream_t st);
-
-// out += order-independent fingerprint of the m x ncols block of a row shard
-// starting at column col0 (row0 = global index of its first row); swap: hash
-// positions as (column, row), the transposed partner's convention
-void launch_block_fingerprint(const void* d, DType dt, size_t ld, size_t m, size_t col0,
-                              size_t ncols, size_t row0, bool swap, unsigned long long* out,
-                              int sms, cudaStream_t st);
 
 // ---- panel kernels (n_pad x WP, k4-interleaved) -----------------------------
 int panel_grid(size_t n_pad, int sms);

@@ -1,14 +1,16 @@
 // Multi-GPU MDS path: D row-sharded over the ranks of one box
 // (one process per GPU), NCCL over NVLink only for the exchange steps.
 //
-//   gram   : K1 over the local rows (row sums / sum d^4 / max |d| — the
-//            reference's row means use full rows, mds.cpp:31-38, which a row
-//            shard has); the symmetry check exchanges the off-diagonal blocks
-//            pairwise (ring shift, send D[R_g, C_h], compare with the local
-//            D[R_g, C_h] transposed against the received D[R_h, C_g]); row
-//            means are all-gathered (every rank keeps the full r) and the
-//            scalars (grand mean, ||G||_F^2 closed form) are reduced in index
-//            order on the host, so they do not depend on the rank count.
+//   gram   : ONE pass over the local rows (row sums / sum d^4 / max |d| —
+//            the reference's row means use full rows, mds.cpp:31-38, which a
+//            row shard has — plus an antisymmetric fingerprint of the rows:
+//            summed over all ranks it is zero iff D is exactly symmetric, so
+//            one 64-bit all-reduce replaces a block exchange); only when it is
+//            nonzero are the off-diagonal blocks exchanged pairwise (ring
+//            shift) to measure max |d_ij - d_ji| against the reference's
+//            tolerance; row means are all-gathered (every rank keeps the full
+//            r) and the grand-mean sums run in one fixed order on the device,
+//            so they do not depend on the rank count. One host sync.
 //   solve  : the panel X (n x w) is replicated; each pass computes the local
 //            rows Y_g = G[R_g, :] X with K2, CholeskyQR all-reduces the w x w
 //            Gram, applies R^{-1} to the local rows and all-gathers the panel
@@ -118,56 +120,66 @@ Matrix gram_sharded(const Matrix& d) {
     Layout L = layout_of(n);
     const size_t m = s.rows, rb = s.row_begin;
     const size_t esz = s.dt == DType::F64 ? 8 : 4;
-    // ---- local row statistics
+    // ---- ONE pass over the local rows: row sums of d^2, row exponents, CTA
+    // partials of sum d^4 / max |d|, and the antisymmetric fingerprint whose
+    // sum over all ranks is zero iff D is exactly symmetric
     const int grid = k1_rows_grid(m, c.sms);
     auto row_mean = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * 8);  // full r
     double* rowsum = static_cast<double*>(c.scratch("sh_rowsum", std::max<size_t>(m, 1) * 8));
-    double* cta = static_cast<double*>(c.scratch("sh_cta", static_cast<size_t>(grid) * 2 * 8));
+    double* cta = static_cast<double*>(c.scratch("sh_cta", static_cast<size_t>(grid) * 3 * 8));
     auto row_exp = std::make_shared<DevBuf>(std::max<size_t>(m, 1) * sizeof(int));  // local rows
+    // red: [0] sum d^4, [1] max |d|, [2] max asym (bits), [3] int8 ratio,
+    //      [4] sum r, [5] sum r^2, [6..7] symmetry fingerprint halves (u64)
     double* red = static_cast<double*>(c.scratch("sh_red", 8 * 8));
+    auto* fp = reinterpret_cast<unsigned long long*>(red + 6);
     DSB_CUDA(cudaMemsetAsync(red, 0, 8 * 8, c.stream));
     cudaEvent_t e0, e1;
     c.make_events(&e0, &e1);
     if (e0) DSB_CUDA(cudaEventRecord(e0, c.stream));
-    if (m) launch_k1_rows(s.buf->p, s.dt, s.ld, m, n, rowsum, cta, grid, c.stream, row_exp->as<int>());
-    // ---- symmetry: local diagonal block, then ring-shift block exchange
-    launch_asym_block(static_cast<const char*>(s.buf->p) + rb * esz, s.ld,
-                      static_cast<const char*>(s.buf->p) + rb * esz, s.ld, s.dt, m, m, red + 2,
-                      c.stream);
-    // cross-rank blocks: fingerprints first (one pass over the local rows, a
-    // world x world all-gather); the exact block exchange only runs when some
-    // block pair differs, to report the exact max |d_ij - d_ji|
-    bool need_exchange = false;
-    if (L.world > 1) {
-        const int W = L.world;
-        auto* fp = static_cast<unsigned long long*>(
-            c.scratch("sh_fp", static_cast<size_t>(W) * W * sizeof(unsigned long long)));
-        DSB_CUDA(cudaMemsetAsync(fp, 0, static_cast<size_t>(W) * W * 8, c.stream));
-        unsigned long long* mine = fp + static_cast<size_t>(L.rank) * W;
-        for (int h = 0; h < W; ++h) {
-            if (h == L.rank) continue;
-            launch_block_fingerprint(s.buf->p, s.dt, s.ld, m, L.rb[h], L.re[h] - L.rb[h], rb,
-                                     L.rank > h, mine + h, c.sms, c.stream);
-        }
-        std::vector<size_t> cnt(W, static_cast<size_t>(W)), dsp(W);
-        for (int r = 0; r < W; ++r) dsp[r] = static_cast<size_t>(r) * W;
-        cm.allgatherv(reinterpret_cast<double*>(fp), cnt.data(), dsp.data(), c.stream);
-        std::vector<unsigned long long> hfp(static_cast<size_t>(W) * W);
-        c.d2h_copy(hfp.data(), fp, hfp.size() * 8);
-        for (int g = 0; g < W && !need_exchange; ++g)
-            for (int h = g + 1; h < W; ++h)
-                if (hfp[static_cast<size_t>(g) * W + h] != hfp[static_cast<size_t>(h) * W + g]) {
-                    need_exchange = true;
-                    break;
-                }
+    if (m) {
+        launch_k1_rows(s.buf->p, s.dt, s.ld, m, n, rb, rowsum, row_mean->as<double>() + rb, cta,
+                       grid, c.stream, row_exp->as<int>(), fp);
+        launch_shard_fold(cta, grid, red, c.stream);
     }
-    if (need_exchange) {
+    cm.allreduce_sum(red, 1, c.stream);
+    cm.allreduce_max(red + 1, 3, c.stream);
+    cm.allreduce_sum_u64(fp, 2, c.stream);
+    {
+        // row means: every rank keeps the full r
+        std::vector<size_t> cnt(L.world), off(L.world);
+        for (int r = 0; r < L.world; ++r) {
+            off[r] = L.rb[r];
+            cnt[r] = L.re[r] - L.rb[r];
+        }
+        cm.allgatherv(row_mean->as<double>(), cnt.data(), off.data(), c.stream);
+    }
+    // grand-mean terms in one fixed order over the full r (rank-count independent)
+    launch_rowmean_sums(row_mean->as<double>(), n, red + 4, c.stream);
+    if (e1) DSB_CUDA(cudaEventRecord(e1, c.stream));
+    c.add_timed(0, e0, e1);
+    double hred[8];
+    c.d2h_copy(hred, red, sizeof(hred));  // the one sync of the common case
+    const double maxabs = hred[1];
+    unsigned long long fp_sum[2];
+    std::memcpy(fp_sum, &hred[6], 16);
+    double maxasym = 0.0;
+    if (((fp_sum[0] | fp_sum[1]) & 0xFFFFFFFFull) != 0) {
+        // some mirrored pair differs: measure max |d_ij - d_ji| exactly (the
+        // reference's tolerance decides, mds.cpp:23-27) — local diagonal block,
+        // then a ring shift of the off-diagonal blocks
+        double* asym = static_cast<double*>(c.scratch("sh_asym", 64));
+        DSB_CUDA(cudaMemsetAsync(asym, 0, 64, c.stream));
+        launch_asym_block(static_cast<const char*>(s.buf->p) + rb * esz, s.ld,
+                          static_cast<const char*>(s.buf->p) + rb * esz, s.ld, s.dt, m, m, asym,
+                          c.stream);
         size_t maxm = 0;
         for (int r = 0; r < L.world; ++r) maxm = std::max(maxm, L.re[r] - L.rb[r]);
         // staging in f64 element units (f32 blocks travel as raw bytes)
         const size_t stage_elems = (maxm * maxm * esz + 7) / 8;
-        double* sbuf = static_cast<double*>(c.scratch("sh_send", stage_elems * 8 + 64));
-        double* rbuf = static_cast<double*>(c.scratch("sh_recv", stage_elems * 8 + 64));
+        double* sbuf =
+            L.world > 1 ? static_cast<double*>(c.scratch("sh_send", stage_elems * 8 + 64)) : nullptr;
+        double* rbuf =
+            L.world > 1 ? static_cast<double*>(c.scratch("sh_recv", stage_elems * 8 + 64)) : nullptr;
         for (int sft = 1; sft < L.world; ++sft) {
             const int ps = (L.rank + sft) % L.world, pr = (L.rank - sft + L.world) % L.world;
             const size_t ms = L.re[ps] - L.rb[ps], mr = L.re[pr] - L.rb[pr];
@@ -181,65 +193,12 @@ Matrix gram_sharded(const Matrix& d) {
                         c.stream);
             // received D[R_pr, C_g] (mr x m) vs local D[R_g, C_pr] (m x mr)
             launch_asym_block(static_cast<const char*>(s.buf->p) + L.rb[pr] * esz, s.ld, rbuf, m,
-                              s.dt, m, mr, red + 2, c.stream);
+                              s.dt, m, mr, asym, c.stream);
         }
-    }
-    // ---- scalars: sum d^4 (fixed-order partials), max |d|, max asym
-    {
-        // fold the CTA partials into red[0] (sum), red[1] (max) on the host
-        std::vector<double> h(static_cast<size_t>(grid) * 2);
-        if (m) {
-            DSB_CUDA(cudaMemcpyAsync(h.data(), cta, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
-            c.sync();
-        }
-        double sum4 = 0.0, mx = 0.0;
-        for (int b = 0; b < (m ? grid : 0); ++b) {
-            sum4 += h[b * 2];
-            mx = std::max(mx, h[b * 2 + 1]);
-        }
-        // dynamic-range bound of the int8 product: max_i 2^e_i / r_i (K1 rule)
-        double ratio = 0.0;
-        if (m) {
-            std::vector<double> rs(m);
-            std::vector<int> ex(m);
-            c.d2h_copy(rs.data(), rowsum, m * 8);
-            c.d2h_copy(ex.data(), row_exp->p, m * sizeof(int));
-            for (size_t i = 0; i < m; ++i) {
-                if (ex[i] <= -1100) continue;
-                const double r = rs[i] / static_cast<double>(n);
-                ratio = std::max(ratio, r > 0.0 ? std::ldexp(1.0, ex[i]) / r : 1e300);
-            }
-        }
-        double hv[2] = {sum4, mx};
-        DSB_CUDA(cudaMemcpyAsync(red, hv, 16, cudaMemcpyHostToDevice, c.stream));
-        DSB_CUDA(cudaMemcpyAsync(red + 3, &ratio, 8, cudaMemcpyHostToDevice, c.stream));
-        c.sync();
-    }
-    cm.allreduce_sum(red, 1, c.stream);
-    cm.allreduce_max(red + 1, 3, c.stream);
-    // ---- row means: local, then all-gathered
-    {
-        std::vector<double> hs(m);
-        if (m) c.d2h_copy(hs.data(), rowsum, m * 8);
-        for (double& v : hs) v /= static_cast<double>(n);
-        if (m) c.h2d_copy(row_mean->as<double>() + rb, hs.data(), m * 8);
-        std::vector<size_t> cnt(L.world), off(L.world);
-        for (int r = 0; r < L.world; ++r) {
-            off[r] = L.rb[r];
-            cnt[r] = L.re[r] - L.rb[r];
-        }
-        cm.allgatherv(row_mean->as<double>(), cnt.data(), off.data(), c.stream);
-    }
-    if (e1) DSB_CUDA(cudaEventRecord(e1, c.stream));
-    c.add_timed(0, e0, e1);
-    double hred[4];
-    c.d2h_copy(hred, red, 32);
-    const double maxabs = hred[1];
-    double maxasym = 0.0;
-    {
-        uint64_t bits;
-        std::memcpy(&bits, &hred[2], 8);
-        std::memcpy(&maxasym, &bits, 8);
+        cm.allreduce_max(asym, 1, c.stream);
+        uint64_t bits = 0;
+        c.d2h_copy(&bits, asym, 8);
+        std::memcpy(&maxasym, &bits, 8);  // non-negative doubles order as integers
     }
     if (maxasym > 1e-12 * std::max(1.0, maxabs))  // ref mds.cpp:23-27
         throw Error(errc::not_symmetric, "distance matrix values are not symmetric");
@@ -250,15 +209,9 @@ Matrix gram_sharded(const Matrix& d) {
     gi.n = n;
     gi.row_mean = row_mean;
     gi.row_exp = row_exp;  // this rank's rows
-    gi.row_mean_h.resize(n);
-    c.d2h_copy(gi.row_mean_h.data(), row_mean->p, n * 8);
-    // grand mean and ||G||_F^2 in index order on the host (rank-count independent)
-    double sr = 0.0, sr2 = 0.0;
-    for (size_t i = 0; i < n; ++i) {
-        sr += gi.row_mean_h[i];
-        sr2 += gi.row_mean_h[i] * gi.row_mean_h[i];
-    }
+    // the host copy of r is fetched on first use (matrix_get / _write)
     const double nf = static_cast<double>(n);
+    const double sr = hred[4], sr2 = hred[5];
     gi.sc[S_GRAND] = sr / nf;
     gi.sc[S_FRO2_LAZY] = 0.25 * (hred[0] - 2.0 * nf * sr2 + nf * nf * gi.sc[S_GRAND] * gi.sc[S_GRAND]);
     gi.sc[S_MAXABS] = maxabs;
@@ -268,8 +221,8 @@ Matrix gram_sharded(const Matrix& d) {
     gi.sc[S_SUMR2] = sr2;
     gi.sc[S_ROWRATIO] = hred[3];
     gi.scalars = std::make_shared<DevBuf>(S_COUNT * 8);
-    c.h2d_copy(gi.scalars->p, gi.sc, S_COUNT * 8);
-    c.sync();
+    // stream-ordered (the source, gi.sc, lives as long as the handle)
+    DSB_CUDA(cudaMemcpyAsync(gi.scalars->p, gi.sc, S_COUNT * 8, cudaMemcpyHostToDevice, c.stream));
     return g;
 }
 

@@ -40,3 +40,28 @@ def coords_match_up_to_sign(a, b):
         d = min(np.max(np.abs(a[:, c] - b[:, c])), np.max(np.abs(a[:, c] + b[:, c])))
         worst = max(worst, d)
     return worst
+
+
+def sym_fingerprint(rows, row0):
+    """numpy restatement of the sharded gram's antisymmetric symmetry
+    fingerprint (k1_shard.cu SymFp) over a block of full rows starting at
+    global row row0: two 32-bit sums over (i, j) of sgn(j - i) times a mix of
+    each half of bits(d_ij) with the unordered position {i, j}. Summed over
+    all shards (mod 2^32) both are 0 iff D is exactly symmetric.
+    Returns (lo, hi)."""
+    import numpy as np
+    m32 = np.uint64(0xFFFFFFFF)
+    v = np.ascontiguousarray(rows, dtype=np.float64).view(np.uint64)
+    vl, vh = v & m32, v >> np.uint64(32)
+    i = (np.arange(rows.shape[0], dtype=np.uint64) + np.uint64(row0))[:, None]
+    j = np.arange(rows.shape[1], dtype=np.uint64)[None, :]
+    lo_, hi_ = np.minimum(i, j), np.maximum(i, j)
+    key = (lo_ * np.uint64(0x9E3779B1) + hi_ * np.uint64(0x85EBCA77)) & m32
+    xl = (((vl ^ key) & m32) * np.uint64(0xC2B2AE3D)) & m32
+    xh = (((vh ^ key ^ np.uint64(0x165667B1)) & m32) * np.uint64(0x27D4EB2F)) & m32
+    out = []
+    for x in (xl, xh):
+        pos = int(np.sum(np.where(j > i, x, np.uint64(0)), dtype=np.uint64))
+        neg = int(np.sum(np.where(j < i, x, np.uint64(0)), dtype=np.uint64))
+        out.append((pos - neg) % 2**32)
+    return tuple(out)

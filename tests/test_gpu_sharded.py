@@ -96,49 +96,55 @@ def test_sharded_from_dvs_rows(ds, oracle, comm1, tmp_path):
     np.testing.assert_allclose(e.eigenvalues, ref.eigenvalues, rtol=1e-10)
 
 
-def _fp_np(block, row0, col0, swap):
-    """numpy restatement of fp_mix summed over a block (k1_shard.cu)."""
-    with np.errstate(over="ignore"):
-        v = np.ascontiguousarray(block, dtype=np.float64).view(np.uint64)
-        i = (np.arange(block.shape[0], dtype=np.uint64) + np.uint64(row0))[:, None]
-        j = (np.arange(block.shape[1], dtype=np.uint64) + np.uint64(col0))[None, :]
-        if swap:
-            i, j = j, i
-        x = v ^ (i * np.uint64(0x9E3779B97F4A7C15)) ^ (j * np.uint64(0xC2B2AE3D27D4EB4F))
-        x ^= x >> np.uint64(31)
-        x *= np.uint64(0x7FB5D329728EA185)
-        x ^= x >> np.uint64(27)
-        x *= np.uint64(0x81DADEF4BC2DD44D)
-        x ^= x >> np.uint64(33)
-        return int(np.sum(x, dtype=np.uint64))
-
-
-def test_block_fingerprints_pair_transposes(ds, oracle):
-    # the sharded symmetry check compares rank g's fingerprint of D[R_g, C_h]
-    # with rank h's swapped fingerprint of D[R_h, C_g] (sharded.cpp)
+def test_symmetry_fingerprint_matches_restatement(ds, oracle):
+    # the sharded gram decides symmetry from one all-reduced pair of 32-bit
+    # sums of per-shard antisymmetric fingerprints (k1_shard.cu, sharded.cpp)
     import ctypes as C
-    fn = ds.lib.divscope_debug_block_fingerprint
-    fn.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(C.c_uint64)]
+    from helpers import sym_fingerprint
+    fn = ds.lib.divscope_debug_sym_fingerprint
+    fn.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
 
-    def fp(m, c0, nc, swap):
-        out = C.c_uint64(0)
-        assert fn(m.handle, c0, nc, int(swap), C.byref(out)) == 0
-        return out.value
+    def fp(m):
+        out = (C.c_uint64 * 2)()
+        assert fn(m.handle, out) == 0
+        return (out[0], out[1])
+
+    def total(*parts):
+        return tuple(sum(p[k] for p in parts) % 2**32 for k in range(2))
 
     n = 700
     d = oracle.euclidean_matrix(ds.synth_points(2, n, 9))
     a = ds.matrix_from_host_rows(d[0:256], n, 0, 256)
     b = ds.matrix_from_host_rows(d[256:700], n, 256, 700)
-    fa, fb = fp(a, 256, 444, False), fp(b, 0, 256, True)
-    assert fa == fb == _fp_np(d[0:256, 256:700], 0, 256, False)
-    assert fb == _fp_np(d[256:700, 0:256], 256, 0, True)
+    fa, fb = fp(a), fp(b)
+    assert fa == sym_fingerprint(d[0:256], 0) and fb == sym_fingerprint(d[256:700], 256)
+    assert total(fa, fb) == (0, 0) and fa != (0, 0)
     d2 = d.copy()
     d2[300, 10] = np.nextafter(d2[300, 10], 1e9)  # one ulp off its mirror
     b2 = ds.matrix_from_host_rows(d2[256:700], n, 256, 700)
-    assert fp(b2, 0, 256, True) != fa
-    # f32 storage hashes the widened values
+    assert total(fa, fp(b2)) != (0, 0)
+    # f32 storage hashes the widened values; an unsharded handle covers all rows
     af = ds.matrix_from_host_rows_f32(d[0:256].astype(np.float32), n, 0, 256)
-    assert fp(af, 256, 444, False) == _fp_np(d[0:256, 256:700].astype(np.float32), 0, 256, False)
+    assert fp(af) == sym_fingerprint(d[0:256].astype(np.float32), 0)
+    assert fp(ds.matrix_from_host(d)) == (0, 0)
+
+
+def test_sharded_gram_tolerates_tiny_asymmetry(ds, oracle, comm1):
+    # a nonzero fingerprint triggers the exact max |d_ij - d_ji| measurement;
+    # the reference's 1e-12 * max(1, max|d|) tolerance decides (mds.cpp:23-27)
+    n = 500
+    d = oracle.euclidean_matrix(ds.synth_points(1, n, 4))
+    near = d.copy()
+    near[3, 7] = np.nextafter(near[3, 7], 1e9)
+    g = ds.gram(ds.matrix_from_host_rows(near, n, 0, n))
+    e = ds.embed(g, rank=5, oversampling=5, power_iters=1, seed=1)
+    ref = ds.embed(ds.gram(ds.matrix_from_host(d)), rank=5, oversampling=5, power_iters=1, seed=1)
+    np.testing.assert_allclose(e.eigenvalues, ref.eigenvalues, rtol=1e-10)
+    far = d.copy()
+    far[7, 3] += 1e-9 * d.max()
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.gram(ds.matrix_from_host_rows(far, n, 0, n))
+    assert ei.value.status == ds.Status.ERR_NOT_SYMMETRIC
 
 
 @pytest.mark.parametrize("rank,over,f32", [(60, 10, False), (100, 20, True)])

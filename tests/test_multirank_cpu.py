@@ -58,7 +58,21 @@ def _worker(rank, world, port, n, k, p, q, seed, out_q):
         dist.all_reduce(t)
         return t.numpy()
 
-    # gram (pass 0): local row sums, gathered row means, grand mean in index order
+    # gram (pass 0): symmetry from the all-reduced antisymmetric fingerprint
+    # of each rank's rows (k1_shard.cu), then local row sums, gathered row
+    # means, grand mean in index order
+    from helpers import sym_fingerprint
+
+    def fp_total(rows):
+        t = torch.tensor(sym_fingerprint(rows, rb), dtype=torch.int64)
+        dist.all_reduce(t)                          # the two 32-bit halves, summed
+        return tuple(int(x) % 2**32 for x in t)
+
+    sym_ok = fp_total(d)
+    bent = d.copy()
+    if rank == 0:
+        bent[3, n - 5] = np.nextafter(bent[3, n - 5], 1e9)  # mirror lives on rank 1
+    sym_bent = fp_total(bent)
     r_full = allgather_rows((d * d).sum(1) / n)
     grand = r_full.sum() / n
     omega = orc.fill_gaussian(seed, n * w).reshape(n, w)  # replicated panel
@@ -85,7 +99,7 @@ def _worker(rank, world, port, n, k, p, q, seed, out_q):
     order = sorted(range(w), key=lambda a: (-abs(lam[a]), -lam[a]))
     vals = lam[order][:k]
     if rank == 0:
-        out_q.put(vals.tolist())
+        out_q.put((vals.tolist(), sym_ok, sym_bent))
     dist.destroy_process_group()
 
 
@@ -111,7 +125,8 @@ def test_two_rank_decomposition_matches_oracle(oracle, ds):
              for r in range(2)]
     for pr in procs:
         pr.start()
-    vals = out_q.get(timeout=240)
+    vals, sym_ok, sym_bent = out_q.get(timeout=240)
+    assert sym_ok == (0, 0) and sym_bent != (0, 0)
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
