@@ -157,9 +157,11 @@ void launch_panel_to_rowmajor(const double* src, size_t n, int w, int wp, double
 void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_pad, int wp,
                     double* partial, double* colsums, int sms, cudaStream_t st,
                     double* pmax = nullptr, int nb = 0, int* col_exp = nullptr);
-// out (wp x wp) = A^T B (deterministic 2-level)
+// out (wp x wp) = A^T B (deterministic 2-level). gate (nullable): skip the
+// kernels unless gate[0] & 1 (the shift flag: a third CholeskyQR pass is only
+// needed after a shifted first pass)
 void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, double* partial,
-                      double* out, int sms, cudaStream_t st);
+                      double* out, int sms, cudaStream_t st, const int* gate = nullptr);
 // stable_rank power iteration, device side (ref rsvd.cpp:160-176): state =
 // {sigma, norm, done, zero, iters, active}; norm of Y column 0, v = w / norm,
 // convergence |norm - sigma| <= 1e-13 norm.
@@ -178,10 +180,10 @@ void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shi
 // rinv = R^{-1} with the shift (pass 0) / drop (later passes) rules; false
 // when WP is not supported (use launch_chol_inv)
 bool launch_chol_inv_elim(const double* w_mat, int wp, int w, size_t n, int pass, double* rinv,
-                          int* flags, cudaStream_t st);
-// q = y * rinv (row-wise, upper-triangular rinv)
+                          int* flags, cudaStream_t st, const int* gate = nullptr);
+// q = y * rinv (row-wise, upper-triangular rinv); gated off: q = y
 void launch_panel_apply(const double* y, const double* rinv, size_t n_pad, int wp, double* q,
-                        cudaStream_t st);
+                        cudaStream_t st, const int* gate = nullptr);
 
 // K3 fast path for wp <= 32: the three CholeskyQR passes y -> t -> y -> out
 // in one cooperative launch (returns false when not applicable / launch

@@ -364,7 +364,9 @@ template <int WP>
 __global__ void __launch_bounds__(256) k_chol_inv_elim(const double* __restrict__ wmat, int w,
                                                        double nrows, int pass,
                                                        double* __restrict__ rinv,
-                                                       int* __restrict__ flags) {
+                                                       int* __restrict__ flags,
+                                                       const int* __restrict__ gate) {
+    if (gate && !(gate[0] & 1)) return;
     __shared__ int dropped_s[WP];
     __shared__ double d0s[WP];
     __shared__ double dpiv[WP];
@@ -405,7 +407,10 @@ __global__ void __launch_bounds__(256) k_chol_inv_elim(const double* __restrict_
                                   dropped_s, dpiv, tri, tri_off))
             break;
         sigma = 11.0 * (nrows * w + static_cast<double>(w) * (w + 1)) * 0x1.0p-53 * tr_s[0];
-        if (tid == 0) flags[0] |= 1;
+        if (tid == 0) {
+            flags[0] |= 1;  // any shift in this solve (reported)
+            flags[1] = 1;   // this orthonormalization shifted: its third pass runs
+        }
         __syncthreads();
     }
     __syncthreads();
@@ -445,14 +450,14 @@ bool launch_orth_fused(double* y, double* t, double* out, size_t n_pad, int wp, 
 }
 
 bool launch_chol_inv_elim(const double* w_mat, int wp, int w, size_t n, int pass, double* rinv,
-                          int* flags, cudaStream_t st) {
+                          int* flags, cudaStream_t st, const int* gate) {
     const size_t smem = static_cast<size_t>(2) * wp * wp * sizeof(double);
     const double nr = static_cast<double>(n);
     switch (wp) {
 #define DSB_CE(W)                                                                              \
     case W:                                                                                    \
         allow_dyn_smem(reinterpret_cast<const void*>(k_chol_inv_elim<W>));                     \
-        k_chol_inv_elim<W><<<1, 256, smem, st>>>(w_mat, w, nr, pass, rinv, flags);             \
+        k_chol_inv_elim<W><<<1, 256, smem, st>>>(w_mat, w, nr, pass, rinv, flags, gate);      \
         break;
         DSB_CE(8) DSB_CE(16) DSB_CE(24) DSB_CE(32) DSB_CE(40) DSB_CE(48) DSB_CE(56) DSB_CE(64)
 #undef DSB_CE

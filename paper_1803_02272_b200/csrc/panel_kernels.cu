@@ -88,7 +88,9 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const double* __restrict
 // its 32 warps take fixed strided subsets of c, combined in warp order, so the
 // result is deterministic for a fixed P.
 __global__ void __launch_bounds__(1024) k_sum_partials(const double* __restrict__ partial, int P,
-                                                       int m, double* __restrict__ out) {
+                                                       int m, double* __restrict__ out,
+                                                       const int* __restrict__ gate = nullptr) {
+    if (gate && !(gate[0] & 1)) return;  // shift-gated third CholeskyQR pass
     __shared__ double sh[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * 32 + lane;
@@ -139,7 +141,9 @@ template <int WP>
 __global__ void __launch_bounds__(256) k_panel_dot_partial(const double* __restrict__ a,
                                                            const double* __restrict__ b,
                                                            size_t n_pad,
-                                                           double* __restrict__ partial) {
+                                                           double* __restrict__ partial,
+                                                           const int* __restrict__ gate) {
+    if (gate && !(gate[0] & 1)) return;
     constexpr int NF = WP / 8;
     constexpr int NT = NF * NF;
     constexpr int TPW = (NT + 7) / 8;  // tiles per warp
@@ -281,11 +285,19 @@ __global__ void __launch_bounds__(128) k_chol_inv(const double* __restrict__ wma
 template <int WP>
 __global__ void __launch_bounds__(256) k_panel_apply(const double* __restrict__ y,
                                                      const double* __restrict__ rinv,
-                                                     size_t n_pad, double* __restrict__ q) {
+                                                     size_t n_pad, double* __restrict__ q,
+                                                     const int* __restrict__ gate) {
+    const size_t nq = n_pad / 4;
+    if (gate && !(gate[0] & 1)) {
+        // gated-off pass: the panel passes through unchanged
+        for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < nq * WP;
+             e += static_cast<size_t>(gridDim.x) * blockDim.x)
+            reinterpret_cast<double4*>(q)[e] = reinterpret_cast<const double4*>(y)[e];
+        return;
+    }
     extern __shared__ double R[];  // [WP * WP]
     for (int e = threadIdx.x; e < WP * WP; e += blockDim.x) R[e] = rinv[e];
     __syncthreads();
-    const size_t nq = n_pad / 4;
     for (size_t item = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
          item < nq * WP; item += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const size_t qb = item / WP;
@@ -311,16 +323,16 @@ __global__ void __launch_bounds__(256) k_panel_apply(const double* __restrict__ 
 
 template <int WP>
 void panel_dot_wp(const double* a, const double* b, size_t n_pad, double* partial, int P,
-                  cudaStream_t st) {
-    k_panel_dot_partial<WP><<<P, 256, 0, st>>>(a, b, n_pad, partial);
+                  cudaStream_t st, const int* gate) {
+    k_panel_dot_partial<WP><<<P, 256, 0, st>>>(a, b, n_pad, partial, gate);
 }
 
 template <int WP>
 void panel_apply_wp(const double* y, const double* rinv, size_t n_pad, double* q, int grid,
-                    cudaStream_t st) {
+                    cudaStream_t st, const int* gate) {
     constexpr size_t smem = static_cast<size_t>(WP) * WP * sizeof(double);
     allow_dyn_smem(reinterpret_cast<const void*>(k_panel_apply<WP>));
-    k_panel_apply<WP><<<grid, 256, smem, st>>>(y, rinv, n_pad, q);
+    k_panel_apply<WP><<<grid, 256, smem, st>>>(y, rinv, n_pad, q, gate);
 }
 
 
@@ -450,12 +462,12 @@ void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_
 }
 
 void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, double* partial,
-                      double* out, int sms, cudaStream_t st) {
+                      double* out, int sms, cudaStream_t st, const int* gate) {
     const int P = panel_grid(n_pad, sms);
     switch (wp) {
 #define DSB_WP(W)                                         \
     case W:                                               \
-        panel_dot_wp<W>(a, b, n_pad, partial, P, st);     \
+        panel_dot_wp<W>(a, b, n_pad, partial, P, st, gate); \
         break;
         DSB_WP(8) DSB_WP(16) DSB_WP(24) DSB_WP(32) DSB_WP(40) DSB_WP(48) DSB_WP(56) DSB_WP(64)
         DSB_WP(72) DSB_WP(80) DSB_WP(88) DSB_WP(96) DSB_WP(104) DSB_WP(112) DSB_WP(120)
@@ -464,7 +476,7 @@ void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, do
         default:
             throw std::invalid_argument("unsupported panel width");
     }
-    k_sum_partials<<<(wp * wp + 31) / 32, 1024, 0, st>>>(partial, P, wp * wp, out);
+    k_sum_partials<<<(wp * wp + 31) / 32, 1024, 0, st>>>(partial, P, wp * wp, out, gate);
     count_launch(2);
 }
 
@@ -478,13 +490,13 @@ void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shi
 }
 
 void launch_panel_apply(const double* y, const double* rinv, size_t n_pad, int wp, double* q,
-                        cudaStream_t st) {
+                        cudaStream_t st, const int* gate) {
     const size_t items = n_pad / 4 * wp;
     const int grid = static_cast<int>(std::min<size_t>((items + 255) / 256, 148 * 8));
     switch (wp) {
 #define DSB_WP(W)                                               \
     case W:                                                     \
-        panel_apply_wp<W>(y, rinv, n_pad, q, grid, st);         \
+        panel_apply_wp<W>(y, rinv, n_pad, q, grid, st, gate);   \
         break;
         DSB_WP(8) DSB_WP(16) DSB_WP(24) DSB_WP(32) DSB_WP(40) DSB_WP(48) DSB_WP(56) DSB_WP(64)
         DSB_WP(72) DSB_WP(80) DSB_WP(88) DSB_WP(96) DSB_WP(104) DSB_WP(112) DSB_WP(120)

@@ -345,12 +345,19 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         double* t = t_full + lo;
         double* o = out_full + lo;
         double* bufs[3][2] = {{y, t}, {t, y}, {y, o}};
+        // CholQR2, or CholQR3 after a shifted first pass: the third pass's
+        // kernels are gated on the device-side shift flag (no host sync); its
+        // all-reduce runs either way so the ranks' collectives stay matched
+        const bool elim = wp <= 64;
+        DSB_CUDA(cudaMemsetAsync(flags + 1, 0, sizeof(int), c.stream));
         for (int ps = 0; ps < 3; ++ps) {
-            launch_panel_dot(bufs[ps][0], bufs[ps][0], m_pad, wp, psmall, wmat, c.sms, c.stream);
+            const int* gate = (ps == 2 && elim) ? flags + 1 : nullptr;
+            launch_panel_dot(bufs[ps][0], bufs[ps][0], m_pad, wp, psmall, wmat, c.sms, c.stream,
+                             gate);
             cm.allreduce_sum(wmat, static_cast<size_t>(wp) * wp, c.stream);
-            if (!launch_chol_inv_elim(wmat, wp, wi, n, ps, rinv, flags, c.stream))
+            if (!launch_chol_inv_elim(wmat, wp, wi, n, ps, rinv, flags, c.stream, gate))
                 launch_chol_inv(wmat, wp, wi, n, ps == 0 ? 1 : 0, rinv, flags, c.stream);
-            launch_panel_apply(bufs[ps][0], rinv, m_pad, wp, bufs[ps][1], c.stream);
+            launch_panel_apply(bufs[ps][0], rinv, m_pad, wp, bufs[ps][1], c.stream, gate);
         }
         cm.allgatherv(out_full, cnt.data(), off.data(), c.stream);
     };

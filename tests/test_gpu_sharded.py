@@ -163,3 +163,19 @@ def test_sharded_wide_panel_matches_unsharded(ds, comm1, product_path, rank, ove
     assert b.dims == a.dims
     np.testing.assert_allclose(b.eigenvalues[:30], a.eigenvalues[:30], rtol=1e-10)
     np.testing.assert_allclose(b.eigenvalues, a.eigenvalues, rtol=1e-6)
+
+
+def test_sharded_rank_deficient_panel_shifts(ds, oracle, comm1):
+    # 3-D points, w = 24: the panel is numerically rank 3, CholeskyQR shifts
+    # on its first pass and the shift-gated third pass runs (sharded.cpp
+    # orth_local); the kept spectrum must match the unsharded solve
+    rng = np.random.default_rng(11)
+    pts = rng.standard_normal((900, 3)) * 5.0
+    d = oracle.euclidean_matrix(pts)
+    a = ds.embed(ds.gram(ds.matrix_from_host(d)), rank=12, oversampling=12, power_iters=2, seed=4)
+    b = ds.embed(ds.gram(ds.matrix_from_host_rows(d, 900, 0, 900)), rank=12, oversampling=12,
+                 power_iters=2, seed=4)
+    assert ds.stats_get().last_orth_shifted == 1
+    assert a.dims == b.dims == 3
+    np.testing.assert_allclose(b.eigenvalues, a.eigenvalues, rtol=1e-10)
+    assert coords_match_up_to_sign(b.coords, a.coords) < 1e-8 * np.sqrt(a.eigenvalues[0])
