@@ -216,6 +216,14 @@ __device__ __forceinline__ long long cta_of(long long t, long long total, long l
 //   mode 1: y = -1/2 (y - r_i s_c - t_c + g s_c)   (rank-3 centering)
 //   mode 0: y as is.
 // Rows >= n are written as zero. Output in the k4-interleaved panel layout.
+// rows of a product row block reduced per CTA (DSB_REDUCE_ROWS; measured at
+// C2: 32 and 16 ~10 us, 8 and 128 slower)
+#ifndef DSB_REDUCE_ROWS
+#define DSB_REDUCE_ROWS 32
+#endif
+constexpr int kReduceRows = DSB_REDUCE_ROWS;
+constexpr int reduce_rows(int bm) { return kReduceRows < bm ? kReduceRows : bm; }
+
 template <int WP, int BM>
 __global__ void __launch_bounds__(256)
     k2_reduce(const double* __restrict__ part, int maxseg, int nk, long long total, int P, int n,
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(256)
               const double* __restrict__ colsums, double* __restrict__ y,
               const int* __restrict__ skip) {
     if (skip && *skip) return;
-    constexpr int kRows = 32;  // rows of the BM-row block handled by this CTA
+    constexpr int kRows = kReduceRows < BM ? kReduceRows : BM;  // rows of the block per CTA
     constexpr int kMaxSlots = 256;  // >= grid + 1 (a row block spans <= grid CTAs)
     __shared__ long long slot_base[kMaxSlots];
     const int b = blockIdx.x / (BM / kRows);
@@ -239,11 +247,19 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     const double g = mode ? scalars[S_GRAND] : 0.0;
+#pragma unroll 4
     for (int e = threadIdx.x; e < kRows * WP; e += blockDim.x) {
         const int r = r0 + e / WP, col = e % WP;
         const int eo = r * WP + col;
+        // the first slots' loads are issued together, then summed in CTA order
+        double p4[4];
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl) p4[sl] = sl < nslot ? part[slot_base[sl] + eo] : 0.0;
         double v = 0.0;
-        for (int sl = 0; sl < nslot; ++sl) v += part[slot_base[sl] + eo];
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl)
+            if (sl < nslot) v += p4[sl];
+        for (int sl = 4; sl < nslot; ++sl) v += part[slot_base[sl] + eo];
         const size_t i = static_cast<size_t>(b) * BM + r;
         if (i >= static_cast<size_t>(n)) {
             v = 0.0;
@@ -295,7 +311,7 @@ void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
             run_product<WP, float, false, CW>(tmap, p, x, part, st, skip);
     }
     if (e1) cudaEventRecord(e1, st);
-    k2_reduce<WP, bm_of<CW>()><<<p.nb * (bm_of<CW>() / 32), 256, 0, st>>>(
+    k2_reduce<WP, bm_of<CW>()><<<p.nb * (bm_of<CW>() / reduce_rows(bm_of<CW>())), 256, 0, st>>>(
         part, p.maxseg, p.nk, p.total, p.grid, p.n, mode, row_mean, scalars, colsums, y, skip);
 }
 
@@ -308,7 +324,8 @@ void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, lo
     switch (wp * 1000 + bm) {
 #define DSB_RED(W, B)                                                                          \
     case W * 1000 + B:                                                                         \
-        k2_reduce<W, B><<<nb * (B / 32), 256, 0, st>>>(part, maxseg, nk, total, P, n, mode,   \
+        k2_reduce<W, B><<<nb * (B / reduce_rows(B)), 256, 0, st>>>(part, maxseg, nk, total, P, \
+                                                                   n, mode,                    \
                                                        row_mean, scalars, colsums, y, skip);   \
         break;
         DSB_RED(8, 128) DSB_RED(16, 128) DSB_RED(24, 128) DSB_RED(32, 128) DSB_RED(40, 128)
