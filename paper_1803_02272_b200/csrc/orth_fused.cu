@@ -31,6 +31,9 @@ namespace {
 constexpr double kShiftTrigF = 1e-10;  // same rules as k_chol_inv
 long long* g_orth_prof = nullptr;      // debug: per-phase cycle counts of CTA 0
 constexpr double kDropTolF = 1e-20;
+#ifndef DSB_ORTH_FAST_RCP
+#define DSB_ORTH_FAST_RCP 1
+#endif
 
 // CTA-wide elimination W = L D L^T (A in shared memory, upper triangle used)
 // that also carries E = L^{-1} along (Gauss-Jordan style, same steps), so the
@@ -70,7 +73,20 @@ __device__ bool cta_chol_inverse(double* __restrict__ A, double* __restrict__ E,
             dropped_s[k] = drop;
             dpiv[k] = drop ? 0.0 : p;
         }
-        const double invp = drop ? 0.0 : 1.0 / p;  // 0 for a dropped column: no elimination
+        // 0 for a dropped column: no elimination with it. The reciprocal is
+        // the MUFU seed + two Newton steps (<= 1 ulp): the IEEE division's
+        // slow-path check sits on this loop's critical path
+        double invp = 0.0;
+        if (!drop) {
+#if DSB_ORTH_FAST_RCP
+            double r;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+            r = fma(r, fma(-p, r, 1.0), r);
+            invp = fma(r, fma(-p, r, 1.0), r);
+#else
+            invp = 1.0 / p;
+#endif
+        }
         const double* rowk = A + k * WP;
         // trailing upper triangle {(i, j): k < i <= j}: a suffix of `tri`
         const int t0 = tri_off[k + 1], t1 = tri_off[WP];
