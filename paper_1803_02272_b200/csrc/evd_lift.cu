@@ -325,6 +325,9 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
     }
 }
 
+// rows of the panel staged per chunk by k_lift (<= 64 KB of shared memory)
+__host__ __device__ constexpr int lift_chunk_rows(int wp) { return wp <= 64 ? 128 : 64; }
+
 // U = Q V_keep (n x r, row-major into coords). CTA c owns rows
 // [n c / P, n (c+1) / P); thread t owns column t % r and rows t / r + k * (256 / r),
 // keeping a running (value at max |u|, first index) that is merged in thread
@@ -334,30 +337,44 @@ __global__ void __launch_bounds__(256) k_lift(const double* __restrict__ q, int 
                                               const int* __restrict__ imeta, int rmax,
                                               double* __restrict__ coords,
                                               double* __restrict__ partial, long long row_off) {
-    extern __shared__ double sv[];  // [w][rmax]
+    extern __shared__ double sm_lift[];
+    double* sv = sm_lift;             // [w][rmax]
+    double* sq = sm_lift + w * rmax;  // staged panel rows (4-row groups)
     __shared__ double best_v[256];
     __shared__ int best_i[256];
     const int r = imeta[1];
     if (r == 0) return;
     for (int e = threadIdx.x; e < w * rmax; e += blockDim.x) sv[e] = vkeep[e];
-    __syncthreads();
     const int row0 = static_cast<int>(static_cast<long long>(n) * blockIdx.x / gridDim.x);
     const int row1 = static_cast<int>(static_cast<long long>(n) * (blockIdx.x + 1) / gridDim.x);
     const int per = 256 / r;  // rows in flight per sweep (r <= 128)
     const int t = threadIdx.x;
+    const int ch = lift_chunk_rows(wp);
     double bv = 0.0;
     int bi = -1;
-    if (t < per * r) {
-        const int c = t % r;
-        for (int i = row0 + t / r; i < row1; i += per) {
-            double s = 0.0;
-            for (int k = 0; k < w; ++k) s += q[pidx(i, k, wp)] * sv[k * rmax + c];
-            coords[static_cast<size_t>(i) * r + c] = s;
-            if (bi < 0 || fabs(s) > fabs(bv)) {
-                bv = s;
-                bi = i;
+    // the CTA's panel rows are staged chunk by chunk with coalesced copies
+    // (their interleaved 4-row groups are contiguous), then every thread's
+    // w-term dot products read shared memory
+    for (int a = row0; a < row1; a += ch) {
+        const int b = min(row1, a + ch);
+        const int g0 = a / 4, g1 = (b + 3) / 4;
+        const size_t base = static_cast<size_t>(g0) * wp * 4;
+        for (int e = threadIdx.x; e < (g1 - g0) * wp * 4; e += blockDim.x) sq[e] = q[base + e];
+        __syncthreads();
+        if (t < per * r) {
+            const int c = t % r;
+            for (int i = a + t / r; i < b; i += per) {
+                const double* qi = sq + static_cast<size_t>(i / 4 - g0) * wp * 4 + (i & 3);
+                double s = 0.0;
+                for (int k = 0; k < w; ++k) s += qi[k * 4] * sv[k * rmax + c];
+                coords[static_cast<size_t>(i) * r + c] = s;
+                if (bi < 0 || fabs(s) > fabs(bv)) {
+                    bv = s;
+                    bi = i;
+                }
             }
         }
+        __syncthreads();
     }
     best_v[t] = bv;
     best_i[t] = bi;
@@ -459,7 +476,9 @@ int lift_grid(size_t n, int sms) {
 void launch_lift_partial(const double* q, size_t n, int wp, int w, const double* vkeep,
                          const int* imeta, int rmax, double* coords, double* partial,
                          long long row_off, int P, cudaStream_t st) {
-    const size_t smem = static_cast<size_t>(w) * rmax * sizeof(double);
+    const size_t smem =
+        (static_cast<size_t>(w) * rmax +
+         static_cast<size_t>(lift_chunk_rows(wp) / 4 + 2) * wp * 4) * sizeof(double);
     allow_dyn_smem(reinterpret_cast<const void*>(k_lift));
     k_lift<<<P, 256, smem, st>>>(q, static_cast<int>(n), wp, w, vkeep, imeta, rmax, coords,
                                  partial, row_off);
