@@ -314,9 +314,12 @@ def b200_arm(args, wl):
         groups = max(int(st.last_product_groups), 1)
         roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": gbs / hbm_peak, "traffic": traffic,
-                    "kernel": "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)",
+                    "kernel": ("k2i_product (3x7-digit int8 slice product of the exact Hamming "
+                               "h^2, tcgen05 kind::i8)" if int(st.last_product_sdigits) == 3 else
+                               "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)"),
                     "peak_source": hbm["peak_source"],
                     "column_groups": groups,
+                    "s_slices": int(st.last_product_sdigits),
                     "streamed_gbs": gbs * groups if groups > 1 else gbs,
                     "fp64_equiv": {"achieved": tflops, "unit": "TFLOP/s",
                                    "fp64_dmma_peak": fp64_peak}, **common}

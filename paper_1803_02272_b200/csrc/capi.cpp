@@ -733,6 +733,7 @@ void divscope_stats_get(divscope_stats* out) {
         out->last_power_iters = c.last_power_iters;
         out->last_product_kernel = c.last_product_kernel;
         out->last_product_groups = c.last_product_groups;
+        out->last_product_sdigits = c.last_product_sdigits;
     } catch (...) {
     }
 }

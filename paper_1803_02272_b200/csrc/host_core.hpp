@@ -128,6 +128,7 @@ public:
     int last_evd_sweeps = 0, last_orth_shifted = 0, last_power_iters = 0;
     int last_product_kernel = 0;  // 0 fp64 DMMA, 1 int8 slice product
     int last_product_groups = 1;  // int8 column groups (reads of D per pass)
+    int last_product_sdigits = 0;  // int8 S slices per element (7, or 3 for Hamming D)
     std::vector<TimedPair> pending;
     std::vector<cudaEvent_t> event_pool;
     void begin_timed(int kind, cudaEvent_t* a);
@@ -171,6 +172,10 @@ struct Store {
     bool symmetric = false;
     DType dt = DType::F64;
     std::shared_ptr<DevBuf> buf;
+    // > 0: every value is fl(h / hamming_len) for an integer 0 <= h <=
+    // hamming_len (the Hamming builder, K7); the int8 product then slices the
+    // exact S = h^2 / L^2 into three bytes instead of seven
+    int hamming_len = 0;
     // cached TMA descriptor for the K2 streaming read
     bool tmap_ok = false;
     CUtensorMap tmap128{}, tmap256{};  // box heights of the two K2 tile shapes

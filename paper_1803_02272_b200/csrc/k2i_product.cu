@@ -123,7 +123,7 @@ constexpr bool kWarpIssue = DSB_K2I_WARP_ISSUE != 0;
 #ifndef DSB_TS_BPROD_NA
 #define DSB_TS_BPROD_NA 1
 #endif
-template <int NB>
+template <int NB, int SD = kDig>
 constexpr bool bprod_ts();
 
 
@@ -135,13 +135,16 @@ constexpr bool bprod_ts();
 // 5..7 — whose MMAs are narrow (N' <= 192) and so pay the shared-memory
 // A floor anyway — from shared memory. Two stages let the conversion of the
 // next k-step proceed while the MMAs of the current one run.
-template <int NB>
+// SD: digits of S per element — 7 (56-bit fixed point of d^2 per row) or 3
+// (Hamming distances: d = h / L with integer h, S = h^2 / L^2 exactly, h^2 <
+// 2^24 in three bytes; see launch_k2i)
+template <int NB, int SD = kDig>
 constexpr bool hybrid_ts() {
-    return NB > 32 && DSB_TS_NB64_HYBRID;
+    return NB > 32 && SD > 4 && DSB_TS_NB64_HYBRID;
 }
-template <int NB>
+template <int NB, int SD = kDig>
 constexpr int tmem_digits_ts() {
-    return hybrid_ts<NB>() ? 4 : kDig;
+    return hybrid_ts<NB, SD>() ? 4 : SD;
 }
 // NB = 32: four 64-column A stages after the 224 accumulator columns (a
 // fifth 56-column stage fits — DSB_TS_NA32=5 DSB_TS_ACOLS32=56
@@ -149,9 +152,9 @@ constexpr int tmem_digits_ts() {
 #ifndef DSB_TS_NA32
 #define DSB_TS_NA32 4
 #endif
-template <int NB>
+template <int NB, int SD = kDig>
 constexpr int a_stages_ts() {
-    return NB <= 32 ? DSB_TS_NA32 : (hybrid_ts<NB>() ? 2 : 1);
+    return NB <= 32 ? DSB_TS_NA32 : ((hybrid_ts<NB, SD>() || 16 * SD <= 64) ? 2 : 1);
 }
 #ifndef DSB_TS_ACOLS32
 #define DSB_TS_ACOLS32 64
@@ -159,37 +162,38 @@ constexpr int a_stages_ts() {
 #ifndef DSB_TS_ABASE32
 #define DSB_TS_ABASE32 256
 #endif
-template <int NB>
+template <int NB, int SD = kDig>
 constexpr uint32_t a_stage_cols_ts() {
-    return hybrid_ts<NB>() ? 32u : (NB <= 32 ? DSB_TS_ACOLS32 : 64u);
+    return SD != kDig ? 8u * SD
+                      : (hybrid_ts<NB, SD>() ? 32u : (NB <= 32 ? DSB_TS_ACOLS32 : 64u));
 }
 template <int NB>
 constexpr uint32_t a_base_ts() {  // first TMEM column of the A stages
     return NB <= 32 ? DSB_TS_ABASE32 : 448u;
 }
-template <int NB>
+template <int NB, int SD = kDig>
 constexpr int a_smem_stage_ts() {  // bytes of shared-memory A digits per stage
-    return (kDig - tmem_digits_ts<NB>()) * kRowsI8 * kKStep;
+    return (SD - tmem_digits_ts<NB, SD>()) * kRowsI8 * kKStep;
 }
-template <int NB>
+template <int NB, int SD = kDig>
 constexpr int b_stages_ts() {
-    return bprod_ts<NB>() ? kBStagesTs : a_stages_ts<NB>();
+    return bprod_ts<NB, SD>() ? kBStagesTs : a_stages_ts<NB, SD>();
 }
-template <int NB>
+template <int NB, int SD>
 constexpr bool bprod_ts() {
-    return a_stages_ts<NB>() <= DSB_TS_BPROD_NA;
+    return a_stages_ts<NB, SD>() <= DSB_TS_BPROD_NA;
 }
-template <int NB, typename TD>
+template <int NB, typename TD, int SD = kDig>
 constexpr int d_stages_ts() {
-    return std::min(8, (DSB_TS_SMEM_KB * 1024 - b_stages_ts<NB>() * b_bytes<NB>() -
-                        a_stages_ts<NB>() * a_smem_stage_ts<NB>()) /
+    return std::min(8, (DSB_TS_SMEM_KB * 1024 - b_stages_ts<NB, SD>() * b_bytes<NB>() -
+                        a_stages_ts<NB, SD>() * a_smem_stage_ts<NB, SD>()) /
                            d_bytes<TD>());
 }
-template <int NB, typename TD>
+template <int NB, typename TD, int SD = kDig>
 constexpr size_t ts_smem() {
-    return 1024 + static_cast<size_t>(d_stages_ts<NB, TD>()) * d_bytes<TD>() +
-           b_stages_ts<NB>() * b_bytes<NB>() + a_stages_ts<NB>() * a_smem_stage_ts<NB>() + 448 +
-           NB * 8;
+    return 1024 + static_cast<size_t>(d_stages_ts<NB, TD, SD>()) * d_bytes<TD>() +
+           b_stages_ts<NB, SD>() * b_bytes<NB>() +
+           a_stages_ts<NB, SD>() * a_smem_stage_ts<NB, SD>() + 448 + NB * 8;
 }
 
 // 8 consecutive d values of row `row`, columns c0..c0+7 of the k-step tile
@@ -247,25 +251,26 @@ __device__ __forceinline__ void pack_digits(const uint32_t (&lo)[8], const uint3
     }
 }
 
-template <int NB, typename TD>
+template <int NB, typename TD, int SD>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
                    const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
                    int nks, int total, double* __restrict__ part, int maxseg, int wp, int cg0,
-                   const int* __restrict__ skip, int dbg) {
+                   const int* __restrict__ skip, int dbg, double hlen) {
     if (skip && *skip) return;
-    constexpr int ND = d_stages_ts<NB, TD>();
-    constexpr int NA = a_stages_ts<NB>();
+    static_assert(SD == kDig || SD == 3, "S digit counts: 7 (general) or 3 (Hamming)");
+    constexpr int ND = d_stages_ts<NB, TD, SD>();
+    constexpr int NA = a_stages_ts<NB, SD>();
     // panel digits: with several A stages they ride with the A stage (loaded
     // by one converter lane when it claims the stage); with a single A stage
     // they get their own ring filled ahead by the producer
-    constexpr bool kBProd = bprod_ts<NB>();
+    constexpr bool kBProd = bprod_ts<NB, SD>();
     constexpr int NBR = kBProd ? kBStagesTs : NA;
     constexpr int DB = d_bytes<TD>();
     constexpr int BB = b_bytes<NB>();
-    constexpr int TD_DIG = tmem_digits_ts<NB>();  // digits 1..TD_DIG in TMEM
-    constexpr int ASB = a_smem_stage_ts<NB>();     // the rest in shared memory
-    constexpr uint32_t ACOLS = a_stage_cols_ts<NB>();
+    constexpr int TD_DIG = tmem_digits_ts<NB, SD>();  // digits 1..TD_DIG in TMEM
+    constexpr int ASB = a_smem_stage_ts<NB, SD>();     // the rest in shared memory
+    constexpr uint32_t ACOLS = a_stage_cols_ts<NB, SD>();
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 const uint32_t asm_base = smem_u32(aring + sa * ASB);
                 if (dbg != 2) {
 #pragma unroll
-                    for (int t = 1; t <= kDig; ++t) {
+                    for (int t = 1; t <= SD; ++t) {
                         constexpr int per = 256 / NB;
                         const int umax = 8 - t;
 #pragma unroll
@@ -445,7 +450,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         int sd = 0, sa = 0, k = 0, nflush = 0;
         uint32_t pd = 0, pa = 0;
         for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
-            if (w.rb != cur_rb) {
+            if (SD == kDig && w.rb != cur_rb) {
                 cur_rb = w.rb;
                 const int grow = w.rb * kRowsI8 + row;
                 const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
@@ -468,19 +473,44 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 if (dbg != 1) {
                     double d[8];
                     load8<TD>(dring + sd * DB, row, c0, d);
-                    uint32_t lo[8], hi[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);
-                        lo[j] = static_cast<uint32_t>(m);
-                        hi[j] = static_cast<uint32_t>(m >> 32);
-                    }
                     const uint32_t ta = tmem_a + static_cast<uint32_t>(sa) * ACOLS + lane_off;
                     unsigned char* as = aring + sa * ASB + umma_tile_off(row, c0);
-                    uint32_t wd[kDig][2];
-                    pack_digits(lo, hi, wd);
+                    uint32_t wd[SD][2];
+                    if constexpr (SD == kDig) {
+                        uint32_t lo[8], hi[8];
 #pragma unroll
-                    for (int t = 1; t <= kDig; ++t) {
+                        for (int j = 0; j < 8; ++j) {
+                            const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);
+                            lo[j] = static_cast<uint32_t>(m);
+                            hi[j] = static_cast<uint32_t>(m >> 32);
+                        }
+                        pack_digits(lo, hi, wd);
+                    } else {
+                        // Hamming: h = L d exactly (d = fl(h / L), h <= L < 2^12),
+                        // S' = h^2 < 2^24 in three bytes, high first
+                        uint32_t s2[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const uint32_t h = static_cast<uint32_t>(__double2int_rn(d[j] * hlen));
+                            s2[j] = h * h;
+                        }
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+                            const int e = 4 * g;
+                            // plane t: byte j = byte (3 - t) of element 4 g + j
+                            const uint32_t h01 = __byte_perm(s2[e], s2[e + 1], 0x0062);
+                            const uint32_t h23 = __byte_perm(s2[e + 2], s2[e + 3], 0x0062);
+                            const uint32_t m01 = __byte_perm(s2[e], s2[e + 1], 0x0051);
+                            const uint32_t m23 = __byte_perm(s2[e + 2], s2[e + 3], 0x0051);
+                            const uint32_t l01 = __byte_perm(s2[e], s2[e + 1], 0x0040);
+                            const uint32_t l23 = __byte_perm(s2[e + 2], s2[e + 3], 0x0040);
+                            wd[0][g] = __byte_perm(h01, h23, 0x5410);
+                            wd[1][g] = __byte_perm(m01, m23, 0x5410);
+                            wd[2][g] = __byte_perm(l01, l23, 0x5410);
+                        }
+                    }
+#pragma unroll
+                    for (int t = 1; t <= SD; ++t) {
                         const uint32_t w0 = wd[t - 1][0], w1 = wd[t - 1][1];
                         if (t <= TD_DIG)
                             tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2), w0, w1);
@@ -489,7 +519,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                                 make_uint2(w0, w1);
                     }
                     tmem_st_wait();
-                    if constexpr (TD_DIG < kDig) fence_proxy_async();
+                    if constexpr (TD_DIG < SD) fence_proxy_async();
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -545,8 +575,13 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 mbar_wait(acc_full, static_cast<uint32_t>(nflush & 1));
                 tc_fence_after();
                 const int grow = w.rb * kRowsI8 + row;
-                const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
-                const double rscale = e > kExpZeroI8 ? ldexp(1.0, e) : 0.0;
+                double rscale;
+                if constexpr (SD == kDig) {
+                    const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
+                    rscale = e > kExpZeroI8 ? ldexp(1.0, e) : 0.0;
+                } else {
+                    rscale = grow < nrows ? 0x1.0p24 / (hlen * hlen) : 0.0;  // S = S' 2^-24 * this
+                }
                 double* prow = part +
                                (static_cast<size_t>(cta) * maxseg + w.seg) * kRowsI8 * wp +
                                static_cast<size_t>(row) * wp;
@@ -641,19 +676,20 @@ int k2i_debug_mode() {
     return m;
 }
 
-template <int NB, typename TD>
+template <int NB, typename TD, int SD = kDig>
 void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
             const int* row_exp, const int* col_exp, double* part, int cg0, cudaStream_t st,
-            const int* skip) {
+            const int* skip, double hlen = 0.0) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k2i_product_ts<NB, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(ts_smem<NB, TD>()));
+        cudaFuncSetAttribute(k2i_product_ts<NB, TD, SD>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(ts_smem<NB, TD, SD>()));
         attr = true;
     }
-    k2i_product_ts<NB, TD><<<p.grid, kThreadsI8, ts_smem<NB, TD>(), st>>>(
+    k2i_product_ts<NB, TD, SD><<<p.grid, kThreadsI8, ts_smem<NB, TD, SD>(), st>>>(
         *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
-        p.maxseg, wp, cg0, skip, k2i_debug_mode());
+        p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen);
 }
 
 }  // namespace
@@ -694,7 +730,7 @@ void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, 
                 size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
                 unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
                 const double* colsums, double* y, size_t y_rows_pad, cudaStream_t st,
-                cudaEvent_t e0, cudaEvent_t e1, const int* skip) {
+                cudaEvent_t e0, cudaEvent_t e1, const int* skip, int hamming_len) {
     // k2_reduce writes the 128-row blocks; the panel rows beyond them (up to
     // the 256-row padding) must read as zero, whatever an earlier, larger
     // solve left in this workspace
@@ -712,7 +748,15 @@ void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, 
             k_panel_digits<<<grid, 256, 0, st>>>(x, p.nks, wp, nb, cg0, col_exp, bdig);
         }
         if (g == 0 && e0) cudaEventRecord(e0, st);
-        if (dt == DType::F64) {
+        if (dt == DType::F64 && hamming_len > 0) {
+            const double hl = static_cast<double>(hamming_len);
+            if (nb == 32)
+                run_i8<32, double, 3>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip,
+                                      hl);
+            else
+                run_i8<64, double, 3>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip,
+                                      hl);
+        } else if (dt == DType::F64) {
             if (nb == 32)
                 run_i8<32, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
             else

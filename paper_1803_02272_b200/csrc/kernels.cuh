@@ -116,7 +116,7 @@ void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, 
                 size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
                 unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
                 const double* colsums, double* y, size_t y_rows_pad, cudaStream_t st,
-                cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr, const int* skip = nullptr);
+                cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr, const int* skip = nullptr, int hamming_len = 0);
 
 // out[0] = sum of `count` doubles in a fixed order
 void launch_sum_fixed(const double* partial, size_t count, double* out, cudaStream_t st);

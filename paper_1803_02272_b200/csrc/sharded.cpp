@@ -295,6 +295,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
     }
     c.last_product_kernel = use_i8 ? 1 : 0;
+    c.last_product_sdigits = use_i8 ? 7 : 0;
     c.last_product_groups = use_i8 ? iplan.ngroups : 1;
     const size_t pbytes = n_pad * wp * 8;
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));

@@ -118,6 +118,16 @@ const double* omega_host(uint64_t seed, size_t n, size_t w) {
 // finite. DSB_K2_INT8=0 forces the fp64 kernel (parity comparisons).
 std::atomic<int> g_product_path{-1};  // -1: not yet read from DSB_K2_INT8
 
+// DSB_K2I_HAMMING=0 keeps Hamming matrices on the general 7-byte slices
+// (parity comparisons)
+bool hamming_slices_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DSB_K2I_HAMMING");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 int product_path() {
     int m = g_product_path.load();
     if (m < 0) {
@@ -206,6 +216,13 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
     }
     c.last_product_groups = use_i8 ? iplan.ngroups : 1;
+    // Hamming distances (K7): three exact S bytes per element (h^2 < 2^24)
+    const int hamming_i8 =
+        (use_i8 && s.dt == DType::F64 && s.hamming_len > 0 && s.hamming_len < 4096 &&
+         hamming_slices_enabled())
+            ? s.hamming_len
+            : 0;
+    c.last_product_sdigits = use_i8 ? (hamming_i8 ? 3 : 7) : 0;
     const size_t pbytes = n_pad * wp * sizeof(double);
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
     double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));
@@ -284,7 +301,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         if (use_i8)
             launch_k2i(s.tmap_for(128), s.dt, iplan, wp, x, n_pad, g.gram->row_exp->as<int>(), pmax,
                        col_exp, bdig, part, row_mean, scal_dev, colsums, y, n_pad, c.stream, e0,
-                       e1);
+                       e1, nullptr, hamming_i8);
         else
             launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums,
                       y, n_pad, c.stream, e0, e1);
@@ -740,6 +757,7 @@ Matrix matrix_hamming(const char* reads, size_t count, size_t length) {
     const auto packed = pack_reads(reads, count, length, words);
     Matrix m;
     m.store = make_store(count, count, true, DType::F64);
+    m.store->hamming_len = static_cast<int>(length);
     DevBuf dp(packed.size() * 8);
     c.h2d_copy(dp.p, packed.data(), packed.size() * 8);
     launch_hamming(dp.as<unsigned long long>(), count, words, static_cast<int>(length),

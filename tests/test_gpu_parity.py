@@ -610,3 +610,30 @@ def test_handles_shared_across_threads(ds):
         assert np.array_equal(vals, want.eigenvalues)
         assert np.array_equal(coords, want.coords)
         assert np.array_equal(sh, want.coords)  # first-access download raced by 6 threads
+
+
+@pytest.mark.parametrize("n,rank,over", [(1500, 10, 10), (2200, 30, 20)])
+def test_int8_hamming_slices_match_fp64_and_oracle(ds, oracle, n, rank, over):
+    # Hamming D (K7) on the int8 path slices the exact S = h^2 / L^2 into
+    # three bytes (k2i_product.cu, SD = 3); NB = 32 and NB = 64 groups
+    reads = ds.synth_reads(n, 400, 20, 0.05, n % 13)
+    d = ds.matrix_hamming(reads)
+    g = ds.gram(d)
+    ds.set_product_path(2)
+    try:
+        e8 = ds.embed(g, rank=rank, oversampling=over, power_iters=2, seed=7)
+        st = ds.stats_get()
+        assert (st.last_product_kernel, st.last_product_sdigits) == (1, 3)
+        ds.set_product_path(1)
+        e64 = ds.embed(g, rank=rank, oversampling=over, power_iters=2, seed=7)
+    finally:
+        ds.set_product_path(0)
+    assert e8.dims == e64.dims
+    top = min(e8.dims, 15)
+    np.testing.assert_allclose(e8.eigenvalues[:top], e64.eigenvalues[:top], rtol=1e-10)
+    dm = d.to_numpy()
+    st_, rm, grand = oracle.gram_stats(dm)
+    want = oracle.embed(rank, over, 2, 7, d=dm, row_mean=rm, grand=grand)
+    np.testing.assert_allclose(e8.eigenvalues[:top], want["eigenvalues"][:top], rtol=1e-10)
+    assert coords_match_up_to_sign(e8.coords[:, :top], want["coords"][:, :top]) < \
+        1e-7 * np.sqrt(want["eigenvalues"][0])
