@@ -222,16 +222,21 @@ def b200_arm(args, wl):
 
     # ---- inputs: D built on the device (K9), host copy for the e2e leg
     rb, re_ = ds.shard_range(n, world, rank) if sharded else (0, n)
+    reads_host = None
     if cfg == 5:
+        # C5's input is the reads: D is built on the GPU by K7 (a row shard
+        # per rank); the e2e leg uploads the reads, not a 20 GB matrix
         reads = ds.synth_reads(n, 400, 50, 0.05, seed)
-        D = ds.matrix_hamming(reads)
-        if sharded:
-            D = ds.matrix_from_host_rows(D.to_numpy()[rb:re_], n, rb, re_)
+        reads_host = torch.empty((n, 400), dtype=torch.uint8, pin_memory=True)
+        reads_host.numpy()[...] = np.frombuffer(b"".join(reads), np.uint8).reshape(n, 400)
+        del reads
+        D = ds.matrix_hamming_rows(reads_host.numpy(), rb, re_) if sharded else \
+            ds.matrix_hamming(reads_host.numpy())
     else:
         pts = ds.synth_points(cfg, n, seed)
         D = ds.matrix_euclidean_rows(pts, rb, re_, store_f32=f32) if sharded else \
             ds.matrix_euclidean(pts, store_f32=f32)
-    if not args.no_e2e:
+    if not args.no_e2e and cfg != 5:
         d_host = torch.empty((re_ - rb, n), dtype=torch.float32 if f32 else torch.float64,
                              pin_memory=True)
         d_np = d_host.numpy()
@@ -246,6 +251,12 @@ def b200_arm(args, wl):
         return e
 
     def step_e2e():
+        if cfg == 5:
+            rh = reads_host.numpy()
+            m = ds.matrix_hamming_rows(rh, rb, re_) if sharded else ds.matrix_hamming(rh)
+            g = ds.gram(m)
+            e = ds.embed(g, rank=k, oversampling=p, power_iters=q, seed=seed)
+            return e.coords
         if sharded:
             m = (ds.matrix_from_host_rows_f32 if f32 else ds.matrix_from_host_rows)(
                 d_np, n, rb, re_)

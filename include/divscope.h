@@ -282,6 +282,11 @@ divscope_status divscope_matrix_from_host_rows(const double* rows, size_t n, siz
 divscope_status divscope_matrix_from_host_rows_f32(const float* rows, size_t n, size_t row_begin,
                                                    size_t row_end, int symmetric,
                                                    divscope_matrix** out);
+/* This rank's rows [row_begin, row_end) of the Hamming distance matrix of
+ * all `count` reads (K7 row shard; same values as divscope_matrix_hamming). */
+divscope_status divscope_matrix_hamming_rows(const char* reads, size_t count, size_t length,
+                                            size_t row_begin, size_t row_end,
+                                            divscope_matrix** out);
 /* This rank's rows of the exact Euclidean distance matrix of all n points. */
 divscope_status divscope_matrix_euclidean_rows(const double* points, size_t n, size_t dim,
                                                int store_f32, size_t row_begin, size_t row_end,

@@ -28,7 +28,7 @@ import numpy as np
 __all__ = [
     "Status", "DivscopeError", "SolverOptions", "Matrix", "Embedding", "Stats", "lib",
     "matrix_from_host", "matrix_from_host_f32", "matrix_read", "matrix_euclidean",
-    "matrix_hamming", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
+    "matrix_hamming", "matrix_hamming_rows", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
     "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
     "stats_enable_timing", "stats_reset", "set_product_path", "matrix_read_rows", "reconstruction_error", "Scoring", "Alignment",
     "align", "distance", "pairwise_self", "pairwise_cross", "stats_get", "set_device", "LIB_PATH",
@@ -158,6 +158,7 @@ def _load() -> C.CDLL:
         "divscope_matrix_from_host_rows": ([_dp, _sz, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
         "divscope_matrix_from_host_rows_f32": ([_fp, _sz, _sz, _sz, C.c_int, C.POINTER(_vp)], _st),
         "divscope_matrix_euclidean_rows": ([_dp, _sz, _sz, C.c_int, _sz, _sz, C.POINTER(_vp)], _st),
+        "divscope_matrix_hamming_rows": ([C.c_char_p, _sz, _sz, _sz, _sz, C.POINTER(_vp)], _st),
         "divscope_stats_enable_timing": ([C.c_int], None),
         "divscope_set_product_path": ([C.c_int], C.c_int),
         "divscope_stats_reset": ([], None),
@@ -312,6 +313,11 @@ def matrix_euclidean(points: np.ndarray, store_f32: bool = False) -> Matrix:
 def _reads_bytes(reads) -> tuple[bytes, int, int]:
     if isinstance(reads, (bytes, bytearray)):
         raise TypeError("pass a list of equal-length reads")
+    if isinstance(reads, np.ndarray):
+        # count x length uint8 array (e.g. pinned host memory): passed in place
+        if reads.dtype != np.uint8 or reads.ndim != 2 or not reads.flags["C_CONTIGUOUS"]:
+            raise TypeError("reads array must be C-contiguous uint8, count x length")
+        return reads.ctypes.data_as(C.c_char_p), reads.shape[0], reads.shape[1]
     reads = [r.encode() if isinstance(r, str) else bytes(r) for r in reads]
     if not reads:
         return b"", 0, 0
@@ -324,6 +330,12 @@ def _reads_bytes(reads) -> tuple[bytes, int, int]:
 def matrix_hamming(reads: Sequence[str | bytes]) -> Matrix:
     buf, count, length = _reads_bytes(reads)
     return _new_matrix(lib.divscope_matrix_hamming, buf, count, length)
+
+
+def matrix_hamming_rows(reads: Sequence[str | bytes], row_begin: int, row_end: int) -> Matrix:
+    """NEW divscope_matrix_hamming_rows: this rank's rows of the Hamming D (K7)."""
+    buf, count, length = _reads_bytes(reads)
+    return _new_matrix(lib.divscope_matrix_hamming_rows, buf, count, length, row_begin, row_end)
 
 
 def hamming_counts(reads: Sequence[str | bytes]) -> np.ndarray:

@@ -386,6 +386,16 @@ divscope_status divscope_matrix_hamming(const char* reads, size_t count, size_t 
     });
 }
 
+divscope_status divscope_matrix_hamming_rows(const char* reads, size_t count, size_t length,
+                                            size_t row_begin, size_t row_end,
+                                            divscope_matrix** out) {
+    if (!reads || !out) return fail_invalid("null argument");
+    return wrap([&] {
+        dsb::Matrix m = dsb::matrix_hamming_rows(reads, count, length, row_begin, row_end);
+        *out = new divscope_matrix{std::move(m)};
+    });
+}
+
 divscope_status divscope_hamming_counts(const char* reads, size_t count, size_t length,
                                         uint32_t* out) {
     if (!reads || !out) return fail_invalid("null argument");

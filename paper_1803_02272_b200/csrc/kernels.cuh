@@ -229,8 +229,18 @@ void launch_euclid(const double* pts, size_t n, int dim, void* d, DType dt, size
 // rows [row0, row0 + nrows) of the n x n matrix into d (row-major, local rows)
 void launch_euclid_rows(const double* pts, size_t n, int dim, void* d, DType dt, size_t ld,
                         size_t row0, size_t nrows, cudaStream_t st);
-void launch_hamming(const unsigned long long* packed, size_t count, int words, int length,
-                    double* d, size_t ld, uint32_t* counts, cudaStream_t st);
+// reads (count x length bytes, device) -> two bit planes lo/hi (count x words
+// uint32 each, 32 bases per word); *bad = smallest linear index of a non-ACGT
+// byte (preset to ~0)
+void launch_pack_reads(const unsigned char* reads, size_t count, int length, int words,
+                       uint32_t* lo, uint32_t* hi, unsigned long long* bad, int sms,
+                       cudaStream_t st);
+// K7: rows [row0, row0 + nrows) of the Hamming matrix from the bit planes:
+// d (f64, D = h / L, leading dimension ld) and/or counts (u32, n x n);
+// the full matrix is built from its upper-triangle tiles
+void launch_hamming(const uint32_t* lo, const uint32_t* hi, size_t count, int words, int length,
+                    double* d, size_t ld, uint32_t* counts, cudaStream_t st, size_t row0 = 0,
+                    size_t nrows = static_cast<size_t>(-1));
 
 // ---- misc ------------------------------------------------------------------
 // Opt a kernel into the full shared-memory carve-out once (dynamic limit =

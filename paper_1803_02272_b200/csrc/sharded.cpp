@@ -295,7 +295,12 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
     }
     c.last_product_kernel = use_i8 ? 1 : 0;
-    c.last_product_sdigits = use_i8 ? 7 : 0;
+    // Hamming shards (divscope_matrix_hamming_rows): three exact S bytes
+    const int hamming_i8 = (use_i8 && s.dt == DType::F64 && s.hamming_len > 0 &&
+                            s.hamming_len < 4096 && hamming_slices_enabled())
+                               ? s.hamming_len
+                               : 0;
+    c.last_product_sdigits = use_i8 ? (hamming_i8 ? 3 : 7) : 0;
     c.last_product_groups = use_i8 ? iplan.ngroups : 1;
     const size_t pbytes = n_pad * wp * 8;
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
@@ -335,7 +340,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         if (use_i8)
             launch_k2i(s.tmap_for(128), s.dt, iplan, wp, x_full, n_pad, g.gram->row_exp->as<int>(),
                        pmax, col_exp, bdig, part, r_full + rb, scal, colsums, y_full + lo, m_pad,
-                       c.stream, e0, e1);
+                       c.stream, e0, e1, nullptr, hamming_i8);
         else if (m)
             launch_k2(s.tmap_for(plan.bm), s.dt, 1, plan, x_full, part, r_full + rb, scal, colsums,
                       y_full + lo, m_pad, c.stream, e0, e1);

@@ -118,16 +118,6 @@ const double* omega_host(uint64_t seed, size_t n, size_t w) {
 // finite. DSB_K2_INT8=0 forces the fp64 kernel (parity comparisons).
 std::atomic<int> g_product_path{-1};  // -1: not yet read from DSB_K2_INT8
 
-// DSB_K2I_HAMMING=0 keeps Hamming matrices on the general 7-byte slices
-// (parity comparisons)
-bool hamming_slices_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("DSB_K2I_HAMMING");
-        return !(e && std::atoi(e) == 0);
-    }();
-    return on;
-}
-
 int product_path() {
     int m = g_product_path.load();
     if (m < 0) {
@@ -141,6 +131,16 @@ int product_path() {
 }
 
 }  // namespace
+
+// DSB_K2I_HAMMING=0 keeps Hamming matrices on the general 7-byte slices
+// (parity comparisons)
+bool hamming_slices_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DSB_K2I_HAMMING");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
 
 void set_product_path(int mode) { g_product_path.store(mode); }
 
@@ -726,27 +726,31 @@ Matrix matrix_euclidean(const double* pts, size_t n, size_t dim, bool f32) {
 }
 
 namespace {
-std::vector<unsigned long long> pack_reads(const char* reads, size_t count, size_t length,
-                                           int& words) {
+// Reads -> the two bit planes of K7 on the device: one host->device copy of
+// the bytes (count x length), packing and validation in a kernel. Errors as
+// a host scan would report them: the first non-A/C/G/T byte in read-major
+// order. Returns lo planes at [0, count * words), hi planes after them.
+std::shared_ptr<DevBuf> pack_reads_device(const char* reads, size_t count, size_t length,
+                                          int& words) {
+    Ctx& c = Ctx::get();
     if (count == 0 || length == 0) throw Error(errc::empty_input, "no reads");
     words = static_cast<int>((length + 31) / 32);
-    std::vector<unsigned long long> packed(count * words, 0ull);
-    for (size_t i = 0; i < count; ++i)
-        for (size_t t = 0; t < length; ++t) {
-            unsigned long long code;
-            switch (reads[i * length + t]) {
-                case 'A': code = 0; break;
-                case 'C': code = 1; break;
-                case 'G': code = 2; break;
-                case 'T': code = 3; break;
-                default:
-                    throw Error(errc::invalid_character,
-                                "read " + std::to_string(i) + ": base " + std::to_string(t + 1) +
-                                    " is not A/C/G/T");
-            }
-            packed[i * words + t / 32] |= code << (2 * (t % 32));
-        }
-    return packed;
+    DevBuf raw(count * length);
+    c.h2d_copy(raw.p, reads, count * length);
+    auto planes = std::make_shared<DevBuf>(2 * count * static_cast<size_t>(words) * 4);
+    auto* bad = static_cast<unsigned long long*>(c.scratch("pack_bad", 8));
+    DSB_CUDA(cudaMemsetAsync(bad, 0xff, 8, c.stream));
+    uint32_t* lo = planes->as<uint32_t>();
+    launch_pack_reads(raw.as<unsigned char>(), count, static_cast<int>(length), words, lo,
+                      lo + count * static_cast<size_t>(words), bad, c.sms, c.stream);
+    unsigned long long first = ~0ull;
+    c.d2h_copy(&first, bad, 8);
+    if (first != ~0ull) {
+        const size_t i = static_cast<size_t>(first / length), t = static_cast<size_t>(first % length);
+        throw Error(errc::invalid_character, "read " + std::to_string(i) + ": base " +
+                                                 std::to_string(t + 1) + " is not A/C/G/T");
+    }
+    return planes;
 }
 }  // namespace
 
@@ -754,14 +758,37 @@ Matrix matrix_hamming(const char* reads, size_t count, size_t length) {
     Ctx& c = Ctx::get();
     std::lock_guard<std::recursive_mutex> lk(c.mu);
     int words = 0;
-    const auto packed = pack_reads(reads, count, length, words);
+    const auto packed = pack_reads_device(reads, count, length, words);
     Matrix m;
     m.store = make_store(count, count, true, DType::F64);
     m.store->hamming_len = static_cast<int>(length);
-    DevBuf dp(packed.size() * 8);
-    c.h2d_copy(dp.p, packed.data(), packed.size() * 8);
-    launch_hamming(dp.as<unsigned long long>(), count, words, static_cast<int>(length),
+    launch_hamming(packed->as<uint32_t>(), packed->as<uint32_t>() + count * static_cast<size_t>(words),
+                   count, words, static_cast<int>(length),
                    m.store->buf->as<double>(), m.store->ld, nullptr, c.stream);
+    c.sync();
+    return m;
+}
+
+// rows [row_begin, row_end) of the Hamming matrix as a row shard (K7 shards
+// by output rows with no communication)
+Matrix matrix_hamming_rows(const char* reads, size_t count, size_t length, size_t row_begin,
+                           size_t row_end) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    if (row_end < row_begin || row_end > count)
+        throw Error(errc::invalid_argument, "bad row range");
+    int words = 0;
+    const auto packed = pack_reads_device(reads, count, length, words);
+    Matrix m;
+    m.store = make_store(row_end - row_begin, count, true, DType::F64);
+    m.store->sharded = true;
+    m.store->n_global = count;
+    m.store->row_begin = row_begin;
+    m.store->hamming_len = static_cast<int>(length);
+    launch_hamming(packed->as<uint32_t>(), packed->as<uint32_t>() + count * static_cast<size_t>(words),
+                   count, words, static_cast<int>(length),
+                   m.store->buf->as<double>(), m.store->ld, nullptr, c.stream, row_begin,
+                   row_end - row_begin);
     c.sync();
     return m;
 }
@@ -770,12 +797,11 @@ void hamming_counts(const char* reads, size_t count, size_t length, uint32_t* ou
     Ctx& c = Ctx::get();
     std::lock_guard<std::recursive_mutex> lk(c.mu);
     int words = 0;
-    const auto packed = pack_reads(reads, count, length, words);
-    DevBuf dp(packed.size() * 8);
+    const auto packed = pack_reads_device(reads, count, length, words);
     DevBuf dc(count * count * sizeof(uint32_t));
-    c.h2d_copy(dp.p, packed.data(), packed.size() * 8);
-    launch_hamming(dp.as<unsigned long long>(), count, words, static_cast<int>(length), nullptr, 0,
-                   dc.as<uint32_t>(), c.stream);
+    launch_hamming(packed->as<uint32_t>(), packed->as<uint32_t>() + count * static_cast<size_t>(words),
+                   count, words, static_cast<int>(length),
+                   nullptr, 0, dc.as<uint32_t>(), c.stream);
     c.d2h_copy(out, dc.p, count * count * sizeof(uint32_t));
 }
 

@@ -72,6 +72,7 @@ double reconstruction_error(const Matrix& g, const Embedding& e);
 // whenever supported (lazy grams, w <= 64)
 void set_product_path(int mode);
 // whether a product pass on this gram uses the int8 slice product
+bool hamming_slices_enabled();  // DSB_K2I_HAMMING (default on)
 bool use_int8_product(const GramInfo& gi, int wp);
 
 // G_ij of a handle (lazy gram evaluated like ref mds.cpp:50-58)
@@ -117,6 +118,8 @@ Embedding embed_sharded(const Matrix& g, size_t rank, SolverOptions opts);
 Spectrum eigs_sharded(const Matrix& g, const SolverOptions& opts);
 Matrix matrix_euclidean(const double* pts, size_t n, size_t dim, bool f32);
 Matrix matrix_hamming(const char* reads, size_t count, size_t length);
+Matrix matrix_hamming_rows(const char* reads, size_t count, size_t length, size_t row_begin,
+                           size_t row_end);
 void hamming_counts(const char* reads, size_t count, size_t length, uint32_t* out);
 
 }  // namespace dsb

@@ -179,3 +179,21 @@ def test_sharded_rank_deficient_panel_shifts(ds, oracle, comm1):
     assert a.dims == b.dims == 3
     np.testing.assert_allclose(b.eigenvalues, a.eigenvalues, rtol=1e-10)
     assert coords_match_up_to_sign(b.coords, a.coords) < 1e-8 * np.sqrt(a.eigenvalues[0])
+
+
+def test_hamming_rows_shard_matches_full(ds, comm1):
+    # K7 row shards (divscope_matrix_hamming_rows) keep the Hamming tag, so the
+    # sharded int8 product slices S in three bytes like the full matrix
+    reads = ds.synth_reads(700, 400, 9, 0.05, 3)
+    full = ds.matrix_hamming(reads)
+    rows = ds.matrix_hamming_rows(np.frombuffer(b"".join(reads), np.uint8).reshape(700, 400),
+                                  0, 700)
+    assert np.array_equal(rows.to_numpy(), full.to_numpy())
+    part = ds.matrix_hamming_rows(reads, 256, 700)
+    assert np.array_equal(part.to_numpy(), full.to_numpy()[256:700])
+    a = ds.embed(ds.gram(full), rank=8, oversampling=8, power_iters=2, seed=2)
+    b = ds.embed(ds.gram(rows), rank=8, oversampling=8, power_iters=2, seed=2)
+    np.testing.assert_allclose(b.eigenvalues, a.eigenvalues, rtol=1e-10)
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.matrix_hamming_rows([b"ACGT", b"ACGN"], 0, 2)
+    assert ei.value.status == ds.Status.ERR_INVALID_CHARACTER
