@@ -637,3 +637,24 @@ def test_int8_hamming_slices_match_fp64_and_oracle(ds, oracle, n, rank, over):
     np.testing.assert_allclose(e8.eigenvalues[:top], want["eigenvalues"][:top], rtol=1e-10)
     assert coords_match_up_to_sign(e8.coords[:, :top], want["coords"][:, :top]) < \
         1e-7 * np.sqrt(want["eigenvalues"][0])
+
+
+def test_hamming_builder_row_bands_and_errors(ds, oracle):
+    # K7 full (upper-triangle tiles + mirror) and arbitrary row bands against
+    # the oracle's popcount restatement; device-side validation reports the
+    # first non-ACGT byte in read-major order
+    reads = ds.synth_reads(333, 150, 7, 0.1, 9)
+    st, want = oracle.hamming_counts(b"".join(reads), 333, 150)
+    assert st == 0
+    assert np.array_equal(ds.hamming_counts(reads), want)
+    full = ds.matrix_hamming(reads).to_numpy()
+    assert np.array_equal(full, want / 150.0)
+    band = ds.matrix_hamming_rows(reads, 100, 301).to_numpy()
+    assert np.array_equal(band, (want / 150.0)[100:301])
+    bad = [bytearray(r) for r in reads]
+    bad[200][17] = ord("N")
+    bad[201][3] = ord("x")
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.matrix_hamming([bytes(r) for r in bad])
+    assert ei.value.status == ds.Status.ERR_INVALID_CHARACTER
+    assert "read 200" in ei.value.message and "base 18" in ei.value.message
