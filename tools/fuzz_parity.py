@@ -13,8 +13,11 @@ from oracle_bindings import Oracle
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+sharded = len(sys.argv) > 3 and sys.argv[3] == "sharded"  # single-rank NCCL, row-shard handles
 orc = Oracle()
 ds.set_device(0)
+if sharded:
+    ds.comm_init(1, 0, ds.comm_unique_id())
 bad = 0
 for c in range(cases):
     cfg = int(rng.integers(1, 5))
@@ -31,7 +34,11 @@ for c in range(cases):
         d = d.astype(np.float32).astype(np.float64)
     ds.set_product_path(path)
     try:
-        m = ds.matrix_from_host_f32(d.astype(np.float32)) if f32 else ds.matrix_from_host(d)
+        if sharded:
+            m = ds.matrix_from_host_rows_f32(d.astype(np.float32), n, 0, n) if f32 else \
+                ds.matrix_from_host_rows(d, n, 0, n)
+        else:
+            m = ds.matrix_from_host_f32(d.astype(np.float32)) if f32 else ds.matrix_from_host(d)
         e = ds.embed(ds.gram(m), rank=rank, oversampling=over, power_iters=q, seed=seed)
         kern = ds.stats_get().last_product_kernel
     finally:
@@ -48,5 +55,5 @@ for c in range(cases):
     print(f"{'ok ' if ok else 'BAD'} cfg={cfg} n={n} rank={rank} p={over} q={q} f32={f32} "
           f"path={path} kernel={kern} dims={e.dims}/{want['r']} eig={ev:.1e} coords={co:.1e}",
           flush=True)
-print(f"{cases - bad}/{cases} cases within tolerance")
+print(f"{cases - bad}/{cases} cases within tolerance{' (sharded path)' if sharded else ''}")
 sys.exit(1 if bad else 0)
