@@ -1,7 +1,10 @@
 // K1 for a row shard of D (multi-GPU pass 0): a warp streams one full row at
 // a time (16-byte loads, 8 in flight per lane), giving the row sum of d^2 in a
-// fixed order, plus per-CTA sum d^4 / max |d|; and the cross-shard symmetry
-// check max |d_ij - d_ji| on exchanged blocks (ref src/mds.cpp:21-41).
+// fixed order, the row mean and int8 row exponent, per-CTA sum d^4 / max |d|
+// / admission ratio, and the shard's antisymmetric symmetry fingerprint
+// (SymFp below) — one read of the shard. The exact max |d_ij - d_ji| on
+// exchanged blocks (k_asym_block) runs only when the all-reduced fingerprint
+// is nonzero (ref src/mds.cpp:21-41).
 #include <algorithm>
 
 #include "device_utils.cuh"
