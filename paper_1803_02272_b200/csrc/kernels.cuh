@@ -179,8 +179,13 @@ void launch_chol_inv(const double* w_mat, int wp, int w, size_t n, int allow_shi
 // the fused kernel's L D L^T elimination (carrying L^{-1}) as one CTA, WP <= 64:
 // rinv = R^{-1} with the shift (pass 0) / drop (later passes) rules; false
 // when WP is not supported (use launch_chol_inv)
+// With y (apply mode): q = y R^{-1} on the panel rows as well, one CTA per
+// SM each computing the factor (rinv, nullable, written once); false when the
+// rows per CTA do not fit shared memory (use the factor + apply kernels).
 bool launch_chol_inv_elim(const double* w_mat, int wp, int w, size_t n, int pass, double* rinv,
-                          int* flags, cudaStream_t st, const int* gate = nullptr);
+                          int* flags, cudaStream_t st, const int* gate = nullptr,
+                          const double* y = nullptr, double* q = nullptr, size_t n_pad = 0,
+                          int sms = 0);
 // q = y * rinv (row-wise, upper-triangular rinv); gated off: q = y
 void launch_panel_apply(const double* y, const double* rinv, size_t n_pad, int wp, double* q,
                         cudaStream_t st, const int* gate = nullptr);

@@ -374,25 +374,43 @@ bool launch_wp(double* y, double* out, size_t n_pad, int w, size_t n, double* pa
                                        dim3(256), args, smem, st) == cudaSuccess;
 }
 
-// Single-CTA W -> T = R^{-1} for the multi-kernel / sharded CholeskyQR
-// (same elimination and pivot rules as the fused kernel's step 3 and 4a).
+// W -> T = R^{-1} for the multi-kernel / sharded CholeskyQR (same
+// elimination and pivot rules as the fused kernel's step 3 and 4a). With y
+// (apply mode, one CTA per SM) every CTA computes the identical T and applies
+// it to its own 4-row groups of the panel, q = y T, staged through shared
+// memory (loaded while the factor is computed) — one launch instead of the
+// factor kernel plus an apply kernel; CTA 0 writes rinv (nullable) and the
+// flags. Gated off (third pass after an unshifted first one): q = y.
 template <int WP>
 __global__ void __launch_bounds__(256) k_chol_inv_elim(const double* __restrict__ wmat, int w,
                                                        double nrows, int pass,
                                                        double* __restrict__ rinv,
                                                        int* __restrict__ flags,
-                                                       const int* __restrict__ gate) {
-    if (gate && !(gate[0] & 1)) return;
+                                                       const int* __restrict__ gate,
+                                                       const double* __restrict__ y,
+                                                       double* __restrict__ q, size_t n_pad) {
+    const size_t nq = n_pad / 4;
+    const size_t g0 = nq * blockIdx.x / gridDim.x, g1 = nq * (blockIdx.x + 1) / gridDim.x;
+    if (gate && !(gate[0] & 1)) {
+        if (y)
+            for (size_t e = g0 * WP + threadIdx.x; e < g1 * WP; e += blockDim.x)
+                reinterpret_cast<double4*>(q)[e] = reinterpret_cast<const double4*>(y)[e];
+        return;
+    }
     __shared__ int dropped_s[WP];
     __shared__ double d0s[WP];
     __shared__ double dpiv[WP];
     __shared__ double tr_s[2];
     __shared__ unsigned short tri[WP * (WP + 1) / 2];
     __shared__ int tri_off[WP + 1];
-    extern __shared__ double ce[];  // R [WP*WP], E [WP*WP]
+    extern __shared__ double ce[];  // R [WP*WP], E [WP*WP], apply mode: the CTA's y rows
     double* R = ce;
     double* E = R + WP * WP;
+    double* ys = E + WP * WP;
     const int tid = threadIdx.x;
+    if (y)  // coalesced copy of this CTA's panel rows, in flight during the factor
+        for (size_t e = tid; e < (g1 - g0) * WP; e += blockDim.x)
+            reinterpret_cast<double4*>(ys)[e] = reinterpret_cast<const double4*>(y)[g0 * WP + e];
     for (int i = tid; i <= WP; i += blockDim.x) {
         const int off = i * WP - (i * (i - 1)) / 2;
         tri_off[i] = off;
@@ -423,7 +441,7 @@ __global__ void __launch_bounds__(256) k_chol_inv_elim(const double* __restrict_
                                   dropped_s, dpiv, tri, tri_off))
             break;
         sigma = 11.0 * (nrows * w + static_cast<double>(w) * (w + 1)) * 0x1.0p-53 * tr_s[0];
-        if (tid == 0) {
+        if (tid == 0 && blockIdx.x == 0) {
             flags[0] |= 1;  // any shift in this solve (reported)
             flags[1] = 1;   // this orthonormalization shifted: its third pass runs
         }
@@ -433,7 +451,27 @@ __global__ void __launch_bounds__(256) k_chol_inv_elim(const double* __restrict_
     for (int e = tid; e < WP * WP; e += blockDim.x) {
         const int i = e / WP, j = e % WP;
         const double dj = dpiv[j];
-        rinv[e] = (i <= j && dj > 0.0) ? E[j * WP + i] * rsqrt(dj) : 0.0;
+        const double t = (i <= j && dj > 0.0) ? E[j * WP + i] * rsqrt(dj) : 0.0;
+        if (rinv && blockIdx.x == 0) rinv[e] = t;
+        R[e] = t;  // E is no longer read: R's slot holds T
+    }
+    if (!y) return;
+    __syncthreads();
+    // q = y T on this CTA's 4-row groups (T upper triangular), from shared memory
+    for (size_t item = tid; item < (g1 - g0) * WP; item += blockDim.x) {
+        const size_t qb = item / WP;
+        const int c = static_cast<int>(item % WP);
+        const double* yb = ys + qb * WP * 4;
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        for (int k = 0; k <= c; ++k) {
+            const double r = R[k * WP + c];
+            const double4 v = *reinterpret_cast<const double4*>(yb + k * 4);
+            s0 += v.x * r;
+            s1 += v.y * r;
+            s2 += v.z * r;
+            s3 += v.w * r;
+        }
+        *reinterpret_cast<double4*>(q + (g0 + qb) * WP * 4 + c * 4) = make_double4(s0, s1, s2, s3);
     }
 }
 
@@ -466,14 +504,26 @@ bool launch_orth_fused(double* y, double* t, double* out, size_t n_pad, int wp, 
 }
 
 bool launch_chol_inv_elim(const double* w_mat, int wp, int w, size_t n, int pass, double* rinv,
-                          int* flags, cudaStream_t st, const int* gate) {
-    const size_t smem = static_cast<size_t>(2) * wp * wp * sizeof(double);
+                          int* flags, cudaStream_t st, const int* gate, const double* y,
+                          double* q, size_t n_pad, int sms) {
+    // apply mode: one CTA per SM, its panel rows staged in shared memory
+    const size_t nq = n_pad / 4;
+    int grid = 1;
+    size_t smem = static_cast<size_t>(2) * wp * wp * sizeof(double);
+    if (y) {
+        grid = static_cast<int>(std::max<size_t>(1, std::min<size_t>(sms, nq)));
+        const size_t rows_per_cta = (nq + grid - 1) / grid * 4;
+        const size_t stage = rows_per_cta * wp * sizeof(double);
+        if (smem + stage > 200 * 1024) return false;  // caller falls back to the two kernels
+        smem += stage;
+    }
     const double nr = static_cast<double>(n);
     switch (wp) {
 #define DSB_CE(W)                                                                              \
     case W:                                                                                    \
         allow_dyn_smem(reinterpret_cast<const void*>(k_chol_inv_elim<W>));                     \
-        k_chol_inv_elim<W><<<1, 256, smem, st>>>(w_mat, w, nr, pass, rinv, flags, gate);      \
+        k_chol_inv_elim<W><<<grid, 256, smem, st>>>(w_mat, w, nr, pass, rinv, flags, gate, y, \
+                                                    q, n_pad);                               \
         break;
         DSB_CE(8) DSB_CE(16) DSB_CE(24) DSB_CE(32) DSB_CE(40) DSB_CE(48) DSB_CE(56) DSB_CE(64)
 #undef DSB_CE

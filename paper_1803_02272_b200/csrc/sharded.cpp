@@ -361,9 +361,14 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
             launch_panel_dot(bufs[ps][0], bufs[ps][0], m_pad, wp, psmall, wmat, c.sms, c.stream,
                              gate);
             cm.allreduce_sum(wmat, static_cast<size_t>(wp) * wp, c.stream);
-            if (!launch_chol_inv_elim(wmat, wp, wi, n, ps, rinv, flags, c.stream, gate))
-                launch_chol_inv(wmat, wp, wi, n, ps == 0 ? 1 : 0, rinv, flags, c.stream);
-            launch_panel_apply(bufs[ps][0], rinv, m_pad, wp, bufs[ps][1], c.stream, gate);
+            // factor + apply in one launch (every CTA factors W redundantly
+            // while its panel rows stream into shared memory); else the two kernels
+            if (!launch_chol_inv_elim(wmat, wp, wi, n, ps, nullptr, flags, c.stream, gate,
+                                      bufs[ps][0], bufs[ps][1], m_pad, c.sms)) {
+                if (!launch_chol_inv_elim(wmat, wp, wi, n, ps, rinv, flags, c.stream, gate))
+                    launch_chol_inv(wmat, wp, wi, n, ps == 0 ? 1 : 0, rinv, flags, c.stream);
+                launch_panel_apply(bufs[ps][0], rinv, m_pad, wp, bufs[ps][1], c.stream, gate);
+            }
         }
         cm.allgatherv(out_full, cnt.data(), off.data(), c.stream);
     };
