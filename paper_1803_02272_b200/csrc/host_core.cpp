@@ -18,17 +18,36 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 }
 
+namespace {
+// kernel attributes are per device: remembered per (device, kernel)
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, size_t> g_attr_set;
+std::atomic<long long> g_live_bufs{0};
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+}  // namespace
+
 void allow_dyn_smem(const void* kernel) {
-    static std::mutex mu;
-    static std::vector<const void*> done;
-    std::lock_guard<std::mutex> lk(mu);
-    for (const void* d : done)
-        if (d == kernel) return;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t& set = g_attr_set[{current_device(), kernel}];
+    if (set == ~size_t(0)) return;
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, kernel);
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(227 * 1024 - fa.sharedSizeBytes));
-    done.push_back(kernel);
+    set = ~size_t(0);
+}
+
+void ensure_dyn_smem(const void* kernel, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t& set = g_attr_set[{current_device(), kernel}];
+    if (set >= bytes) return;
+    DSB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes)));
+    set = bytes;
 }
 
 void count_launch(int k) { g_launches.fetch_add(static_cast<uint64_t>(k)); }
@@ -52,10 +71,14 @@ DevBuf::DevBuf(size_t b) : bytes(b) {
         throw Error(errc::internal, "device out of memory allocating " + std::to_string(b) +
                                         " bytes: " + cudaGetErrorString(e));
     }
+    g_live_bufs.fetch_add(1);
 }
 
 DevBuf::~DevBuf() {
-    if (p) cudaFreeAsync(p, Ctx::get().stream);
+    if (p) {
+        cudaFreeAsync(p, Ctx::get().stream);
+        g_live_bufs.fetch_sub(1);
+    }
 }
 
 Ctx::Ctx() = default;
@@ -100,16 +123,34 @@ void Ctx::init() {
     inited_ = true;
 }
 
+// One device per process (the multi-GPU path is one process per GPU). A
+// switch is allowed only while no device memory is alive: the workspace, the
+// resident Omega panel, pooled events and the stream all belong to the old
+// device and are dropped here; kernel attributes are tracked per device.
 void Ctx::set_device(int dev) {
     std::lock_guard<std::recursive_mutex> lk(mu);
-    DSB_CUDA(cudaSetDevice(dev));
-    if (inited_ && dev != device) {
+    if (inited_ && dev == device) return;
+    if (inited_) {
+        DSB_CUDA(cudaStreamSynchronize(stream));
         arena_.clear();
-        if (stream) cudaStreamDestroy(stream);
+        if (g_live_bufs.load() != 0)
+            throw Error(errc::invalid_argument,
+                        "cannot change device while handles hold memory on device " +
+                            std::to_string(device) + " (free them first)");
+        for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
+        event_pool.clear();
+        for (auto& t : pending) {
+            cudaEventDestroy(t.a);
+            cudaEventDestroy(t.b);
+        }
+        pending.clear();
+        omega_key = OmegaKey{};
+        cudaStreamDestroy(stream);
         stream = nullptr;
         inited_ = false;
     }
-    if (!inited_) init();
+    DSB_CUDA(cudaSetDevice(dev));
+    init();
 }
 
 void* Ctx::scratch(const std::string& slot, size_t bytes) {

@@ -151,6 +151,13 @@ public:
 
     void set_device(int dev);
 
+    // key of the device-resident Omega panel ("omega_panel" scratch slot)
+    struct OmegaKey {
+        bool ok = false;
+        uint64_t seed = 0;
+        size_t n = 0, w = 0, n_pad = 0;
+    } omega_key;
+
 private:
     Ctx();
     void init();

@@ -379,21 +379,11 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
     const int nbt = static_cast<int>((n + kT - 1) / kT);
     const size_t part_ld = static_cast<size_t>(nbt) * kT;
     if (dt == DType::F64) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k1_tile_pairs<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(k1_smem<double>()));
-            attr = true;
-        }
+        ensure_dyn_smem(reinterpret_cast<const void*>(k1_tile_pairs<double>), k1_smem<double>());
         k1_tile_pairs<double><<<w.grid, kK1Threads + 32, k1_smem<double>(), st>>>(
             *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
     } else {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k1_tile_pairs<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(k1_smem<float>()));
-            attr = true;
-        }
+        ensure_dyn_smem(reinterpret_cast<const void*>(k1_tile_pairs<float>), k1_smem<float>());
         k1_tile_pairs<float><<<w.grid, kK1Threads + 32, k1_smem<float>(), st>>>(
             *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
     }

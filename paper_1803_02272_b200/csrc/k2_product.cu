@@ -274,12 +274,7 @@ __global__ void __launch_bounds__(256)
 template <int WP, typename TD, bool SQ, int CW, int KS>
 void run_product_ks(const CUtensorMap* tmap, const K2Plan& p, const double* x, double* part,
                     cudaStream_t st, const int* skip) {
-    static size_t set_for = 0;  // per instantiation
-    if (p.smem > set_for) {
-        cudaFuncSetAttribute(k2_product<WP, TD, SQ, CW, KS>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
-        set_for = p.smem;
-    }
+    ensure_dyn_smem(reinterpret_cast<const void*>(k2_product<WP, TD, SQ, CW, KS>), p.smem);
     k2_product<WP, TD, SQ, CW, KS><<<p.grid, (CW + 1) * 32, p.smem, st>>>(
         *tmap, x, p.nk, p.total, part, p.maxseg, p.stages, skip);
 }

@@ -680,13 +680,8 @@ template <int NB, typename TD, int SD = kDig>
 void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
             const int* row_exp, const int* col_exp, double* part, int cg0, cudaStream_t st,
             const int* skip, double hlen = 0.0) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k2i_product_ts<NB, TD, SD>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(ts_smem<NB, TD, SD>()));
-        attr = true;
-    }
+    ensure_dyn_smem(reinterpret_cast<const void*>(k2i_product_ts<NB, TD, SD>),
+                    ts_smem<NB, TD, SD>());
     k2i_product_ts<NB, TD, SD><<<p.grid, kThreadsI8, ts_smem<NB, TD, SD>(), st>>>(
         *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
         p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen);

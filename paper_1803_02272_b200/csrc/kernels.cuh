@@ -252,6 +252,8 @@ void launch_hamming(const uint32_t* lo, const uint32_t* hi, size_t count, int wo
 // 227 KB minus its static shared memory), so static + dynamic may exceed the
 // 48 KB default.
 void allow_dyn_smem(const void* kernel);
+// dynamic shared memory >= bytes for `kernel` on the current device
+void ensure_dyn_smem(const void* kernel, size_t bytes);
 uint64_t kernel_launch_count();
 void count_launch(int k = 1);
 

@@ -21,6 +21,8 @@
 // With one rank the same code runs with every collective a no-op.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 
@@ -47,25 +49,57 @@ Layout layout_of(size_t n) {
     return L;
 }
 
-// interleaved-panel chunk of rank r: rows [rb_r, re_r) padded to the block
-// (last rank to n_pad)
-void panel_chunks(const Layout& L, size_t n_pad, int wp, std::vector<size_t>& cnt,
-                  std::vector<size_t>& off) {
-    cnt.resize(L.world);
-    off.resize(L.world);
-    for (int r = 0; r < L.world; ++r) {
-        const size_t b = L.rb[r];
-        const size_t e = (r == L.world - 1) ? n_pad : L.rb[r + 1];
-        off[r] = b * wp;
-        cnt[r] = (e > b ? e - b : 0) * wp;
-    }
-}
-
 void check_shard(const Store& s) {
     Layout L = layout_of(s.n_global);
     if (s.row_begin != L.rb[L.rank] || s.row_begin + s.rows != L.re[L.rank])
         throw Error(errc::shape_mismatch,
                     "row shard does not match this rank's range (divscope_shard_range)");
+}
+
+// Cross-rank agreement before the first collective of a call: every rank
+// runs its local validation, then one all-reduce of (error code, call
+// signature, -signature) decides. A rank whose validation failed and its
+// peers all return an error (the failing rank's own code; peers get the same
+// code), and ranks that entered the call with different arguments (n, w, q,
+// seed, mode) all fail with INVALID_ARGUMENT — instead of the peers blocking
+// forever in a collective the failing rank never reaches.
+template <typename F>
+void agree_or_throw(uint64_t signature, F&& validate) {
+    Ctx& c = Ctx::get();
+    Comm& cm = Comm::get();
+    int code = 0;
+    std::string msg;
+    try {
+        validate();
+    } catch (const Error& e) {
+        code = static_cast<int>(e.code());
+        msg = e.what();
+    }
+    if (!cm.active() || cm.world() == 1) {
+        if (code) throw Error(static_cast<errc>(code), msg);
+        return;
+    }
+    const double sig = static_cast<double>(signature & ((1ull << 52) - 1));
+    double h[3] = {static_cast<double>(code), sig, -sig};
+    double* d = static_cast<double*>(c.scratch("sh_agree", sizeof(h)));
+    DSB_CUDA(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, c.stream));
+    cm.allreduce_max(d, 3, c.stream);
+    c.d2h_copy(h, d, sizeof(h));
+    if (code) throw Error(static_cast<errc>(code), msg);
+    if (h[0] != 0.0)
+        throw Error(static_cast<errc>(static_cast<int>(h[0])),
+                    "a peer rank failed this call's validation");
+    if (h[1] != -h[2])
+        throw Error(errc::invalid_argument, "ranks entered the call with different arguments");
+}
+
+uint64_t mix_sig(std::initializer_list<uint64_t> v) {
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    for (uint64_t x : v) {
+        h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        h *= 0xBF58476D1CE4E5B9ull;
+    }
+    return h;
 }
 
 }  // namespace
@@ -112,11 +146,13 @@ Matrix gram_sharded(const Matrix& d) {
     std::lock_guard<std::recursive_mutex> lk(c.mu);
     Comm& cm = Comm::get();
     const Store& s = *d.store;
-    if (!s.square() || !s.symmetric)
-        throw Error(errc::not_symmetric, "gram matrix requires a symmetric distance matrix");
     const size_t n = s.n_global;
-    if (n == 0) throw Error(errc::empty_input, "empty distance matrix");
-    check_shard(s);
+    agree_or_throw(mix_sig({1, n}), [&] {
+        if (!s.square() || !s.symmetric)
+            throw Error(errc::not_symmetric, "gram matrix requires a symmetric distance matrix");
+        if (n == 0) throw Error(errc::empty_input, "empty distance matrix");
+        check_shard(s);
+    });
     Layout L = layout_of(n);
     const size_t m = s.rows, rb = s.row_begin;
     const size_t esz = s.dt == DType::F64 ? 8 : 4;
@@ -253,23 +289,16 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     Ctx& c = Ctx::get();
     Comm& cm = Comm::get();
     Store& s = *g.store;
-    if (!g.gram) throw Error(errc::invalid_argument, "sharded solve needs a gram handle");
     const size_t n = s.n_global, m = s.rows, rb = s.row_begin;
-    check_shard(s);
-    Layout L = layout_of(n);
-    if (rank < 1) throw Error(errc::invalid_argument, "rank must be >= 1");
     const size_t w = rank + p;
-    if (w > n) throw Error(errc::rank_too_large, "rank + oversampling exceeds matrix order");
-    if (w > static_cast<size_t>(kMaxWP))
-        throw Error(errc::invalid_argument,
-                    "rank + oversampling > 128 is not supported by the GPU path");
-    const int wi = static_cast<int>(w), wp = static_cast<int>(round_up(w, 8));
-    const size_t n_pad = round_up(n, kRowPad);
-    // local panel rows: block-aligned, last rank up to n_pad
-    const size_t m_pad = (L.rank == L.world - 1) ? n_pad - rb : (L.re[L.rank] - rb);
-    const double* r_full = g.gram->row_mean->as<double>();
-    const double* scal = g.gram->scalars->as<double>();
-    {
+    agree_or_throw(mix_sig({2, n, rank, p, q, seed, embed_mode ? 1u : 0u, requested}), [&] {
+        if (!g.gram) throw Error(errc::invalid_argument, "sharded solve needs a gram handle");
+        check_shard(s);
+        if (rank < 1) throw Error(errc::invalid_argument, "rank must be >= 1");
+        if (w > n) throw Error(errc::rank_too_large, "rank + oversampling exceeds matrix order");
+        if (w > static_cast<size_t>(kMaxWP))
+            throw Error(errc::invalid_argument,
+                        "rank + oversampling > 128 is not supported by the GPU path");
         std::lock_guard<std::mutex> lk(s.mu);
         if (!s.tmap_ok) {
             if (!c.encode_tmap(&s.tmap128, s.buf->p, s.dt, std::max<size_t>(m, 1), s.cols, s.ld,
@@ -279,7 +308,15 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
                 throw Error(errc::internal, "cuTensorMapEncodeTiled failed");
             s.tmap_ok = true;
         }
-    }
+    });
+    Layout L = layout_of(n);
+    const int wi = static_cast<int>(w), wp = static_cast<int>(round_up(w, 8));
+    // every rank owns one equal panel chunk (its rows, zero-padded): the
+    // panel is world * chunk rows and all-gathers with ncclAllGather
+    const size_t m_pad = shard_chunk_rows(n, L.world);
+    const size_t n_pad = m_pad * static_cast<size_t>(L.world);
+    const double* r_full = g.gram->row_mean->as<double>();
+    const double* scal = g.gram->scalars->as<double>();
     const K2Plan plan = k2_plan_rect(std::max<size_t>(m, 1), n, wp, s.dt, c.sms);
     // int8 slice product on this rank's rows (same admission rule as 1 GPU)
     const bool use_i8 = m > 0 && use_int8_product(*g.gram, wp);
@@ -318,15 +355,13 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     int* flags = static_cast<int*>(c.scratch("flags", 64));
     DSB_CUDA(cudaMemsetAsync(flags, 0, 64, c.stream));
     DSB_CUDA(cudaMemsetAsync(P1, 0, pbytes, c.stream));
-    std::vector<size_t> cnt, off;
-    panel_chunks(L, n_pad, wp, cnt, off);
     {
         const double* om = omega_pinned(seed, n, w);
         double* stage = static_cast<double*>(c.scratch("omega_rm", n * w * 8));
         c.h2d_copy(stage, om, n * w * 8);
         launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, P0, c.stream);
     }
-    const size_t lo = rb * wp;  // local chunk offset in a panel
+    const size_t lo = static_cast<size_t>(L.rank) * m_pad * wp;  // this rank's panel chunk
     auto product = [&](const double* x_full, double* y_full) {
         // s = 1^T X, t = r^T X over the full replicated panel (+ the int8
         // column exponents: identical on every rank)
@@ -370,7 +405,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
                 launch_panel_apply(bufs[ps][0], rinv, m_pad, wp, bufs[ps][1], c.stream, gate);
             }
         }
-        cm.allgatherv(out_full, cnt.data(), off.data(), c.stream);
+        cm.allgather(out_full, m_pad * wp, c.stream);
     };
     product(P0, P1);
     orth_local(P1, P2, P0);
@@ -399,7 +434,11 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         const size_t rq = std::max<size_t>(req, 1);
         dcoords = std::make_shared<DevBuf>(n * rq * 8);
         coords = dcoords->as<double>();
-        const int P = lift_grid(std::max<size_t>(m, 1), c.sms);
+        // the partial-table geometry must agree on every rank (it sizes the
+        // gather): CTAs per rank from the largest shard, not the local one
+        size_t maxm = 1;
+        for (int k = 0; k < L.world; ++k) maxm = std::max(maxm, L.re[k] - L.rb[k]);
+        const int P = lift_grid(maxm, c.sms);
         // all ranks' CTA partials side by side: [world][P][rmax][2]
         double* lp = static_cast<double*>(
             c.scratch("lift_part_all", (static_cast<size_t>(L.world) * P * 2 + 1) * rq * 8));
@@ -412,9 +451,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
             launch_lift_partial(P0 + lo, m, wp, wi, eo.vkeep, eo.imeta, static_cast<int>(req),
                                 my_coords, lp + static_cast<size_t>(L.rank) * P * 2 * rq,
                                 static_cast<long long>(rb), P, c.stream);
-        std::vector<size_t> pc(L.world, static_cast<size_t>(P) * 2 * rq), po(L.world);
-        for (int r = 0; r < L.world; ++r) po[r] = static_cast<size_t>(r) * P * 2 * rq;
-        cm.allgatherv(lp, pc.data(), po.data(), c.stream);
+        cm.allgather(lp, static_cast<size_t>(P) * 2 * rq, c.stream);
         double* scale = lp + static_cast<size_t>(L.world) * P * 2 * rq;
         launch_lift_finish(m, eo.imeta, L.world * P, static_cast<int>(req), eo.kept_vals, lp, scale,
                            my_coords, c.stream);

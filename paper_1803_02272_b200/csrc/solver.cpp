@@ -243,20 +243,15 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     // device once per (seed, n, w) and kept resident (a pure function of the
     // seed); every solve starts from a device copy of it
     {
-        static uint64_t key_seed = 0;
-        static size_t key_n = 0, key_w = 0, key_np = 0;
-        static bool key_ok = false;
+        Ctx::OmegaKey& key = c.omega_key;
         double* cached = static_cast<double*>(c.scratch("omega_panel", pbytes));
-        if (!key_ok || key_seed != seed || key_n != n || key_w != w || key_np != n_pad) {
+        if (!key.ok || key.seed != seed || key.n != n || key.w != w || key.n_pad != n_pad) {
+            key.ok = false;  // the slot may have been reallocated by the scratch call above
             const double* om = omega_host(seed, n, w);
             double* stage = static_cast<double*>(c.scratch("omega_rm", n * w * sizeof(double)));
             c.h2d_copy(stage, om, n * w * sizeof(double));
             launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, cached, c.stream);
-            key_seed = seed;
-            key_n = n;
-            key_w = w;
-            key_np = n_pad;
-            key_ok = true;
+            key = Ctx::OmegaKey{true, seed, n, w, n_pad};
         }
         DSB_CUDA(cudaMemcpyAsync(P0, cached, pbytes, cudaMemcpyDeviceToDevice, c.stream));
     }

@@ -55,6 +55,19 @@ __global__ void dmma16_loop(double* out, int iters) {
     if (s == 12345.678) out[0] = s;
 }
 
+// a launch that failed (e.g. too many registers for the block size) must not
+// print a rate: the events around it measure nothing
+static bool launch_ok(const char* what, int threads, int bps) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        printf("%s threads=%d bps=%d: launch failed (%s), skipped\n", what, threads, bps,
+               cudaGetErrorString(e));
+        return false;
+    }
+    return true;
+}
+
 int main() {
     double* d; cudaMalloc(&d, 8);
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -70,21 +83,24 @@ int main() {
             cudaEventRecord(e1); cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1);
             double flops = 2.0 * 16 * iters * (double)threads * grid.x;
-            printf("DFMA threads=%d bps=%d: %.2f TFLOP/s\n", threads, bps, flops / ms / 1e9);
+            if (launch_ok("DFMA", threads, bps))
+                printf("DFMA threads=%d bps=%d: %.2f TFLOP/s\n", threads, bps, flops / ms / 1e9);
             dmma_loop<<<grid, threads>>>(d, 16);
             cudaEventRecord(e0);
             dmma_loop<<<grid, threads>>>(d, iters);
             cudaEventRecord(e1); cudaEventSynchronize(e1);
             cudaEventElapsedTime(&ms, e0, e1);
             flops = 2.0 * 8 * 8 * 4 * 8 * iters * (double)(threads / 32) * grid.x;
-            printf("DMMA884 threads=%d bps=%d: %.2f TFLOP/s\n", threads, bps, flops / ms / 1e9);
+            if (launch_ok("DMMA884", threads, bps))
+                printf("DMMA884 threads=%d bps=%d: %.2f TFLOP/s\n", threads, bps, flops / ms / 1e9);
             dmma16_loop<<<grid, threads>>>(d, 16);
             cudaEventRecord(e0);
             dmma16_loop<<<grid, threads>>>(d, iters);
             cudaEventRecord(e1); cudaEventSynchronize(e1);
             cudaEventElapsedTime(&ms, e0, e1);
             flops = 2.0 * 16 * 8 * 4 * 8 * iters * (double)(threads / 32) * grid.x;
-            printf("DMMA1684 threads=%d bps=%d: %.2f TFLOP/s\n", threads, bps, flops / ms / 1e9);
+            if (launch_ok("DMMA1684", threads, bps))
+                printf("DMMA1684 threads=%d bps=%d: %.2f TFLOP/s\n", threads, bps, flops / ms / 1e9);
         }
     }
     cudaError_t err = cudaGetLastError();
