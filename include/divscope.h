@@ -217,6 +217,14 @@ divscope_status divscope_eigs(const divscope_matrix* gram, const divscope_solver
                               double* resid);
 
 /* ref divscope.h:157-158: ||G||_F^2 / ||G||_S^2 (power iteration on the GPU). */
+/* NEW (the reference has it in C++ only: eigs_sym's Spectrum::vectors,
+ * src/rsvd.hpp:29-33, :43-62): divscope_eigs plus the Ritz vectors, row-major
+ * n x count into `vectors` (n * opts->rank doubles), column a pairing with
+ * eigenvalues[a]; sign as the eigensolver leaves it. Unsharded handles only. */
+divscope_status divscope_eigs_vectors(const divscope_matrix* gram,
+                                      const divscope_solver_options* opts, unsigned threads,
+                                      double* eigenvalues, double* vectors, size_t* count,
+                                      double* resid);
 divscope_status divscope_stable_rank(const divscope_matrix* gram, unsigned threads,
                                      double* out);
 

@@ -23,6 +23,7 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <atomic>
 #include <string_view>
 #include <vector>
 
@@ -97,6 +98,10 @@ struct GramOp {
     const double* row_mean = nullptr;
     double grand = 0.0;
     std::size_t n = 0;
+    // d verified BIT-symmetric (exact_symmetric below): the mirrored entry
+    // d_ji is then read from row i (same bits, cache-friendly); the
+    // expression and its operand order stay the reference's
+    bool row_sym = false;
 
     // mds.cpp:50-51 for i <= j; lower triangle mirrored (mds.cpp:57-58)
     double at(std::size_t i, std::size_t j) const {
@@ -105,31 +110,62 @@ struct GramOp {
             const double dij = d[i * n + j];
             return -0.5 * (dij * dij - row_mean[i] - row_mean[j] + grand);
         }
-        const double dji = d[j * n + i];
+        const double dji = row_sym ? d[i * n + j] : d[j * n + i];
         return -0.5 * (dji * dji - row_mean[j] - row_mean[i] + grand);
     }
 };
 
-// src/rsvd.cpp:18-36
+// true iff d_ij and d_ji have identical bits for every pair (64 x 64 tiles,
+// threaded over tile rows)
+bool exact_symmetric(const double* d, std::size_t n, unsigned threads) {
+    constexpr std::size_t T = 64;
+    const std::size_t nt = (n + T - 1) / T;
+    std::vector<char> bad(nt, 0);
+    chunks(nt, threads, [&](std::size_t b0, std::size_t b1) {
+        for (std::size_t bi = b0; bi < b1; ++bi)
+            for (std::size_t bj = bi; bj < nt && !bad[bi]; ++bj)
+                for (std::size_t i = bi * T; i < std::min(n, bi * T + T); ++i)
+                    for (std::size_t j = std::max(i + 1, bj * T); j < std::min(n, bj * T + T); ++j)
+                        if (std::memcmp(d + i * n + j, d + j * n + i, sizeof(double)) != 0)
+                            bad[bi] = 1;
+    });
+    for (char b : bad)
+        if (b) return false;
+    return true;
+}
+
+// src/rsvd.cpp:18-36. Every output row is the reference's loop — zero-fill,
+// then j ascending, skipping g_ij == 0, out_i[c] += g_ij * m_j[c] — so the
+// result is bit-identical; rows are processed in blocks of kIB against
+// column blocks of kJB only so that a block of m stays in cache while the
+// rows of the block consume it (the per-row order of additions is unchanged).
 void multiply(const GramOp& op, const double* m, std::size_t k, double* out, unsigned threads) {
+    constexpr std::size_t kIB = 32, kJB = 512;
     const std::size_t n = op.n;
     chunks(n, threads, [&](std::size_t begin, std::size_t end) {
-        std::vector<double> grow(op.g ? 0 : n);
-        for (std::size_t i = begin; i < end; ++i) {
-            double* out_row = out + i * k;
-            std::fill(out_row, out_row + k, 0.0);
-            const double* row;
-            if (op.g) {
-                row = op.g + i * n;
-            } else {
-                for (std::size_t j = 0; j < n; ++j) grow[j] = op.at(i, j);
-                row = grow.data();
-            }
-            for (std::size_t j = 0; j < n; ++j) {
-                const double gij = row[j];
-                if (gij == 0.0) continue;
-                const double* mrow = m + j * k;
-                for (std::size_t c = 0; c < k; ++c) out_row[c] += gij * mrow[c];
+        std::vector<double> gblk(kIB * kJB);
+        for (std::size_t i0 = begin; i0 < end; i0 += kIB) {
+            const std::size_t i1 = std::min(end, i0 + kIB);
+            for (std::size_t i = i0; i < i1; ++i) std::fill(out + i * k, out + i * k + k, 0.0);
+            for (std::size_t j0 = 0; j0 < n; j0 += kJB) {
+                const std::size_t j1 = std::min(n, j0 + kJB);
+                for (std::size_t i = i0; i < i1; ++i) {
+                    double* out_row = out + i * k;
+                    const double* row;
+                    if (op.g) {
+                        row = op.g + i * n + j0;
+                    } else {
+                        double* gr = gblk.data() + (i - i0) * kJB;
+                        for (std::size_t j = j0; j < j1; ++j) gr[j - j0] = op.at(i, j);
+                        row = gr;
+                    }
+                    for (std::size_t j = j0; j < j1; ++j) {
+                        const double gij = row[j - j0];
+                        if (gij == 0.0) continue;
+                        const double* mrow = m + j * k;
+                        for (std::size_t c = 0; c < k; ++c) out_row[c] += gij * mrow[c];
+                    }
+                }
             }
         }
     });
@@ -358,12 +394,29 @@ int orc_gram_stats(const double* d, std::size_t rows, std::size_t cols, int sym,
     if (rows != cols || !sym) return NOT_SYMMETRIC;
     const std::size_t n = rows;
     if (n == 0) return EMPTY_INPUT;
+    // max |d| and the pairwise test of mds.cpp:21-27 (order-independent
+    // decisions, so threaded and tiled; exact symmetry short-cuts the test)
+    std::vector<double> part_max(std::max(threads, 1u), 0.0);
+    {
+        std::atomic<unsigned> slot{0};
+        chunks(n, threads, [&](std::size_t b, std::size_t e) {
+            double mx = 0.0;
+            for (std::size_t k = b * n; k < e * n; ++k) mx = std::max(mx, std::abs(d[k]));
+            part_max[slot.fetch_add(1)] = mx;
+        });
+    }
     double maxabs = 0.0;
-    for (std::size_t k = 0; k < n * n; ++k) maxabs = std::max(maxabs, std::abs(d[k]));
-    for (std::size_t i = 0; i < n; ++i)
-        for (std::size_t j = i + 1; j < n; ++j)
-            if (std::abs(d[i * n + j] - d[j * n + i]) > 1e-12 * std::max(1.0, maxabs))
-                return NOT_SYMMETRIC;
+    for (double v : part_max) maxabs = std::max(maxabs, v);
+    if (!exact_symmetric(d, n, threads)) {
+        const double tol = 1e-12 * std::max(1.0, maxabs);
+        std::atomic<int> bad{0};
+        chunks(n, threads, [&](std::size_t b, std::size_t e) {
+            for (std::size_t i = b; i < e; ++i)
+                for (std::size_t j = i + 1; j < n; ++j)
+                    if (std::abs(d[i * n + j] - d[j * n + i]) > tol) bad = 1;
+        });
+        if (bad) return NOT_SYMMETRIC;
+    }
     chunks(n, threads, [&](std::size_t begin, std::size_t end) {
         for (std::size_t i = begin; i < end; ++i) {
             const double* row = d + i * n;
@@ -405,6 +458,7 @@ void orc_multiply_sym(const double* g, std::size_t n, const double* m, std::size
 void orc_multiply_gram_otf(const double* d, std::size_t n, const double* row_mean, double grand,
                            const double* m, std::size_t k, unsigned threads, double* out) {
     GramOp op{nullptr, d, row_mean, grand, n};
+    op.row_sym = exact_symmetric(d, n, threads);
     multiply(op, m, k, out, threads);
 }
 
@@ -431,6 +485,7 @@ int orc_eigs(const double* g, const double* d, const double* row_mean, double gr
              unsigned threads, double* vals_out, double* vecs_out, std::size_t* keep_out,
              double* resid_out) {
     GramOp op{g, d, row_mean, grand, n};
+    if (d) op.row_sym = exact_symmetric(d, n, threads);
     Spectrum s;
     if (int e = eigs(op, rank, p, q, seed, threads, s)) return e;
     *keep_out = s.keep;
@@ -449,6 +504,7 @@ int orc_embed(const double* g, const double* d, const double* row_mean, double g
     if (rank < 1 || rank > n) return RANK_TOO_LARGE;  // mds.cpp:118-119
     p = std::min(p, n - rank);                         // mds.cpp:121
     GramOp op{g, d, row_mean, grand, n};
+    if (d) op.row_sym = exact_symmetric(d, n, threads);
     Spectrum s;
     if (int e = eigs(op, rank, p, q, seed, threads, s)) return e;
     double maxabs = 0.0;

@@ -260,4 +260,49 @@ int ref_write_matrix_tsv(const char* path, const double* v, std::size_t rows, st
     });
 }
 
+// Acceptance check #4's input (ref tests/acceptance.cpp:125-154), built with
+// the reference's own types and RNG: std::normal_distribution over
+// std::mt19937_64(404) for a 500 x 20 Gaussian panel, its Householder Q
+// (eigen shim), spectrum 100 * 0.8^i with every third value negated, and
+// symmetric 1e-8 noise on the upper triangle mirrored. g_out: n x n.
+// dense_out: the shim's full EVD sorted by |lambda| descending, positive
+// first (the acceptance check's ordering).
+void ref_acceptance4_matrix(double* g_out, double* dense_out) {
+    const std::size_t n = 500, k = 20;
+    std::mt19937_64 eng(404);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    RowMatrix a(n, k);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < k; ++j) a(i, j) = gauss(eng);
+    const RowMatrix v =
+        Eigen::HouseholderQR<RowMatrix>(a).householderQ() * RowMatrix::Identity(n, k);
+    std::vector<double> lam(k);
+    for (std::size_t i = 0; i < k; ++i)
+        lam[i] = 100.0 * std::pow(0.8, double(i)) * ((i % 3 == 2) ? -1.0 : 1.0);
+    // v diag(lam) v^T (the shim has no asDiagonal; the product is an input
+    // whose exact bits the fixture stores)
+    RowMatrix g(n, n);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < n; ++j) {
+            double acc = 0.0;
+            for (std::size_t c = 0; c < k; ++c) acc += v(i, c) * lam[c] * v(j, c);
+            g(i, j) = acc;
+        }
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = i; j < n; ++j) {
+            const double x = g(i, j) + 1e-8 * gauss(eng);
+            g(i, j) = x;
+            g(j, i) = x;
+        }
+    Eigen::SelfAdjointEigenSolver<RowMatrix> evd(g);
+    std::vector<double> dense(evd.eigenvalues().data(), evd.eigenvalues().data() + n);
+    std::sort(dense.begin(), dense.end(), [](double x, double y) {
+        if (std::abs(x) != std::abs(y)) return std::abs(x) > std::abs(y);
+        return x > y;
+    });
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < n; ++j) g_out[i * n + j] = g(i, j);
+    std::copy(dense.begin(), dense.end(), dense_out);
+}
+
 }  // extern "C"

@@ -32,7 +32,8 @@ __all__ = [
     "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
     "stats_enable_timing", "stats_reset", "set_product_path", "matrix_read_rows", "reconstruction_error", "Scoring", "Alignment",
     "align", "distance", "pairwise_self", "pairwise_cross", "stats_get", "set_device", "LIB_PATH",
-    "fp64_tensor_peak_tflops", "stream_ptr",
+    "fp64_tensor_peak_tflops", "stream_ptr", "eigs_vectors", "debug_omega_panel",
+    "debug_fill_gaussian",
 ]
 
 LIB_PATH = Path(os.environ.get("DSB_LIB_OVERRIDE") or Path(__file__).resolve().parent / "libdivscope_b200.so")
@@ -133,6 +134,10 @@ def _load() -> C.CDLL:
         "divscope_solver_options_init": ([C.POINTER(SolverOptions)], None),
         "divscope_gram": ([_vp, C.c_uint, C.POINTER(_vp)], _st),
         "divscope_eigs": ([_vp, C.POINTER(SolverOptions), C.c_uint, _dp, C.POINTER(_sz), _dp], _st),
+        "divscope_eigs_vectors": ([_vp, C.POINTER(SolverOptions), C.c_uint, _dp, _dp,
+                                   C.POINTER(_sz), _dp], _st),
+        "divscope_debug_omega_panel": ([C.c_uint64, _sz, _sz, _dp], C.c_int),
+        "divscope_debug_fill_gaussian": ([C.c_uint64, _sz, _dp], C.c_int),
         "divscope_stable_rank": ([_vp, C.c_uint, _dp], _st),
         "divscope_embed": ([_vp, C.POINTER(SolverOptions), C.c_uint, _vp, C.POINTER(_vp)], _st),
         "divscope_embedding_rows": ([_vp], _sz),
@@ -360,6 +365,37 @@ def eigs(g: Matrix, rank=None, oversampling=None, power_iters=None, seed=None, o
     _check(lib.divscope_eigs(g.handle, C.byref(o), threads, vals.ctypes.data_as(_dp),
                              C.byref(count), C.byref(resid)))
     return vals[: count.value].copy(), resid.value
+
+
+def eigs_vectors(g: Matrix, rank=None, oversampling=None, power_iters=None, seed=None,
+                 opts=None, threads: int = 1) -> tuple[np.ndarray, np.ndarray, float]:
+    """divscope_eigs_vectors — the reference's C++ eigs_sym (rsvd.hpp:43-62)
+    with Spectrum::vectors: (eigenvalues[count], vectors n x count, resid)."""
+    o = _opts(rank, oversampling, power_iters, seed, opts)
+    n = g.rows
+    k = max(int(o.rank), 1)
+    vals = np.zeros(k, np.float64)
+    vecs = np.zeros(n * k, np.float64)
+    count = _sz(0)
+    resid = C.c_double(-1.0)
+    _check(lib.divscope_eigs_vectors(g.handle, C.byref(o), threads, vals.ctypes.data_as(_dp),
+                                     vecs.ctypes.data_as(_dp), C.byref(count), C.byref(resid)))
+    c = count.value
+    return vals[:c].copy(), vecs[: n * c].reshape(n, c).copy(), resid.value
+
+
+def debug_omega_panel(seed: int, n: int, w: int) -> np.ndarray:
+    """Test hook: Omega (n x w) exactly as a solve uploads it to the device."""
+    out = np.zeros(n * w, np.float64)
+    _check(lib.divscope_debug_omega_panel(seed, n, w, out.ctypes.data_as(_dp)))
+    return out.reshape(n, w)
+
+
+def debug_fill_gaussian(seed: int, count: int) -> np.ndarray:
+    """Test hook (host only): the product's fill_gaussian over mt19937_64(seed)."""
+    out = np.zeros(count, np.float64)
+    _check(lib.divscope_debug_fill_gaussian(seed, count, out.ctypes.data_as(_dp)))
+    return out
 
 
 def stable_rank(g: Matrix, threads: int = 1) -> float:

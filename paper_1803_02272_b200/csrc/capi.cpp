@@ -509,6 +509,23 @@ divscope_status divscope_eigs(const divscope_matrix* gram, const divscope_solver
     });
 }
 
+divscope_status divscope_eigs_vectors(const divscope_matrix* gram,
+                                      const divscope_solver_options* opts, unsigned threads,
+                                      double* eigenvalues, double* vectors, size_t* count,
+                                      double* resid) {  // ref rsvd.hpp:43-62 eigs_sym
+    (void)threads;
+    if (!gram || !opts || !eigenvalues || !vectors) return fail_invalid("null argument");
+    return wrap([&] {
+        if (!gram->m.store->square())
+            throw Error(errc::not_symmetric, "matrix is not square");
+        const dsb::Spectrum s = dsb::eigs_sym_vectors(gram->m, to_options(opts));
+        for (size_t i = 0; i < s.eigenvalues.size(); ++i) eigenvalues[i] = s.eigenvalues[i];
+        std::copy(s.vectors.begin(), s.vectors.end(), vectors);
+        if (count) *count = s.eigenvalues.size();
+        if (resid) *resid = s.resid;
+    });
+}
+
 divscope_status divscope_stable_rank(const divscope_matrix* gram, unsigned threads,
                                      double* out) {  // ref capi.cpp:327-335
     (void)threads;
@@ -781,5 +798,22 @@ extern "C" int divscope_debug_sym_fingerprint(const divscope_matrix* m, unsigned
         c.d2h_copy(out, d, 16);
         out[0] &= 0xFFFFFFFFull;
         out[1] &= 0xFFFFFFFFull;
+    });
+}
+
+// test hook: Omega of (seed, n, w) as the solver uploads it (rng.hpp
+// fill_gaussian on the host, relayout on the device), read back row-major
+extern "C" int divscope_debug_omega_panel(uint64_t seed, size_t n, size_t w, double* out) {
+    if (!out) return DIVSCOPE_ERR_INVALID_ARGUMENT;
+    return wrap([&] { dsb::debug_omega_panel(seed, n, w, out); });
+}
+
+// test hook, host only: the product's fill_gaussian (host_core.cpp) driven
+// by std::mt19937_64(seed), as omega_host fills the pinned Omega buffer
+extern "C" int divscope_debug_fill_gaussian(uint64_t seed, size_t count, double* out) {
+    if (!out) return DIVSCOPE_ERR_INVALID_ARGUMENT;
+    return wrap([&] {
+        std::mt19937_64 eng(seed);
+        dsb::fill_gaussian(eng, out, count);
     });
 }

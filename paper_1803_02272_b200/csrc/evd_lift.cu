@@ -207,7 +207,9 @@ __device__ void evd_finish_dg(const double* __restrict__ dg, const double* __res
         double mass = 0.0;
         for (int a = 0; a < keep; ++a) {
             const double lam = o.vals[a];
-            if (lam > eps && cnt < requested)
+            if (requested < 0)  // eigenvector mode: the first keep, any sign
+                kept[cnt++] = order[a];
+            else if (lam > eps && cnt < requested)
                 kept[cnt++] = order[a];
             else if (lam < 0.0)
                 mass += -lam;
@@ -217,15 +219,16 @@ __device__ void evd_finish_dg(const double* __restrict__ dg, const double* __res
         o.dmeta[2] = sumsq;
         o.imeta[0] = keep;
         o.imeta[1] = cnt;
-        o.imeta[2] = cnt < requested ? 1 : 0;
+        o.imeta[2] = requested >= 0 && cnt < requested ? 1 : 0;
         o.imeta[3] = sweeps;
         o.imeta[4] = done;
         for (int c = 0; c < cnt; ++c) o.kept_vals[c] = dg[kept[c]];
     }
     __syncthreads();
     const int r = o.imeta[1];
-    for (int e = tid; e < w * requested; e += nt) {
-        const int x = e / requested, c = e % requested;
+    const int rq = requested < 0 ? o.imeta[0] : requested;  // columns of vkeep
+    for (int e = tid; e < w * rq; e += nt) {
+        const int x = e / rq, c = e % rq;
         o.vkeep[e] = c < r ? V[x * ldv + kept[c]] : 0.0;
     }
 }

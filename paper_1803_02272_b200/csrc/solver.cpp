@@ -3,6 +3,7 @@
 // enqueued on the library stream with no host round trip until the final
 // read-back (ref src/rsvd.cpp:81-145, src/mds.cpp:14-124).
 #include "solver.hpp"
+#include "device_utils.cuh"
 
 #include <algorithm>
 #include <atomic>
@@ -160,9 +161,10 @@ struct RunOut {
     size_t keep = 0;
     double resid = 0.0;
     Embedding emb;
+    std::vector<double> vectors;  // EigsVectors: n x keep
 };
 
-enum class What { Eigs, Embed, Range };
+enum class What { Eigs, Embed, Range, EigsVectors };
 
 RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What what,
            size_t requested, double* range_out) {
@@ -345,6 +347,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     product(P0, P1);
     launch_panel_dot(P0, P1, n_pad, wp, psmall, wmat, c.sms, c.stream);
     const size_t req = what == What::Embed ? requested : std::min(rank, w);
+    // eigenvector mode: k_evd keeps the first `keep` vectors whatever their sign
+    const int evd_req = what == What::EigsVectors ? -1 : static_cast<int>(req);
     EvdOut eo;
     eo.vals = static_cast<double*>(c.scratch("evd_vals", kMaxWP * sizeof(double)));
     eo.vkeep = static_cast<double*>(c.scratch("evd_vkeep", w * std::max<size_t>(req, 1) * 8));
@@ -352,8 +356,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     eo.dmeta = static_cast<double*>(c.scratch("evd_dmeta", 8 * sizeof(double)));
     eo.imeta = static_cast<int*>(c.scratch("evd_imeta", 8 * sizeof(int)));
     mark("ritz_gram");
-    launch_evd(wmat, wp, wi, static_cast<int>(rank), static_cast<int>(req), scal_dev, fro_index,
-               eo, c.stream);
+    launch_evd(wmat, wp, wi, static_cast<int>(rank), evd_req, scal_dev, fro_index, eo, c.stream);
     mark("evd");
     double* coords = nullptr;
     std::shared_ptr<DevBuf> dcoords;
@@ -367,6 +370,16 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
             c.scratch("lift_part", (static_cast<size_t>(P) * 2 + 1) * std::max<size_t>(req, 1) * 8));
         launch_lift(P0, n, wp, wi, eo.vkeep, eo.kept_vals, eo.imeta, static_cast<int>(req),
                     coords, lp, c.sms, c.stream);
+    }
+    std::unique_ptr<DevBuf> dvec;
+    if (what == What::EigsVectors) {
+        // U = Q V_keep for the keep Ritz pairs (no sign rule, no scaling)
+        dvec = std::make_unique<DevBuf>(n * std::max<size_t>(req, 1) * 8);
+        const int P = lift_grid(n, c.sms);
+        double* lp = static_cast<double*>(
+            c.scratch("lift_part", (static_cast<size_t>(P) * 2 + 1) * std::max<size_t>(req, 1) * 8));
+        launch_lift_partial(P0, n, wp, wi, eo.vkeep, eo.imeta, static_cast<int>(req),
+                            dvec->as<double>(), lp, 0, P, c.stream);
     }
     DSB_CUDA(cudaGetLastError());
     // read back into pinned memory, one sync for all of it
@@ -404,6 +417,10 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     out.vals.assign(meta.vals, meta.vals + w);
     out.keep = static_cast<size_t>(meta.imeta[0]);
     out.resid = meta.dmeta[0];
+    if (dvec) {
+        out.vectors.resize(n * out.keep);
+        c.d2h_copy(out.vectors.data(), dvec->p, out.vectors.size() * sizeof(double));
+    }
     if (what == What::Embed) {
         Embedding& e = out.emb;
         e.n = n;
@@ -463,6 +480,20 @@ Spectrum eigs_sym(const Matrix& g, const SolverOptions& opts) {
     Spectrum s;
     s.eigenvalues.assign(r.vals.begin(), r.vals.begin() + r.keep);
     s.resid = r.resid;
+    return s;
+}
+
+Spectrum eigs_sym_vectors(const Matrix& g, const SolverOptions& opts) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    if (g.store->sharded)
+        throw Error(errc::invalid_argument, "eigenvectors are not available on row shards");
+    RunOut r = run(g, opts.rank, opts.oversampling, opts.power_iters, opts.seed,
+                   What::EigsVectors, opts.rank, nullptr);
+    Spectrum s;
+    s.eigenvalues.assign(r.vals.begin(), r.vals.begin() + r.keep);
+    s.resid = r.resid;
+    s.vectors = std::move(r.vectors);
     return s;
 }
 
@@ -798,6 +829,30 @@ void hamming_counts(const char* reads, size_t count, size_t length, uint32_t* ou
                    count, words, static_cast<int>(length),
                    nullptr, 0, dc.as<uint32_t>(), c.stream);
     c.d2h_copy(out, dc.p, count * count * sizeof(uint32_t));
+}
+
+// test hook (divscope_debug_omega_panel): the Omega panel exactly as a
+// solve starts from it — host fill_gaussian into the pinned buffer, H2D,
+// relayout into the k4-interleaved device panel — read back row-major
+void debug_omega_panel(uint64_t seed, size_t n, size_t w, double* out) {
+    Ctx& c = Ctx::get();
+    std::lock_guard<std::recursive_mutex> lk(c.mu);
+    if (n == 0 || w == 0 || w > static_cast<size_t>(kMaxWP))
+        throw Error(errc::invalid_argument, "bad Omega shape");
+    const int wp = static_cast<int>(round_up(w, 8));
+    const size_t n_pad = round_up(n, kRowPad);
+    DevBuf panel(n_pad * wp * sizeof(double));
+    DevBuf stage(n * w * sizeof(double));
+    c.h2d_copy(stage.p, omega_host(seed, n, w), n * w * sizeof(double));
+    launch_panel_from_rowmajor(stage.as<double>(), n, static_cast<int>(w), wp, n_pad,
+                               panel.as<double>(), c.stream);
+    std::vector<double> h(n_pad * wp);
+    c.d2h_copy(h.data(), panel.p, h.size() * sizeof(double));
+    for (size_t i = 0; i < n; ++i)
+        for (size_t k = 0; k < w; ++k) out[i * w + k] = h[pidx(i, static_cast<int>(k), wp)];
+    for (size_t i = n; i < n_pad; ++i)  // padding rows must be zero
+        for (int k = 0; k < wp; ++k)
+            if (h[pidx(i, k, wp)] != 0.0) throw Error(errc::internal, "nonzero Omega padding");
 }
 
 }  // namespace dsb

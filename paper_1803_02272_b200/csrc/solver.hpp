@@ -31,6 +31,9 @@ struct Matrix {
 struct Spectrum {
     std::vector<double> eigenvalues;  // keep = min(rank, w), reference order
     double resid = 0.0;
+    // n x keep row-major Ritz vectors, column a pairs with eigenvalues[a]
+    // (ref rsvd.hpp:29-33 Spectrum::vectors); filled by eigs_sym_vectors only
+    std::vector<double> vectors;
 };
 
 // ref src/mds.hpp:21-28
@@ -57,6 +60,8 @@ Matrix gram_from_distances(const Matrix& d);
 
 // ref src/rsvd.cpp:102-145
 Spectrum eigs_sym(const Matrix& g, const SolverOptions& opts);
+// eigs_sym with the Ritz vectors Q V_keep (ref rsvd.cpp:129-138), unsharded
+Spectrum eigs_sym_vectors(const Matrix& g, const SolverOptions& opts);
 
 // ref src/mds.cpp:116-124 (rank overrides opts.rank, p clamped to n - rank)
 Embedding embed(const Matrix& g, size_t rank, SolverOptions opts);
@@ -121,5 +126,8 @@ Matrix matrix_hamming(const char* reads, size_t count, size_t length);
 Matrix matrix_hamming_rows(const char* reads, size_t count, size_t length, size_t row_begin,
                            size_t row_end);
 void hamming_counts(const char* reads, size_t count, size_t length, uint32_t* out);
+
+// test hook: the device-resident Omega panel of a solve, row-major n x w
+void debug_omega_panel(uint64_t seed, size_t n, size_t w, double* out);
 
 }  // namespace dsb

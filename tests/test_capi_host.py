@@ -148,3 +148,16 @@ def test_synth_points_cluster_structure(ds):
     c = np.cov(pts.T)
     ev = np.sort(eigvalsh(c))[::-1]
     assert ev[:4].min() > 20 and ev[5:].max() < 2  # 4 between-cluster directions + unit noise
+
+
+def test_product_fill_gaussian_bit_exact_vs_reference(ds):
+    # the host RNG the solver fills Omega with (host_core.cpp fill_gaussian
+    # over std::mt19937_64(seed)) against the reference's own fill_gaussian
+    # (ref src/rng.hpp:26-48 through oracle/_ref, tests/golden/rng.npz),
+    # including the odd-count tail that discards the sine
+    import numpy as np
+    from pathlib import Path
+    z = np.load(Path(__file__).resolve().parent / "golden" / "rng.npz")
+    assert np.array_equal(ds.debug_fill_gaussian(7, 1001), z["gauss_7_1001"])
+    assert np.array_equal(ds.debug_fill_gaussian(0, 4096), z["gauss_0_4096"])
+    assert np.array_equal(ds.debug_fill_gaussian(42, 600), z["gauss_42_30x20"])

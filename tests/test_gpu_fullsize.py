@@ -1,0 +1,211 @@
+"""GPU parity at the BASELINE.json configurations' full sizes, past the int8
+product's int32 chunk edge, and the reference KATs that need eigenvectors.
+
+* C2 (the bench workload: n = 20,000, k 20, p 10, q 2) on both product
+  kernels (fp64 DMMA and the int8 slice product) against the oracle's
+  restatement of gram_from_distances + embed (ref src/mds.cpp:14-124,
+  src/rsvd.cpp:81-145), the gram evaluated on the fly (no n^2 G in RAM);
+* n = 8,200 and 16,500: the int8 kernel accumulates at most 256 k-steps
+  (8192 columns) in int32, then flushes and read-modify-writes its partial
+  slot (k2i_product.cu kChunk, Walk::seg_first) — one and two flushes;
+* C5 (n = 50,000 reads, Hamming D, three-byte S slices) and, with
+  DSB_SLOW=1, C3 (n = 100,000, 80 GB D, two column groups);
+* the product's Omega read back from the device, bit for bit against the
+  reference's fill_gaussian (ref src/rng.hpp:26-48);
+* acceptance check #4 (ref tests/acceptance.cpp:125-189) on the reference's
+  own input matrix (tests/golden/acceptance4.npz, std::normal_distribution
+  through oracle/_ref) and the Rayleigh-quotient KAT (ref
+  tests/test_rsvd.cpp:185-200), both through divscope_eigs_vectors.
+
+Tolerances (BASELINE north_star): eigenvalues relative 1e-10; coordinates
+per column up to sign within 1e-8 * sqrt(lambda_1); subspace sin(theta)
+1e-8; |resid^2 - resid_ref^2| <= 1e-11 ||G||_F^2.
+"""
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from helpers import coords_match_up_to_sign, rel_err, sin_subspace, with_spectrum
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+SLOW = os.environ.get("DSB_SLOW") == "1"
+
+
+def oracle_embed(oracle, d, k, p, q, seed):
+    st, rm, grand = oracle.gram_stats(d)
+    assert st == 0
+    ref = oracle.embed(k, p, q, seed, d=d, row_mean=rm, grand=grand)
+    assert ref["status"] == 0
+    return ref
+
+
+def check_embedding(e, ref):
+    assert e.dims == ref["r"]
+    assert rel_err(e.eigenvalues, ref["eigenvalues"]) < 1e-10
+    lam1 = ref["eigenvalues"][0]
+    assert coords_match_up_to_sign(e.coords, ref["coords"]) < 1e-8 * np.sqrt(lam1)
+    assert sin_subspace(e.coords, ref["coords"]) < 1e-8
+    assert e.dropped_negative_mass == pytest.approx(ref["dropped_negative_mass"], rel=1e-8,
+                                                    abs=1e-9 * lam1)
+    assert bool(e.truncated) == bool(ref["truncated"])
+
+
+def embed_on(ds, path, d, k, p, q, seed):
+    ds.set_product_path(path)
+    try:
+        e = ds.embed(ds.gram(d), rank=k, oversampling=p, power_iters=q, seed=seed)
+        kernel = ds.stats_get().last_product_kernel
+    finally:
+        ds.set_product_path(0)
+    return e, kernel
+
+
+# ---------------------------------------------------------------- Omega
+
+def test_omega_panel_bit_exact_vs_reference(ds, oracle):
+    z = np.load(GOLDEN / "rng.npz")  # ref fill_gaussian, oracle/_ref
+    assert np.array_equal(ds.debug_omega_panel(42, 30, 20).ravel(), z["gauss_42_30x20"])
+    assert np.array_equal(ds.debug_omega_panel(7, 143, 7).ravel(), z["gauss_7_1001"])
+    # the bench workload's panel (odd tail: n w = 600,000 is even; 20,001 x 29 is odd)
+    for seed, n, w in [(2, 20000, 30), (5, 20001, 29)]:
+        want = oracle.fill_gaussian(seed, n * w).reshape(n, w)
+        assert np.array_equal(ds.debug_omega_panel(seed, n, w), want)
+
+
+# ---------------------------------------------------------------- C2
+
+@pytest.fixture(scope="module")
+def c2(ds, oracle):
+    n, k, p, q, seed = 20000, 20, 10, 2, 2
+    pts = ds.synth_points(2, n, seed)
+    dm = ds.matrix_euclidean(pts)
+    d = dm.to_numpy()
+    assert np.array_equal(d, oracle.euclidean_matrix_mt(pts))  # K9 bit-exact at full size
+    ref = oracle_embed(oracle, d, k, p, q, seed)
+    yield dict(dm=dm, d=d, ref=ref, k=k, p=p, q=q, seed=seed)
+
+
+@pytest.mark.parametrize("path", [1, 2], ids=["fp64", "int8"])
+def test_c2_full_size_matches_oracle(ds, c2, path):
+    e, kernel = embed_on(ds, path, c2["dm"], c2["k"], c2["p"], c2["q"], c2["seed"])
+    assert kernel == (1 if path == 2 else 0)
+    check_embedding(e, c2["ref"])
+    # eigs on the same gram: values and resid (cancellation-prone, so
+    # compared as squares against ||G||_F^2)
+    ds.set_product_path(path)
+    try:
+        g = ds.gram(c2["dm"])
+        vals, resid = ds.eigs(g, rank=c2["k"], oversampling=c2["p"], power_iters=c2["q"],
+                              seed=c2["seed"])
+    finally:
+        ds.set_product_path(0)
+    ref = c2["ref"]
+    assert ref["r"] == len(vals) == c2["k"]  # all kept values positive at C2
+    assert rel_err(vals, ref["eigenvalues"]) < 1e-10
+    fro2 = ref["resid"] ** 2 + np.sum(ref["eigenvalues"] ** 2)
+    assert abs(resid ** 2 - ref["resid"] ** 2) <= 1e-11 * fro2
+
+
+# ---------------------------------------------------------------- int32 chunk edge
+
+@pytest.mark.parametrize("n", [8200, 16500])
+@pytest.mark.parametrize("path", [1, 2], ids=["fp64", "int8"])
+def test_int8_chunk_flush_matches_oracle(ds, oracle, n, path):
+    # nks = ceil(n / 32) = 257 / 516 k-steps: one / two int32 flushes per row
+    # block, each followed by a read-modify-write of the partial slot
+    k, p, q, seed = 16, 16, 2, 11
+    pts = ds.synth_points(1, n, 13)
+    dm = ds.matrix_euclidean(pts)
+    d = dm.to_numpy()
+    ref = oracle_embed(oracle, d, k, p, q, seed)
+    e, kernel = embed_on(ds, path, dm, k, p, q, seed)
+    assert kernel == (1 if path == 2 else 0)
+    check_embedding(e, ref)
+
+
+# ---------------------------------------------------------------- C5
+
+def test_c5_full_size_hamming_matches_oracle(ds, oracle):
+    n, k, p, q, seed = 50000, 30, 20, 2, 5
+    reads = ds.synth_reads(n, 400, 50, 0.05, seed)
+    dm = ds.matrix_hamming(reads)
+    d = dm.to_numpy()
+    # the integer counts, bit-exact on a sample of rows (the definition:
+    # differing positions, plain character comparison)
+    arr = np.frombuffer(b"".join(reads), np.uint8).reshape(n, 400)
+    rng = np.random.default_rng(1)
+    for i in rng.choice(n, 24, replace=False):
+        h = np.count_nonzero(arr != arr[i], axis=1)
+        assert np.array_equal(d[i], h.astype(np.float64) / 400.0)
+    ref = oracle_embed(oracle, d, k, p, q, seed)
+    e, kernel = embed_on(ds, 0, dm, k, p, q, seed)
+    st = ds.stats_get()
+    assert kernel == 1 and st.last_product_sdigits == 3  # three-byte Hamming slices
+    check_embedding(e, ref)
+
+
+# ---------------------------------------------------------------- C3 (slow)
+
+@pytest.mark.slow
+@pytest.mark.skipif(not SLOW, reason="C3 full size (80 GB D, ~10 min of oracle): DSB_SLOW=1")
+def test_c3_full_size_matches_oracle(ds, oracle):
+    n, k, p, q, seed = 100000, 50, 20, 2, 3
+    dm = ds.matrix_euclidean(ds.synth_points(3, n, seed))
+    e, kernel = embed_on(ds, 0, dm, k, p, q, seed)
+    assert kernel == 1 and ds.stats_get().last_product_groups >= 1
+    d = dm.to_numpy()
+    del dm
+    ref = oracle_embed(oracle, d, k, p, q, seed)
+    check_embedding(e, ref)
+
+
+# ---------------------------------------------------------------- KATs with vectors
+
+def test_acceptance4_rsvd_vs_dense(ds):
+    # ref tests/acceptance.cpp:125-189: 50 seeds, >= 49 with eigenvalue
+    # relative error <= 1e-6 and ||G - V diag(lambda) V^T||_F <= 3 x optimal
+    z = np.load(GOLDEN / "acceptance4.npz")
+    g, dense = z["g"], z["dense"]
+    k = 20
+    optimal = np.sqrt(np.sum(dense[k:] ** 2))
+    gm = ds.matrix_from_host(g)
+    good = 0
+    for seed in range(1, 51):
+        vals, vecs, _ = ds.eigs_vectors(gm, rank=k, oversampling=10, power_iters=2, seed=seed)
+        eig_rel = np.max(np.abs(vals - dense[:k]) / np.abs(dense[:k]))
+        err = np.linalg.norm(g - vecs @ np.diag(vals) @ vecs.T)
+        # and the reference's own eigs_sym on this matrix, same seed
+        assert rel_err(vals, z["ref_vals"][seed - 1]) < 1e-9
+        if eig_rel <= 1e-6 and err / optimal <= 3.0:
+            good += 1
+    assert good >= 49
+
+
+def test_rayleigh_quotient_matches_eigenvalues(ds, oracle):
+    # ref tests/test_rsvd.cpp:185-200
+    g = with_spectrum([50, 20, 10, 5, 2, 1, 0.5, 0.1, 0, 0], 321, oracle)
+    vals, vecs, _ = ds.eigs_vectors(ds.matrix_from_host(g), rank=5, oversampling=5)
+    assert vecs.shape == (10, 5)
+    for a in range(5):
+        u = vecs[:, a]
+        rq = u @ g @ u / (u @ u)
+        assert rq == pytest.approx(vals[a], rel=1e-8)
+
+
+def test_eigs_vectors_match_oracle_and_eigs(ds, oracle):
+    # the vectors of divscope_eigs_vectors are the reference's
+    # Spectrum::vectors (Q V_keep, rsvd.cpp:129-138): orthonormal, any sign
+    # kept (negative eigenvalues too), matching the oracle up to sign
+    g = with_spectrum([9.0, -7.0, 5.0, -3.0, 1.0, 0.5] + [0.0] * 34, 77, oracle)
+    vals, vecs, resid = ds.eigs_vectors(ds.matrix_from_host(g), rank=4, oversampling=6,
+                                        power_iters=2, seed=3)
+    st, ovals, ovecs, oresid = oracle.eigs(4, 6, 2, 3, g=g)
+    assert st == 0
+    assert rel_err(vals, ovals) < 1e-10
+    assert coords_match_up_to_sign(vecs, ovecs) < 1e-9
+    np.testing.assert_allclose(vecs.T @ vecs, np.eye(4), atol=1e-12)
+    v2, r2 = ds.eigs(ds.matrix_from_host(g), rank=4, oversampling=6, power_iters=2, seed=3)
+    assert np.array_equal(v2, vals) and r2 == resid
