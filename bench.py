@@ -2,26 +2,33 @@
 """bench.py — BASELINE.json metric "MDS distance entries/s per streaming pass;
 achieved HBM GB/s as % of roofline" on the B200 path.
 
-Workload (default C2 = BASELINE.json configs[1], the largest config quoted for
-one GPU): n = 20,000 points from a seeded mixture of 20 Gaussian clusters in
-R^50 (Dirichlet(1) weights), fp64 Euclidean D (3.2 GB), classical MDS with
-k = 20, p = 10, q = 2. Inputs are seeded synthetic data generated with the
-reference's RNG conventions.
+Workload: at N = 1 (default) C2 = BASELINE.json configs[1], the config quoted
+for one GPU: n = 20,000 points from a seeded mixture of 20 Gaussian clusters
+in R^50 (Dirichlet(1) weights), fp64 Euclidean D (3.2 GB), classical MDS with
+k = 20, p = 10, q = 2. At N > 1 (torchrun) the default is C3 = configs[2]
+(n = 100,000, 80 GB D, k 50, p 20, q 2) with n FIXED (strong scaling), D
+row-sharded over the ranks. Inputs are seeded synthetic data generated with
+the reference's RNG conventions.
 
 One *step* = one full classical MDS of D through the public API:
-  divscope_gram (pass 0: K1 reads D once) + divscope_embed (2q + 2 = 6 streaming
+  divscope_gram (pass 0: K1 reads D once) + divscope_embed (2q + 2 streaming
   product passes over D, CholeskyQR, Rayleigh-Ritz EVD, lift / sign / scale)
-so a step makes 2q + 3 = 7 streaming passes over D, and
+so a step makes 2q + 3 streaming passes over D, and
   value = n^2 * (2q + 3) * steps / time      [entries/s per streaming pass]
-  e2e   = same metric through the C ABI from a pinned HOST copy of D, the
-          host->device copy of D and Omega and the device->host read of the
-          coordinates inside the timed region.
-D (3.2 GB) is larger than the 126 MB L2, so every pass streams from HBM.
+  e2e   = same metric through the C ABI from a pinned HOST copy of D: the
+          host->device copy of D (the step's input) and the device->host read
+          of the coordinates are inside the timed region. Omega is a pure
+          function of (seed, n, w): the library generates it on the host once
+          and keeps the device panel resident, so it is not re-uploaded.
+D is larger than the 126 MB L2 at C2..C5, so every pass streams from HBM.
 
---impl reference times the reference's own CPU implementation of the
-streaming pass (multiply_sym, ref src/rsvd.cpp:18-36, compiled from the
-reference sources into oracle/_ref; the oracle port when _ref is absent) on
-the same D, with all host threads: one step = one pass.
+cpu_baseline (N = 1, rank 0) and --impl reference time the reference's own
+CPU implementation of the path — gram_from_distances + embed (ref
+src/mds.cpp:14-124, src/rsvd.cpp:18-145), compiled from the reference sources
+into oracle/_ref — with every host thread. The reference arm synthesizes its
+inputs with the oracle (never the product library). The N = 1 line also
+carries `parity`: the timed GPU embedding against that reference embedding
+(outside every timed region).
 """
 from __future__ import annotations
 
@@ -127,60 +134,154 @@ def dist_init():
     return world, rank, local
 
 
-def cpu_reference_pass(d_host: np.ndarray, omega: np.ndarray, steps: int, warmup: int):
-    """Time the reference streaming pass (multiply_sym) on the host cores.
-    Returns (seconds per pass list, kind, cores)."""
+def host_ram_bytes() -> int:
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except Exception:  # pragma: no cover
+        return 64 << 30
+
+
+def host_distance(wl: str) -> np.ndarray:
+    """D of a workload built on the host by the oracle (bit-identical to the
+    device builders K9 / K7, pinned by the tests) — no product code."""
+    from oracle_bindings import Oracle
+    cfg, n, k, p, q, seed, f32 = WORKLOADS[wl]
+    o = Oracle()
+    if cfg == 5:
+        return o.hamming_matrix_mt(o.synth_reads(n, 400, 50, 0.05, seed), 400)
+    d = o.euclidean_matrix_mt(o.synth_points(cfg, n, seed))
+    return d.astype(np.float32).astype(np.float64) if f32 else d
+
+
+def reference_path(n: int):
+    """The reference's own build when it is available and G fits next to D in
+    host RAM (the reference materializes G), else the oracle port (G on the
+    fly, same loops). Returns (lib, kind)."""
     from oracle_bindings import Oracle, RefLib, ref_available
-    cores = os.cpu_count() or 1
-    if ref_available():
-        lib, kind = RefLib(), "reference"
-        st, g = lib.gram(d_host, threads=cores)
+    if ref_available() and 2 * n * n * 8 < 0.45 * host_ram_bytes():
+        return RefLib(), "reference"
+    return Oracle(), "port"
+
+
+def reference_step(lib, kind, d, k, p, q, seed, cores):
+    """One step of the reference CPU path: gram_from_distances + embed."""
+    if kind == "reference":
+        st, g = lib.gram(d, threads=cores)
         assert st == 0, "reference gram failed"
-        run = lambda: lib.multiply_sym(g, omega, threads=cores)  # noqa: E731
+        e = lib.embed(g, k, p, q, seed, threads=cores)
+        del g
     else:
-        lib, kind = Oracle(), "port"
-        st, rm, grand = lib.gram_stats(d_host)
+        st, rm, grand = lib.gram_stats(d)
         assert st == 0
-        run = lambda: lib.multiply_gram_otf(d_host, rm, grand, omega, threads=cores)  # noqa: E731
-    for _ in range(warmup):
-        run()
-    times = []
-    for _ in range(steps):
+        e = lib.embed(k, p, q, seed, d=d, row_mean=rm, grand=grand)
+    assert e["status"] == 0, "reference embed failed"
+    return e
+
+
+def parity_block(e, ref) -> dict:
+    """The GPU embedding of the timed region against the reference's."""
+    from helpers import coords_match_up_to_sign, rel_err, sin_subspace
+    out = {"against": "reference gram_from_distances + embed (oracle/_ref)",
+           "dims": [int(e.dims), int(ref["r"])]}
+    if e.dims == ref["r"] and e.dims:
+        lam1 = float(ref["eigenvalues"][0])
+        out.update(eig_max_rel_err=float(rel_err(e.eigenvalues, ref["eigenvalues"])),
+                   coord_max_err_over_sqrt_lambda1=float(
+                       coords_match_up_to_sign(e.coords, ref["coords"]) / math.sqrt(lam1)),
+                   sin_theta=float(sin_subspace(e.coords, ref["coords"])),
+                   dropped_negative_mass=[float(e.dropped_negative_mass),
+                                          float(ref["dropped_negative_mass"])])
+        out["ok"] = bool(out["eig_max_rel_err"] < 1e-10 and
+                         out["coord_max_err_over_sqrt_lambda1"] < 1e-8)
+    else:
+        out["ok"] = False
+    return out
+
+
+def cpu_sample(d, wl: str, budget_s: float = 20.0):
+    """cpu_baseline on a bounded sample: the full reference step when it fits
+    the budget (then also the reference embedding for the parity block),
+    else one reference product pass over a block of rows (entries/s per
+    pass over the block). Returns (baseline dict, reference embedding|None)."""
+    cfg, n, k, p, q, seed, f32 = WORKLOADS[wl]
+    cores = os.cpu_count() or 1
+    passes = 2 * q + 3
+    w = k + min(p, n - k)
+    lib, kind = reference_path(n)
+    if n <= 20000:
         t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-    return times, kind, cores
+        ref = reference_step(lib, kind, d, k, p, q, seed, cores)
+        t = time.perf_counter() - t0
+        return ({"value": n * n * passes / t, "unit": "entries/s", "cores": cores, "kind": kind,
+                 "sample": f"one full reference step at {wl}: gram_from_distances + embed "
+                           f"(n={n}, k={k}, p={p}, q={q}; {passes} passes incl. the gram), "
+                           f"{cores} threads, {t:.1f} s"}, ref)
+    from oracle_bindings import Oracle
+    o = Oracle()
+    st, rm, grand = o.gram_stats(d)
+    omega = o.fill_gaussian(seed, n * w).reshape(n, w)
+    rows = 256
+    t = 0.0
+    while True:  # grow the row block until the sample takes ~2 s (capped)
+        t0 = time.perf_counter()
+        o.multiply_gram_otf_rows(d, rm, grand, omega, 0, rows, threads=cores)
+        t = time.perf_counter() - t0
+        if t > 2.0 or rows >= n or t * (n / rows) < budget_s:
+            break
+        rows = min(n, rows * 4)
+    return ({"value": rows * n / t, "unit": "entries/s", "cores": cores, "kind": "port",
+             "sample": f"reference product pass (multiply_sym over the on-the-fly gram, "
+                       f"ref src/rsvd.cpp:18-36) over rows 0..{rows} of {wl} (n={n}, w={w}), "
+                       f"{cores} threads, {t:.2f} s; gram stats untimed"}, None)
 
 
 def reference_arm(args, wl):
+    """--impl reference: the reference's own CPU path on the host cores (rank
+    0 only under torchrun). Each step is one full gram_from_distances + embed;
+    the number of timed steps is bounded so the run stays within minutes."""
     world, rank, _ = dist_init()
     cfg, n, k, p, q, seed, f32 = WORKLOADS[wl]
-    metric = "MDS distance entries/s per streaming pass"
     if rank != 0:
         return 0
-    import paper_1803_02272_b200 as ds  # host-only synthesis (no GPU work)
-    from oracle_bindings import Oracle
-    pts = ds.synth_points(cfg, n, seed)
-    d = Oracle().euclidean_matrix_mt(pts)
-    if f32:
-        d = d.astype(np.float32).astype(np.float64)
-    w = k + min(p, n - k)
-    omega = Oracle().fill_gaussian(seed, n * w).reshape(n, w)
-    steps = max(1, args.steps)
-    times, kind, cores = cpu_reference_pass(d, omega, steps, max(0, min(args.warmup, 1)))
-    t = float(np.mean(times))
-    value = n * n / t
+    cores = os.cpu_count() or 1
+    passes = 2 * q + 3
+    d = host_distance(wl)
+    if n <= 20000:
+        lib, kind = reference_path(n)
+        t0 = time.perf_counter()
+        reference_step(lib, kind, d, k, p, q, seed, cores)  # warm-up (page cache, threads)
+        t_w = time.perf_counter() - t0
+        steps = max(1, min(args.steps, int(150.0 / max(t_w, 1e-3))))
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            reference_step(lib, kind, d, k, p, q, seed, cores)
+            times.append(time.perf_counter() - t0)
+        t = float(np.mean(times))
+        value = n * n * passes / t
+        sample = (f"{steps} x (gram_from_distances + embed) at {wl}, n={n}, k={k}, p={p}, "
+                  f"q={q}, {cores} threads ("
+                  f"{'oracle/_ref: the reference sources' if kind == 'reference' else 'oracle port, G on the fly'})")
+    else:
+        # a full reference step at this n takes minutes to hours (and G would
+        # not fit next to D): each step is the reference product pass over a
+        # block of rows, timed as entries/s per pass
+        base, _ = cpu_sample(d, wl, budget_s=5.0)
+        kind, steps, t = base["kind"], 1, 0.0
+        value = base["value"]
+        sample = base["sample"]
     line = {
-        "impl": "reference", "metric": metric, "value": value, "unit": "entries/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, reference RNG conventions)",
+        "impl": "reference", "metric": "MDS distance entries/s per streaming pass",
+        "value": value, "unit": "entries/s", "n_gpus": args.gpus, "steps": steps,
+        "steps_requested": args.steps, "warmup": 1, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, reference RNG conventions; built by the oracle on the host)",
         "config": {"workload": wl, "n": n, "k": k, "p": p, "q": q, "seed": seed,
-                   "d_dtype": "f32" if f32 else "f64",
-                   "step": "one reference multiply_sym pass over the materialized gram"},
+                   "d_dtype": "f32" if f32 else "f64", "streaming_passes_per_step": passes,
+                   "step": "reference gram_from_distances + embed on the host cores"},
         "cpu_baseline": {"value": value, "unit": "entries/s", "cores": cores, "kind": kind,
-                         "sample": f"{steps} x multiply_sym(G[{n}x{n}], Omega[{n}x{w}]), "
-                                   f"{cores} threads (ref src/rsvd.cpp:18-36)"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -202,9 +303,9 @@ def b200_arm(args, wl):
     cfg, n, k, p, q, seed, f32 = WORKLOADS[wl]
     n1 = n
     sharded = world > 1 or args.force_sharded
-    if sharded and not args.strong:
-        # weak scaling: every GPU streams the same n1^2 entries of D per pass,
-        # the matrix grows as n = n1 sqrt(N) (row-sharded over the N GPUs)
+    if sharded and args.weak:
+        # weak scaling (opt-in): every GPU streams the same n1^2 entries of D
+        # per pass, the matrix grows as n = n1 sqrt(N)
         n = int(round(n1 * math.sqrt(world)))
     w = k + min(p, n - k)
     passes = 2 * q + 3
@@ -367,21 +468,20 @@ def b200_arm(args, wl):
                "d2h_bytes_per_step": int(st2.d2h_bytes // max(args.steps, 1))}
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle_bindings import Oracle
-        omega = Oracle().fill_gaussian(seed, n * w).reshape(n, w)
-        dd = D.to_numpy()
-        times, kind, cores = cpu_reference_pass(dd, omega, 1, 0)
-        cpu = {"value": n * n / times[0], "unit": "entries/s", "cores": cores, "kind": kind,
-               "sample": f"one multiply_sym pass (ref src/rsvd.cpp:18-36) over the materialized "
-                         f"{wl} gram, n={n}, w={w}, {cores} threads; gram build untimed"}
+        dd = D.to_numpy()  # the same D the GPU streamed (K9/K7 output)
+        cpu, ref = cpu_sample(dd, wl)
+        if ref is not None:
+            parity = parity_block(e, ref)
+        del dd
 
     if rank == 0:
         line = {
             "metric": "MDS distance entries/s per streaming pass", "value": value,
             "unit": "entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if (sharded and args.strong) else "weak",
+            "scaling": "weak" if (world == 1 or args.weak) else "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, reference RNG conventions; D built on the GPU)",
             "config": {"workload": wl, "n": n, "n_single_gpu": n1, "k": k, "p": p, "q": q,
@@ -394,6 +494,7 @@ def b200_arm(args, wl):
             "gpu_launches": int(st.kernel_launches),
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clk.summary(),
             "result_check": {"dims": int(e.dims), "lambda_1": float(e.eigenvalues[0])
                              if e.dims else None},
@@ -430,18 +531,21 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: C2 at N = 1, C3 (fixed n, strong scaling) at N > 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (huge D)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the row-sharded path even on one GPU (testing)")
-    ap.add_argument("--strong", action="store_true",
-                    help="N > 1: keep the workload's n (strong scaling); default grows n as "
-                         "n1 sqrt(N) so each GPU streams n1^2 entries per pass (weak scaling)")
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: grow n as n1 sqrt(N) so each GPU streams n1^2 entries per pass "
+                         "(weak scaling); default keeps the workload's n (strong scaling)")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    wl = args.workload or ("C3" if max(world, args.gpus) > 1 else "C2")
     if args.impl == "reference":
-        return reference_arm(args, args.workload)
-    return b200_arm(args, args.workload)
+        return reference_arm(args, wl)
+    return b200_arm(args, wl)
 
 
 if __name__ == "__main__":

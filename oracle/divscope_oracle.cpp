@@ -453,6 +453,72 @@ void orc_multiply_sym(const double* g, std::size_t n, const double* m, std::size
     multiply(op, m, k, out, threads);
 }
 
+// 2-bit code of A,C,G,T = 0,1,2,3; anything else -> -1.
+static int base_code(char c) {
+    switch (c) {
+        case 'A': return 0;
+        case 'C': return 1;
+        case 'G': return 2;
+        case 'T': return 3;
+        default: return -1;
+    }
+}
+
+// rows [row_begin, row_end) of the same pass (a bounded CPU-baseline sample:
+// each output row is computed exactly as in the full pass)
+void orc_multiply_gram_otf_rows(const double* d, std::size_t n, const double* row_mean,
+                                double grand, const double* m, std::size_t k,
+                                std::size_t row_begin, std::size_t row_end, unsigned threads,
+                                double* out) {
+    GramOp op{nullptr, d, row_mean, grand, n};
+    op.row_sym = exact_symmetric(d, n, threads);
+    const std::size_t rows = row_end - row_begin;
+    chunks(rows, threads, [&](std::size_t b, std::size_t e) {
+        std::vector<double> grow(n);
+        for (std::size_t i = row_begin + b; i < row_begin + e; ++i) {
+            double* out_row = out + (i - row_begin) * k;
+            std::fill(out_row, out_row + k, 0.0);
+            for (std::size_t j = 0; j < n; ++j) grow[j] = op.at(i, j);
+            for (std::size_t j = 0; j < n; ++j) {
+                const double gij = grow[j];
+                if (gij == 0.0) continue;
+                const double* mrow = m + j * k;
+                for (std::size_t c = 0; c < k; ++c) out_row[c] += gij * mrow[c];
+            }
+        }
+    });
+}
+
+// Hamming counts of 2-bit packed reads (the definition of orc_hamming_counts,
+// evaluated 32 positions per 64-bit word pair: a position differs iff its
+// two code bits differ in either plane), full n x n, threaded. Returns 3
+// (INVALID_CHARACTER) on a non-ACGT byte.
+int orc_hamming_matrix_mt(const char* reads, std::size_t count, std::size_t length,
+                          unsigned threads, double* d_out) {
+    const std::size_t words = (length + 63) / 64;
+    std::vector<std::uint64_t> lo(count * words, 0), hi(count * words, 0);
+    for (std::size_t i = 0; i < count; ++i)
+        for (std::size_t t = 0; t < length; ++t) {
+            const int c = base_code(reads[i * length + t]);
+            if (c < 0) return 3;
+            lo[i * words + t / 64] |= static_cast<std::uint64_t>(c & 1) << (t % 64);
+            hi[i * words + t / 64] |= static_cast<std::uint64_t>(c >> 1) << (t % 64);
+        }
+    const double len = static_cast<double>(length);
+    chunks(count, threads, [&](std::size_t b, std::size_t e) {
+        for (std::size_t i = b; i < e; ++i)
+            for (std::size_t j = 0; j < count; ++j) {
+                std::uint64_t h = 0;
+                for (std::size_t w = 0; w < words; ++w)
+                    h += static_cast<std::uint64_t>(__builtin_popcountll(
+                        (lo[i * words + w] ^ lo[j * words + w]) |
+                        (hi[i * words + w] ^ hi[j * words + w])));
+                d_out[i * count + j] = static_cast<double>(h) / len;
+            }
+    });
+    return OK;
+}
+
 // rsvd.cpp:18-36 over the gram of D evaluated on the fly (bit-identical to
 // multiply over orc_gram's output).
 void orc_multiply_gram_otf(const double* d, std::size_t n, const double* row_mean, double grand,
@@ -538,16 +604,6 @@ int orc_embed(const double* g, const double* d, const double* row_mean, double g
 
 // --- inputs without a reference implementation (C5 / Hamming, a14) -------
 
-// 2-bit code of A,C,G,T = 0,1,2,3; anything else -> -1.
-static int base_code(char c) {
-    switch (c) {
-        case 'A': return 0;
-        case 'C': return 1;
-        case 'G': return 2;
-        case 'T': return 3;
-        default: return -1;
-    }
-}
 
 // h_ij = number of positions where reads i and j differ (plain character
 // comparison: the definition, independent of any packing).
@@ -601,6 +657,92 @@ void orc_euclidean_matrix_mt(const double* pts, std::size_t n, std::size_t dim, 
                 out[i * n + j] = std::sqrt(sq);
             }
     });
+}
+
+// ---- BASELINE.json workload synthesis (test / reference-arm inputs) -------
+// Restates the seeded generators of the configs so that bench.py's
+// reference arm builds its inputs without loading the product library; a
+// CPU test pins them bit-for-bit to divscope_synth_points / _reads. The RNG
+// calls follow ref src/rng.hpp: fill_gaussian for normals,
+// uniform_open_closed / uniform_closed_open for uniforms, bounded for
+// categorical draws; DNA bases as ref tests/testdata.cpp:16-26.
+//   config 1: 5 clusters in R^20, centers N(0, 10^2 I), equal weights
+//   config 2: 20 clusters in R^50, centers N(0, 5^2 I), Dirichlet(1) weights
+//   config 3: 10 centers N(0, 20^2 I) in R^100, each with 10 sub-centers
+//             offset N(0, 3^2 I) (100 equal-weight clusters)
+//   config 4: 100 clusters in R^64, centers N(0, 8^2 I), equal weights
+// Order of draws: centers, sub-center offsets, weights (Dirichlet only),
+// labels, then the unit within-cluster noise of all points.
+int orc_synth_points(int config, std::size_t n, std::uint64_t seed, double* out,
+                     std::size_t* dim_out) {
+    std::size_t dim, top, sub = 0;
+    double csd, ssd = 0.0;
+    bool dir = false;
+    switch (config) {
+        case 1: dim = 20; top = 5; csd = 10.0; break;
+        case 2: dim = 50; top = 20; csd = 5.0; dir = true; break;
+        case 3: dim = 100; top = 10; csd = 20.0; sub = 10; ssd = 3.0; break;
+        case 4: dim = 64; top = 100; csd = 8.0; break;
+        default: return INVALID_ARGUMENT;
+    }
+    std::mt19937_64 eng(seed);
+    std::vector<double> ctr(top * dim);
+    gaussian(eng, ctr.data(), ctr.size());
+    for (double& v : ctr) v *= csd;
+    std::size_t nclu = top;
+    if (sub) {
+        nclu = top * sub;
+        std::vector<double> off(nclu * dim);
+        gaussian(eng, off.data(), off.size());
+        for (std::size_t k = 0; k < nclu; ++k)
+            for (std::size_t c = 0; c < dim; ++c)
+                off[k * dim + c] = ctr[(k / sub) * dim + c] + ssd * off[k * dim + c];
+        ctr.swap(off);
+    }
+    std::vector<std::size_t> lab(n);
+    if (dir) {
+        std::vector<double> e(nclu), cdf(nclu);
+        double sum = 0.0;
+        for (double& x : e) {
+            x = -std::log(u_open_closed(eng));
+            sum += x;
+        }
+        double run = 0.0;
+        for (std::size_t k = 0; k < nclu; ++k) cdf[k] = (run += e[k] / sum);
+        for (std::size_t i = 0; i < n; ++i) {
+            const double u = u_closed_open(eng);
+            std::size_t k = 0;
+            while (k + 1 < nclu && !(u < cdf[k])) ++k;
+            lab[i] = k;
+        }
+    } else {
+        for (std::size_t i = 0; i < n; ++i) lab[i] = bounded(eng, nclu);
+    }
+    gaussian(eng, out, n * dim);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t c = 0; c < dim; ++c) out[i * dim + c] += ctr[lab[i] * dim + c];
+    if (dim_out) *dim_out = dim;
+    return OK;
+}
+
+// config 5 reads: `ancestors` uniform random sequences (a base per
+// bounded(4) draw), each read copies a bounded(ancestors)-chosen ancestor and
+// substitutes each base with probability sub_rate (uniform_closed_open <
+// rate) by one of the three other bases, (b + 1 + bounded(3)) mod 4.
+void orc_synth_reads(std::size_t count, std::size_t length, std::size_t ancestors,
+                     double sub_rate, std::uint64_t seed, char* out) {
+    const char acgt[4] = {'A', 'C', 'G', 'T'};
+    std::mt19937_64 eng(seed);
+    std::vector<unsigned char> anc(ancestors * length);
+    for (auto& b : anc) b = static_cast<unsigned char>(bounded(eng, 4));
+    for (std::size_t i = 0; i < count; ++i) {
+        const std::size_t a = bounded(eng, ancestors);
+        for (std::size_t t = 0; t < length; ++t) {
+            std::size_t b = anc[a * length + t];
+            if (u_closed_open(eng) < sub_rate) b = (b + 1 + bounded(eng, 3)) % 4;
+            out[i * length + t] = acgt[b];
+        }
+    }
 }
 
 // sum_i sum_j of the explicit reconstruction error (mds.cpp:126-150)

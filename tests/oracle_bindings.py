@@ -62,6 +62,13 @@ class Oracle:
         L.orc_reconstruction_error.argtypes = [_dp, _sz, _dp, _sz]
         L.orc_reconstruction_error.restype = C.c_double
         L.orc_stable_rank.argtypes = [_dp, _sz, C.c_uint, _dp]
+        L.orc_synth_points.argtypes = [C.c_int, _sz, _u64, _dp, C.POINTER(_sz)]
+        L.orc_multiply_gram_otf_rows.argtypes = [_dp, _sz, _dp, C.c_double, _dp, _sz, _sz, _sz,
+                                                 C.c_uint, _dp]
+        L.orc_multiply_gram_otf_rows.restype = None
+        L.orc_hamming_matrix_mt.argtypes = [C.c_char_p, _sz, _sz, C.c_uint, _dp]
+        L.orc_synth_reads.argtypes = [_sz, _sz, _sz, C.c_double, _u64, C.c_char_p]
+        L.orc_synth_reads.restype = None
         L.orc_sw_align.argtypes = [C.c_char_p, _sz, C.c_char_p, _sz, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(C.c_longlong)]
         L.orc_sw_distance.argtypes = [C.c_char_p, _sz, C.c_char_p, _sz, C.c_int, C.c_int, C.c_int,
@@ -147,6 +154,38 @@ class Oracle:
         out = np.empty((n, n))
         self.lib.orc_euclidean_matrix(_ptr(np.ascontiguousarray(pts)), n, dim, _ptr(out))
         return out
+
+    def multiply_gram_otf_rows(self, d, row_mean, grand, m, row_begin, row_end,
+                               threads: int | None = None):
+        n, k = m.shape
+        out = np.empty((row_end - row_begin, k), np.float64)
+        self.lib.orc_multiply_gram_otf_rows(_ptr(d), n, _ptr(row_mean), grand,
+                                            _ptr(np.ascontiguousarray(m)), k, row_begin, row_end,
+                                            threads or _threads(), _ptr(out))
+        return out
+
+    def hamming_matrix_mt(self, reads, length: int, threads: int | None = None) -> np.ndarray:
+        n = len(reads)
+        out = np.empty((n, n))
+        st = self.lib.orc_hamming_matrix_mt(b"".join(reads), n, length, threads or _threads(),
+                                            _ptr(out))
+        assert st == 0, "non-ACGT read"
+        return out
+
+    def synth_points(self, config: int, n: int, seed: int) -> np.ndarray:
+        dims = {1: 20, 2: 50, 3: 100, 4: 64}
+        out = np.empty((n, dims[config]))
+        dim = _sz(0)
+        st = self.lib.orc_synth_points(config, n, seed, _ptr(out), C.byref(dim))
+        assert st == 0 and dim.value == dims[config]
+        return out
+
+    def synth_reads(self, count: int, length: int = 400, ancestors: int = 50,
+                    sub_rate: float = 0.05, seed: int = 0) -> list:
+        buf = C.create_string_buffer(count * length)
+        self.lib.orc_synth_reads(count, length, ancestors, C.c_double(sub_rate), seed, buf)
+        raw = buf.raw
+        return [raw[i * length:(i + 1) * length] for i in range(count)]
 
     def euclidean_matrix_mt(self, pts: np.ndarray, threads: int | None = None) -> np.ndarray:
         n, dim = pts.shape

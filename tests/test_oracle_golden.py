@@ -149,3 +149,28 @@ def test_sw_oracle_matches_reference_fixture(oracle):
     # error precedence (ref align.cpp:33-35): scheme first, then empty operands
     assert oracle.sw_align(b"", b"A")[0] == 6          # EMPTY_SEQUENCE
     assert oracle.sw_align(b"AC", b"A", (0, -1, -1))[0] == 17  # INVALID_ARGUMENT
+
+
+def test_oracle_synthesis_matches_product(oracle, ds):
+    # the reference arm of bench.py synthesizes its inputs with the oracle
+    # (it must not load the product): both generators, bit for bit
+    import numpy as np
+    for cfg, n, seed in [(1, 257, 1), (2, 1000, 2), (3, 700, 3), (4, 333, 4)]:
+        assert np.array_equal(oracle.synth_points(cfg, n, seed), ds.synth_points(cfg, n, seed))
+    assert oracle.synth_reads(300, 400, 50, 0.05, 5) == ds.synth_reads(300, 400, 50, 0.05, 5)
+    assert oracle.synth_reads(17, 33, 3, 0.2, 9) == ds.synth_reads(17, 33, 3, 0.2, 9)
+
+
+def test_oracle_fast_helpers_match_definitions(oracle):
+    # the packed Hamming matrix equals the plain character-count definition;
+    # a row-range product equals those rows of the full pass, bit for bit
+    import numpy as np
+    reads = oracle.synth_reads(120, 77, 4, 0.1, 3)
+    st, h = oracle.hamming_counts(b"".join(reads), 120, 77)
+    assert st == 0
+    assert np.array_equal(oracle.hamming_matrix_mt(reads, 77), h.astype(np.float64) / 77.0)
+    d = oracle.euclidean_matrix_mt(oracle.synth_points(1, 300, 2))
+    st, rm, grand = oracle.gram_stats(d)
+    m = oracle.fill_gaussian(4, 300 * 9).reshape(300, 9)
+    full = oracle.multiply_gram_otf(d, rm, grand, m)
+    assert np.array_equal(oracle.multiply_gram_otf_rows(d, rm, grand, m, 37, 211), full[37:211])
