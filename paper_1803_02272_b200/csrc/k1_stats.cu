@@ -22,7 +22,6 @@ namespace dsb {
 namespace {
 
 constexpr int kT = 64;          // tile edge
-constexpr int kK1Threads = 256; // 8 warps, 8 rows each
 
 template <typename T>
 struct Pair2;
@@ -72,6 +71,14 @@ __device__ __forceinline__ void pair_of(long long p, int nbt, int& I, int& J) {
 // sums it sequentially, and two xor-shuffles complete the 64-column row sum.
 template <typename T>
 struct K1Cfg {
+    // consumer warps: 8 for f64 tiles (HBM-bound), 16 for f32 tiles (twice the
+    // elements per byte: more warps to hide the FP64 / conversion latency).
+    // Warp w owns rows 8 (w % 8) .. +7 and column part w / 8 (H parts of 64 / H
+    // columns); each lane (row l % 8, quarter l / 8) EL consecutive columns.
+    static constexpr int CW = sizeof(T) == 4 ? 16 : 8;
+    static constexpr int H = CW / 8;
+    static constexpr int EL = 16 / H;
+    static constexpr int THREADS = CW * 32 + 32;
     static constexpr int E = sizeof(T);
     static constexpr int BC = 128 / E;           // columns per 128-byte box row
     static constexpr int NB = kT / BC;           // boxes per 64-column tile
@@ -107,7 +114,7 @@ __device__ __forceinline__ int exp_above_hi(uint32_t hmax) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kK1Threads + 32, 1)
+__global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
     k1_tile_pairs(const __grid_constant__ CUtensorMap tm, int n, int nbt,
                   double* __restrict__ part, int* __restrict__ pexp, size_t part_ld,
                   double* __restrict__ cta_stats) {
@@ -116,18 +123,22 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
     unsigned char* sm = k1_raw + ((1024u - (smem_u32(k1_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::STAGES * C::STAGE);
     uint64_t* empty = full + C::STAGES;
-    __shared__ double red[4][kK1Threads / 32];
+    // tile-pair coordinates of each stage, written by the producer before its
+    // expect_tx arrival (release) and read after the full wait (acquire), so
+    // the consumers do not each re-derive them (a double sqrt per pair)
+    int2* stage_ij = reinterpret_cast<int2*>(empty + C::STAGES);
+    __shared__ double red[4][C::CW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long npairs = static_cast<long long>(nbt) * (nbt + 1) / 2;
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kK1Threads / 32);
+            mbar_init(&empty[s], C::CW);
         }
         fence_mbar_init();
     }
     __syncthreads();
-    if (warp == kK1Threads / 32) {  // producer
+    if (warp == C::CW) {  // producer
         if (lane == 0) {
             prefetch_tmap(&tm);
             int s = 0;
@@ -138,6 +149,7 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
                 int I, J;
                 pair_of(p, nbt, I, J);
                 unsigned char* st = sm + s * C::STAGE;
+                stage_ij[s] = make_int2(I, J);
                 mbar_arrive_expect_tx(&full[s], (I != J ? 2 : 1) * C::TILE);
                 for (int b = 0; b < C::NB; ++b)
                     tma_load_2d(st + b * (kT * 128), &tm, J * kT + b * C::BC, I * kT, &full[s]);
@@ -154,64 +166,106 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
         return;
     }
     double sum4 = 0.0, maxabs = 0.0, maxabs_up = 0.0, maxasym = 0.0;
-    const int r = warp * 8 + (lane & 7), q = lane >> 3;
+    float maxf = 0.0f, maxup_f = 0.0f;  // f32 tiles: the maxima in the float domain
+    const int r = (warp & 7) * 8 + (lane & 7), q = lane >> 3, h = warp >> 3;
+    const int col0 = h * (kT / C::H) + q * C::EL;  // first tile column of this lane
     int s = 0;
     uint32_t ph = 0;
     for (long long p = blockIdx.x; p < npairs; p += gridDim.x) {
-        int I, J;
-        pair_of(p, nbt, I, J);
         mbar_wait(&full[s], ph);
+        const int2 ij = stage_ij[s];
+        const int I = ij.x, J = ij.y;
         const unsigned char* A = sm + s * C::STAGE;
         const unsigned char* B = (I != J) ? A + C::TILE : A;
-        double a[16];
+        double a[C::EL];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) a[j] = static_cast<double>(*tile_at<T>(A, r, q * 16 + j));
-        double rs = 0.0;
+        for (int j = 0; j < C::EL; ++j) a[j] = static_cast<double>(*tile_at<T>(A, r, col0 + j));
+        // four independent accumulation chains (a 16-long dependent DADD chain
+        // per row segment left the FP64 latency exposed, worst with f32 tiles)
+        double rsp[4] = {0.0, 0.0, 0.0, 0.0}, s4p[4] = {0.0, 0.0, 0.0, 0.0};
         uint32_t rmx = 0u;
+        float rmaxf = 0.0f;  // f32 tiles: max |d| of the row segment
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < C::EL; ++j) {
             const double sq = a[j] * a[j];
-            rs += sq;
-            rmx = max(rmx, hi_bits(sq));
-            sum4 += sq * sq;
+            rsp[j & 3] += sq;
+            s4p[j & 3] += sq * sq;
+            const bool upper = I != J || col0 + j >= r;
             // (x > m ? x : m): NaN is never selected, as std::max(m, x) in the
             // reference's scans (mds.cpp:21-27, rsvd.cpp:50-54); cheaper than fmax
-            if (I != J || q * 16 + j >= r) maxabs_up = max_keep(maxabs_up, fabs(a[j]));
+            if constexpr (sizeof(T) == 4) {
+                // max |d| in the float domain (widening is monotonic, so the
+                // widened max is the max of the widened values); the row
+                // exponent follows from the row max: max d^2 = (max |d|)^2
+                const float af = fabsf(*tile_at<T>(A, r, col0 + j));
+                rmaxf = af > rmaxf ? af : rmaxf;
+                if (upper) maxup_f = af > maxup_f ? af : maxup_f;
+            } else {
+                rmx = max(rmx, hi_bits(sq));
+                if (upper) maxabs_up = max_keep(maxabs_up, fabs(a[j]));
+            }
             // symmetry: A[r][c] vs B[c][r] (d_ij vs d_ji)
-            const double m = static_cast<double>(*tile_at<T>(B, q * 16 + j, r));
-            maxasym = max_keep(maxasym, fabs(a[j] - m));
+            const T mt = *tile_at<T>(B, col0 + j, r);
+            if constexpr (sizeof(T) == 4) {
+                // identical bits (the symmetric case) give 0; only differing
+                // entries pay for the f64 difference the reference takes
+                if (__float_as_uint(mt) != __float_as_uint(*tile_at<T>(A, r, col0 + j)))
+                    maxasym = max_keep(maxasym, fabs(a[j] - static_cast<double>(mt)));
+            } else {
+                maxasym = max_keep(maxasym, fabs(a[j] - mt));
+            }
         }
-        if (I == J) {  // diagonal tile: maxabs_up saw only its upper part
+        if constexpr (sizeof(T) == 4) {
+            const double m = static_cast<double>(rmaxf);
+            rmx = hi_bits(m * m);
+            if (I == J) maxf = rmaxf > maxf ? rmaxf : maxf;
+        } else if (I == J) {  // diagonal tile: maxabs_up saw only its upper part
 #pragma unroll
-            for (int j = 0; j < 16; ++j) maxabs = max_keep(maxabs, fabs(a[j]));
+            for (int j = 0; j < C::EL; ++j) maxabs = max_keep(maxabs, fabs(a[j]));
         }
+        double rs = (rsp[0] + rsp[1]) + (rsp[2] + rsp[3]);
+        sum4 += (s4p[0] + s4p[1]) + (s4p[2] + s4p[3]);
         rs += __shfl_xor_sync(0xffffffffu, rs, 8);
         rs += __shfl_xor_sync(0xffffffffu, rs, 16);
         rmx = max(rmx, __shfl_xor_sync(0xffffffffu, rmx, 8));
         rmx = max(rmx, __shfl_xor_sync(0xffffffffu, rmx, 16));
         if (q == 0 && I * kT + r < n) {
-            part[static_cast<size_t>(J) * part_ld + I * kT + r] = rs;
-            pexp[static_cast<size_t>(J) * part_ld + I * kT + r] = exp_above_hi(rmx);
+            part[static_cast<size_t>(J * C::H + h) * part_ld + I * kT + r] = rs;
+            pexp[static_cast<size_t>(J * C::H + h) * part_ld + I * kT + r] = exp_above_hi(rmx);
         }
         if (I != J) {
-            double rb = 0.0;
+            double rbp[4] = {0.0, 0.0, 0.0, 0.0}, b4p[4] = {0.0, 0.0, 0.0, 0.0};
             uint32_t bmx = 0u;
+            float bmaxf = 0.0f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const double b = static_cast<double>(*tile_at<T>(B, r, q * 16 + j));
+            for (int j = 0; j < C::EL; ++j) {
+                const T bt = *tile_at<T>(B, r, col0 + j);
+                const double b = static_cast<double>(bt);
                 const double sq = b * b;
-                rb += sq;
-                bmx = max(bmx, hi_bits(sq));
-                sum4 += sq * sq;
-                maxabs = max_keep(maxabs, fabs(b));
+                rbp[j & 3] += sq;
+                b4p[j & 3] += sq * sq;
+                if constexpr (sizeof(T) == 4) {
+                    const float bf = fabsf(bt);
+                    bmaxf = bf > bmaxf ? bf : bmaxf;
+                } else {
+                    bmx = max(bmx, hi_bits(sq));
+                    maxabs = max_keep(maxabs, fabs(b));
+                }
             }
+            if constexpr (sizeof(T) == 4) {
+                const double m = static_cast<double>(bmaxf);
+                bmx = hi_bits(m * m);
+                maxf = bmaxf > maxf ? bmaxf : maxf;
+            }
+            double rb = (rbp[0] + rbp[1]) + (rbp[2] + rbp[3]);
+            sum4 += (b4p[0] + b4p[1]) + (b4p[2] + b4p[3]);
             rb += __shfl_xor_sync(0xffffffffu, rb, 8);
             rb += __shfl_xor_sync(0xffffffffu, rb, 16);
             bmx = max(bmx, __shfl_xor_sync(0xffffffffu, bmx, 8));
             bmx = max(bmx, __shfl_xor_sync(0xffffffffu, bmx, 16));
             if (q == 0 && J * kT + r < n) {
-                part[static_cast<size_t>(I) * part_ld + J * kT + r] = rb;
-                pexp[static_cast<size_t>(I) * part_ld + J * kT + r] = exp_above_hi(bmx);
+                part[static_cast<size_t>(I * C::H + h) * part_ld + J * kT + r] = rb;
+                pexp[static_cast<size_t>(I * C::H + h) * part_ld + J * kT + r] = exp_above_hi(bmx);
             }
         }
         __syncwarp();
@@ -220,6 +274,10 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
             s = 0;
             ph ^= 1;
         }
+    }
+    if constexpr (sizeof(T) == 4) {
+        maxabs = static_cast<double>(maxf);
+        maxabs_up = static_cast<double>(maxup_f);
     }
     // every off-diagonal A tile entry is an upper entry: max|a| over all
     // entries = max(max over upper entries, B tiles, diagonal tiles)
@@ -235,10 +293,10 @@ __global__ void __launch_bounds__(kK1Threads + 32, 1)
         red[2][warp] = maxabs_up;
         red[3][warp] = maxasym;
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(kK1Threads));  // consumers only
+    asm volatile("bar.sync 1, %0;" ::"n"(C::CW * 32));  // consumers only
     if (threadIdx.x == 0) {
         double su = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
-        for (int w = 0; w < kK1Threads / 32; ++w) {
+        for (int w = 0; w < C::CW; ++w) {
             su += red[0][w];
             m1 = fmax(m1, red[1][w]);
             m2 = fmax(m2, red[2][w]);
@@ -363,7 +421,7 @@ __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ ct
 
 size_t k1_part_elems(size_t n) {
     const size_t nbt = (n + kT - 1) / kT;
-    return nbt * nbt * kT;
+    return nbt * nbt * kT * 2;  // up to 2 column parts per tile (f32: K1Cfg<float>::H)
 }
 
 int k1_grid(size_t n, int sms) {
@@ -380,15 +438,16 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
     const size_t part_ld = static_cast<size_t>(nbt) * kT;
     if (dt == DType::F64) {
         ensure_dyn_smem(reinterpret_cast<const void*>(k1_tile_pairs<double>), k1_smem<double>());
-        k1_tile_pairs<double><<<w.grid, kK1Threads + 32, k1_smem<double>(), st>>>(
+        k1_tile_pairs<double><<<w.grid, K1Cfg<double>::THREADS, k1_smem<double>(), st>>>(
             *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
     } else {
         ensure_dyn_smem(reinterpret_cast<const void*>(k1_tile_pairs<float>), k1_smem<float>());
-        k1_tile_pairs<float><<<w.grid, kK1Threads + 32, k1_smem<float>(), st>>>(
+        k1_tile_pairs<float><<<w.grid, K1Cfg<float>::THREADS, k1_smem<float>(), st>>>(
             *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
     }
     const int nblk = static_cast<int>((n + kRmRows - 1) / kRmRows);
-    k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, w.pexp, part_ld, nbt, static_cast<int>(n),
+    const int nparts = nbt * (dt == DType::F64 ? K1Cfg<double>::H : K1Cfg<float>::H);
+    k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, w.pexp, part_ld, nparts, static_cast<int>(n),
                                       row_mean, row_exp, w.blk_stats);
     k1_finalize<<<1, 256, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),
                                    scalars);

@@ -35,6 +35,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -140,7 +143,7 @@ constexpr bool bprod_ts();
 // 2^24 in three bytes; see launch_k2i)
 template <int NB, int SD = kDig>
 constexpr bool hybrid_ts() {
-    return NB > 32 && SD > 4 && DSB_TS_NB64_HYBRID;
+    return NB > 48 && SD > 4 && DSB_TS_NB64_HYBRID;
 }
 template <int NB, int SD = kDig>
 constexpr int tmem_digits_ts() {
@@ -153,8 +156,19 @@ constexpr int tmem_digits_ts() {
 #define DSB_TS_NA32 4
 #endif
 template <int NB, int SD = kDig>
+constexpr uint32_t a_stage_cols_ts();
+template <int NB>
+constexpr uint32_t a_base_ts();
+template <int NB, int SD = kDig>
 constexpr int a_stages_ts() {
-    return NB <= 32 ? DSB_TS_NA32 : ((hybrid_ts<NB, SD>() || 16 * SD <= 64) ? 2 : 1);
+    // NB = 32: four 64-column stages; NB = 48: the 3 x 56 columns after the
+    // 336 accumulator columns; NB = 64: two (hybrid / 3-byte) or one stage
+    return NB <= 32 ? DSB_TS_NA32
+                    : (NB <= 48 ? static_cast<int>((512u - a_base_ts<NB>()) / a_stage_cols_ts<NB, SD>()) > 4
+                                      ? 4
+                                      : static_cast<int>((512u - a_base_ts<NB>()) /
+                                                         a_stage_cols_ts<NB, SD>())
+                                : ((hybrid_ts<NB, SD>() || 16 * SD <= 64) ? 2 : 1));
 }
 #ifndef DSB_TS_ACOLS32
 #define DSB_TS_ACOLS32 64
@@ -162,14 +176,15 @@ constexpr int a_stages_ts() {
 #ifndef DSB_TS_ABASE32
 #define DSB_TS_ABASE32 256
 #endif
-template <int NB, int SD = kDig>
+template <int NB, int SD>
 constexpr uint32_t a_stage_cols_ts() {
     return SD != kDig ? 8u * SD
-                      : (hybrid_ts<NB, SD>() ? 32u : (NB <= 32 ? DSB_TS_ACOLS32 : 64u));
+                      : (hybrid_ts<NB, SD>() ? 32u
+                                             : (NB <= 32 ? DSB_TS_ACOLS32 : (NB <= 48 ? 56u : 64u)));
 }
 template <int NB>
 constexpr uint32_t a_base_ts() {  // first TMEM column of the A stages
-    return NB <= 32 ? DSB_TS_ABASE32 : 448u;
+    return NB <= 32 ? DSB_TS_ABASE32 : static_cast<uint32_t>(7 * NB);
 }
 template <int NB, int SD = kDig>
 constexpr int a_smem_stage_ts() {  // bytes of shared-memory A digits per stage
@@ -183,15 +198,22 @@ template <int NB, int SD>
 constexpr bool bprod_ts() {
     return a_stages_ts<NB, SD>() <= DSB_TS_BPROD_NA;
 }
-template <int NB, typename TD, int SD = kDig>
+// shared-memory budget of the rings: the CTA pair (NB = 48 and the pair's
+// NB = 64 launches) feeds TWO SMs' bandwidth from one D ring, so it takes the
+// maximum; the single-CTA kernel keeps the measured-best 208 KB
+#ifndef DSB_TS_PAIR_SMEM_KB
+#define DSB_TS_PAIR_SMEM_KB 224
+#endif
+template <int NB, typename TD, int SD = kDig, int CL = 1>
 constexpr int d_stages_ts() {
-    return std::min(8, (DSB_TS_SMEM_KB * 1024 - b_stages_ts<NB, SD>() * b_bytes<NB>() -
+    return std::min(8, ((CL > 1 ? DSB_TS_PAIR_SMEM_KB : DSB_TS_SMEM_KB) * 1024 -
+                        b_stages_ts<NB, SD>() * b_bytes<NB>() -
                         a_stages_ts<NB, SD>() * a_smem_stage_ts<NB, SD>()) /
                            d_bytes<TD>());
 }
-template <int NB, typename TD, int SD = kDig>
+template <int NB, typename TD, int SD = kDig, int CL = 1>
 constexpr size_t ts_smem() {
-    return 1024 + static_cast<size_t>(d_stages_ts<NB, TD, SD>()) * d_bytes<TD>() +
+    return 1024 + static_cast<size_t>(d_stages_ts<NB, TD, SD, CL>()) * d_bytes<TD>() +
            b_stages_ts<NB, SD>() * b_bytes<NB>() +
            a_stages_ts<NB, SD>() * a_smem_stage_ts<NB, SD>() + 448 + NB * 8;
 }
@@ -251,15 +273,29 @@ __device__ __forceinline__ void pack_digits(const uint32_t (&lo)[8], const uint3
     }
 }
 
-template <int NB, typename TD, int SD>
+// CL = 2: a cluster of two CTAs (on two SMs) shares every D tile — each
+// CTA TMA-loads one 64-row half of the tile and multicasts it to both, so D
+// is read from HBM once per pass — and each CTA multiplies it into its own
+// column group (panel columns cg0 + rank NB ..): two 48- or 64-column groups
+// cover w <= 128 in ONE pass, where one SM's TMEM holds at most 64 columns x
+// 7 diagonal accumulators. Both CTAs convert the whole tile (their MMAs need
+// every row's digits in their own TMEM); a slot of the D ring is refilled
+// only after the consumers of BOTH CTAs released it (each consumer warp
+// arrives on its own and on the peer's empty barrier). tmD then has 64-row
+// boxes; bdig holds the groups' digit planes bdig_stride bytes apart.
+template <int NB, typename TD, int SD, int CL>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
                    const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
                    int nks, int total, double* __restrict__ part, int maxseg, int wp, int cg0,
-                   const int* __restrict__ skip, int dbg, double hlen) {
+                   const int* __restrict__ skip, int dbg, double hlen, size_t bdig_stride) {
     if (skip && *skip) return;
+    static_assert(CL == 1 || CL == 2, "one CTA, or a pair sharing the D tiles");
+    const int crank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+    cg0 += crank * NB;
+    bdig += static_cast<size_t>(crank) * bdig_stride;
     static_assert(SD == kDig || SD == 3, "S digit counts: 7 (general) or 3 (Hamming)");
-    constexpr int ND = d_stages_ts<NB, TD, SD>();
+    constexpr int ND = d_stages_ts<NB, TD, SD, CL>();
     constexpr int NA = a_stages_ts<NB, SD>();
     // panel digits: with several A stages they ride with the A stage (loaded
     // by one converter lane when it claims the stage); with a single A stage
@@ -290,14 +326,16 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     double* colscale = reinterpret_cast<double*>(bars + 56);  // <= 34 barriers + slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cta = blockIdx.x;
-    const int t0 = static_cast<int>(static_cast<long long>(total) * cta / gridDim.x);
-    const int t1 = static_cast<int>(static_cast<long long>(total) * (cta + 1) / gridDim.x);
+    // work unit: the CTA, or the pair (both CTAs walk the same items)
+    const int cta = blockIdx.x / CL;
+    const int units = gridDim.x / CL;
+    const int t0 = static_cast<int>(static_cast<long long>(total) * cta / units);
+    const int t1 = static_cast<int>(static_cast<long long>(total) * (cta + 1) / units);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < ND; ++s) {
             mbar_init(&full_d[s], 1);
-            mbar_init(&empty_d[s], kConv);
+            mbar_init(&empty_d[s], kConv * CL);  // both CTAs' converters
         }
         for (int s = 0; s < NA; ++s) {
             // with the digits riding on the A stage, their expect_tx arrival
@@ -324,7 +362,10 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CL > 1)
+        cluster_sync_all();  // the peer's barriers are initialized before any remote use
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t tmem_a = tmem + a_base_ts<NB>();
@@ -338,8 +379,17 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
                 if (k >= ND) mbar_wait(&empty_d[sd], pd ^ 1);
                 unsigned char* dst = dring + sd * DB;
-                mbar_arrive_expect_tx(&full_d[sd], DB);
-                if constexpr (sizeof(TD) == 8) {
+                mbar_arrive_expect_tx(&full_d[sd], DB);  // the whole tile
+                if constexpr (CL > 1) {
+                    // this CTA's 64-row half of the tile, into both CTAs
+                    // (64 rows x 128 B keeps the SWIZZLE_128B phase)
+                    const int r0 = w.rb * kRowsI8 + 64 * crank;
+                    unsigned char* hd = dst + crank * (64 * 128);
+                    tma_load_2d_mc(hd, &tmD, w.ks * kKStep, r0, &full_d[sd], 0x3);
+                    if constexpr (sizeof(TD) == 8)
+                        tma_load_2d_mc(hd + kRowsI8 * 128, &tmD, w.ks * kKStep + 16, r0,
+                                       &full_d[sd], 0x3);
+                } else if constexpr (sizeof(TD) == 8) {
                     tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[sd]);
                     tma_load_2d(dst + kRowsI8 * 128, &tmD, w.ks * kKStep + 16, w.rb * kRowsI8,
                                 &full_d[sd]);
@@ -527,6 +577,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     mbar_arrive(&empty_d[sd]);
                     mbar_arrive(&full_a[sa]);
                 }
+                if constexpr (CL > 1)
+                    if (lane == 1) mbar_arrive_peer(&empty_d[sd], crank ^ 1);
             } else {
                 // single A stage: convert into registers while the MMAs of the
                 // previous k-step still read the stage, then store
@@ -548,7 +600,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     tc_fence_after();
                 }
                 if (dbg != 1) {
-                    const uint32_t ta = tmem_a + static_cast<uint32_t>(sa * 64) + lane_off;
+                    const uint32_t ta = tmem_a + static_cast<uint32_t>(sa) * ACOLS + lane_off;
 #pragma unroll
                     for (int t = 1; t <= kDig; ++t)
                         tmem_st2(ta + static_cast<uint32_t>((t - 1) * 8 + part_k * 2),
@@ -561,6 +613,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     mbar_arrive(&empty_d[sd]);
                     mbar_arrive(&full_a[sa]);
                 }
+                if constexpr (CL > 1)
+                    if (lane == 1) mbar_arrive_peer(&empty_d[sd], crank ^ 1);
             }
             if (++sd == ND) {
                 sd = 0;
@@ -617,7 +671,10 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CL > 1)
+        cluster_sync_all();  // no CTA leaves while its peer may still signal or fill it
+    else
+        __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -666,6 +723,16 @@ __global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__
     }
 }
 
+// DSB_K2I_PAIR=0: w > 64 in separate column-group passes (one read of D
+// each) instead of the CTA-pair kernel (comparisons)
+bool k2i_pair_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DSB_K2I_PAIR");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 // DSB_K2I_DEBUG: 1 = skip the digit conversion, 2 = skip the MMAs (timing
 // experiments only; results are wrong)
 int k2i_debug_mode() {
@@ -676,38 +743,113 @@ int k2i_debug_mode() {
     return m;
 }
 
-template <int NB, typename TD, int SD = kDig>
+template <int NB, typename TD, int SD = kDig, int CL = 1>
 void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
-            const int* row_exp, const int* col_exp, double* part, int cg0, cudaStream_t st,
-            const int* skip, double hlen = 0.0) {
-    ensure_dyn_smem(reinterpret_cast<const void*>(k2i_product_ts<NB, TD, SD>),
-                    ts_smem<NB, TD, SD>());
-    k2i_product_ts<NB, TD, SD><<<p.grid, kThreadsI8, ts_smem<NB, TD, SD>(), st>>>(
-        *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
-        p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen);
+            size_t bdig_stride, const int* row_exp, const int* col_exp, double* part, int cg0,
+            cudaStream_t st, const int* skip, double hlen = 0.0) {
+    const void* fn = reinterpret_cast<const void*>(k2i_product_ts<NB, TD, SD, CL>);
+    ensure_dyn_smem(fn, ts_smem<NB, TD, SD, CL>());
+    if constexpr (CL == 1) {
+        k2i_product_ts<NB, TD, SD, 1><<<p.grid, kThreadsI8, ts_smem<NB, TD, SD>(), st>>>(
+            *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
+            p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen, bdig_stride);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(p.grid * CL));
+        cfg.blockDim = dim3(kThreadsI8);
+        cfg.dynamicSmemBytes = ts_smem<NB, TD, SD, CL>();
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        DSB_CUDA(cudaLaunchKernelEx(&cfg, k2i_product_ts<NB, TD, SD, CL>, *tmap, bdig, row_exp,
+                                    col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
+                                    p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen,
+                                    bdig_stride));
+    }
+}
+
+// Co-resident CTA pairs (clusters of 2 with one ~210 KB CTA per SM): at most
+// sms / 2, fewer when some GPC leaves an SM without a partner. Queried once
+// per device for the pair kernel's shared-memory footprint.
+int pair_units(int sms) {
+    static std::mutex mu;
+    static std::map<int, int> units;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = units.find(dev);
+    if (it != units.end()) return it->second;
+    const void* fn = reinterpret_cast<const void*>(k2i_product_ts<48, double, kDig, 2>);
+    ensure_dyn_smem(fn, ts_smem<48, double, kDig, 2>());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(sms));
+    cfg.blockDim = dim3(kThreadsI8);
+    cfg.dynamicSmemBytes = ts_smem<48, double, kDig, 2>();
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = sms / 2;
+    }
+    n = std::min(n, sms / 2);
+    if (const char* e = std::getenv("DSB_K2I_UNITS")) n = std::max(1, std::min(n, std::atoi(e)));
+    if (std::getenv("DSB_TRACE")) std::fprintf(stderr, "[k2i] CTA pairs co-resident: %d\n", n);
+    units[dev] = n;
+    return n;
 }
 
 }  // namespace
 
 K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms) {
     K2iPlan p;
-    // column groups, one full pass over D each: NB = 64 groups while more
-    // than 32 columns remain, then one NB = 32 or 64 group for the rest
-    for (int c0 = 0; c0 < wp && p.ngroups < K2iPlan::kMaxGroups; ++p.ngroups) {
-        const int rest = wp - c0;
-        const int nb = rest <= 32 ? 32 : 64;
-        p.gc0[p.ngroups] = c0;
-        p.gnb[p.ngroups] = nb;
-        p.bdig_bytes = std::max(p.bdig_bytes, static_cast<size_t>((ncols + kKStep - 1) / kKStep) *
-                                                  kDig * nb * kKStep);
-        c0 += nb;
-        p.nb = c0;
+    const size_t nks = (ncols + kKStep - 1) / kKStep;
+    // the CTA pair only for 64 < WP <= 96 (two 48-column groups): at
+    // WP > 96 each CTA's 64-column digit MMAs bind (C4-like w = 120: pair
+    // 6.2 vs 5.7 ms per pass on f32 D, equal on f64), at WP <= 96 one read of
+    // D beats two (w = 70, n = 40k: 4.61 vs 5.07 ms; C3: 32.4 vs 36.3 ms)
+    if (wp <= 64 || wp > 96 || !k2i_pair_enabled()) {
+        // column groups, one full pass over D each: NB = 64 groups while more
+        // than 32 columns remain, then one NB = 32 or 64 group for the rest
+        for (int c0 = 0; c0 < wp && p.ngroups < K2iPlan::kMaxGroups; ++p.ngroups) {
+            const int rest = wp - c0;
+            const int nb = rest <= 32 ? 32 : 64;
+            p.gc0[p.ngroups] = c0;
+            p.gnb[p.ngroups] = nb;
+            p.bdig_bytes = std::max(p.bdig_bytes, nks * kDig * nb * kKStep);
+            c0 += nb;
+            p.nb = c0;
+        }
+    } else {
+        // 64 < WP <= 96: one pass, a CTA pair sharing each D tile, one
+        // 48-column group per CTA
+        const int nb = 48;
+        p.pair = true;
+        p.ngroups = 2;
+        p.gc0[0] = 0;
+        p.gc0[1] = nb;
+        p.gnb[0] = p.gnb[1] = nb;
+        p.nb = 2 * nb;
+        p.bdig_stride = nks * kDig * nb * kKStep;
+        p.bdig_bytes = 2 * p.bdig_stride;
+        sms = 2 * pair_units(sms);  // the work units below are pairs
     }
     p.nrows = static_cast<int>(nrows);
     p.nblk = static_cast<int>((nrows + kRowsI8 - 1) / kRowsI8);
     p.nks = static_cast<int>((ncols + kKStep - 1) / kKStep);
     p.total = static_cast<long long>(p.nblk) * p.nks;
-    p.grid = static_cast<int>(std::min<long long>(sms, p.total));
+    // work units (CTAs, or CTA pairs): one partial slot each
+    p.grid = static_cast<int>(std::min<long long>(p.pair ? sms / 2 : sms, p.total));
     int maxseg = 1;
     for (long long c = 0; c < p.grid; ++c) {
         const long long a = p.total * c / p.grid, b = p.total * (c + 1) / p.grid;
@@ -721,11 +863,11 @@ K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms) {
 
 bool k2i_supported(int wp) { return wp >= 8 && wp <= 128; }
 
-void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, const double* x,
-                size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
-                unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
-                const double* colsums, double* y, size_t y_rows_pad, cudaStream_t st,
-                cudaEvent_t e0, cudaEvent_t e1, const int* skip, int hamming_len) {
+void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt, const K2iPlan& p,
+                int wp, const double* x, size_t x_rows_pad, const int* row_exp, double* pmax,
+                int* col_exp, unsigned char* bdig, double* part, const double* row_mean,
+                const double* scalars, const double* colsums, double* y, size_t y_rows_pad,
+                cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, const int* skip, int hamming_len) {
     // k2_reduce writes the 128-row blocks; the panel rows beyond them (up to
     // the 256-row padding) must read as zero, whatever an earlier, larger
     // solve left in this workspace
@@ -735,38 +877,66 @@ void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, 
                                  st));
     (void)x_rows_pad;
     (void)pmax;  // column exponents come from launch_colsums (same pass over X)
-    for (int g = 0; g < p.ngroups; ++g) {
-        const int nb = p.gnb[g], cg0 = p.gc0[g];
-        {
-            const long long items = static_cast<long long>(p.nks) * nb * 8;
-            const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
-            k_panel_digits<<<grid, 256, 0, st>>>(x, p.nks, wp, nb, cg0, col_exp, bdig);
+    auto digits = [&](int nb, int cg0, unsigned char* dst) {
+        const long long items = static_cast<long long>(p.nks) * nb * 8;
+        const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
+        k_panel_digits<<<grid, 256, 0, st>>>(x, p.nks, wp, nb, cg0, col_exp, dst);
+    };
+    const double hl = static_cast<double>(hamming_len);
+    const bool ham = dt == DType::F64 && hamming_len > 0;
+    if (p.pair) {
+        // one launch: the CTA pair shares every D tile (64-row multicast
+        // boxes), CTA r computes panel columns gc0[r] .. with its digits
+        const int nb = p.gnb[0];
+        digits(nb, p.gc0[0], bdig);
+        digits(nb, p.gc0[1], bdig + p.bdig_stride);
+        if (e0) cudaEventRecord(e0, st);
+        const size_t bs = p.bdig_stride;
+        (void)nb;  // 48 (k2i_plan)
+        if (ham)
+            run_i8<48, double, 3, 2>(tmap64, p, wp, bdig, bs, row_exp, col_exp, part, 0, st, skip,
+                                     hl);
+        else if (dt == DType::F64)
+            run_i8<48, double, kDig, 2>(tmap64, p, wp, bdig, bs, row_exp, col_exp, part, 0, st,
+                                        skip);
+        else
+            run_i8<48, float, kDig, 2>(tmap64, p, wp, bdig, bs, row_exp, col_exp, part, 0, st,
+                                       skip);
+        count_launch(2);
+    } else {
+        for (int g = 0; g < p.ngroups; ++g) {
+            const int nb = p.gnb[g], cg0 = p.gc0[g];
+            digits(nb, cg0, bdig);
+            if (g == 0 && e0) cudaEventRecord(e0, st);
+            if (ham) {
+                if (nb == 32)
+                    run_i8<32, double, 3>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
+                                          skip, hl);
+                else
+                    run_i8<64, double, 3>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
+                                          skip, hl);
+            } else if (dt == DType::F64) {
+                if (nb == 32)
+                    run_i8<32, double>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
+                                       skip);
+                else
+                    run_i8<64, double>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
+                                       skip);
+            } else {
+                if (nb == 32)
+                    run_i8<32, float>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
+                                      skip);
+                else
+                    run_i8<64, float>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
+                                      skip);
+            }
         }
-        if (g == 0 && e0) cudaEventRecord(e0, st);
-        if (dt == DType::F64 && hamming_len > 0) {
-            const double hl = static_cast<double>(hamming_len);
-            if (nb == 32)
-                run_i8<32, double, 3>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip,
-                                      hl);
-            else
-                run_i8<64, double, 3>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip,
-                                      hl);
-        } else if (dt == DType::F64) {
-            if (nb == 32)
-                run_i8<32, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
-            else
-                run_i8<64, double>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
-        } else {
-            if (nb == 32)
-                run_i8<32, float>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
-            else
-                run_i8<64, float>(tmap128, p, wp, bdig, row_exp, col_exp, part, cg0, st, skip);
-        }
+        count_launch(2 * p.ngroups);
     }
     if (e1) cudaEventRecord(e1, st);
     launch_k2_reduce(wp, kRowsI8, part, p.maxseg, p.nks, p.total, p.grid, p.nrows, 1, row_mean,
                      scalars, colsums, y, st, skip);
-    count_launch(2 * p.ngroups + 1);
+    count_launch(1);
 }
 
 }  // namespace dsb

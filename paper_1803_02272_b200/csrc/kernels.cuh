@@ -105,18 +105,22 @@ struct K2iPlan {
     int gnb[kMaxGroups] = {};  // MMA N per digit of each group (32 or 64)
     int nrows = 0, nblk = 0, nks = 0;
     long long total = 0;
-    int grid = 0, maxseg = 0, colmax_grid = 0;
+    int grid = 0, maxseg = 0, colmax_grid = 0;  // grid: work units (CTAs, or CTA pairs)
     size_t part_elems = 0;  // doubles
     size_t bdig_bytes = 0;  // panel digit planes
+    bool pair = false;      // w > 64: one pass by CTA pairs (a column group per CTA)
+    size_t bdig_stride = 0; // pair: bytes between the two groups' digit planes
 };
 bool k2i_supported(int wp);
 K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms);
 // pmax: colmax_grid * wp doubles; col_exp: nb ints (<= 128); bdig: bdig_bytes
-void launch_k2i(const CUtensorMap* tmap128, DType dt, const K2iPlan& p, int wp, const double* x,
-                size_t x_rows_pad, const int* row_exp, double* pmax, int* col_exp,
-                unsigned char* bdig, double* part, const double* row_mean, const double* scalars,
-                const double* colsums, double* y, size_t y_rows_pad, cudaStream_t st,
-                cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr, const int* skip = nullptr, int hamming_len = 0);
+// tmap64: 64-row boxes of the same D (the pair kernel's multicast halves)
+void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt, const K2iPlan& p,
+                int wp, const double* x, size_t x_rows_pad, const int* row_exp, double* pmax,
+                int* col_exp, unsigned char* bdig, double* part, const double* row_mean,
+                const double* scalars, const double* colsums, double* y, size_t y_rows_pad,
+                cudaStream_t st, cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr,
+                const int* skip = nullptr, int hamming_len = 0);
 
 // out[0] = sum of `count` doubles in a fixed order
 void launch_sum_fixed(const double* partial, size_t count, double* out, cudaStream_t st);

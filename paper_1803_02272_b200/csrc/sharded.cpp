@@ -304,8 +304,11 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
             if (!c.encode_tmap(&s.tmap128, s.buf->p, s.dt, std::max<size_t>(m, 1), s.cols, s.ld,
                                128) ||
                 !c.encode_tmap(&s.tmap256, s.buf->p, s.dt, std::max<size_t>(m, 1), s.cols, s.ld,
-                               256))
+                               256) ||
+                !c.encode_tmap(&s.tmap64, s.buf->p, s.dt, std::max<size_t>(m, 1), s.cols, s.ld,
+                               64))
                 throw Error(errc::internal, "cuTensorMapEncodeTiled failed");
+            s.tmap64_ok = true;
             s.tmap_ok = true;
         }
     });
@@ -373,7 +376,8 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         cudaEvent_t e0, e1;
         c.make_events(&e0, &e1);
         if (use_i8)
-            launch_k2i(s.tmap_for(128), s.dt, iplan, wp, x_full, n_pad, g.gram->row_exp->as<int>(),
+            launch_k2i(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x_full, n_pad,
+                       g.gram->row_exp->as<int>(),
                        pmax, col_exp, bdig, part, r_full + rb, scal, colsums, y_full + lo, m_pad,
                        c.stream, e0, e1, nullptr, hamming_i8);
         else if (m)

@@ -68,6 +68,11 @@ void ensure_tmap(Store& s) {
     if (!Ctx::get().encode_tmap(&s.tmap128, s.buf->p, s.dt, s.rows, s.cols, s.ld, 128) ||
         !Ctx::get().encode_tmap(&s.tmap256, s.buf->p, s.dt, s.rows, s.cols, s.ld, 256))
         throw Error(errc::internal, "cuTensorMapEncodeTiled failed");
+    if (!s.tmap64_ok) {  // K1's boxes, also the CTA-pair product's multicast halves
+        if (!Ctx::get().encode_tmap(&s.tmap64, s.buf->p, s.dt, s.rows, s.cols, s.ld, 64))
+            throw Error(errc::internal, "cuTensorMapEncodeTiled failed");
+        s.tmap64_ok = true;
+    }
     s.tmap_ok = true;
 }
 
@@ -296,7 +301,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         cudaEvent_t e0, e1;
         c.make_events(&e0, &e1);
         if (use_i8)
-            launch_k2i(s.tmap_for(128), s.dt, iplan, wp, x, n_pad, g.gram->row_exp->as<int>(), pmax,
+            launch_k2i(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x, n_pad,
+                       g.gram->row_exp->as<int>(), pmax,
                        col_exp, bdig, part, row_mean, scal_dev, colsums, y, n_pad, c.stream, e0,
                        e1, nullptr, hamming_i8);
         else
