@@ -30,7 +30,7 @@ __device__ __forceinline__ int pk(int a, int b, int w) {
 }
 
 // Rotation of pair (p, q) annihilating a_pq (Rutishauser's formulas, as the
-// oracle's Jacobi): returns c, s with J = [[c, s], [-s, c]] on (p, q).
+// oracle's Jacobi; jacobi_rot2 below): J = [[c, s], [-s, c]] on (p, q).
 // theta = (a_qq - a_pp) / (2 a_pq), t = sgn(theta) / (|theta| + sqrt(theta^2+1)),
 // c = 1 / sqrt(t^2 + 1), s = t c. The reciprocals / square roots use the
 // MUFU seeds plus Newton steps (a few ulps): any c, s with c^2 + s^2 = 1 to
@@ -47,22 +47,24 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
     double y = rsqrt(x);  // MUFU.RSQ64H + refinement in libdevice
     return y;
 }
-__device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, double& c,
-                                           double& s) {
+
+// Rotation from d = a_qq - a_pp and a_pq without forming theta:
+// t = 2 a_pq sgn(d) / (|d| + sqrt(d^2 + 4 a_pq^2)) (the same angle as
+// jacobi_rot: t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)) with theta =
+// d / (2 a_pq)), one reciprocal and two reciprocal square roots on the
+// dependent chain instead of two and two.
+__device__ __forceinline__ void jacobi_rot2(double app, double aqq, double apq, double& c,
+                                            double& s) {
     c = 1.0;
     s = 0.0;
     if (fabs(apq) >= 1e-300) {
-        const double theta = (aqq - app) * (0.5 * rcp_nr(apq));
-        const double th2 = theta * theta;
-        double t;
-        if (th2 < 1e300) {
-            const double hyp = (th2 + 1.0) * rsqrt_nr(th2 + 1.0);  // sqrt(theta^2 + 1)
-            t = rcp_nr(fabs(theta) + hyp);
-            if (theta < 0.0) t = -t;
-        } else {
-            t = 0.5 * rcp_nr(theta);
-        }
-        c = rsqrt_nr(t * t + 1.0);
+        const double d = aqq - app;
+        const double a2 = apq + apq;
+        const double h2 = fma(d, d, a2 * a2);
+        const double r = h2 * rsqrt_nr(h2);  // sqrt(d^2 + 4 a_pq^2)
+        double t = a2 * rcp_nr(fabs(d) + r);
+        if (d < 0.0) t = -t;
+        c = rsqrt_nr(fma(t, t, 1.0));
         s = t * c;
     }
 }
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
                 const int pq = sched[r * h + k];
                 const int p = pq >> 8, q = pq & 0xff;
                 double c = 1.0, s = 0.0;
-                if (q < w) jacobi_rot(A[pk(p, p, w)], A[pk(q, q, w)], A[pk(p, q, w)], c, s);
+                if (q < w) jacobi_rot2(A[pk(p, p, w)], A[pk(q, q, w)], A[pk(p, q, w)], c, s);
                 pp[k] = p;
                 qq[k] = q;
                 cs[k] = c;
@@ -444,6 +446,7 @@ __global__ void k_lift_scale(int n, const int* __restrict__ imeta,
          e += static_cast<size_t>(gridDim.x) * blockDim.x)
         coords[e] *= scale[e % r];
 }
+
 
 }  // namespace
 
