@@ -305,4 +305,23 @@ void ref_acceptance4_matrix(double* g_out, double* dense_out) {
     std::copy(dense.begin(), dense.end(), dense_out);
 }
 
+// The reference CLI's `mds` flow on a DVS file (tools/divscope_main.cpp:
+// 267-282): read_matrix, gram_from_distances, rank clamped to n, embed with
+// ids "0".."n-1", write_embedding_tsv + write_embedding_meta.
+int ref_mds_files(const char* dvs_path, std::size_t rank, std::size_t p, std::size_t q,
+                  std::uint64_t seed, unsigned threads, const char* tsv_path,
+                  const char* meta_path) {
+    return guarded([&] {
+        const DistanceMatrix d = read_matrix(dvs_path);
+        const GramMatrix g = gram_from_distances(d, threads);
+        const std::size_t n = g.n;
+        const std::size_t r = rank < n ? rank : n;
+        const Embedding e = embed(SymView{g.values.data(), n}, r, make_opts(r, p, q, seed), threads);
+        std::vector<std::string> ids(n);
+        for (std::size_t i = 0; i < n; ++i) ids[i] = std::to_string(i);
+        write_embedding_tsv(e, ids, tsv_path);
+        write_embedding_meta(e, meta_path);
+    });
+}
+
 }  // extern "C"

@@ -161,3 +161,17 @@ def test_product_fill_gaussian_bit_exact_vs_reference(ds):
     assert np.array_equal(ds.debug_fill_gaussian(7, 1001), z["gauss_7_1001"])
     assert np.array_equal(ds.debug_fill_gaussian(0, 4096), z["gauss_0_4096"])
     assert np.array_equal(ds.debug_fill_gaussian(42, 600), z["gauss_42_30x20"])
+
+
+def test_c_caller_builds_against_the_header():
+    # tools/divscope_mds.c: a plain C99 program compiled with -I include and
+    # linked against libdivscope_b200.so (make -C paper_1803_02272_b200/csrc
+    # caller); without a GPU it still runs its argument handling
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parent.parent / "tools" / "divscope_mds"
+    if not exe.exists():
+        subprocess.run(["make", "-C", str(exe.parent.parent / "paper_1803_02272_b200" / "csrc"),
+                        "caller"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 2 and "usage: divscope_mds mds" in r.stderr
