@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
                 int I, J;
                 pair_of(p, nbt, I, J);
                 unsigned char* st = sm + s * C::STAGE;
-                stage_ij[s] = make_int2(I, J);
+                if constexpr (sizeof(T) == 4) stage_ij[s] = make_int2(I, J);
                 mbar_arrive_expect_tx(&full[s], (I != J ? 2 : 1) * C::TILE);
                 for (int b = 0; b < C::NB; ++b)
                     tma_load_2d(st + b * (kT * 128), &tm, J * kT + b * C::BC, I * kT, &full[s]);
@@ -172,9 +172,17 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
     int s = 0;
     uint32_t ph = 0;
     for (long long p = blockIdx.x; p < npairs; p += gridDim.x) {
-        mbar_wait(&full[s], ph);
-        const int2 ij = stage_ij[s];
-        const int I = ij.x, J = ij.y;
+        int I, J;
+        if constexpr (sizeof(T) == 4) {
+            mbar_wait(&full[s], ph);
+            const int2 ij = stage_ij[s];
+            I = ij.x;
+            J = ij.y;
+        } else {
+            // f64 tiles: deriving (I, J) overlaps the wait (measured faster)
+            pair_of(p, nbt, I, J);
+            mbar_wait(&full[s], ph);
+        }
         const unsigned char* A = sm + s * C::STAGE;
         const unsigned char* B = (I != J) ? A + C::TILE : A;
         double a[C::EL];
@@ -182,14 +190,17 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
         for (int j = 0; j < C::EL; ++j) a[j] = static_cast<double>(*tile_at<T>(A, r, col0 + j));
         // four independent accumulation chains (a 16-long dependent DADD chain
         // per row segment left the FP64 latency exposed, worst with f32 tiles)
+        // f32 tiles: four independent accumulation chains (a 16-long dependent
+        // DADD chain left the FP64 latency exposed); f64 tiles: one (faster there)
+        constexpr int NCH = sizeof(T) == 4 ? 4 : 1;
         double rsp[4] = {0.0, 0.0, 0.0, 0.0}, s4p[4] = {0.0, 0.0, 0.0, 0.0};
         uint32_t rmx = 0u;
         float rmaxf = 0.0f;  // f32 tiles: max |d| of the row segment
 #pragma unroll
         for (int j = 0; j < C::EL; ++j) {
             const double sq = a[j] * a[j];
-            rsp[j & 3] += sq;
-            s4p[j & 3] += sq * sq;
+            rsp[j % NCH] += sq;
+            s4p[j % NCH] += sq * sq;
             const bool upper = I != J || col0 + j >= r;
             // (x > m ? x : m): NaN is never selected, as std::max(m, x) in the
             // reference's scans (mds.cpp:21-27, rsvd.cpp:50-54); cheaper than fmax
@@ -242,8 +253,8 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
                 const T bt = *tile_at<T>(B, r, col0 + j);
                 const double b = static_cast<double>(bt);
                 const double sq = b * b;
-                rbp[j & 3] += sq;
-                b4p[j & 3] += sq * sq;
+                rbp[j % NCH] += sq;
+                b4p[j % NCH] += sq * sq;
                 if constexpr (sizeof(T) == 4) {
                     const float bf = fabsf(bt);
                     bmaxf = bf > bmaxf ? bf : bmaxf;

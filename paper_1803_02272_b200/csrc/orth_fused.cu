@@ -105,6 +105,89 @@ __device__ bool cta_chol_inverse(double* __restrict__ A, double* __restrict__ E,
     return false;
 }
 
+// The same elimination by ONE warp, warp-synchronous (__syncwarp between
+// steps instead of a CTA barrier): the 32 x 32 (or 64 x 64) update of a step
+// is a few independent FMAs per lane, so the step is latency-bound and the
+// CTA-wide barrier was most of it. Same pivot decisions, same arithmetic per
+// entry (a_ij -= a_ki a_kj / d_k, e_ic -= (a_ki / d_k) e_kc), so the factor
+// is the same up to the order in which independent entries are written.
+// All threads of the CTA call it; warps other than 0 wait at the final
+// barrier. The shift request is broadcast through shared memory.
+template <int WP>
+__device__ bool warp_chol_inverse(double* __restrict__ A, double* __restrict__ E, int w,
+                                  const double* __restrict__ d0s, double maxdiag,
+                                  bool first_shifting, bool drop_mode, int* __restrict__ dropped_s,
+                                  double* __restrict__ dpiv, const unsigned short* __restrict__ tri,
+                                  const int* __restrict__ tri_off) {
+    __shared__ int shift_req;
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        const int lane = tid;
+        for (int e = lane; e < WP * WP; e += 32) E[e] = (e / WP == e % WP) ? 1.0 : 0.0;
+        if (lane == 0) shift_req = 0;
+        __syncwarp();
+        for (int k = 0; k < WP; ++k) {
+            const double p = A[k * WP + k];
+            const double d0k = d0s[k];
+            bool drop = (k >= w) || !(d0k > 0.0) || !(p > 0.0);
+            bool shift = false;
+            if (first_shifting) {
+                if (k < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift = true;
+                drop = drop && !(k < w && d0k > 0.0);
+            } else if (drop_mode && p <= kDropTolF * maxdiag) {
+                drop = true;
+            }
+            if (shift) {  // warp-uniform
+                if (lane == 0) shift_req = 1;
+                break;
+            }
+            if (lane == 0) {
+                dropped_s[k] = drop;
+                dpiv[k] = drop ? 0.0 : p;
+            }
+            double invp = 0.0;
+            if (!drop) {
+                double r;
+                asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+                r = fma(r, fma(-p, r, 1.0), r);
+                invp = fma(r, fma(-p, r, 1.0), r);
+            }
+            const double* rowk = A + k * WP;
+            const int t0 = tri_off[k + 1], t1 = tri_off[WP];
+            for (int t = t0 + lane; t < t1; t += 32) {
+                const int i = tri[t] >> 8, j = tri[t] & 0xff;
+                A[i * WP + j] -= rowk[i] * rowk[j] * invp;
+            }
+            // E rows i > k, columns c <= k (E[k][c] = 0 for c > k)
+            for (int i = k + 1 + lane; i < WP; i += 32) {
+                const double f = rowk[i] * invp;
+                for (int cc = 0; cc <= k; ++cc) E[i * WP + cc] -= f * E[k * WP + cc];
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    return shift_req != 0;
+}
+
+#ifndef DSB_ORTH_WARP_CHOL
+#define DSB_ORTH_WARP_CHOL 0
+#endif
+template <int WP>
+__device__ __forceinline__ bool chol_inverse(double* __restrict__ A, double* __restrict__ E, int w,
+                                             const double* __restrict__ d0s, double maxdiag,
+                                             bool first_shifting, bool drop_mode,
+                                             int* __restrict__ dropped_s, double* __restrict__ dpiv,
+                                             const unsigned short* __restrict__ tri,
+                                             const int* __restrict__ tri_off) {
+    if constexpr (DSB_ORTH_WARP_CHOL != 0)
+        return warp_chol_inverse<WP>(A, E, w, d0s, maxdiag, first_shifting, drop_mode, dropped_s,
+                                     dpiv, tri, tri_off);
+    else
+        return cta_chol_inverse<WP>(A, E, w, d0s, maxdiag, first_shifting, drop_mode, dropped_s,
+                                    dpiv, tri, tri_off);
+}
+
 template <int WP>
 __global__ void __launch_bounds__(256, 1)
     k_orth_fused(const double* __restrict__ y, double* __restrict__ out, size_t n_pad, int w,
@@ -144,10 +227,26 @@ __global__ void __launch_bounds__(256, 1)
     const size_t q0 = nq * c / P, q1 = nq * (c + 1) / P;
     const int nrow = static_cast<int>((q1 - q0) * 4);
     {
+        // the CTA's rows (contiguous in the interleaved panel) into shared
+        // memory, column-major: 8 independent loads in flight per thread
+        // (a load-store loop serialized on the global latency, ~5 us)
         const double* src = y + q0 * WP * 4;
-        for (int e = threadIdx.x; e < nrow * WP; e += blockDim.x) {
-            const int qb = e / (WP * 4), cc = (e / 4) % WP, rr = e & 3;
-            ps[cc * ldr + 4 * qb + rr] = src[e];
+        const int ne = nrow * WP, nt = blockDim.x;
+        for (int e0 = threadIdx.x; e0 < ne; e0 += 8 * nt) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * nt;
+                v[u] = e < ne ? __ldg(src + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * nt;
+                if (e < ne) {
+                    const int qb = e / (WP * 4), cc = (e / 4) % WP, rr = e & 3;
+                    ps[cc * ldr + 4 * qb + rr] = v[u];
+                }
+            }
         }
     }
     if (threadIdx.x == 0) skip_third = 0;
@@ -234,7 +333,7 @@ __global__ void __launch_bounds__(256, 1)
                 __syncthreads();
                 const bool first_shifting = pass == 0 && attempt == 0;
                 const bool drop_mode = pass != 0;
-                if (!cta_chol_inverse<WP>(R, E, w, d0s, tr_s[1], first_shifting, drop_mode,
+                if (!chol_inverse<WP>(R, E, w, d0s, tr_s[1], first_shifting, drop_mode,
                                           dropped_s, dpiv, tri, tri_off))
                     break;
                 sigma = 11.0 * (nrows * w + static_cast<double>(w) * (w + 1)) * 0x1.0p-53 * tr_s[0];
@@ -437,7 +536,7 @@ __global__ void __launch_bounds__(256) k_chol_inv_elim(const double* __restrict_
             R[e] = v;
         }
         __syncthreads();
-        if (!cta_chol_inverse<WP>(R, E, w, d0s, tr_s[1], pass == 0 && attempt == 0, pass != 0,
+        if (!chol_inverse<WP>(R, E, w, d0s, tr_s[1], pass == 0 && attempt == 0, pass != 0,
                                   dropped_s, dpiv, tri, tri_off))
             break;
         sigma = 11.0 * (nrows * w + static_cast<double>(w) * (w + 1)) * 0x1.0p-53 * tr_s[0];
