@@ -56,6 +56,7 @@ WORKLOADS = {
     "C5": (5, 50000, 30, 20, 2, 5, False),   # Hamming D of 50k reads (L=400, 50 ancestors)
 }
 FP64_FALLBACK_TFLOPS = 37.1  # DMMA microbenchmark on this pool (profiles/fp64_peak_r01.txt)
+INT8_PEAK_TOPS = 4533.5  # tcgen05 kind::i8, measured (profiles/r02_umma_seq.txt)
 
 
 def make_distance(ds, wl: str):
@@ -424,8 +425,24 @@ def b200_arm(args, wl):
         # per column group (w <= 64: one group), HBM-bound; `achieved` counts
         # the pass's algorithmic bytes (D once), `streamed_gbs` every read
         groups = max(int(st.last_product_groups), 1)
+        # the int8 tensor roof of the same pass: digit products x MMA columns
+        # (k2i_plan: WP <= 32 one 32-wide group, <= 64 one 64-wide, <= 96 a
+        # CTA pair of 48 + 48, else 64 + 64), at the measured kind::i8 peak
+        wpad = (w + 7) // 8 * 8
+        mma_cols = 32 if wpad <= 32 else 64 if wpad <= 64 else 96 if wpad <= 96 else 128
+        products = 18 if int(st.last_product_sdigits) == 3 else 28
+        i8_ops = 2.0 * m_rows * n * mma_cols * products
+        i8_ms = i8_ops / (INT8_PEAK_TOPS * 1e12) * 1e3
+        hbm_ms = bytes_per_launch / (hbm_peak * 1e9) * 1e3 * (groups if wpad > 96 else 1)
+        binding = "int8" if i8_ms > hbm_ms else "hbm"
         roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": gbs / hbm_peak, "traffic": traffic,
+                    "binding_roof": {"bound": binding, "roof_ms": max(i8_ms, hbm_ms),
+                                     "frac": max(i8_ms, hbm_ms) / k2_ms,
+                                     "hbm_ms": hbm_ms, "int8_ms": i8_ms,
+                                     "int8_ops_per_launch": i8_ops,
+                                     "int8_peak_tops": INT8_PEAK_TOPS,
+                                     "int8_peak_source": "profiles/r02_umma_seq.txt (7 x N=256 kind::i8 MMAs, A in TMEM)"},
                     "kernel": ("k2i_product (3x7-digit int8 slice product of the exact Hamming "
                                "h^2, tcgen05 kind::i8)" if int(st.last_product_sdigits) == 3 else
                                "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)"),
