@@ -186,10 +186,22 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
         const unsigned char* A = sm + s * C::STAGE;
         const unsigned char* B = (I != J) ? A + C::TILE : A;
         double a[C::EL];
+        T av[C::EL];  // the raw row segment (f32: two 16-byte loads per 8 values)
+        if constexpr (sizeof(T) == 4) {
 #pragma unroll
-        for (int j = 0; j < C::EL; ++j) a[j] = static_cast<double>(*tile_at<T>(A, r, col0 + j));
-        // four independent accumulation chains (a 16-long dependent DADD chain
-        // per row segment left the FP64 latency exposed, worst with f32 tiles)
+            for (int j = 0; j < C::EL; j += 4) {
+                const float4 v = *reinterpret_cast<const float4*>(tile_at<T>(A, r, col0 + j));
+                av[j] = v.x;
+                av[j + 1] = v.y;
+                av[j + 2] = v.z;
+                av[j + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < C::EL; ++j) av[j] = *tile_at<T>(A, r, col0 + j);
+        }
+#pragma unroll
+        for (int j = 0; j < C::EL; ++j) a[j] = static_cast<double>(av[j]);
         // f32 tiles: four independent accumulation chains (a 16-long dependent
         // DADD chain left the FP64 latency exposed); f64 tiles: one (faster there)
         constexpr int NCH = sizeof(T) == 4 ? 4 : 1;
@@ -208,7 +220,7 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
                 // max |d| in the float domain (widening is monotonic, so the
                 // widened max is the max of the widened values); the row
                 // exponent follows from the row max: max d^2 = (max |d|)^2
-                const float af = fabsf(*tile_at<T>(A, r, col0 + j));
+                const float af = fabsf(av[j]);
                 rmaxf = af > rmaxf ? af : rmaxf;
                 if (upper) maxup_f = af > maxup_f ? af : maxup_f;
             } else {
@@ -220,7 +232,7 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
             if constexpr (sizeof(T) == 4) {
                 // identical bits (the symmetric case) give 0; only differing
                 // entries pay for the f64 difference the reference takes
-                if (__float_as_uint(mt) != __float_as_uint(*tile_at<T>(A, r, col0 + j)))
+                if (__float_as_uint(mt) != __float_as_uint(av[j]))
                     maxasym = max_keep(maxasym, fabs(a[j] - static_cast<double>(mt)));
             } else {
                 maxasym = max_keep(maxasym, fabs(a[j] - mt));
@@ -248,9 +260,23 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
             double rbp[4] = {0.0, 0.0, 0.0, 0.0}, b4p[4] = {0.0, 0.0, 0.0, 0.0};
             uint32_t bmx = 0u;
             float bmaxf = 0.0f;
+            T bv[C::EL];
+            if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                for (int j = 0; j < C::EL; j += 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(tile_at<T>(B, r, col0 + j));
+                    bv[j] = v.x;
+                    bv[j + 1] = v.y;
+                    bv[j + 2] = v.z;
+                    bv[j + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < C::EL; ++j) bv[j] = *tile_at<T>(B, r, col0 + j);
+            }
 #pragma unroll
             for (int j = 0; j < C::EL; ++j) {
-                const T bt = *tile_at<T>(B, r, col0 + j);
+                const T bt = bv[j];
                 const double b = static_cast<double>(bt);
                 const double sq = b * b;
                 rbp[j % NCH] += sq;
