@@ -105,73 +105,95 @@ __device__ bool cta_chol_inverse(double* __restrict__ A, double* __restrict__ E,
     return false;
 }
 
-// The same elimination by ONE warp, warp-synchronous (__syncwarp between
-// steps instead of a CTA barrier): the 32 x 32 (or 64 x 64) update of a step
-// is a few independent FMAs per lane, so the step is latency-bound and the
-// CTA-wide barrier was most of it. Same pivot decisions, same arithmetic per
-// entry (a_ij -= a_ki a_kj / d_k, e_ic -= (a_ki / d_k) e_kc), so the factor
-// is the same up to the order in which independent entries are written.
-// All threads of the CTA call it; warps other than 0 wait at the final
-// barrier. The shift request is broadcast through shared memory.
+// The same elimination blocked by 4 pivots (right-looking LDL^T): warp 0
+// factors the block's 4 pivot rows in order (the per-pivot shift / drop
+// decisions and updates of k_chol_inv, restricted to the block's rows and
+// their E rows, with __syncwarp between pivots), then the whole CTA applies
+// the 4 pivots to the trailing rows of A and E as one rank-4 update (one
+// barrier) — 8 CTA barriers instead of 32 per 32 x 32 factor. Every entry
+// receives the same updates with the same pivot-row values as in the
+// one-pivot-at-a-time order (the panel rows are final before the trailing
+// update reads them); only the order of independent writes changes.
 template <int WP>
-__device__ bool warp_chol_inverse(double* __restrict__ A, double* __restrict__ E, int w,
-                                  const double* __restrict__ d0s, double maxdiag,
-                                  bool first_shifting, bool drop_mode, int* __restrict__ dropped_s,
-                                  double* __restrict__ dpiv, const unsigned short* __restrict__ tri,
-                                  const int* __restrict__ tri_off) {
+__device__ bool cta_chol_inverse_b4(double* __restrict__ A, double* __restrict__ E, int w,
+                                    const double* __restrict__ d0s, double maxdiag,
+                                    bool first_shifting, bool drop_mode, int* __restrict__ dropped_s,
+                                    double* __restrict__ dpiv, const unsigned short* __restrict__ tri,
+                                    const int* __restrict__ tri_off) {
+    __shared__ double invs[4];
     __shared__ int shift_req;
-    const int tid = threadIdx.x;
-    if (tid < 32) {
-        const int lane = tid;
-        for (int e = lane; e < WP * WP; e += 32) E[e] = (e / WP == e % WP) ? 1.0 : 0.0;
-        if (lane == 0) shift_req = 0;
-        __syncwarp();
-        for (int k = 0; k < WP; ++k) {
-            const double p = A[k * WP + k];
-            const double d0k = d0s[k];
-            bool drop = (k >= w) || !(d0k > 0.0) || !(p > 0.0);
-            bool shift = false;
-            if (first_shifting) {
-                if (k < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift = true;
-                drop = drop && !(k < w && d0k > 0.0);
-            } else if (drop_mode && p <= kDropTolF * maxdiag) {
-                drop = true;
-            }
-            if (shift) {  // warp-uniform
-                if (lane == 0) shift_req = 1;
-                break;
-            }
-            if (lane == 0) {
-                dropped_s[k] = drop;
-                dpiv[k] = drop ? 0.0 : p;
-            }
-            double invp = 0.0;
-            if (!drop) {
-                double r;
-                asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
-                r = fma(r, fma(-p, r, 1.0), r);
-                invp = fma(r, fma(-p, r, 1.0), r);
-            }
-            const double* rowk = A + k * WP;
-            const int t0 = tri_off[k + 1], t1 = tri_off[WP];
-            for (int t = t0 + lane; t < t1; t += 32) {
-                const int i = tri[t] >> 8, j = tri[t] & 0xff;
-                A[i * WP + j] -= rowk[i] * rowk[j] * invp;
-            }
-            // E rows i > k, columns c <= k (E[k][c] = 0 for c > k)
-            for (int i = k + 1 + lane; i < WP; i += 32) {
-                const double f = rowk[i] * invp;
-                for (int cc = 0; cc <= k; ++cc) E[i * WP + cc] -= f * E[k * WP + cc];
-            }
-            __syncwarp();
-        }
-    }
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < WP * WP; e += nt) E[e] = (e / WP == e % WP) ? 1.0 : 0.0;
+    if (tid == 0) shift_req = 0;
     __syncthreads();
-    return shift_req != 0;
+    for (int k0 = 0; k0 < WP; k0 += 4) {
+        if (tid < 32) {
+            const int lane = tid;
+            for (int kk = k0; kk < k0 + 4; ++kk) {
+                const double p = A[kk * WP + kk];
+                const double d0k = d0s[kk];
+                bool drop = (kk >= w) || !(d0k > 0.0) || !(p > 0.0);
+                bool shift = false;
+                if (first_shifting) {
+                    if (kk < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift = true;
+                    drop = drop && !(kk < w && d0k > 0.0);
+                } else if (drop_mode && p <= kDropTolF * maxdiag) {
+                    drop = true;
+                }
+                if (shift) {  // warp-uniform
+                    if (lane == 0) shift_req = 1;
+                    break;
+                }
+                double invp = 0.0;
+                if (!drop) {
+                    double r;
+                    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+                    r = fma(r, fma(-p, r, 1.0), r);
+                    invp = fma(r, fma(-p, r, 1.0), r);
+                }
+                if (lane == 0) {
+                    dropped_s[kk] = drop;
+                    dpiv[kk] = drop ? 0.0 : p;
+                    invs[kk - k0] = invp;
+                }
+                const double* rowk = A + kk * WP;
+                // the block's later pivot rows, every column j >= i
+                for (int i = kk + 1; i < k0 + 4; ++i) {
+                    const double f = rowk[i] * invp;
+                    for (int jj = i + lane; jj < WP; jj += 32) A[i * WP + jj] -= f * rowk[jj];
+                    for (int c = lane; c <= kk; c += 32) E[i * WP + c] -= f * E[kk * WP + c];
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        if (shift_req) return true;  // uniform: the caller rewrites A next
+        // trailing rows i >= k0 + 4 of A (upper part) and of E: rank-4 update
+        const double i0 = invs[0], i1 = invs[1], i2 = invs[2], i3 = invs[3];
+        const double* r0 = A + k0 * WP;
+        const double* r1 = r0 + WP;
+        const double* r2 = r1 + WP;
+        const double* r3 = r2 + WP;
+        const int t0 = tri_off[k0 + 4], t1 = tri_off[WP];
+        for (int t = t0 + tid; t < t1; t += nt) {
+            const int i = tri[t] >> 8, j = tri[t] & 0xff;
+            A[i * WP + j] -= ((r0[i] * i0) * r0[j] + (r1[i] * i1) * r1[j]) +
+                             ((r2[i] * i2) * r2[j] + (r3[i] * i3) * r3[j]);
+        }
+        const int ncol = k0 + 4, nrow = WP - k0 - 4;
+        for (int e = tid; e < nrow * ncol; e += nt) {
+            const int i = k0 + 4 + e / ncol, cc = e % ncol;
+            E[i * WP + cc] -= ((r0[i] * i0) * E[k0 * WP + cc] + (r1[i] * i1) * E[(k0 + 1) * WP + cc]) +
+                              ((r2[i] * i2) * E[(k0 + 2) * WP + cc] +
+                               (r3[i] * i3) * E[(k0 + 3) * WP + cc]);
+        }
+        __syncthreads();
+    }
+    return false;
 }
 
-#ifndef DSB_ORTH_WARP_CHOL
-#define DSB_ORTH_WARP_CHOL 0
+#ifndef DSB_ORTH_BLOCKED
+#define DSB_ORTH_BLOCKED 1
 #endif
 template <int WP>
 __device__ __forceinline__ bool chol_inverse(double* __restrict__ A, double* __restrict__ E, int w,
@@ -180,9 +202,9 @@ __device__ __forceinline__ bool chol_inverse(double* __restrict__ A, double* __r
                                              int* __restrict__ dropped_s, double* __restrict__ dpiv,
                                              const unsigned short* __restrict__ tri,
                                              const int* __restrict__ tri_off) {
-    if constexpr (DSB_ORTH_WARP_CHOL != 0)
-        return warp_chol_inverse<WP>(A, E, w, d0s, maxdiag, first_shifting, drop_mode, dropped_s,
-                                     dpiv, tri, tri_off);
+    if constexpr (DSB_ORTH_BLOCKED != 0)
+        return cta_chol_inverse_b4<WP>(A, E, w, d0s, maxdiag, first_shifting, drop_mode,
+                                       dropped_s, dpiv, tri, tri_off);
     else
         return cta_chol_inverse<WP>(A, E, w, d0s, maxdiag, first_shifting, drop_mode, dropped_s,
                                     dpiv, tri, tri_off);
