@@ -268,9 +268,10 @@ def reference_arm(args, wl):
         # not fit next to D): each step is the reference product pass over a
         # block of rows, timed as entries/s per pass
         base, _ = cpu_sample(d, wl, budget_s=5.0)
-        kind, steps, t = base["kind"], 1, 0.0
+        kind, steps = base["kind"], 1
         value = base["value"]
-        sample = base["sample"]
+        t = passes * n * n / value  # a full step at the sampled rate (extrapolated)
+        sample = base["sample"] + f"; ms_per_step extrapolated to {passes} full passes"
     line = {
         "impl": "reference", "metric": "MDS distance entries/s per streaming pass",
         "value": value, "unit": "entries/s", "n_gpus": args.gpus, "steps": steps,
@@ -448,6 +449,8 @@ def b200_arm(args, wl):
                                "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)"),
                     "peak_source": hbm["peak_source"],
                     "column_groups": groups,
+                    "reads_of_D_per_pass": 1 if int(st.last_product_pair) else groups,
+                    "cta_pair": bool(int(st.last_product_pair)),
                     "s_slices": int(st.last_product_sdigits),
                     "streamed_gbs": gbs * groups if groups > 1 else gbs,
                     "fp64_equiv": {"achieved": tflops, "unit": "TFLOP/s",

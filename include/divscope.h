@@ -338,6 +338,8 @@ typedef struct divscope_stats {
     int32_t last_product_kernel; /* 0 fp64 DMMA (k2_product), 1 int8 slice product */
     int32_t last_product_groups; /* int8 path: column groups = reads of D per product pass */
     int32_t last_product_sdigits; /* int8 path: bytes per S element (7; 3 for Hamming D) */
+    int32_t last_product_pair;    /* int8 path: 1 when a CTA pair shared each D tile (64 < WP <= 96:
+                                     both column groups in ONE read of D) */
 } divscope_stats;
 
 /* timing on => CUDA events are recorded around K1/K2 on the library stream */

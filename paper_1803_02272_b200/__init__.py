@@ -81,7 +81,8 @@ class Stats(C.Structure):
                 ("stats_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("last_evd_sweeps", C.c_int32), ("last_orth_shifted", C.c_int32),
                 ("last_power_iters", C.c_int32), ("last_product_kernel", C.c_int32),
-                ("last_product_groups", C.c_int32), ("last_product_sdigits", C.c_int32)]
+                ("last_product_groups", C.c_int32), ("last_product_sdigits", C.c_int32),
+                ("last_product_pair", C.c_int32)]
 
 
 _dp = C.POINTER(C.c_double)

@@ -761,6 +761,7 @@ void divscope_stats_get(divscope_stats* out) {
         out->last_product_kernel = c.last_product_kernel;
         out->last_product_groups = c.last_product_groups;
         out->last_product_sdigits = c.last_product_sdigits;
+        out->last_product_pair = c.last_product_pair;
     } catch (...) {
     }
 }

@@ -133,6 +133,7 @@ void Ctx::set_device(int dev) {
     if (inited_) {
         DSB_CUDA(cudaStreamSynchronize(stream));
         arena_.clear();
+        omega_key = OmegaKey{};  // its panel lived in the arena
         if (g_live_bufs.load() != 0)
             throw Error(errc::invalid_argument,
                         "cannot change device while handles hold memory on device " +
@@ -144,7 +145,6 @@ void Ctx::set_device(int dev) {
             cudaEventDestroy(t.b);
         }
         pending.clear();
-        omega_key = OmegaKey{};
         cudaStreamDestroy(stream);
         stream = nullptr;
         inited_ = false;

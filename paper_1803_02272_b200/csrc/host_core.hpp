@@ -129,6 +129,7 @@ public:
     int last_product_kernel = 0;  // 0 fp64 DMMA, 1 int8 slice product
     int last_product_groups = 1;  // int8 column groups (reads of D per pass)
     int last_product_sdigits = 0;  // int8 S slices per element (7, or 3 for Hamming D)
+    int last_product_pair = 0;     // int8: the CTA-pair kernel (one read of D for two groups)
     std::vector<TimedPair> pending;
     std::vector<cudaEvent_t> event_pool;
     void begin_timed(int kind, cudaEvent_t* a);

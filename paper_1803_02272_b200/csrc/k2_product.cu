@@ -247,19 +247,23 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     const double g = mode ? scalars[S_GRAND] : 0.0;
-#pragma unroll 4
     for (int e = threadIdx.x; e < kRows * WP; e += blockDim.x) {
         const int r = r0 + e / WP, col = e % WP;
         const int eo = r * WP + col;
-        // the first slots' loads are issued together, then summed in CTA order
-        double p4[4];
-#pragma unroll
-        for (int sl = 0; sl < 4; ++sl) p4[sl] = sl < nslot ? part[slot_base[sl] + eo] : 0.0;
+        // the slots' loads are issued together (up to 16 in flight: small n
+        // splits a row block over ~20 CTAs, one L2 round trip each if
+        // serialized), then summed in CTA order
+        constexpr int kBatch = 16;
         double v = 0.0;
+        for (int s0 = 0; s0 < nslot; s0 += kBatch) {
+            double pb[kBatch];
 #pragma unroll
-        for (int sl = 0; sl < 4; ++sl)
-            if (sl < nslot) v += p4[sl];
-        for (int sl = 4; sl < nslot; ++sl) v += part[slot_base[sl] + eo];
+            for (int sl = 0; sl < kBatch; ++sl)
+                pb[sl] = s0 + sl < nslot ? part[slot_base[s0 + sl] + eo] : 0.0;
+#pragma unroll
+            for (int sl = 0; sl < kBatch; ++sl)
+                if (s0 + sl < nslot) v += pb[sl];
+        }
         const size_t i = static_cast<size_t>(b) * BM + r;
         if (i >= static_cast<size_t>(n)) {
             v = 0.0;

@@ -230,6 +230,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
             ? s.hamming_len
             : 0;
     c.last_product_sdigits = use_i8 ? (hamming_i8 ? 3 : 7) : 0;
+    c.last_product_pair = use_i8 && iplan.pair ? 1 : 0;
     const size_t pbytes = n_pad * wp * sizeof(double);
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
     double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));

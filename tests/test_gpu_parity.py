@@ -520,7 +520,8 @@ def test_int8_product_admission_and_f32(ds, oracle, product_path):
 
 @pytest.mark.parametrize("rank,over", [(60, 10), (100, 20), (100, 28)])
 def test_int8_column_groups_match_fp64(ds, oracle, rank, over):
-    # w = 70 -> groups of 64 + 32 columns (wp 72); w = 120, 128 -> 64 + 64
+    # w = 70 (wp 72): the CTA pair, 48 + 48 columns in ONE read of D;
+    # w = 120, 128: two 64-column group passes
     n = 900
     d = oracle.euclidean_matrix(ds.synth_points(3, n, 7))
     g = ds.gram(ds.matrix_from_host(d))
@@ -529,6 +530,7 @@ def test_int8_column_groups_match_fp64(ds, oracle, rank, over):
         e8 = ds.embed(g, rank=rank, oversampling=over, power_iters=2, seed=4)
         st = ds.stats_get()
         assert (st.last_product_kernel, st.last_product_groups) == (1, 2)
+        assert st.last_product_pair == (1 if rank + over <= 96 else 0)
         ds.set_product_path(1)
         e64 = ds.embed(g, rank=rank, oversampling=over, power_iters=2, seed=4)
         assert ds.stats_get().last_product_kernel == 0
@@ -658,3 +660,19 @@ def test_hamming_builder_row_bands_and_errors(ds, oracle):
         ds.matrix_hamming([bytes(r) for r in bad])
     assert ei.value.status == ds.Status.ERR_INVALID_CHARACTER
     assert "read 200" in ei.value.message and "base 18" in ei.value.message
+
+
+def test_device_switch_refused_while_handles_live(ds, oracle, product_path):
+    # one device per process: with handles holding device memory
+    # a switch is refused, and the context keeps working on its device
+    # (including the resident Omega panel, dropped with the workspace)
+    d = oracle.euclidean_matrix(ds.synth_points(1, 300, 2))
+    g = ds.gram(ds.matrix_from_host(d))
+    a = ds.embed(g, rank=5, oversampling=5, power_iters=1, seed=3)
+    with pytest.raises(ds.DivscopeError) as ei:
+        ds.set_device(1)
+    assert ei.value.status == ds.Status.ERR_INVALID_ARGUMENT
+    ds.set_device(0)  # same device: a no-op
+    b = ds.embed(g, rank=5, oversampling=5, power_iters=1, seed=3)
+    assert np.array_equal(a.eigenvalues, b.eigenvalues)
+    assert np.array_equal(a.coords, b.coords)
