@@ -275,6 +275,9 @@ void launch_hamming(const uint32_t* lo, const uint32_t* hi, size_t count, int wo
                                                          static_cast<int>(nrows));
         }
     };
+    // D on the int8 tensor cores (hamming_tc.cu) unless disabled or the row
+    // band is not 128-aligned
+    if (d && launch_hamming_tc(lo, hi, count, words, length, d, ld, st, row0, nrows)) d = nullptr;
     if (d) {
         if (sym) go(d, ld, std::true_type{});
         else go(d, ld, std::false_type{});

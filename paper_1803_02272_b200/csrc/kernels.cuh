@@ -251,6 +251,12 @@ void launch_hamming(const uint32_t* lo, const uint32_t* hi, size_t count, int wo
                     double* d, size_t ld, uint32_t* counts, cudaStream_t st, size_t row0 = 0,
                     size_t nrows = static_cast<size_t>(-1));
 
+// K7 on the int8 tensor cores (D only): false when not applicable (disabled
+// by DSB_HAMMING_TC=0, or row0 not a multiple of 128), nothing launched
+bool launch_hamming_tc(const uint32_t* lo, const uint32_t* hi, size_t count, int words, int length,
+                       double* d, size_t ld, cudaStream_t st, size_t row0, size_t nrows);
+bool hamming_tc_enabled();
+
 // ---- misc ------------------------------------------------------------------
 // Opt a kernel into the full shared-memory carve-out once (dynamic limit =
 // 227 KB minus its static shared memory), so static + dynamic may exceed the

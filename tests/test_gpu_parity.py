@@ -68,6 +68,32 @@ def test_hamming_edge_cases(ds, oracle):
     assert err(ds, ds.hamming_counts, [b"ACGN"]) == ds.Status.ERR_INVALID_CHARACTER
 
 
+@pytest.mark.parametrize("count,length", [(1, 1), (3, 5), (127, 10), (128, 11), (129, 33),
+                                          (300, 400), (1000, 150), (257, 1000), (140, 4095)])
+def test_hamming_tensor_core_builder_bit_exact(ds, count, length):
+    # K7's D on the int8 tensor cores (hamming_tc.cu: +-1 encoding, one GEMM,
+    # h = (3 L - acc) / 4) against plain character comparison, the POPC
+    # counts kernel, and 128-aligned row bands (tensor cores) next to
+    # unaligned ones (POPC kernel)
+    rng = np.random.default_rng(count * 7919 + length)
+    arr = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, (count, length))]
+    if count > 2:
+        arr[1] = arr[0]  # an identical pair
+        arr[2, : length // 2] = arr[0, : length // 2]
+    reads = [r.tobytes() for r in arr]
+    h = (arr[:, None, :] != arr[None, :, :]).sum(-1) if count * count * length < 2e8 else None
+    d = ds.matrix_hamming(reads).to_numpy()
+    counts = ds.hamming_counts(reads)
+    if h is not None:
+        assert np.array_equal(counts, h)
+    assert np.array_equal(d, counts.astype(np.float64) / length)
+    for r0, r1 in [(128, count), (0, min(count, 200)), (5, min(count, 140))]:
+        if r0 >= r1:
+            continue
+        band = ds.matrix_hamming_rows(reads, r0, r1).to_numpy()
+        assert np.array_equal(band, d[r0:r1])
+
+
 # ---------------------------------------------------------------- gram
 
 def test_gram_two_point_exact(ds):
