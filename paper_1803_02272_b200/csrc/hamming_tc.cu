@@ -16,14 +16,12 @@
 // Kernel: persistent, one CTA per SM over 128 x 128 output tiles (upper tiles
 // I <= J of the full matrix in 32 x 32-tile super-tiles, or every tile of a
 // 128-aligned row band). Warp 0 streams the A / B k-step tiles through a
-// 4-stage mbarrier ring of 4 k-steps each (evict_last: E stays in L2); warp 1 issues per k-step
-// the tile's M = N = 128, K = 32 MMA and, off the diagonal, the mirror tile's
-// (operands swapped), into one of two pairs of 128-column TMEM accumulators;
-// warps 4..11 turn the other pair into D and store it row-major straight from
-// 16 x 256b TMEM fragments (16-byte evict-first stores, whole sectors). The D
-// stream (8 n^2 bytes) bounds the kernel; the doubled MMA work (the mirror is
-// recomputed rather than transposed through shared memory) is spare tensor
-// time.
+// 3-stage mbarrier ring of 4 k-steps each (evict_last: E stays in L2); warp 1
+// issues one M = N = 128, K = 32 MMA per k-step into one of four 128-column
+// TMEM accumulators; warps 4..11 turn finished accumulators into D, stage
+// each 32 x 32 chunk in shared memory as rows of the tile and, off the
+// diagonal, transposed as rows of the mirror tile, and store both with TMA
+// tensor stores. The D stream (8 n^2 bytes) bounds the kernel.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -42,13 +40,14 @@ namespace {
 
 constexpr int kTT = 128;      // output tile edge (M = N)
 constexpr int kTK = 32;       // K bytes per MMA
-constexpr int kKPer = 4;                        // k-steps per ring stage
-constexpr int kTStages = 4;
-constexpr int kStageOps = 2 * kKPer * 4096;     // A | B, 32 KB
-constexpr int kEpiWarps = 8;  // warps 4..11
+constexpr int kKPer = 4;                     // k-steps per ring stage
+constexpr int kTStages = 3;
+constexpr int kStageOps = 2 * kKPer * 4096;  // A | B, 32 KB
+constexpr int kAccBufs = 4;                  // 4 x 128 TMEM columns
+constexpr int kEpiWarps = 8;                 // warps 4..11
 constexpr int kTThreads = 128 + 32 * kEpiWarps;
-constexpr int kWarpStage = 16 * 64 * 8;              // per epilogue warp: 4 boxes of 16 x 16 doubles
-constexpr int kStageBytes = kEpiWarps * kWarpStage;  // 64 KB
+constexpr int kWarpStage = 2 * 2 * 32 * 16 * 8;      // per epilogue warp: main + mirror, 2 boxes each
+constexpr int kStageBytes = kEpiWarps * kWarpStage;  // 128 KB
 constexpr int kTileBytes = kTT * kTK;  // 4 KB operand tile
 
 // E tiles from the bit planes (k_pack_reads): thread per (row, k-step, 4-byte
@@ -128,27 +127,11 @@ __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// tcgen05.ld 16x256b.x8: lanes [taddr.lane, + 16), 64 columns; lane l gets
-// v[4 n + {0, 1}] = (row l / 4, columns 8 n + 2 (l % 4) + {0, 1}) and
-// v[4 n + {2, 3}] = (row l / 4 + 8, the same columns)
-__device__ __forceinline__ void tmem_ld_16x256b_x8(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
-        "%28, %29, %30, %31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-}
-
 // Persistent: one CTA per SM walks tiles t = blockIdx.x, += gridDim.x. Warp 0
 // streams operand k-steps through the ring across tile boundaries, warp 1
-// alternates two TMEM accumulators (acc_full / acc_empty), so the MMAs of tile
-// t + 1 run while warps 4..11 convert and store tile t — the store stream,
-// which bounds the kernel, never waits for operands.
+// rotates four TMEM accumulators (acc_full / acc_empty), so the MMAs of later
+// tiles run while warps 4..11 convert and store earlier ones — the store
+// stream, which bounds the kernel, never waits for operands.
 template <bool SYM, bool FASTDIV>
 __global__ void __launch_bounds__(kTThreads, 1)
     k_hamming_tc(const __grid_constant__ CUtensorMap dmap, const int8_t* __restrict__ enc,
@@ -157,28 +140,26 @@ __global__ void __launch_bounds__(kTThreads, 1)
                  size_t ld, int row0, int nrows) {
     extern __shared__ __align__(1024) unsigned char smh[];
     unsigned char* sm = smh + ((1024u - (smem_u32(smh) & 1023u)) & 1023u);
-    unsigned char* ring = sm;                                                     // [stages][A | B]
-    // staged D blocks: per epilogue warp, 4 boxes of 16 rows x 16 columns in
-    // the TMA's 128-byte-swizzled layout
-    unsigned char* stage = ring + kTStages * kStageOps;
+    unsigned char* ring = sm;                            // [stages][A kKPer x 4 KB | B ...]
+    unsigned char* stage = ring + kTStages * kStageOps;  // [warp][2 x 8 KB] staged D boxes
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + kStageBytes);
     uint64_t* empty = full + kTStages;
-    uint64_t* acc_full = empty + kTStages;  // [2]
-    uint64_t* acc_empty = acc_full + 2;     // [2]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* acc_full = empty + kTStages;     // [kAccBufs]
+    uint64_t* acc_empty = acc_full + kAccBufs;  // [kAccBufs]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + kAccBufs);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kAccBufs; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], kEpiWarps);
         }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tslot, 4 * kTT);
+    if (warp == 1) tmem_alloc(tslot, kAccBufs * kTT);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -217,26 +198,19 @@ __global__ void __launch_bounds__(kTThreads, 1)
         int u = 0;  // tiles issued
         const uint32_t idesc = umma_idesc_i8(kTT, true, true);  // s8 x s8 -> s32
         for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++u) {
-            const int b = u & 1;
-            if (u >= 2) mbar_wait(&acc_empty[b], ((u >> 1) - 1) & 1);
+            const int b = u % kAccBufs;
+            if (u >= kAccBufs) mbar_wait(&acc_empty[b], ((u / kAccBufs) - 1) & 1);
             tc_fence_after();
-            const int I = order[t].x, J = order[t].y;
-            const bool mirror = SYM && I != J;
-            const uint32_t acc = tmem + static_cast<uint32_t>(b * 2 * kTT);
+            const uint32_t acc = tmem + static_cast<uint32_t>(b * kTT);
             for (int ks = 0; ks < nks; ks += kKPer) {
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
                 const uint32_t base = smem_u32(ring + s * kStageOps);
                 const int cnt = min(kKPer, nks - ks);
-                for (int kk = 0; kk < cnt; ++kk) {
-                    const uint64_t da = umma_desc_k_interleave(base + kk * kTileBytes);
-                    const uint64_t db = umma_desc_k_interleave(base + (kKPer + kk) * kTileBytes);
-                    const int accum = (ks + kk) > 0 ? 1 : 0;
-                    umma_i8_w(acc, da, db, idesc, accum);
-                    // the mirror tile (J, I) as its own product: its rows are
-                    // then stored row-major like the tile's (tensor time is spare)
-                    if (mirror) umma_i8_w(acc + kTT, db, da, idesc, accum);
-                }
+                for (int kk = 0; kk < cnt; ++kk)
+                    umma_i8_w(acc, umma_desc_k_interleave(base + kk * kTileBytes),
+                              umma_desc_k_interleave(base + (kKPer + kk) * kTileBytes), idesc,
+                              (ks + kk) > 0 ? 1 : 0);
                 umma_commit_w(&empty[s]);
                 if (++s == kTStages) {
                     s = 0;
@@ -247,18 +221,19 @@ __global__ void __launch_bounds__(kTThreads, 1)
         }
     } else if (warp >= 4) {
         // epilogue: warp ew = warp - 4 owns TMEM lanes 32 (warp & 3) .. + 31
-        // and columns [64 (ew >> 2), + 64) of each accumulator, read as
-        // 16 x 256b fragments (lane l: rows l / 4 and l / 4 + 8, columns
-        // 2 (l % 4) + {0, 1} of every 8-column chunk). Each warp stages its
-        // 16 x 64 block as 4 boxes of 16 x 16 doubles in the 128-byte swizzled
-        // layout (conflict-free 16-byte writes) and one lane hands them to
-        // the TMA (tensor stores, evict-first; edge tiles clipped by the
-        // tensor map), off the load/store pipe — no barriers between warps.
-        // With an odd leading dimension (no tensor map) 16-byte pieces are
-        // stored from registers instead.
+        // (tile rows) and columns [64 (ew >> 2), + 64), read 32 columns at a
+        // time (lane = row, 32 consecutive columns). Each 32 x 32 chunk is
+        // staged twice in the TMA's 128-byte-swizzled box layout (boxes of 32
+        // rows x 16 columns): as rows of the tile (16-byte writes) and, off
+        // the diagonal, transposed as rows of the mirror tile (J, I) (8-byte
+        // writes, a warp covering one 256-byte mirror row) — both
+        // conflict-free — and one lane hands the boxes to the TMA (tensor
+        // stores, evict-first, edge tiles clipped by the tensor map). The
+        // mirror costs shared-memory bandwidth once, not a second product.
+        // With an odd leading dimension (no tensor map) 8-byte stores go
+        // straight from registers instead.
         const int ew = warp - 4, q = warp & 3, cw = (ew >> 2) * 64;
-        const int tr = lane >> 2, tcol = 2 * (lane & 3);
-        unsigned char* wst = stage + ew * kWarpStage;
+        unsigned char* wst = stage + ew * kWarpStage;  // [main 8 KB | mirror 8 KB]
         const int l3 = 3 * length;
         const double L = static_cast<double>(length), rinv = 1.0 / L;
         const bool vec = (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
@@ -269,8 +244,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
         // from the reciprocal and one remainder step, bit-identical to it;
         // the factor 4 is folded into the constants (exact power-of-2 scaling)
         const double L4 = 4.0 * L, rinv4 = 0.25 * rinv;
-        auto conv = [&](uint32_t acc) -> double {
-            const int x = l3 - static_cast<int>(acc);  // 0 <= x = 4 h <= 4 L
+        auto conv = [&](int32_t acc) -> double {
+            const int x = l3 - acc;  // 0 <= x = 4 h <= 4 L
             const double xd = __hiloint2double(0x43300000, x) - 4503599627370496.0;  // exact
             if constexpr (!FASTDIV) {
                 return (0.25 * xd) / L;
@@ -283,67 +258,70 @@ __global__ void __launch_bounds__(kTThreads, 1)
         for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++u) {
             const int I = order[t].x, J = order[t].y;
             const bool mirror = SYM && I != J;
-            const int b = u & 1;
-            mbar_wait(&acc_full[b], (u >> 1) & 1);
+            const int b = u % kAccBufs;
+            mbar_wait(&acc_full[b], (u / kAccBufs) & 1);
             tc_fence_after();
+            const int r0 = I * kTT + q * 32;  // this warp's first tile row
 #pragma unroll 1
-            for (int a = 0; a < (mirror ? 2 : 1); ++a) {
-                const int rb = (a == 0 ? I : J) * kTT, cb = (a == 0 ? J : I) * kTT + cw;
-                const int rend = (a == 0 && !SYM) ? row0 + nrows : count;
-                const int roff = (a == 0 && !SYM) ? row0 : 0;
-#pragma unroll 1
-                for (int lg = 0; lg < 2; ++lg) {
-                    uint32_t v[32];
-                    tmem_ld_16x256b_x8(tmem + (static_cast<uint32_t>(q * 32 + lg * 16) << 16) +
-                                           static_cast<uint32_t>(b * 2 * kTT + a * kTT + cw),
-                                       v);
-                    tmem_ld_wait();
-                    if (lg == 1 && a == (mirror ? 1 : 0)) {
-                        // this warp's accumulator reads are done: the MMA
-                        // warp may reuse buffer b
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&acc_empty[b]);
-                    }
-                    const int r16 = rb + q * 32 + lg * 16;  // first row of the block
-                    if (vec) {
-                        // the staged block is free once the previous stores read it
-                        if (lane == 0 && pending) bulk_wait_read0();
-                        __syncwarp();
+            for (int ch = 0; ch < 2; ++ch) {
+                const int c0 = J * kTT + cw + ch * 32;  // first column of the chunk
+                int32_t v[32];
+                tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) +
+                              static_cast<uint32_t>(b * kTT + cw + ch * 32),
+                          v);
+                tmem_ld_wait();
+                if (ch == 1) {
+                    // this warp's accumulator reads are done: the MMA warp
+                    // may reuse buffer b
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&acc_empty[b]);
+                }
+                double dv[32];
 #pragma unroll
-                        for (int half = 0; half < 2; ++half)
+                for (int j = 0; j < 32; ++j) dv[j] = conv(v[j]);
+                if (!vec) {
+                    const int i = r0 + lane;
+                    if (i < (SYM ? count : row0 + nrows))
+                        for (int j = 0; j < 32; ++j)
+                            if (c0 + j < count) out[static_cast<size_t>(i - (SYM ? 0 : row0)) * ld + c0 + j] = dv[j];
+                    if (mirror)
+                        for (int j = 0; j < 32; ++j)
+                            if (c0 + j < count && r0 + lane < count)
+                                out[static_cast<size_t>(c0 + j) * ld + r0 + lane] = dv[j];
+                    continue;
+                }
+                // the staged boxes are free once the previous stores read them
+                if (lane == 0 && pending) bulk_wait_read0();
+                __syncwarp();
+                // tile rows: box k = j / 16 (32 rows x 16 columns), row = lane,
+                // 16-byte chunk (j % 16) / 2 swizzled with lane & 7
 #pragma unroll
-                            for (int n = 0; n < 8; ++n) {
-                                // row 8 half + tr of box n / 2, 16-byte chunk
-                                // 4 (n & 1) + lane % 4 swizzled with the row (& 7 = tr)
-                                const int ch = 4 * (n & 1) + (lane & 3);
-                                *reinterpret_cast<double2*>(wst + (n >> 1) * 2048 + (half * 8 + tr) * 128 +
-                                                            ((ch ^ tr) << 4)) =
-                                    make_double2(conv(v[4 * n + 2 * half]), conv(v[4 * n + 2 * half + 1]));
-                            }
-                        fence_proxy_async();  // generic-proxy writes -> TMA reads
-                        __syncwarp();
-                        if (lane == 0 && r16 < rend) {
+                for (int j = 0; j < 32; j += 2)
+                    *reinterpret_cast<double2*>(wst + (j >> 4) * 4096 + lane * 128 +
+                                                ((((j & 15) >> 1) ^ (lane & 7)) << 4)) =
+                        make_double2(dv[j], dv[j + 1]);
+                if (mirror) {
+                    // mirror rows c0 + j, columns r0 + lane: box lane / 16,
+                    // row j, chunk (lane % 16) / 2 swizzled with j & 7
+                    unsigned char* mb = wst + 8192 + (lane >> 4) * 4096 + (lane & 1) * 8;
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                tma_store_2d(&dmap, wst + k * 2048, cb + 16 * k, r16 - roff, pol);
-                            bulk_commit();
-                            pending = true;
-                        }
-                        continue;
-                    }
+                    for (int j = 0; j < 32; ++j)
+                        *reinterpret_cast<double*>(mb + j * 128 + ((((lane & 15) >> 1) ^ (j & 7)) << 4)) =
+                            dv[j];
+                }
+                fence_proxy_async();  // generic-proxy writes -> TMA reads
+                __syncwarp();
+                if (lane == 0) {
+                    const int rr = r0 - (SYM ? 0 : row0);
 #pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        const int i = r16 + 8 * half + tr;
-                        if (i >= rend) continue;
-                        double* orow = out + static_cast<size_t>(i - roff) * ld + cb + tcol;
+                    for (int k = 0; k < 2; ++k) tma_store_2d(&dmap, wst + k * 4096, c0 + 16 * k, rr, pol);
+                    if (mirror)
 #pragma unroll
-                        for (int n = 0; n < 8; ++n) {
-                            const int j = cb + tcol + 8 * n;
-                            if (j < count) __stcs(orow + 8 * n, conv(v[4 * n + 2 * half]));
-                            if (j + 1 < count) __stcs(orow + 8 * n + 1, conv(v[4 * n + 2 * half + 1]));
-                        }
-                    }
+                        for (int k = 0; k < 2; ++k)
+                            tma_store_2d(&dmap, wst + 8192 + k * 4096, r0 + 16 * k, c0, pol);
+                    bulk_commit();
+                    pending = true;
                 }
             }
         }
@@ -351,12 +329,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 4 * kTT);
+    if (warp == 1) tmem_dealloc(tmem, kAccBufs * kTT);
 }
 
 size_t hamming_tc_smem() {
     return 1024 + static_cast<size_t>(kTStages) * kStageOps +
-           static_cast<size_t>(kStageBytes) + (2 * kTStages + 4) * 8 + 64;
+           static_cast<size_t>(kStageBytes) + (2 * kTStages + 2 * kAccBufs) * 8 + 64;
 }
 
 // q = h (1 / L) corrected by one remainder step equals the IEEE quotient h / L
@@ -395,11 +373,11 @@ bool launch_hamming_tc(const uint32_t* lo, const uint32_t* hi, size_t count, int
         k_hamming_encode<<<grid, 256, 0, st>>>(lo, hi, static_cast<int>(count), words, length,
                                                nblk, nks, enc.as<int8_t>());
     }
-    // D's tensor map (box 16 columns x 16 rows, 128-byte swizzle): rows of
+    // D's tensor map (box 16 columns x 32 rows, 128-byte swizzle): rows of
     // the band (or the whole matrix), 16-byte aligned rows only
     CUtensorMap dmap{};
     if ((ld & 1) == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 &&
-        !Ctx::get().encode_tmap(&dmap, d, DType::F64, nrows, count, ld, 16))
+        !Ctx::get().encode_tmap(&dmap, d, DType::F64, nrows, count, ld, 32))
         throw Error(errc::internal, "cuTensorMapEncodeTiled failed (Hamming D)");
     const size_t smem = hamming_tc_smem();
     const bool fast_div = fast_div_exact(length);
