@@ -330,6 +330,144 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
     }
 }
 
+// Small problems (w <= 20): one warp, the matrix in registers. Lane i holds
+// row i of A (full storage) and row i of V. The tournament is run on fixed
+// positions — pairs (k, M-1-k) every round — and the data moves instead
+// (circle method: position 0 fixed, position j -> j+1, M-1 -> 1), so every
+// register index is a compile-time constant: column updates and the column
+// move are register operations, rotation inputs, the partner row and the row
+// move are shuffles. No shared memory and no barriers in the sweep. Same
+// rotations (jacobi_rot2), same convergence test, same tail (evd_finish_dg
+// with eigenvalues in original index order). Padded positions (w odd) keep
+// a_pq = 0, so their rotations are exact identities.
+template <int M>
+__global__ void __launch_bounds__(32, 1) k_evd_warp(const double* __restrict__ bmat, int wp, int w,
+                                                    int rank, int requested,
+                                                    const double* __restrict__ scalars,
+                                                    int fro_index, EvdOut o) {
+    constexpr int H = M / 2;
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ double dg[32], Vs[32 * 32];
+    __shared__ int order[32], kept[32];
+    const int lane = threadIdx.x;
+    const long long t_a = clock64();
+    double a[M], v[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        a[j] = (lane < w && j < w) ? 0.5 * (bmat[lane * wp + j] + bmat[j * wp + lane]) : 0.0;
+        v[j] = (j == lane) ? 1.0 : 0.0;
+    }
+    const bool isp = lane < H;
+    const int partner = lane < M ? M - 1 - lane : lane;
+    const int from = lane == 0 ? 0 : (lane == 1 ? M - 1 : (lane < M ? lane - 1 : lane));
+    int done = __all_sync(FULL, w <= 1) ? 1 : 0, sweeps = 0;
+    long long rounds = 0;
+    for (; sweeps < 60 && !done; ++sweeps) {
+#pragma unroll 1
+        for (int r = 0; r < M - 1; ++r, ++rounds) {
+            // rotation of this lane's pair (lanes < H): A[k][k], A[q][q], A[k][q]
+            double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const double x = __shfl_sync(FULL, a[k], k);
+                const double y = __shfl_sync(FULL, a[M - 1 - k], M - 1 - k);
+                const double z = __shfl_sync(FULL, a[M - 1 - k], k);
+                if (lane == k) {
+                    app = x;
+                    aqq = y;
+                    apq = z;
+                }
+            }
+            double c, s;
+            jacobi_rot2(app, aqq, apq, c, s);
+            // A J and V J: columns (k, M-1-k) of every row
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const double ck = __shfl_sync(FULL, c, k), sk = __shfl_sync(FULL, s, k);
+                const double ap = a[k], aq = a[M - 1 - k];
+                a[k] = ck * ap - sk * aq;
+                a[M - 1 - k] = sk * ap + ck * aq;
+                const double vp = v[k], vq = v[M - 1 - k];
+                v[k] = ck * vp - sk * vq;
+                v[M - 1 - k] = sk * vp + ck * vq;
+            }
+            // J^T (A J): rows p' = c p - s q, q' = s p + c q with the own pair's rotation
+            const double co = __shfl_sync(FULL, c, isp ? lane : partner);
+            const double so = __shfl_sync(FULL, s, isp ? lane : partner);
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                const double t = __shfl_sync(FULL, a[j], partner);
+                a[j] = isp ? co * a[j] - so * t : so * t + co * a[j];
+            }
+#pragma unroll
+            for (int k = 0; k < H; ++k) {  // the annihilated pair, exactly
+                if (lane == k) a[M - 1 - k] = 0.0;
+                if (lane == M - 1 - k) a[k] = 0.0;
+            }
+            // move the data one tournament step: columns in registers, rows by shuffle
+            {
+                const double al = a[M - 1], vl = v[M - 1];
+#pragma unroll
+                for (int j = M - 1; j >= 2; --j) {
+                    a[j] = a[j - 1];
+                    v[j] = v[j - 1];
+                }
+                if (M > 1) {
+                    a[1] = al;
+                    v[1] = vl;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < M; ++j) a[j] = __shfl_sync(FULL, a[j], from);
+        }
+        // convergence: off-diagonal vs diagonal energy (as jacobi_converged)
+        double off = 0.0, dgs = 0.0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            if (j == lane) dgs += a[j] * a[j];
+            else off += a[j] * a[j];
+        }
+        off = warp_sum(off);
+        dgs = warp_sum(dgs);
+        // a vote keeps the loop condition warp-uniform for the compiler (no
+        // collective fallback around the shuffles)
+        done = __all_sync(FULL, off == 0.0 || off <= 1e-34 * dgs) ? 1 : 0;
+    }
+    const long long t_b = clock64();
+    // position j holds original index 1 + (j - 1 - rounds) mod (M - 1) (0 stays)
+    const int sh = M > 1 ? static_cast<int>(rounds % (M - 1)) : 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const int oj = j == 0 ? 0 : 1 + ((j - 1 - sh + (M - 1)) % (M - 1));
+        if (oj < w) {
+            if (lane == j) dg[oj] = a[j];
+            if (lane < w) Vs[lane * w + oj] = v[j];
+        }
+    }
+    __syncwarp();
+    evd_finish_dg(dg, Vs, w, w, rank, requested, scalars, fro_index, o, sweeps, done, order, kept);
+    if (lane == 0) {
+        g_evd_prof[0] = t_b - t_a;
+        g_evd_prof[1] = 0;
+        g_evd_prof[2] = 0;
+        g_evd_prof[3] = 0;
+        g_evd_prof[4] = clock64() - t_b;
+        g_evd_prof[5] = sweeps;
+    }
+}
+
+template <int M>
+void launch_evd_warp_m(int m, const double* b, int wp, int w, int rank, int requested_rank,
+                       const double* scalars, int fro_index, const EvdOut& o, cudaStream_t st) {
+    if constexpr (M <= 20) {
+        if (m == M) {
+            k_evd_warp<M><<<1, 32, 0, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
+            return;
+        }
+        launch_evd_warp_m<M + 2>(m, b, wp, w, rank, requested_rank, scalars, fro_index, o, st);
+    }
+}
+
 // rows of the panel staged per chunk by k_lift (<= 64 KB of shared memory)
 __host__ __device__ constexpr int lift_chunk_rows(int wp) { return wp <= 64 ? 128 : 64; }
 
@@ -456,11 +594,28 @@ extern "C" void divscope_debug_evd_prof(long long* host16) {
 
 void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
                 const double* scalars, int fro_index, const EvdOut& o, cudaStream_t st) {
+    static const bool warp_evd = [] {
+        const char* e = std::getenv("DSB_EVD_WARP");
+        return !(e && std::atoi(e) == 0);
+    }();
+    // the register kernel wins up to w = 20 (measured: w = 12 63k vs 101k
+    // cycles, w = 20 162k vs 174k); wider, its single warp is latency-bound
+    // (w = 30: 867k vs 337k) and the CTA kernel is used
+    if (warp_evd && w >= 1 && w <= 20) {
+        launch_evd_warp_m<2>(w + (w & 1), b, wp, w, rank, requested_rank, scalars, fro_index, o,
+                             st);
+        count_launch();
+        return;
+    }
     {
         const size_t smem = (static_cast<size_t>(w) * (w + 1) / 2 + static_cast<size_t>(w) * w) *
                             sizeof(double);
         allow_dyn_smem(reinterpret_cast<const void*>(k_evd));
-        const int threads = w <= 32 ? 128 : (w <= 64 ? 256 : kEvdThreads);
+        static const int forced = [] {
+            const char* e = std::getenv("DSB_EVD_THREADS");
+            return e ? std::atoi(e) : 0;
+        }();
+        const int threads = forced > 0 ? forced : (w <= 32 ? 128 : (w <= 64 ? 256 : kEvdThreads));
         k_evd<<<1, threads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
     }
     count_launch();
