@@ -53,6 +53,15 @@ void ensure_dyn_smem(const void* kernel, size_t bytes) {
 void count_launch(int k) { g_launches.fetch_add(static_cast<uint64_t>(k)); }
 uint64_t kernel_launch_count() { return g_launches.load(); }
 
+void record_timing_event(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else
+        cudaEventRecord(e, st);
+}
+
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
         throw Error(errc::internal, std::string("CUDA error: ") + cudaGetErrorString(e) + " (" +
@@ -132,6 +141,7 @@ void Ctx::set_device(int dev) {
     if (inited_ && dev == device) return;
     if (inited_) {
         DSB_CUDA(cudaStreamSynchronize(stream));
+        clear_graphs();  // they address the arena
         arena_.clear();
         omega_key = OmegaKey{};  // its panel lived in the arena
         if (g_live_bufs.load() != 0)
@@ -151,6 +161,17 @@ void Ctx::set_device(int dev) {
     }
     DSB_CUDA(cudaSetDevice(dev));
     init();
+}
+
+void Ctx::clear_graphs() {
+    for (auto& kv : graphs) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        for (auto& e : kv.second.timed) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+    }
+    graphs.clear();
 }
 
 void* Ctx::scratch(const std::string& slot, size_t bytes) {

@@ -152,6 +152,19 @@ public:
 
     void set_device(int dev);
 
+    // captured solve sequences (solver.cpp run): signature -> executable
+    // graph, the kernel launches it contains, its product passes and, when
+    // captured with timing on, the graph-owned event pair of each pass
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t launches = 0;
+        int products = 0;
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
+    };
+    std::map<uint64_t, GraphEntry> graphs;
+    bool graphs_broken = false;  // a capture failed once: eager from then on
+    void clear_graphs();
+
     // key of the device-resident Omega panel ("omega_panel" scratch slot)
     struct OmegaKey {
         bool ok = false;

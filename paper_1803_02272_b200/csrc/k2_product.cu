@@ -297,7 +297,7 @@ void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
                double* part, const double* row_mean, const double* scalars,
                const double* colsums, double* y, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
                const int* skip) {
-    if (e0) cudaEventRecord(e0, st);
+    if (e0) record_timing_event(e0, st);
     if (dt == DType::F64) {
         if (mode)
             run_product<WP, double, true, CW>(tmap, p, x, part, st, skip);
@@ -309,7 +309,7 @@ void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
         else
             run_product<WP, float, false, CW>(tmap, p, x, part, st, skip);
     }
-    if (e1) cudaEventRecord(e1, st);
+    if (e1) record_timing_event(e1, st);
     k2_reduce<WP, bm_of<CW>()><<<p.nb * (bm_of<CW>() / reduce_rows(bm_of<CW>())), 256, 0, st>>>(
         part, p.maxseg, p.nk, p.total, p.grid, p.n, mode, row_mean, scalars, colsums, y, skip);
 }

@@ -890,7 +890,7 @@ void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
         const int nb = p.gnb[0];
         digits(nb, p.gc0[0], bdig);
         digits(nb, p.gc0[1], bdig + p.bdig_stride);
-        if (e0) cudaEventRecord(e0, st);
+        if (e0) record_timing_event(e0, st);
         const size_t bs = p.bdig_stride;
         (void)nb;  // 48 (k2i_plan)
         if (ham)
@@ -907,7 +907,7 @@ void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
         for (int g = 0; g < p.ngroups; ++g) {
             const int nb = p.gnb[g], cg0 = p.gc0[g];
             digits(nb, cg0, bdig);
-            if (g == 0 && e0) cudaEventRecord(e0, st);
+            if (g == 0 && e0) record_timing_event(e0, st);
             if (ham) {
                 if (nb == 32)
                     run_i8<32, double, 3>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
@@ -933,7 +933,8 @@ void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
         }
         count_launch(2 * p.ngroups);
     }
-    if (e1) cudaEventRecord(e1, st);
+    // (external records: real event nodes when the solve is captured as a graph)
+    if (e1) record_timing_event(e1, st);
     launch_k2_reduce(wp, kRowsI8, part, p.maxseg, p.nks, p.total, p.grid, p.nrows, 1, row_mean,
                      scalars, colsums, y, st, skip);
     count_launch(1);

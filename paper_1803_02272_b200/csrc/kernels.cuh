@@ -265,6 +265,9 @@ void allow_dyn_smem(const void* kernel);
 // dynamic shared memory >= bytes for `kernel` on the current device
 void ensure_dyn_smem(const void* kernel, size_t bytes);
 uint64_t kernel_launch_count();
+// cudaEventRecord, as an event node when the stream is being captured into a
+// graph (a plain record there only marks a capture dependency)
+void record_timing_event(cudaEvent_t e, cudaStream_t st);
 void count_launch(int k = 1);
 
 }  // namespace dsb

@@ -245,23 +245,21 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     double* wmat = static_cast<double*>(c.scratch("wmat", wp * wp * sizeof(double)));
     double* rinv = static_cast<double*>(c.scratch("rinv", wp * wp * sizeof(double)));
     int* flags = static_cast<int*>(c.scratch("flags", 64));
-    DSB_CUDA(cudaMemsetAsync(flags, 0, 64, c.stream));
 
     // Omega: host-generated (bit-identical to the reference), relayout on the
     // device once per (seed, n, w) and kept resident (a pure function of the
     // seed); every solve starts from a device copy of it
+    double* omega_cached = static_cast<double*>(c.scratch("omega_panel", pbytes));
     {
         Ctx::OmegaKey& key = c.omega_key;
-        double* cached = static_cast<double*>(c.scratch("omega_panel", pbytes));
         if (!key.ok || key.seed != seed || key.n != n || key.w != w || key.n_pad != n_pad) {
             key.ok = false;  // the slot may have been reallocated by the scratch call above
             const double* om = omega_host(seed, n, w);
             double* stage = static_cast<double*>(c.scratch("omega_rm", n * w * sizeof(double)));
             c.h2d_copy(stage, om, n * w * sizeof(double));
-            launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, cached, c.stream);
+            launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, omega_cached, c.stream);
             key = Ctx::OmegaKey{true, seed, n, w, n_pad};
         }
-        DSB_CUDA(cudaMemcpyAsync(P0, cached, pbytes, cudaMemcpyDeviceToDevice, c.stream));
     }
 
     // DSB_TRACE=1: device timestamps between the stages of this solve (stderr)
@@ -280,13 +278,47 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         cudaEventRecord(e, c.stream);
         marks.emplace_back(what_, e);
     };
-    mark("start");
-    if (trace) std::fprintf(stderr, "[trace] host setup %.1f us\n", host_us());
     // per-CTA column statistics left by the fused orth kernel for the next
     // product pass (saves its separate column-statistics pass)
     double* cstat = static_cast<double*>(c.scratch(
         "orth_cstat", static_cast<size_t>(orth_fused_grid(n_pad, c.sms)) * 3 * wp * sizeof(double)));
+    // every workspace of the solve is claimed before any work is enqueued, so
+    // the sequence below can be captured as a graph (no allocation inside)
+    const size_t req = what == What::Embed ? requested : std::min(rank, w);
+    // eigenvector mode: k_evd keeps the first `keep` vectors whatever their sign
+    const int evd_req = what == What::EigsVectors ? -1 : static_cast<int>(req);
+    EvdOut eo;
+    eo.vals = static_cast<double*>(c.scratch("evd_vals", kMaxWP * sizeof(double)));
+    eo.vkeep = static_cast<double*>(c.scratch("evd_vkeep", w * std::max<size_t>(req, 1) * 8));
+    eo.kept_vals = static_cast<double*>(c.scratch("evd_kept", kMaxWP * sizeof(double)));
+    eo.dmeta = static_cast<double*>(c.scratch("evd_dmeta", 8 * sizeof(double)));
+    eo.imeta = static_cast<int*>(c.scratch("evd_imeta", 8 * sizeof(int)));
+    const int lift_P = lift_grid(n, c.sms);
+    double* lp = nullptr;
+    double* res_out = nullptr;  // U (n x req): coordinates or Ritz vectors
+    if (what == What::Embed || what == What::EigsVectors) {
+        lp = static_cast<double*>(c.scratch(
+            "lift_part", (static_cast<size_t>(lift_P) * 2 + 1) * std::max<size_t>(req, 1) * 8));
+        res_out = static_cast<double*>(
+            c.scratch("lift_out", n * std::max<size_t>(req, 1) * sizeof(double)));
+    }
+    // read back into pinned memory, one sync for all of it
+    struct Meta {
+        double vals[kMaxWP];
+        double kept[kMaxWP];
+        double dmeta[8];
+        int imeta[8];
+        int flags;
+    };
+    Meta& meta = *static_cast<Meta*>(c.pinned_scratch("run_meta", sizeof(Meta)));
+
+    // the solve as one stream sequence: eager, or captured once per signature
+    // (shape, product kernel, workspace addresses) and replayed as a CUDA
+    // graph — 25-40 dependent launches per solve, whose launch gaps are most
+    // of a small solve's time
     bool stats_ready = false;
+    int nprod = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* graph_timed = nullptr;
     auto product = [&](const double* x, double* y) {
         if (stats_ready) {
             // the orth kernel that produced x left its column statistics
@@ -299,8 +331,17 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
             launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
         }
         stats_ready = false;
-        cudaEvent_t e0, e1;
-        c.make_events(&e0, &e1);
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (graph_timed) {
+            // graph-owned timing events (read after every replay)
+            if (c.timing) {
+                DSB_CUDA(cudaEventCreate(&e0));
+                DSB_CUDA(cudaEventCreate(&e1));
+                graph_timed->emplace_back(e0, e1);
+            }
+        } else {
+            c.make_events(&e0, &e1);
+        }
         if (use_i8)
             launch_k2i(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x, n_pad,
                        g.gram->row_exp->as<int>(), pmax,
@@ -309,7 +350,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         else
             launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums,
                       y, n_pad, c.stream, e0, e1);
-        c.add_timed(1, e0, e1);
+        if (!graph_timed) c.add_timed(1, e0, e1);
+        ++nprod;
         mark("product");
     };
     // CholeskyQR3 with shift/drop handling: y -> t -> y -> out
@@ -332,81 +374,158 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         launch_chol_inv(wmat, wp, wi, n, 0, rinv, flags, c.stream);
         launch_panel_apply(y, rinv, n_pad, wp, out, c.stream);
     };
+    // ref rsvd.cpp:94-98, then (not for the range) :108-145
+    auto enqueue = [&] {
+        stats_ready = false;
+        nprod = 0;
+        DSB_CUDA(cudaMemsetAsync(flags, 0, 64, c.stream));
+        DSB_CUDA(cudaMemcpyAsync(P0, omega_cached, pbytes, cudaMemcpyDeviceToDevice, c.stream));
+        mark("start");
+        product(P0, P1);
+        orth(P1, P2, P0);
+        for (size_t it = 0; it < q; ++it) {
+            product(P0, P1);
+            orth(P1, P2, P0);
+            product(P0, P1);
+            orth(P1, P2, P0);
+        }
+        if (what == What::Range) return;
+        // ref rsvd.cpp:108-110: GQ, B = Q^T GQ (symmetrized inside K5)
+        product(P0, P1);
+        launch_panel_dot(P0, P1, n_pad, wp, psmall, wmat, c.sms, c.stream);
+        mark("ritz_gram");
+        launch_evd(wmat, wp, wi, static_cast<int>(rank), evd_req, scal_dev, fro_index, eo,
+                   c.stream);
+        mark("evd");
+        if (what == What::Embed)
+            launch_lift(P0, n, wp, wi, eo.vkeep, eo.kept_vals, eo.imeta, static_cast<int>(req),
+                        res_out, lp, c.sms, c.stream);
+        if (what == What::EigsVectors)  // U = Q V_keep (no sign rule, no scaling)
+            launch_lift_partial(P0, n, wp, wi, eo.vkeep, eo.imeta, static_cast<int>(req), res_out,
+                                lp, 0, lift_P, c.stream);
+        DSB_CUDA(cudaGetLastError());
+        DSB_CUDA(cudaMemcpyAsync(meta.vals, eo.vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
+        DSB_CUDA(cudaMemcpyAsync(meta.kept, eo.kept_vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
+        DSB_CUDA(cudaMemcpyAsync(meta.dmeta, eo.dmeta, 8 * 8, cudaMemcpyDeviceToHost, c.stream));
+        DSB_CUDA(cudaMemcpyAsync(meta.imeta, eo.imeta, 8 * sizeof(int), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        DSB_CUDA(cudaMemcpyAsync(&meta.flags, flags, sizeof(int), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        mark("lift");
+    };
 
-    // ref rsvd.cpp:94-98
-    product(P0, P1);
-    orth(P1, P2, P0);
-    for (size_t it = 0; it < q; ++it) {
-        product(P0, P1);
-        orth(P1, P2, P0);
-        product(P0, P1);
-        orth(P1, P2, P0);
-    }
     RunOut out;
     if (what == What::Range) {
+        enqueue();
         double* rm = static_cast<double*>(c.scratch("range_rm", n * w * sizeof(double)));
         launch_panel_to_rowmajor(P0, n, wi, wp, rm, c.stream);
         DSB_CUDA(cudaGetLastError());
         c.d2h_copy(range_out, rm, n * w * sizeof(double));
         return out;
     }
-    // ref rsvd.cpp:108-110: GQ, B = Q^T GQ (symmetrized inside K5)
-    product(P0, P1);
-    launch_panel_dot(P0, P1, n_pad, wp, psmall, wmat, c.sms, c.stream);
-    const size_t req = what == What::Embed ? requested : std::min(rank, w);
-    // eigenvector mode: k_evd keeps the first `keep` vectors whatever their sign
-    const int evd_req = what == What::EigsVectors ? -1 : static_cast<int>(req);
-    EvdOut eo;
-    eo.vals = static_cast<double*>(c.scratch("evd_vals", kMaxWP * sizeof(double)));
-    eo.vkeep = static_cast<double*>(c.scratch("evd_vkeep", w * std::max<size_t>(req, 1) * 8));
-    eo.kept_vals = static_cast<double*>(c.scratch("evd_kept", kMaxWP * sizeof(double)));
-    eo.dmeta = static_cast<double*>(c.scratch("evd_dmeta", 8 * sizeof(double)));
-    eo.imeta = static_cast<int*>(c.scratch("evd_imeta", 8 * sizeof(int)));
-    mark("ritz_gram");
-    launch_evd(wmat, wp, wi, static_cast<int>(rank), evd_req, scal_dev, fro_index, eo, c.stream);
-    mark("evd");
-    double* coords = nullptr;
-    std::shared_ptr<DevBuf> dcoords;
-    if (what == What::Embed) {
-        // owned by the returned embedding (host copy on first access)
-        dcoords = std::make_shared<DevBuf>(n * std::max<size_t>(req, 1) * 8);
-        coords = dcoords->as<double>();
-        const int P = static_cast<int>(std::min<size_t>(static_cast<size_t>(c.sms) * 2,
-                                                        std::max<size_t>(n / 64, 1)));
-        double* lp = static_cast<double*>(
-            c.scratch("lift_part", (static_cast<size_t>(P) * 2 + 1) * std::max<size_t>(req, 1) * 8));
-        launch_lift(P0, n, wp, wi, eo.vkeep, eo.kept_vals, eo.imeta, static_cast<int>(req),
-                    coords, lp, c.sms, c.stream);
+    static const bool graphs_on = [] {
+        const char* e = std::getenv("DSB_GRAPH");
+        return !(e && std::atoi(e) == 0);
+    }();
+    Ctx::GraphEntry* ge = nullptr;
+    if (graphs_on && !trace && !c.graphs_broken) {
+        uint64_t h = 1469598103934665603ull;
+        auto mix = [&](uint64_t v) {
+            for (int i = 0; i < 8; ++i) {
+                h ^= (v >> (8 * i)) & 0xff;
+                h *= 1099511628211ull;
+            }
+        };
+        auto mixp = [&](const void* ptr) { mix(reinterpret_cast<uintptr_t>(ptr)); };
+        mix(n); mix(w); mix(wp); mix(q); mix(rank); mix(req); mix(static_cast<uint64_t>(evd_req));
+        mix(static_cast<uint64_t>(what)); mix(use_i8); mix(static_cast<uint64_t>(hamming_i8));
+        mix(mode); mix(static_cast<uint64_t>(s.dt)); mix(s.rows); mix(s.cols); mix(s.ld);
+        mix(static_cast<uint64_t>(fro_index)); mix(c.timing); mix(static_cast<uint64_t>(c.sms));
+        mix(static_cast<uint64_t>(product_path()));
+        mixp(s.buf ? s.buf->p : nullptr); mixp(scal_dev); mixp(row_mean);
+        mixp(use_i8 ? g.gram->row_exp->p : nullptr);
+        for (const void* ptr : {static_cast<const void*>(P0), static_cast<const void*>(P1),
+                                static_cast<const void*>(P2), static_cast<const void*>(part),
+                                static_cast<const void*>(psmall),
+                                static_cast<const void*>(colsums),
+                                static_cast<const void*>(wmat), static_cast<const void*>(rinv),
+                                static_cast<const void*>(flags), static_cast<const void*>(cstat),
+                                static_cast<const void*>(pmax), static_cast<const void*>(col_exp),
+                                static_cast<const void*>(bdig),
+                                static_cast<const void*>(omega_cached),
+                                static_cast<const void*>(eo.vals),
+                                static_cast<const void*>(eo.vkeep),
+                                static_cast<const void*>(eo.kept_vals),
+                                static_cast<const void*>(eo.dmeta),
+                                static_cast<const void*>(eo.imeta), static_cast<const void*>(lp),
+                                static_cast<const void*>(res_out),
+                                static_cast<const void*>(&meta)})
+            mixp(ptr);
+        auto it = c.graphs.find(h);
+        if (it != c.graphs.end()) {
+            ge = &it->second;
+            count_launch(static_cast<int>(ge->launches));
+        } else {
+            if (c.graphs.size() >= 16) c.clear_graphs();
+            Ctx::GraphEntry e;
+            graph_timed = &e.timed;
+            const uint64_t l0 = kernel_launch_count();
+            cudaGraph_t graph = nullptr;
+            DSB_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+            try {
+                enqueue();
+            } catch (...) {
+                cudaStreamEndCapture(c.stream, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                graph_timed = nullptr;
+                for (auto& ev : e.timed) {
+                    cudaEventDestroy(ev.first);
+                    cudaEventDestroy(ev.second);
+                }
+                throw;
+            }
+            graph_timed = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(c.stream, &graph);
+            cudaGraphExec_t exec = nullptr;
+            if (ce == cudaSuccess && graph &&
+                cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+                e.exec = exec;
+                e.launches = kernel_launch_count() - l0;
+                e.products = nprod;
+                ge = &(c.graphs[h] = std::move(e));
+            } else {
+                // this sequence does not capture here: eager from now on
+                (void)cudaGetLastError();
+                c.graphs_broken = true;
+                for (auto& ev : e.timed) {
+                    cudaEventDestroy(ev.first);
+                    cudaEventDestroy(ev.second);
+                }
+            }
+            if (graph) cudaGraphDestroy(graph);
+        }
     }
-    std::unique_ptr<DevBuf> dvec;
-    if (what == What::EigsVectors) {
-        // U = Q V_keep for the keep Ritz pairs (no sign rule, no scaling)
-        dvec = std::make_unique<DevBuf>(n * std::max<size_t>(req, 1) * 8);
-        const int P = lift_grid(n, c.sms);
-        double* lp = static_cast<double*>(
-            c.scratch("lift_part", (static_cast<size_t>(P) * 2 + 1) * std::max<size_t>(req, 1) * 8));
-        launch_lift_partial(P0, n, wp, wi, eo.vkeep, eo.imeta, static_cast<int>(req),
-                            dvec->as<double>(), lp, 0, P, c.stream);
+    if (ge) {
+        DSB_CUDA(cudaGraphLaunch(ge->exec, c.stream));
+        c.k2_launches += static_cast<uint64_t>(ge->products);
+    } else {
+        enqueue();
     }
-    DSB_CUDA(cudaGetLastError());
-    // read back into pinned memory, one sync for all of it
-    struct Meta {
-        double vals[kMaxWP];
-        double kept[kMaxWP];
-        double dmeta[8];
-        int imeta[8];
-        int flags;
-    };
-    Meta& meta = *static_cast<Meta*>(c.pinned_scratch("run_meta", sizeof(Meta)));
-    DSB_CUDA(cudaMemcpyAsync(meta.vals, eo.vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
-    DSB_CUDA(cudaMemcpyAsync(meta.kept, eo.kept_vals, w * 8, cudaMemcpyDeviceToHost, c.stream));
-    DSB_CUDA(cudaMemcpyAsync(meta.dmeta, eo.dmeta, 8 * 8, cudaMemcpyDeviceToHost, c.stream));
-    DSB_CUDA(cudaMemcpyAsync(meta.imeta, eo.imeta, 8 * sizeof(int), cudaMemcpyDeviceToHost,
-                             c.stream));
-    DSB_CUDA(cudaMemcpyAsync(&meta.flags, flags, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    mark("lift");
+    // the solve's own copy of its result (the workspace is reused)
+    std::shared_ptr<DevBuf> dres;
+    if (res_out) {
+        dres = std::make_shared<DevBuf>(n * std::max<size_t>(req, 1) * 8);
+        DSB_CUDA(cudaMemcpyAsync(dres->p, res_out, n * std::max<size_t>(req, 1) * 8,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+    }
     if (trace) std::fprintf(stderr, "[trace] host enqueue done %.1f us\n", host_us());
     c.sync();
+    if (ge && c.timing)
+        for (auto& ev : ge->timed) {
+            float ms = 0.f;
+            DSB_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+            c.k2_ms += ms;
+        }
     if (trace) std::fprintf(stderr, "[trace] host meta synced %.1f us\n", host_us());
     if (trace) {
         for (size_t i = 1; i < marks.size(); ++i) {
@@ -424,9 +543,9 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     out.vals.assign(meta.vals, meta.vals + w);
     out.keep = static_cast<size_t>(meta.imeta[0]);
     out.resid = meta.dmeta[0];
-    if (dvec) {
+    if (what == What::EigsVectors) {
         out.vectors.resize(n * out.keep);
-        c.d2h_copy(out.vectors.data(), dvec->p, out.vectors.size() * sizeof(double));
+        c.d2h_copy(out.vectors.data(), dres->p, out.vectors.size() * sizeof(double));
     }
     if (what == What::Embed) {
         Embedding& e = out.emb;
@@ -437,7 +556,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         e.resid = meta.dmeta[0];
         e.eigenvalues.assign(meta.kept, meta.kept + e.r);
         // the lift wrote n x req with row stride r (= kept columns)
-        e.dcoords = std::move(dcoords);
+        e.dcoords = std::move(dres);
     }
     if (trace) std::fprintf(stderr, "[trace] host coords done %.1f us\n", host_us());
     return out;
