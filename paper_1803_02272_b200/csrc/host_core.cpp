@@ -143,6 +143,7 @@ void Ctx::set_device(int dev) {
         DSB_CUDA(cudaStreamSynchronize(stream));
         clear_graphs();  // they address the arena
         arena_.clear();
+        tables_.clear();
         omega_key = OmegaKey{};  // its panel lived in the arena
         if (g_live_bufs.load() != 0)
             throw Error(errc::invalid_argument,
@@ -161,6 +162,17 @@ void Ctx::set_device(int dev) {
     }
     DSB_CUDA(cudaSetDevice(dev));
     init();
+}
+
+const void* Ctx::const_table(const std::string& name, const void* host, size_t bytes) {
+    auto it = tables_.find(name);
+    if (it != tables_.end()) return it->second->p;
+    auto buf = std::make_unique<DevBuf>(std::max<size_t>(bytes, 256));
+    DSB_CUDA(cudaMemcpyAsync(buf->p, host, bytes, cudaMemcpyHostToDevice, stream));
+    DSB_CUDA(cudaStreamSynchronize(stream));
+    const void* p = buf->p;
+    tables_[name] = std::move(buf);
+    return p;
 }
 
 void Ctx::clear_graphs() {

@@ -119,6 +119,10 @@ public:
 
     // grow-only workspace arena
     void* scratch(const std::string& slot, size_t bytes);
+    // immutable device table named by its content key: uploaded on first
+    // use (never inside a graph capture), then returned as is
+    bool has_table(const std::string& name) const { return tables_.count(name) != 0; }
+    const void* const_table(const std::string& name, const void* host, size_t bytes);
 
     // instrumentation
     bool timing = false;
@@ -177,6 +181,7 @@ private:
     void init();
     bool inited_ = false;
     std::map<std::string, std::unique_ptr<DevBuf>> arena_;
+    std::map<std::string, std::unique_ptr<DevBuf>> tables_;
     std::map<std::string, std::unique_ptr<PinnedVec>> pinned_arena_;
     void* encode_fn_ = nullptr;
 };

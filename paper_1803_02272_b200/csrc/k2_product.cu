@@ -30,8 +30,12 @@
 #include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
 
 #include "device_utils.cuh"
+#include "host_core.hpp"
 #include "kernels.cuh"
 
 namespace dsb {
@@ -203,76 +207,100 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     }
 }
 
-__device__ __forceinline__ long long cta_of(long long t, long long total, long long P) {
-    long long c = static_cast<long long>((static_cast<double>(t) * P) / static_cast<double>(total));
-    if (c > P - 1) c = P - 1;
-    if (c < 0) c = 0;
-    while (c + 1 < P && chunk_begin(total, c + 1, P) <= t) ++c;
-    while (c > 0 && chunk_begin(total, c, P) > t) --c;
-    return c;
-}
-
 // Sum the partial slots of each row block in CTA order, then
 //   mode 1: y = -1/2 (y - r_i s_c - t_c + g s_c)   (rank-3 centering)
 //   mode 0: y as is.
-// Rows >= n are written as zero. Output in the k4-interleaved panel layout.
-// rows of a product row block reduced per CTA (DSB_REDUCE_ROWS; measured at
-// C2: 32 and 16 ~10 us, 8 and 128 slower)
-#ifndef DSB_REDUCE_ROWS
-#define DSB_REDUCE_ROWS 32
-#endif
-constexpr int kReduceRows = DSB_REDUCE_ROWS;
-constexpr int reduce_rows(int bm) { return kReduceRows < bm ? kReduceRows : bm; }
-
-template <int WP, int BM>
+// Rows >= n are written as zero. Output in the k4-interleaved panel layout,
+// one element per thread in panel order (coalesced stores). `tab` is the
+// split's slot table (k2_slot_table): tab[b] .. tab[b + 1] index the slots
+// (cta * maxseg + segment) of row block b in tab[nb + 1 ..], in CTA order.
+template <int WP, int BM, int RPT>
 __global__ void __launch_bounds__(256)
-    k2_reduce(const double* __restrict__ part, int maxseg, int nk, long long total, int P, int n,
+    k2_reduce(const double* __restrict__ part, const int* __restrict__ tab, int nb, int n,
               int mode, const double* __restrict__ row_mean, const double* __restrict__ scalars,
               const double* __restrict__ colsums, double* __restrict__ y,
               const int* __restrict__ skip) {
     if (skip && *skip) return;
-    constexpr int kRows = kReduceRows < BM ? kReduceRows : BM;  // rows of the block per CTA
-    constexpr int kMaxSlots = 256;  // >= grid + 1 (a row block spans <= grid CTAs)
-    __shared__ long long slot_base[kMaxSlots];
-    const int b = blockIdx.x / (BM / kRows);
-    const int r0 = (blockIdx.x % (BM / kRows)) * kRows;
-    // CTAs whose stream-K range touches row block b, and their slot offsets
-    const long long c_lo = cta_of(static_cast<long long>(b) * nk, total, P);
-    const long long c_hi = cta_of(static_cast<long long>(b + 1) * nk - 1, total, P);
-    const int nslot = static_cast<int>(c_hi - c_lo + 1);
-    for (int k = threadIdx.x; k < nslot && k < kMaxSlots; k += blockDim.x) {
-        const long long cc = c_lo + k;
-        const int seg = b - static_cast<int>(chunk_begin(total, cc, P) / nk);
-        slot_base[k] = (cc * maxseg + seg) * static_cast<long long>(BM) * WP;
+    // RPT = 4: thread = one 4-row group of one column, panel elements
+    // 4 t .. 4 t + 3 (one 32-byte store); RPT = 1 (small n, few elements,
+    // many slots): thread = one element. Every load is issued before any sum.
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    size_t i0;
+    int col;
+    if constexpr (RPT == 4) {
+        i0 = static_cast<size_t>(t / WP) * 4;
+        col = static_cast<int>(t % WP);
+    } else {
+        i0 = static_cast<size_t>((t / (4 * WP)) * 4 + (t & 3));
+        col = static_cast<int>((t >> 2) % WP);
     }
-    __syncthreads();
-    const double g = mode ? scalars[S_GRAND] : 0.0;
-    for (int e = threadIdx.x; e < kRows * WP; e += blockDim.x) {
-        const int r = r0 + e / WP, col = e % WP;
-        const int eo = r * WP + col;
-        // the slots' loads are issued together (up to 16 in flight: small n
-        // splits a row block over ~20 CTAs, one L2 round trip each if
-        // serialized), then summed in CTA order
-        constexpr int kBatch = 16;
-        double v = 0.0;
-        for (int s0 = 0; s0 < nslot; s0 += kBatch) {
-            double pb[kBatch];
+    const int b = static_cast<int>(i0 / BM), r0 = static_cast<int>(i0 % BM);
+    const int s_begin = tab[b], nslot = tab[b + 1] - s_begin;
+    const int* slots = tab + nb + 1 + s_begin;
+    double rm[RPT], cs = 0.0, ct = 0.0, gr = 0.0;
+    if (mode) {
+        cs = colsums[col];
+        ct = colsums[WP + col];
+        gr = scalars[S_GRAND];
 #pragma unroll
-            for (int sl = 0; sl < kBatch; ++sl)
-                pb[sl] = s0 + sl < nslot ? part[slot_base[s0 + sl] + eo] : 0.0;
-#pragma unroll
-            for (int sl = 0; sl < kBatch; ++sl)
-                if (s0 + sl < nslot) v += pb[sl];
-        }
-        const size_t i = static_cast<size_t>(b) * BM + r;
-        if (i >= static_cast<size_t>(n)) {
-            v = 0.0;
-        } else if (mode) {
-            const double s = colsums[col], t = colsums[WP + col];
-            v = -0.5 * (v - row_mean[i] * s - t + g * s);
-        }
-        y[pidx(i, col, WP)] = v;
+        for (int j = 0; j < RPT; ++j) rm[j] = i0 + j < static_cast<size_t>(n) ? row_mean[i0 + j] : 0.0;
     }
+    const double* pp = part + static_cast<long long>(r0) * WP + col;
+    // slot loads issued in batches, summed in CTA order (deterministic); the
+    // batch width follows the slot count (2-3 at large n, ~20 at small n)
+    double v[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) v[j] = 0.0;
+    auto sum_batches = [&](auto width) {
+        constexpr int kB = decltype(width)::value;
+        for (int s0 = 0; s0 < nslot; s0 += kB) {
+            int si[kB];
+#pragma unroll
+            for (int sl = 0; sl < kB; ++sl) si[sl] = s0 + sl < nslot ? slots[s0 + sl] : 0;
+            double pb[kB][RPT];
+#pragma unroll
+            for (int sl = 0; sl < kB; ++sl)
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+                    pb[sl][j] = s0 + sl < nslot
+                                    ? pp[static_cast<long long>(si[sl]) * (BM * WP) + j * WP]
+                                    : 0.0;
+#pragma unroll
+            for (int sl = 0; sl < kB; ++sl)
+                if (s0 + sl < nslot)
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) v[j] += pb[sl][j];
+        }
+    };
+    if (nslot <= 4)
+        sum_batches(std::integral_constant<int, 4>{});
+    else
+        sum_batches(std::integral_constant<int, 32 / RPT>{});
+    double o[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        if (i0 + j >= static_cast<size_t>(n)) o[j] = 0.0;
+        else if (mode) o[j] = -0.5 * (v[j] - rm[j] * cs - ct + gr * cs);
+        else o[j] = v[j];
+    }
+    if constexpr (RPT == 4)
+        *reinterpret_cast<double4*>(y + pidx(i0, col, WP)) = make_double4(o[0], o[1], o[2], o[3]);
+    else
+        y[pidx(i0, col, WP)] = o[0];
+}
+
+// 4 rows per thread when that still fills the GPU (>= 4 CTAs per SM), else 1
+template <int WP, int BM>
+void reduce_launch(const double* part, const int* tab, int nb, int n, int mode,
+                   const double* row_mean, const double* scalars, const double* colsums, double* y,
+                   cudaStream_t st, const int* skip) {
+    const long long elems = static_cast<long long>(nb) * BM * WP;
+    if (elems / 4 >= 148LL * 4 * 256)
+        k2_reduce<WP, BM, 4><<<static_cast<unsigned>(elems / 1024), 256, 0, st>>>(
+            part, tab, nb, n, mode, row_mean, scalars, colsums, y, skip);
+    else
+        k2_reduce<WP, BM, 1><<<static_cast<unsigned>(elems / 256), 256, 0, st>>>(
+            part, tab, nb, n, mode, row_mean, scalars, colsums, y, skip);
 }
 
 template <int WP, typename TD, bool SQ, int CW, int KS>
@@ -310,22 +338,47 @@ void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
             run_product<WP, float, false, CW>(tmap, p, x, part, st, skip);
     }
     if (e1) record_timing_event(e1, st);
-    k2_reduce<WP, bm_of<CW>()><<<p.nb * (bm_of<CW>() / reduce_rows(bm_of<CW>())), 256, 0, st>>>(
-        part, p.maxseg, p.nk, p.total, p.grid, p.n, mode, row_mean, scalars, colsums, y, skip);
+    const int* tab = k2_slot_table(p.nb, p.nk, p.total, p.grid, p.maxseg);
+    reduce_launch<WP, bm_of<CW>()>(part, tab, p.nb, p.n, mode, row_mean, scalars, colsums, y, st,
+                                   skip);
 }
 
 }  // namespace
+
+const int* k2_slot_table(int nb, int nk, long long total, int P, int maxseg) {
+    const std::string name = "k2_slots_" + std::to_string(nb) + "_" + std::to_string(nk) + "_" +
+                             std::to_string(total) + "_" + std::to_string(P) + "_" +
+                             std::to_string(maxseg);
+    std::vector<std::vector<int>> per(nb);
+    if (!Ctx::get().has_table(name)) {
+        for (long long c = 0; c < P; ++c) {
+            const long long t0 = total * c / P, t1 = total * (c + 1) / P;
+            if (t1 <= t0) continue;
+            const long long bf = t0 / nk, bl = (t1 - 1) / nk;
+            for (long long b = bf; b <= bl && b < nb; ++b)
+                per[b].push_back(static_cast<int>(c * maxseg + (b - bf)));
+        }
+    }
+    std::vector<int> host;
+    if (!Ctx::get().has_table(name)) {
+        host.resize(nb + 1);
+        host[0] = 0;
+        for (int b = 0; b < nb; ++b) host[b + 1] = host[b] + static_cast<int>(per[b].size());
+        for (int b = 0; b < nb; ++b) host.insert(host.end(), per[b].begin(), per[b].end());
+    }
+    return static_cast<const int*>(
+        Ctx::get().const_table(name, host.data(), host.size() * sizeof(int)));
+}
 
 void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, long long total,
                       int P, int n, int mode, const double* row_mean, const double* scalars,
                       const double* colsums, double* y, cudaStream_t st, const int* skip) {
     const int nb = (n + bm - 1) / bm;
+    const int* tab = k2_slot_table(nb, nk, total, P, maxseg);
     switch (wp * 1000 + bm) {
 #define DSB_RED(W, B)                                                                          \
     case W * 1000 + B:                                                                         \
-        k2_reduce<W, B><<<nb * (B / reduce_rows(B)), 256, 0, st>>>(part, maxseg, nk, total, P, \
-                                                                   n, mode,                    \
-                                                       row_mean, scalars, colsums, y, skip);   \
+        reduce_launch<W, B>(part, tab, nb, n, mode, row_mean, scalars, colsums, y, st, skip);  \
         break;
         DSB_RED(8, 128) DSB_RED(16, 128) DSB_RED(24, 128) DSB_RED(32, 128) DSB_RED(40, 128)
         DSB_RED(48, 128) DSB_RED(56, 128) DSB_RED(64, 128) DSB_RED(72, 128) DSB_RED(80, 128)

@@ -90,6 +90,9 @@ void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
                cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr, const int* skip = nullptr);
 
 // k2_reduce for an explicit row-block height (bm = 128 or 256)
+// slot table of a stream-K split (k2_reduce), uploaded once per split and
+// kept in the workspace arena; call before a graph capture
+const int* k2_slot_table(int nb, int nk, long long total, int P, int maxseg);
 void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, long long total,
                       int P, int n, int mode, const double* row_mean, const double* scalars,
                       const double* colsums, double* y, cudaStream_t st, const int* skip);

@@ -312,6 +312,12 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     };
     Meta& meta = *static_cast<Meta*>(c.pinned_scratch("run_meta", sizeof(Meta)));
 
+    // the reduce's slot table of this split (uploaded here, outside a capture)
+    const int* slot_tab =
+        use_i8 ? k2_slot_table((static_cast<int>(n) + 127) / 128, iplan.nks, iplan.total, iplan.grid,
+                               iplan.maxseg)
+               : k2_slot_table(plan.nb, plan.nk, plan.total, plan.grid, plan.maxseg);
+
     // the solve as one stream sequence: eager, or captured once per signature
     // (shape, product kernel, workspace addresses) and replayed as a CUDA
     // graph — 25-40 dependent launches per solve, whose launch gaps are most
@@ -459,7 +465,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
                                 static_cast<const void*>(eo.dmeta),
                                 static_cast<const void*>(eo.imeta), static_cast<const void*>(lp),
                                 static_cast<const void*>(res_out),
-                                static_cast<const void*>(&meta)})
+                                static_cast<const void*>(&meta),
+                                static_cast<const void*>(slot_tab)})
             mixp(ptr);
         auto it = c.graphs.find(h);
         if (it != c.graphs.end()) {

@@ -4,8 +4,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import bench, paper_1803_02272_b200 as ds
 ds.set_device(0)
 cfg, n, k, p, q, seed, f32 = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
-assert cfg != 5
-D = ds.matrix_euclidean(ds.synth_points(cfg, n, seed))
+
+D = bench.make_distance(ds, sys.argv[1] if len(sys.argv) > 1 else "C2")
 for _ in range(3):
     e = ds.embed(ds.gram(D), rank=k, oversampling=p, power_iters=q, seed=seed)
 buf = (C.c_longlong * 16)()
