@@ -276,9 +276,14 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
         pair_at(r, k, m, p, q);
         sched[e] = static_cast<unsigned short>((p << 8) | q);
     }
-    // V rotation mapping: thread -> (pair vi, first row vk0), rows stride vks
-    const int vact = (nt / h) * h;  // active threads in the V phase
-    const int vi = tid % h, vk0 = tid / h, vks = nt / h;
+    // V rotation mapping: thread -> (pair vi, first row vk0), rows stride vks.
+    // With enough threads the block updates (first half) and the V row pairs
+    // (second half) run on different warps, side by side
+    const int vbase = (nt >= 256 && nblk <= nt / 2) ? nt / 2 : 0;
+    const int nbt = vbase ? vbase : nt;  // threads of the block-update phase
+    const int tv = tid - vbase, ntv = nt - vbase;
+    const int vact = (ntv / h) * h;  // active threads in the V phase
+    const int vi = tv >= 0 ? tv % h : 0, vk0 = tv >= 0 ? tv / h : 0, vks = ntv / h;
     __syncthreads();
     int done = (w <= 1), sweeps = 0;
     long long t_a = clock64(), acc1 = 0, acc2 = 0, acc3 = 0;
@@ -298,11 +303,11 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
             __syncthreads();
             const long long t1 = clock64();
             acc1 += t1 - t0;
-            for (int e = tid; e < nblk; e += nt) {
+            for (int e = tid; e < nblk && tid < nbt; e += nbt) {
                 const int i = blk_i[e], j = blk_j[e];
                 block_update(A, A, w, pp[i], qq[i], pp[j], qq[j], cs[i], sn[i], cs[j], sn[j], i == j);
             }
-            if (tid < vact && qq[vi] < w) {
+            if (tv >= 0 && tv < vact && qq[vi] < w) {
                 const int p = pp[vi], q = qq[vi];
                 const double c = cs[vi], s = sn[vi];
                 for (int k = vk0; k < w; k += vks) {
@@ -615,7 +620,7 @@ void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
             const char* e = std::getenv("DSB_EVD_THREADS");
             return e ? std::atoi(e) : 0;
         }();
-        const int threads = forced > 0 ? forced : (w <= 32 ? 128 : (w <= 64 ? 256 : kEvdThreads));
+        const int threads = forced > 0 ? forced : (w <= 64 ? 256 : kEvdThreads);
         k_evd<<<1, threads, smem, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
     }
     count_launch();
