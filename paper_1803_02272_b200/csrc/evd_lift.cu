@@ -285,6 +285,11 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
     const int vact = (ntv / h) * h;  // active threads in the V phase
     const int vi = tv >= 0 ? tv % h : 0, vk0 = tv >= 0 ? tv / h : 0, vks = ntv / h;
     __syncthreads();
+    // a thread's own block (when every block has one) is fixed for the
+    // whole solve: its pair indices stay in registers
+    const bool one_block = nblk <= nbt;
+    const int my_i = (one_block && tid < nblk) ? blk_i[tid] : 0;
+    const int my_j = (one_block && tid < nblk) ? blk_j[tid] : 0;
     int done = (w <= 1), sweeps = 0;
     long long t_a = clock64(), acc1 = 0, acc2 = 0, acc3 = 0;
     for (; sweeps < 60 && !done; ++sweeps) {
@@ -303,17 +308,38 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
             __syncthreads();
             const long long t1 = clock64();
             acc1 += t1 - t0;
-            for (int e = tid; e < nblk && tid < nbt; e += nbt) {
-                const int i = blk_i[e], j = blk_j[e];
-                block_update(A, A, w, pp[i], qq[i], pp[j], qq[j], cs[i], sn[i], cs[j], sn[j], i == j);
+            if (one_block) {
+                if (tid < nblk)
+                    block_update(A, A, w, pp[my_i], qq[my_i], pp[my_j], qq[my_j], cs[my_i],
+                                 sn[my_i], cs[my_j], sn[my_j], my_i == my_j);
+            } else {
+                for (int e = tid; e < nblk && tid < nbt; e += nbt) {
+                    const int i = blk_i[e], j = blk_j[e];
+                    block_update(A, A, w, pp[i], qq[i], pp[j], qq[j], cs[i], sn[i], cs[j], sn[j],
+                                 i == j);
+                }
             }
             if (tv >= 0 && tv < vact && qq[vi] < w) {
                 const int p = pp[vi], q = qq[vi];
                 const double c = cs[vi], s = sn[vi];
-                for (int k = vk0; k < w; k += vks) {
-                    const double vp = V[k * w + p], vq = V[k * w + q];
-                    V[k * w + p] = c * vp - s * vq;
-                    V[k * w + q] = s * vp + c * vq;
+                // the rows' loads first, then the rotations and stores (the
+                // row pairs are disjoint; 4 in flight per thread)
+                for (int k0 = vk0; k0 < w; k0 += 4 * vks) {
+                    double vp[4], vq[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int k = k0 + u * vks;
+                        vp[u] = k < w ? V[k * w + p] : 0.0;
+                        vq[u] = k < w ? V[k * w + q] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int k = k0 + u * vks;
+                        if (k < w) {
+                            V[k * w + p] = c * vp[u] - s * vq[u];
+                            V[k * w + q] = s * vp[u] + c * vq[u];
+                        }
+                    }
                 }
             }
             __syncthreads();
