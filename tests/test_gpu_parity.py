@@ -372,6 +372,45 @@ def test_deterministic(ds):
     assert np.array_equal(a.coords, b.coords) and np.array_equal(a.eigenvalues, b.eigenvalues)
 
 
+def test_graph_replay_follows_inputs(ds, oracle):
+    # a solve is captured as a CUDA graph on the first call of its signature
+    # and replayed afterwards (solver.cpp run): replays must follow a new seed
+    # (Omega re-uploaded into the same workspace slot), a second matrix of the
+    # same shape, and eigs / embed / eigs_vectors interleaved on one gram
+    n, k, p, q = 900, 10, 8, 1
+    d = oracle.euclidean_matrix(ds.synth_points(2, n, 4))
+    d2 = oracle.euclidean_matrix(ds.synth_points(2, n, 9))
+    g, g2 = ds.gram(ds.matrix_from_host(d)), ds.gram(ds.matrix_from_host(d2))
+    refs = {}
+    for dd, key in ((d, 1), (d2, 2)):
+        st, rm, grand = oracle.gram_stats(dd)
+        assert st == 0
+        for seed in (5, 6):
+            refs[key, seed] = oracle.embed(k, p, q, seed, d=dd, row_mean=rm, grand=grand)
+    first = {}
+    for key, gm, seed in [(1, g, 5), (1, g, 6), (2, g2, 5), (1, g, 5), (2, g2, 6), (1, g, 6)]:
+        e = ds.embed(gm, rank=k, oversampling=p, power_iters=q, seed=seed)
+        ref = refs[key, seed]
+        assert e.dims == ref["r"]
+        assert rel_err(e.eigenvalues, ref["eigenvalues"]) < 1e-10
+        assert coords_match_up_to_sign(e.coords, ref["coords"]) < 1e-8 * np.sqrt(ref["eigenvalues"][0])
+        if (key, seed) in first:  # a replay: bit-identical to the captured run
+            assert np.array_equal(e.coords, first[key, seed])
+        first[key, seed] = e.coords
+        vals, _ = ds.eigs(gm, rank=k, oversampling=p, power_iters=q, seed=seed)
+        vv, vecs, _ = ds.eigs_vectors(gm, rank=k, oversampling=p, power_iters=q, seed=seed)
+        assert np.array_equal(vals, vv) and vecs.shape == (n, k)
+    # the launch counter advances by the same count on every replay (the
+    # first call re-lays out Omega for the new seed: one launch more)
+    ds.embed(g, rank=k, oversampling=p, power_iters=q, seed=5)
+    l0 = ds.stats_get().kernel_launches
+    ds.embed(g, rank=k, oversampling=p, power_iters=q, seed=5)
+    l1 = ds.stats_get().kernel_launches
+    ds.embed(g, rank=k, oversampling=p, power_iters=q, seed=5)
+    l2 = ds.stats_get().kernel_launches
+    assert l2 - l1 == l1 - l0 > 0
+
+
 # ---------------------------------------------------------------- stable rank
 
 def test_stable_rank(ds):
