@@ -366,7 +366,11 @@ bool launch_hamming_tc(const uint32_t* lo, const uint32_t* hi, size_t count, int
     if (row0 % kTT != 0) return false;  // row bands start on a 128-row block
     const int nblk = static_cast<int>((count + kTT - 1) / kTT);
     const int nks = static_cast<int>((3 * static_cast<size_t>(length) + kTK - 1) / kTK);
-    DevBuf enc(static_cast<size_t>(nblk) * nks * kTileBytes);
+    // E is 3 bytes per base and read: beyond a few GB (very long reads at
+    // large n) the POPC kernel, which needs no E, builds D instead
+    const size_t enc_bytes = static_cast<size_t>(nblk) * nks * kTileBytes;
+    if (enc_bytes > (static_cast<size_t>(4) << 30)) return false;
+    DevBuf enc(enc_bytes);
     {
         const long long items = static_cast<long long>(nblk) * kTT * nks * 8;
         const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 148 * 16));
