@@ -117,6 +117,9 @@ void Ctx::init() {
                                         prop.name);
     sms = prop.multiProcessorCount;
     DSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    DSB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    DSB_CUDA(cudaEventCreateWithFlags(&side_ready, cudaEventDisableTiming));
+    DSB_CUDA(cudaEventCreateWithFlags(&side_done, cudaEventDisableTiming));
     {
         cudaMemPool_t pool;
         DSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -156,6 +159,11 @@ void Ctx::set_device(int dev) {
             cudaEventDestroy(t.b);
         }
         pending.clear();
+        cudaStreamSynchronize(side);
+        cudaEventDestroy(side_ready);
+        cudaEventDestroy(side_done);
+        cudaStreamDestroy(side);
+        side = nullptr;
         cudaStreamDestroy(stream);
         stream = nullptr;
         inited_ = false;

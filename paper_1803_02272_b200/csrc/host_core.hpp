@@ -115,6 +115,10 @@ public:
     int device = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;
+    // a second stream (the sharded path's panel all-gather, overlapped with
+    // the product over the locally-owned columns) and its two events
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_ready = nullptr, side_done = nullptr;
     std::recursive_mutex mu;  // one solver at a time per process
 
     // grow-only workspace arena

@@ -345,22 +345,25 @@ void launch_wp(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
 
 }  // namespace
 
-const int* k2_slot_table(int nb, int nk, long long total, int P, int maxseg) {
-    const std::string name = "k2_slots_" + std::to_string(nb) + "_" + std::to_string(nk) + "_" +
-                             std::to_string(total) + "_" + std::to_string(P) + "_" +
-                             std::to_string(maxseg);
-    std::vector<std::vector<int>> per(nb);
-    if (!Ctx::get().has_table(name)) {
-        for (long long c = 0; c < P; ++c) {
-            const long long t0 = total * c / P, t1 = total * (c + 1) / P;
-            if (t1 <= t0) continue;
-            const long long bf = t0 / nk, bl = (t1 - 1) / nk;
-            for (long long b = bf; b <= bl && b < nb; ++b)
-                per[b].push_back(static_cast<int>(c * maxseg + (b - bf)));
-        }
-    }
+const int* k2_slot_table_multi(int nb, const std::vector<K2Split>& splits) {
+    std::string name = "k2_slots_" + std::to_string(nb);
+    for (const K2Split& sp : splits)
+        name += "_" + std::to_string(sp.nk) + "_" + std::to_string(sp.total) + "_" +
+                std::to_string(sp.P) + "_" + std::to_string(sp.maxseg) + "_" +
+                std::to_string(sp.slot_base);
     std::vector<int> host;
     if (!Ctx::get().has_table(name)) {
+        // row block -> the slots (slot_base + cta * maxseg + segment) of the
+        // CTAs that touched it: split by split, each in CTA order
+        std::vector<std::vector<int>> per(nb);
+        for (const K2Split& sp : splits)
+            for (long long c = 0; c < sp.P; ++c) {
+                const long long t0 = sp.total * c / sp.P, t1 = sp.total * (c + 1) / sp.P;
+                if (t1 <= t0) continue;
+                const long long bf = t0 / sp.nk, bl = (t1 - 1) / sp.nk;
+                for (long long b = bf; b <= bl && b < nb; ++b)
+                    per[b].push_back(static_cast<int>(sp.slot_base + c * sp.maxseg + (b - bf)));
+            }
         host.resize(nb + 1);
         host[0] = 0;
         for (int b = 0; b < nb; ++b) host[b + 1] = host[b] + static_cast<int>(per[b].size());
@@ -370,11 +373,15 @@ const int* k2_slot_table(int nb, int nk, long long total, int P, int maxseg) {
         Ctx::get().const_table(name, host.data(), host.size() * sizeof(int)));
 }
 
-void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, long long total,
-                      int P, int n, int mode, const double* row_mean, const double* scalars,
-                      const double* colsums, double* y, cudaStream_t st, const int* skip) {
+const int* k2_slot_table(int nb, int nk, long long total, int P, int maxseg) {
+    return k2_slot_table_multi(nb, {K2Split{nk, total, P, maxseg, 0}});
+}
+
+void launch_k2_reduce_multi(int wp, int bm, const double* part, const std::vector<K2Split>& splits,
+                            int n, int mode, const double* row_mean, const double* scalars,
+                            const double* colsums, double* y, cudaStream_t st, const int* skip) {
     const int nb = (n + bm - 1) / bm;
-    const int* tab = k2_slot_table(nb, nk, total, P, maxseg);
+    const int* tab = k2_slot_table_multi(nb, splits);
     switch (wp * 1000 + bm) {
 #define DSB_RED(W, B)                                                                          \
     case W * 1000 + B:                                                                         \
@@ -388,6 +395,13 @@ void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, lo
         default:
             throw std::invalid_argument("unsupported reduce shape");
     }
+}
+
+void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, long long total,
+                      int P, int n, int mode, const double* row_mean, const double* scalars,
+                      const double* colsums, double* y, cudaStream_t st, const int* skip) {
+    launch_k2_reduce_multi(wp, bm, part, {K2Split{nk, total, P, maxseg, 0}}, n, mode, row_mean,
+                           scalars, colsums, y, st, skip);
 }
 
 int k2_warps(int wp) { return wp <= 64 ? 16 : 8; }

@@ -288,7 +288,10 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
                    const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
                    int nks, int total, double* __restrict__ part, int maxseg, int wp, int cg0,
-                   const int* __restrict__ skip, int dbg, double hlen, size_t bdig_stride) {
+                   const int* __restrict__ skip, int dbg, double hlen, size_t bdig_stride,
+                   int k_off) {
+    // k_off: first global k-step of this launch (a column range of D and the
+    // matching panel rows; the walk's k-steps are local to the range)
     if (skip && *skip) return;
     static_assert(CL == 1 || CL == 2, "one CTA, or a pair sharing the D tiles");
     const int crank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
@@ -385,16 +388,16 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     // (64 rows x 128 B keeps the SWIZZLE_128B phase)
                     const int r0 = w.rb * kRowsI8 + 64 * crank;
                     unsigned char* hd = dst + crank * (64 * 128);
-                    tma_load_2d_mc(hd, &tmD, w.ks * kKStep, r0, &full_d[sd], 0x3);
+                    tma_load_2d_mc(hd, &tmD, (k_off + w.ks) * kKStep, r0, &full_d[sd], 0x3);
                     if constexpr (sizeof(TD) == 8)
-                        tma_load_2d_mc(hd + kRowsI8 * 128, &tmD, w.ks * kKStep + 16, r0,
+                        tma_load_2d_mc(hd + kRowsI8 * 128, &tmD, (k_off + w.ks) * kKStep + 16, r0,
                                        &full_d[sd], 0x3);
                 } else if constexpr (sizeof(TD) == 8) {
-                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[sd]);
-                    tma_load_2d(dst + kRowsI8 * 128, &tmD, w.ks * kKStep + 16, w.rb * kRowsI8,
-                                &full_d[sd]);
+                    tma_load_2d(dst, &tmD, (k_off + w.ks) * kKStep, w.rb * kRowsI8, &full_d[sd]);
+                    tma_load_2d(dst + kRowsI8 * 128, &tmD, (k_off + w.ks) * kKStep + 16,
+                                w.rb * kRowsI8, &full_d[sd]);
                 } else {
-                    tma_load_2d(dst, &tmD, w.ks * kKStep, w.rb * kRowsI8, &full_d[sd]);
+                    tma_load_2d(dst, &tmD, (k_off + w.ks) * kKStep, w.rb * kRowsI8, &full_d[sd]);
                 }
                 if (++sd == ND) {
                     sd = 0;
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 if constexpr (kBProd) {
                     if (k >= NBR) mbar_wait(&empty_b[sb], pb ^ 1);
                     mbar_arrive_expect_tx(&full_b[sb], BB);
-                    bulk_load(bring + sb * BB, bdig + static_cast<size_t>(w.ks) * BB, BB,
+                    bulk_load(bring + sb * BB, bdig + static_cast<size_t>(k_off + w.ks) * BB, BB,
                               &full_b[sb]);
                     if (++sb == NBR) {
                         sb = 0;
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 }
                 if (!kBProd && warp == 2 && lane == 0) {
                     mbar_arrive_expect_tx(&full_a[sa], BB);
-                    bulk_load(bring + sa * BB, bdig + static_cast<size_t>(w.ks) * BB, BB,
+                    bulk_load(bring + sa * BB, bdig + static_cast<size_t>(k_off + w.ks) * BB, BB,
                               &full_a[sa]);
                 }
                 if (dbg != 1) {
@@ -681,16 +684,18 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 // ---- B digits of the panel (per pass) --------------------------------------
 // one thread per (k-step, column, 4 rows): balanced base-256 digits of
 // round(X 2^(56 - f_c)), written as 7 byte planes in the UMMA layout
-__global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__ x, int nks, int wp,
-                                                      int nb, int cg0, const int* __restrict__ col_exp,
+__global__ void __launch_bounds__(256) k_panel_digits(const double* __restrict__ x, int ks0, int nks,
+                                                      int wp, int nb, int cg0,
+                                                      const int* __restrict__ col_exp,
                                                       unsigned char* __restrict__ bdig) {
+    // k-steps ks0 .. ks0 + nks - 1
     const long long total = static_cast<long long>(nks) * nb * 8;
     const int bb = kDig * nb * kKStep;
     for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int kq = static_cast<int>(e & 7);
         const int c = static_cast<int>((e >> 3) % nb);
-        const long long ks = (e >> 3) / nb;
+        const long long ks = ks0 + (e >> 3) / nb;
         uint32_t word[kDig];
 #pragma unroll
         for (int u = 0; u < kDig; ++u) word[u] = 0;
@@ -746,13 +751,13 @@ int k2i_debug_mode() {
 template <int NB, typename TD, int SD = kDig, int CL = 1>
 void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
             size_t bdig_stride, const int* row_exp, const int* col_exp, double* part, int cg0,
-            cudaStream_t st, const int* skip, double hlen = 0.0) {
+            cudaStream_t st, const int* skip, double hlen = 0.0, int k_off = 0) {
     const void* fn = reinterpret_cast<const void*>(k2i_product_ts<NB, TD, SD, CL>);
     ensure_dyn_smem(fn, ts_smem<NB, TD, SD, CL>());
     if constexpr (CL == 1) {
         k2i_product_ts<NB, TD, SD, 1><<<p.grid, kThreadsI8, ts_smem<NB, TD, SD>(), st>>>(
             *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
-            p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen, bdig_stride);
+            p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen, bdig_stride, k_off);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(p.grid * CL));
@@ -769,7 +774,7 @@ void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned ch
         DSB_CUDA(cudaLaunchKernelEx(&cfg, k2i_product_ts<NB, TD, SD, CL>, *tmap, bdig, row_exp,
                                     col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
                                     p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen,
-                                    bdig_stride));
+                                    bdig_stride, k_off));
     }
 }
 
@@ -880,7 +885,7 @@ void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
     auto digits = [&](int nb, int cg0, unsigned char* dst) {
         const long long items = static_cast<long long>(p.nks) * nb * 8;
         const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
-        k_panel_digits<<<grid, 256, 0, st>>>(x, p.nks, wp, nb, cg0, col_exp, dst);
+        k_panel_digits<<<grid, 256, 0, st>>>(x, 0, p.nks, wp, nb, cg0, col_exp, dst);
     };
     const double hl = static_cast<double>(hamming_len);
     const bool ham = dt == DType::F64 && hamming_len > 0;
@@ -937,6 +942,119 @@ void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
     if (e1) record_timing_event(e1, st);
     launch_k2_reduce(wp, kRowsI8, part, p.maxseg, p.nks, p.total, p.grid, p.nrows, 1, row_mean,
                      scalars, colsums, y, st, skip);
+    count_launch(1);
+}
+
+size_t k2i_ranges_part_elems(const K2iPlan& full, int wp,
+                             const std::vector<std::pair<int, int>>& ranges, int sms) {
+    size_t slots = 0;
+    for (const auto& r : ranges) {
+        const K2iPlan pr = k2i_plan(full.nrows, static_cast<size_t>(r.second - r.first) * kKStep,
+                                    wp, sms);
+        slots += static_cast<size_t>(pr.grid) * pr.maxseg;
+    }
+    return slots * kRowsI8 * wp;
+}
+
+void launch_k2i_ranges(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
+                       const K2iPlan& full, int wp, const double* x, const int* row_exp,
+                       const int* col_exp, unsigned char* bdig, double* part,
+                       const double* row_mean, const double* scalars, const double* colsums,
+                       double* y, size_t y_rows_pad, cudaStream_t st, cudaEvent_t gathered,
+                       const std::vector<std::pair<int, int>>& ranges, int sms, cudaEvent_t e0,
+                       cudaEvent_t e1, int hamming_len) {
+    const size_t r_done = static_cast<size_t>(full.nblk) * kRowsI8;
+    if (y_rows_pad > r_done)
+        DSB_CUDA(cudaMemsetAsync(y + r_done * wp, 0, (y_rows_pad - r_done) * wp * sizeof(double),
+                                 st));
+    const double hl = static_cast<double>(hamming_len);
+    const bool ham = dt == DType::F64 && hamming_len > 0;
+    std::vector<K2iPlan> plans;
+    std::vector<K2Split> splits;
+    long long slot = 0;
+    for (const auto& r : ranges) {
+        plans.push_back(k2i_plan(full.nrows, static_cast<size_t>(r.second - r.first) * kKStep, wp,
+                                 sms));
+        const K2iPlan& pr = plans.back();
+        splits.push_back(K2Split{pr.nks, pr.total, pr.grid, pr.maxseg, slot});
+        slot += static_cast<long long>(pr.grid) * pr.maxseg;
+    }
+    auto digits = [&](int ri, int nb, int cg0, unsigned char* dst) {
+        const int k0 = ranges[ri].first, nk = ranges[ri].second - ranges[ri].first;
+        const long long items = static_cast<long long>(nk) * nb * 8;
+        const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
+        k_panel_digits<<<grid, 256, 0, st>>>(x, k0, nk, wp, nb, cg0, col_exp, dst);
+        count_launch();
+    };
+    auto run = [&](int ri, int g, unsigned char* bd, size_t bs) {
+        const K2iPlan& pr = plans[ri];
+        double* pp = part + static_cast<size_t>(splits[ri].slot_base) * kRowsI8 * wp;
+        const int k0 = ranges[ri].first;
+        if (full.pair) {
+            if (ham)
+                run_i8<48, double, 3, 2>(tmap64, pr, wp, bd, bs, row_exp, col_exp, pp, 0, st,
+                                         nullptr, hl, k0);
+            else if (dt == DType::F64)
+                run_i8<48, double, kDig, 2>(tmap64, pr, wp, bd, bs, row_exp, col_exp, pp, 0, st,
+                                            nullptr, 0.0, k0);
+            else
+                run_i8<48, float, kDig, 2>(tmap64, pr, wp, bd, bs, row_exp, col_exp, pp, 0, st,
+                                           nullptr, 0.0, k0);
+        } else {
+            const int nb = full.gnb[g], cg0 = full.gc0[g];
+            if (ham) {
+                if (nb == 32)
+                    run_i8<32, double, 3>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
+                                          nullptr, hl, k0);
+                else
+                    run_i8<64, double, 3>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
+                                          nullptr, hl, k0);
+            } else if (dt == DType::F64) {
+                if (nb == 32)
+                    run_i8<32, double>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
+                                       nullptr, 0.0, k0);
+                else
+                    run_i8<64, double>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
+                                       nullptr, 0.0, k0);
+            } else {
+                if (nb == 32)
+                    run_i8<32, float>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
+                                      nullptr, 0.0, k0);
+                else
+                    run_i8<64, float>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
+                                      nullptr, 0.0, k0);
+            }
+        }
+        count_launch();
+    };
+    bool waited = gathered == nullptr;
+    auto wait_gathered = [&] {
+        if (!waited) DSB_CUDA(cudaStreamWaitEvent(st, gathered, 0));
+        waited = true;
+    };
+    if (e0) record_timing_event(e0, st);
+    if (full.pair) {
+        // one launch per range; the pair's two 48-column groups' digits sit
+        // bdig_stride apart (the full plan's layout: global k-steps)
+        for (size_t ri = 0; ri < ranges.size(); ++ri) {
+            if (ri > 0) wait_gathered();
+            digits(static_cast<int>(ri), full.gnb[0], full.gc0[0], bdig);
+            digits(static_cast<int>(ri), full.gnb[1], full.gc0[1], bdig + full.bdig_stride);
+            run(static_cast<int>(ri), 0, bdig, full.bdig_stride);
+        }
+    } else {
+        // column groups share one digit buffer: group-major, every range of a
+        // group before the next group's digits
+        for (int g = 0; g < full.ngroups; ++g)
+            for (size_t ri = 0; ri < ranges.size(); ++ri) {
+                if (ri > 0) wait_gathered();
+                digits(static_cast<int>(ri), full.gnb[g], full.gc0[g], bdig);
+                run(static_cast<int>(ri), g, bdig, 0);
+            }
+    }
+    if (e1) record_timing_event(e1, st);
+    launch_k2_reduce_multi(wp, kRowsI8, part, splits, full.nrows, 1, row_mean, scalars, colsums,
+                           y, st, nullptr);
     count_launch(1);
 }
 

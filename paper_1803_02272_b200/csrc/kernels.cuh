@@ -7,6 +7,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <utility>
+#include <vector>
 
 namespace dsb {
 
@@ -93,6 +95,19 @@ void launch_k2(const CUtensorMap* tmap, DType dt, int mode, const K2Plan& p, con
 // slot table of a stream-K split (k2_reduce), uploaded once per split and
 // kept in the workspace arena; call before a graph capture
 const int* k2_slot_table(int nb, int nk, long long total, int P, int maxseg);
+// one stream-K split of a product launch: nk k-steps per row block, `total`
+// items over P work units, its partial slots start at slot `slot_base`
+struct K2Split {
+    int nk;
+    long long total;
+    int P, maxseg;
+    long long slot_base;
+};
+const int* k2_slot_table_multi(int nb, const std::vector<K2Split>& splits);
+// one reduce over several splits' partial slots (summed split by split)
+void launch_k2_reduce_multi(int wp, int bm, const double* part, const std::vector<K2Split>& splits,
+                            int n, int mode, const double* row_mean, const double* scalars,
+                            const double* colsums, double* y, cudaStream_t st, const int* skip);
 void launch_k2_reduce(int wp, int bm, const double* part, int maxseg, int nk, long long total,
                       int P, int n, int mode, const double* row_mean, const double* scalars,
                       const double* colsums, double* y, cudaStream_t st, const int* skip);
@@ -116,6 +131,18 @@ struct K2iPlan {
 };
 bool k2i_supported(int wp);
 K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms);
+// the sharded product over k-step ranges of D's columns (panel all-gather
+// overlapped: ranges[0] needs only the local panel rows, the rest wait on
+// `gathered`), one stream-K split and slot set per range, one reduce
+size_t k2i_ranges_part_elems(const K2iPlan& full, int wp,
+                             const std::vector<std::pair<int, int>>& ranges, int sms);
+void launch_k2i_ranges(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
+                       const K2iPlan& full, int wp, const double* x, const int* row_exp,
+                       const int* col_exp, unsigned char* bdig, double* part,
+                       const double* row_mean, const double* scalars, const double* colsums,
+                       double* y, size_t y_rows_pad, cudaStream_t st, cudaEvent_t gathered,
+                       const std::vector<std::pair<int, int>>& ranges, int sms, cudaEvent_t e0,
+                       cudaEvent_t e1, int hamming_len);
 // pmax: colmax_grid * wp doubles; col_exp: nb ints (<= 128); bdig: bdig_bytes
 // tmap64: 64-row boxes of the same D (the pair kernel's multicast halves)
 void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt, const K2iPlan& p,
@@ -164,6 +191,11 @@ void launch_panel_to_rowmajor(const double* src, size_t n, int w, int wp, double
 void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_pad, int wp,
                     double* partial, double* colsums, int sms, cudaStream_t st,
                     double* pmax = nullptr, int nb = 0, int* col_exp = nullptr);
+// per-column max |x| from launch_colsums' pmax partials (P of them), and the
+// int8 column exponents from such maxima (sharded product: local maxima are
+// reduced over the ranks in between)
+void launch_colmax(const double* pmax, int P, int wp, double* cmax, cudaStream_t st);
+void launch_colexp(const double* cmax, int wp, int nb, int* col_exp, cudaStream_t st);
 // out (wp x wp) = A^T B (deterministic 2-level). gate (nullable): skip the
 // kernels unless gate[0] & 1 (the shift flag: a third CholeskyQR pass is only
 // needed after a shifted first pass)

@@ -461,6 +461,26 @@ void launch_colsums(const double* x, const double* row_mean, size_t n, size_t n_
     }
 }
 
+// column maxima of the colsum partials' pmax (P x wp) -> cmax (wp)
+__global__ void __launch_bounds__(256) k_colmax_final(const double* __restrict__ pmax, int P,
+                                                      int wp, double* __restrict__ cmax) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < wp; c += gridDim.x * blockDim.x) {
+        double m = 0.0;
+        for (int b = 0; b < P; ++b) m = fmax(m, pmax[static_cast<size_t>(b) * wp + c]);
+        cmax[c] = m;
+    }
+}
+
+void launch_colmax(const double* pmax, int P, int wp, double* cmax, cudaStream_t st) {
+    k_colmax_final<<<1, 256, 0, st>>>(pmax, P, wp, cmax);
+    count_launch();
+}
+
+void launch_colexp(const double* cmax, int wp, int nb, int* col_exp, cudaStream_t st) {
+    k_colexp_final<<<1, 1024, 0, st>>>(cmax, 1, wp, nb, col_exp);
+    count_launch();
+}
+
 void launch_panel_dot(const double* a, const double* b, size_t n_pad, int wp, double* partial,
                       double* out, int sms, cudaStream_t st, const int* gate) {
     const int P = panel_grid(n_pad, sms);

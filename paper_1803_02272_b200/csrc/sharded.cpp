@@ -327,12 +327,34 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     double* pmax = nullptr;
     int* col_exp = nullptr;
     unsigned char* bdig = nullptr;
+    // the panel all-gather overlapped with the product over this rank's own
+    // columns (DSB_SHARD_OVERLAP=0: gather, then product). The choice is the
+    // same on every rank (the collective sequence must match); ranks without
+    // the int8 product still run the same collectives
+    static const bool overlap_env = [] {
+        const char* e = std::getenv("DSB_SHARD_OVERLAP");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const bool overlap = L.world > 1 && overlap_env;
     if (use_i8) {
         iplan = k2i_plan(m, n, wp, c.sms);
-        pmax = static_cast<double*>(c.scratch(
-            "i8_pmax", static_cast<size_t>(panel_grid(n_pad, c.sms)) * wp * sizeof(double)));
         col_exp = static_cast<int*>(c.scratch("i8_colexp", 128 * sizeof(int)));
         bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
+    }
+    if (use_i8 || overlap)
+        pmax = static_cast<double*>(c.scratch(
+            "i8_pmax", static_cast<size_t>(panel_grid(n_pad, c.sms)) * wp * sizeof(double)));
+    double* cmax = overlap ? static_cast<double*>(c.scratch("shard_cmax", wp * sizeof(double)))
+                           : nullptr;
+    // k-step ranges of this rank's product: its own panel rows' columns first
+    std::vector<std::pair<int, int>> ranges;
+    if (use_i8 && overlap) {
+        const int nks = (static_cast<int>(n) + 31) / 32;
+        const int k_lo = static_cast<int>(std::min(n, L.rank * m_pad) / 32);
+        const int k_hi = static_cast<int>((std::min(n, (L.rank + 1) * m_pad) + 31) / 32);
+        if (k_hi > k_lo) ranges.emplace_back(k_lo, k_hi);
+        if (k_lo > 0) ranges.emplace_back(0, k_lo);
+        if (nks > k_hi) ranges.emplace_back(k_hi, nks);
     }
     c.last_product_kernel = use_i8 ? 1 : 0;
     // Hamming shards (divscope_matrix_hamming_rows): three exact S bytes
@@ -347,8 +369,10 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));
     double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));
     double* P2 = static_cast<double*>(c.scratch("panel2", pbytes));
-    double* part = static_cast<double*>(c.scratch(
-        "k2_part", std::max(plan.part_elems, use_i8 ? iplan.part_elems : 0) * 8 + 64));
+    const size_t part_elems =
+        std::max({plan.part_elems, use_i8 ? iplan.part_elems : size_t(0),
+                  ranges.empty() ? size_t(0) : k2i_ranges_part_elems(iplan, wp, ranges, c.sms)});
+    double* part = static_cast<double*>(c.scratch("k2_part", part_elems * 8 + 64));
     const int pg = panel_grid(std::max<size_t>(m_pad, 4), c.sms);
     const int pgf = panel_grid(n_pad, c.sms);
     double* psmall = static_cast<double*>(c.scratch(
@@ -366,7 +390,42 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         launch_panel_from_rowmajor(stage, n, wi, wp, n_pad, P0, c.stream);
     }
     const size_t lo = static_cast<size_t>(L.rank) * m_pad * wp;  // this rank's panel chunk
-    auto product = [&](const double* x_full, double* y_full) {
+    // gather: the panel's other chunks must first be all-gathered (every
+    // product after a CholeskyQR; the first one multiplies the replicated Omega)
+    auto product = [&](double* x_full, double* y_full, bool gather) {
+        cudaEvent_t e0, e1;
+        if (gather && overlap) {
+            // s = 1^T X, t = r^T X and the column maxima of this rank's rows,
+            // reduced over the ranks; then the all-gather on the side stream
+            // while the product runs over the locally-owned columns
+            launch_colsums(x_full + lo, r_full + rb, m, m_pad, wp, psmall, colsums, c.sms,
+                           c.stream, pmax, 0, nullptr);
+            launch_colmax(pmax, panel_grid(m_pad, c.sms), wp, cmax, c.stream);
+            cm.allreduce_sum(colsums, static_cast<size_t>(2) * wp, c.stream);
+            cm.allreduce_max(cmax, static_cast<size_t>(wp), c.stream);
+            if (use_i8) launch_colexp(cmax, wp, iplan.nb, col_exp, c.stream);
+            DSB_CUDA(cudaEventRecord(c.side_ready, c.stream));
+            DSB_CUDA(cudaStreamWaitEvent(c.side, c.side_ready, 0));
+            cm.allgather(x_full, m_pad * wp, c.side);
+            DSB_CUDA(cudaEventRecord(c.side_done, c.side));
+            c.make_events(&e0, &e1);
+            if (use_i8) {
+                launch_k2i_ranges(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x_full,
+                                  g.gram->row_exp->as<int>(), col_exp, bdig, part, r_full + rb,
+                                  scal, colsums, y_full + lo, m_pad, c.stream, c.side_done, ranges,
+                                  c.sms, e0, e1, hamming_i8);
+            } else {
+                DSB_CUDA(cudaStreamWaitEvent(c.stream, c.side_done, 0));
+                if (m)
+                    launch_k2(s.tmap_for(plan.bm), s.dt, 1, plan, x_full, part, r_full + rb, scal,
+                              colsums, y_full + lo, m_pad, c.stream, e0, e1);
+            }
+            // every later collective (and panel write) comes after the gather
+            DSB_CUDA(cudaStreamWaitEvent(c.stream, c.side_done, 0));
+            c.add_timed(1, e0, e1);
+            return;
+        }
+        if (gather) cm.allgather(x_full, m_pad * wp, c.stream);
         // s = 1^T X, t = r^T X over the full replicated panel (+ the int8
         // column exponents: identical on every rank)
         if (use_i8)
@@ -374,7 +433,6 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
                            iplan.nb, col_exp);
         else
             launch_colsums(x_full, r_full, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
-        cudaEvent_t e0, e1;
         c.make_events(&e0, &e1);
         if (use_i8)
             launch_k2i(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x_full, n_pad,
@@ -410,17 +468,17 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
                 launch_panel_apply(bufs[ps][0], rinv, m_pad, wp, bufs[ps][1], c.stream, gate);
             }
         }
-        cm.allgather(out_full, m_pad * wp, c.stream);
+        (void)out_full;  // its other chunks are all-gathered by the next product
     };
-    product(P0, P1);
+    product(P0, P1, false);
     orth_local(P1, P2, P0);
     for (size_t it = 0; it < q; ++it) {
-        product(P0, P1);
+        product(P0, P1, true);
         orth_local(P1, P2, P0);
-        product(P0, P1);
+        product(P0, P1, true);
         orth_local(P1, P2, P0);
     }
-    product(P0, P1);
+    product(P0, P1, true);
     launch_panel_dot(P0 + lo, P1 + lo, m_pad, wp, psmall, wmat, c.sms, c.stream);
     cm.allreduce_sum(wmat, static_cast<size_t>(wp) * wp, c.stream);
     const size_t req = embed_mode ? requested : std::min(rank, w);

@@ -6,7 +6,8 @@ invariance (ref tests/test_rsvd.cpp:81-101): every rank's solve must match
 the oracle and the one-process result.
 
 Covered on real ranks: unequal shards (the last rank's padded panel chunk),
-a rank with no rows at all, the panel all-gather, the per-rank lift
+a rank with no rows at all, the panel all-gather (overlapped with the
+product over each rank's own columns, and gather-first), the per-rank lift
 partials and the coordinate all-gather, the ring-shift block exchange of
 the symmetry check, both product kernels (fp64 DMMA and the int8 slice
 product, two column groups), Hamming row shards, and errors: one rank
@@ -28,9 +29,9 @@ pytestmark = pytest.mark.gpu
 HERE = Path(__file__).resolve().parent
 
 
-def run_ranks(world, case, tmp_path, timeout=300):
+def run_ranks(world, case, tmp_path, timeout=300, extra_env=None):
     uid = str(tmp_path / "uid.bin")
-    env = dict(os.environ, DSB_COMM_TRANSPORT="host")
+    env = dict(os.environ, DSB_COMM_TRANSPORT="host", **(extra_env or {}))
     procs, outs = [], []
     for r in range(world):
         out = str(tmp_path / f"rank{r}.npz")
@@ -114,6 +115,23 @@ def test_ranks_match_oracle_and_one_process(ds, oracle, tmp_path, world, product
     # eigs on the same sharded gram
     for o in res:
         assert rel_err(o["eig_vals"], res[0]["eigenvalues"][: len(o["eig_vals"])]) < 1e-12
+
+
+@pytest.mark.parametrize("product", [0, 2], ids=["auto", "int8"])
+def test_overlapped_gather_matches_gather_first(ds, oracle, tmp_path, product):
+    # the panel all-gather overlapped with the product over each rank's own
+    # columns (k-step ranges, one slot set each, colsums reduced from the
+    # ranks' rows) against gather-then-product (DSB_SHARD_OVERLAP=0)
+    case = dict(BASE, product=product)
+    (tmp_path / "on").mkdir()
+    (tmp_path / "off").mkdir()
+    on = run_ranks(3, case, tmp_path / "on")
+    off = run_ranks(3, case, tmp_path / "off", extra_env={"DSB_SHARD_OVERLAP": "0"})
+    lam1 = on[0]["eigenvalues"][0]
+    for a, b in zip(on, off):
+        assert rel_err(a["eigenvalues"], b["eigenvalues"]) < 1e-12
+        assert coords_match_up_to_sign(a["coords"], b["coords"]) < 1e-10 * np.sqrt(lam1)
+    check_against(ds, oracle, case, on)
 
 
 def test_rank_without_rows(ds, oracle, tmp_path):
