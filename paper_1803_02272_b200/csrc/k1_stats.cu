@@ -219,10 +219,14 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
             if constexpr (sizeof(T) == 4) {
                 // max |d| in the float domain (widening is monotonic, so the
                 // widened max is the max of the widened values); the row
-                // exponent follows from the row max: max d^2 = (max |d|)^2
+                // exponent follows from the row max: max d^2 = (max |d|)^2.
+                // fmaxf (one FMNMX) never returns a NaN operand over a
+                // non-NaN one, as (x > m ? x : m) in the reference's scans;
+                // off the diagonal every entry is upper: the segment max
+                // covers it below
                 const float af = fabsf(av[j]);
-                rmaxf = af > rmaxf ? af : rmaxf;
-                if (upper) maxup_f = af > maxup_f ? af : maxup_f;
+                rmaxf = fmaxf(rmaxf, af);
+                if (I == J && upper) maxup_f = fmaxf(maxup_f, af);
             } else {
                 rmx = max(rmx, hi_bits(sq));
                 if (upper) maxabs_up = max_keep(maxabs_up, fabs(a[j]));
@@ -241,7 +245,8 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
         if constexpr (sizeof(T) == 4) {
             const double m = static_cast<double>(rmaxf);
             rmx = hi_bits(m * m);
-            if (I == J) maxf = rmaxf > maxf ? rmaxf : maxf;
+            if (I == J) maxf = fmaxf(maxf, rmaxf);
+            else maxup_f = fmaxf(maxup_f, rmaxf);
         } else if (I == J) {  // diagonal tile: maxabs_up saw only its upper part
 #pragma unroll
             for (int j = 0; j < C::EL; ++j) maxabs = max_keep(maxabs, fabs(a[j]));
@@ -282,8 +287,7 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
                 rbp[j % NCH] += sq;
                 b4p[j % NCH] += sq * sq;
                 if constexpr (sizeof(T) == 4) {
-                    const float bf = fabsf(bt);
-                    bmaxf = bf > bmaxf ? bf : bmaxf;
+                    bmaxf = fmaxf(bmaxf, fabsf(bt));
                 } else {
                     bmx = max(bmx, hi_bits(sq));
                     maxabs = max_keep(maxabs, fabs(b));
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
             if constexpr (sizeof(T) == 4) {
                 const double m = static_cast<double>(bmaxf);
                 bmx = hi_bits(m * m);
-                maxf = bmaxf > maxf ? bmaxf : maxf;
+                maxf = fmaxf(maxf, bmaxf);
             }
             double rb = (rbp[0] + rbp[1]) + (rbp[2] + rbp[3]);
             sum4 += (b4p[0] + b4p[1]) + (b4p[2] + b4p[3]);
