@@ -22,6 +22,9 @@ namespace dsb {
 namespace {
 
 constexpr int kT = 64;          // tile edge
+#ifndef DSB_K1_NCH32
+#define DSB_K1_NCH32 2  // f32 tiles: independent accumulation chains per lane (2: 0.7 % over 4)
+#endif
 
 template <typename T>
 struct Pair2;
@@ -202,9 +205,9 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
         }
 #pragma unroll
         for (int j = 0; j < C::EL; ++j) a[j] = static_cast<double>(av[j]);
-        // f32 tiles: four independent accumulation chains (a 16-long dependent
+        // f32 tiles: DSB_K1_NCH32 independent accumulation chains (a 16-long dependent
         // DADD chain left the FP64 latency exposed); f64 tiles: one (faster there)
-        constexpr int NCH = sizeof(T) == 4 ? 4 : 1;
+        constexpr int NCH = sizeof(T) == 4 ? DSB_K1_NCH32 : 1;
         double rsp[4] = {0.0, 0.0, 0.0, 0.0}, s4p[4] = {0.0, 0.0, 0.0, 0.0};
         uint32_t rmx = 0u;
         float rmaxf = 0.0f;  // f32 tiles: max |d| of the row segment
