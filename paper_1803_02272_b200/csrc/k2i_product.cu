@@ -121,10 +121,11 @@ constexpr int kBStagesTs = 4;
 #endif
 constexpr bool kWarpIssue = DSB_K2I_WARP_ISSUE != 0;
 // panel digits get their own producer-filled ring when the A ring is this
-// shallow or shallower (a single A stage); riding on the 2-deep NB = 64 A
-// ring measured as fast as a separate ring (DSB_TS_BPROD_NA=2)
+// shallow or shallower: the 2-deep NB = 64 A ring too (w = 120 on f32 D,
+// n = 60k: 13.3 -> 12.7 ms per pass; NB = 64 f64 and the Hamming slices
+// unchanged)
 #ifndef DSB_TS_BPROD_NA
-#define DSB_TS_BPROD_NA 1
+#define DSB_TS_BPROD_NA 2
 #endif
 template <int NB, int SD = kDig>
 constexpr bool bprod_ts();
