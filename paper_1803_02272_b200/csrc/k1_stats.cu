@@ -211,6 +211,8 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
         double rsp[4] = {0.0, 0.0, 0.0, 0.0}, s4p[4] = {0.0, 0.0, 0.0, 0.0};
         uint32_t rmx = 0u;
         float rmaxf = 0.0f;  // f32 tiles: max |d| of the row segment
+        T mtv[C::EL];        // f32 tiles: the mirror entries B[c][r] of the segment
+        uint32_t diff = 0u;  // f32 tiles: OR of the pairs' bit differences
 #pragma unroll
         for (int j = 0; j < C::EL; ++j) {
             const double sq = a[j] * a[j];
@@ -235,14 +237,23 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
                 if (upper) maxabs_up = max_keep(maxabs_up, fabs(a[j]));
             }
             // symmetry: A[r][c] vs B[c][r] (d_ij vs d_ji)
-            const T mt = *tile_at<T>(B, col0 + j, r);
             if constexpr (sizeof(T) == 4) {
-                // identical bits (the symmetric case) give 0; only differing
-                // entries pay for the f64 difference the reference takes
-                if (__float_as_uint(mt) != __float_as_uint(av[j]))
-                    maxasym = max_keep(maxasym, fabs(a[j] - static_cast<double>(mt)));
+                // identical bits (the symmetric case) give 0: only the bit
+                // difference is accumulated here; a segment with any
+                // differing pair takes the f64 differences below
+                mtv[j] = *tile_at<T>(B, col0 + j, r);
+                diff |= __float_as_uint(mtv[j]) ^ __float_as_uint(av[j]);
             } else {
+                const T mt = *tile_at<T>(B, col0 + j, r);
                 maxasym = max_keep(maxasym, fabs(a[j] - mt));
+            }
+        }
+        if constexpr (sizeof(T) == 4) {
+            if (diff != 0u) {  // rare: the reference's f64 difference per pair
+#pragma unroll
+                for (int j = 0; j < C::EL; ++j)
+                    if (__float_as_uint(mtv[j]) != __float_as_uint(av[j]))
+                        maxasym = max_keep(maxasym, fabs(a[j] - static_cast<double>(mtv[j])));
             }
         }
         if constexpr (sizeof(T) == 4) {
