@@ -11,6 +11,7 @@ python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
 python bench.py --workload C1 > $O/bench_c1.json 2> $O/bench_c1.err
 python bench.py --workload C5 --steps 5 > $O/bench_c5.json 2> $O/bench_c5.err
 python bench.py --workload C3 --steps 3 --no-e2e > $O/bench_c3.json 2> $O/bench_c3.err
+python bench.py --workload C4 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/bench_c4.json 2> $O/bench_c4.err
 python bench.py --impl reference --steps 3 --warmup 3 > $O/reference_arm.json 2> $O/reference_arm.err
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/plain_launch.json 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
