@@ -973,9 +973,14 @@ void launch_k2i_ranges(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DT
     std::vector<K2iPlan> plans;
     std::vector<K2Split> splits;
     long long slot = 0;
-    for (const auto& r : ranges) {
+    for (size_t ri = 0; ri < ranges.size(); ++ri) {
+        const auto& r = ranges[ri];
+        // the range that runs next to the all-gather leaves a few SMs free:
+        // the persistent product otherwise fills every SM and the collective's
+        // kernel could only start after it
+        const int sms_r = (ri == 0 && gathered) ? std::max(sms - 8, sms / 2) : sms;
         plans.push_back(k2i_plan(full.nrows, static_cast<size_t>(r.second - r.first) * kKStep, wp,
-                                 sms));
+                                 sms_r));
         const K2iPlan& pr = plans.back();
         splits.push_back(K2Split{pr.nks, pr.total, pr.grid, pr.maxseg, slot});
         slot += static_cast<long long>(pr.grid) * pr.maxseg;
