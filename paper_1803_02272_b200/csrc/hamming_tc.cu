@@ -373,7 +373,8 @@ bool launch_hamming_tc(const uint32_t* lo, const uint32_t* hi, size_t count, int
     DevBuf enc(enc_bytes);
     {
         const long long items = static_cast<long long>(nblk) * kTT * nks * 8;
-        const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 148 * 16));
+        const int grid =
+            static_cast<int>(std::min<long long>((items + 255) / 256, Ctx::get().sms * 16LL));
         k_hamming_encode<<<grid, 256, 0, st>>>(lo, hi, static_cast<int>(count), words, length,
                                                nblk, nks, enc.as<int8_t>());
     }

@@ -175,6 +175,12 @@ void Ctx::set_device(int dev) {
 const void* Ctx::const_table(const std::string& name, const void* host, size_t bytes) {
     auto it = tables_.find(name);
     if (it != tables_.end()) return it->second->p;
+    if (tables_.size() >= 256) {
+        // many distinct shapes: start over (graphs may address the tables)
+        DSB_CUDA(cudaStreamSynchronize(stream));
+        clear_graphs();
+        tables_.clear();
+    }
     auto buf = std::make_unique<DevBuf>(std::max<size_t>(bytes, 256));
     DSB_CUDA(cudaMemcpyAsync(buf->p, host, bytes, cudaMemcpyHostToDevice, stream));
     DSB_CUDA(cudaStreamSynchronize(stream));
