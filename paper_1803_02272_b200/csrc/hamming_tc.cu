@@ -21,7 +21,9 @@
 // TMEM accumulators; warps 4..11 turn finished accumulators into D, stage
 // each 32 x 32 chunk in shared memory as rows of the tile and, off the
 // diagonal, transposed as rows of the mirror tile, and store both with TMA
-// tensor stores. The D stream (8 n^2 bytes) bounds the kernel.
+// tensor stores. The D stream (8 n^2 bytes) is the roofline; measured at
+// 0.80 of it at C5 (profiles/r02_k7_hamming.txt), the operand reads through
+// L2 and the shared-memory staging sharing the rest.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
