@@ -141,6 +141,28 @@ def test_gram_tolerance_boundary(ds):
     assert err(ds, ds.gram, ds.matrix_from_host(d)) == ds.Status.ERR_NOT_SYMMETRIC
 
 
+@pytest.mark.parametrize("where", ["diag_tile", "off_tile", "tail_tile", "zero_vs_neg_zero"])
+def test_gram_f32_symmetry_check(ds, oracle, where):
+    # f32 tiles compare the mirrored pairs by their bits (k1_stats.cu) and
+    # take the reference's f64 difference only for a differing pair: one
+    # asymmetric pair anywhere (inside a diagonal 64 x 64 tile, an
+    # off-diagonal one, the ragged last tile) is found; -0.0 against +0.0
+    # differs in bits but not in value, as in the reference
+    n = 200
+    d = oracle.euclidean_matrix(ds.synth_points(1, n, 3)).astype(np.float32)
+    ds.gram(ds.matrix_from_host_f32(d))
+    i, j = {"diag_tile": (5, 40), "off_tile": (150, 20), "tail_tile": (199, 130),
+            "zero_vs_neg_zero": (7, 7)}[where]
+    bad = d.copy()
+    if where == "zero_vs_neg_zero":
+        bad[3, 9] = bad[9, 3] = 0.0
+        bad[3, 9] = -0.0
+        ds.gram(ds.matrix_from_host_f32(bad))  # |0 - (-0)| = 0: symmetric
+        return
+    bad[i, j] = np.nextafter(bad[i, j], np.float32(1e9))
+    assert err(ds, ds.gram, ds.matrix_from_host_f32(bad)) == ds.Status.ERR_NOT_SYMMETRIC
+
+
 # ---------------------------------------------------------------- eigs KATs
 
 def test_eigs_signed_diagonal(ds):
