@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kEvdThreads) k_evd(const double* __restrict__ 
     }
 }
 
-// Small problems (w <= 20): one warp, the matrix in registers. Lane i holds
+// Small problems (w <= 16): one warp, the matrix in registers. Lane i holds
 // row i of A (full storage) and row i of V. The tournament is run on fixed
 // positions — pairs (k, M-1-k) every round — and the data moves instead
 // (circle method: position 0 fixed, position j -> j+1, M-1 -> 1), so every
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(32, 1) k_evd_warp(const double* __restrict__ b
 template <int M>
 void launch_evd_warp_m(int m, const double* b, int wp, int w, int rank, int requested_rank,
                        const double* scalars, int fro_index, const EvdOut& o, cudaStream_t st) {
-    if constexpr (M <= 20) {
+    if constexpr (M <= 16) {
         if (m == M) {
             k_evd_warp<M><<<1, 32, 0, st>>>(b, wp, w, rank, requested_rank, scalars, fro_index, o);
             return;
@@ -629,10 +629,11 @@ void launch_evd(const double* b, int wp, int w, int rank, int requested_rank,
         const char* e = std::getenv("DSB_EVD_WARP");
         return !(e && std::atoi(e) == 0);
     }();
-    // the register kernel wins up to w = 20 (measured: w = 12 63k vs 101k
-    // cycles, w = 20 162k vs 174k); wider, its single warp is latency-bound
-    // (w = 30: 867k vs 337k) and the CTA kernel is used
-    if (warp_evd && w >= 1 && w <= 20) {
+    // the register kernel wins up to w = 16 (measured against the CTA kernel
+    // with its split block / V warps: w = 12 63k vs 97k cycles, w = 16 95k vs
+    // 127k, w = 20 even — 162k vs 159k, one sweep more); wider, its single
+    // warp is latency-bound (w = 30: 867k vs 292k)
+    if (warp_evd && w >= 1 && w <= 16) {
         launch_evd_warp_m<2>(w + (w & 1), b, wp, w, rank, requested_rank, scalars, fro_index, o,
                              st);
         count_launch();
