@@ -21,6 +21,11 @@ so a step makes 2q + 3 streaming passes over D, and
           function of (seed, n, w): the library generates it on the host once
           and keeps the device panel resident, so it is not re-uploaded.
 D is larger than the 126 MB L2 at C2..C5, so every pass streams from HBM.
+With the S-digit cache (default when it fits) the first
+product pass of a solve also stores the exact digit planes of D o D and the
+remaining 2q + 1 passes stream those (7 bytes per element, 3 for Hamming D)
+instead of D; `roofline` then describes that streaming pass and carries the
+storing pass as `store_pass`.
 
 cpu_baseline (N = 1, rank 0) and --impl reference time the reference's own
 CPU implementation of the path — gram_from_distances + embed (ref
@@ -400,6 +405,24 @@ def b200_arm(args, wl):
     k2_ms = st.product_ms / max(st.product_launches, 1)
     m_rows = re_ - rb  # rows of D this rank streams per product pass
     bytes_per_launch = m_rows * n * (4 if f32 else 8) + n * w * 8 + m_rows * w * 8 + m_rows * 8
+    # with the S-digit cache (k2i_product.cu) the solve's first pass reads D
+    # and stores the digit planes of D o D (SD bytes per element of each
+    # 128-row x 32-column item), the other 2q+1 passes — the dominant kernel —
+    # stream those planes instead of D
+    sdig = int(st.last_product_kernel) == 1 and int(st.last_product_sdig) == 1
+    store_pass = None
+    if sdig:
+        nfirst = max(int(st.product_first_launches), 1)
+        first_ms = st.product_first_ms / nfirst
+        k2_ms = (st.product_ms - st.product_first_ms) / max(int(st.product_launches) - nfirst, 1)
+        item_bytes = ((m_rows + 127) // 128) * ((n + 31) // 32) * int(st.last_product_sdigits) * 4096
+        d_bytes = m_rows * n * (4 if f32 else 8)
+        bytes_per_launch = item_bytes + n * w * 8 + m_rows * w * 8 + m_rows * 8
+        store_bytes = d_bytes + item_bytes + n * w * 8 + m_rows * w * 8 + m_rows * 8
+        store_pass = {"launches_per_step": 1, "avg_ms": first_ms,
+                      "bytes_per_launch": store_bytes,
+                      "achieved_gbs": store_bytes / (first_ms * 1e-3) / 1e9,
+                      "what": "reads D, stores the S digit planes (and runs the product)"}
     flops_per_launch = 2.0 * m_rows * n * w
     tflops = flops_per_launch / (k2_ms * 1e-3) / 1e12
     gbs = bytes_per_launch / (k2_ms * 1e-3) / 1e9
@@ -417,6 +440,7 @@ def b200_arm(args, wl):
            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
            else "fallback 6650 GB/s (B200_PROFILING.md)"}
     common = {"k2_avg_ms": k2_ms, "k2_launches": int(st.product_launches),
+              "sdig_cache": sdig, "store_pass": store_pass,
               "flops_per_launch": flops_per_launch, "bytes_per_launch": bytes_per_launch,
               "pass0": {"k1_avg_ms": st.stats_ms / max(st.stats_launches, 1),
                         "achieved_gbs": m_rows * n * (4 if f32 else 8) /
@@ -446,7 +470,8 @@ def b200_arm(args, wl):
                                      "int8_peak_source": "profiles/r02_umma_seq.txt (7 x N=256 kind::i8 MMAs, A in TMEM)"},
                     "kernel": ("k2i_product (3x7-digit int8 slice product of the exact Hamming "
                                "h^2, tcgen05 kind::i8)" if int(st.last_product_sdigits) == 3 else
-                               "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)"),
+                               "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)") +
+                              (", streaming the S-digit cache (passes 2..)" if sdig else ""),
                     "peak_source": hbm["peak_source"],
                     "column_groups": groups,
                     "reads_of_D_per_pass": 1 if int(st.last_product_pair) else groups,

@@ -321,6 +321,13 @@ divscope_status divscope_synth_reads(size_t count, size_t length, size_t ancesto
  * else fp64 DMMA), 1 = fp64 DMMA only, 2 = int8 whenever supported. */
 divscope_status divscope_set_product_path(int mode);
 
+/* NEW. S-digit cache of the int8 product: 0 = off, 1 = auto (default: on
+ * when the device has room for it next to a reserve of max(1 GB, 2 %)),
+ * 2 = on whenever it fits. With it, a solve's first product pass stores the exact digit
+ * bytes of D o D and the later passes read those instead of D. Results are
+ * bit-identical either way. */
+divscope_status divscope_set_sdig_cache(int mode);
+
 /* Select the CUDA device used by this process (default: current device). */
 divscope_status divscope_set_device(int device);
 
@@ -340,6 +347,12 @@ typedef struct divscope_stats {
     int32_t last_product_sdigits; /* int8 path: bytes per S element (7; 3 for Hamming D) */
     int32_t last_product_pair;    /* int8 path: 1 when a CTA pair shared each D tile (64 < WP <= 96:
                                      both column groups in ONE read of D) */
+    int32_t last_product_sdig;    /* int8 path: 1 when the S-digit cache was used (the first pass
+                                     stored each element's SD digit bytes, the later passes read
+                                     those instead of D) */
+    uint64_t product_first_launches; /* the first product pass of each solve (also counted in
+                                        product_launches): the storing pass with the cache on */
+    double product_first_ms;          /* its summed device time, when timing on */
 } divscope_stats;
 
 /* timing on => CUDA events are recorded around K1/K2 on the library stream */

@@ -30,7 +30,7 @@ __all__ = [
     "matrix_from_host", "matrix_from_host_f32", "matrix_read", "matrix_euclidean",
     "matrix_hamming", "matrix_hamming_rows", "hamming_counts", "gram", "eigs", "embed", "stable_rank",
     "randomized_range", "embedding_load", "synth_points", "synth_reads", "solver_options_init",
-    "stats_enable_timing", "stats_reset", "set_product_path", "matrix_read_rows", "reconstruction_error", "Scoring", "Alignment",
+    "stats_enable_timing", "stats_reset", "set_product_path", "set_sdig_cache", "matrix_read_rows", "reconstruction_error", "Scoring", "Alignment",
     "align", "distance", "pairwise_self", "pairwise_cross", "stats_get", "set_device", "LIB_PATH",
     "fp64_tensor_peak_tflops", "stream_ptr", "eigs_vectors", "debug_omega_panel",
     "debug_fill_gaussian",
@@ -82,7 +82,8 @@ class Stats(C.Structure):
                 ("last_evd_sweeps", C.c_int32), ("last_orth_shifted", C.c_int32),
                 ("last_power_iters", C.c_int32), ("last_product_kernel", C.c_int32),
                 ("last_product_groups", C.c_int32), ("last_product_sdigits", C.c_int32),
-                ("last_product_pair", C.c_int32)]
+                ("last_product_pair", C.c_int32), ("last_product_sdig", C.c_int32),
+                ("product_first_launches", C.c_uint64), ("product_first_ms", C.c_double)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -167,6 +168,7 @@ def _load() -> C.CDLL:
         "divscope_matrix_hamming_rows": ([C.c_char_p, _sz, _sz, _sz, _sz, C.POINTER(_vp)], _st),
         "divscope_stats_enable_timing": ([C.c_int], None),
         "divscope_set_product_path": ([C.c_int], C.c_int),
+        "divscope_set_sdig_cache": ([C.c_int], C.c_int),
         "divscope_stats_reset": ([], None),
         "divscope_stats_get": ([C.POINTER(Stats)], None),
         "divscope_stream": ([], _vp),
@@ -634,6 +636,11 @@ def set_device(device: int) -> None:
 def set_product_path(mode: int) -> None:
     """0 auto, 1 fp64 DMMA only, 2 int8 slice product whenever supported."""
     _check(lib.divscope_set_product_path(int(mode)))
+
+
+def set_sdig_cache(mode: int) -> None:
+    """S-digit cache of the int8 product: 0 off, 1 auto, 2 whenever it fits."""
+    _check(lib.divscope_set_sdig_cache(int(mode)))
 
 
 def stats_enable_timing(on: bool = True) -> None:

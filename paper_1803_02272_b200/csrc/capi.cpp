@@ -715,6 +715,12 @@ divscope_status divscope_set_product_path(int mode) {
     return DIVSCOPE_OK;
 }
 
+divscope_status divscope_set_sdig_cache(int mode) {
+    if (mode < 0 || mode > 2) return fail_invalid("mode must be 0, 1 or 2");
+    dsb::set_sdig_policy(mode);
+    return DIVSCOPE_OK;
+}
+
 divscope_status divscope_set_device(int device) {
     return wrap([&] { dsb::Ctx::get().set_device(device); });
 }
@@ -733,8 +739,8 @@ void divscope_stats_reset(void) {
         dsb::Ctx& c = dsb::Ctx::get();
         std::lock_guard<std::recursive_mutex> lk(c.mu);
         c.drain_timing();
-        c.k2_ms = c.k1_ms = 0.0;
-        c.k2_launches = c.k1_launches = 0;
+        c.k2_ms = c.k1_ms = c.k2_first_ms = 0.0;
+        c.k2_launches = c.k1_launches = c.k2_first_launches = 0;
         c.h2d = c.d2h = 0;
         c.launches_base = dsb::kernel_launch_count();
     } catch (...) {
@@ -762,6 +768,9 @@ void divscope_stats_get(divscope_stats* out) {
         out->last_product_groups = c.last_product_groups;
         out->last_product_sdigits = c.last_product_sdigits;
         out->last_product_pair = c.last_product_pair;
+        out->last_product_sdig = c.last_product_sdig;
+        out->product_first_launches = c.k2_first_launches;
+        out->product_first_ms = c.k2_first_ms;
     } catch (...) {
     }
 }

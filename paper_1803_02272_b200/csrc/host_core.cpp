@@ -74,8 +74,15 @@ void cuda_check(cudaError_t e, const char* what) {
 // synchronizing cudaMalloc/cudaFree of gigabytes every time.
 DevBuf::DevBuf(size_t b) : bytes(b) {
     if (b == 0) return;
-    const cudaError_t e = cudaMallocAsync(&p, b, Ctx::get().stream);
+    cudaError_t e = cudaMallocAsync(&p, b, Ctx::get().stream);
     if (e != cudaSuccess) {
+        // the evictable workspace (S-digit cache) yields to data and other
+        // workspace: drop it and try once more
+        cudaGetLastError();
+        if (Ctx::get().evict_scratch()) e = cudaMallocAsync(&p, b, Ctx::get().stream);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
         p = nullptr;
         throw Error(errc::internal, "device out of memory allocating " + std::to_string(b) +
                                         " bytes: " + cudaGetErrorString(e));
@@ -212,6 +219,53 @@ void* Ctx::scratch(const std::string& slot, size_t bytes) {
     return b->p;
 }
 
+namespace {
+bool evictable_slot(const std::string& slot) { return slot == "i8_sdig"; }
+}  // namespace
+
+void* Ctx::try_scratch(const std::string& slot, size_t bytes) {
+    auto it = arena_.find(slot);
+    if (it != arena_.end() && it->second && it->second->bytes >= bytes) return it->second->p;
+    size_t fr = 0, tot = 0;
+    DSB_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t reserve = std::max<size_t>(size_t(1) << 30, tot / 50);
+    if (it != arena_.end()) {
+        DSB_CUDA(cudaStreamSynchronize(stream));
+        arena_.erase(it);
+    }
+    // probe for the slot plus the reserve, then keep only the slot (the
+    // stream-ordered pool hands the probe's block back)
+    void* probe = nullptr;
+    if (cudaMallocAsync(&probe, bytes + reserve, stream) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    cudaFreeAsync(probe, stream);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    cudaFreeAsync(p, stream);
+    return scratch(slot, bytes);
+}
+
+bool Ctx::evict_scratch() {
+    bool any = false;
+    for (auto it = arena_.begin(); it != arena_.end();) {
+        if (evictable_slot(it->first)) {
+            if (!any) DSB_CUDA(cudaStreamSynchronize(stream));
+            clear_graphs();  // they address the slot
+            it = arena_.erase(it);
+            any = true;
+        } else {
+            ++it;
+        }
+    }
+    if (any) DSB_CUDA(cudaStreamSynchronize(stream));
+    return any;
+}
+
 void* Ctx::pinned_scratch(const std::string& name, size_t bytes) {
     auto& b = pinned_arena_[name];
     const size_t elems = (bytes + sizeof(double) - 1) / sizeof(double);
@@ -268,8 +322,9 @@ void Ctx::make_events(cudaEvent_t* a, cudaEvent_t* b) {
 }
 
 void Ctx::add_timed(int kind, cudaEvent_t a, cudaEvent_t b) {
-    if (kind == 1) ++k2_launches;
+    if (kind == 1 || kind == 3) ++k2_launches;
     else ++k1_launches;
+    if (kind == 3) ++k2_first_launches;
     if (a && b) pending.push_back({a, b, kind});
 }
 
@@ -279,7 +334,8 @@ void Ctx::drain_timing() {
     for (auto& t : pending) {
         float ms = 0.0f;
         DSB_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
-        (t.kind == 1 ? k2_ms : k1_ms) += ms;
+        (t.kind == 1 || t.kind == 3 ? k2_ms : k1_ms) += ms;
+        if (t.kind == 3) k2_first_ms += ms;
         event_pool.push_back(t.a);
         event_pool.push_back(t.b);
     }

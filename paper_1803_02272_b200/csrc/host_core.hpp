@@ -123,6 +123,12 @@ public:
 
     // grow-only workspace arena
     void* scratch(const std::string& slot, size_t bytes);
+    // an evictable slot (the S-digit cache): nullptr instead of an error
+    // when `bytes` plus `reserve` bytes are not available; a failed device
+    // allocation elsewhere evicts these slots (evict_scratch) and retries
+    // (reserve: max(1 GB, 2 % of the device))
+    void* try_scratch(const std::string& slot, size_t bytes);
+    bool evict_scratch();
     // immutable device table named by its content key: uploaded on first
     // use (never inside a graph capture), then returned as is
     bool has_table(const std::string& name) const { return tables_.count(name) != 0; }
@@ -133,10 +139,15 @@ public:
     uint64_t launches_base = 0;
     uint64_t k2_launches = 0, k1_launches = 0, h2d = 0, d2h = 0;
     double k2_ms = 0.0, k1_ms = 0.0;
+    // the first product pass of each solve (kind 3 below; also in k2_*):
+    // the pass that stores the S-digit cache when it is on
+    uint64_t k2_first_launches = 0;
+    double k2_first_ms = 0.0;
     int last_evd_sweeps = 0, last_orth_shifted = 0, last_power_iters = 0;
     int last_product_kernel = 0;  // 0 fp64 DMMA, 1 int8 slice product
     int last_product_groups = 1;  // int8 column groups (reads of D per pass)
     int last_product_sdigits = 0;  // int8 S slices per element (7, or 3 for Hamming D)
+    int last_product_sdig = 0;     // int8: the S-digit cache fed passes 2.. of the last solve
     int last_product_pair = 0;     // int8: the CTA-pair kernel (one read of D for two groups)
     std::vector<TimedPair> pending;
     std::vector<cudaEvent_t> event_pool;

@@ -127,7 +127,7 @@ constexpr bool kWarpIssue = DSB_K2I_WARP_ISSUE != 0;
 #ifndef DSB_TS_BPROD_NA
 #define DSB_TS_BPROD_NA 2
 #endif
-template <int NB, int SD = kDig>
+template <int NB, int SD = kDig, int DM = 0>
 constexpr bool bprod_ts();
 
 
@@ -191,13 +191,16 @@ template <int NB, int SD = kDig>
 constexpr int a_smem_stage_ts() {  // bytes of shared-memory A digits per stage
     return (SD - tmem_digits_ts<NB, SD>()) * kRowsI8 * kKStep;
 }
-template <int NB, int SD = kDig>
+template <int NB, int SD = kDig, int DM = 0>
 constexpr int b_stages_ts() {
-    return bprod_ts<NB, SD>() ? kBStagesTs : a_stages_ts<NB, SD>();
+    return bprod_ts<NB, SD, DM>() ? kBStagesTs : a_stages_ts<NB, SD>();
 }
-template <int NB, int SD>
+// streaming the S-digit cache (DM = 2) an A stage turns over in ~the MMA
+// time, too fast to hide a panel-digit load issued when the stage is claimed:
+// the producer streams them ahead then too
+template <int NB, int SD, int DM>
 constexpr bool bprod_ts() {
-    return a_stages_ts<NB, SD>() <= DSB_TS_BPROD_NA;
+    return DM == 2 || a_stages_ts<NB, SD>() <= DSB_TS_BPROD_NA;
 }
 // shared-memory budget of the rings: the CTA pair (NB = 48 and the pair's
 // NB = 64 launches) feeds TWO SMs' bandwidth from one D ring, so it takes the
@@ -205,17 +208,43 @@ constexpr bool bprod_ts() {
 #ifndef DSB_TS_PAIR_SMEM_KB
 #define DSB_TS_PAIR_SMEM_KB 224
 #endif
-template <int NB, typename TD, int SD = kDig, int CL = 1>
+// ---- S-digit cache -----------------------------------------------------------
+// The S digits of a (128-row block, 32-column k-step) item depend only on D
+// and the K1 row exponents, which every product pass of a solve shares. With
+// the cache on, the solve's first pass (DM = 1) also stores each item's digit
+// planes (SD x 4 KB) to HBM, and the later passes (DM = 2) stream those
+// planes with one bulk copy per item instead of the D tile: SD bytes per
+// element instead of 8 (Hamming: 3), and no conversion — the bound of the
+// conversion-limited launches (the CTA pair, NB = 64, the Hamming slices).
+// Item layout (bytes): half h = row / 64, plane t, converter column part p
+// (8 columns), row % 64, 8 digit bytes: h SD 2048 + ((t-1) 4 + p) 512 +
+// (row % 64) 8 — a converter warp's 32 rows are 256 contiguous bytes per
+// plane, and each 64-row half is contiguous (the pair's multicast halves).
+template <int SD>
+constexpr int sdig_item_bytes() {
+    return SD * 4 * kRowsI8 * 8;
+}
+__device__ __forceinline__ uint32_t sdig_off(int row, int part, int t, int sd) {
+    return static_cast<uint32_t>((row >> 6) * sd * 2048 + ((t - 1) * 4 + part) * 512 +
+                                 (row & 63) * 8);
+}
+// bytes of one ring slot: the D tile, or (DM = 2) an item's digit planes
+template <typename TD, int SD, int DM>
+constexpr int slot_bytes() {
+    return DM == 2 ? sdig_item_bytes<SD>() : d_bytes<TD>();
+}
+template <int NB, typename TD, int SD = kDig, int CL = 1, int DM = 0>
 constexpr int d_stages_ts() {
     return std::min(8, ((CL > 1 ? DSB_TS_PAIR_SMEM_KB : DSB_TS_SMEM_KB) * 1024 -
-                        b_stages_ts<NB, SD>() * b_bytes<NB>() -
+                        b_stages_ts<NB, SD, DM>() * b_bytes<NB>() -
                         a_stages_ts<NB, SD>() * a_smem_stage_ts<NB, SD>()) /
-                           d_bytes<TD>());
+                           slot_bytes<TD, SD, DM>());
 }
-template <int NB, typename TD, int SD = kDig, int CL = 1>
+template <int NB, typename TD, int SD = kDig, int CL = 1, int DM = 0>
 constexpr size_t ts_smem() {
-    return 1024 + static_cast<size_t>(d_stages_ts<NB, TD, SD, CL>()) * d_bytes<TD>() +
-           b_stages_ts<NB, SD>() * b_bytes<NB>() +
+    return 1024 +
+           static_cast<size_t>(d_stages_ts<NB, TD, SD, CL, DM>()) * slot_bytes<TD, SD, DM>() +
+           b_stages_ts<NB, SD, DM>() * b_bytes<NB>() +
            a_stages_ts<NB, SD>() * a_smem_stage_ts<NB, SD>() + 448 + NB * 8;
 }
 
@@ -274,6 +303,27 @@ __device__ __forceinline__ void pack_digits(const uint32_t (&lo)[8], const uint3
     }
 }
 
+// an item's digit planes t = 1..SD of (row, converter part) from a ring
+// slot / into the cache (sdig_off layout)
+template <int SD>
+__device__ __forceinline__ void sdig_read(const unsigned char* slot, int row, int part,
+                                          uint32_t (&wd)[SD][2]) {
+#pragma unroll
+    for (int t = 1; t <= SD; ++t) {
+        const uint2 v = *reinterpret_cast<const uint2*>(slot + sdig_off(row, part, t, SD));
+        wd[t - 1][0] = v.x;
+        wd[t - 1][1] = v.y;
+    }
+}
+template <int SD>
+__device__ __forceinline__ void sdig_write(unsigned char* item, int row, int part,
+                                           const uint32_t (&wd)[SD][2]) {
+#pragma unroll
+    for (int t = 1; t <= SD; ++t)
+        *reinterpret_cast<uint2*>(item + sdig_off(row, part, t, SD)) =
+            make_uint2(wd[t - 1][0], wd[t - 1][1]);
+}
+
 // CL = 2: a cluster of two CTAs (on two SMs) shares every D tile — each
 // CTA TMA-loads one 64-row half of the tile and multicasts it to both, so D
 // is read from HBM once per pass — and each CTA multiplies it into its own
@@ -284,13 +334,16 @@ __device__ __forceinline__ void pack_digits(const uint32_t (&lo)[8], const uint3
 // only after the consumers of BOTH CTAs released it (each consumer warp
 // arrives on its own and on the peer's empty barrier). tmD then has 64-row
 // boxes; bdig holds the groups' digit planes bdig_stride bytes apart.
-template <int NB, typename TD, int SD, int CL>
+// DM: S-digit cache mode (see sdig_item_bytes): 0 off, 1 convert and store
+// the items' digit planes at sdig, 2 stream them from sdig (no D tile, no
+// conversion). Items are indexed rb * nks_c + global k-step.
+template <int NB, typename TD, int SD, int CL, int DM = 0>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
                    const int* __restrict__ row_exp, const int* __restrict__ col_exp, int nrows,
                    int nks, int total, double* __restrict__ part, int maxseg, int wp, int cg0,
                    const int* __restrict__ skip, int dbg, double hlen, size_t bdig_stride,
-                   int k_off) {
+                   int k_off, unsigned char* __restrict__ sdig, int nks_c) {
     // k_off: first global k-step of this launch (a column range of D and the
     // matching panel rows; the walk's k-steps are local to the range)
     if (skip && *skip) return;
@@ -299,14 +352,16 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     cg0 += crank * NB;
     bdig += static_cast<size_t>(crank) * bdig_stride;
     static_assert(SD == kDig || SD == 3, "S digit counts: 7 (general) or 3 (Hamming)");
-    constexpr int ND = d_stages_ts<NB, TD, SD, CL>();
+    static_assert(DM >= 0 && DM <= 2, "S-digit cache mode");
+    constexpr int ND = d_stages_ts<NB, TD, SD, CL, DM>();
     constexpr int NA = a_stages_ts<NB, SD>();
     // panel digits: with several A stages they ride with the A stage (loaded
     // by one converter lane when it claims the stage); with a single A stage
     // they get their own ring filled ahead by the producer
-    constexpr bool kBProd = bprod_ts<NB, SD>();
+    constexpr bool kBProd = bprod_ts<NB, SD, DM>();
     constexpr int NBR = kBProd ? kBStagesTs : NA;
-    constexpr int DB = d_bytes<TD>();
+    constexpr int DB = slot_bytes<TD, SD, DM>();  // one slot of the D ring
+    constexpr int IB = sdig_item_bytes<SD>();
     constexpr int BB = b_bytes<NB>();
     constexpr int TD_DIG = tmem_digits_ts<NB, SD>();  // digits 1..TD_DIG in TMEM
     constexpr int ASB = a_smem_stage_ts<NB, SD>();     // the rest in shared memory
@@ -377,14 +432,24 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     if (warp == 0) {
         // ---------------- TMA producer: D tiles and panel digits ----------------
         if (lane == 0) {
-            prefetch_tmap(&tmD);
+            if constexpr (DM != 2) prefetch_tmap(&tmD);
             int sd = 0, sb = 0, k = 0;
             uint32_t pd = 0, pb = 0;
             for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
                 if (k >= ND) mbar_wait(&empty_d[sd], pd ^ 1);
                 unsigned char* dst = dring + sd * DB;
-                mbar_arrive_expect_tx(&full_d[sd], DB);  // the whole tile
-                if constexpr (CL > 1) {
+                mbar_arrive_expect_tx(&full_d[sd], DB);  // the whole tile / item
+                if constexpr (DM == 2) {
+                    // the item's digit planes (each CTA of a pair fetches one
+                    // 64-row half into both)
+                    const unsigned char* src =
+                        sdig + (static_cast<size_t>(w.rb) * nks_c + k_off + w.ks) * IB;
+                    if constexpr (CL > 1)
+                        bulk_load_mc(dst + crank * (IB / 2), src + crank * (IB / 2), IB / 2,
+                                     &full_d[sd], 0x3);
+                    else
+                        bulk_load(dst, src, IB, &full_d[sd]);
+                } else if constexpr (CL > 1) {
                     // this CTA's 64-row half of the tile, into both CTAs
                     // (64 rows x 128 B keeps the SWIZZLE_128B phase)
                     const int r0 = w.rb * kRowsI8 + 64 * crank;
@@ -525,11 +590,14 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                               &full_a[sa]);
                 }
                 if (dbg != 1) {
-                    double d[8];
-                    load8<TD>(dring + sd * DB, row, c0, d);
                     const uint32_t ta = tmem_a + static_cast<uint32_t>(sa) * ACOLS + lane_off;
                     unsigned char* as = aring + sa * ASB + umma_tile_off(row, c0);
                     uint32_t wd[SD][2];
+                    if constexpr (DM == 2) {
+                        sdig_read<SD>(dring + sd * DB, row, part_k, wd);
+                    } else {
+                    double d[8];
+                    load8<TD>(dring + sd * DB, row, c0, d);
                     if constexpr (SD == kDig) {
                         uint32_t lo[8], hi[8];
 #pragma unroll
@@ -563,6 +631,12 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                             wd[2][g] = __byte_perm(l01, l23, 0x5410);
                         }
                     }
+                    if constexpr (DM == 1)
+                        if (CL == 1 || (row >> 6) == crank)
+                            sdig_write<SD>(
+                                sdig + (static_cast<size_t>(w.rb) * nks_c + k_off + w.ks) * IB,
+                                row, part_k, wd);
+                    }
 #pragma unroll
                     for (int t = 1; t <= SD; ++t) {
                         const uint32_t w0 = wd[t - 1][0], w1 = wd[t - 1][1];
@@ -587,17 +661,27 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 // single A stage: convert into registers while the MMAs of the
                 // previous k-step still read the stage, then store
                 uint32_t wd[kDig][2];
+                static_assert(NA > 1 || SD == kDig, "one A stage: general slices only");
                 if (dbg != 1) {
-                    double d[8];
-                    load8<TD>(dring + sd * DB, row, c0, d);
-                    uint32_t lo[8], hi[8];
+                    if constexpr (DM == 2) {
+                        sdig_read<kDig>(dring + sd * DB, row, part_k, wd);
+                    } else {
+                        double d[8];
+                        load8<TD>(dring + sd * DB, row, c0, d);
+                        uint32_t lo[8], hi[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);
-                        lo[j] = static_cast<uint32_t>(m);
-                        hi[j] = static_cast<uint32_t>(m >> 32);
+                        for (int j = 0; j < 8; ++j) {
+                            const unsigned long long m = __double2ull_rz((d[j] * d[j]) * sc);
+                            lo[j] = static_cast<uint32_t>(m);
+                            hi[j] = static_cast<uint32_t>(m >> 32);
+                        }
+                        pack_digits(lo, hi, wd);
+                        if constexpr (DM == 1)
+                            if (CL == 1 || (row >> 6) == crank)
+                                sdig_write<kDig>(
+                                    sdig + (static_cast<size_t>(w.rb) * nks_c + k_off + w.ks) * IB,
+                                    row, part_k, wd);
                     }
-                    pack_digits(lo, hi, wd);
                 }
                 if (k >= NA) {
                     mbar_wait(&empty_a[sa], pa ^ 1);
@@ -749,21 +833,23 @@ int k2i_debug_mode() {
     return m;
 }
 
-template <int NB, typename TD, int SD = kDig, int CL = 1>
-void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
-            size_t bdig_stride, const int* row_exp, const int* col_exp, double* part, int cg0,
-            cudaStream_t st, const int* skip, double hlen = 0.0, int k_off = 0) {
-    const void* fn = reinterpret_cast<const void*>(k2i_product_ts<NB, TD, SD, CL>);
-    ensure_dyn_smem(fn, ts_smem<NB, TD, SD, CL>());
+template <int NB, typename TD, int SD, int CL, int DM>
+void run_i8_dm(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
+               size_t bdig_stride, const int* row_exp, const int* col_exp, double* part, int cg0,
+               cudaStream_t st, const int* skip, double hlen, int k_off, unsigned char* sdig,
+               int nks_c) {
+    const void* fn = reinterpret_cast<const void*>(k2i_product_ts<NB, TD, SD, CL, DM>);
+    constexpr size_t smem = ts_smem<NB, TD, SD, CL, DM>();
+    ensure_dyn_smem(fn, smem);
     if constexpr (CL == 1) {
-        k2i_product_ts<NB, TD, SD, 1><<<p.grid, kThreadsI8, ts_smem<NB, TD, SD>(), st>>>(
+        k2i_product_ts<NB, TD, SD, 1, DM><<<p.grid, kThreadsI8, smem, st>>>(
             *tmap, bdig, row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
-            p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen, bdig_stride, k_off);
+            p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen, bdig_stride, k_off, sdig, nks_c);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(p.grid * CL));
         cfg.blockDim = dim3(kThreadsI8);
-        cfg.dynamicSmemBytes = ts_smem<NB, TD, SD, CL>();
+        cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -772,11 +858,28 @@ void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned ch
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        DSB_CUDA(cudaLaunchKernelEx(&cfg, k2i_product_ts<NB, TD, SD, CL>, *tmap, bdig, row_exp,
-                                    col_exp, p.nrows, p.nks, static_cast<int>(p.total), part,
-                                    p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen,
-                                    bdig_stride, k_off));
+        DSB_CUDA(cudaLaunchKernelEx(&cfg, k2i_product_ts<NB, TD, SD, CL, DM>, *tmap, bdig,
+                                    row_exp, col_exp, p.nrows, p.nks, static_cast<int>(p.total),
+                                    part, p.maxseg, wp, cg0, skip, k2i_debug_mode(), hlen,
+                                    bdig_stride, k_off, sdig, nks_c));
     }
+}
+// dm: S-digit cache mode of this launch (0 off, 1 store, 2 stream; sdig and
+// nks_c as in k2i_product_ts)
+template <int NB, typename TD, int SD = kDig, int CL = 1>
+void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned char* bdig,
+            size_t bdig_stride, const int* row_exp, const int* col_exp, double* part, int cg0,
+            cudaStream_t st, const int* skip, double hlen = 0.0, int k_off = 0, int dm = 0,
+            unsigned char* sdig = nullptr, int nks_c = 0) {
+    if (dm == 1)
+        run_i8_dm<NB, TD, SD, CL, 1>(tmap, p, wp, bdig, bdig_stride, row_exp, col_exp, part, cg0,
+                                     st, skip, hlen, k_off, sdig, nks_c);
+    else if (dm == 2)
+        run_i8_dm<NB, TD, SD, CL, 2>(tmap, p, wp, bdig, bdig_stride, row_exp, col_exp, part, cg0,
+                                     st, skip, hlen, k_off, sdig, nks_c);
+    else
+        run_i8_dm<NB, TD, SD, CL, 0>(tmap, p, wp, bdig, bdig_stride, row_exp, col_exp, part, cg0,
+                                     st, skip, hlen, k_off, nullptr, 0);
 }
 
 // Co-resident CTA pairs (clusters of 2 with one ~210 KB CTA per SM): at most
@@ -869,11 +972,19 @@ K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms) {
 
 bool k2i_supported(int wp) { return wp >= 8 && wp <= 128; }
 
+size_t k2i_sdig_bytes(const K2iPlan& p, int sdigits) {
+    return static_cast<size_t>(p.nblk) * p.nks * (sdigits == 3 ? sdig_item_bytes<3>()
+                                                               : sdig_item_bytes<kDig>());
+}
+
 void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt, const K2iPlan& p,
                 int wp, const double* x, size_t x_rows_pad, const int* row_exp, double* pmax,
                 int* col_exp, unsigned char* bdig, double* part, const double* row_mean,
                 const double* scalars, const double* colsums, double* y, size_t y_rows_pad,
-                cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, const int* skip, int hamming_len) {
+                cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, const int* skip, int hamming_len,
+                unsigned char* sdig, int sdig_mode) {
+    if (!sdig) sdig_mode = 0;
+    const int nks_c = p.nks;
     // k2_reduce writes the 128-row blocks; the panel rows beyond them (up to
     // the 256-row padding) must read as zero, whatever an earlier, larger
     // solve left in this workspace
@@ -899,42 +1010,45 @@ void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
         if (e0) record_timing_event(e0, st);
         const size_t bs = p.bdig_stride;
         (void)nb;  // 48 (k2i_plan)
+        const int dm = sdig_mode;
         if (ham)
             run_i8<48, double, 3, 2>(tmap64, p, wp, bdig, bs, row_exp, col_exp, part, 0, st, skip,
-                                     hl);
+                                     hl, 0, dm, sdig, nks_c);
         else if (dt == DType::F64)
             run_i8<48, double, kDig, 2>(tmap64, p, wp, bdig, bs, row_exp, col_exp, part, 0, st,
-                                        skip);
+                                        skip, 0.0, 0, dm, sdig, nks_c);
         else
             run_i8<48, float, kDig, 2>(tmap64, p, wp, bdig, bs, row_exp, col_exp, part, 0, st,
-                                       skip);
+                                       skip, 0.0, 0, dm, sdig, nks_c);
         count_launch(2);
     } else {
         for (int g = 0; g < p.ngroups; ++g) {
             const int nb = p.gnb[g], cg0 = p.gc0[g];
             digits(nb, cg0, bdig);
             if (g == 0 && e0) record_timing_event(e0, st);
+            // the first group of a storing pass stores, the later ones stream
+            const int dm = (sdig_mode == 1 && g > 0) ? 2 : sdig_mode;
             if (ham) {
                 if (nb == 32)
                     run_i8<32, double, 3>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
-                                          skip, hl);
+                                          skip, hl, 0, dm, sdig, nks_c);
                 else
                     run_i8<64, double, 3>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
-                                          skip, hl);
+                                          skip, hl, 0, dm, sdig, nks_c);
             } else if (dt == DType::F64) {
                 if (nb == 32)
                     run_i8<32, double>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
-                                       skip);
+                                       skip, 0.0, 0, dm, sdig, nks_c);
                 else
                     run_i8<64, double>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
-                                       skip);
+                                       skip, 0.0, 0, dm, sdig, nks_c);
             } else {
                 if (nb == 32)
                     run_i8<32, float>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
-                                      skip);
+                                      skip, 0.0, 0, dm, sdig, nks_c);
                 else
                     run_i8<64, float>(tmap128, p, wp, bdig, 0, row_exp, col_exp, part, cg0, st,
-                                      skip);
+                                      skip, 0.0, 0, dm, sdig, nks_c);
             }
         }
         count_launch(2 * p.ngroups);

@@ -150,7 +150,12 @@ void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
                 int* col_exp, unsigned char* bdig, double* part, const double* row_mean,
                 const double* scalars, const double* colsums, double* y, size_t y_rows_pad,
                 cudaStream_t st, cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr,
-                const int* skip = nullptr, int hamming_len = 0);
+                const int* skip = nullptr, int hamming_len = 0, unsigned char* sdig = nullptr,
+                int sdig_mode = 0);
+// bytes of the S-digit cache of a plan (sdigits: 7, or 3 for Hamming slices):
+// the solve's first product pass stores every (row block, k-step) item's
+// digit planes there (sdig_mode 1), the later passes stream them (mode 2)
+size_t k2i_sdig_bytes(const K2iPlan& p, int sdigits);
 
 // out[0] = sum of `count` doubles in a fixed order
 void launch_sum_fixed(const double* partial, size_t count, double* out, cudaStream_t st);

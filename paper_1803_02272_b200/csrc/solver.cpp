@@ -150,6 +150,20 @@ bool hamming_slices_enabled() {
 
 void set_product_path(int mode) { g_product_path.store(mode); }
 
+std::atomic<int> g_sdig_policy{-1};  // -1: not yet read from DSB_SDIG
+
+int sdig_policy() {
+    int m = g_sdig_policy.load();
+    if (m < 0) {
+        const char* e = std::getenv("DSB_SDIG");
+        m = e ? std::min(2, std::max(0, std::atoi(e))) : 1;
+        g_sdig_policy.store(m);
+    }
+    return m;
+}
+
+void set_sdig_policy(int mode) { g_sdig_policy.store(mode); }
+
 bool use_int8_product(const GramInfo& gi, int wp) {
     const int mode = product_path();
     if (mode == 1 || !gi.row_exp || !k2i_supported(wp)) return false;
@@ -318,6 +332,27 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
                                iplan.maxseg)
                : k2_slot_table(plan.nb, plan.nk, plan.total, plan.grid, plan.maxseg);
 
+    // S-digit cache (k2i_product.cu, sdig_item_bytes): the first product
+    // pass stores every item's S digit planes, the later passes stream them
+    // instead of D: no conversion (the bound of the CTA pair, the NB = 64
+    // groups and the Hamming slices) and SD instead of 8 bytes per element
+    // (measured per later pass: C5 4.3 -> 2.4 ms, n = 40k w = 70 5.0 -> 3.5
+    // ms, w = 50 3.6 -> 2.7 ms; the HBM-bound C2 pass 0.556 -> 0.437 ms
+    // against a storing pass of 1.07 ms: 3.34 -> 3.25 ms per solve).
+    // Claimed last (evictable: a later failed allocation drops it); skipped
+    // when it would leave less than max(1 GB, 2 %) of the device free.
+    // DSB_SDIG / divscope_set_sdig_cache: 0 off, 1 auto (default: on when it
+    // fits), 2 on.
+    unsigned char* sdig = nullptr;
+    if (use_i8) {
+        const int pol = sdig_policy();
+        if (pol > 0)
+            sdig = static_cast<unsigned char*>(
+                c.try_scratch("i8_sdig", k2i_sdig_bytes(iplan, hamming_i8 ? 3 : 7)));
+    }
+    c.last_product_sdig = sdig ? 1 : 0;
+    int sdig_pass = 0;
+
     // the solve as one stream sequence: eager, or captured once per signature
     // (shape, product kernel, workspace addresses) and replayed as a CUDA
     // graph — 25-40 dependent launches per solve, whose launch gaps are most
@@ -352,11 +387,11 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
             launch_k2i(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x, n_pad,
                        g.gram->row_exp->as<int>(), pmax,
                        col_exp, bdig, part, row_mean, scal_dev, colsums, y, n_pad, c.stream, e0,
-                       e1, nullptr, hamming_i8);
+                       e1, nullptr, hamming_i8, sdig, sdig ? (sdig_pass++ == 0 ? 1 : 2) : 0);
         else
             launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums,
                       y, n_pad, c.stream, e0, e1);
-        if (!graph_timed) c.add_timed(1, e0, e1);
+        if (!graph_timed) c.add_timed(nprod == 0 ? 3 : 1, e0, e1);
         ++nprod;
         mark("product");
     };
@@ -384,6 +419,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     auto enqueue = [&] {
         stats_ready = false;
         nprod = 0;
+        sdig_pass = 0;  // every solve stores the cache in its first pass
         DSB_CUDA(cudaMemsetAsync(flags, 0, 64, c.stream));
         DSB_CUDA(cudaMemcpyAsync(P0, omega_cached, pbytes, cudaMemcpyDeviceToDevice, c.stream));
         mark("start");
@@ -458,6 +494,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
                                 static_cast<const void*>(flags), static_cast<const void*>(cstat),
                                 static_cast<const void*>(pmax), static_cast<const void*>(col_exp),
                                 static_cast<const void*>(bdig),
+                                static_cast<const void*>(sdig),
                                 static_cast<const void*>(omega_cached),
                                 static_cast<const void*>(eo.vals),
                                 static_cast<const void*>(eo.vkeep),
@@ -515,6 +552,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     if (ge) {
         DSB_CUDA(cudaGraphLaunch(ge->exec, c.stream));
         c.k2_launches += static_cast<uint64_t>(ge->products);
+        if (ge->products > 0) ++c.k2_first_launches;
     } else {
         enqueue();
     }
@@ -528,10 +566,11 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     if (trace) std::fprintf(stderr, "[trace] host enqueue done %.1f us\n", host_us());
     c.sync();
     if (ge && c.timing)
-        for (auto& ev : ge->timed) {
+        for (size_t i = 0; i < ge->timed.size(); ++i) {
             float ms = 0.f;
-            DSB_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+            DSB_CUDA(cudaEventElapsedTime(&ms, ge->timed[i].first, ge->timed[i].second));
             c.k2_ms += ms;
+            if (i == 0) c.k2_first_ms += ms;
         }
     if (trace) std::fprintf(stderr, "[trace] host meta synced %.1f us\n", host_us());
     if (trace) {

@@ -76,6 +76,9 @@ double reconstruction_error(const Matrix& g, const Embedding& e);
 // product kernel choice: 0 auto, 1 fp64 DMMA only, 2 int8 slice product
 // whenever supported (lazy grams, w <= 64)
 void set_product_path(int mode);
+// S-digit cache policy (divscope_set_sdig_cache): 0 off, 1 auto, 2 on
+void set_sdig_policy(int mode);
+int sdig_policy();
 // whether a product pass on this gram uses the int8 slice product
 bool hamming_slices_enabled();  // DSB_K2I_HAMMING (default on)
 bool use_int8_product(const GramInfo& gi, int wp);

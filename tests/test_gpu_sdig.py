@@ -1,0 +1,106 @@
+"""S-digit cache of the int8 product (k2i_product.cu, sdig_item_bytes): the
+solve's first product pass stores every (row block, k-step) item's digit
+planes of D o D, the later passes stream them instead of D. The digits are
+the same bytes the converters would produce, so a solve with the cache must
+be BIT-identical to one without it — on every kernel variant the cache
+feeds: the single-CTA NB = 32 / 64 groups, the CTA pair (multicast halves),
+the Hamming 3-byte slices, f32 D, two column groups in one pass (the first
+group stores, the second streams), ragged n and the int32 chunk edge.
+The oracle comparison (ref src/rsvd.cpp:81-145, mds.cpp:81-124) runs on the
+cached path of each case as well.
+"""
+import numpy as np
+import pytest
+
+from helpers import coords_match_up_to_sign
+
+pytestmark = pytest.mark.gpu
+
+
+def _solve(ds, g, k, p, q, seed, cache):
+    ds.set_product_path(2)
+    ds.set_sdig_cache(cache)
+    try:
+        e = ds.embed(g, rank=k, oversampling=p, power_iters=q, seed=seed)
+        st = ds.stats_get()
+    finally:
+        ds.set_product_path(0)
+        ds.set_sdig_cache(1)
+    return e, st
+
+
+CASES = [
+    # (kind, n, rank, over, expect pair, sdigits)
+    ("f64", 4133, 20, 10, 0, 7),   # NB = 32, ragged n
+    ("f64", 4500, 40, 10, 0, 7),   # NB = 64 hybrid (digits 5-7 via shared memory)
+    ("f64", 4250, 50, 20, 1, 7),   # w = 70: CTA pair, multicast item halves
+    ("f32", 4200, 100, 20, 0, 7),  # w = 120 on f32 D: two 64-column groups
+    ("ham", 4300, 30, 20, 0, 3),   # Hamming slices, NB = 64
+    ("ham", 4400, 10, 10, 0, 3),   # Hamming slices, NB = 32
+    ("ham", 4100, 50, 20, 1, 3),   # Hamming slices on the CTA pair
+]
+
+
+def _matrix(ds, kind, n, seed):
+    if kind == "ham":
+        return ds.matrix_hamming(ds.synth_reads(n, 400, 20, 0.05, seed))
+    return ds.matrix_euclidean(ds.synth_points(2, n, seed), store_f32=(kind == "f32"))
+
+
+@pytest.mark.parametrize("kind,n,rank,over,pair,sdigits", CASES)
+def test_sdig_cache_bit_identical(ds, oracle, kind, n, rank, over, pair, sdigits):
+    d = _matrix(ds, kind, n, n % 11)
+    g = ds.gram(d)
+    off, st0 = _solve(ds, g, rank, over, 2, 3, 0)
+    assert st0.last_product_kernel == 1 and st0.last_product_sdig == 0
+    on, st1 = _solve(ds, g, rank, over, 2, 3, 2)
+    assert st1.last_product_kernel == 1 and st1.last_product_sdig == 1
+    assert (st1.last_product_pair, st1.last_product_sdigits) == (pair, sdigits)
+    assert np.array_equal(on.eigenvalues, off.eigenvalues)
+    assert np.array_equal(on.coords, off.coords)
+    # a second cached solve (graph replay) stores and streams again
+    again, _ = _solve(ds, g, rank, over, 2, 3, 2)
+    assert np.array_equal(again.coords, on.coords)
+    if kind != "f32":
+        dm = d.to_numpy()
+        _, rm, grand = oracle.gram_stats(dm)
+        want = oracle.embed(rank, over, 2, 3, d=dm, row_mean=rm, grand=grand)
+        top = min(on.dims, 12)
+        np.testing.assert_allclose(on.eigenvalues[:top], want["eigenvalues"][:top], rtol=1e-10)
+        assert coords_match_up_to_sign(on.coords[:, :top], want["coords"][:, :top]) < \
+            1e-7 * np.sqrt(want["eigenvalues"][0])
+
+
+def test_sdig_cache_chunk_edge(ds, oracle):
+    # n > 8192 columns: the int32 accumulation flushes mid-row (kChunk); the
+    # streamed passes follow the same walk
+    n = 8400
+    d = ds.matrix_euclidean(ds.synth_points(1, n, 4))
+    g = ds.gram(d)
+    off, _ = _solve(ds, g, 40, 10, 1, 9, 0)
+    on, st = _solve(ds, g, 40, 10, 1, 9, 2)
+    assert st.last_product_sdig == 1
+    assert np.array_equal(on.coords, off.coords)
+
+
+def test_sdig_cache_auto_policy(ds):
+    # auto: on whenever the int8 path runs and the cache fits; policy 0
+    # disables it; the first-pass statistics count one storing pass per solve
+    g = ds.gram(ds.matrix_euclidean(ds.synth_points(2, 4200, 5)))
+    ds.set_product_path(2)
+    try:
+        ds.stats_reset()
+        ds.embed(g, rank=40, oversampling=10, power_iters=1, seed=1)
+        st = ds.stats_get()
+        assert st.last_product_sdig == 1
+        assert (st.product_launches, st.product_first_launches) == (4, 1)
+        ds.embed(g, rank=20, oversampling=10, power_iters=1, seed=1)
+        assert ds.stats_get().last_product_sdig == 1
+        ds.set_sdig_cache(0)
+        ds.embed(g, rank=40, oversampling=10, power_iters=1, seed=1)
+        assert ds.stats_get().last_product_sdig == 0
+    finally:
+        ds.set_product_path(0)
+        ds.set_sdig_cache(1)
+    with pytest.raises(ds.DivscopeError):
+        ds.set_sdig_cache(3)
