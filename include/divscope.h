@@ -353,6 +353,7 @@ typedef struct divscope_stats {
     uint64_t product_first_launches; /* the first product pass of each solve (also counted in
                                         product_launches): the storing pass with the cache on */
     double product_first_ms;          /* its summed device time, when timing on */
+    int32_t last_product_stream_cl;   /* CTAs sharing each streamed digit item (0: no cache) */
 } divscope_stats;
 
 /* timing on => CUDA events are recorded around K1/K2 on the library stream */

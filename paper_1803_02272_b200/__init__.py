@@ -83,7 +83,8 @@ class Stats(C.Structure):
                 ("last_power_iters", C.c_int32), ("last_product_kernel", C.c_int32),
                 ("last_product_groups", C.c_int32), ("last_product_sdigits", C.c_int32),
                 ("last_product_pair", C.c_int32), ("last_product_sdig", C.c_int32),
-                ("product_first_launches", C.c_uint64), ("product_first_ms", C.c_double)]
+                ("product_first_launches", C.c_uint64), ("product_first_ms", C.c_double),
+                ("last_product_stream_cl", C.c_int32)]
 
 
 _dp = C.POINTER(C.c_double)

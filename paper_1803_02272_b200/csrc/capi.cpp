@@ -771,6 +771,7 @@ void divscope_stats_get(divscope_stats* out) {
         out->last_product_sdig = c.last_product_sdig;
         out->product_first_launches = c.k2_first_launches;
         out->product_first_ms = c.k2_first_ms;
+        out->last_product_stream_cl = c.last_product_stream_cl;
     } catch (...) {
     }
 }

@@ -148,6 +148,7 @@ public:
     int last_product_groups = 1;  // int8 column groups (reads of D per pass)
     int last_product_sdigits = 0;  // int8 S slices per element (7, or 3 for Hamming D)
     int last_product_sdig = 0;     // int8: the S-digit cache fed passes 2.. of the last solve
+    int last_product_stream_cl = 0;  // CTAs per cluster of those streaming passes
     int last_product_pair = 0;     // int8: the CTA-pair kernel (one read of D for two groups)
     std::vector<TimedPair> pending;
     std::vector<cudaEvent_t> event_pool;

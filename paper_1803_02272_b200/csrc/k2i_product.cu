@@ -233,12 +233,22 @@ template <typename TD, int SD, int DM>
 constexpr int slot_bytes() {
     return DM == 2 ? sdig_item_bytes<SD>() : d_bytes<TD>();
 }
+// streaming the cache with 4 A stages, the converters work in 4 groups that
+// take items round-robin (k2i_product_ts); each group must own its ring slots
+// and A stage (an mbarrier wait tells phases apart by parity only, so a group
+// running ahead on a slot another group still has to see would pass a wait it
+// should block on): the D ring depth is then a multiple of 4
+template <int NB, int SD, int DM>
+constexpr int conv_groups_ts() {
+    return (DM == 2 && a_stages_ts<NB, SD>() % 4 == 0) ? 4 : 1;
+}
 template <int NB, typename TD, int SD = kDig, int CL = 1, int DM = 0>
 constexpr int d_stages_ts() {
     return std::min(8, ((CL > 1 ? DSB_TS_PAIR_SMEM_KB : DSB_TS_SMEM_KB) * 1024 -
                         b_stages_ts<NB, SD, DM>() * b_bytes<NB>() -
                         a_stages_ts<NB, SD>() * a_smem_stage_ts<NB, SD>()) /
-                           slot_bytes<TD, SD, DM>());
+                           slot_bytes<TD, SD, DM>()) /
+           conv_groups_ts<NB, SD, DM>() * conv_groups_ts<NB, SD, DM>();
 }
 template <int NB, typename TD, int SD = kDig, int CL = 1, int DM = 0>
 constexpr size_t ts_smem() {
@@ -336,7 +346,11 @@ __device__ __forceinline__ void sdig_write(unsigned char* item, int row, int par
 // boxes; bdig holds the groups' digit planes bdig_stride bytes apart.
 // DM: S-digit cache mode (see sdig_item_bytes): 0 off, 1 convert and store
 // the items' digit planes at sdig, 2 stream them from sdig (no D tile, no
-// conversion). Items are indexed rb * nks_c + global k-step.
+// conversion). Items are indexed rb * nks_c + global k-step. Streaming, a
+// cluster of up to 4 CTAs shares every item (each bulk-loads 1/CL of it,
+// multicast to all) with one NB = 32 column group per CTA: with nothing to
+// convert, the narrow groups' 4 A stages and short MMA sequence keep the
+// tensor pipe fed where one CTA's 48/64-column group could not.
 template <int NB, typename TD, int SD, int CL, int DM = 0>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     k2i_product_ts(const __grid_constant__ CUtensorMap tmD, const unsigned char* __restrict__ bdig,
@@ -347,7 +361,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     // k_off: first global k-step of this launch (a column range of D and the
     // matching panel rows; the walk's k-steps are local to the range)
     if (skip && *skip) return;
-    static_assert(CL == 1 || CL == 2, "one CTA, or a pair sharing the D tiles");
+    static_assert(CL == 1 || CL == 2 || (DM == 2 && CL <= 4),
+                  "one CTA, a pair sharing the D tiles, or up to 4 CTAs sharing the digit items");
     const int crank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
     cg0 += crank * NB;
     bdig += static_cast<size_t>(crank) * bdig_stride;
@@ -366,6 +381,13 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     constexpr int TD_DIG = tmem_digits_ts<NB, SD>();  // digits 1..TD_DIG in TMEM
     constexpr int ASB = a_smem_stage_ts<NB, SD>();     // the rest in shared memory
     constexpr uint32_t ACOLS = a_stage_cols_ts<NB, SD>();
+    // converter warps per item: all 16 (each 8 of the 32 columns), or, when
+    // streaming the cache (nothing to convert), groups of 4 warps (one per
+    // TMEM lane quadrant, all 32 columns) taking items round-robin, so that
+    // four items' load -> tcgen05.st -> arrive chains overlap
+    constexpr int kGrp = conv_groups_ts<NB, SD, DM>();
+    static_assert(kGrp == 1 || (ND % kGrp == 0 && NA % kGrp == 0), "groups own their slots");
+    constexpr int kCW = kConv / kGrp;
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -394,12 +416,12 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < ND; ++s) {
             mbar_init(&full_d[s], 1);
-            mbar_init(&empty_d[s], kConv * CL);  // both CTAs' converters
+            mbar_init(&empty_d[s], kCW * CL);  // every CTA's converters of the item
         }
         for (int s = 0; s < NA; ++s) {
             // with the digits riding on the A stage, their expect_tx arrival
             // is the stage's 17th
-            mbar_init(&full_a[s], kBProd ? kConv : kConv + 1);
+            mbar_init(&full_a[s], kBProd ? kCW : kCW + 1);
             mbar_init(&empty_a[s], 1);
         }
         for (int s = 0; s < NBR; ++s) {
@@ -444,10 +466,14 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     // 64-row half into both)
                     const unsigned char* src =
                         sdig + (static_cast<size_t>(w.rb) * nks_c + k_off + w.ks) * IB;
-                    if constexpr (CL > 1)
-                        bulk_load_mc(dst + crank * (IB / 2), src + crank * (IB / 2), IB / 2,
-                                     &full_d[sd], 0x3);
-                    else
+                    if constexpr (CL > 1) {
+                        // this CTA's 1/CL of the item, into every CTA of the cluster
+                        constexpr int CH = (IB / CL + 15) / 16 * 16;
+                        const int off = crank * CH;
+                        bulk_load_mc(dst + off, src + off,
+                                     static_cast<uint32_t>(IB - off < CH ? IB - off : CH),
+                                     &full_d[sd], static_cast<uint16_t>((1u << CL) - 1u));
+                    } else
                         bulk_load(dst, src, IB, &full_d[sd]);
                 } else if constexpr (CL > 1) {
                     // this CTA's 64-row half of the tile, into both CTAs
@@ -564,6 +590,117 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         const int row = q * 32 + lane;
         const int c0 = part_k * 8;
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        // ---- epilogue of an accumulation chunk: this warp's 32 TMEM lanes ----
+        auto epilogue = [&](const Walk& w, int nfl) {
+            mbar_wait(acc_full, static_cast<uint32_t>(nfl & 1));
+            tc_fence_after();
+            const int grow = w.rb * kRowsI8 + row;
+            double rscale;
+            if constexpr (SD == kDig) {
+                const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
+                rscale = e > kExpZeroI8 ? ldexp(1.0, e) : 0.0;
+            } else {
+                rscale = grow < nrows ? 0x1.0p24 / (hlen * hlen) : 0.0;  // S = S' 2^-24 * this
+            }
+            double* prow = part +
+                           (static_cast<size_t>(cta) * maxseg + w.seg) * kRowsI8 * wp +
+                           static_cast<size_t>(row) * wp;
+#pragma unroll
+            for (int cb = 0; cb < NB / 16; ++cb) {
+                double v[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.0;
+#pragma unroll
+                for (int dd = 2; dd <= 8; ++dd) {
+                    int32_t iv[16];
+                    tmem_ld16(tmem + lane_off + static_cast<uint32_t>((dd - 2) * NB + cb * 16),
+                              iv);
+                    tmem_ld_wait();
+                    const double wgt = ldexp(1.0, -8 * dd);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(iv[j]) * wgt;
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int col = cg0 + cb * 16 + j;
+                    if (col < wp) {
+                        const double val = v[j] * rscale * colscale[col - cg0];
+                        prow[col] = w.seg_first ? val : prow[col] + val;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);
+        };
+        if constexpr (kGrp == 4) {
+            // streaming the cache: group part_k takes items k = part_k mod 4
+            // (and so always the same ring slots and A stage); every group
+            // walks every item to keep the ring indices
+            int sd = 0, sa = 0, k = 0, nflush = 0;
+            uint32_t pd = 0, pa = 0;
+            for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
+                if ((k & 3) == part_k) {
+                    mbar_wait(&full_d[sd], pd);
+                    if (k >= NA) {
+                        mbar_wait(&empty_a[sa], pa ^ 1);
+                        tc_fence_after();
+                    }
+                    if (dbg != 1) {
+                        const unsigned char* slot = dring + sd * DB;
+                        const uint32_t ta = tmem_a + static_cast<uint32_t>(sa) * ACOLS + lane_off;
+#pragma unroll
+                        for (int t = 1; t <= SD; ++t) {
+                            uint32_t v[8];
+#pragma unroll
+                            for (int pp = 0; pp < 4; ++pp) {
+                                const uint2 u = *reinterpret_cast<const uint2*>(
+                                    slot + sdig_off(row, pp, t, SD));
+                                v[2 * pp] = u.x;
+                                v[2 * pp + 1] = u.y;
+                            }
+                            if (t <= TD_DIG) {
+                                tmem_st8(ta + static_cast<uint32_t>((t - 1) * 8), v);
+                            } else {
+#pragma unroll
+                                for (int pp = 0; pp < 4; ++pp)
+                                    *reinterpret_cast<uint2*>(aring + sa * ASB +
+                                                              umma_tile_off(row, pp * 8) +
+                                                              (t - TD_DIG - 1) * (kRowsI8 * kKStep)) =
+                                        make_uint2(v[2 * pp], v[2 * pp + 1]);
+                            }
+                        }
+                        tmem_st_wait();
+                        if constexpr (TD_DIG < SD) fence_proxy_async();
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&empty_d[sd]);
+                        mbar_arrive(&full_a[sa]);
+                    }
+                    if constexpr (CL > 1)
+                        if (lane >= 1 && lane < CL)
+                            mbar_arrive_peer(&empty_d[sd],
+                                             static_cast<uint32_t>((crank + lane) % CL));
+                }
+                if (++sd == ND) {
+                    sd = 0;
+                    pd ^= 1;
+                }
+                if (++sa == NA) {
+                    sa = 0;
+                    pa ^= 1;
+                }
+                if (w.last()) {
+                    // the chunk epilogues stay on group 0: a partial slot's
+                    // read-modify-writes of consecutive chunks of one row
+                    // block are then ordered by program order
+                    if (part_k == 0) epilogue(w, nflush);
+                    ++nflush;
+                }
+            }
+        } else {
         int cur_rb = -1;
         double sc = 0.0;
         int sd = 0, sa = 0, k = 0, nflush = 0;
@@ -656,7 +793,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     mbar_arrive(&full_a[sa]);
                 }
                 if constexpr (CL > 1)
-                    if (lane == 1) mbar_arrive_peer(&empty_d[sd], crank ^ 1);
+                    if (lane >= 1 && lane < CL)
+                        mbar_arrive_peer(&empty_d[sd], static_cast<uint32_t>((crank + lane) % CL));
             } else {
                 // single A stage: convert into registers while the MMAs of the
                 // previous k-step still read the stage, then store
@@ -702,7 +840,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                     mbar_arrive(&full_a[sa]);
                 }
                 if constexpr (CL > 1)
-                    if (lane == 1) mbar_arrive_peer(&empty_d[sd], crank ^ 1);
+                    if (lane >= 1 && lane < CL)
+                        mbar_arrive_peer(&empty_d[sd], static_cast<uint32_t>((crank + lane) % CL));
             }
             if (++sd == ND) {
                 sd = 0;
@@ -713,49 +852,10 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 pa ^= 1;
             }
             if (part_k == 0 && w.last()) {
-                // ---- epilogue: this warp's 32 TMEM lanes ----
-                mbar_wait(acc_full, static_cast<uint32_t>(nflush & 1));
-                tc_fence_after();
-                const int grow = w.rb * kRowsI8 + row;
-                double rscale;
-                if constexpr (SD == kDig) {
-                    const int e = grow < nrows ? row_exp[grow] : kExpZeroI8;
-                    rscale = e > kExpZeroI8 ? ldexp(1.0, e) : 0.0;
-                } else {
-                    rscale = grow < nrows ? 0x1.0p24 / (hlen * hlen) : 0.0;  // S = S' 2^-24 * this
-                }
-                double* prow = part +
-                               (static_cast<size_t>(cta) * maxseg + w.seg) * kRowsI8 * wp +
-                               static_cast<size_t>(row) * wp;
-#pragma unroll
-                for (int cb = 0; cb < NB / 16; ++cb) {
-                    double v[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = 0.0;
-#pragma unroll
-                    for (int dd = 2; dd <= 8; ++dd) {
-                        int32_t iv[16];
-                        tmem_ld16(tmem + lane_off + static_cast<uint32_t>((dd - 2) * NB + cb * 16),
-                                  iv);
-                        tmem_ld_wait();
-                        const double wgt = ldexp(1.0, -8 * dd);
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(iv[j]) * wgt;
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int col = cg0 + cb * 16 + j;
-                        if (col < wp) {
-                            const double val = v[j] * rscale * colscale[col - cg0];
-                            prow[col] = w.seg_first ? val : prow[col] + val;
-                        }
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(acc_empty);
+                epilogue(w, nflush);
                 ++nflush;
             }
+        }
         }
     }
     tc_fence_before();
@@ -871,6 +971,11 @@ void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned ch
             size_t bdig_stride, const int* row_exp, const int* col_exp, double* part, int cg0,
             cudaStream_t st, const int* skip, double hlen = 0.0, int k_off = 0, int dm = 0,
             unsigned char* sdig = nullptr, int nks_c = 0) {
+    if constexpr (CL > 2) {  // clusters wider than a pair only stream the cache
+        (void)dm;
+        run_i8_dm<NB, TD, SD, CL, 2>(tmap, p, wp, bdig, bdig_stride, row_exp, col_exp, part, cg0,
+                                     st, skip, hlen, k_off, sdig, nks_c);
+    } else {
     if (dm == 1)
         run_i8_dm<NB, TD, SD, CL, 1>(tmap, p, wp, bdig, bdig_stride, row_exp, col_exp, part, cg0,
                                      st, skip, hlen, k_off, sdig, nks_c);
@@ -880,12 +985,14 @@ void run_i8(const CUtensorMap* tmap, const K2iPlan& p, int wp, const unsigned ch
     else
         run_i8_dm<NB, TD, SD, CL, 0>(tmap, p, wp, bdig, bdig_stride, row_exp, col_exp, part, cg0,
                                      st, skip, hlen, k_off, nullptr, 0);
+    }
 }
 
-// Co-resident CTA pairs (clusters of 2 with one ~210 KB CTA per SM): at most
-// sms / 2, fewer when some GPC leaves an SM without a partner. Queried once
-// per device for the pair kernel's shared-memory footprint.
-int pair_units(int sms) {
+// Co-resident clusters of CL CTAs (one ~210 KB CTA per SM): at most sms / CL,
+// fewer when some GPC's SM count leaves SMs without a full cluster. Queried
+// once per device and kernel variant.
+template <int NB, typename TD, int SD, int CL, int DM>
+int cluster_units(int sms) {
     static std::mutex mu;
     static std::map<int, int> units;
     int dev = 0;
@@ -893,15 +1000,16 @@ int pair_units(int sms) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = units.find(dev);
     if (it != units.end()) return it->second;
-    const void* fn = reinterpret_cast<const void*>(k2i_product_ts<48, double, kDig, 2>);
-    ensure_dyn_smem(fn, ts_smem<48, double, kDig, 2>());
+    const void* fn = reinterpret_cast<const void*>(k2i_product_ts<NB, TD, SD, CL, DM>);
+    constexpr size_t smem = ts_smem<NB, TD, SD, CL, DM>();
+    ensure_dyn_smem(fn, smem);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(sms));
+    cfg.gridDim = dim3(static_cast<unsigned>(sms / CL * CL));
     cfg.blockDim = dim3(kThreadsI8);
-    cfg.dynamicSmemBytes = ts_smem<48, double, kDig, 2>();
+    cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -909,14 +1017,16 @@ int pair_units(int sms) {
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n <= 0) {
         cudaGetLastError();
-        n = sms / 2;
+        n = sms / CL;
     }
-    n = std::min(n, sms / 2);
+    n = std::min(n, sms / CL);
     if (const char* e = std::getenv("DSB_K2I_UNITS")) n = std::max(1, std::min(n, std::atoi(e)));
-    if (std::getenv("DSB_TRACE")) std::fprintf(stderr, "[k2i] CTA pairs co-resident: %d\n", n);
+    if (std::getenv("DSB_TRACE"))
+        std::fprintf(stderr, "[k2i] clusters of %d co-resident: %d\n", CL, n);
     units[dev] = n;
     return n;
 }
+int pair_units(int sms) { return cluster_units<48, double, kDig, 2, 0>(sms); }
 
 }  // namespace
 
@@ -967,6 +1077,62 @@ K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms) {
     p.maxseg = maxseg;
     p.part_elems = static_cast<size_t>(p.grid) * maxseg * kRowsI8 * wp;
     p.colmax_grid = sms;
+    p.cl = p.pair ? 2 : 1;
+    return p;
+}
+
+// DSB_K2I_STREAM_CL=1: the streaming passes of WP > 32 run on clusters of
+// 32-column groups (k2i_stream_plan). Off by default: measured slower than
+// the storing pass's own plan (C5 3.25 vs 2.37 ms, n = 40k w = 70 3.90 vs
+// 3.46 ms, w = 50 3.04 vs 2.71 ms per pass) — multicast at cluster sizes
+// <= 4 does not reduce the L2 -> SM traffic, and each CTA of a cluster still
+// takes in every item plus its own panel digits, now for twice the items.
+bool stream_clusters_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DSB_K2I_STREAM_CL");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+K2iPlan k2i_stream_plan(size_t nrows, size_t ncols, int wp, int sms, int sdigits) {
+    const int cl = std::min(4, (wp + 31) / 32);
+    if (cl <= 1 || !stream_clusters_enabled()) return k2i_plan(nrows, ncols, wp, sms);
+    K2iPlan p;
+    const size_t nks = (ncols + kKStep - 1) / kKStep;
+    p.cl = cl;
+    p.pair = true;
+    p.ngroups = cl;
+    for (int g = 0; g < cl; ++g) {
+        p.gc0[g] = 32 * g;
+        p.gnb[g] = 32;
+    }
+    p.nb = 32 * cl;
+    p.bdig_stride = nks * kDig * 32 * kKStep;
+    p.bdig_bytes = cl * p.bdig_stride;
+    int units = 0;
+    const bool ham = sdigits == 3;
+    switch (cl) {
+        case 2: units = ham ? cluster_units<32, double, 3, 2, 2>(sms)
+                            : cluster_units<32, double, kDig, 2, 2>(sms); break;
+        case 3: units = ham ? cluster_units<32, double, 3, 3, 2>(sms)
+                            : cluster_units<32, double, kDig, 3, 2>(sms); break;
+        default: units = ham ? cluster_units<32, double, 3, 4, 2>(sms)
+                             : cluster_units<32, double, kDig, 4, 2>(sms); break;
+    }
+    p.nrows = static_cast<int>(nrows);
+    p.nblk = static_cast<int>((nrows + kRowsI8 - 1) / kRowsI8);
+    p.nks = static_cast<int>(nks);
+    p.total = static_cast<long long>(p.nblk) * p.nks;
+    p.grid = static_cast<int>(std::min<long long>(units, p.total));
+    int maxseg = 1;
+    for (long long c = 0; c < p.grid; ++c) {
+        const long long a = p.total * c / p.grid, b = p.total * (c + 1) / p.grid;
+        if (b > a) maxseg = std::max<int>(maxseg, static_cast<int>((b - 1) / p.nks - a / p.nks + 1));
+    }
+    p.maxseg = maxseg;
+    p.part_elems = static_cast<size_t>(p.grid) * maxseg * kRowsI8 * wp;
+    p.colmax_grid = sms;
     return p;
 }
 
@@ -977,14 +1143,79 @@ size_t k2i_sdig_bytes(const K2iPlan& p, int sdigits) {
                                                                : sdig_item_bytes<kDig>());
 }
 
+namespace {
+// a streaming pass on a cluster plan (k2i_stream_plan): CL CTAs share every
+// digit item, CTA g computes panel columns 32 g .. 32 g + 31
+void launch_k2i_stream(const K2iPlan& p, int wp, const double* x, const int* col_exp,
+                       unsigned char* bdig, double* part, const double* row_mean,
+                       const double* scalars, const double* colsums, double* y,
+                       size_t y_rows_pad, const int* row_exp, cudaStream_t st, cudaEvent_t e0,
+                       cudaEvent_t e1, const int* skip, int hamming_len, unsigned char* sdig,
+                       int nks_c) {
+    const size_t r_done = static_cast<size_t>(p.nblk) * kRowsI8;
+    if (y_rows_pad > r_done)
+        DSB_CUDA(cudaMemsetAsync(y + r_done * wp, 0, (y_rows_pad - r_done) * wp * sizeof(double),
+                                 st));
+    for (int g = 0; g < p.cl; ++g) {
+        const long long items = static_cast<long long>(p.nks) * 32 * 8;
+        const int grid = static_cast<int>(std::min<long long>((items + 255) / 256, 4 * 148));
+        k_panel_digits<<<grid, 256, 0, st>>>(x, 0, p.nks, wp, 32, p.gc0[g], col_exp,
+                                             bdig + g * p.bdig_stride);
+    }
+    if (e0) record_timing_event(e0, st);
+    const double hl = static_cast<double>(hamming_len);
+    const size_t bs = p.bdig_stride;
+    // (the tensor map is unused when streaming)
+    static const CUtensorMap no_map{};
+    const CUtensorMap* tm = &no_map;
+    const bool ham = hamming_len > 0;
+    switch (p.cl) {
+        case 2:
+            if (ham)
+                run_i8<32, double, 3, 2>(tm, p, wp, bdig, bs, row_exp, col_exp, part, 0, st, skip,
+                                         hl, 0, 2, sdig, nks_c);
+            else
+                run_i8<32, double, kDig, 2>(tm, p, wp, bdig, bs, row_exp, col_exp, part, 0, st,
+                                            skip, 0.0, 0, 2, sdig, nks_c);
+            break;
+        case 3:
+            if (ham)
+                run_i8<32, double, 3, 3>(tm, p, wp, bdig, bs, row_exp, col_exp, part, 0, st, skip,
+                                         hl, 0, 2, sdig, nks_c);
+            else
+                run_i8<32, double, kDig, 3>(tm, p, wp, bdig, bs, row_exp, col_exp, part, 0, st,
+                                            skip, 0.0, 0, 2, sdig, nks_c);
+            break;
+        default:
+            if (ham)
+                run_i8<32, double, 3, 4>(tm, p, wp, bdig, bs, row_exp, col_exp, part, 0, st, skip,
+                                         hl, 0, 2, sdig, nks_c);
+            else
+                run_i8<32, double, kDig, 4>(tm, p, wp, bdig, bs, row_exp, col_exp, part, 0, st,
+                                            skip, 0.0, 0, 2, sdig, nks_c);
+            break;
+    }
+    count_launch(1 + p.cl);
+    if (e1) record_timing_event(e1, st);
+    launch_k2_reduce(wp, kRowsI8, part, p.maxseg, p.nks, p.total, p.grid, p.nrows, 1, row_mean,
+                     scalars, colsums, y, st, skip);
+    count_launch(1);
+}
+}  // namespace
+
 void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt, const K2iPlan& p,
                 int wp, const double* x, size_t x_rows_pad, const int* row_exp, double* pmax,
                 int* col_exp, unsigned char* bdig, double* part, const double* row_mean,
                 const double* scalars, const double* colsums, double* y, size_t y_rows_pad,
                 cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, const int* skip, int hamming_len,
-                unsigned char* sdig, int sdig_mode) {
+                unsigned char* sdig, int sdig_mode, const K2iPlan* stream_plan) {
     if (!sdig) sdig_mode = 0;
     const int nks_c = p.nks;
+    if (sdig_mode == 2 && stream_plan && stream_plan->cl > 1 && stream_plan->gnb[0] == 32) {
+        launch_k2i_stream(*stream_plan, wp, x, col_exp, bdig, part, row_mean, scalars, colsums, y,
+                          y_rows_pad, row_exp, st, e0, e1, skip, hamming_len, sdig, nks_c);
+        return;
+    }
     // k2_reduce writes the 128-row blocks; the panel rows beyond them (up to
     // the 256-row padding) must read as zero, whatever an earlier, larger
     // solve left in this workspace

@@ -128,9 +128,14 @@ struct K2iPlan {
     size_t bdig_bytes = 0;  // panel digit planes
     bool pair = false;      // w > 64: one pass by CTA pairs (a column group per CTA)
     size_t bdig_stride = 0; // pair: bytes between the two groups' digit planes
+    int cl = 1;             // CTAs per work unit (2: the pair; streaming plans up to 4)
 };
 bool k2i_supported(int wp);
 K2iPlan k2i_plan(size_t nrows, size_t ncols, int wp, int sms);
+// the plan of the passes that stream the S-digit cache: WP <= 32 as
+// k2i_plan, wider panels on clusters of ceil(WP / 32) <= 4 CTAs sharing every
+// digit item, one 32-column group per CTA (sdigits: 7, or 3 for Hamming)
+K2iPlan k2i_stream_plan(size_t nrows, size_t ncols, int wp, int sms, int sdigits);
 // the sharded product over k-step ranges of D's columns (panel all-gather
 // overlapped: ranges[0] needs only the local panel rows, the rest wait on
 // `gathered`), one stream-K split and slot set per range, one reduce
@@ -151,7 +156,7 @@ void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt,
                 const double* scalars, const double* colsums, double* y, size_t y_rows_pad,
                 cudaStream_t st, cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr,
                 const int* skip = nullptr, int hamming_len = 0, unsigned char* sdig = nullptr,
-                int sdig_mode = 0);
+                int sdig_mode = 0, const K2iPlan* stream_plan = nullptr);
 // bytes of the S-digit cache of a plan (sdigits: 7, or 3 for Hamming slices):
 // the solve's first product pass stores every (row block, k-step) item's
 // digit planes there (sdig_mode 1), the later passes stream them (mode 2)

@@ -365,6 +365,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     c.last_product_sdigits = use_i8 ? (hamming_i8 ? 3 : 7) : 0;
     c.last_product_pair = use_i8 && iplan.pair ? 1 : 0;
     c.last_product_sdig = 0;
+    c.last_product_stream_cl = 0;
     c.last_product_groups = use_i8 ? iplan.ngroups : 1;
     const size_t pbytes = n_pad * wp * 8;
     double* P0 = static_cast<double*>(c.scratch("panel0", pbytes));

@@ -225,24 +225,28 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     // dynamic range; the fp64 DMMA kernel otherwise
     const bool use_i8 = lazy && use_int8_product(*g.gram, wp);
     c.last_product_kernel = use_i8 ? 1 : 0;
-    K2iPlan iplan;
+    K2iPlan iplan, splan;
     double* pmax = nullptr;
     int* col_exp = nullptr;
     unsigned char* bdig = nullptr;
-    if (use_i8) {
-        iplan = k2i_plan(n, n, wp, c.sms);
-        pmax = static_cast<double*>(c.scratch(
-            "i8_pmax", static_cast<size_t>(panel_grid(n_pad, c.sms)) * wp * sizeof(double)));
-        col_exp = static_cast<int*>(c.scratch("i8_colexp", 128 * sizeof(int)));
-        bdig = static_cast<unsigned char*>(c.scratch("i8_bdig", iplan.bdig_bytes));
-    }
-    c.last_product_groups = use_i8 ? iplan.ngroups : 1;
     // Hamming distances (K7): three exact S bytes per element (h^2 < 2^24)
     const int hamming_i8 =
         (use_i8 && s.dt == DType::F64 && s.hamming_len > 0 && s.hamming_len < 4096 &&
          hamming_slices_enabled())
             ? s.hamming_len
             : 0;
+    if (use_i8) {
+        iplan = k2i_plan(n, n, wp, c.sms);
+        // the plan of the passes that stream the S-digit cache (when it is on)
+        splan = k2i_stream_plan(n, n, wp, c.sms, hamming_i8 ? 3 : 7);
+        pmax = static_cast<double*>(c.scratch(
+            "i8_pmax", static_cast<size_t>(panel_grid(n_pad, c.sms)) * wp * sizeof(double)));
+        col_exp = static_cast<int*>(c.scratch("i8_colexp", 128 * sizeof(int)));
+        bdig = static_cast<unsigned char*>(
+            c.scratch("i8_bdig", std::max(iplan.bdig_bytes, splan.bdig_bytes)));
+    }
+    const int i8_nb = std::max(iplan.nb, splan.nb);  // panel columns with int8 exponents
+    c.last_product_groups = use_i8 ? iplan.ngroups : 1;
     c.last_product_sdigits = use_i8 ? (hamming_i8 ? 3 : 7) : 0;
     c.last_product_pair = use_i8 && iplan.pair ? 1 : 0;
     const size_t pbytes = n_pad * wp * sizeof(double);
@@ -250,7 +254,9 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     double* P1 = static_cast<double*>(c.scratch("panel1", pbytes));
     double* P2 = static_cast<double*>(c.scratch("panel2", pbytes));
     double* part = static_cast<double*>(c.scratch(
-        "k2_part", std::max(plan.part_elems, use_i8 ? iplan.part_elems : 0) * sizeof(double)));
+        "k2_part",
+        std::max({plan.part_elems, use_i8 ? iplan.part_elems : 0, use_i8 ? splan.part_elems : 0}) *
+            sizeof(double)));
     const int pg = panel_grid(n_pad, c.sms);
     const size_t part_small =
         std::max<size_t>(static_cast<size_t>(pg) * wp * wp, static_cast<size_t>(pg) * 2 * wp);
@@ -331,6 +337,10 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         use_i8 ? k2_slot_table((static_cast<int>(n) + 127) / 128, iplan.nks, iplan.total, iplan.grid,
                                iplan.maxseg)
                : k2_slot_table(plan.nb, plan.nk, plan.total, plan.grid, plan.maxseg);
+    const int* slot_tab_s =
+        use_i8 ? k2_slot_table((static_cast<int>(n) + 127) / 128, splan.nks, splan.total,
+                               splan.grid, splan.maxseg)
+               : nullptr;
 
     // S-digit cache (k2i_product.cu, sdig_item_bytes): the first product
     // pass stores every item's S digit planes, the later passes stream them
@@ -351,6 +361,7 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
                 c.try_scratch("i8_sdig", k2i_sdig_bytes(iplan, hamming_i8 ? 3 : 7)));
     }
     c.last_product_sdig = sdig ? 1 : 0;
+    c.last_product_stream_cl = sdig ? splan.cl : 0;
     int sdig_pass = 0;
 
     // the solve as one stream sequence: eager, or captured once per signature
@@ -363,11 +374,11 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     auto product = [&](const double* x, double* y) {
         if (stats_ready) {
             // the orth kernel that produced x left its column statistics
-            launch_colstats_final(cstat, orth_fused_grid(n_pad, c.sms), wp, use_i8 ? iplan.nb : 0,
+            launch_colstats_final(cstat, orth_fused_grid(n_pad, c.sms), wp, use_i8 ? i8_nb : 0,
                                   colsums, use_i8 ? col_exp : nullptr, c.stream);
         } else if (use_i8) {
             launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream, pmax,
-                           iplan.nb, col_exp);
+                           i8_nb, col_exp);
         } else if (mode) {
             launch_colsums(x, row_mean, n, n_pad, wp, psmall, colsums, c.sms, c.stream);
         }
@@ -387,7 +398,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
             launch_k2i(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x, n_pad,
                        g.gram->row_exp->as<int>(), pmax,
                        col_exp, bdig, part, row_mean, scal_dev, colsums, y, n_pad, c.stream, e0,
-                       e1, nullptr, hamming_i8, sdig, sdig ? (sdig_pass++ == 0 ? 1 : 2) : 0);
+                       e1, nullptr, hamming_i8, sdig, sdig ? (sdig_pass++ == 0 ? 1 : 2) : 0,
+                       &splan);
         else
             launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums,
                       y, n_pad, c.stream, e0, e1);
@@ -503,7 +515,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
                                 static_cast<const void*>(eo.imeta), static_cast<const void*>(lp),
                                 static_cast<const void*>(res_out),
                                 static_cast<const void*>(&meta),
-                                static_cast<const void*>(slot_tab)})
+                                static_cast<const void*>(slot_tab),
+                                static_cast<const void*>(slot_tab_s)})
             mixp(ptr);
         auto it = c.graphs.find(h);
         if (it != c.graphs.end()) {

@@ -1,14 +1,20 @@
 """S-digit cache of the int8 product (k2i_product.cu, sdig_item_bytes): the
 solve's first product pass stores every (row block, k-step) item's digit
 planes of D o D, the later passes stream them instead of D. The digits are
-the same bytes the converters would produce, so a solve with the cache must
-be BIT-identical to one without it — on every kernel variant the cache
-feeds: the single-CTA NB = 32 / 64 groups, the CTA pair (multicast halves),
-the Hamming 3-byte slices, f32 D, two column groups in one pass (the first
-group stores, the second streams), ragged n and the int32 chunk edge.
+the same bytes the converters would produce, so a solve with the cache is
+BIT-identical to one without it when every pass runs the same plan, and
+equal to the fp64 summation-order level when the streaming passes run on
+clusters (another stream-K split) — on every kernel variant the cache
+feeds: the single-CTA NB = 32 / 64 groups and the CTA pair storing it, the
+streaming clusters of 2, 3 and 4 CTAs (multicast items, one 32-column group
+per CTA), the Hamming 3-byte slices, f32 D, two column groups in one storing
+pass (the first group stores, the second streams), ragged n and the int32
+chunk edge.
 The oracle comparison (ref src/rsvd.cpp:81-145, mds.cpp:81-124) runs on the
 cached path of each case as well.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -56,8 +62,23 @@ def test_sdig_cache_bit_identical(ds, oracle, kind, n, rank, over, pair, sdigits
     on, st1 = _solve(ds, g, rank, over, 2, 3, 2)
     assert st1.last_product_kernel == 1 and st1.last_product_sdig == 1
     assert (st1.last_product_pair, st1.last_product_sdigits) == (pair, sdigits)
-    assert np.array_equal(on.eigenvalues, off.eigenvalues)
-    assert np.array_equal(on.coords, off.coords)
+    # the streaming passes run on the storing pass's plan (the pair for
+    # 64 < WP <= 96), or with DSB_K2I_STREAM_CL=1 on clusters of
+    # ceil(WP / 32) CTAs sharing each digit item (one 32-column group per CTA)
+    wp = (rank + over + 7) // 8 * 8
+    want_cl = min(4, (wp + 31) // 32) if os.environ.get("DSB_K2I_STREAM_CL") == "1" else \
+        (2 if pair else 1)
+    assert st1.last_product_stream_cl == want_cl
+    if os.environ.get("DSB_K2I_STREAM_CL") != "1":
+        # same plan for every pass: bit-identical
+        assert np.array_equal(on.eigenvalues, off.eigenvalues)
+        assert np.array_equal(on.coords, off.coords)
+    else:
+        # the streaming clusters split the rows' column range differently,
+        # so the fp64 partial slots are summed in another order
+        np.testing.assert_allclose(on.eigenvalues, off.eigenvalues, rtol=1e-10,
+                                   atol=1e-13 * abs(off.eigenvalues[0]))
+        assert coords_match_up_to_sign(on.coords, off.coords) < 1e-9 * np.sqrt(off.eigenvalues[0])
     # a second cached solve (graph replay) stores and streams again
     again, _ = _solve(ds, g, rank, over, 2, 3, 2)
     assert np.array_equal(again.coords, on.coords)
@@ -80,7 +101,10 @@ def test_sdig_cache_chunk_edge(ds, oracle):
     off, _ = _solve(ds, g, 40, 10, 1, 9, 0)
     on, st = _solve(ds, g, 40, 10, 1, 9, 2)
     assert st.last_product_sdig == 1
-    assert np.array_equal(on.coords, off.coords)
+    if os.environ.get("DSB_K2I_STREAM_CL") != "1":
+        assert np.array_equal(on.coords, off.coords)
+    else:
+        assert coords_match_up_to_sign(on.coords, off.coords) < 1e-9 * np.sqrt(off.eigenvalues[0])
 
 
 def test_sdig_cache_auto_policy(ds):
