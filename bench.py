@@ -434,6 +434,8 @@ def b200_arm(args, wl):
         try:
             tv = json.loads(tp.read_text()).get(wl)
             traffic = tv.get(kname) if isinstance(tv, dict) else (None if int8_path else tv)
+            if store_pass is not None and isinstance(tv, dict):
+                store_pass["traffic"] = tv.get("k2i_product_store")
         except Exception:
             traffic = None
     hbm = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,

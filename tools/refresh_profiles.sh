@@ -1,9 +1,10 @@
 #!/bin/bash
 # Round measurement set (run on a B200 box via gpurun): bench lines for
-# C1/C2/C3/C5 and the reference arm, the launch lists of the C1 and C2 bench
-# commands, one full ncu capture of the C2 product kernel, of the CTA-pair
-# product kernel (w = 70) and of the K7 tensor-core Hamming builder (n = 50k).
-# Outputs in gpurun_out/ (copied to profiles/ by hand).
+# C1/C2/C3/C4/C5 and the reference arm, the launch list of the C2 bench
+# command, full ncu captures of the C2 product kernel (a streaming pass of the
+# S-digit cache and the storing pass), of the C5 streaming pass, of the
+# CTA-pair kernel (w = 70) and of the K7 tensor-core Hamming builder.
+# Outputs in gpurun_out/ (copied to profiles/ by tools/collect_profiles.py).
 set -u
 O=gpurun_out
 mkdir -p $O
@@ -21,13 +22,18 @@ python bench.py --workload C1 --steps 2 --warmup 3 --no-cpu-baseline > $O/plain_
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/launches_c1.csv python bench.py --workload C1 --steps 2 --warmup 3 \
     --no-cpu-baseline > $O/ncu_launches_c1.log 2>&1
+# k2i_time: one solve (launch 0 stores the cache, 1-5 stream it), then timed solves
 python tools/k2i_time.py C2 > $O/plain_k2i.txt 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:k2i_product_ts -s 2 -c 1 \
-    -o $O/k2i_c2 -f python tools/k2i_time.py C2 > $O/ncu_k2i.log 2>&1
+    -o $O/k2i_c2_stream -f python tools/k2i_time.py C2 > $O/ncu_k2i.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:k2i_product_ts -s 0 -c 1 \
+    -o $O/k2i_c2_store -f python tools/k2i_time.py C2 > $O/ncu_k2i_store.log 2>&1
+python tools/k2i_time.py C5 > $O/plain_k2i_c5.txt 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:k2i_product_ts -s 2 -c 1 \
+    -o $O/k2i_c5_stream -f python tools/k2i_time.py C5 > $O/ncu_k2i_c5.log 2>&1
 python tools/k2i_probe.py 40000 50 20 > $O/plain_pair.txt 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:k2i_product_ts -s 2 -c 1 \
     -o $O/k2i_pair -f python tools/k2i_probe.py 40000 50 20 > $O/ncu_pair.log 2>&1
-python tools/k7_time.py 50000 > $O/plain_k7.txt 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:k_hamming_tc -c 1 \
-    -o $O/k7_tc -f python tools/k7_time.py 50000 > $O/ncu_k7.log 2>&1
+for a in "20000 20 10" "50000 30 20 ham" "40000 50 20" "40000 40 10"; do
+    python tools/k2i_passes.py $a; done > $O/k2i_passes.txt 2>&1
 echo done
