@@ -60,16 +60,6 @@ __device__ __forceinline__ void jacobi_rot2(double app, double aqq, double apq, 
     if (fabs(apq) >= 1e-300) {
         const double d = aqq - app;
         const double a2 = apq + apq;
-        if (fabs(a2) <= 0x1p-27 * fabs(d)) {
-            // small angle (the late sweeps): a2^2 is below half an ulp of d^2,
-            // so sqrt(d^2 + a2^2) = |d| and t^2 < 2^-56 leaves c = 1 exactly —
-            // the same rotation from one reciprocal instead of the
-            // rsqrt -> rcp -> rsqrt chain
-            double t = a2 * rcp_nr(fabs(d) + fabs(d));
-            if (d < 0.0) t = -t;
-            s = t;
-            return;
-        }
         const double h2 = fma(d, d, a2 * a2);
         const double r = h2 * rsqrt_nr(h2);  // sqrt(d^2 + 4 a_pq^2)
         double t = a2 * rcp_nr(fabs(d) + r);
