@@ -409,13 +409,18 @@ def b200_arm(args, wl):
     # and stores the digit planes of D o D (SD bytes per element of each
     # 128-row x 32-column item), the other 2q+1 passes — the dominant kernel —
     # stream those planes instead of D
-    sdig = int(st.last_product_kernel) == 1 and int(st.last_product_sdig) == 1
+    # (last_product_sdig 2: K1 — pass 0, the gram — wrote the planes while
+    # reading D, and every product pass streams them)
+    sdig_mode = int(st.last_product_sdig) if int(st.last_product_kernel) == 1 else 0
+    sdig = sdig_mode >= 1
     store_pass = None
-    if sdig:
+    item_bytes = ((m_rows + 127) // 128) * ((n + 31) // 32) * int(st.last_product_sdigits) * 4096
+    if sdig_mode == 2:
+        bytes_per_launch = item_bytes + n * w * 8 + m_rows * w * 8 + m_rows * 8
+    if sdig_mode == 1:
         nfirst = max(int(st.product_first_launches), 1)
         first_ms = st.product_first_ms / nfirst
         k2_ms = (st.product_ms - st.product_first_ms) / max(int(st.product_launches) - nfirst, 1)
-        item_bytes = ((m_rows + 127) // 128) * ((n + 31) // 32) * int(st.last_product_sdigits) * 4096
         d_bytes = m_rows * n * (4 if f32 else 8)
         bytes_per_launch = item_bytes + n * w * 8 + m_rows * w * 8 + m_rows * 8
         store_bytes = d_bytes + item_bytes + n * w * 8 + m_rows * w * 8 + m_rows * 8
@@ -442,11 +447,15 @@ def b200_arm(args, wl):
            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
            else "fallback 6650 GB/s (B200_PROFILING.md)"}
     common = {"k2_avg_ms": k2_ms, "k2_launches": int(st.product_launches),
-              "sdig_cache": sdig, "store_pass": store_pass,
+              "sdig_cache": ("written by K1 (pass 0)" if sdig_mode == 2 else
+                             "stored by the first product pass" if sdig_mode == 1 else None),
+              "store_pass": store_pass,
               "flops_per_launch": flops_per_launch, "bytes_per_launch": bytes_per_launch,
               "pass0": {"k1_avg_ms": st.stats_ms / max(st.stats_launches, 1),
-                        "achieved_gbs": m_rows * n * (4 if f32 else 8) /
-                        (st.stats_ms / max(st.stats_launches, 1) * 1e-3) / 1e9}}
+                        "achieved_gbs": (m_rows * n * (4 if f32 else 8) +
+                                         (item_bytes if sdig_mode == 2 else 0)) /
+                        (st.stats_ms / max(st.stats_launches, 1) * 1e-3) / 1e9,
+                        "writes_digit_planes_bytes": item_bytes if sdig_mode == 2 else 0}}
     if int8_path:
         # exact integer slice product on the int8 tensor cores: one read of D
         # per column group (w <= 64: one group), HBM-bound; `achieved` counts
@@ -473,7 +482,7 @@ def b200_arm(args, wl):
                     "kernel": ("k2i_product (3x7-digit int8 slice product of the exact Hamming "
                                "h^2, tcgen05 kind::i8)" if int(st.last_product_sdigits) == 3 else
                                "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)") +
-                              (", streaming the S-digit cache (passes 2..)" if sdig else ""),
+                              (", streaming the S-digit cache" if sdig else ""),
                     "peak_source": hbm["peak_source"],
                     "column_groups": groups,
                     "reads_of_D_per_pass": 1 if int(st.last_product_pair) else groups,

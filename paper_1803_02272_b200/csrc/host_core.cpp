@@ -256,6 +256,7 @@ bool Ctx::evict_scratch() {
         if (evictable_slot(it->first)) {
             if (!any) DSB_CUDA(cudaStreamSynchronize(stream));
             clear_graphs();  // they address the slot
+            ++sdig_gen;      // a gram's K1 digits are gone with it
             it = arena_.erase(it);
             any = true;
         } else {
@@ -264,6 +265,20 @@ bool Ctx::evict_scratch() {
     }
     if (any) DSB_CUDA(cudaStreamSynchronize(stream));
     return any;
+}
+
+// debug: copy the first `bytes` of the S-digit cache slot to host memory
+extern "C" int divscope_debug_sdig_read(void* host, size_t bytes) {
+    try {
+        Ctx& c = Ctx::get();
+        void* p = c.try_scratch("i8_sdig", 0);
+        if (!p) return -1;
+        DSB_CUDA(cudaStreamSynchronize(c.stream));
+        DSB_CUDA(cudaMemcpy(host, p, bytes, cudaMemcpyDeviceToHost));
+        return 0;
+    } catch (...) {
+        return -2;
+    }
 }
 
 void* Ctx::pinned_scratch(const std::string& name, size_t bytes) {

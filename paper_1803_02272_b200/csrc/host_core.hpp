@@ -147,7 +147,10 @@ public:
     int last_product_kernel = 0;  // 0 fp64 DMMA, 1 int8 slice product
     int last_product_groups = 1;  // int8 column groups (reads of D per pass)
     int last_product_sdigits = 0;  // int8 S slices per element (7, or 3 for Hamming D)
-    int last_product_sdig = 0;     // int8: the S-digit cache fed passes 2.. of the last solve
+    int last_product_sdig = 0;     // int8 S-digit cache: 1 stored by the first pass, 2 by K1
+    // generation of the "i8_sdig" slot's contents: bumped whenever K1 or a
+    // storing pass writes it and when it is evicted
+    uint64_t sdig_gen = 0;
     int last_product_stream_cl = 0;  // CTAs per cluster of those streaming passes
     int last_product_pair = 0;     // int8: the CTA-pair kernel (one read of D for two groups)
     std::vector<TimedPair> pending;
@@ -240,6 +243,13 @@ struct GramInfo {
     std::vector<double> row_mean_h;       // host copy (for _get / _write)
     std::shared_ptr<DevBuf> scalars;      // [S_COUNT]
     double sc[S_COUNT] = {};
+    // S-digit cache written by this gram's K1 pass: its generation (matches
+    // Ctx::sdig_gen while the "i8_sdig" slot still holds it; 0 = none), the
+    // digits per element (7 or 3) and, for 7, the bound row exponents the
+    // digits are scaled by
+    uint64_t sdig_gen = 0;
+    int sdig_sd = 0;
+    std::shared_ptr<DevBuf> row_eb;
     std::mutex mu;
 };
 

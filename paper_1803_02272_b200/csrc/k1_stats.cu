@@ -16,6 +16,7 @@
 
 #include "device_utils.cuh"
 #include "kernels.cuh"
+#include "sdig.cuh"
 
 namespace dsb {
 
@@ -90,6 +91,11 @@ struct K1Cfg {
     static constexpr int STAGES = (192 * 1024) / STAGE;
 };
 
+template <typename T>
+struct C_EL_IS_16 {
+    static constexpr bool value = K1Cfg<T>::EL == 16 && K1Cfg<T>::H == 1;
+};
+
 // element (r, c) of a swizzled tile (box-major)
 template <typename T>
 __device__ __forceinline__ const T* tile_at(const unsigned char* tile, int r, int c) {
@@ -116,11 +122,55 @@ __device__ __forceinline__ int exp_above_hi(uint32_t hmax) {
     return be - 1022;
 }
 
-template <typename T>
+// K1 writing the S-digit cache: the 16 values v of tile row r, tile columns
+// 16 q .. 16 q + 15, of the 64 x 64 tile (tr, tc) -> item (tr / 2, 2 tc +
+// q / 2), half tr % 2, converter parts 2 (q % 2) + {0, 1} (sdig.cuh layout).
+// DG = 7: the 56-bit fixed point of v^2 relative to 2^e (sc = 2^(56 - e)),
+// as the product's converters form it; DG = 3: the bytes of h^2, h = L v.
+template <int DG>
+__device__ __forceinline__ void k1_write_digits(unsigned char* __restrict__ sdig, int nks, int tr,
+                                                int tc, int r, int q, const double (&v)[16],
+                                                double sc, double hlen) {
+    const int ks = 2 * tc + (q >> 1);
+    if (ks >= nks) return;  // the last tile's padding columns past the last k-step
+    const size_t item = static_cast<size_t>(tr >> 1) * nks + ks;
+    unsigned char* base =
+        sdig + item * sdig_item_bytes<DG>() + (tr & 1) * DG * 2048 + r * 8 + (q & 1) * 2 * 512;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        uint32_t w[DG][2];
+        if constexpr (DG == 7) {
+            uint32_t lo[8], hi[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const unsigned long long m = __double2ull_rz((v[8 * g + j] * v[8 * g + j]) * sc);
+                lo[j] = static_cast<uint32_t>(m);
+                hi[j] = static_cast<uint32_t>(m >> 32);
+            }
+            pack_digits(lo, hi, w);
+        } else {
+            uint32_t s2[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t h = static_cast<uint32_t>(__double2int_rn(v[8 * g + j] * hlen));
+                s2[j] = h * h;
+            }
+            pack_digits3(s2, w);
+        }
+#pragma unroll
+        for (int t = 1; t <= DG; ++t)
+            *reinterpret_cast<uint2*>(base + ((t - 1) * 4 + g) * 512) = make_uint2(w[t - 1][0],
+                                                                                  w[t - 1][1]);
+    }
+}
+
+template <typename T, int DG>
 __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
     k1_tile_pairs(const __grid_constant__ CUtensorMap tm, int n, int nbt,
                   double* __restrict__ part, int* __restrict__ pexp, size_t part_ld,
-                  double* __restrict__ cta_stats) {
+                  double* __restrict__ cta_stats, unsigned char* __restrict__ sdig,
+                  const int* __restrict__ row_eb, int nks, double hlen) {
+    static_assert(DG == 0 || (sizeof(T) == 8 && C_EL_IS_16<T>::value), "digits: f64 tiles");
     using C = K1Cfg<T>;
     extern __shared__ __align__(1024) unsigned char k1_raw[];
     unsigned char* sm = k1_raw + ((1024u - (smem_u32(k1_raw) & 1023u)) & 1023u);
@@ -267,6 +317,15 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
         }
         double rs = (rsp[0] + rsp[1]) + (rsp[2] + rsp[3]);
         sum4 += (s4p[0] + s4p[1]) + (s4p[2] + s4p[3]);
+        if constexpr (DG != 0) {
+            double sc = 0.0;
+            if constexpr (DG == 7) {
+                const int gr = I * kT + r;
+                const int e = gr < n ? row_eb[gr] : kExpZero;
+                sc = e > kExpZero ? ldexp(1.0, 56 - e) : 0.0;
+            }
+            k1_write_digits<DG>(sdig, nks, I, J, r, q, a, sc, hlen);
+        }
         rs += __shfl_xor_sync(0xffffffffu, rs, 8);
         rs += __shfl_xor_sync(0xffffffffu, rs, 16);
         rmx = max(rmx, __shfl_xor_sync(0xffffffffu, rmx, 8));
@@ -311,6 +370,18 @@ __global__ void __launch_bounds__(K1Cfg<T>::THREADS, 1)
                 const double m = static_cast<double>(bmaxf);
                 bmx = hi_bits(m * m);
                 maxf = fmaxf(maxf, bmaxf);
+            }
+            if constexpr (DG != 0) {
+                double bd[C::EL];
+#pragma unroll
+                for (int j = 0; j < C::EL; ++j) bd[j] = static_cast<double>(bv[j]);
+                double sc = 0.0;
+                if constexpr (DG == 7) {
+                    const int gr = J * kT + r;
+                    const int e = gr < n ? row_eb[gr] : kExpZero;
+                    sc = e > kExpZero ? ldexp(1.0, 56 - e) : 0.0;
+                }
+                k1_write_digits<DG>(sdig, nks, J, I, r, q, bd, sc, hlen);
             }
             double rb = (rbp[0] + rbp[1]) + (rbp[2] + rbp[3]);
             sum4 += (b4p[0] + b4p[1]) + (b4p[2] + b4p[3]);
@@ -472,6 +543,39 @@ __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ ct
     }
 }
 
+// row_eb from row 0 of D: max_j d_ij <= d_i0 + d_0j <= |d_0i| + M0 (triangle
+// inequality, d_i0 = d_0i), M0 = max_j |d_0j| (NaN-ignoring selects, as K1);
+// the sum and square rounded up
+__global__ void __launch_bounds__(1024) k_row0_bound(const double* __restrict__ d0, int n,
+                                                     int* __restrict__ row_eb) {
+    __shared__ double red[32];
+    double m = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) m = max_keep(m, fabs(d0[j]));
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    double m0 = 0.0;
+    for (int w = 0; w < 32; ++w) m0 = max_keep(m0, red[w]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double b = __dadd_ru(fabs(d0[i]), m0);
+        row_eb[i] = exp_above_hi(hi_bits(__dmul_ru(b, b)));
+    }
+}
+
+// the bound exponents must cover every row's true exponent, and stay within
+// 3 bits of it (the digits keep >= 53 bits relative to the row maximum)
+__global__ void __launch_bounds__(1024) k_sdig_check(const int* __restrict__ row_exp,
+                                                     const int* __restrict__ row_eb, int n,
+                                                     double* __restrict__ scalars) {
+    int bad = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int e = row_exp[i], eb = row_eb[i];
+        if (e > eb || (e > kExpZero && eb - e > 3)) bad = 1;
+    }
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) scalars[S_SDIG_BAD] = bad ? 1.0 : 0.0;
+}
+
 }  // namespace
 
 size_t k1_part_elems(size_t n) {
@@ -487,18 +591,30 @@ int k1_grid(size_t n, int sms) {
 }
 
 void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, double* row_mean,
-               int* row_exp, double* scalars, int sms, cudaStream_t st) {
+               int* row_exp, double* scalars, int sms, cudaStream_t st, const K1Digits* dig) {
     (void)sms;
     const int nbt = static_cast<int>((n + kT - 1) / kT);
     const size_t part_ld = static_cast<size_t>(nbt) * kT;
+    const int dg = (dig && dig->sdig && dt == DType::F64) ? dig->sd : 0;
+    auto run64 = [&](auto kern) {
+        ensure_dyn_smem(reinterpret_cast<const void*>(kern), k1_smem<double>());
+        kern<<<w.grid, K1Cfg<double>::THREADS, k1_smem<double>(), st>>>(
+            *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats,
+            dg ? dig->sdig : nullptr, dg == 7 ? dig->row_eb : nullptr, dg ? dig->nks : 0,
+            dg == 3 ? dig->hlen : 0.0);
+    };
     if (dt == DType::F64) {
-        ensure_dyn_smem(reinterpret_cast<const void*>(k1_tile_pairs<double>), k1_smem<double>());
-        k1_tile_pairs<double><<<w.grid, K1Cfg<double>::THREADS, k1_smem<double>(), st>>>(
-            *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
+        if (dg == 7)
+            run64(k1_tile_pairs<double, 7>);
+        else if (dg == 3)
+            run64(k1_tile_pairs<double, 3>);
+        else
+            run64(k1_tile_pairs<double, 0>);
     } else {
-        ensure_dyn_smem(reinterpret_cast<const void*>(k1_tile_pairs<float>), k1_smem<float>());
-        k1_tile_pairs<float><<<w.grid, K1Cfg<float>::THREADS, k1_smem<float>(), st>>>(
-            *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats);
+        ensure_dyn_smem(reinterpret_cast<const void*>(k1_tile_pairs<float, 0>), k1_smem<float>());
+        k1_tile_pairs<float, 0><<<w.grid, K1Cfg<float>::THREADS, k1_smem<float>(), st>>>(
+            *tmap64, static_cast<int>(n), nbt, w.part, w.pexp, part_ld, w.cta_stats, nullptr,
+            nullptr, 0, 0.0);
     }
     const int nblk = static_cast<int>((n + kRmRows - 1) / kRmRows);
     const int nparts = nbt * (dt == DType::F64 ? K1Cfg<double>::H : K1Cfg<float>::H);
@@ -507,6 +623,15 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
     k1_finalize<<<1, 256, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),
                                    scalars);
     count_launch(3);
+    if (dg == 7) {
+        k_sdig_check<<<1, 1024, 0, st>>>(row_exp, dig->row_eb, static_cast<int>(n), scalars);
+        count_launch(1);
+    }
+}
+
+void launch_row0_bound(const double* d, size_t n, int* row_eb, cudaStream_t st) {
+    k_row0_bound<<<1, 1024, 0, st>>>(d, static_cast<int>(n), row_eb);
+    count_launch(1);
 }
 
 }  // namespace dsb

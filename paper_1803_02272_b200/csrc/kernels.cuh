@@ -27,6 +27,8 @@ enum Scalar : int {
     S_SUMR = 7,        // sum_i r_i
     S_SUMR2 = 8,       // sum_i r_i^2
     S_ROWRATIO = 9,    // max_i 2^e_i / r_i (row max of d^2 over row mean, bound)
+    S_SDIG_BAD = 10,   // K1 digits: 1 when a bound exponent is below a row's true
+                       // exponent or more than 3 above it (the digits are unused)
     S_COUNT = 16,
 };
 
@@ -45,8 +47,23 @@ size_t k1_part_elems(size_t n);
 int k1_grid(size_t n, int sms);
 // tmap64: TMA descriptor of D with 64-row x 128-byte boxes (SWIZZLE_128B)
 // row_exp[i]: smallest e with d_ij^2 < 2^e for all j (the int8 slice scale)
+// K1 writing the S-digit cache (f64 D): sd = 7 with row exponents row_eb
+// (a bound from row 0, launch_row0_bound) or sd = 3 for Hamming D (hlen = L);
+// nks = ceil(n / 32) k-steps per row block
+struct K1Digits {
+    unsigned char* sdig = nullptr;
+    int* row_eb = nullptr;
+    int nks = 0;
+    int sd = 0;
+    double hlen = 0.0;
+};
 void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, double* row_mean,
-               int* row_exp, double* scalars, int sms, cudaStream_t st);
+               int* row_exp, double* scalars, int sms, cudaStream_t st,
+               const K1Digits* dig = nullptr);
+// row_eb[i] = smallest e with (|d_0i| + max_j |d_0j|)^2 < 2^e, rounded up: by
+// the triangle inequality a bound on row i's max d_ij^2 for a metric D (K1
+// verifies it: scalars[S_SDIG_BAD])
+void launch_row0_bound(const double* d, size_t n, int* row_eb, cudaStream_t st);
 
 // ---- K1 for a row shard (rectangular rows x cols block): row sums of d^2,
 // sum d^4 and max |d| (deterministic per-CTA partials), plus the shard's

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <thread>
 #include <atomic>
 #include <cmath>
@@ -30,7 +31,10 @@ struct StatsOut {
 };
 
 // K1 over a store; returns scalars (host) plus device scalars/row means.
-StatsOut run_k1(Store& s) {
+// claim_digits (lazy grams of f64 D): called after every other allocation of
+// the pass (a failed one would evict the cache slot) to set up the S-digit
+// cache K1 writes; returns nullptr when there is none
+StatsOut run_k1(Store& s, const std::function<const K1Digits*()>& claim_digits = nullptr) {
     Ctx& c = Ctx::get();
     {
         std::lock_guard<std::mutex> lk(s.mu);
@@ -54,8 +58,10 @@ StatsOut run_k1(Store& s) {
     DSB_CUDA(cudaMemsetAsync(o.scalars->p, 0, S_COUNT * sizeof(double), c.stream));
     cudaEvent_t ev;
     c.begin_timed(0, &ev);
+    const K1Digits* dig = claim_digits ? claim_digits() : nullptr;
+    if (dig && dig->row_eb) launch_row0_bound(s.buf->as<double>(), n, dig->row_eb, c.stream);
     launch_k1(&s.tmap64, s.dt, n, w, o.row_mean->as<double>(), o.row_exp->as<int>(),
-              o.scalars->as<double>(), c.sms, c.stream);
+              o.scalars->as<double>(), c.sms, c.stream, dig);
     c.end_timed(0, ev);
     DSB_CUDA(cudaGetLastError());
     c.d2h_copy(o.sc, o.scalars->p, S_COUNT * sizeof(double));
@@ -354,13 +360,25 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     // DSB_SDIG / divscope_set_sdig_cache: 0 off, 1 auto (default: on when it
     // fits), 2 on.
     unsigned char* sdig = nullptr;
+    // the gram's K1 pass already wrote the digits (and nothing has written
+    // or evicted the slot since): every pass streams them
+    const bool k1dig = use_i8 && sdig_policy() > 0 && g.gram->sdig_gen != 0 &&
+                       g.gram->sdig_gen == c.sdig_gen &&
+                       g.gram->sdig_sd == (hamming_i8 ? 3 : 7);
     if (use_i8) {
         const int pol = sdig_policy();
         if (pol > 0)
             sdig = static_cast<unsigned char*>(
                 c.try_scratch("i8_sdig", k2i_sdig_bytes(iplan, hamming_i8 ? 3 : 7)));
     }
-    c.last_product_sdig = sdig ? 1 : 0;
+    const bool stores = sdig && !k1dig;
+    if (stores) ++c.sdig_gen;  // this solve's first pass overwrites the slot
+    // the row exponents the product scales by: the digits' own
+    const int* prod_row_exp =
+        !use_i8 ? nullptr
+                : (k1dig && g.gram->sdig_sd == 7 ? g.gram->row_eb->as<int>()
+                                                 : g.gram->row_exp->as<int>());
+    c.last_product_sdig = sdig ? (k1dig ? 2 : 1) : 0;
     c.last_product_stream_cl = sdig ? splan.cl : 0;
     int sdig_pass = 0;
 
@@ -396,9 +414,10 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         }
         if (use_i8)
             launch_k2i(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x, n_pad,
-                       g.gram->row_exp->as<int>(), pmax,
+                       prod_row_exp, pmax,
                        col_exp, bdig, part, row_mean, scal_dev, colsums, y, n_pad, c.stream, e0,
-                       e1, nullptr, hamming_i8, sdig, sdig ? (sdig_pass++ == 0 ? 1 : 2) : 0,
+                       e1, nullptr, hamming_i8, sdig,
+                       sdig ? ((k1dig || sdig_pass++ > 0) ? 2 : 1) : 0,
                        &splan);
         else
             launch_k2(s.tmap_for(plan.bm), s.dt, mode, plan, x, part, row_mean, scal_dev, colsums,
@@ -498,6 +517,8 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         mix(static_cast<uint64_t>(product_path()));
         mixp(s.buf ? s.buf->p : nullptr); mixp(scal_dev); mixp(row_mean);
         mixp(use_i8 ? g.gram->row_exp->p : nullptr);
+        mixp(prod_row_exp);
+        mix(k1dig);
         for (const void* ptr : {static_cast<const void*>(P0), static_cast<const void*>(P1),
                                 static_cast<const void*>(P2), static_cast<const void*>(part),
                                 static_cast<const void*>(psmall),
@@ -642,7 +663,35 @@ Matrix gram_from_distances(const Matrix& d) {
         throw Error(errc::not_symmetric, "gram matrix requires a symmetric distance matrix");
     const size_t n = s.rows;
     if (n == 0) throw Error(errc::empty_input, "empty distance matrix");
-    StatsOut o = run_k1(s);
+    // K1 also writes the S-digit cache when the solves on this gram will run
+    // the int8 product (f64 D, n >= 4096, unsharded) and the cache fits: the
+    // row exponents of the digits are then a bound from row 0 (verified by
+    // K1 against the true ones); Hamming slices need none
+    K1Digits dig;
+    std::shared_ptr<DevBuf> row_eb;
+    const int ham_sd = (s.hamming_len > 0 && s.hamming_len < 4096 && hamming_slices_enabled());
+    auto claim = [&]() -> const K1Digits* {
+        if (!(s.dt == DType::F64 && !s.sharded && n >= 4096 && sdig_policy() > 0 &&
+              product_path() != 1))
+            return nullptr;
+        const size_t nblk = (n + 127) / 128, nks = (n + 31) / 32;
+        dig.sd = ham_sd ? 3 : 7;
+        dig.nks = static_cast<int>(nks);
+        dig.hlen = static_cast<double>(s.hamming_len);
+        if (dig.sd == 7) {
+            row_eb = std::make_shared<DevBuf>(n * sizeof(int));
+            dig.row_eb = row_eb->as<int>();
+        }
+        dig.sdig = static_cast<unsigned char*>(
+            c.try_scratch("i8_sdig", nblk * nks * static_cast<size_t>(dig.sd) * 4096));
+        return dig.sdig ? &dig : nullptr;
+    };
+    StatsOut o = run_k1(s, claim);
+    uint64_t gen = 0;
+    if (dig.sdig) {
+        gen = ++c.sdig_gen;  // whatever the slot held before is overwritten
+        if (dig.sd == 7 && o.sc[S_SDIG_BAD] != 0.0) gen = 0;  // bound failed: unused
+    }
     // ref mds.cpp:21-27
     if (o.sc[S_MAXASYM] > 1e-12 * std::max(1.0, o.sc[S_MAXABS]))
         throw Error(errc::not_symmetric, "distance matrix values are not symmetric");
@@ -654,6 +703,9 @@ Matrix gram_from_distances(const Matrix& d) {
     g.gram->row_exp = o.row_exp;
     g.gram->scalars = o.scalars;
     std::memcpy(g.gram->sc, o.sc, sizeof(o.sc));
+    g.gram->sdig_gen = gen;
+    g.gram->sdig_sd = gen ? dig.sd : 0;
+    g.gram->row_eb = gen ? row_eb : nullptr;
     return g;
 }
 

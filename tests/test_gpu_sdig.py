@@ -35,6 +35,16 @@ def _solve(ds, g, k, p, q, seed, cache):
     return e, st
 
 
+def _gram(ds, d, cache):
+    """gram() with the cache policy `cache`: 0 keeps K1 from writing the
+    digit planes (the solves then store them in their first pass)."""
+    ds.set_sdig_cache(cache)
+    try:
+        return ds.gram(d)
+    finally:
+        ds.set_sdig_cache(1)
+
+
 CASES = [
     # (kind, n, rank, over, expect pair, sdigits)
     ("f64", 4133, 20, 10, 0, 7),   # NB = 32, ragged n
@@ -56,7 +66,7 @@ def _matrix(ds, kind, n, seed):
 @pytest.mark.parametrize("kind,n,rank,over,pair,sdigits", CASES)
 def test_sdig_cache_bit_identical(ds, oracle, kind, n, rank, over, pair, sdigits):
     d = _matrix(ds, kind, n, n % 11)
-    g = ds.gram(d)
+    g = _gram(ds, d, 0)  # the first product pass stores the cache
     off, st0 = _solve(ds, g, rank, over, 2, 3, 0)
     assert st0.last_product_kernel == 1 and st0.last_product_sdig == 0
     on, st1 = _solve(ds, g, rank, over, 2, 3, 2)
@@ -97,7 +107,7 @@ def test_sdig_cache_chunk_edge(ds, oracle):
     # streamed passes follow the same walk
     n = 8400
     d = ds.matrix_euclidean(ds.synth_points(1, n, 4))
-    g = ds.gram(d)
+    g = _gram(ds, d, 0)
     off, _ = _solve(ds, g, 40, 10, 1, 9, 0)
     on, st = _solve(ds, g, 40, 10, 1, 9, 2)
     assert st.last_product_sdig == 1
@@ -110,7 +120,7 @@ def test_sdig_cache_chunk_edge(ds, oracle):
 def test_sdig_cache_auto_policy(ds):
     # auto: on whenever the int8 path runs and the cache fits; policy 0
     # disables it; the first-pass statistics count one storing pass per solve
-    g = ds.gram(ds.matrix_euclidean(ds.synth_points(2, 4200, 5)))
+    g = _gram(ds, ds.matrix_euclidean(ds.synth_points(2, 4200, 5)), 0)
     ds.set_product_path(2)
     try:
         ds.stats_reset()
@@ -128,3 +138,73 @@ def test_sdig_cache_auto_policy(ds):
         ds.set_sdig_cache(1)
     with pytest.raises(ds.DivscopeError):
         ds.set_sdig_cache(3)
+
+
+K1_CASES = [
+    # (kind, n, rank, over): K1 writes the planes while it reads D for the gram
+    ("f64", 4133, 20, 10),   # NB = 32, ragged n (odd 64-row tile count)
+    ("f64", 4300, 20, 10),   # the last 64-column tile ends past the last k-step
+    ("f64", 4500, 40, 10),   # NB = 64 hybrid
+    ("f64", 4250, 50, 20),   # the CTA pair
+    ("ham", 4300, 30, 20),   # Hamming slices: no exponents needed
+    ("ham", 4100, 50, 20),   # Hamming slices on the pair
+]
+
+
+@pytest.mark.parametrize("kind,n,rank,over", K1_CASES)
+def test_k1_written_cache_matches_oracle(ds, oracle, kind, n, rank, over):
+    # every product pass streams the planes K1 wrote (digits of d^2 scaled
+    # by the row-0 triangle bound, within 3 bits of the true row exponent)
+    d = _matrix(ds, kind, n, n % 7)
+    g = _gram(ds, d, 1)
+    off, _ = _solve(ds, g, rank, over, 2, 5, 0)
+    on, st = _solve(ds, g, rank, over, 2, 5, 1)
+    assert st.last_product_kernel == 1 and st.last_product_sdig == 2
+    assert st.product_first_launches >= 1
+    np.testing.assert_allclose(on.eigenvalues, off.eigenvalues, rtol=1e-10,
+                               atol=1e-13 * abs(off.eigenvalues[0]))
+    dm = d.to_numpy()
+    _, rm, grand = oracle.gram_stats(dm)
+    want = oracle.embed(rank, over, 2, 5, d=dm, row_mean=rm, grand=grand)
+    top = min(on.dims, 12)
+    np.testing.assert_allclose(on.eigenvalues[:top], want["eigenvalues"][:top], rtol=1e-10)
+    assert coords_match_up_to_sign(on.coords[:, :top], want["coords"][:, :top]) < \
+        1e-7 * np.sqrt(want["eigenvalues"][0])
+    if kind == "ham":
+        # exact slices: the same digits as the storing pass, bit-identical
+        g0 = _gram(ds, d, 0)
+        stored, st0 = _solve(ds, g0, rank, over, 2, 5, 1)
+        assert st0.last_product_sdig == 1
+        assert np.array_equal(stored.coords, on.coords)
+
+
+def test_k1_cache_non_metric_falls_back(ds, oracle):
+    # a point 1e-3 from every other one breaks the triangle inequality the
+    # row-0 bound rests on: K1's check rejects its planes, the solve stores
+    # its own
+    n = 4200
+    d = ds.matrix_euclidean(ds.synth_points(2, n, 3)).to_numpy()
+    d[0, 1:] = 1e-3
+    d[1:, 0] = 1e-3
+    m = ds.matrix_from_host(d)
+    g = _gram(ds, m, 1)
+    on, st = _solve(ds, g, 20, 10, 1, 2, 1)
+    assert st.last_product_kernel == 1 and st.last_product_sdig == 1
+    off, _ = _solve(ds, g, 20, 10, 1, 2, 0)
+    assert np.array_equal(on.coords, off.coords)
+
+
+def test_k1_cache_generation(ds):
+    # a later gram (or a storing solve) overwrites the slot: an older gram's
+    # solves must not stream it
+    a = _gram(ds, ds.matrix_euclidean(ds.synth_points(2, 4400, 1)), 1)
+    ref_a, _ = _solve(ds, a, 20, 10, 1, 4, 0)
+    b = _gram(ds, ds.matrix_euclidean(ds.synth_points(3, 4400, 2)), 1)
+    got_a, st = _solve(ds, a, 20, 10, 1, 4, 1)
+    assert st.last_product_sdig == 1  # a's planes are gone: stored again
+    assert np.array_equal(got_a.coords, ref_a.coords)
+    got_b, st = _solve(ds, b, 20, 10, 1, 4, 1)
+    assert st.last_product_sdig == 1  # a's storing solve overwrote b's planes
+    again_a, st = _solve(ds, a, 20, 10, 1, 4, 1)
+    assert st.last_product_sdig == 1
+    assert np.array_equal(again_a.coords, got_a.coords)
