@@ -210,6 +210,74 @@ __device__ __forceinline__ bool chol_inverse(double* __restrict__ A, double* __r
                                     dpiv, tri, tri_off);
 }
 
+// WP <= 32: the factor on ONE warp, the matrix in registers (lane j holds
+// column j's upper part A[0..j][j]); step k broadcasts the pivot and, lane
+// by lane, row k (A[k][i] from lane i's register k), and every lane applies
+// the same update as cta_chol_inverse — A[i][j] -= A[k][i] A[k][j] / p —
+// with the same shift / drop decisions. No barriers, no shared-memory
+// round trips on the pivot chain (the CTA elimination spends ~800 cycles per
+// pivot on them). Writes L (Lm[j][k] = A[k][j] / p_k below the diagonal,
+// zero for a dropped pivot), dpiv and dropped_s; the caller applies
+// Q = Y L^-T D^-1/2 by forward substitution, so no inverse is formed.
+// Returns true when the first (shift-allowed) attempt asks for a shift.
+#ifndef DSB_ORTH_WARP_LDL
+#define DSB_ORTH_WARP_LDL 1
+#endif
+template <int WP>
+__device__ bool warp_ldl(const double* __restrict__ A, double* __restrict__ Lm, int w,
+                         const double* __restrict__ d0s, double maxdiag, bool first_shifting,
+                         bool drop_mode, int* __restrict__ dropped_s,
+                         double* __restrict__ dpiv) {
+    static_assert(WP <= 32, "one row per lane");
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned FULL = 0xffffffffu;
+    double a[WP];
+#pragma unroll
+    for (int i = 0; i < WP; ++i) a[i] = (lane < WP && i <= lane) ? A[i * WP + lane] : 0.0;
+#pragma unroll
+    for (int k = 0; k < WP; ++k) {
+        const double p = __shfl_sync(FULL, a[k], k);
+        const double d0k = d0s[k];
+        bool drop = (k >= w) || !(d0k > 0.0) || !(p > 0.0);
+        bool shift = false;
+        if (first_shifting) {
+            if (k < w && d0k > 0.0 && (drop || p <= kShiftTrigF * d0k)) shift = true;
+            drop = drop && !(k < w && d0k > 0.0);
+        } else if (drop_mode && p <= kDropTolF * maxdiag) {
+            drop = true;
+        }
+        if (shift) return true;  // uniform
+        if (lane == 0) {
+            dropped_s[k] = drop;
+            dpiv[k] = drop ? 0.0 : p;
+        }
+        double invp = 0.0;
+        if (!drop) {
+            double r;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+            r = fma(r, fma(-p, r, 1.0), r);
+            invp = fma(r, fma(-p, r, 1.0), r);
+        }
+        const double akj = a[k];  // A[k][j] of this lane's column j
+        // (fixed trip counts: the inner loops unroll before the outer one,
+        // so every register index stays static)
+#pragma unroll
+        for (int i = 0; i < WP; ++i) {
+            if (i > k) {
+                const double aki = __shfl_sync(FULL, a[k], i);  // A[k][i] from lane i
+                if (lane >= i) a[i] -= aki * akj * invp;
+            }
+        }
+        // L[j][k] (lanes j > k), once every lane has read A[k][j]
+        if (lane > k) a[k] = akj * invp;
+    }
+    if (lane < WP) {
+#pragma unroll
+        for (int k = 0; k < WP; ++k) Lm[lane * WP + k] = k < lane ? a[k] : 0.0;
+    }
+    return false;
+}
+
 template <int WP>
 __global__ void __launch_bounds__(256, 1)
     k_orth_fused(const double* __restrict__ y, double* __restrict__ out, size_t n_pad, int w,
@@ -237,6 +305,12 @@ __global__ void __launch_bounds__(256, 1)
     __shared__ unsigned short tri[WP * (WP + 1) / 2];
     __shared__ int tri_off[WP + 1];
     __shared__ int skip_third;
+    __shared__ int shift_flag;
+    // the warp factor + forward-substitution apply up to WP = 24 (C1, w = 20:
+    // factor 18.5k -> 12.1k cycles per pass); at WP = 32 the fully unrolled
+    // code (255 registers, ~1k shuffles) lost to the CTA elimination
+    // (factor 32k / 17k vs 26k / 26k cycles, apply 21k / 8.5k vs 9.4k / 9.0k)
+    constexpr bool kWarpLdl = DSB_ORTH_WARP_LDL != 0 && WP <= 24;
     // the CTA's rows stay in shared memory for all passes, column-major with
     // leading dimension ldr = 4 (mod 16): conflict-free MMA fragments and
     // conflict-free thread-per-row access
@@ -271,7 +345,10 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
     }
-    if (threadIdx.x == 0) skip_third = 0;
+    if (threadIdx.x == 0) {
+        skip_third = 0;
+        shift_flag = 0;
+    }
     for (int i = threadIdx.x; i <= WP; i += blockDim.x) {  // upper-triangle list sorted by row
         const int off = i * WP - (i * (i - 1)) / 2;
         tri_off[i] = off;
@@ -355,9 +432,22 @@ __global__ void __launch_bounds__(256, 1)
                 __syncthreads();
                 const bool first_shifting = pass == 0 && attempt == 0;
                 const bool drop_mode = pass != 0;
-                if (!chol_inverse<WP>(R, E, w, d0s, tr_s[1], first_shifting, drop_mode,
-                                          dropped_s, dpiv, tri, tri_off))
+                if constexpr (kWarpLdl) {
+                    // warp 0 factors into E (= L); the CTA waits for it
+                    if (threadIdx.x < 32 &&
+                        warp_ldl<WP>(R, E, w, d0s, tr_s[1], first_shifting, drop_mode, dropped_s,
+                                     dpiv) &&
+                        threadIdx.x == 0)
+                        shift_flag = 1;
+                    __syncthreads();
+                    const bool sh = shift_flag != 0;
+                    __syncthreads();
+                    if (threadIdx.x == 0) shift_flag = 0;
+                    if (!sh) break;
+                } else if (!chol_inverse<WP>(R, E, w, d0s, tr_s[1], first_shifting, drop_mode,
+                                             dropped_s, dpiv, tri, tri_off)) {
                     break;
+                }
                 sigma = 11.0 * (nrows * w + static_cast<double>(w) * (w + 1)) * 0x1.0p-53 * tr_s[0];
                 shifted = true;
             }
@@ -368,6 +458,38 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncthreads();
         mark();
+        if constexpr (kWarpLdl) {
+            // ---- 4'. Q = Y L^-T D^-1/2 row by row: x L^T = y by forward
+            // substitution (L from the warp factor, broadcast from shared
+            // memory), x_k / sqrt(d_k); each thread owns whole rows
+            for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
+                double x[WP];
+#pragma unroll
+                for (int k = 0; k < WP; ++k) x[k] = ps[k * ldr + r];
+#pragma unroll
+                for (int k = 1; k < WP; ++k) {
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int i = 0; i < WP; ++i) {
+                        if (i < k) {
+                            if (i & 1)
+                                s1 = fma(E[k * WP + i], x[i], s1);
+                            else
+                                s0 = fma(E[k * WP + i], x[i], s0);
+                        }
+                    }
+                    x[k] -= s0 + s1;
+                }
+#pragma unroll
+                for (int k = 0; k < WP; ++k) {
+                    const double dk = dpiv[k];
+                    ps[k * ldr + r] = dk > 0.0 ? x[k] * rsqrt(dk) : 0.0;
+                }
+            }
+            __syncthreads();
+            mark();
+            continue;
+        }
         // ---- 4. T = R^{-1} = L^{-T} D^{-1/2} (into R), then Q = Y T for this
         // CTA's rows: outputs kept in registers until every thread has read
         // its inputs, then written back in place
