@@ -221,7 +221,10 @@ constexpr int slot_bytes() {
 // should block on): the D ring depth is then a multiple of 4
 template <int NB, int SD, int DM>
 constexpr int conv_groups_ts() {
-    return (DM == 2 && a_stages_ts<NB, SD>() % 4 == 0) ? 4 : 1;
+    // one group of 4 converter warps per A stage (2, 3 or 4 stages)
+    return (DM == 2 && a_stages_ts<NB, SD>() >= 2 && a_stages_ts<NB, SD>() <= 4)
+               ? a_stages_ts<NB, SD>()
+               : 1;
 }
 template <int NB, typename TD, int SD = kDig, int CL = 1, int DM = 0>
 constexpr int d_stages_ts() {
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     // four items' load -> tcgen05.st -> arrive chains overlap
     constexpr int kGrp = conv_groups_ts<NB, SD, DM>();
     static_assert(kGrp == 1 || (ND % kGrp == 0 && NA % kGrp == 0), "groups own their slots");
-    constexpr int kCW = kConv / kGrp;
+    constexpr int kCW = kGrp > 1 ? 4 : kConv;  // converter warps per item
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -585,14 +588,14 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_empty);
         };
-        if constexpr (kGrp == 4) {
-            // streaming the cache: group part_k takes items k = part_k mod 4
+        if constexpr (kGrp > 1) {
+            // streaming the cache: group part_k takes items k = part_k mod kGrp
             // (and so always the same ring slots and A stage); every group
             // walks every item to keep the ring indices
             int sd = 0, sa = 0, k = 0, nflush = 0;
             uint32_t pd = 0, pa = 0;
             for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
-                if ((k & 3) == part_k) {
+                if (k % kGrp == part_k) {
                     mbar_wait(&full_d[sd], pd);
                     if (k >= NA) {
                         mbar_wait(&empty_a[sa], pa ^ 1);
