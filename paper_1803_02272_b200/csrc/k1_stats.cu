@@ -447,11 +447,17 @@ size_t k1_smem() {
 // A block owns 32 rows; its 8 warps stride over the tile columns J (warp w:
 // J = w, w + 8, ...) and the 8 partials are added in warp order (fixed).
 constexpr int kRmRows = 32;
+// row_eb (K1 writing the S-digit cache): the bound exponents its digits
+// used; blk_bad[b] = 1 when a row of block b is not covered by its bound or
+// the bound is more than 3 bits above the row's exponent (k1_finalize ORs
+// them into scalars[S_SDIG_BAD])
 __global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ part,
                                                    const int* __restrict__ pexp, size_t part_ld,
                                                    int nbt, int n, double* __restrict__ row_mean,
                                                    int* __restrict__ row_exp,
-                                                   double* __restrict__ blk_stats) {
+                                                   double* __restrict__ blk_stats,
+                                                   const int* __restrict__ row_eb,
+                                                   int* __restrict__ blk_bad) {
     __shared__ double ps[8][kRmRows];
     __shared__ int pe[8][kRmRows];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,6 +475,7 @@ __global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ pa
     __syncthreads();
     if (warp == 0) {
         double rowsum = 0.0, r = 0.0, ratio = 0.0;
+        int bad = 0;
         if (i < n) {
             int ee = kExpZero;
             for (int w = 0; w < 8; ++w) {
@@ -478,11 +485,17 @@ __global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ pa
             r = rowsum / static_cast<double>(n);
             row_mean[i] = r;
             row_exp[i] = ee;
+            if (row_eb) {
+                const int eb = row_eb[i];
+                bad = (ee > eb || (ee > kExpZero && eb - ee > 3)) ? 1 : 0;
+            }
             if (ee > kExpZero) ratio = (r > 0.0) ? ldexp(1.0, ee) / r : 1e300;
         }
         const double v0 = warp_sum(rowsum), v1 = warp_sum(r), v2 = warp_sum(r * r),
                      v3 = warp_max(ratio);
+        bad = __any_sync(0xffffffffu, bad != 0) ? 1 : 0;
         if (lane == 0) {
+            blk_bad[blockIdx.x] = bad;
             blk_stats[blockIdx.x * 4 + 0] = v0;
             blk_stats[blockIdx.x * 4 + 1] = v1;
             blk_stats[blockIdx.x * 4 + 2] = v2;
@@ -495,7 +508,8 @@ __global__ void __launch_bounds__(256) k1_rowmeans(const double* __restrict__ pa
 // fixed-order tree over the 256 threads — deterministic.
 __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ cta_stats, int ncta,
                                                    const double* __restrict__ blk_stats, int nblk,
-                                                   int n, double* __restrict__ scalars) {
+                                                   int n, double* __restrict__ scalars,
+                                                   const int* __restrict__ blk_bad) {
     __shared__ double sh[8][256];
     const int t = threadIdx.x;
     double sum4 = 0, m1 = 0, m2 = 0, m3 = 0, rows = 0, sr = 0, sr2 = 0, rr = 0;
@@ -505,7 +519,9 @@ __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ ct
         m2 = fmax(m2, cta_stats[c * 4 + 2]);
         m3 = fmax(m3, cta_stats[c * 4 + 3]);
     }
+    int bad = 0;
     for (int b = t; b < nblk; b += 256) {
+        bad |= blk_bad[b];
         rows += blk_stats[b * 4 + 0];
         sr += blk_stats[b * 4 + 1];
         sr2 += blk_stats[b * 4 + 2];
@@ -513,7 +529,7 @@ __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ ct
     }
     sh[0][t] = sum4; sh[1][t] = m1; sh[2][t] = m2; sh[3][t] = m3;
     sh[4][t] = rows; sh[5][t] = sr; sh[6][t] = sr2; sh[7][t] = rr;
-    __syncthreads();
+    bad = __syncthreads_or(bad);
     for (int off = 128; off > 0; off >>= 1) {
         if (t < off) {
             sh[0][t] += sh[0][t + off];
@@ -540,40 +556,36 @@ __global__ void __launch_bounds__(256) k1_finalize(const double* __restrict__ ct
         scalars[S_SUMR] = sh[5][0];
         scalars[S_SUMR2] = sh[6][0];
         scalars[S_ROWRATIO] = sh[7][0];
+        scalars[S_SDIG_BAD] = bad ? 1.0 : 0.0;
     }
 }
 
 // row_eb from row 0 of D: max_j d_ij <= d_i0 + d_0j <= |d_0i| + M0 (triangle
 // inequality, d_i0 = d_0i), M0 = max_j |d_0j| (NaN-ignoring selects, as K1);
-// the sum and square rounded up
+// the sum and square rounded up. Every CTA forms M0 itself (4 loads in
+// flight per thread), then bounds its own 1024 rows
 __global__ void __launch_bounds__(1024) k_row0_bound(const double* __restrict__ d0, int n,
                                                      int* __restrict__ row_eb) {
     __shared__ double red[32];
-    double m = 0.0;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) m = max_keep(m, fabs(d0[j]));
-    m = warp_max(m);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    double m[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j0 = threadIdx.x; j0 < n; j0 += 4 * blockDim.x) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * blockDim.x;
+            if (j < n) m[u] = max_keep(m[u], fabs(__ldg(d0 + j)));
+        }
+    }
+    double mm = max_keep(max_keep(m[0], m[1]), max_keep(m[2], m[3]));
+    mm = warp_max(mm);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mm;
     __syncthreads();
     double m0 = 0.0;
     for (int w = 0; w < 32; ++w) m0 = max_keep(m0, red[w]);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
         const double b = __dadd_ru(fabs(d0[i]), m0);
         row_eb[i] = exp_above_hi(hi_bits(__dmul_ru(b, b)));
     }
-}
-
-// the bound exponents must cover every row's true exponent, and stay within
-// 3 bits of it (the digits keep >= 53 bits relative to the row maximum)
-__global__ void __launch_bounds__(1024) k_sdig_check(const int* __restrict__ row_exp,
-                                                     const int* __restrict__ row_eb, int n,
-                                                     double* __restrict__ scalars) {
-    int bad = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int e = row_exp[i], eb = row_eb[i];
-        if (e > eb || (e > kExpZero && eb - e > 3)) bad = 1;
-    }
-    bad = __syncthreads_or(bad);
-    if (threadIdx.x == 0) scalars[S_SDIG_BAD] = bad ? 1.0 : 0.0;
 }
 
 }  // namespace
@@ -619,18 +631,16 @@ void launch_k1(const CUtensorMap* tmap64, DType dt, size_t n, const K1Work& w, d
     const int nblk = static_cast<int>((n + kRmRows - 1) / kRmRows);
     const int nparts = nbt * (dt == DType::F64 ? K1Cfg<double>::H : K1Cfg<float>::H);
     k1_rowmeans<<<nblk, 256, 0, st>>>(w.part, w.pexp, part_ld, nparts, static_cast<int>(n),
-                                      row_mean, row_exp, w.blk_stats);
+                                      row_mean, row_exp, w.blk_stats,
+                                      dg == 7 ? dig->row_eb : nullptr, w.blk_bad);
     k1_finalize<<<1, 256, 0, st>>>(w.cta_stats, w.grid, w.blk_stats, nblk, static_cast<int>(n),
-                                   scalars);
+                                   scalars, w.blk_bad);
     count_launch(3);
-    if (dg == 7) {
-        k_sdig_check<<<1, 1024, 0, st>>>(row_exp, dig->row_eb, static_cast<int>(n), scalars);
-        count_launch(1);
-    }
 }
 
 void launch_row0_bound(const double* d, size_t n, int* row_eb, cudaStream_t st) {
-    k_row0_bound<<<1, 1024, 0, st>>>(d, static_cast<int>(n), row_eb);
+    k_row0_bound<<<static_cast<unsigned>((n + 1023) / 1024), 1024, 0, st>>>(
+        d, static_cast<int>(n), row_eb);
     count_launch(1);
 }
 

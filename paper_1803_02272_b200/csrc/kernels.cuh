@@ -41,6 +41,7 @@ struct K1Work {
     int* pexp;           // [nbt][n_pad64] per-tile-column row exponents of max d^2
     double* cta_stats;   // [grid][4]
     double* blk_stats;   // [nblk][4]
+    int* blk_bad;        // [nblk] S-digit bound violations per row block
     int grid;
 };
 size_t k1_part_elems(size_t n);

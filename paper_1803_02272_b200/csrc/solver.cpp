@@ -51,6 +51,7 @@ StatsOut run_k1(Store& s, const std::function<const K1Digits*()>& claim_digits =
     w.cta_stats = static_cast<double*>(c.scratch("k1_cta", static_cast<size_t>(w.grid) * 4 * 8));
     w.pexp = static_cast<int*>(c.scratch("k1_pexp", k1_part_elems(n) * sizeof(int)));
     w.blk_stats = static_cast<double*>(c.scratch("k1_blk", ((n + 31) / 32) * 4 * 8 + 64));
+    w.blk_bad = static_cast<int*>(c.scratch("k1_blkbad", ((n + 31) / 32) * sizeof(int) + 64));
     StatsOut o;
     o.row_mean = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * sizeof(double));
     o.row_exp = std::make_shared<DevBuf>(std::max<size_t>(n, 1) * sizeof(int));

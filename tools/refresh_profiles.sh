@@ -2,7 +2,7 @@
 # Round measurement set (run on a B200 box via gpurun): bench lines for
 # C1/C2/C3/C4/C5 and the reference arm, the launch list of the C2 bench
 # command, full ncu captures of the C2 product kernel (a streaming pass of the
-# S-digit cache and the storing pass), of the C5 streaming pass, of the
+# S-digit cache) and of K1 writing the cache, of the C5 streaming pass, of the
 # CTA-pair kernel (w = 70) and of the K7 tensor-core Hamming builder.
 # Outputs in gpurun_out/ (copied to profiles/ by tools/collect_profiles.py).
 set -u
@@ -22,12 +22,13 @@ python bench.py --workload C1 --steps 2 --warmup 3 --no-cpu-baseline > $O/plain_
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/launches_c1.csv python bench.py --workload C1 --steps 2 --warmup 3 \
     --no-cpu-baseline > $O/ncu_launches_c1.log 2>&1
-# k2i_time: one solve (launch 0 stores the cache, 1-5 stream it), then timed solves
+# k2i_time: solves streaming the S-digit cache K1 wrote (every launch)
 python tools/k2i_time.py C2 > $O/plain_k2i.txt 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:k2i_product_ts -s 2 -c 1 \
     -o $O/k2i_c2_stream -f python tools/k2i_time.py C2 > $O/ncu_k2i.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:k2i_product_ts -s 0 -c 1 \
-    -o $O/k2i_c2_store -f python tools/k2i_time.py C2 > $O/ncu_k2i_store.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k1_tile_pairs -s 3 -c 1 \
+    -o $O/k1dig_c2 -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
+    > $O/ncu_k1dig.log 2>&1
 python tools/k2i_time.py C5 > $O/plain_k2i_c5.txt 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:k2i_product_ts -s 2 -c 1 \
     -o $O/k2i_c5_stream -f python tools/k2i_time.py C5 > $O/ncu_k2i_c5.log 2>&1
