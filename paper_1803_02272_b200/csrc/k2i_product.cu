@@ -410,6 +410,11 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         // ---------------- TMA producer: D tiles and panel digits ----------------
         if (lane == 0) {
             if constexpr (DM != 2) prefetch_tmap(&tmD);
+            // streaming: the items pass through L2 once (evict first), the
+            // panel digits every row block re-reads stay (evict last)
+            const uint64_t pol_item = l2_policy(true), pol_panel = l2_policy(false);
+            (void)pol_item;
+            (void)pol_panel;
             int sd = 0, sb = 0, k = 0;
             uint32_t pd = 0, pb = 0;
             for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
@@ -425,11 +430,12 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                         // this CTA's 1/CL of the item, into every CTA of the cluster
                         constexpr int CH = (IB / CL + 15) / 16 * 16;
                         const int off = crank * CH;
-                        bulk_load_mc(dst + off, src + off,
-                                     static_cast<uint32_t>(IB - off < CH ? IB - off : CH),
-                                     &full_d[sd], static_cast<uint16_t>((1u << CL) - 1u));
+                        bulk_load_mc_pol(dst + off, src + off,
+                                         static_cast<uint32_t>(IB - off < CH ? IB - off : CH),
+                                         &full_d[sd], static_cast<uint16_t>((1u << CL) - 1u),
+                                         pol_item);
                     } else
-                        bulk_load(dst, src, IB, &full_d[sd]);
+                        bulk_load_pol(dst, src, IB, &full_d[sd], pol_item);
                 } else if constexpr (CL > 1) {
                     // this CTA's 64-row half of the tile, into both CTAs
                     // (64 rows x 128 B keeps the SWIZZLE_128B phase)
@@ -453,8 +459,13 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 if constexpr (kBProd) {
                     if (k >= NBR) mbar_wait(&empty_b[sb], pb ^ 1);
                     mbar_arrive_expect_tx(&full_b[sb], BB);
-                    bulk_load(bring + sb * BB, bdig + static_cast<size_t>(k_off + w.ks) * BB, BB,
-                              &full_b[sb]);
+                    if constexpr (DM == 2)
+                        bulk_load_pol(bring + sb * BB,
+                                      bdig + static_cast<size_t>(k_off + w.ks) * BB, BB,
+                                      &full_b[sb], pol_panel);
+                    else
+                        bulk_load(bring + sb * BB, bdig + static_cast<size_t>(k_off + w.ks) * BB,
+                                  BB, &full_b[sb]);
                     if (++sb == NBR) {
                         sb = 0;
                         pb ^= 1;
