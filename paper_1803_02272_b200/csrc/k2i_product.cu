@@ -1274,7 +1274,8 @@ void launch_k2i_ranges(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DT
                        const double* row_mean, const double* scalars, const double* colsums,
                        double* y, size_t y_rows_pad, cudaStream_t st, cudaEvent_t gathered,
                        const std::vector<std::pair<int, int>>& ranges, int sms, cudaEvent_t e0,
-                       cudaEvent_t e1, int hamming_len) {
+                       cudaEvent_t e1, int hamming_len, unsigned char* sdig, int sdig_mode) {
+    if (!sdig) sdig_mode = 0;
     const size_t r_done = static_cast<size_t>(full.nblk) * kRowsI8;
     if (y_rows_pad > r_done)
         DSB_CUDA(cudaMemsetAsync(y + r_done * wp, 0, (y_rows_pad - r_done) * wp * sizeof(double),
@@ -1303,43 +1304,47 @@ void launch_k2i_ranges(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DT
         k_panel_digits<<<grid, 256, 0, st>>>(x, k0, nk, wp, nb, cg0, col_exp, dst);
         count_launch();
     };
+    // cache items are indexed by global k-step (k_off) over the full plan's
+    // k-steps; a storing pass's later column groups already find them
     auto run = [&](int ri, int g, unsigned char* bd, size_t bs) {
         const K2iPlan& pr = plans[ri];
+        const int dm = (sdig_mode == 1 && g > 0) ? 2 : sdig_mode;
+        const int nkc = full.nks;
         double* pp = part + static_cast<size_t>(splits[ri].slot_base) * kRowsI8 * wp;
         const int k0 = ranges[ri].first;
         if (full.pair) {
             if (ham)
                 run_i8<48, double, 3, 2>(tmap64, pr, wp, bd, bs, row_exp, col_exp, pp, 0, st,
-                                         nullptr, hl, k0);
+                                         nullptr, hl, k0, dm, sdig, nkc);
             else if (dt == DType::F64)
                 run_i8<48, double, kDig, 2>(tmap64, pr, wp, bd, bs, row_exp, col_exp, pp, 0, st,
-                                            nullptr, 0.0, k0);
+                                            nullptr, 0.0, k0, dm, sdig, nkc);
             else
                 run_i8<48, float, kDig, 2>(tmap64, pr, wp, bd, bs, row_exp, col_exp, pp, 0, st,
-                                           nullptr, 0.0, k0);
+                                           nullptr, 0.0, k0, dm, sdig, nkc);
         } else {
             const int nb = full.gnb[g], cg0 = full.gc0[g];
             if (ham) {
                 if (nb == 32)
                     run_i8<32, double, 3>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
-                                          nullptr, hl, k0);
+                                          nullptr, hl, k0, dm, sdig, nkc);
                 else
                     run_i8<64, double, 3>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
-                                          nullptr, hl, k0);
+                                          nullptr, hl, k0, dm, sdig, nkc);
             } else if (dt == DType::F64) {
                 if (nb == 32)
                     run_i8<32, double>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
-                                       nullptr, 0.0, k0);
+                                       nullptr, 0.0, k0, dm, sdig, nkc);
                 else
                     run_i8<64, double>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
-                                       nullptr, 0.0, k0);
+                                       nullptr, 0.0, k0, dm, sdig, nkc);
             } else {
                 if (nb == 32)
                     run_i8<32, float>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
-                                      nullptr, 0.0, k0);
+                                      nullptr, 0.0, k0, dm, sdig, nkc);
                 else
                     run_i8<64, float>(tmap128, pr, wp, bd, 0, row_exp, col_exp, pp, cg0, st,
-                                      nullptr, 0.0, k0);
+                                      nullptr, 0.0, k0, dm, sdig, nkc);
             }
         }
         count_launch();

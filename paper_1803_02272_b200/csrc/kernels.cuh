@@ -165,7 +165,8 @@ void launch_k2i_ranges(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DT
                        const double* row_mean, const double* scalars, const double* colsums,
                        double* y, size_t y_rows_pad, cudaStream_t st, cudaEvent_t gathered,
                        const std::vector<std::pair<int, int>>& ranges, int sms, cudaEvent_t e0,
-                       cudaEvent_t e1, int hamming_len);
+                       cudaEvent_t e1, int hamming_len, unsigned char* sdig = nullptr,
+                       int sdig_mode = 0);
 // pmax: colmax_grid * wp doubles; col_exp: nb ints (<= 128); bdig: bdig_bytes
 // tmap64: 64-row boxes of the same D (the pair kernel's multicast halves)
 void launch_k2i(const CUtensorMap* tmap128, const CUtensorMap* tmap64, DType dt, const K2iPlan& p,

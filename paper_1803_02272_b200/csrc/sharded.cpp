@@ -364,7 +364,6 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
                                : 0;
     c.last_product_sdigits = use_i8 ? (hamming_i8 ? 3 : 7) : 0;
     c.last_product_pair = use_i8 && iplan.pair ? 1 : 0;
-    c.last_product_sdig = 0;
     c.last_product_stream_cl = 0;
     c.last_product_groups = use_i8 ? iplan.ngroups : 1;
     const size_t pbytes = n_pad * wp * 8;
@@ -383,6 +382,16 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     double* wmat = static_cast<double*>(c.scratch("wmat", wp * wp * 8));
     double* rinv = static_cast<double*>(c.scratch("rinv", wp * wp * 8));
     int* flags = static_cast<int*>(c.scratch("flags", 64));
+    // the rank's S-digit cache (k2i_product.cu): its rows x every k-step;
+    // the first product pass stores it, the later ones stream it. Local to
+    // the rank (no collective depends on it), claimed last (evictable)
+    unsigned char* sdig = nullptr;
+    if (use_i8 && sdig_policy() > 0 && m > 0)
+        sdig = static_cast<unsigned char*>(
+            c.try_scratch("i8_sdig", k2i_sdig_bytes(iplan, hamming_i8 ? 3 : 7)));
+    if (sdig) ++c.sdig_gen;  // overwrites whatever the slot held
+    c.last_product_sdig = sdig ? 1 : 0;
+    int sdig_pass = 0;
     DSB_CUDA(cudaMemsetAsync(flags, 0, 64, c.stream));
     DSB_CUDA(cudaMemsetAsync(P1, 0, pbytes, c.stream));
     {
@@ -396,6 +405,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     // product after a CholeskyQR; the first one multiplies the replicated Omega)
     auto product = [&](double* x_full, double* y_full, bool gather) {
         cudaEvent_t e0, e1;
+        const int sdm = sdig ? (sdig_pass++ == 0 ? 1 : 2) : 0;
         if (gather && overlap) {
             // s = 1^T X, t = r^T X and the column maxima of this rank's rows,
             // reduced over the ranks; then the all-gather on the side stream
@@ -415,7 +425,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
                 launch_k2i_ranges(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x_full,
                                   g.gram->row_exp->as<int>(), col_exp, bdig, part, r_full + rb,
                                   scal, colsums, y_full + lo, m_pad, c.stream, c.side_done, ranges,
-                                  c.sms, e0, e1, hamming_i8);
+                                  c.sms, e0, e1, hamming_i8, sdig, sdm);
             } else {
                 DSB_CUDA(cudaStreamWaitEvent(c.stream, c.side_done, 0));
                 if (m)
@@ -440,7 +450,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
             launch_k2i(s.tmap_for(128), &s.tmap64, s.dt, iplan, wp, x_full, n_pad,
                        g.gram->row_exp->as<int>(),
                        pmax, col_exp, bdig, part, r_full + rb, scal, colsums, y_full + lo, m_pad,
-                       c.stream, e0, e1, nullptr, hamming_i8);
+                       c.stream, e0, e1, nullptr, hamming_i8, sdig, sdm);
         else if (m)
             launch_k2(s.tmap_for(plan.bm), s.dt, 1, plan, x_full, part, r_full + rb, scal, colsums,
                       y_full + lo, m_pad, c.stream, e0, e1);

@@ -93,7 +93,8 @@ def main():
         vals, resid = ds.eigs(g, rank=k, oversampling=p, power_iters=q, seed=seed)
         res.update(eig_vals=vals, resid=resid)
         st = ds.stats_get()
-        res.update(product_kernel=st.last_product_kernel, groups=st.last_product_groups)
+        res.update(product_kernel=st.last_product_kernel, groups=st.last_product_groups,
+                   sdig=st.last_product_sdig)
     ds.comm_destroy()
     np.savez(out, **{key: np.asarray(v) for key, v in res.items()})
 

@@ -111,6 +111,10 @@ def test_ranks_match_oracle_and_one_process(ds, oracle, tmp_path, world, product
     assert sum(sizes) == case["n"] and len(set(sizes)) > 1
     if product == 2:
         assert all(int(o["product_kernel"]) == 1 for o in res)
+        # each rank stores its rows' S-digit planes in the first product pass
+        # and streams them in the others (k-step ranges of the overlapped
+        # gather index the items by global k-step)
+        assert all(int(o["sdig"]) == 1 for o in res)
     check_against(ds, oracle, case, res)
     # eigs on the same sharded gram
     for o in res:
