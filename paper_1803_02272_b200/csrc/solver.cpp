@@ -329,6 +329,11 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
         res_out = static_cast<double*>(
             c.scratch("lift_out", n * std::max<size_t>(req, 1) * sizeof(double)));
     }
+    // the solve's own copy of its result (the workspace is reused), allocated
+    // here: an allocation that fails evicts the S-digit slot and the captured
+    // graphs, so none may happen once the slot is claimed (below)
+    std::shared_ptr<DevBuf> dres;
+    if (res_out) dres = std::make_shared<DevBuf>(n * std::max<size_t>(req, 1) * 8);
     // read back into pinned memory, one sync for all of it
     struct Meta {
         double vals[kMaxWP];
@@ -591,13 +596,9 @@ RunOut run(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t seed, What
     } else {
         enqueue();
     }
-    // the solve's own copy of its result (the workspace is reused)
-    std::shared_ptr<DevBuf> dres;
-    if (res_out) {
-        dres = std::make_shared<DevBuf>(n * std::max<size_t>(req, 1) * 8);
+    if (res_out)
         DSB_CUDA(cudaMemcpyAsync(dres->p, res_out, n * std::max<size_t>(req, 1) * 8,
                                  cudaMemcpyDeviceToDevice, c.stream));
-    }
     if (trace) std::fprintf(stderr, "[trace] host enqueue done %.1f us\n", host_us());
     c.sync();
     if (ge && c.timing)
