@@ -267,6 +267,19 @@ bool Ctx::evict_scratch() {
     return any;
 }
 
+// debug / tests: what a failed device allocation does first — drop the
+// evictable workspace (the S-digit cache) and the graphs that address it;
+// returns 1 when something was evicted
+extern "C" int divscope_debug_evict_workspace(void) {
+    try {
+        Ctx& c = Ctx::get();
+        std::lock_guard<std::recursive_mutex> lk(c.mu);
+        return c.evict_scratch() ? 1 : 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
 // debug: copy the first `bytes` of the S-digit cache slot to host memory
 extern "C" int divscope_debug_sdig_read(void* host, size_t bytes) {
     try {

@@ -208,3 +208,23 @@ def test_k1_cache_generation(ds):
     again_a, st = _solve(ds, a, 20, 10, 1, 4, 1)
     assert st.last_product_sdig == 1
     assert np.array_equal(again_a.coords, got_a.coords)
+
+
+def test_evicted_cache_is_stored_again(ds):
+    # a failed device allocation drops the slot (and the graphs that address
+    # it): the gram's planes are gone, its next solve stores them again and
+    # gets the same answer; with the slot back, later solves stream it
+    import ctypes as C
+    ev = ds.lib.divscope_debug_evict_workspace
+    ev.restype = C.c_int
+    g = _gram(ds, ds.matrix_euclidean(ds.synth_points(2, 4600, 6)), 1)
+    first, st = _solve(ds, g, 20, 10, 1, 8, 1)
+    assert st.last_product_sdig == 2
+    assert ev() == 1
+    again, st = _solve(ds, g, 20, 10, 1, 8, 1)
+    assert st.last_product_sdig == 1
+    np.testing.assert_allclose(again.eigenvalues, first.eigenvalues, rtol=1e-12)
+    assert coords_match_up_to_sign(again.coords, first.coords) < 1e-9 * np.sqrt(first.eigenvalues[0])
+    third, st = _solve(ds, g, 20, 10, 1, 8, 1)
+    assert st.last_product_sdig == 1
+    assert np.array_equal(third.coords, again.coords)
