@@ -157,11 +157,31 @@ __device__ bool cta_chol_inverse_b4(double* __restrict__ A, double* __restrict__
                     invs[kk - k0] = invp;
                 }
                 const double* rowk = A + kk * WP;
-                // the block's later pivot rows, every column j >= i
-                for (int i = kk + 1; i < k0 + 4; ++i) {
-                    const double f = rowk[i] * invp;
-                    for (int jj = i + lane; jj < WP; jj += 32) A[i * WP + jj] -= f * rowk[jj];
-                    for (int c = lane; c <= kk; c += 32) E[i * WP + c] -= f * E[kk * WP + c];
+                // the block's later pivot rows (at most 3), every column
+                // j >= i, and their E rows: all multipliers and row-k values
+                // are read first, then the (independent) row updates run side
+                // by side instead of one row after another
+                double f[3];
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    const int i = kk + 1 + t;
+                    f[t] = i < k0 + 4 ? rowk[i] * invp : 0.0;
+                }
+                for (int jj = lane; jj < WP; jj += 32) {
+                    const double rj = rowk[jj];
+#pragma unroll
+                    for (int t = 0; t < 3; ++t) {
+                        const int i = kk + 1 + t;
+                        if (i < k0 + 4 && jj >= i) A[i * WP + jj] -= f[t] * rj;
+                    }
+                }
+                for (int c = lane; c <= kk; c += 32) {
+                    const double ek = E[kk * WP + c];
+#pragma unroll
+                    for (int t = 0; t < 3; ++t) {
+                        const int i = kk + 1 + t;
+                        if (i < k0 + 4) E[i * WP + c] -= f[t] * ek;
+                    }
                 }
                 __syncwarp();
             }
