@@ -96,6 +96,8 @@ def c2(ds, oracle):
 def test_c2_full_size_matches_oracle(ds, c2, path):
     e, kernel = embed_on(ds, path, c2["dm"], c2["k"], c2["p"], c2["q"], c2["seed"])
     assert kernel == (1 if path == 2 else 0)
+    # int8: every product pass streams the S-digit planes K1 wrote
+    assert ds.stats_get().last_product_sdig == (2 if path == 2 else 0)
     check_embedding(e, c2["ref"])
     # eigs on the same gram: values and resid (cancellation-prone, so
     # compared as squares against ||G||_F^2)
@@ -127,6 +129,7 @@ def test_int8_chunk_flush_matches_oracle(ds, oracle, n, path):
     ref = oracle_embed(oracle, d, k, p, q, seed)
     e, kernel = embed_on(ds, path, dm, k, p, q, seed)
     assert kernel == (1 if path == 2 else 0)
+    assert ds.stats_get().last_product_sdig == (2 if path == 2 else 0)
     check_embedding(e, ref)
 
 
@@ -148,6 +151,7 @@ def test_c5_full_size_hamming_matches_oracle(ds, oracle):
     e, kernel = embed_on(ds, 0, dm, k, p, q, seed)
     st = ds.stats_get()
     assert kernel == 1 and st.last_product_sdigits == 3  # three-byte Hamming slices
+    assert st.last_product_sdig == 2  # streamed from the planes K1 wrote
     check_embedding(e, ref)
 
 
@@ -159,7 +163,8 @@ def test_c3_full_size_matches_oracle(ds, oracle):
     n, k, p, q, seed = 100000, 50, 20, 2, 3
     dm = ds.matrix_euclidean(ds.synth_points(3, n, seed))
     e, kernel = embed_on(ds, 0, dm, k, p, q, seed)
-    assert kernel == 1 and ds.stats_get().last_product_groups >= 1
+    st = ds.stats_get()
+    assert kernel == 1 and st.last_product_pair == 1 and st.last_product_sdig == 2
     d = dm.to_numpy()
     del dm
     ref = oracle_embed(oracle, d, k, p, q, seed)

@@ -4,7 +4,8 @@
 # command, full ncu captures of the C2 product kernel (a streaming pass of the
 # S-digit cache) and of K1 writing the cache, of the C5 streaming pass, of the
 # CTA-pair kernel (w = 70) and of the K7 tensor-core Hamming builder.
-# Outputs in gpurun_out/ (copied to profiles/ by tools/collect_profiles.py).
+# Outputs in gpurun_out/ (summarized into profiles/r02_final_* by hand: tools/launch_summary.py,
+# ncu -i ... --page details / --page raw).
 set -u
 O=gpurun_out
 mkdir -p $O
