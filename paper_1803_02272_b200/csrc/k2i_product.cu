@@ -55,6 +55,12 @@ constexpr int kRowsI8 = 128;   // M
 constexpr int kKStep = 32;     // int8 MMA K
 constexpr int kDig = 7;        // digits of S and of X
 constexpr int kChunk = 256;    // k-steps per int32 accumulation chunk (8192 columns)
+// Hamming slices: a diagonal sums at most 3 digit products (t <= 3), so
+// 3 * 255 * 128 * 16384 < 2^31: chunks twice as long, half the flushes
+template <int SD>
+constexpr int chunk_ks() {
+    return SD == 3 ? 512 : kChunk;
+}
 constexpr int kConv = 16;      // converter warps (8 rows each)
 constexpr int kThreadsI8 = (2 + kConv) * 32;
 constexpr int kExpZeroI8 = -1100;  // matches K1's exponent of an all-zero row
@@ -70,6 +76,7 @@ constexpr int d_bytes() {
 // Walks a CTA's stream-K range [t0, t1) of (row block, k-step) items without
 // divisions: row block, k-step, segment index and position in the int32
 // accumulation chunk (chunks restart at every row block).
+template <int CH = kChunk>
 struct Walk {
     int it, t1, nks, rb, ks, seg, pos;
     bool seg_first;  // the current chunk is the first one of its segment
@@ -78,7 +85,7 @@ struct Walk {
           seg_first(true) {}
     __device__ bool more() const { return it < t1; }
     __device__ bool first() const { return pos == 0; }
-    __device__ bool last() const { return it + 1 == t1 || ks + 1 == nks || pos + 1 == kChunk; }
+    __device__ bool last() const { return it + 1 == t1 || ks + 1 == nks || pos + 1 == CH; }
     __device__ void next() {
         ++it;
         ++ks;
@@ -89,7 +96,7 @@ struct Walk {
             ++seg;
             pos = 0;
             seg_first = true;
-        } else if (pos == kChunk) {
+        } else if (pos == CH) {
             pos = 0;
             seg_first = false;
         }
@@ -417,7 +424,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             (void)pol_panel;
             int sd = 0, sb = 0, k = 0;
             uint32_t pd = 0, pb = 0;
-            for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
+            for (Walk<chunk_ks<SD>()> w(t0, t1, nks); w.more(); w.next(), ++k) {
                 if (k >= ND) mbar_wait(&empty_d[sd], pd ^ 1);
                 unsigned char* dst = dring + sd * DB;
                 mbar_arrive_expect_tx(&full_d[sd], DB);  // the whole tile / item
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             int sa = 0, sb = 0, nflush = 0;
             uint32_t pa = 0, pb = 0;
             bool started = false;
-            for (Walk w(t0, t1, nks); w.more(); w.next()) {
+            for (Walk<chunk_ks<SD>()> w(t0, t1, nks); w.more(); w.next()) {
                 mbar_wait(&full_a[sa], pa);
                 if constexpr (kBProd) mbar_wait(&full_b[sb], pb);
                 tc_fence_after();
@@ -557,7 +564,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         const int c0 = part_k * 8;
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         // ---- epilogue of an accumulation chunk: this warp's 32 TMEM lanes ----
-        auto epilogue = [&](const Walk& w, int nfl) {
+        auto epilogue = [&](const Walk<chunk_ks<SD>()>& w, int nfl) {
             mbar_wait(acc_full, static_cast<uint32_t>(nfl & 1));
             tc_fence_after();
             const int grow = w.rb * kRowsI8 + row;
@@ -605,7 +612,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             // walks every item to keep the ring indices
             int sd = 0, sa = 0, k = 0, nflush = 0;
             uint32_t pd = 0, pa = 0;
-            for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
+            for (Walk<chunk_ks<SD>()> w(t0, t1, nks); w.more(); w.next(), ++k) {
                 if (k % kGrp == part_k) {
                     mbar_wait(&full_d[sd], pd);
                     if (k >= NA) {
@@ -671,7 +678,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         double sc = 0.0;
         int sd = 0, sa = 0, k = 0, nflush = 0;
         uint32_t pd = 0, pa = 0;
-        for (Walk w(t0, t1, nks); w.more(); w.next(), ++k) {
+        for (Walk<chunk_ks<SD>()> w(t0, t1, nks); w.more(); w.next(), ++k) {
             if (SD == kDig && w.rb != cur_rb) {
                 cur_rb = w.rb;
                 const int grow = w.rb * kRowsI8 + row;
