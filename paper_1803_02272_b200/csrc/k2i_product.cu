@@ -13,8 +13,9 @@
 //          of round(X 2^(56-f_c)), |X| 2^-f_c < 1/4)
 //   (S X)_ic = 2^(e_i+f_c) sum_{d=2..8} 2^-8d acc_d,  acc_d = sum_j sum_{t+u=d} a_t b_u
 // The terms with t+u >= 9 (weight <= 2^-72) are dropped; each acc_d is an
-// exact int32 sum over at most 8192 columns (7 * 255 * 128 * 8192 < 2^31),
-// after which it is flushed to fp64. Digits of S are produced on the fly from
+// exact int32 sum over at most 8192 columns (7 * 255 * 128 * 8192 < 2^31;
+// Hamming slices: 3 products per diagonal, 16384 columns), after which it is
+// flushed to fp64. Digits of S are produced on the fly from
 // the fp64 (or fp32) D tile, so HBM traffic is exactly one read of D per
 // pass, as in the fp64 kernel.
 //
