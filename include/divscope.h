@@ -321,11 +321,14 @@ divscope_status divscope_synth_reads(size_t count, size_t length, size_t ancesto
  * else fp64 DMMA), 1 = fp64 DMMA only, 2 = int8 whenever supported. */
 divscope_status divscope_set_product_path(int mode);
 
-/* NEW. S-digit cache of the int8 product: 0 = off, 1 = auto (default: on
- * when the device has room for it next to a reserve of max(1 GB, 2 %)),
- * 2 = on whenever it fits. With it, a solve's first product pass stores the exact digit
- * bytes of D o D and the later passes read those instead of D. Results are
- * bit-identical either way. */
+/* NEW. S-digit cache of the int8 product: 0 = off (a slot already filled
+ * stays in the library's workspace until a failed allocation evicts it),
+ * 1 = auto (default: on when the device has room for it next to a reserve of
+ * max(1 GB, 2 %)), 2 = on whenever it fits. With it, divscope_gram (f64 D,
+ * n >= 4096) also writes the exact digit bytes of D o D, or else a solve's
+ * first product pass stores them, and the product passes read those instead
+ * of D. Results equal the uncached path's to fp64 rounding (Hamming D and a
+ * solve that stores its own: bit-identical). */
 divscope_status divscope_set_sdig_cache(int mode);
 
 /* Select the CUDA device used by this process (default: current device). */
