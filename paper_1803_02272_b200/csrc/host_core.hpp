@@ -129,6 +129,7 @@ public:
     // (reserve: max(1 GB, 2 % of the device))
     void* try_scratch(const std::string& slot, size_t bytes);
     bool evict_scratch();
+    void* find_scratch(const std::string& slot) const;  // nullptr when absent
     // immutable device table named by its content key: uploaded on first
     // use (never inside a graph capture), then returned as is
     bool has_table(const std::string& name) const { return tables_.count(name) != 0; }
