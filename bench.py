@@ -484,6 +484,12 @@ def b200_arm(args, wl):
                                "k2i_product (7x7-digit int8 slice product, tcgen05 kind::i8)") +
                               (", streaming the S-digit cache" if sdig else ""),
                     "peak_source": hbm["peak_source"],
+                    **({"peak_note": "frac > 1: the peak is MEASURED_PEAKS.json's device copy "
+                                     "(read + write traffic); this pass is a pure read stream of "
+                                     "the S-digit planes, which HBM serves faster — ncu DRAM bytes "
+                                     "for the same kernel: 2.818 GB read in 0.416 ms (profiles/"
+                                     "r02_final_ncu_k2i_c2_stream.txt, k2_traffic.json)"}
+                       if gbs > hbm_peak else {}),
                     "column_groups": groups,
                     "reads_of_D_per_pass": 1 if int(st.last_product_pair) else groups,
                     "cta_pair": bool(int(st.last_product_pair)),
