@@ -405,7 +405,9 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
     // product after a CholeskyQR; the first one multiplies the replicated Omega)
     auto product = [&](double* x_full, double* y_full, bool gather) {
         cudaEvent_t e0, e1;
-        const int sdm = sdig ? (sdig_pass++ == 0 ? 1 : 2) : 0;
+        const int timed_kind = sdig_pass == 0 ? 3 : 1;  // the first pass: kind 3
+        const int sdm = sdig ? (sdig_pass == 0 ? 1 : 2) : 0;
+        ++sdig_pass;
         if (gather && overlap) {
             // s = 1^T X, t = r^T X and the column maxima of this rank's rows,
             // reduced over the ranks; then the all-gather on the side stream
@@ -434,7 +436,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
             }
             // every later collective (and panel write) comes after the gather
             DSB_CUDA(cudaStreamWaitEvent(c.stream, c.side_done, 0));
-            c.add_timed(1, e0, e1);
+            c.add_timed(timed_kind, e0, e1);
             return;
         }
         if (gather) cm.allgather(x_full, m_pad * wp, c.stream);
@@ -454,7 +456,7 @@ ShardOut run_sharded(const Matrix& g, size_t rank, size_t p, size_t q, uint64_t 
         else if (m)
             launch_k2(s.tmap_for(plan.bm), s.dt, 1, plan, x_full, part, r_full + rb, scal, colsums,
                       y_full + lo, m_pad, c.stream, e0, e1);
-        c.add_timed(1, e0, e1);
+        c.add_timed(timed_kind, e0, e1);
     };
     auto orth_local = [&](double* y_full, double* t_full, double* out_full) {
         double* y = y_full + lo;
